@@ -1,0 +1,317 @@
+"""FP64 CPU oracle for the MASK hot path — TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline`` /
+``--impl reference`` legs may import this package.  The product path
+(``paper_2208_02734_b200``) never imports it and shares no code with it; the
+only module both sides use is ``datagen`` (seeded inputs, no method arithmetic).
+
+The arithmetic lives in ``mask_oracle.c`` (plain C, FP64, compiled here with
+gcc; see its header for the paper passages each function follows).  This
+module only marshals numpy arrays into it and derives the child lists
+``children_l(j) = {i : labels_l[i] = j}`` in ascending i (PAPER.md P:655/P:658
+``layerLabels``; D7).
+
+Parity status: every function here is pinned by ``tests/test_oracle.py``
+(hand-derived worked example S:107, closed forms, brute force against scipy /
+numpy library routines, invariants).  No function is "parity unpinned".
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+import threading
+from typing import List, Optional, Sequence, Tuple
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "mask_oracle.c")
+_LIB_PATH = os.path.join(_HERE, "_build", "liboracle.so")
+_lock = threading.Lock()
+_lib = None
+
+dp = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
+i64p = np.ctypeslib.ndpointer(dtype=np.int64, flags="C_CONTIGUOUS")
+i32p = np.ctypeslib.ndpointer(dtype=np.int32, flags="C_CONTIGUOUS")
+
+
+def build(force: bool = False) -> str:
+    """Compile mask_oracle.c -> oracle/_build/liboracle.so (gcc -O2 -fopenmp, IEEE FP)."""
+    os.makedirs(os.path.dirname(_LIB_PATH), exist_ok=True)
+    if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(_SRC):
+        tmp = _LIB_PATH + f".tmp{os.getpid()}"
+        subprocess.check_call(
+            ["gcc", "-O2", "-std=c11", "-fPIC", "-shared", "-fopenmp", "-fno-fast-math",
+             "-ffp-contract=off", "-o", tmp, _SRC, "-lm"]
+        )
+        os.replace(tmp, _LIB_PATH)
+    return _LIB_PATH
+
+
+def lib():
+    global _lib
+    with _lock:
+        if _lib is None:
+            L = C.CDLL(build())
+            L.orc_num_threads.restype = C.c_int
+            L.orc_dist2.restype = C.c_double
+            L.orc_dist2.argtypes = [C.c_int, dp, dp]
+            L.orc_dist2_csr_dense.restype = C.c_double
+            L.orc_dist2_csr_dense.argtypes = [C.c_int64, i32p, dp, dp, C.c_double]
+            L.orc_dist2_csr_csr.restype = C.c_double
+            L.orc_dist2_csr_csr.argtypes = [C.c_int64, i32p, dp, C.c_int64, i32p, dp]
+            L.orc_assign.argtypes = [C.c_int64, C.c_int, dp, C.c_int64, dp, i32p, dp, dp]
+            L.orc_assign_csr.argtypes = [C.c_int64, C.c_int, i64p, i32p, dp, C.c_int64, dp, i32p, dp, dp]
+            L.orc_cluster_sums.argtypes = [C.c_int64, C.c_int, dp, i32p, C.c_int64, dp, i64p]
+            L.orc_cluster_sums_csr.argtypes = [C.c_int64, C.c_int, i64p, i32p, dp, i32p, C.c_int64, dp, i64p]
+            L.orc_means_from_sums.restype = C.c_double
+            L.orc_means_from_sums.argtypes = [C.c_int64, C.c_int, dp, i64p, dp, dp]
+            lloyd_args = [C.c_int64, i64p, C.c_int, C.c_double, dp, i32p, dp, i64p, C.POINTER(C.c_int)]
+            L.orc_lloyd.restype = C.c_int
+            L.orc_lloyd.argtypes = [C.c_int64, C.c_int, dp] + lloyd_args
+            L.orc_lloyd_csr.restype = C.c_int
+            L.orc_lloyd_csr.argtypes = [C.c_int64, C.c_int, i64p, i32p, dp] + lloyd_args
+            _lib = L
+        return _lib
+
+
+def num_threads() -> int:
+    return int(lib().orc_num_threads())
+
+
+def _f64(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _csr(csr):
+    rp, col, val = csr
+    return (np.ascontiguousarray(rp, dtype=np.int64), np.ascontiguousarray(col, dtype=np.int32), _f64(val))
+
+
+# ------------------------------------------------------------------ primitives
+def dist2(y, c) -> float:
+    y, c = _f64(y), _f64(c)
+    return float(lib().orc_dist2(y.size, y, c))
+
+
+def assign(Y, P) -> Tuple[np.ndarray, np.ndarray, np.ndarray]:
+    """labels (lowest j on ties), best d^2, second-best d^2 (dense rows)."""
+    Y, P = _f64(Y), _f64(P)
+    n, d = Y.shape
+    k = P.shape[0]
+    lab = np.empty(n, np.int32)
+    b1 = np.empty(n, np.float64)
+    b2 = np.empty(n, np.float64)
+    lib().orc_assign(n, d, Y, k, P, lab, b1, b2)
+    return lab, b1, b2
+
+
+def assign_csr(csr, dim: int, P):
+    rp, col, val = _csr(csr)
+    P = _f64(P)
+    n = rp.size - 1
+    lab = np.empty(n, np.int32)
+    b1 = np.empty(n, np.float64)
+    b2 = np.empty(n, np.float64)
+    lib().orc_assign_csr(n, dim, rp, col, val, P.shape[0], P, lab, b1, b2)
+    return lab, b1, b2
+
+
+def cluster_sums(Y, labels, k: int):
+    Y = _f64(Y)
+    n, d = Y.shape
+    S = np.empty((k, d), np.float64)
+    cnt = np.empty(k, np.int64)
+    lib().orc_cluster_sums(n, d, Y, np.ascontiguousarray(labels, np.int32), k, S, cnt)
+    return S, cnt
+
+
+def cluster_sums_csr(csr, dim: int, labels, k: int):
+    rp, col, val = _csr(csr)
+    S = np.empty((k, dim), np.float64)
+    cnt = np.empty(k, np.int64)
+    lib().orc_cluster_sums_csr(rp.size - 1, dim, rp, col, val, np.ascontiguousarray(labels, np.int32), k, S, cnt)
+    return S, cnt
+
+
+def means_from_sums(S, counts, P_old):
+    S, P_old = _f64(S), _f64(P_old)
+    k, d = P_old.shape
+    P_new = np.empty_like(P_old)
+    md = lib().orc_means_from_sums(k, d, S, np.ascontiguousarray(counts, np.int64), P_old, P_new)
+    return P_new, float(md)
+
+
+def means(Y, labels, P_old):
+    """Prototype update: member means, empty clusters keep P_old (D5)."""
+    S, cnt = cluster_sums(Y, labels, P_old.shape[0])
+    return means_from_sums(S, cnt, P_old)[0], cnt
+
+
+# ------------------------------------------------------------------ Lloyd / build
+class LevelResult:
+    def __init__(self, P, labels, J, changed, updates):
+        self.P = P
+        self.labels = labels
+        self.J = J
+        self.changed = changed
+        self.updates = updates
+
+
+def lloyd(Y, init_idx, T: int, tol: float = 0.0, csr_dim: Optional[int] = None) -> LevelResult:
+    """One level: Lloyd from Y[init_idx], T iterations, then a final assignment."""
+    init_idx = np.ascontiguousarray(init_idx, np.int64)
+    k = init_idx.size
+    J = np.zeros(T + 1, np.float64)
+    ch = np.zeros(T + 1, np.int64)
+    upd = C.c_int(0)
+    if csr_dim is None:
+        Y = _f64(Y)
+        n, d = Y.shape
+        P = np.empty((k, d), np.float64)
+        lab = np.empty(n, np.int32)
+        passes = lib().orc_lloyd(n, d, Y, k, init_idx, T, tol, P, lab, J, ch, C.byref(upd))
+    else:
+        rp, col, val = _csr(Y)
+        n, d = rp.size - 1, csr_dim
+        P = np.empty((k, d), np.float64)
+        lab = np.empty(n, np.int32)
+        passes = lib().orc_lloyd_csr(n, d, rp, col, val, k, init_idx, T, tol, P, lab, J, ch, C.byref(upd))
+    return LevelResult(P, lab, J[:passes], ch[:passes], upd.value)
+
+
+def children(labels, k: int) -> Tuple[np.ndarray, np.ndarray]:
+    """CSR child lists: offsets (k+1), members ascending i within each prototype."""
+    labels = np.asarray(labels, np.int64)
+    counts = np.bincount(labels, minlength=k)
+    offsets = np.zeros(k + 1, np.int64)
+    np.cumsum(counts, out=offsets[1:])
+    members = np.argsort(labels, kind="stable").astype(np.int64)
+    return offsets, members
+
+
+class Index:
+    """Oracle multilevel index: per level P (k_l x d, FP64), labels, child lists, traces."""
+
+    def __init__(self, levels: List[LevelResult], offsets: List[np.ndarray], members: List[np.ndarray], dim: int):
+        self.levels = levels
+        self.offsets = offsets
+        self.members = members
+        self.dim = dim
+
+    @property
+    def P(self):
+        return [lv.P for lv in self.levels]
+
+
+def build_index(X, init_idx: Sequence[np.ndarray], T: int, tol: float = 0.0, csr_dim: Optional[int] = None) -> Index:
+    """Bottom-up levels: level 1 clusters X, level l+1 clusters P_l (D1, D6)."""
+    levels, offs, mems = [], [], []
+    Y = X
+    dim = csr_dim
+    for l, idx in enumerate(init_idx):
+        res = lloyd(Y, idx, T, tol, csr_dim=csr_dim if l == 0 else None)
+        levels.append(res)
+        o, m = children(res.labels, res.P.shape[0])
+        offs.append(o)
+        mems.append(m)
+        Y = res.P
+        dim = res.P.shape[1]
+    return Index(levels, offs, mems, dim)
+
+
+# ------------------------------------------------------------------ queries
+def _ptr_array(arrs, ctype):
+    return (C.POINTER(ctype) * len(arrs))(*[a.ctypes.data_as(C.POINTER(ctype)) for a in arrs])
+
+
+def query(P: Sequence[np.ndarray], offsets: Sequence[np.ndarray], members: Sequence[np.ndarray], X, Q,
+          knn: int, beam: int = 1, dim: Optional[int] = None, x_csr: bool = False, q_csr: bool = False):
+    """Descent over a given index (the oracle's own, or a GPU-built one exported via getters).
+
+    Returns ids (nq x knn, int64, -1 padded), d2 (nq x knn, FP64, +inf padded) and the per-query
+    minimum relative gap over all selections (for the 1e-5 tie-window exemption)."""
+    L = len(P)
+    Pd = [_f64(p) for p in P]
+    Of = [np.ascontiguousarray(o, np.int64) for o in offsets]
+    Me = [np.ascontiguousarray(m, np.int64) for m in members]
+    d = Pd[0].shape[1] if dim is None else dim
+    kpl = np.array([p.shape[0] for p in Pd], np.int64)
+    null_d = C.POINTER(C.c_double)()
+    null_i64 = C.POINTER(C.c_int64)()
+    null_i32 = C.POINTER(C.c_int32)()
+    if x_csr:
+        xrp, xcol, xval = _csr(X)
+        xargs = [null_d, xrp.ctypes.data_as(C.POINTER(C.c_int64)), xcol.ctypes.data_as(C.POINTER(C.c_int32)),
+                 xval.ctypes.data_as(C.POINTER(C.c_double))]
+        keep_x = (xrp, xcol, xval)
+    else:
+        Xd = _f64(X)
+        xargs = [Xd.ctypes.data_as(C.POINTER(C.c_double)), null_i64, null_i32, null_d]
+        keep_x = (Xd,)
+    if q_csr:
+        qrp, qcol, qval = _csr(Q)
+        nq = qrp.size - 1
+        qargs = [null_d, qrp.ctypes.data_as(C.POINTER(C.c_int64)), qcol.ctypes.data_as(C.POINTER(C.c_int32)),
+                 qval.ctypes.data_as(C.POINTER(C.c_double))]
+        keep_q = (qrp, qcol, qval)
+    else:
+        Qd = _f64(Q)
+        nq = Qd.shape[0]
+        qargs = [Qd.ctypes.data_as(C.POINTER(C.c_double)), null_i64, null_i32, null_d]
+        keep_q = (Qd,)
+    ids = np.empty((nq, knn), np.int64)
+    d2 = np.empty((nq, knn), np.float64)
+    gap = np.empty(nq, np.float64)
+    f = lib().orc_query
+    f.restype = None
+    f(C.c_int(L), kpl.ctypes.data_as(C.POINTER(C.c_int64)), _ptr_array(Pd, C.c_double),
+      _ptr_array(Of, C.c_int64), _ptr_array(Me, C.c_int64), C.c_int(d), *xargs,
+      C.c_int64(nq), *qargs, C.c_int(knn), C.c_int(beam),
+      ids.ctypes.data_as(C.POINTER(C.c_int64)), d2.ctypes.data_as(C.POINTER(C.c_double)),
+      gap.ctypes.data_as(C.POINTER(C.c_double)))
+    del keep_x, keep_q
+    return ids, d2, gap
+
+
+def knn_exact(X, Q, knn: int, csr: bool = False):
+    """Brute-force exact k-NN by (d^2, id): ids, d2, relative gap between k-th and (k+1)-th."""
+    null_d = C.POINTER(C.c_double)()
+    null_i64 = C.POINTER(C.c_int64)()
+    null_i32 = C.POINTER(C.c_int32)()
+    if csr:
+        xrp, xcol, xval = _csr(X)
+        qrp, qcol, qval = _csr(Q)
+        n, nq, d = xrp.size - 1, qrp.size - 1, 0
+        xargs = [null_d, xrp.ctypes.data_as(C.POINTER(C.c_int64)), xcol.ctypes.data_as(C.POINTER(C.c_int32)),
+                 xval.ctypes.data_as(C.POINTER(C.c_double))]
+        qargs = [null_d, qrp.ctypes.data_as(C.POINTER(C.c_int64)), qcol.ctypes.data_as(C.POINTER(C.c_int32)),
+                 qval.ctypes.data_as(C.POINTER(C.c_double))]
+        keep = (xrp, xcol, xval, qrp, qcol, qval)
+    else:
+        Xd, Qd = _f64(X), _f64(Q)
+        n, d = Xd.shape
+        nq = Qd.shape[0]
+        xargs = [Xd.ctypes.data_as(C.POINTER(C.c_double)), null_i64, null_i32, null_d]
+        qargs = [Qd.ctypes.data_as(C.POINTER(C.c_double)), null_i64, null_i32, null_d]
+        keep = (Xd, Qd)
+    ids = np.empty((nq, knn), np.int64)
+    d2 = np.empty((nq, knn), np.float64)
+    gap = np.empty(nq, np.float64)
+    f = lib().orc_knn_exact
+    f.restype = None
+    f(C.c_int64(n), C.c_int(d), *xargs, C.c_int64(nq), *qargs, C.c_int(knn),
+      ids.ctypes.data_as(C.POINTER(C.c_int64)), d2.ctypes.data_as(C.POINTER(C.c_double)),
+      gap.ctypes.data_as(C.POINTER(C.c_double)))
+    del keep
+    return ids, d2, gap
+
+
+def recall(result_ids: np.ndarray, exact_ids: np.ndarray) -> float:
+    """recall@k = |result ∩ exact| / k averaged over queries (padding ids -1 never match)."""
+    nq, k = exact_ids.shape
+    hits = 0
+    for r, e in zip(result_ids, exact_ids):
+        hits += len(set(int(v) for v in r if v >= 0) & set(int(v) for v in e))
+    return hits / float(nq * k) if nq else 1.0

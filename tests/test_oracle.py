@@ -1,0 +1,324 @@
+"""Pins for the FP64 oracle (oracle/) against things other than itself.
+
+Each test pins the oracle to a value the paper/SPEC prints for a worked example, a closed
+form, a special case that reduces to a library routine (scipy / numpy), brute force on a
+tiny input, or an invariant of the method.  Chosen so that a dropped term, a wrong sign,
+a wrong index, a transposed operand or a wrong tie rule fails at least one of them.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+from scipy.spatial.distance import cdist
+
+import datagen
+import oracle
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+# ------------------------------------------------------------------ distances
+def test_dist_345_triangle():
+    # SPEC.md:51 [TRIVIAL]: L2 (0,0)-(3,4) = 5  -> squared 25 (D9)
+    assert oracle.dist2([0.0, 0.0], [3.0, 4.0]) == 25.0
+    assert oracle.dist2([3.0, 4.0], [0.0, 0.0]) == 25.0
+    assert oracle.dist2([1.5, -2.0], [1.5, -2.0]) == 0.0
+
+
+def test_dist_matches_scipy():
+    rng = np.random.default_rng(0)
+    a = rng.standard_normal((7, 13))
+    b = rng.standard_normal((5, 13))
+    ref = cdist(a, b, "sqeuclidean")
+    for i in range(7):
+        for j in range(5):
+            assert oracle.dist2(a[i], b[j]) == pytest.approx(ref[i, j], rel=1e-14)
+
+
+def test_sparse_dense_identity_equals_densified():
+    # sparse-dense distance == densified result (<= 1e-12 relative)
+    rp, col, val = datagen.random_csr(5, 20, 300, 12)
+    P = np.random.default_rng(1).standard_normal((9, 300))
+    dense = np.zeros((20, 300))
+    for i in range(20):
+        dense[i, col[rp[i]:rp[i + 1]]] = val[rp[i]:rp[i + 1]]
+    ref = cdist(dense, P, "sqeuclidean")
+    L = oracle.lib()
+    for i in range(20):
+        c = np.ascontiguousarray(col[rp[i]:rp[i + 1]], np.int32)
+        v = np.ascontiguousarray(val[rp[i]:rp[i + 1]], np.float64)
+        for j in range(9):
+            cn2 = float(np.dot(P[j], P[j]))
+            got = L.orc_dist2_csr_dense(c.size, c, v, np.ascontiguousarray(P[j]), cn2)
+            assert got == pytest.approx(ref[i, j], rel=1e-12)
+    # sparse {} vs (3,4): SPEC.md:61 distance from origin
+    got = L.orc_dist2_csr_dense(0, np.zeros(1, np.int32), np.zeros(1), np.array([3.0, 4.0]), 25.0)
+    assert got == 25.0
+    # sparse-sparse union form == densified
+    for i in range(19):
+        a0, a1, b0, b1 = rp[i], rp[i + 1], rp[i + 1], rp[i + 2]
+        got = L.orc_dist2_csr_csr(a1 - a0, np.ascontiguousarray(col[a0:a1]), np.ascontiguousarray(val[a0:a1], np.float64),
+                                  b1 - b0, np.ascontiguousarray(col[b0:b1]), np.ascontiguousarray(val[b0:b1], np.float64))
+        assert got == pytest.approx(float(((dense[i] - dense[i + 1]) ** 2).sum()), rel=1e-12)
+
+
+# ------------------------------------------------------------------ assignment
+def test_assign_brute_force_scipy():
+    rng = np.random.default_rng(2)
+    for n, d, k in [(50, 3, 7), (200, 16, 33), (31, 1, 5), (64, 9, 64)]:
+        Y = rng.standard_normal((n, d))
+        P = rng.standard_normal((k, d))
+        lab, b1, b2 = oracle.assign(Y, P)
+        D = cdist(Y, P, "sqeuclidean")
+        assert np.array_equal(lab, D.argmin(axis=1))  # numpy argmin also returns the first minimum
+        Ds = np.sort(D, axis=1)
+        np.testing.assert_allclose(b1, Ds[:, 0], rtol=1e-13)
+        if k > 1:
+            np.testing.assert_allclose(b2, Ds[:, 1], rtol=1e-13)
+
+
+def test_assign_ties_lowest_ordinal():
+    # exact match -> that centroid; equidistant -> lowest ordinal (D4)
+    lab, b1, _ = oracle.assign([[0.0, 0.0]], [[0.0, 0.0], [5.0, 5.0]])
+    assert lab[0] == 0 and b1[0] == 0.0
+    lab, _, _ = oracle.assign([[0.0, 0.0]], [[5.0, 5.0], [1.0, 0.0], [-1.0, 0.0], [0.0, 1.0]])
+    assert lab[0] == 1
+    # duplicated prototypes: the lower copy wins
+    lab, _, _ = oracle.assign([[2.0, 2.0]], [[9.0, 9.0], [2.0, 2.1], [2.0, 2.1]])
+    assert lab[0] == 1
+
+
+def test_assign_k1_second_is_inf():
+    lab, b1, b2 = oracle.assign([[1.0], [2.0]], [[0.0]])
+    assert list(lab) == [0, 0] and np.all(np.isinf(b2))
+
+
+# ------------------------------------------------------------------ update
+def test_means_against_numpy_add_at():
+    rng = np.random.default_rng(3)
+    Y = rng.standard_normal((500, 6))
+    k = 40
+    lab = rng.integers(0, k - 3, size=500).astype(np.int32)  # last 3 clusters empty
+    P_old = rng.standard_normal((k, 6))
+    P_new, cnt = oracle.means(Y, lab, P_old)
+    S = np.zeros((k, 6))
+    np.add.at(S, lab, Y)
+    c = np.bincount(lab, minlength=k)
+    assert np.array_equal(cnt, c)
+    nz = c > 0
+    np.testing.assert_allclose(P_new[nz], S[nz] / c[nz, None], rtol=1e-13)
+    assert np.array_equal(P_new[~nz], P_old[~nz])  # empty clusters keep their prototype (D5)
+
+
+def test_cluster_sums_csr_equals_densified():
+    rp, col, val = datagen.random_csr(7, 60, 50, 5)
+    dense = np.zeros((60, 50))
+    for i in range(60):
+        dense[i, col[rp[i]:rp[i + 1]]] = val[rp[i]:rp[i + 1]]
+    lab = (np.arange(60) % 7).astype(np.int32)
+    S1, c1 = oracle.cluster_sums_csr((rp, col, val), 50, lab, 7)
+    S2, c2 = oracle.cluster_sums(dense, lab, 7)
+    assert np.array_equal(c1, c2)
+    np.testing.assert_allclose(S1, S2, rtol=0, atol=1e-15)
+
+
+# ------------------------------------------------------------------ Lloyd
+def test_golden_spec_s107_trajectories():
+    g = json.load(open(os.path.join(GOLDEN, "spec_s107_two_clusters.json")))
+    Y = np.array(g["points"], np.float64)
+    for case in g["cases"]:
+        r = oracle.lloyd(Y, np.array(case["init"]), T=10)
+        np.testing.assert_array_equal(r.P, np.array(case["final_P"]))
+        np.testing.assert_array_equal(r.labels, case["labels_per_pass"][-1])
+        np.testing.assert_array_equal(r.J[:-1], case["J_per_pass"])  # passes before the final one
+        assert r.J[-1] == case["final_J"]
+        assert r.updates == case["updates"]
+        # the per-pass labels: pass 0 from the init prototypes
+        lab0, _, _ = oracle.assign(Y, Y[case["init"]])
+        np.testing.assert_array_equal(lab0, case["labels_per_pass"][0])
+
+
+def test_lloyd_empty_cluster_keeps_prototype_and_ties():
+    # hand-derived: points 0,0,5 with both inits at 0 -> pass 0 all ties -> label 0 (lowest);
+    # P0 <- mean(0,0,5)=5/3, P1 empty keeps 0; pass 1: 0,0 -> P1, 5 -> P0; P0 <- 5, P1 <- 0.
+    Y = np.array([[0.0], [0.0], [5.0]])
+    r = oracle.lloyd(Y, np.array([0, 1]), T=10)
+    np.testing.assert_array_equal(r.P, [[5.0], [0.0]])
+    np.testing.assert_array_equal(r.labels, [1, 1, 0])
+    assert r.J[0] == 25.0 and r.J[-1] == 0.0
+
+
+def test_lloyd_k1_is_global_mean():
+    # SPEC.md:109 [TRIVIAL]: k = 1 -> the componentwise mean, labels all 0
+    Y = datagen.random_dense(4, 300, 5, scale=3.0, offset=1.0).astype(np.float64)
+    r = oracle.lloyd(Y, np.array([17]), T=3)
+    np.testing.assert_allclose(r.P[0], Y.mean(axis=0), rtol=1e-12)
+    assert np.all(r.labels == 0)
+    assert r.J[-1] == pytest.approx(((Y - Y.mean(axis=0)) ** 2).sum(), rel=1e-12)
+
+
+def test_lloyd_k_equals_n_identity():
+    # SPEC.md:108 [TRIVIAL]: k = |points|, distinct points -> each point its own prototype, J = 0
+    Y = datagen.random_dense(5, 40, 3).astype(np.float64)
+    r = oracle.lloyd(Y, np.arange(40), T=5)
+    np.testing.assert_array_equal(r.P, Y)
+    np.testing.assert_array_equal(r.labels, np.arange(40))
+    assert r.J[-1] == 0.0
+
+
+def test_lloyd_monotone_and_fixed_point():
+    # inertia non-increasing; labels = brute-force nearest; converged P = member means
+    Y = datagen.blobs(6, 2000, 4, 8).astype(np.float64)
+    idx = datagen.init_indices(99, 1, 2000, 50)
+    r = oracle.lloyd(Y, idx, T=200)
+    assert np.all(np.diff(r.J) <= 1e-12 * r.J[:-1])
+    D = cdist(Y, r.P, "sqeuclidean")
+    np.testing.assert_array_equal(r.labels, D.argmin(axis=1))
+    assert r.changed[-1] == 0  # converged inside 200 iterations
+    S = np.zeros_like(r.P)
+    np.add.at(S, r.labels, Y)
+    c = np.bincount(r.labels, minlength=50)
+    np.testing.assert_allclose(r.P[c > 0], S[c > 0] / c[c > 0, None], rtol=1e-12)
+
+
+def test_lloyd_T0_is_plain_assignment():
+    Y = datagen.blobs(8, 300, 2, 4).astype(np.float64)
+    idx = np.array([5, 60, 7])
+    r = oracle.lloyd(Y, idx, T=0)
+    np.testing.assert_array_equal(r.P, Y[idx])
+    np.testing.assert_array_equal(r.labels, cdist(Y, Y[idx], "sqeuclidean").argmin(axis=1))
+    assert r.updates == 0 and len(r.J) == 1
+
+
+def test_lloyd_tol_stop():
+    Y = datagen.blobs(9, 1000, 3, 5).astype(np.float64)
+    idx = datagen.init_indices(98, 1, 1000, 20)
+    r_inf = oracle.lloyd(Y, idx, T=3, tol=1e9)  # any displacement <= tol -> one update
+    assert r_inf.updates == 1
+
+
+def test_lloyd_csr_equals_densified():
+    rp, col, val = datagen.random_csr(10, 120, 40, 6)
+    dense = np.zeros((120, 40))
+    for i in range(120):
+        dense[i, col[rp[i]:rp[i + 1]]] = val[rp[i]:rp[i + 1]]
+    idx = datagen.init_indices(97, 1, 120, 9)
+    a = oracle.lloyd((rp, col, val), idx, T=6, csr_dim=40)
+    b = oracle.lloyd(dense, idx, T=6)
+    np.testing.assert_array_equal(a.labels, b.labels)
+    np.testing.assert_allclose(a.P, b.P, rtol=0, atol=1e-13)
+    np.testing.assert_allclose(a.J, b.J, rtol=1e-12)
+
+
+def test_children_lists():
+    lab = np.array([2, 0, 2, 1, 2, 0], np.int32)
+    off, mem = oracle.children(lab, 4)
+    assert list(off) == [0, 2, 3, 6, 6]
+    assert list(mem) == [1, 5, 3, 0, 2, 4]
+
+
+# ------------------------------------------------------------------ queries
+def _exact_numpy(X, Q, k):
+    D = cdist(Q, X, "sqeuclidean")
+    ids = np.array([np.lexsort((np.arange(X.shape[0]), row))[:k] for row in D])
+    return ids, np.take_along_axis(D, ids, axis=1)
+
+
+def test_knn_exact_against_numpy():
+    X = datagen.blobs(11, 400, 3, 5).astype(np.float64)
+    Q = datagen.blobs(12, 30, 3, 5).astype(np.float64)
+    ids, d2, _ = oracle.knn_exact(X, Q, 7)
+    ids2, d22 = _exact_numpy(X, Q, 7)
+    np.testing.assert_array_equal(ids, ids2)
+    np.testing.assert_allclose(d2, d22, rtol=1e-13)
+    # ties by id: duplicated points
+    Xd = np.array([[0.0], [1.0], [1.0], [1.0], [3.0]])
+    ids, _, _ = oracle.knn_exact(Xd, np.array([[1.0]]), 3)
+    assert list(ids[0]) == [1, 2, 3]
+
+
+def test_query_single_level_k1_is_exact_knn():
+    # SURVEY §8(c) pins: L=1, k_1=1 -> the leaf is all N points -> result = exact k-NN, recall 1
+    X = datagen.blobs(13, 500, 2, 6).astype(np.float64)
+    Q = datagen.blobs(14, 40, 2, 6).astype(np.float64)
+    idx = oracle.build_index(X, [np.array([3])], T=2)
+    ids, d2, _ = oracle.query(idx.P, idx.offsets, idx.members, X, Q, 10, 1)
+    eids, ed2, _ = oracle.knn_exact(X, Q, 10)
+    np.testing.assert_array_equal(ids, eids)
+    assert oracle.recall(ids, eids) == 1.0
+
+
+def test_query_wide_beam_is_exact_knn():
+    # beam >= max_l k_l -> every partition scanned -> exact k-NN
+    X = datagen.blobs(15, 800, 3, 8).astype(np.float64)
+    Q = datagen.blobs(16, 25, 3, 8).astype(np.float64)
+    inits = [datagen.init_indices(96, 1, 800, 40), datagen.init_indices(96, 2, 40, 6)]
+    idx = oracle.build_index(X, inits, T=5)
+    ids, _, _ = oracle.query(idx.P, idx.offsets, idx.members, X, Q, 5, beam=40)
+    eids, _, _ = oracle.knn_exact(X, Q, 5)
+    np.testing.assert_array_equal(ids, eids)
+
+
+def test_query_identity_levels_self_query():
+    # P:1864-1867 "1:1 ratio ... renders perfect accuracy (exact search)": identity levels
+    X = datagen.random_dense(17, 64, 4).astype(np.float64)
+    inits = [np.arange(64), np.arange(64)]
+    idx = oracle.build_index(X, inits, T=3)
+    ids, d2, _ = oracle.query(idx.P, idx.offsets, idx.members, X, X, 1, 1)
+    np.testing.assert_array_equal(ids[:, 0], np.arange(64))
+    assert np.all(d2 == 0.0)
+
+
+def test_query_padding_and_descent_invariants():
+    X = datagen.blobs(18, 300, 2, 5).astype(np.float64)
+    Q = datagen.blobs(19, 20, 2, 5).astype(np.float64)
+    inits = [datagen.init_indices(95, 1, 300, 60), datagen.init_indices(95, 2, 60, 7)]
+    idx = oracle.build_index(X, inits, T=4)
+    ids, d2, _ = oracle.query(idx.P, idx.offsets, idx.members, X, Q, 50, 1)
+    eids, ed2, _ = oracle.knn_exact(X, Q, 1)
+    for q in range(20):
+        valid = ids[q] >= 0
+        # padded with (-1, +inf) after the partition is exhausted (D8)
+        assert np.all(np.isinf(d2[q][~valid]))
+        assert np.all(np.diff(d2[q][valid]) >= 0)
+        # one-sided approximation: top hit never closer than the true NN
+        assert d2[q][0] >= ed2[q][0]
+        # every hit lies in the single level-1 partition that was reached
+        lab1 = idx.levels[0].labels
+        assert len(set(lab1[ids[q][valid]].tolist())) == 1
+        # the reached level-1 prototype is the nearest non-empty child of the nearest top prototype
+        P2, P1 = idx.P[1], idx.P[0]
+        off2, mem2 = idx.offsets[1], idx.members[1]
+        off1 = idx.offsets[0]
+        top = [j for j in range(P2.shape[0]) if off2[j + 1] > off2[j]]
+        t = min(top, key=lambda j: (oracle.dist2(Q[q], P2[j]), j))
+        ch = [int(j) for j in mem2[off2[t]:off2[t + 1]] if off1[j + 1] > off1[j]]
+        c = min(ch, key=lambda j: (oracle.dist2(Q[q], P1[j]), j))
+        assert lab1[ids[q][0]] == c
+
+
+def test_query_sparse_matches_densified():
+    rp, col, val = datagen.random_csr(20, 150, 60, 6)
+    qrp, qcol, qval = datagen.random_csr(21, 12, 60, 6)
+    dense = np.zeros((150, 60))
+    for i in range(150):
+        dense[i, col[rp[i]:rp[i + 1]]] = val[rp[i]:rp[i + 1]]
+    qd = np.zeros((12, 60))
+    for i in range(12):
+        qd[i, qcol[qrp[i]:qrp[i + 1]]] = qval[qrp[i]:qrp[i + 1]]
+    inits = [datagen.init_indices(94, 1, 150, 15), datagen.init_indices(94, 2, 15, 3)]
+    idx = oracle.build_index((rp, col, val), inits, T=4, csr_dim=60)
+    a_ids, a_d2, _ = oracle.query(idx.P, idx.offsets, idx.members, (rp, col, val), (qrp, qcol, qval), 5, 1,
+                                  dim=60, x_csr=True, q_csr=True)
+    b_ids, b_d2, _ = oracle.query(idx.P, idx.offsets, idx.members, dense, qd, 5, 1)
+    np.testing.assert_array_equal(a_ids, b_ids)
+    np.testing.assert_allclose(a_d2, b_d2, rtol=1e-12, atol=1e-15)
+    e1, _, _ = oracle.knn_exact((rp, col, val), (qrp, qcol, qval), 5, csr=True)
+    e2, _, _ = oracle.knn_exact(dense, qd, 5)
+    np.testing.assert_array_equal(e1, e2)
+
+
+def test_recall_definition():
+    assert oracle.recall(np.array([[1, 2, 3]]), np.array([[3, 2, 9]])) == pytest.approx(2 / 3)
+    assert oracle.recall(np.array([[-1, -1]]), np.array([[0, 1]])) == 0.0
