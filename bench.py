@@ -1,0 +1,408 @@
+#!/usr/bin/env python
+"""Benchmark of the MASK hot path on B200: one step = one full multilevel index build
+(all levels, T Lloyd iterations + final assignment per level) + one batched k-NN query
+over the config's query set, on seeded synthetic data resident in HBM.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl mask|reference]
+
+N > 1 is launched with torch.distributed.run (one rank per GPU, NCCL): rows are sharded
+(weak scaling: every rank owns one config-sized block of rows of the same block-seeded
+generator) and mask_build combines the per-iteration partial sums with one NCCL allreduce.
+
+Prints ONE JSON line on rank 0 (contract in DESIGN.md "Measurement").  Metric: Lloyd
+point·prototype distances/s = (sum over levels and assignment passes of n_items * k_l)
+/ step time; the step time includes the query batch.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import datagen  # noqa: E402
+
+METRIC = "Lloyd point·prototype distances/s"
+UNIT = "distances/s"
+L2_FLUSH_BYTES = 512 << 20
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--impl", default="mask", choices=["mask", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--force-simt", action="store_true")
+    return ap.parse_args()
+
+
+# --------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+
+        sm = [num(r[1]) for r in self.rows if num(r[1]) is not None]
+        smax = [num(r[2]) for r in self.rows if num(r[2]) is not None]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for nm, v in zip(names, r[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+# --------------------------------------------------------------------------- helpers
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        p = json.load(open(path))
+        return {"hbm_gbs": p.get("hbm_gbs", 6650.0), "bf16_tflops": p.get("bf16_tflops", 1590.0),
+                "bf16_tflops_sustained": p.get("bf16_tflops_sustained", 1400.0),
+                "sm_max_mhz": p.get("sm_max_mhz", 1965.0), "source": "measured"}
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "sm_max_mhz": 1965.0,
+            "source": "fallback"}
+
+
+def lloyd_distances(idx, n_levels):
+    tot = 0
+    per = []
+    for l in range(1, n_levels + 1):
+        info = idx.level_info(l)
+        dist = info["passes"] * info["n_items"] * info["k"]
+        per.append(dist)
+        tot += dist
+    return tot, per
+
+
+# --------------------------------------------------------------------------- reference arm
+def run_reference(args, rank, world):
+    """The oracle (FP64 CPU, as it stands) on a bounded sample of the same workload."""
+    if rank != 0:
+        return
+    import oracle
+
+    cfg = datagen.CONFIGS[args.config]
+    k = cfg.levels[0]
+    P = datagen.data(cfg, 0, cfg.n)[datagen.init_indices(cfg.cid, 1, cfg.n, k)].astype(np.float64)
+    cores = oracle.num_threads()
+    # rows per step: ~3 s of one oracle Lloyd pass (assignment + update) on the box's cores
+    probe = datagen.data(cfg, 0, 4096).astype(np.float64)
+    t0 = time.perf_counter()
+    oracle.assign(probe, P)
+    rate = 4096 * k / max(time.perf_counter() - t0, 1e-6)
+    rows = int(min(cfg.n, max(4096, 3.0 * rate / k)))
+    Y = datagen.data(cfg, 0, rows).astype(np.float64)
+    times = []
+    for s in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        lab, _, _ = oracle.assign(Y, P)
+        oracle.means(Y, lab, P)
+        dt = time.perf_counter() - t0
+        if s >= args.warmup:
+            times.append(dt)
+    ms = 1000.0 * sum(times) / len(times)
+    value = rows * k / (ms / 1000.0)
+    sample = f"one Lloyd pass (assign + update) of the first {rows} rows of {cfg.name} level 1 against k={k}"
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg.name, "n": cfg.n, "dim": cfg.dim, "levels": list(cfg.levels), "iters": cfg.iters},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def cpu_baseline(cfg, P0):
+    """Oracle timed on the host cores on a bounded sample (~10-20 s): level-1 assignment rows."""
+    import oracle
+
+    k = P0.shape[0]
+    Pd = P0.astype(np.float64)
+    probe = datagen.data(cfg, 0, 2048).astype(np.float64)
+    t0 = time.perf_counter()
+    oracle.assign(probe, Pd)
+    rate = 2048 * k / max(time.perf_counter() - t0, 1e-6)
+    rows = int(min(cfg.n, max(2048, 10.0 * rate / k)))
+    Y = datagen.data(cfg, 0, rows).astype(np.float64)
+    t0 = time.perf_counter()
+    lab, _, _ = oracle.assign(Y, Pd)
+    oracle.means(Y, lab, Pd)
+    dt = time.perf_counter() - t0
+    return {"value": rows * k / dt, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
+            "sample": f"one FP64 Lloyd pass (assign + update) over the first {rows} rows of {cfg.name} "
+                      f"level 1 against its k={k} seeded init prototypes ({dt:.1f} s)"}
+
+
+# --------------------------------------------------------------------------- main arm
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if args.warmup < 3:
+        print("warning: --warmup < 3 violates the timing contract", file=sys.stderr)
+
+    import torch
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    import paper_2208_02734_b200 as mk
+    from paper_2208_02734_b200 import buildlib
+
+    if rank == 0:
+        buildlib.build()
+    comm = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+        if rank != 0:
+            dist.barrier()
+        else:
+            dist.barrier()
+        comm = mk.Comm.from_process_group()
+
+    cfg = datagen.CONFIGS[args.config]
+    # weak scaling: rank r owns rows [r*n, (r+1)*n) of the block-seeded generator
+    n_local = cfg.n
+    n_global = n_local * world
+    X_host = datagen.data(cfg, rank * n_local, n_local)
+    inits = []
+    prev = n_global
+    for l, kk in enumerate(cfg.levels, start=1):
+        inits.append(datagen.init_indices(cfg.cid, l, prev, kk))
+        prev = kk
+    qlo, qhi = mk.query_range(cfg.n_queries * world, world, rank)
+    Q_host = datagen.queries(cfg, count=cfg.n_queries * world)[qlo:qhi]
+    X = torch.from_numpy(X_host).to(dev)
+    Q = torch.from_numpy(np.ascontiguousarray(Q_host)).to(dev)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+    flags = mk.MASK_TIME_KERNELS | (mk.MASK_FORCE_SIMT if args.force_simt else 0)
+    if world == 1:
+        flags |= mk.MASK_BORROW_DATA
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        idx = mk.build(X, cfg.levels, cfg.iters, inits, flags=flags, comm=comm, n_global=n_global,
+                       row_offset=rank * n_local, stream=stream)
+        ids, d2 = idx.query(Q, knn=cfg.knn, beam=1, stream=stream)
+        return idx, ids, d2
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize(dev)
+
+    for _ in range(args.warmup):
+        idx, _, _ = step()
+        idx.free()
+    barrier()
+    sampler = ClockSampler(local) if rank == 0 else None
+    if sampler:
+        sampler.start()
+    launches0 = mk.kernel_launches()
+    step_ms = []
+    kt = {"assign": 0.0, "assign_n": 0, "update": 0.0, "update_n": 0}
+    dist_total = 0
+    per_level = None
+    build_ms = []
+    query_ms = []
+    for s in range(args.steps):
+        flush.zero_()  # L2 flush between timed iterations (inputs are smaller than L2)
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e2 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        idx = mk.build(X, cfg.levels, cfg.iters, inits, flags=flags, comm=comm, n_global=n_global,
+                       row_offset=rank * n_local, stream=stream)
+        e1.record(stream)
+        ids, d2 = idx.query(Q, knn=cfg.knn, beam=1, stream=stream)
+        e2.record(stream)
+        barrier()
+        step_ms.append(e0.elapsed_time(e2))
+        build_ms.append(e0.elapsed_time(e1))
+        query_ms.append(e1.elapsed_time(e2))
+        dt, per_level = lloyd_distances(idx, len(cfg.levels))
+        dist_total += dt
+        tm = idx.timing(1)
+        kt["assign"] += tm["assign"]["ms"]
+        kt["assign_n"] += tm["assign"]["launches"]
+        kt["update"] += tm["update"]["ms"]
+        kt["update_n"] += tm["update"]["launches"]
+        if s < args.steps - 1:
+            idx.free()
+    launches = mk.kernel_launches() - launches0
+    if sampler:
+        sampler.stop()
+    total_ms = sum(step_ms)
+    if world > 1:
+        t = torch.tensor([total_ms, float(dist_total)], dtype=torch.float64, device=dev)
+        tmax = t.clone()
+        torch.distributed.all_reduce(tmax[:1], op=torch.distributed.ReduceOp.MAX)
+        total_ms = float(tmax[0])
+        dist_all = torch.tensor([float(dist_total)], dtype=torch.float64, device=dev)
+        # level-1 passes count every global row once per rank's view (n_items = n_global) -> no sum
+        dist_total = float(dist_all[0])
+    value = dist_total / (total_ms / 1000.0)
+
+    # ---- roofline of the dominant kernel (level-1 assignment), measured live above
+    pk = peaks()
+    lvl1 = idx.level_info(1)
+    n1, k1, d = n_local, lvl1["k"], cfg.dim
+    assign_avg_ms = kt["assign"] / max(kt["assign_n"], 1)
+    use_tc = (not args.force_simt) and d % 8 == 0 and d >= 8
+    if use_tc:
+        flops = 6.0 * n1 * k1 * d  # 3xTF32: three TF32 products per useful multiply-add
+        peak = 0.5 * pk["bf16_tflops"]
+        roof = {"bound": "tensor", "kernel": "K1 tcgen05 3xTF32 assignment (level 1)", "unit": "TFLOP/s",
+                "peak_basis": f"TF32 dense = 0.5 x {pk['source']} bf16 {pk['bf16_tflops']} TFLOP/s (nominal ratio)"}
+    else:
+        flops = 3.0 * n1 * k1 * d  # sub + fma per coordinate
+        peak = 148 * 128 * 2 * pk["sm_max_mhz"] * 1e6 / 1e12
+        roof = {"bound": "alu", "kernel": "K2 FP32 SIMT assignment (level 1)", "unit": "TFLOP/s",
+                "peak_basis": "FP32 SIMT = 148 SMs x 128 lanes x 2 flop x sm_max_mhz"}
+    achieved = flops / (assign_avg_ms / 1000.0) / 1e12 if assign_avg_ms > 0 else 0.0
+    roof.update({"achieved": achieved, "peak": peak, "frac": achieved / peak if peak else None,
+                 "traffic": None, "avg_launch_ms": assign_avg_ms,
+                 "share_of_step": kt["assign"] / total_ms if total_ms else None})
+    upd_avg = kt["update"] / max(kt["update_n"], 1)
+    upd_bytes = n1 * d * 4 + n1 * 4 + k1 * (d + 1) * 4
+    upd = {"kernel": "K5 update (sums+counts)", "avg_launch_ms": upd_avg,
+           "achieved_gbs": upd_bytes / (upd_avg / 1000.0) / 1e9 if upd_avg > 0 else None,
+           "peak_gbs": pk["hbm_gbs"]}
+    if upd["achieved_gbs"]:
+        upd["frac"] = upd["achieved_gbs"] / pk["hbm_gbs"]
+
+    # ---- recall of the query batch on a sample (oracle exact k-NN is the definition)
+    recall = None
+    if rank == 0 and world == 1:
+        try:
+            import oracle
+
+            m = 200
+            eids, _, gap = oracle.knn_exact(X_host, Q_host[:m], cfg.knn)
+            recall = oracle.recall(ids[:m].cpu().numpy(), eids)
+        except Exception as e:  # the recall sample is a report, not the timed value
+            recall = f"unavailable: {e}"
+
+    # ---- e2e through the C-ABI with HOST buffers (H2D/D2H copies inside the call)
+    e2e = None
+    if not args.no_e2e and world == 1:
+        Xp = torch.from_numpy(X_host).pin_memory().numpy()
+        Qp = torch.from_numpy(np.ascontiguousarray(Q_host)).pin_memory().numpy()
+        h_ms = []
+        for s in range(2):
+            flush.zero_()
+            torch.cuda.synchronize(dev)
+            t0 = time.perf_counter()
+            idx_h = mk.build(Xp, cfg.levels, cfg.iters, inits, flags=mk.MASK_TIME_KERNELS, stream=stream)
+            ids_h, d2_h = idx_h.query(Qp, knn=cfg.knn, beam=1, stream=stream)
+            torch.cuda.synchronize(dev)
+            h_ms.append((time.perf_counter() - t0) * 1000.0)
+            dh, _ = lloyd_distances(idx_h, len(cfg.levels))
+            idx_h.free()
+        e2e = {"value": dh / (min(h_ms) / 1000.0), "unit": UNIT, "ms_per_step": min(h_ms),
+               "h2d_bytes_per_step": int(X_host.nbytes + Q_host.nbytes),
+               "d2h_bytes_per_step": int(ids_h.nbytes + d2_h.nbytes)}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            P0 = X_host[inits[0]]
+            cpu = cpu_baseline(cfg, P0)
+        except Exception as e:
+            cpu = {"value": None, "unit": UNIT, "cores": None, "kind": "oracle", "sample": f"failed: {e}"}
+
+    if rank == 0:
+        clocks = sampler.summary() if sampler else None
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": cfg.name, "n_per_gpu": n_local, "n_global": n_global, "dim": cfg.dim,
+                       "levels": list(cfg.levels), "iters": cfg.iters, "queries": cfg.n_queries * world,
+                       "knn": cfg.knn, "beam": 1, "parallelism": f"dp{world}" if world > 1 else "single",
+                       "l2": "flushed between timed steps (512 MiB write)"},
+            "per_level_distances": per_level, "build_ms": statistics.mean(build_ms),
+            "query_ms": statistics.mean(query_ms),
+            "query_qps": (cfg.n_queries * world) / (statistics.mean(query_ms) / 1000.0),
+            "recall_at_10_sample200": recall, "roofline": roof, "update_roofline": upd,
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches // max(args.steps, 1)),
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    idx.free()
+    if comm:
+        comm.free()
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,218 @@
+/*
+ * mask.h -- C-ABI of libmask.so, the B200 (sm_100a) hot path of MASK
+ * ("Multilevel Approximate Similarity search with k-means", arXiv 2208.02734).
+ *
+ * Citations: "P:n" = line n of the paper text; "D#" = a reading of the paper
+ * recorded in DESIGN.md (the paper is silent/ambiguous there).
+ *
+ * Problem statement implemented:
+ *   - a dataset X of n feature vectors in R^dim under the Euclidean distance;
+ *   - a multilevel index: level 1 clusters X into k[0] prototypes with Lloyd k-means
+ *     (P:654-655), level l+1 clusters the k[l-1] prototypes of level l into k[l]
+ *     (P:634-637), one global k-means per level (D1), seeded random-point initialisation
+ *     (D2), T Lloyd iterations or a tolerance, then a final assignment (D3);
+ *   - batched approximate k-NN: descend from the top level through the children of the
+ *     selected prototype(s) and rank the reached data partition (Algorithm 2).
+ *
+ * Conventions shared by every entry point:
+ *   - every function returns a mask_status (0 = OK, < 0 = error) unless noted; on error
+ *     mask_last_error() returns a thread-local human-readable message;
+ *   - "device" pointers are CUDA global-memory pointers on the caller's current device;
+ *     "host" pointers are ordinary (preferably pinned) host memory.  mask_matrix.memory
+ *     says which one its arrays are;
+ *   - `stream` is a cudaStream_t passed as void* (NULL = the legacy default stream).  All
+ *     work is enqueued on it and every call returns only after the stream has completed the
+ *     call's work, so device faults surface as MASK_ERR_CUDA from the same call;
+ *   - all input pointers are borrowed for the duration of the call only, except with
+ *     MASK_BORROW_DATA (see mask_build);
+ *   - the library never falls back to the CPU: every arithmetic step runs in its CUDA
+ *     kernels; a missing GPU is MASK_ERR_CUDA.
+ */
+#ifndef MASK_H_
+#define MASK_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MASK_ABI_VERSION 1
+
+typedef enum {
+  MASK_OK = 0,
+  MASK_ERR_ARG = -1,         /* invalid argument / shape / inconsistent CSR               */
+  MASK_ERR_NONFINITE = -2,   /* NaN/Inf input (only checked with MASK_VALIDATE_FINITE)    */
+  MASK_ERR_OOM = -3,         /* device allocation failed                                  */
+  MASK_ERR_CUDA = -4,        /* CUDA runtime/launch/device fault, or no usable GPU        */
+  MASK_ERR_NCCL = -5,        /* NCCL failure (multi-GPU)                                  */
+  MASK_ERR_UNSUPPORTED = -6  /* valid request this build does not implement               */
+} mask_status;
+
+/* mask_matrix.format */
+enum { MASK_DENSE_F32 = 0, MASK_CSR_F32 = 1 };
+/* mask_matrix.memory */
+enum { MASK_MEM_DEVICE = 0, MASK_MEM_HOST = 1 };
+/* mask_build_params.empty_policy (D5) */
+enum { MASK_EMPTY_KEEP = 0 };
+/* mask_build_params.flags */
+enum {
+  MASK_VALIDATE_FINITE = 1 << 0, /* scan inputs for NaN/Inf -> MASK_ERR_NONFINITE          */
+  MASK_BORROW_DATA = 1 << 1,     /* index keeps a pointer to device `data` instead of a copy */
+  MASK_FORCE_SIMT = 1 << 2,      /* dense assignment on the FP32 SIMT kernel only (testing) */
+  MASK_NO_FIXUP = 1 << 3,        /* disable the near-tie re-check of the tensor path (testing)*/
+  MASK_SYNC_STATS = 1 << 4,      /* reserved: J/changed are read every pass (always on)       */
+  MASK_TIME_KERNELS = 1 << 5     /* record CUDA-event device times of the step kernels        */
+};
+
+/* kernel classes of mask_get_timing */
+enum { MASK_T_ASSIGN = 0, MASK_T_FIXUP = 1, MASK_T_UPDATE = 2, MASK_T_FINALIZE = 3, MASK_T_NCLASS = 4 };
+
+/*
+ * A matrix of `rows` points in R^dim.
+ *   MASK_DENSE_F32: `values` = rows*dim fp32, row-major, row stride dim.
+ *   MASK_CSR_F32:   row_ptr = rows+1 int64 (row_ptr[0] = 0, non-decreasing, row_ptr[rows]
+ *                   = nnz), col_idx = nnz int32 strictly increasing within a row and < dim,
+ *                   values = nnz fp32.
+ * Multi-GPU (mask_build with a communicator): the matrix is this rank's shard, global rows
+ * [row_offset, row_offset + rows) of an n_global-row dataset.  Single GPU: row_offset = 0,
+ * n_global = rows.
+ */
+typedef struct {
+  int32_t format;          /* MASK_DENSE_F32 | MASK_CSR_F32                          */
+  int32_t memory;          /* MASK_MEM_DEVICE | MASK_MEM_HOST                        */
+  int32_t dim;             /* >= 1                                                   */
+  int32_t _pad;
+  int64_t rows;            /* >= 0 local rows                                        */
+  int64_t n_global;        /* total rows over all ranks (== rows on one GPU)         */
+  int64_t row_offset;      /* first global row of this shard                         */
+  const float* values;     /* dense values or CSR values                             */
+  const int64_t* row_ptr;  /* CSR only                                               */
+  const int32_t* col_idx;  /* CSR only                                               */
+  int64_t nnz;             /* CSR only                                               */
+} mask_matrix;
+
+/*
+ * Test-only step-parity hook, called after every assignment pass of every level (pass =
+ * 0..passes-1, the last one being the final assignment) with HOST copies of the prototypes
+ * P_t (k x dim fp32) that pass used and of the labels it produced (this rank's items).
+ */
+typedef void (*mask_iter_cb)(int32_t level, int32_t pass, const float* P_host, int64_t k,
+                             int32_t dim, const int32_t* labels_host, int64_t n_items,
+                             void* user);
+
+typedef struct {
+  int32_t num_levels;             /* L >= 1                                                */
+  int32_t max_iters;              /* T >= 0 Lloyd (assign, update) pairs (D3)              */
+  const int64_t* k;               /* host, k[0..L-1] bottom first; 1 <= k[l] <= n_l where
+                                     n_0 = n_global, n_l = k[l-1]                          */
+  double tol;                     /* >= 0; > 0 also stops when max_j |c_j'-c_j| <= tol     */
+  uint64_t seed;                  /* reserved (init indices are passed explicitly)         */
+  const int64_t* const* init_idx; /* host; init_idx[l] = k[l] distinct indices into the
+                                     level-l input (global row ids for level 1) (D2)       */
+  int32_t empty_policy;           /* MASK_EMPTY_KEEP                                       */
+  int32_t flags;                  /* MASK_* flags above                                    */
+  mask_iter_cb iter_cb;           /* NULL in production                                    */
+  void* iter_cb_user;
+} mask_build_params;
+
+typedef struct mask_comm mask_comm;   /* wraps an NCCL communicator; NULL = single GPU */
+typedef struct mask_index mask_index; /* opaque; owns every device buffer it allocated */
+
+/* ---------------------------------------------------------------- library */
+int32_t mask_abi_version(void);
+/* thread-local message of the last failure on this thread ("" if none); never NULL */
+const char* mask_last_error(void);
+/* 1 if a CUDA device usable by this build (sm_100) is present, else 0 */
+int32_t mask_device_ok(void);
+
+/* ---------------------------------------------------------------- multi-GPU
+ * One process per GPU.  Rank 0 calls mask_comm_unique_id, the caller broadcasts the 128
+ * bytes over its own process group, then every rank calls mask_comm_init (collective).
+ * The communicator is used by mask_build (one allreduce of [sums | counts] per Lloyd
+ * iteration, BASELINE.json north_star) and must outlive the builds that use it. */
+int32_t mask_comm_unique_id(uint8_t id_out[128]);
+int32_t mask_comm_init(const uint8_t id[128], int32_t world, int32_t rank, mask_comm** out);
+void mask_comm_free(mask_comm* comm); /* NULL-safe */
+
+/* ---------------------------------------------------------------- build
+ * Build the multilevel index (Algorithm 1 levels, read as one global Lloyd
+ * k-means per level, D1).  Collective over `comm` when comm != NULL (every rank calls it
+ * with identical params and its own shard).  On success *out owns: per level the
+ * prototypes (k_l x dim fp32), labels of the level's items, child lists, the per-pass trace
+ * (J_t, changed_t); and a copy of the data for leaf scans (all n_global rows on every rank
+ * after the build), unless MASK_BORROW_DATA is set with device data on one GPU, in which
+ * case the caller keeps `data` alive and unchanged until mask_free.
+ * Errors: MASK_ERR_ARG (L < 1, k[l] out of range, bad init indices, bad CSR, dim < 1),
+ * MASK_ERR_NONFINITE, MASK_ERR_OOM, MASK_ERR_CUDA, MASK_ERR_NCCL. *out is NULL on error. */
+int32_t mask_build(const mask_matrix* data, const mask_build_params* params, mask_comm* comm,
+                   void* stream, mask_index** out);
+
+/* ---------------------------------------------------------------- query
+ * Batched approximate k-NN (Algorithm 2) of `queries` (same dim/format family
+ * as the index: dense queries against a dense index, CSR queries against a CSR index).
+ * beam b >= 1 prototypes are kept per level (b = 1 is Algorithm 2; D7); childless
+ * prototypes are skipped.  Results: ids_out[q*k_nn + r] (global row id, int64) and
+ * d2_out[...] (squared Euclidean distance, fp32) sorted by (d2, id) (D4); a partition
+ * smaller than k_nn is padded with (-1, +inf) (D8).  Output buffers live in the same
+ * memory kind as `queries` (device or host).  Non-collective; concurrent calls on one
+ * index are allowed.  Errors: MASK_ERR_ARG (k_nn < 1 or > 32, beam < 1 or > 32, dim or
+ * format mismatch), MASK_ERR_CUDA. */
+int32_t mask_query(const mask_index* idx, const mask_matrix* queries, int32_t k_nn,
+                   int32_t beam, int64_t* ids_out, float* d2_out, void* stream);
+
+void mask_free(mask_index* idx); /* NULL-safe */
+
+/* ---------------------------------------------------------------- step entry points
+ * The two Lloyd steps of one level as separate calls (the §8(a) rows a3-a7, a9), used by
+ * the kernel parity tests and the per-kernel timing of bench.py.  Single GPU.
+ *
+ * mask_assign: a_i = argmin_j ||x_i - c_j||^2 (lowest j on ties, D4) for every
+ * row of `data` against prototypes P (device, k x dim fp32, row-major).  Writes device
+ * labels_out[rows] (int32) and, if non-NULL, device d2_out[rows] (fp32 squared distance
+ * to the chosen prototype).  Dense rows use the tcgen05 3xTF32 kernel with a near-tie
+ * FP32 re-check when dim allows, else the FP32 SIMT kernel; CSR rows the sparse kernel.
+ * *n_flagged (optional, host) receives the number of rows the near-tie re-check recomputed.
+ */
+int32_t mask_assign(const mask_matrix* data, const float* P, int64_t k, int32_t flags,
+                    int32_t* labels_out, float* d2_out, int64_t* n_flagged, void* stream);
+
+/* mask_update: P_out_j = mean of the rows with labels == j, or P_in_j if none (D5).
+ * P_in/P_out device k x dim fp32 (may alias); counts_out device int32[k] (optional).
+ * *max_disp (optional, host) = max_j ||P_out_j - P_in_j||. */
+int32_t mask_update(const mask_matrix* data, const int32_t* labels, int64_t k,
+                    const float* P_in, float* P_out, int32_t* counts_out, double* max_disp,
+                    void* stream);
+
+/* ---------------------------------------------------------------- introspection
+ * Levels are numbered 1..L (level 1 = prototypes over the data). Host outputs. */
+int32_t mask_num_levels(const mask_index* idx);
+int32_t mask_level_info(const mask_index* idx, int32_t level, int64_t* n_items, int64_t* k,
+                        int32_t* dim, int32_t* passes, int32_t* updates);
+int32_t mask_get_prototypes(const mask_index* idx, int32_t level, float* host_out /* k*dim */);
+int32_t mask_get_labels(const mask_index* idx, int32_t level,
+                        int32_t* host_out /* n_items of the level (level 1: n_global) */);
+/* children of prototype j: members[offsets[j] .. offsets[j+1]) in ascending item id */
+int32_t mask_get_children(const mask_index* idx, int32_t level, int64_t* host_offsets /* k+1 */,
+                          int64_t* host_members /* n_items */);
+/* per assignment pass: J_t = sum_i ||y_i - c_{a_i}||^2 (GPU estimate), changed_t = rows whose
+ * label changed vs the previous pass (all rows at pass 0), empties_t = prototypes left
+ * without members by the update that followed (0 for the final pass).  Returns the number
+ * of passes written (<= cap) or < 0 on error. */
+int32_t mask_get_trace(const mask_index* idx, int32_t level, double* J, int64_t* changed,
+                       int64_t* empties, int32_t cap);
+
+/* ---------------------------------------------------------------- diagnostics
+ * Cumulative number of CUDA kernel launches issued by this library in this process. */
+int64_t mask_kernel_launches(void);
+/* Device time of the step kernels of one level, measured with CUDA events recorded on the
+ * build stream around each launch (only when the build ran with MASK_TIME_KERNELS):
+ * out[2*c] = total milliseconds, out[2*c+1] = number of launches, for kernel class
+ * c = MASK_T_ASSIGN .. MASK_T_FINALIZE; cap = number of doubles out can hold (>= 2*c+2 for
+ * class c to be written).  Returns the number of doubles written or < 0 on error. */
+int32_t mask_get_timing(const mask_index* idx, int32_t level, double* out, int32_t cap);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MASK_H_ */

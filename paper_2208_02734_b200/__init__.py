@@ -1,0 +1,24 @@
+"""B200-native MASK hot path: multilevel Lloyd k-means index build + batched k-NN query.
+
+MASK = "Multilevel Approximate Similarity search with k-means" (arXiv 2208.02734).  The
+compute lives in ``libmask.so`` (hand-written sm_100a CUDA behind the C-ABI of
+``include/mask.h``); this package is the argument-marshalling binding plus host-side
+sharding helpers.  Importing it does not require a GPU; calling it does (no CPU fallback).
+"""
+from . import _lib
+from .api import Comm, Csr, Index, assign, build, device_ok, kernel_launches, matrix, update
+from ._lib import (
+    MASK_BORROW_DATA,
+    MASK_FORCE_SIMT,
+    MASK_NO_FIXUP,
+    MASK_TIME_KERNELS,
+    MASK_VALIDATE_FINITE,
+    MaskError,
+)
+from .shard import query_range, row_range
+
+__all__ = [
+    "Comm", "Csr", "Index", "assign", "build", "device_ok", "kernel_launches", "matrix", "update", "row_range",
+    "query_range", "MaskError", "MASK_BORROW_DATA", "MASK_FORCE_SIMT", "MASK_NO_FIXUP",
+    "MASK_VALIDATE_FINITE", "MASK_TIME_KERNELS",
+]

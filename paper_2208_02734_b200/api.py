@@ -1,0 +1,303 @@
+"""Thin Python binding over the libmask C-ABI (include/mask.h): argument marshalling only.
+
+Every step of the hot path runs in libmask.so's CUDA kernels; this module turns torch
+tensors / numpy arrays into pointers and sizes, calls the C entry point of the same name,
+and wraps the returned handle.  PyTorch is used for device memory and streams only.
+
+Dense data: a 2-D float32 tensor (CUDA -> device memory, CPU/numpy -> host memory).
+Sparse data: a ``Csr(row_ptr int64, col int32, val float32, dim)`` of tensors/arrays.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Any, Callable, List, Optional, Sequence, Tuple
+
+import numpy as np
+
+from . import _lib
+from ._lib import MaskBuildParams, MaskMatrix, check, load
+
+try:
+    import torch
+except ImportError:  # pragma: no cover - torch is part of the image
+    torch = None
+
+
+@dataclass
+class Csr:
+    row_ptr: Any
+    col: Any
+    val: Any
+    dim: int
+
+    @property
+    def rows(self) -> int:
+        return int(self.row_ptr.shape[0]) - 1
+
+
+def _is_cuda(a) -> bool:
+    return torch is not None and isinstance(a, torch.Tensor) and a.is_cuda
+
+
+def _ptr(a) -> int:
+    if a is None:
+        return 0
+    if torch is not None and isinstance(a, torch.Tensor):
+        return a.data_ptr()
+    return a.ctypes.data
+
+
+def _prep(a, dtype):
+    """Contiguous array of the requested dtype, keeping device placement."""
+    if torch is not None and isinstance(a, torch.Tensor):
+        tdt = {np.float32: torch.float32, np.int32: torch.int32, np.int64: torch.int64}[dtype]
+        if a.dtype != tdt:
+            raise TypeError(f"expected {tdt}, got {a.dtype}")
+        return a.contiguous()
+    a = np.ascontiguousarray(a)
+    if a.dtype != dtype:
+        raise TypeError(f"expected {np.dtype(dtype)}, got {a.dtype}")
+    return a
+
+
+def matrix(data, n_global: Optional[int] = None, row_offset: int = 0) -> Tuple[MaskMatrix, tuple]:
+    """mask_matrix for dense (2-D float32) or Csr data; returns (struct, keepalive)."""
+    m = MaskMatrix()
+    if isinstance(data, Csr):
+        rp = _prep(data.row_ptr, np.int64)
+        col = _prep(data.col, np.int32)
+        val = _prep(data.val, np.float32)
+        dev = _is_cuda(rp)
+        if dev != _is_cuda(col) or dev != _is_cuda(val):
+            raise ValueError("CSR arrays must all live on the same side")
+        m.format = _lib.MASK_CSR_F32
+        m.memory = _lib.MASK_MEM_DEVICE if dev else _lib.MASK_MEM_HOST
+        m.dim = int(data.dim)
+        m.rows = int(rp.shape[0]) - 1
+        m.values, m.row_ptr, m.col_idx = _ptr(val), _ptr(rp), _ptr(col)
+        m.nnz = int(col.shape[0])
+        keep = (rp, col, val)
+    else:
+        x = _prep(data, np.float32)
+        if x.ndim != 2:
+            raise ValueError("dense data must be 2-D (rows x dim)")
+        m.format = _lib.MASK_DENSE_F32
+        m.memory = _lib.MASK_MEM_DEVICE if _is_cuda(x) else _lib.MASK_MEM_HOST
+        m.dim = int(x.shape[1])
+        m.rows = int(x.shape[0])
+        m.values = _ptr(x)
+        keep = (x,)
+    m.n_global = m.rows if n_global is None else int(n_global)
+    m.row_offset = int(row_offset)
+    return m, keep
+
+
+def _stream(stream) -> int:
+    if stream is not None:
+        return int(stream.cuda_stream) if hasattr(stream, "cuda_stream") else int(stream)
+    if torch is not None and torch.cuda.is_available():
+        return int(torch.cuda.current_stream().cuda_stream)
+    return 0
+
+
+class Comm:
+    """NCCL communicator (one process per GPU); id exchanged over the caller's process group."""
+
+    def __init__(self, handle: int, world: int, rank: int):
+        self.handle = handle
+        self.world = world
+        self.rank = rank
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = (C.c_uint8 * 128)()
+        check(load().mask_comm_unique_id(C.cast(buf, C.c_void_p)))
+        return bytes(buf)
+
+    @classmethod
+    def init(cls, uid: bytes, world: int, rank: int) -> "Comm":
+        buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+        out = C.c_void_p()
+        check(load().mask_comm_init(C.cast(buf, C.c_void_p), world, rank, C.byref(out)))
+        return cls(out.value, world, rank)
+
+    @classmethod
+    def from_process_group(cls) -> "Comm":
+        """Create from an initialised torch.distributed default group (broadcasts the id)."""
+        import torch.distributed as dist
+
+        rank, world = dist.get_rank(), dist.get_world_size()
+        obj = [cls.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        return cls.init(obj[0], world, rank)
+
+    def free(self) -> None:
+        if self.handle:
+            load().mask_comm_free(self.handle)
+            self.handle = None
+
+
+class Index:
+    """A built multilevel index (owns its device memory until ``free``)."""
+
+    def __init__(self, handle: int, keep: tuple, dim: int, csr: bool):
+        self.handle = handle
+        self._keep = keep  # borrowed data must outlive the index (MASK_BORROW_DATA)
+        self.dim = dim
+        self.csr = csr
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+    def free(self) -> None:
+        if getattr(self, "handle", None):
+            load().mask_free(self.handle)
+            self.handle = None
+
+    # ---------------------------------------------------------------- query
+    def query(self, queries, knn: int = 10, beam: int = 1, stream=None, out=None):
+        """Batched k-NN (Algorithm 2).  Device queries -> device (ids int64, d2 float32)
+        tensors; host queries -> numpy arrays."""
+        m, keep = matrix(queries)
+        nq = m.rows
+        if m.memory == _lib.MASK_MEM_DEVICE:
+            dev = (keep[0]).device
+            ids = out[0] if out is not None else torch.empty((nq, knn), dtype=torch.int64, device=dev)
+            d2 = out[1] if out is not None else torch.empty((nq, knn), dtype=torch.float32, device=dev)
+        else:
+            ids = out[0] if out is not None else np.empty((nq, knn), np.int64)
+            d2 = out[1] if out is not None else np.empty((nq, knn), np.float32)
+        check(load().mask_query(self.handle, C.byref(m), knn, beam, _ptr(ids), _ptr(d2), _stream(stream)))
+        del keep
+        return ids, d2
+
+    # ---------------------------------------------------------------- introspection
+    @property
+    def num_levels(self) -> int:
+        return int(load().mask_num_levels(self.handle))
+
+    def level_info(self, level: int) -> dict:
+        n, k = C.c_int64(), C.c_int64()
+        d, passes, upd = C.c_int32(), C.c_int32(), C.c_int32()
+        check(load().mask_level_info(self.handle, level, C.byref(n), C.byref(k), C.byref(d), C.byref(passes),
+                                     C.byref(upd)))
+        return dict(n_items=n.value, k=k.value, dim=d.value, passes=passes.value, updates=upd.value)
+
+    def prototypes(self, level: int) -> np.ndarray:
+        info = self.level_info(level)
+        out = np.empty((info["k"], info["dim"]), np.float32)
+        check(load().mask_get_prototypes(self.handle, level, out.ctypes.data))
+        return out
+
+    def labels(self, level: int) -> np.ndarray:
+        info = self.level_info(level)
+        out = np.empty(info["n_items"], np.int32)
+        check(load().mask_get_labels(self.handle, level, out.ctypes.data))
+        return out
+
+    def children(self, level: int) -> Tuple[np.ndarray, np.ndarray]:
+        info = self.level_info(level)
+        off = np.empty(info["k"] + 1, np.int64)
+        mem = np.empty(max(info["n_items"], 1), np.int64)
+        check(load().mask_get_children(self.handle, level, off.ctypes.data, mem.ctypes.data))
+        return off, mem[: info["n_items"]]
+
+    def trace(self, level: int) -> dict:
+        cap = self.level_info(level)["passes"]
+        J = np.zeros(cap, np.float64)
+        ch = np.zeros(cap, np.int64)
+        em = np.zeros(cap, np.int64)
+        n = load().mask_get_trace(self.handle, level, J.ctypes.data, ch.ctypes.data, em.ctypes.data, cap)
+        if n < 0:
+            check(n)
+        return dict(J=J[:n], changed=ch[:n], empties=em[:n])
+
+    def timing(self, level: int) -> dict:
+        """CUDA-event device times of the step kernels (build with MASK_TIME_KERNELS)."""
+        out = np.zeros(8, np.float64)
+        n = load().mask_get_timing(self.handle, level, out.ctypes.data, 8)
+        if n < 0:
+            check(n)
+        names = ["assign", "fixup", "update", "finalize"]
+        return {nm: dict(ms=float(out[2 * i]), launches=int(out[2 * i + 1])) for i, nm in enumerate(names)}
+
+
+def kernel_launches() -> int:
+    """Cumulative kernel launches issued by libmask in this process."""
+    return int(load().mask_kernel_launches())
+
+
+def build(data, levels: Sequence[int], iters: int, init_idx: Sequence[np.ndarray], tol: float = 0.0,
+          flags: int = 0, comm: Optional[Comm] = None, iter_cb: Optional[Callable] = None, stream=None,
+          n_global: Optional[int] = None, row_offset: int = 0) -> Index:
+    """mask_build: multilevel index over ``data`` (this rank's shard when ``comm`` is given).
+
+    iter_cb(level, pass, P (k x dim float32 numpy), labels (int32 numpy)) is the test-only
+    step-parity hook."""
+    m, keep = matrix(data, n_global=n_global, row_offset=row_offset)
+    L = len(levels)
+    ks = (C.c_int64 * L)(*[int(k) for k in levels])
+    idx_arrays = [np.ascontiguousarray(a, dtype=np.int64) for a in init_idx]
+    if len(idx_arrays) != L:
+        raise ValueError("one init index array per level")
+    ptrs = (C.POINTER(C.c_int64) * L)(*[a.ctypes.data_as(C.POINTER(C.c_int64)) for a in idx_arrays])
+    p = MaskBuildParams()
+    p.num_levels = L
+    p.max_iters = int(iters)
+    p.k = ks
+    p.tol = float(tol)
+    p.seed = 0
+    p.init_idx = ptrs
+    p.empty_policy = _lib.MASK_EMPTY_KEEP
+    p.flags = int(flags)
+    cb_ref = None
+    if iter_cb is not None:
+        def _cb(level, pass_, P, k, dim, labels, n_items, user):
+            Pa = np.ctypeslib.as_array(P, shape=(k, dim)).copy()
+            la = np.ctypeslib.as_array(labels, shape=(n_items,)).copy() if n_items else np.zeros(0, np.int32)
+            iter_cb(int(level), int(pass_), Pa, la)
+
+        cb_ref = _lib.ITER_CB(_cb)
+        p.iter_cb = cb_ref
+    out = C.c_void_p()
+    rc = load().mask_build(C.byref(m), C.byref(p), comm.handle if comm else None, _stream(stream), C.byref(out))
+    check(rc)
+    keep_all = keep if (flags & _lib.MASK_BORROW_DATA) else ()
+    return Index(out.value, keep_all, m.dim, m.format == _lib.MASK_CSR_F32)
+
+
+def assign(data, P, flags: int = 0, stream=None):
+    """mask_assign: one assignment pass on the device. Returns (labels int32, d2 float32, n_flagged)."""
+    m, keep = matrix(data)
+    P = _prep(P, np.float32)
+    n = m.rows
+    dev = P.device
+    labels = torch.empty(n, dtype=torch.int32, device=dev)
+    d2 = torch.empty(n, dtype=torch.float32, device=dev)
+    nf = C.c_int64(0)
+    check(load().mask_assign(C.byref(m), _ptr(P), int(P.shape[0]), int(flags), _ptr(labels), _ptr(d2),
+                             C.byref(nf), _stream(stream)))
+    del keep
+    return labels, d2, int(nf.value)
+
+
+def update(data, labels, P_in, stream=None):
+    """mask_update: member means (empty clusters keep P_in). Returns (P_out, counts, max_disp)."""
+    m, keep = matrix(data)
+    P_in = _prep(P_in, np.float32)
+    labels = _prep(labels, np.int32)
+    P_out = torch.empty_like(P_in)
+    counts = torch.empty(P_in.shape[0], dtype=torch.int32, device=P_in.device)
+    md = C.c_double(0.0)
+    check(load().mask_update(C.byref(m), _ptr(labels), int(P_in.shape[0]), _ptr(P_in), _ptr(P_out),
+                             _ptr(counts), C.byref(md), _stream(stream)))
+    del keep
+    return P_out, counts, float(md.value)
+
+
+def device_ok() -> bool:
+    return bool(load().mask_device_ok())

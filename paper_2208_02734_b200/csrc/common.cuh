@@ -1,0 +1,171 @@
+// common.cuh -- host/device helpers shared by the libmask kernels (not by the oracle).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+#include "../../include/mask.h"
+
+namespace mask {
+
+// Host-side error carried up to the C boundary, which converts it to a mask_status.
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+__host__ __device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
+
+[[noreturn]] inline void fail(int code, const std::string& msg) { throw Error(code, msg); }
+
+#define MASK_CUDA(x)                                                                        \
+  do {                                                                                      \
+    cudaError_t e_ = (x);                                                                   \
+    if (e_ != cudaSuccess)                                                                  \
+      ::mask::fail(e_ == cudaErrorMemoryAllocation ? MASK_ERR_OOM : MASK_ERR_CUDA,          \
+                   std::string(#x) + ": " + cudaGetErrorString(e_) + " (" + __FILE__ + ":" + \
+                       std::to_string(__LINE__) + ")");                                     \
+  } while (0)
+
+// every kernel launch is followed by exactly one MASK_LAUNCH_CHECK (it also counts launches)
+void count_launch();
+#define MASK_LAUNCH_CHECK()           \
+  do {                                \
+    ::mask::count_launch();           \
+    MASK_CUDA(cudaGetLastError());    \
+  } while (0)
+
+#define MASK_REQUIRE(cond, code, msg)               \
+  do {                                                \
+    if (!(cond)) ::mask::fail((code), std::string(msg)); \
+  } while (0)
+
+// Owning device buffer (cudaMalloc/cudaFree).
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DevBuf() = default;
+  explicit DevBuf(size_t count) { alloc(count); }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) { release(); p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+    return *this;
+  }
+  ~DevBuf() { release(); }
+  void alloc(size_t count) {
+    release();
+    n = count;
+    if (count) MASK_CUDA(cudaMalloc(&p, count * sizeof(T)));
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  T* get() const { return p; }
+};
+
+inline unsigned grid_for(int64_t work, int block, int64_t cap = 148LL * 64) {
+  int64_t g = (work + block - 1) / block;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return (unsigned)g;
+}
+
+inline int num_sms() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
+}
+
+// ------------------------------------------------------------------ kernel entry points
+// (defined in the .cu files; all enqueue on `st` and never synchronise)
+
+// K2: FP32 SIMT assignment, direct (x - c)^2 sums; labels + squared distance of the winner.
+void launch_assign_simt(const float* X, int64_t n, int d, const float* P, int64_t k,
+                        int32_t* labels, float* best, cudaStream_t st);
+
+// K1: tcgen05 3xTF32 assignment (dense, d % 8 == 0, d <= 256).  Writes labels, best (d^2
+// estimate incl. ||x||^2), and appends rows whose top-2 gap is within the error bound to
+// flag_rows / flag_count (device).  Returns false if the shape is unsupported.
+bool tc_supported(int64_t n, int d, int64_t k);
+void launch_assign_tc(const float* X, int64_t n, int d, const float* Pb, const float* Ps,
+                      const float* cn2, int64_t k, const float* xn2, int32_t* labels,
+                      float* best, int32_t* flag_rows, int32_t* flag_count, float tau_rel,
+                      cudaStream_t st);
+// K4: exact FP32 direct re-check of flagged rows against all k prototypes.
+void launch_fixup(const float* X, int d, const float* P, int64_t k, const int32_t* flag_rows,
+                  const int32_t* flag_count, int64_t max_flags, int32_t* labels, float* best,
+                  cudaStream_t st);
+// prototype operands for K1: Pb = tf32_rn(-2c), Ps = tf32_rn(-2c - Pb), cn2 = ||c||^2
+void launch_prep_protos(const float* P, int64_t k, int d, float* Pb, float* Ps, float* cn2,
+                        cudaStream_t st);
+void launch_row_norms(const float* X, int64_t n, int d, float* xn2, cudaStream_t st);
+
+// K3: CSR rows x dense prototypes (sparse assignment).
+void launch_assign_csr(const int64_t* row_ptr, const int32_t* col, const float* val, int64_t n,
+                       int d, const float* PT /* d x k transposed */, const float* cn2, int64_t k,
+                       int32_t* labels, float* best, cudaStream_t st);
+void launch_transpose(const float* P, int64_t k, int d, float* PT, cudaStream_t st);
+
+// K5/K6: cluster sums and counts (S, counts must be zeroed by the caller).
+void launch_update_dense(const float* X, int64_t n, int d, const int32_t* labels, int64_t k,
+                         float* S, int32_t* counts, cudaStream_t st);
+void launch_update_csr(const int64_t* row_ptr, const int32_t* col, const float* val, int64_t n,
+                       int d, const int32_t* labels, float* S, int32_t* counts, cudaStream_t st);
+// K7: P_j <- S_j / n_j (keep if n_j == 0); zeroes S and counts; stats[0] = max disp^2 (as
+// float bits, atomicMax), stats[1] = empties.  `stat` must be zeroed by the caller.
+void launch_finalize(float* P, float* S, int32_t* counts, int64_t k, int d, uint32_t* stat,
+                     int keep_counts, cudaStream_t st);
+// pass statistics: J = sum best (double), changed = #(cur != prev)
+void launch_pass_stats(const int32_t* cur, const int32_t* prev, const float* best, int64_t n,
+                       double* J, unsigned long long* changed, cudaStream_t st);
+// K10: P[j] = Y[idx[j]] (dense) / densified CSR row
+void launch_gather_rows(const float* Y, int d, const int64_t* idx, int64_t k, int64_t row_offset,
+                        int64_t n_local, float* P, cudaStream_t st);
+void launch_gather_csr_rows(const int64_t* row_ptr, const int32_t* col, const float* val, int d,
+                            const int64_t* idx, int64_t k, int64_t row_offset, int64_t n_local,
+                            float* P, cudaStream_t st);
+// K8: child lists by counting sort: offsets (k+1, int64), members (n, int32; order within a
+// segment unspecified)
+void launch_children(const int32_t* labels, int64_t n, int64_t k, int64_t* offsets,
+                     int32_t* members, int32_t* cursor_ws, cudaStream_t st);
+// finite check: flag set to 1 if any non-finite value
+void launch_check_finite(const float* v, int64_t count, int32_t* flag, cudaStream_t st);
+
+// K9: batched query descent.
+struct QLevel {
+  const float* P;
+  const int64_t* offsets;
+  const int32_t* members;
+  int64_t k;
+};
+constexpr int kMaxLevels = 16;
+struct QIndex {
+  QLevel lv[kMaxLevels];
+  int L;
+  int dim;
+  const float* X;           // dense data rows (n x dim) or nullptr
+  const int64_t* xrp;       // CSR data
+  const int32_t* xcol;
+  const float* xval;
+};
+void launch_query_dense(const QIndex& qi, const float* Q, int64_t nq, int knn, int beam,
+                        int64_t* ids, float* d2, cudaStream_t st);
+void launch_query_csr(const QIndex& qi, const float* cn2_levels_flat, const int64_t* cn2_off,
+                      const int64_t* qrp, const int32_t* qcol, const float* qval, int64_t nq,
+                      int knn, int beam, int64_t* ids, float* d2, cudaStream_t st);
+void launch_level_norms(const float* P, int64_t k, int d, float* cn2, cudaStream_t st);
+
+}  // namespace mask

@@ -1,0 +1,537 @@
+// kernels_lloyd.cu -- SIMT kernels of one Lloyd level:
+//   K2  FP32 SIMT assignment (small d / upper levels / fallback)
+//   K4  near-tie FP32 re-check of rows flagged by the tensor-core assignment (K1)
+//   K5  dense cluster sums + counts,  K6 CSR cluster sums + counts
+//   K7  finalize: c_j <- S_j / n_j, keep empty (D5), displacement, empties
+//   K8  child lists by counting sort
+//   K10 seeded-init gather
+// plus per-pass statistics, row norms and the 3xTF32 prototype operand split.
+//
+// Paper: assignment = `euclideanDistance` + `searchPosMin`, update =
+// k-means prototype = mean of members, levels P:631-638.
+#include <cuda_runtime.h>
+
+#include <cfloat>
+#include <cstdint>
+
+#include "common.cuh"
+
+namespace mask {
+
+// ====================================================================== K2 SIMT assignment
+// One thread per row; prototypes staged through shared memory in chunks and read by
+// broadcast.  Direct squared distance sum_i (x_i - c_i)^2 with FP32 FMA accumulation;
+// strict "<" over ascending j keeps the lowest ordinal on ties (D4).
+template <int DT>
+__global__ void __launch_bounds__(256) k_assign_simt(const float* __restrict__ X, int64_t n,
+                                                     int d, const float* __restrict__ P,
+                                                     int64_t k, int kc_max,
+                                                     int32_t* __restrict__ labels,
+                                                     float* __restrict__ best_out) {
+  extern __shared__ float sP[];
+  const int D = DT > 0 ? DT : d;
+  const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool valid = row < n;
+  float x[DT > 0 ? DT : 1];
+  if (DT > 0) {
+#pragma unroll
+    for (int i = 0; i < (DT > 0 ? DT : 1); ++i) x[i] = valid ? X[row * D + i] : 0.f;
+  }
+  float b1 = INFINITY;
+  int64_t a = 0;
+  for (int64_t j0 = 0; j0 < k; j0 += kc_max) {
+    const int kc = (int)min64(kc_max, k - j0);
+    __syncthreads();
+    for (int t = threadIdx.x; t < kc * D; t += blockDim.x) sP[t] = P[j0 * D + t];
+    __syncthreads();
+    if (valid) {
+      for (int jj = 0; jj < kc; ++jj) {
+        const float* c = sP + jj * D;
+        float s = 0.f;
+        if (DT > 0) {
+#pragma unroll
+          for (int i = 0; i < (DT > 0 ? DT : 1); ++i) {
+            float t = x[i] - c[i];
+            s = fmaf(t, t, s);
+          }
+        } else {
+          const float* xr = X + row * D;
+          for (int i = 0; i < D; ++i) {
+            float t = __ldg(xr + i) - c[i];
+            s = fmaf(t, t, s);
+          }
+        }
+        if (s < b1) {
+          b1 = s;
+          a = j0 + jj;
+        }
+      }
+    }
+  }
+  if (valid) {
+    labels[row] = (int32_t)a;
+    if (best_out) best_out[row] = b1;
+  }
+}
+
+void launch_assign_simt(const float* X, int64_t n, int d, const float* P, int64_t k,
+                        int32_t* labels, float* best, cudaStream_t st) {
+  if (n <= 0) return;
+  const int block = 256;
+  int kc = (int)min64(k, 40 * 1024 / (4 * (int64_t)d));
+  if (kc < 1) kc = 1;
+  size_t smem = (size_t)kc * d * sizeof(float);
+  if (smem > 48 * 1024) {
+    MASK_REQUIRE(smem <= 200 * 1024, MASK_ERR_UNSUPPORTED, "SIMT assignment: dim too large");
+  }
+  unsigned grid = (unsigned)((n + block - 1) / block);
+#define MASK_SIMT_CASE(DV)                                                                \
+  case DV: {                                                                              \
+    if (smem > 48 * 1024)                                                                 \
+      MASK_CUDA(cudaFuncSetAttribute(k_assign_simt<DV>,                                   \
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+    k_assign_simt<DV><<<grid, block, smem, st>>>(X, n, d, P, k, kc, labels, best);        \
+    break;                                                                                \
+  }
+  switch (d) {
+    MASK_SIMT_CASE(1)
+    MASK_SIMT_CASE(2)
+    MASK_SIMT_CASE(3)
+    MASK_SIMT_CASE(4)
+    MASK_SIMT_CASE(8)
+    MASK_SIMT_CASE(16)
+    MASK_SIMT_CASE(32)
+    MASK_SIMT_CASE(64)
+    default: {
+      if (smem > 48 * 1024)
+        MASK_CUDA(cudaFuncSetAttribute(k_assign_simt<0>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      k_assign_simt<0><<<grid, block, smem, st>>>(X, n, d, P, k, kc, labels, best);
+    }
+  }
+#undef MASK_SIMT_CASE
+  MASK_LAUNCH_CHECK();
+}
+
+// ====================================================================== K4 near-tie re-check
+// One warp per flagged row: lanes sweep the prototypes (j = lane, lane+32, ...) with the
+// direct FP32 form, then a warp (d^2, j) argmin.  Rewrites labels[row] and best[row].
+__global__ void __launch_bounds__(256) k_fixup(const float* __restrict__ X, int d,
+                                               const float* __restrict__ P, int64_t k,
+                                               const int32_t* __restrict__ flag_rows,
+                                               const int32_t* __restrict__ flag_count,
+                                               int64_t max_flags, int32_t* __restrict__ labels,
+                                               float* __restrict__ best) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nf = min64(*flag_count, max_flags);
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t f = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); f < nf;
+       f += warps) {
+    const int64_t row = flag_rows[f];
+    const float* x = X + row * d;
+    float b = INFINITY;
+    int64_t a = INT64_MAX;
+    for (int64_t j = lane; j < k; j += 32) {
+      const float* c = P + j * d;
+      float s = 0.f;
+      for (int i = 0; i < d; ++i) {
+        float t = __ldg(x + i) - __ldg(c + i);
+        s = fmaf(t, t, s);
+      }
+      if (s < b) {
+        b = s;
+        a = j;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      float ob = __shfl_xor_sync(0xffffffffu, b, o);
+      int64_t oa = __shfl_xor_sync(0xffffffffu, a, o);
+      if (ob < b || (ob == b && oa < a)) {
+        b = ob;
+        a = oa;
+      }
+    }
+    if (lane == 0) {
+      labels[row] = (int32_t)a;
+      best[row] = b;
+    }
+  }
+}
+
+void launch_fixup(const float* X, int d, const float* P, int64_t k, const int32_t* flag_rows,
+                  const int32_t* flag_count, int64_t max_flags, int32_t* labels, float* best,
+                  cudaStream_t st) {
+  k_fixup<<<num_sms() * 4, 256, 0, st>>>(X, d, P, k, flag_rows, flag_count, max_flags, labels,
+                                         best);
+  MASK_LAUNCH_CHECK();
+}
+
+// ====================================================================== operand prep
+__device__ __forceinline__ float tf32_rn(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+// One warp per prototype: Pb = tf32(-2c), Ps = tf32(-2c - Pb) (3xTF32 split of the B operand,
+// the factor -2 is exact), cn2 = ||c||^2 accumulated in FP64 then rounded.
+__global__ void k_prep_protos(const float* __restrict__ P, int64_t k, int d, float* __restrict__ Pb,
+                              float* __restrict__ Ps, float* __restrict__ cn2) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t j = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); j < k; j += warps) {
+    double s = 0.0;
+    for (int i = lane; i < d; i += 32) {
+      float c = P[j * d + i];
+      s += (double)c * (double)c;
+      float m2 = -2.f * c;
+      float b = tf32_rn(m2);
+      float r = tf32_rn(m2 - b);
+      if (Pb) Pb[j * d + i] = b;
+      if (Ps) Ps[j * d + i] = r;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0 && cn2) cn2[j] = (float)s;
+  }
+}
+
+void launch_prep_protos(const float* P, int64_t k, int d, float* Pb, float* Ps, float* cn2,
+                        cudaStream_t st) {
+  k_prep_protos<<<grid_for(k * 32, 256), 256, 0, st>>>(P, k, d, Pb, Ps, cn2);
+  MASK_LAUNCH_CHECK();
+}
+
+void launch_level_norms(const float* P, int64_t k, int d, float* cn2, cudaStream_t st) {
+  launch_prep_protos(P, k, d, nullptr, nullptr, cn2, st);
+}
+
+__global__ void k_row_norms(const float* __restrict__ X, int64_t n, int d, float* __restrict__ xn2) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double s = 0.0;
+  const float* x = X + i * d;
+  for (int c = 0; c < d; ++c) {
+    double v = x[c];
+    s += v * v;
+  }
+  xn2[i] = (float)s;
+}
+
+void launch_row_norms(const float* X, int64_t n, int d, float* xn2, cudaStream_t st) {
+  if (n <= 0) return;
+  k_row_norms<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(X, n, d, xn2);
+  MASK_LAUNCH_CHECK();
+}
+
+// ====================================================================== K5 dense update
+// Element-parallel: thread e covers X[e] (coalesced reads), scatters into S[label*d + col]
+// with L2 float atomics (red.global.add); the col == 0 thread counts the row.
+// Rows with d % 4 == 0 use one 16-byte vector red per 4 columns.
+__global__ void k_update_dense_v4(const float4* __restrict__ X4, int64_t n, int d4,
+                                  const int32_t* __restrict__ labels, float* __restrict__ S,
+                                  int32_t* __restrict__ counts) {
+  const int64_t total = n * (int64_t)d4;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += stride) {
+    const int64_t row = e / d4;
+    const int c4 = (int)(e - row * d4);
+    const int32_t j = __ldg(labels + row);
+    float4 v = __ldg(X4 + e);
+    float* dst = S + ((int64_t)j * d4 + c4) * 4;
+    asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "f"(v.x), "f"(v.y),
+                 "f"(v.z), "f"(v.w)
+                 : "memory");
+    if (c4 == 0) atomicAdd(counts + j, 1);
+  }
+}
+
+__global__ void k_update_dense(const float* __restrict__ X, int64_t n, int d,
+                               const int32_t* __restrict__ labels, float* __restrict__ S,
+                               int32_t* __restrict__ counts) {
+  const int64_t total = n * (int64_t)d;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += stride) {
+    const int64_t row = e / d;
+    const int c = (int)(e - row * d);
+    const int32_t j = __ldg(labels + row);
+    atomicAdd(S + (int64_t)j * d + c, __ldg(X + e));
+    if (c == 0) atomicAdd(counts + j, 1);
+  }
+}
+
+void launch_update_dense(const float* X, int64_t n, int d, const int32_t* labels, int64_t k,
+                         float* S, int32_t* counts, cudaStream_t st) {
+  (void)k;
+  if (n <= 0) return;
+  if (d % 4 == 0 && ((uintptr_t)X % 16) == 0) {
+    const int d4 = d / 4;
+    k_update_dense_v4<<<grid_for(n * d4, 256, (int64_t)num_sms() * 16), 256, 0, st>>>(
+        reinterpret_cast<const float4*>(X), n, d4, labels, S, counts);
+  } else {
+    k_update_dense<<<grid_for(n * d, 256, (int64_t)num_sms() * 16), 256, 0, st>>>(X, n, d, labels,
+                                                                                 S, counts);
+  }
+  MASK_LAUNCH_CHECK();
+}
+
+// ====================================================================== K6 CSR update
+// Warp per row: lanes over the row's non-zeros scatter into S[label*d + col].
+__global__ void k_update_csr(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
+                             const float* __restrict__ val, int64_t n, int d,
+                             const int32_t* __restrict__ labels, float* __restrict__ S,
+                             int32_t* __restrict__ counts) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < n; r += warps) {
+    const int32_t j = labels[r];
+    float* Sj = S + (int64_t)j * d;
+    for (int64_t p = rp[r] + lane; p < rp[r + 1]; p += 32) atomicAdd(Sj + col[p], val[p]);
+    if (lane == 0) atomicAdd(counts + j, 1);
+  }
+}
+
+void launch_update_csr(const int64_t* row_ptr, const int32_t* col, const float* val, int64_t n,
+                       int d, const int32_t* labels, float* S, int32_t* counts, cudaStream_t st) {
+  if (n <= 0) return;
+  k_update_csr<<<grid_for(n * 32, 256, (int64_t)num_sms() * 16), 256, 0, st>>>(row_ptr, col, val,
+                                                                              n, d, labels, S,
+                                                                              counts);
+  MASK_LAUNCH_CHECK();
+}
+
+// ====================================================================== K7 finalize
+// Warp per prototype.  stat[0] = max over j of ||c_new - c_old||^2 (float bits, atomicMax on
+// non-negative floats), stat[1] = number of empty prototypes.  S and counts are zeroed for
+// the next pass (unless keep_counts, which leaves counts for the caller to read).
+__global__ void k_finalize(float* __restrict__ P, float* __restrict__ S, int32_t* __restrict__ counts,
+                           int64_t k, int d, uint32_t* __restrict__ stat, int keep_counts) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t j = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); j < k; j += warps) {
+    const int32_t cnt = counts[j];
+    float disp = 0.f;
+    if (cnt > 0) {
+      for (int i = lane; i < d; i += 32) {
+        const float s = S[j * d + i];
+        const float c = __fdiv_rn(s, (float)cnt);
+        const float t = c - P[j * d + i];
+        disp = fmaf(t, t, disp);
+        P[j * d + i] = c;
+        S[j * d + i] = 0.f;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) disp += __shfl_xor_sync(0xffffffffu, disp, o);
+    if (lane == 0) {
+      atomicMax(stat, __float_as_uint(disp));
+      if (cnt == 0) atomicAdd(stat + 1, 1u);
+      if (!keep_counts) counts[j] = 0;
+    }
+  }
+}
+
+void launch_finalize(float* P, float* S, int32_t* counts, int64_t k, int d, uint32_t* stat,
+                     int keep_counts, cudaStream_t st) {
+  k_finalize<<<grid_for(k * 32, 256), 256, 0, st>>>(P, S, counts, k, d, stat, keep_counts);
+  MASK_LAUNCH_CHECK();
+}
+
+// ====================================================================== pass statistics
+__global__ void k_pass_stats(const int32_t* __restrict__ cur, const int32_t* __restrict__ prev,
+                             const float* __restrict__ best, int64_t n, double* __restrict__ J,
+                             unsigned long long* __restrict__ changed) {
+  double s = 0.0;
+  unsigned long long c = 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    s += (double)best[i];
+    c += (cur[i] != prev[i]);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    s += __shfl_xor_sync(0xffffffffu, s, o);
+    c += __shfl_xor_sync(0xffffffffu, c, o);
+  }
+  __shared__ double ss[32];
+  __shared__ unsigned long long sc[32];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) {
+    ss[w] = s;
+    sc[w] = c;
+  }
+  __syncthreads();
+  if (w == 0) {
+    const int nw = blockDim.x >> 5;
+    s = lane < nw ? ss[lane] : 0.0;
+    c = lane < nw ? sc[lane] : 0ull;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      s += __shfl_xor_sync(0xffffffffu, s, o);
+      c += __shfl_xor_sync(0xffffffffu, c, o);
+    }
+    if (lane == 0) {
+      atomicAdd(J, s);
+      atomicAdd(changed, c);
+    }
+  }
+}
+
+void launch_pass_stats(const int32_t* cur, const int32_t* prev, const float* best, int64_t n,
+                       double* J, unsigned long long* changed, cudaStream_t st) {
+  if (n <= 0) return;
+  k_pass_stats<<<grid_for(n, 256, (int64_t)num_sms() * 4), 256, 0, st>>>(cur, prev, best, n, J,
+                                                                         changed);
+  MASK_LAUNCH_CHECK();
+}
+
+// ====================================================================== K10 init gather
+// P[j] = Y[idx[j] - row_offset] if that global row is owned by this shard, else zeros (the
+// multi-GPU init allreduce sums the owners' copies).
+__global__ void k_gather_rows(const float* __restrict__ Y, int d, const int64_t* __restrict__ idx,
+                              int64_t k, int64_t row_offset, int64_t n_local, float* __restrict__ P) {
+  const int64_t total = k * (int64_t)d;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = e / d;
+    const int c = (int)(e - j * d);
+    const int64_t r = idx[j] - row_offset;
+    P[e] = (r >= 0 && r < n_local) ? Y[r * d + c] : 0.f;
+  }
+}
+
+void launch_gather_rows(const float* Y, int d, const int64_t* idx, int64_t k, int64_t row_offset,
+                        int64_t n_local, float* P, cudaStream_t st) {
+  k_gather_rows<<<grid_for(k * d, 256), 256, 0, st>>>(Y, d, idx, k, row_offset, n_local, P);
+  MASK_LAUNCH_CHECK();
+}
+
+__global__ void k_gather_csr_rows(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
+                                  const float* __restrict__ val, int d,
+                                  const int64_t* __restrict__ idx, int64_t k, int64_t row_offset,
+                                  int64_t n_local, float* __restrict__ P) {
+  // P must be zeroed by the caller; warp per prototype scatters its row's non-zeros.
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t j = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); j < k; j += warps) {
+    const int64_t r = idx[j] - row_offset;
+    if (r < 0 || r >= n_local) continue;
+    for (int64_t p = rp[r] + lane; p < rp[r + 1]; p += 32) P[j * d + col[p]] = val[p];
+  }
+}
+
+void launch_gather_csr_rows(const int64_t* row_ptr, const int32_t* col, const float* val, int d,
+                            const int64_t* idx, int64_t k, int64_t row_offset, int64_t n_local,
+                            float* P, cudaStream_t st) {
+  k_gather_csr_rows<<<grid_for(k * 32, 256), 256, 0, st>>>(row_ptr, col, val, d, idx, k, row_offset,
+                                                           n_local, P);
+  MASK_LAUNCH_CHECK();
+}
+
+// ====================================================================== K8 child lists
+__global__ void k_histogram(const int32_t* __restrict__ labels, int64_t n, int32_t* __restrict__ cnt) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(cnt + labels[i], 1);
+}
+
+// Single-block exclusive scan of k counts into offsets[0..k] (k <= a few million).
+__global__ void __launch_bounds__(1024) k_scan_offsets(const int32_t* __restrict__ cnt, int64_t k,
+                                                       int64_t* __restrict__ offsets,
+                                                       int32_t* __restrict__ cursor) {
+  __shared__ int64_t warp_tot[32];
+  __shared__ int64_t carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int64_t base = 0; base < k; base += 1024) {
+    const int64_t j = base + threadIdx.x;
+    int64_t v = j < k ? cnt[j] : 0;
+    int64_t incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int64_t t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    if (lane == 31) warp_tot[w] = incl;
+    __syncthreads();
+    if (w == 0) {
+      int64_t t = warp_tot[lane];
+      int64_t ti = t;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int64_t u = __shfl_up_sync(0xffffffffu, ti, o);
+        if (lane >= o) ti += u;
+      }
+      warp_tot[lane] = ti - t;  // exclusive prefix of warp totals
+    }
+    __syncthreads();
+    const int64_t excl = carry + warp_tot[w] + incl - v;
+    if (j < k) {
+      offsets[j] = excl;
+      cursor[j] = (int32_t)excl;
+    }
+    __syncthreads();
+    if (threadIdx.x == 1023) carry = excl + v;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) offsets[k] = carry;
+}
+
+__global__ void k_scatter_members(const int32_t* __restrict__ labels, int64_t n,
+                                  int32_t* __restrict__ cursor, int32_t* __restrict__ members) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t pos = atomicAdd(cursor + labels[i], 1);
+    members[pos] = (int32_t)i;
+  }
+}
+
+void launch_children(const int32_t* labels, int64_t n, int64_t k, int64_t* offsets,
+                     int32_t* members, int32_t* cursor_ws, cudaStream_t st) {
+  MASK_CUDA(cudaMemsetAsync(cursor_ws, 0, sizeof(int32_t) * k, st));
+  if (n > 0) k_histogram<<<grid_for(n, 256), 256, 0, st>>>(labels, n, cursor_ws);
+  MASK_LAUNCH_CHECK();
+  // counts live in cursor_ws; scan writes offsets and resets cursor to the segment starts
+  k_scan_offsets<<<1, 1024, 0, st>>>(cursor_ws, k, offsets, cursor_ws);
+  MASK_LAUNCH_CHECK();
+  if (n > 0) k_scatter_members<<<grid_for(n, 256), 256, 0, st>>>(labels, n, cursor_ws, members);
+  MASK_LAUNCH_CHECK();
+}
+
+// ====================================================================== misc
+__global__ void k_check_finite(const float* __restrict__ v, int64_t count, int32_t* flag) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x)
+    if (!isfinite(v[i])) *flag = 1;
+}
+
+void launch_check_finite(const float* v, int64_t count, int32_t* flag, cudaStream_t st) {
+  if (count <= 0) return;
+  k_check_finite<<<grid_for(count, 256), 256, 0, st>>>(v, count, flag);
+  MASK_LAUNCH_CHECK();
+}
+
+// PT[i * k + j] = P[j * d + i] (d x k), used by the sparse assignment.
+__global__ void k_transpose(const float* __restrict__ P, int64_t k, int d, float* __restrict__ PT) {
+  __shared__ float tile[32][33];
+  const int64_t j0 = (int64_t)blockIdx.x * 32, i0 = (int64_t)blockIdx.y * 32;
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int64_t j = j0 + r, i = i0 + threadIdx.x;
+    tile[r][threadIdx.x] = (j < k && i < d) ? P[j * d + i] : 0.f;
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int64_t i = i0 + r, j = j0 + threadIdx.x;
+    if (i < d && j < k) PT[i * k + j] = tile[threadIdx.x][r];
+  }
+}
+
+void launch_transpose(const float* P, int64_t k, int d, float* PT, cudaStream_t st) {
+  dim3 grid((unsigned)((k + 31) / 32), (unsigned)((d + 31) / 32));
+  k_transpose<<<grid, dim3(32, 8), 0, st>>>(P, k, d, PT);
+  MASK_LAUNCH_CHECK();
+}
+
+}  // namespace mask

@@ -1,0 +1,955 @@
+// mask_api.cu -- the C-ABI of libmask.so (include/mask.h) and the host orchestrator:
+// argument validation, the level loop (Algorithm 1, read as one global
+// k-means per level, D1), the Lloyd loop of each level (D2/D3/D5), the NCCL
+// combine step for row-sharded multi-GPU builds (BASELINE.json north_star: "each
+// iteration's partial sums and counts are combined with a single NCCL allreduce"), child
+// lists, the query entry point (Algorithm 2) and introspection.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <unordered_set>
+#include <vector>
+
+#include "common.cuh"
+
+#include <atomic>
+
+using namespace mask;
+
+namespace {
+std::atomic<int64_t> g_launches{0};
+}
+
+void mask::count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+namespace {
+
+thread_local std::string g_err;
+
+// CUDA-event timer for one kernel class (MASK_TIME_KERNELS): start/stop recorded on the
+// build stream around the launch, read back at the next stream synchronisation.
+struct KTimer {
+  cudaEvent_t a = nullptr, b = nullptr;
+  bool pending = false;
+  double ms = 0.0;
+  int64_t count = 0;
+  ~KTimer() {
+    if (a) cudaEventDestroy(a);
+    if (b) cudaEventDestroy(b);
+  }
+  void start(cudaStream_t st) {
+    if (!a) {
+      MASK_CUDA(cudaEventCreate(&a));
+      MASK_CUDA(cudaEventCreate(&b));
+    }
+    collect();
+    MASK_CUDA(cudaEventRecord(a, st));
+  }
+  void stop(cudaStream_t st) {
+    MASK_CUDA(cudaEventRecord(b, st));
+    pending = true;
+  }
+  void collect() {
+    if (!pending) return;
+    MASK_CUDA(cudaEventSynchronize(b));
+    float t = 0.f;
+    MASK_CUDA(cudaEventElapsedTime(&t, a, b));
+    ms += t;
+    ++count;
+    pending = false;
+  }
+};
+
+struct Timers {
+  KTimer t[MASK_T_NCLASS];
+  void collect() {
+    for (auto& k : t) k.collect();
+  }
+};
+
+template <class F>
+int32_t guarded(F&& f) {
+  try {
+    g_err.clear();
+    f();
+    return MASK_OK;
+  } catch (const Error& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_err = "host allocation failed";
+    return MASK_ERR_OOM;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return MASK_ERR_CUDA;
+  }
+}
+
+#define MASK_NCCL(x)                                                                     \
+  do {                                                                                   \
+    ncclResult_t r_ = (x);                                                               \
+    if (r_ != ncclSuccess)                                                               \
+      ::mask::fail(MASK_ERR_NCCL, std::string(#x) + ": " + ncclGetErrorString(r_));      \
+  } while (0)
+
+// Pinned host scratch for per-pass statistics.
+struct HostStats {
+  double* J = nullptr;
+  unsigned long long* changed = nullptr;
+  uint32_t* fin = nullptr;
+  int32_t* flags = nullptr;
+  void* base = nullptr;
+  HostStats() {
+    MASK_CUDA(cudaMallocHost(&base, 64));
+    J = reinterpret_cast<double*>(base);
+    changed = reinterpret_cast<unsigned long long*>(static_cast<char*>(base) + 8);
+    fin = reinterpret_cast<uint32_t*>(static_cast<char*>(base) + 16);
+    flags = reinterpret_cast<int32_t*>(static_cast<char*>(base) + 24);
+  }
+  ~HostStats() {
+    if (base) cudaFreeHost(base);
+  }
+};
+
+}  // namespace
+
+struct mask_comm {
+  ncclComm_t comm = nullptr;
+  int world = 1;
+  int rank = 0;
+};
+
+namespace {
+
+struct Level {
+  int64_t n_items = 0;  // items clustered at this level (level 1: n_global)
+  int64_t k = 0;
+  int dim = 0;
+  DevBuf<float> P;            // k x dim
+  DevBuf<int32_t> labels;     // n_items
+  DevBuf<int64_t> offsets;    // k + 1
+  DevBuf<int32_t> members;    // n_items
+  std::vector<double> J;
+  std::vector<int64_t> changed, empties;
+  int updates = 0;
+  double t_ms[MASK_T_NCLASS] = {0, 0, 0, 0};
+  int64_t t_count[MASK_T_NCLASS] = {0, 0, 0, 0};
+};
+
+// A level's input rows as seen by this rank.
+struct Input {
+  int format = MASK_DENSE_F32;
+  int dim = 0;
+  int64_t n_local = 0, n_global = 0, row_offset = 0;
+  const float* X = nullptr;
+  const int64_t* rp = nullptr;
+  const int32_t* col = nullptr;
+  const float* val = nullptr;
+  int64_t nnz = 0;
+};
+
+}  // namespace
+
+struct mask_index {
+  int dim = 0;
+  int format = MASK_DENSE_F32;
+  int64_t n_global = 0;
+  // data rows for leaf scans (global row ids)
+  const float* X = nullptr;
+  const int64_t* rp = nullptr;
+  const int32_t* col = nullptr;
+  const float* val = nullptr;
+  DevBuf<float> own_X, own_val;
+  DevBuf<int64_t> own_rp;
+  DevBuf<int32_t> own_col;
+  std::vector<Level> levels;
+  // sparse-query support: ||c||^2 per level, flattened
+  DevBuf<float> cn2_flat;
+  DevBuf<int64_t> cn2_off;
+};
+
+namespace {
+
+cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+void check_matrix(const mask_matrix* m, const char* what) {
+  MASK_REQUIRE(m != nullptr, MASK_ERR_ARG, std::string(what) + ": NULL matrix");
+  MASK_REQUIRE(m->format == MASK_DENSE_F32 || m->format == MASK_CSR_F32, MASK_ERR_ARG,
+               std::string(what) + ": unknown format");
+  MASK_REQUIRE(m->memory == MASK_MEM_DEVICE || m->memory == MASK_MEM_HOST, MASK_ERR_ARG,
+               std::string(what) + ": unknown memory kind");
+  MASK_REQUIRE(m->dim >= 1, MASK_ERR_ARG, std::string(what) + ": dim must be >= 1");
+  MASK_REQUIRE(m->rows >= 0, MASK_ERR_ARG, std::string(what) + ": rows must be >= 0");
+  MASK_REQUIRE(m->rows < (int64_t(1) << 31), MASK_ERR_UNSUPPORTED,
+               std::string(what) + ": rows must be < 2^31");
+  if (m->rows > 0) MASK_REQUIRE(m->values != nullptr, MASK_ERR_ARG, std::string(what) + ": NULL values");
+  if (m->format == MASK_CSR_F32) {
+    MASK_REQUIRE(m->row_ptr != nullptr && (m->nnz == 0 || m->col_idx != nullptr), MASK_ERR_ARG,
+                 std::string(what) + ": NULL CSR arrays");
+    MASK_REQUIRE(m->nnz >= 0, MASK_ERR_ARG, std::string(what) + ": nnz < 0");
+  }
+}
+
+// Host-side CSR structure check (sorted, unique, in range); device CSR is copied down first.
+void check_csr_structure(const mask_matrix* m, cudaStream_t st) {
+  std::vector<int64_t> rp(m->rows + 1);
+  std::vector<int32_t> col(m->nnz);
+  if (m->memory == MASK_MEM_HOST) {
+    std::memcpy(rp.data(), m->row_ptr, sizeof(int64_t) * rp.size());
+    if (m->nnz) std::memcpy(col.data(), m->col_idx, sizeof(int32_t) * col.size());
+  } else {
+    MASK_CUDA(cudaMemcpyAsync(rp.data(), m->row_ptr, sizeof(int64_t) * rp.size(),
+                              cudaMemcpyDeviceToHost, st));
+    if (m->nnz)
+      MASK_CUDA(cudaMemcpyAsync(col.data(), m->col_idx, sizeof(int32_t) * col.size(),
+                                cudaMemcpyDeviceToHost, st));
+    MASK_CUDA(cudaStreamSynchronize(st));
+  }
+  MASK_REQUIRE(rp[0] == 0 && rp[m->rows] == m->nnz, MASK_ERR_ARG, "CSR: row_ptr[0] must be 0 and row_ptr[rows] == nnz");
+  for (int64_t r = 0; r < m->rows; ++r) {
+    MASK_REQUIRE(rp[r + 1] >= rp[r], MASK_ERR_ARG, "CSR: row_ptr not non-decreasing");
+    for (int64_t p = rp[r]; p < rp[r + 1]; ++p) {
+      MASK_REQUIRE(col[p] >= 0 && col[p] < m->dim, MASK_ERR_ARG, "CSR: column index out of range");
+      if (p > rp[r]) MASK_REQUIRE(col[p] > col[p - 1], MASK_ERR_ARG, "CSR: columns not strictly increasing in a row");
+    }
+  }
+}
+
+// Scratch of one level's Lloyd loop.
+struct LloydWS {
+  DevBuf<int32_t> lab_prev, lab_cur;
+  DevBuf<float> best;
+  DevBuf<float> S;
+  DevBuf<int32_t> counts;
+  DevBuf<double> J;
+  DevBuf<unsigned long long> changed;
+  DevBuf<uint32_t> fin;
+  DevBuf<float> Pb, Ps, cn2, xn2, PT;
+  DevBuf<int32_t> flag_rows, flag_count;
+  bool xn2_ready = false;
+};
+
+// One assignment pass: labels_out[i] = argmin_j ||x_i - c_j||^2, best[i] = its d^2.
+int64_t assign_pass(const Input& in, const float* P, int64_t k, int flags, int32_t* labels_out,
+                    float* best, LloydWS& ws, cudaStream_t st, HostStats* hs, Timers* tm = nullptr) {
+  const int64_t n = in.n_local;
+  const int d = in.dim;
+  if (n == 0) return 0;
+  if (in.format == MASK_CSR_F32) {
+    if (!ws.PT.p) ws.PT.alloc((size_t)k * d);
+    if (!ws.cn2.p) ws.cn2.alloc(k);
+    launch_transpose(P, k, d, ws.PT.p, st);
+    launch_level_norms(P, k, d, ws.cn2.p, st);
+    if (tm) tm->t[MASK_T_ASSIGN].start(st);
+    launch_assign_csr(in.rp, in.col, in.val, n, d, ws.PT.p, ws.cn2.p, k, labels_out, best, st);
+    if (tm) tm->t[MASK_T_ASSIGN].stop(st);
+    return 0;
+  }
+  const bool use_tc = !(flags & MASK_FORCE_SIMT) && tc_supported(n, d, k) &&
+                      ((uintptr_t)in.X % 16 == 0);
+  if (!use_tc) {
+    if (tm) tm->t[MASK_T_ASSIGN].start(st);
+    launch_assign_simt(in.X, n, d, P, k, labels_out, best, st);
+    if (tm) tm->t[MASK_T_ASSIGN].stop(st);
+    return 0;
+  }
+  if (!ws.Pb.p) {
+    ws.Pb.alloc((size_t)k * d);
+    ws.Ps.alloc((size_t)k * d);
+    ws.cn2.alloc(k);
+    ws.flag_rows.alloc(n);
+    ws.flag_count.alloc(1);
+  }
+  if (!ws.xn2_ready) {
+    ws.xn2.alloc(n);
+    launch_row_norms(in.X, n, d, ws.xn2.p, st);
+    ws.xn2_ready = true;
+  }
+  launch_prep_protos(P, k, d, ws.Pb.p, ws.Ps.p, ws.cn2.p, st);
+  MASK_CUDA(cudaMemsetAsync(ws.flag_count.p, 0, sizeof(int32_t), st));
+  if (tm) tm->t[MASK_T_ASSIGN].start(st);
+  launch_assign_tc(in.X, n, d, ws.Pb.p, ws.Ps.p, ws.cn2.p, k, ws.xn2.p, labels_out, best,
+                   ws.flag_rows.p, ws.flag_count.p, 1e-5f, st);
+  if (tm) tm->t[MASK_T_ASSIGN].stop(st);
+  if (!(flags & MASK_NO_FIXUP)) {
+    if (tm) tm->t[MASK_T_FIXUP].start(st);
+    launch_fixup(in.X, d, P, k, ws.flag_rows.p, ws.flag_count.p, n, labels_out, best, st);
+    if (tm) tm->t[MASK_T_FIXUP].stop(st);
+  }
+  if (hs) {
+    MASK_CUDA(cudaMemcpyAsync(hs->flags, ws.flag_count.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    MASK_CUDA(cudaStreamSynchronize(st));
+    return *hs->flags;
+  }
+  return -1;
+}
+
+// Lloyd k-means for one level (SURVEY §8(c) pseudo-code; mirrors the oracle's order):
+//   P <- init rows; for t < T: a <- assign(P); trace; stop if no label changed (t > 0);
+//   P <- means (empty keeps, D5); stop if tol > 0 and max displacement <= tol;
+//   final assignment -> labels.
+void run_level(const Input& in, int64_t k, const int64_t* init_idx_host, const mask_build_params* p,
+               mask_comm* comm, int level_no, cudaStream_t st, Level& L, HostStats& hs) {
+  const int d = in.dim;
+  const int64_t n = in.n_local;
+  L.k = k;
+  L.dim = d;
+  L.P.alloc((size_t)k * d);
+  LloydWS ws;
+  ws.lab_prev.alloc(std::max<int64_t>(n, 1));
+  ws.lab_cur.alloc(std::max<int64_t>(n, 1));
+  ws.best.alloc(std::max<int64_t>(n, 1));
+  ws.S.alloc((size_t)k * d);
+  ws.counts.alloc(k);
+  ws.J.alloc(1);
+  ws.changed.alloc(1);
+  ws.fin.alloc(2);
+  MASK_CUDA(cudaMemsetAsync(ws.S.p, 0, sizeof(float) * k * d, st));
+  MASK_CUDA(cudaMemsetAsync(ws.counts.p, 0, sizeof(int32_t) * k, st));
+  MASK_CUDA(cudaMemsetAsync(ws.lab_prev.p, 0xff, sizeof(int32_t) * std::max<int64_t>(n, 1), st));
+
+  // ---- seeded init (D2): gather the owned init rows, combine across ranks
+  {
+    DevBuf<int64_t> idx(k);
+    MASK_CUDA(cudaMemcpyAsync(idx.p, init_idx_host, sizeof(int64_t) * k, cudaMemcpyHostToDevice, st));
+    if (in.format == MASK_CSR_F32) {
+      MASK_CUDA(cudaMemsetAsync(L.P.p, 0, sizeof(float) * k * d, st));
+      launch_gather_csr_rows(in.rp, in.col, in.val, d, idx.p, k, in.row_offset, n, L.P.p, st);
+    } else {
+      launch_gather_rows(in.X, d, idx.p, k, in.row_offset, n, L.P.p, st);
+    }
+    if (comm) MASK_NCCL(ncclAllReduce(L.P.p, L.P.p, (size_t)k * d, ncclFloat, ncclSum, comm->comm, st));
+    MASK_CUDA(cudaStreamSynchronize(st));
+  }
+
+  auto emit_cb = [&](int pass, const int32_t* labels_dev) {
+    if (!p->iter_cb) return;
+    std::vector<float> Ph((size_t)k * d);
+    std::vector<int32_t> lh(n);
+    MASK_CUDA(cudaMemcpyAsync(Ph.data(), L.P.p, sizeof(float) * Ph.size(), cudaMemcpyDeviceToHost, st));
+    if (n) MASK_CUDA(cudaMemcpyAsync(lh.data(), labels_dev, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st));
+    MASK_CUDA(cudaStreamSynchronize(st));
+    p->iter_cb(level_no, pass, Ph.data(), k, d, lh.data(), n, p->iter_cb_user);
+  };
+
+  // pass statistics (J_t, changed_t), combined over ranks; one 16-byte D2H read per pass
+  auto pass_stats = [&](const int32_t* cur, const int32_t* prev) {
+    MASK_CUDA(cudaMemsetAsync(ws.J.p, 0, sizeof(double), st));
+    MASK_CUDA(cudaMemsetAsync(ws.changed.p, 0, sizeof(unsigned long long), st));
+    launch_pass_stats(cur, prev, ws.best.p, n, ws.J.p, ws.changed.p, st);
+    if (comm) {
+      MASK_NCCL(ncclGroupStart());
+      MASK_NCCL(ncclAllReduce(ws.J.p, ws.J.p, 1, ncclDouble, ncclSum, comm->comm, st));
+      MASK_NCCL(ncclAllReduce(ws.changed.p, ws.changed.p, 1, ncclUint64, ncclSum, comm->comm, st));
+      MASK_NCCL(ncclGroupEnd());
+    }
+    MASK_CUDA(cudaMemcpyAsync(hs.J, ws.J.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+    MASK_CUDA(cudaMemcpyAsync(hs.changed, ws.changed.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    MASK_CUDA(cudaStreamSynchronize(st));
+    L.J.push_back(*hs.J);
+    L.changed.push_back((int64_t)*hs.changed);
+  };
+
+  const int T = p->max_iters;
+  int updates = 0;
+  Timers timers;
+  Timers* tm = (p->flags & MASK_TIME_KERNELS) ? &timers : nullptr;
+  bool fin_pending = false;  // empties of the last update not yet read back (tol == 0)
+  auto read_fin = [&]() {
+    if (!fin_pending) return;
+    L.empties.push_back((int64_t)hs.fin[1]);
+    fin_pending = false;
+  };
+  for (int t = 0; t < T; ++t) {
+    assign_pass(in, L.P.p, k, p->flags, ws.lab_cur.p, ws.best.p, ws, st, nullptr, tm);
+    pass_stats(ws.lab_cur.p, ws.lab_prev.p);  // synchronises the stream
+    read_fin();
+    emit_cb(t, ws.lab_cur.p);
+    if (t > 0 && L.changed.back() == 0) {
+      L.empties.push_back(0);
+      break;
+    }
+    // ---- update: S_j, n_j (K5/K6) -> allreduce (N1) -> P_j = S_j / n_j (K7)
+    if (tm) tm->t[MASK_T_UPDATE].start(st);
+    if (in.format == MASK_CSR_F32)
+      launch_update_csr(in.rp, in.col, in.val, n, d, ws.lab_cur.p, ws.S.p, ws.counts.p, st);
+    else
+      launch_update_dense(in.X, n, d, ws.lab_cur.p, k, ws.S.p, ws.counts.p, st);
+    if (tm) tm->t[MASK_T_UPDATE].stop(st);
+    if (comm) {
+      MASK_NCCL(ncclGroupStart());
+      MASK_NCCL(ncclAllReduce(ws.S.p, ws.S.p, (size_t)k * d, ncclFloat, ncclSum, comm->comm, st));
+      MASK_NCCL(ncclAllReduce(ws.counts.p, ws.counts.p, (size_t)k, ncclInt32, ncclSum, comm->comm, st));
+      MASK_NCCL(ncclGroupEnd());
+    }
+    MASK_CUDA(cudaMemsetAsync(ws.fin.p, 0, sizeof(uint32_t) * 2, st));
+    if (tm) tm->t[MASK_T_FINALIZE].start(st);
+    launch_finalize(L.P.p, ws.S.p, ws.counts.p, k, d, ws.fin.p, 0, st);
+    if (tm) tm->t[MASK_T_FINALIZE].stop(st);
+    ++updates;
+    std::swap(ws.lab_prev, ws.lab_cur);
+    MASK_CUDA(cudaMemcpyAsync(hs.fin, ws.fin.p, sizeof(uint32_t) * 2, cudaMemcpyDeviceToHost, st));
+    fin_pending = true;
+    if (p->tol > 0.0) {
+      MASK_CUDA(cudaStreamSynchronize(st));
+      float maxdisp2;
+      std::memcpy(&maxdisp2, &hs.fin[0], sizeof(float));
+      read_fin();
+      if (std::sqrt((double)maxdisp2) <= p->tol) break;
+    }
+  }
+  // ---- final assignment with the final prototypes (D3)
+  assign_pass(in, L.P.p, k, p->flags, ws.lab_cur.p, ws.best.p, ws, st, nullptr, tm);
+  pass_stats(ws.lab_cur.p, ws.lab_prev.p);
+  read_fin();
+  L.empties.push_back(0);
+  emit_cb((int)L.J.size() - 1, ws.lab_cur.p);
+  L.updates = updates;
+  L.labels = std::move(ws.lab_cur);
+  L.n_items = n;
+  if (tm) {
+    tm->collect();
+    for (int c = 0; c < MASK_T_NCLASS; ++c) {
+      L.t_ms[c] += tm->t[c].ms;
+      L.t_count[c] += tm->t[c].count;
+    }
+  }
+}
+
+// Gather per-rank row blocks into one n_global buffer on every rank (ncclBroadcast per root).
+template <class T>
+void allgather_rows(mask_comm* comm, const T* local, int64_t local_count, T* global,
+                    const std::vector<int64_t>& counts, cudaStream_t st, ncclDataType_t ty) {
+  (void)local_count;
+  int64_t off = 0;
+  MASK_NCCL(ncclGroupStart());
+  for (int r = 0; r < comm->world; ++r) {
+    if (counts[r] > 0)
+      MASK_NCCL(ncclBroadcast(r == comm->rank ? (const void*)local : (const void*)(global + off),
+                              global + off, (size_t)counts[r], ty, r, comm->comm, st));
+    off += counts[r];
+  }
+  MASK_NCCL(ncclGroupEnd());
+}
+
+std::vector<int64_t> allgather_scalar(mask_comm* comm, int64_t v, cudaStream_t st) {
+  DevBuf<int64_t> buf(comm->world);
+  DevBuf<int64_t> mine(1);
+  MASK_CUDA(cudaMemcpyAsync(mine.p, &v, sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  MASK_NCCL(ncclAllGather(mine.p, buf.p, 1, ncclInt64, comm->comm, st));
+  std::vector<int64_t> out(comm->world);
+  MASK_CUDA(cudaMemcpyAsync(out.data(), buf.p, sizeof(int64_t) * comm->world, cudaMemcpyDeviceToHost, st));
+  MASK_CUDA(cudaStreamSynchronize(st));
+  return out;
+}
+
+__global__ void k_add_offset(int64_t* v, int64_t n, int64_t off) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    v[i] += off;
+}
+
+void build_impl(const mask_matrix* data, const mask_build_params* p, mask_comm* comm,
+                cudaStream_t st, mask_index** out) {
+  MASK_REQUIRE(out != nullptr, MASK_ERR_ARG, "out is NULL");
+  *out = nullptr;
+  check_matrix(data, "data");
+  MASK_REQUIRE(p != nullptr, MASK_ERR_ARG, "params is NULL");
+  MASK_REQUIRE(p->num_levels >= 1 && p->num_levels <= kMaxLevels, MASK_ERR_ARG,
+               "num_levels must be in [1, 16]");
+  MASK_REQUIRE(p->max_iters >= 0, MASK_ERR_ARG, "max_iters must be >= 0");
+  MASK_REQUIRE(p->tol >= 0.0, MASK_ERR_ARG, "tol must be >= 0");
+  MASK_REQUIRE(p->k != nullptr && p->init_idx != nullptr, MASK_ERR_ARG, "k / init_idx are NULL");
+  MASK_REQUIRE(p->empty_policy == MASK_EMPTY_KEEP, MASK_ERR_UNSUPPORTED, "only MASK_EMPTY_KEEP");
+  const int world = comm ? comm->world : 1;
+  const int rank = comm ? comm->rank : 0;
+  if (!comm) {
+    MASK_REQUIRE(data->n_global == data->rows && data->row_offset == 0, MASK_ERR_ARG,
+                 "single GPU: n_global must equal rows and row_offset must be 0");
+  } else {
+    MASK_REQUIRE(data->row_offset >= 0 && data->row_offset + data->rows <= data->n_global, MASK_ERR_ARG,
+                 "shard outside [0, n_global)");
+  }
+  const int64_t N = data->n_global;
+  MASK_REQUIRE(N >= 1, MASK_ERR_ARG, "empty dataset");
+  int64_t n_prev = N;
+  for (int l = 0; l < p->num_levels; ++l) {
+    const int64_t k = p->k[l];
+    MASK_REQUIRE(k >= 1 && k <= n_prev, MASK_ERR_ARG,
+                 "k[" + std::to_string(l) + "] must be in [1, n_items of the level]");
+    MASK_REQUIRE(p->init_idx[l] != nullptr, MASK_ERR_ARG, "init_idx[l] is NULL");
+    std::unordered_set<int64_t> seen;
+    seen.reserve((size_t)k * 2);
+    for (int64_t j = 0; j < k; ++j) {
+      const int64_t v = p->init_idx[l][j];
+      MASK_REQUIRE(v >= 0 && v < n_prev, MASK_ERR_ARG, "init index out of range");
+      MASK_REQUIRE(seen.insert(v).second, MASK_ERR_ARG, "init indices must be distinct");
+    }
+    n_prev = k;
+  }
+  if (data->format == MASK_CSR_F32 && data->memory == MASK_MEM_HOST) check_csr_structure(data, st);
+  int ndev = 0;
+  MASK_CUDA(cudaGetDeviceCount(&ndev));
+  MASK_REQUIRE(ndev > 0, MASK_ERR_CUDA, "no CUDA device");
+  if (data->format == MASK_CSR_F32 && data->memory == MASK_MEM_DEVICE) check_csr_structure(data, st);
+
+  auto idx = std::make_unique<mask_index>();
+  idx->dim = data->dim;
+  idx->format = data->format;
+  idx->n_global = N;
+  const int d = data->dim;
+
+  // ---- bring this rank's shard to the device
+  Input in;
+  in.format = data->format;
+  in.dim = d;
+  in.n_local = data->rows;
+  in.n_global = N;
+  in.row_offset = data->row_offset;
+  in.nnz = data->nnz;
+  DevBuf<float> loc_X, loc_val;
+  DevBuf<int64_t> loc_rp;
+  DevBuf<int32_t> loc_col;
+  const bool borrow = (p->flags & MASK_BORROW_DATA) && data->memory == MASK_MEM_DEVICE && !comm;
+  if (data->format == MASK_DENSE_F32) {
+    const size_t cnt = (size_t)data->rows * d;
+    if (data->memory == MASK_MEM_DEVICE && (borrow || comm)) {
+      in.X = data->values;
+    } else {
+      loc_X.alloc(std::max<size_t>(cnt, 1));
+      MASK_CUDA(cudaMemcpyAsync(loc_X.p, data->values, sizeof(float) * cnt,
+                                data->memory == MASK_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, st));
+      in.X = loc_X.p;
+    }
+  } else {
+    if (data->memory == MASK_MEM_DEVICE && (borrow || comm)) {
+      in.rp = data->row_ptr;
+      in.col = data->col_idx;
+      in.val = data->values;
+    } else {
+      const auto kind = data->memory == MASK_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+      loc_rp.alloc(data->rows + 1);
+      loc_col.alloc(std::max<int64_t>(data->nnz, 1));
+      loc_val.alloc(std::max<int64_t>(data->nnz, 1));
+      MASK_CUDA(cudaMemcpyAsync(loc_rp.p, data->row_ptr, sizeof(int64_t) * (data->rows + 1), kind, st));
+      if (data->nnz) {
+        MASK_CUDA(cudaMemcpyAsync(loc_col.p, data->col_idx, sizeof(int32_t) * data->nnz, kind, st));
+        MASK_CUDA(cudaMemcpyAsync(loc_val.p, data->values, sizeof(float) * data->nnz, kind, st));
+      }
+      in.rp = loc_rp.p;
+      in.col = loc_col.p;
+      in.val = loc_val.p;
+    }
+  }
+  if (p->flags & MASK_VALIDATE_FINITE) {
+    DevBuf<int32_t> flag(1);
+    MASK_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(int32_t), st));
+    if (data->format == MASK_DENSE_F32) launch_check_finite(in.X, (int64_t)data->rows * d, flag.p, st);
+    else launch_check_finite(in.val, data->nnz, flag.p, st);
+    int32_t h = 0;
+    MASK_CUDA(cudaMemcpyAsync(&h, flag.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    MASK_CUDA(cudaStreamSynchronize(st));
+    if (comm) {
+      // every rank must agree on the outcome
+      DevBuf<int32_t> f2(1);
+      MASK_CUDA(cudaMemcpyAsync(f2.p, &h, sizeof(int32_t), cudaMemcpyHostToDevice, st));
+      MASK_NCCL(ncclAllReduce(f2.p, f2.p, 1, ncclInt32, ncclMax, comm->comm, st));
+      MASK_CUDA(cudaMemcpyAsync(&h, f2.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+      MASK_CUDA(cudaStreamSynchronize(st));
+    }
+    MASK_REQUIRE(h == 0, MASK_ERR_NONFINITE, "data contains NaN or Inf");
+  }
+
+  HostStats hs;
+  idx->levels.resize(p->num_levels);
+  // ---- level 1: the (sharded) data
+  run_level(in, p->k[0], p->init_idx[0], p, comm, 1, st, idx->levels[0], hs);
+
+  // ---- end of level 1: every rank gets all labels (and all data rows for leaf scans)
+  if (comm && world > 1) {
+    const auto counts = allgather_scalar(comm, data->rows, st);
+    Level& L1 = idx->levels[0];
+    DevBuf<int32_t> glab(N);
+    allgather_rows<int32_t>(comm, L1.labels.p, data->rows, glab.p, counts, st, ncclInt32);
+    L1.labels = std::move(glab);
+    L1.n_items = N;
+    if (data->format == MASK_DENSE_F32) {
+      idx->own_X.alloc((size_t)N * d);
+      std::vector<int64_t> ecounts(world);
+      for (int r = 0; r < world; ++r) ecounts[r] = counts[r] * d;
+      allgather_rows<float>(comm, in.X, data->rows * d, idx->own_X.p, ecounts, st, ncclFloat);
+      idx->X = idx->own_X.p;
+    } else {
+      const auto nnzs = allgather_scalar(comm, data->nnz, st);
+      int64_t total = 0;
+      std::vector<int64_t> nnz_off(world + 1, 0);
+      for (int r = 0; r < world; ++r) nnz_off[r + 1] = nnz_off[r] + nnzs[r];
+      total = nnz_off[world];
+      idx->own_col.alloc(std::max<int64_t>(total, 1));
+      idx->own_val.alloc(std::max<int64_t>(total, 1));
+      idx->own_rp.alloc(N + 1);
+      allgather_rows<int32_t>(comm, in.col, data->nnz, idx->own_col.p, nnzs, st, ncclInt32);
+      allgather_rows<float>(comm, in.val, data->nnz, idx->own_val.p, nnzs, st, ncclFloat);
+      // row_ptr: each rank contributes rows entries rebased by its nnz offset
+      DevBuf<int64_t> rp_loc(std::max<int64_t>(data->rows, 1));
+      if (data->rows) {
+        MASK_CUDA(cudaMemcpyAsync(rp_loc.p, in.rp, sizeof(int64_t) * data->rows, cudaMemcpyDeviceToDevice, st));
+        k_add_offset<<<grid_for(data->rows, 256), 256, 0, st>>>(rp_loc.p, data->rows, nnz_off[rank]);
+        MASK_LAUNCH_CHECK();
+      }
+      allgather_rows<int64_t>(comm, rp_loc.p, data->rows, idx->own_rp.p, counts, st, ncclInt64);
+      MASK_CUDA(cudaMemcpyAsync(idx->own_rp.p + N, &total, sizeof(int64_t), cudaMemcpyHostToDevice, st));
+      idx->rp = idx->own_rp.p;
+      idx->col = idx->own_col.p;
+      idx->val = idx->own_val.p;
+    }
+    MASK_CUDA(cudaStreamSynchronize(st));
+  } else {
+    // single GPU: keep the working copy (or the borrowed pointer)
+    if (data->format == MASK_DENSE_F32) {
+      if (loc_X.p) idx->own_X = std::move(loc_X);
+      idx->X = idx->own_X.p ? idx->own_X.p : in.X;
+    } else {
+      if (loc_rp.p) {
+        idx->own_rp = std::move(loc_rp);
+        idx->own_col = std::move(loc_col);
+        idx->own_val = std::move(loc_val);
+      }
+      idx->rp = idx->own_rp.p ? idx->own_rp.p : in.rp;
+      idx->col = idx->own_col.p ? idx->own_col.p : in.col;
+      idx->val = idx->own_val.p ? idx->own_val.p : in.val;
+    }
+  }
+
+  // ---- levels 2..L: replicated on every rank (P6); rank 0's result is broadcast so the
+  //      replicas stay bitwise identical whatever the atomics' summation order
+  for (int l = 1; l < p->num_levels; ++l) {
+    Level& prev = idx->levels[l - 1];
+    Input up;
+    up.format = MASK_DENSE_F32;
+    up.dim = d;
+    up.n_local = up.n_global = prev.k;
+    up.row_offset = 0;
+    up.X = prev.P.p;
+    run_level(up, p->k[l], p->init_idx[l], p, nullptr, l + 1, st, idx->levels[l], hs);
+    if (comm && world > 1) {
+      Level& L = idx->levels[l];
+      MASK_NCCL(ncclGroupStart());
+      MASK_NCCL(ncclBroadcast(L.P.p, L.P.p, (size_t)L.k * d, ncclFloat, 0, comm->comm, st));
+      MASK_NCCL(ncclBroadcast(L.labels.p, L.labels.p, (size_t)L.n_items, ncclInt32, 0, comm->comm, st));
+      MASK_NCCL(ncclGroupEnd());
+    }
+  }
+  // ---- child lists (K8) for every level
+  for (auto& L : idx->levels) {
+    L.offsets.alloc(L.k + 1);
+    L.members.alloc(std::max<int64_t>(L.n_items, 1));
+    DevBuf<int32_t> cursor(L.k);
+    launch_children(L.labels.p, L.n_items, L.k, L.offsets.p, L.members.p, cursor.p, st);
+    MASK_CUDA(cudaStreamSynchronize(st));
+  }
+  if (idx->format == MASK_CSR_F32) {
+    // ||c||^2 per level for sparse queries
+    int64_t tot = 0;
+    std::vector<int64_t> off(p->num_levels);
+    for (int l = 0; l < p->num_levels; ++l) {
+      off[l] = tot;
+      tot += idx->levels[l].k;
+    }
+    idx->cn2_flat.alloc(tot);
+    idx->cn2_off.alloc(p->num_levels);
+    for (int l = 0; l < p->num_levels; ++l)
+      launch_level_norms(idx->levels[l].P.p, idx->levels[l].k, d, idx->cn2_flat.p + off[l], st);
+    MASK_CUDA(cudaMemcpyAsync(idx->cn2_off.p, off.data(), sizeof(int64_t) * off.size(), cudaMemcpyHostToDevice, st));
+  }
+  MASK_CUDA(cudaStreamSynchronize(st));
+  *out = idx.release();
+}
+
+const Level& level_of(const mask_index* idx, int level) {
+  MASK_REQUIRE(idx != nullptr, MASK_ERR_ARG, "index is NULL");
+  MASK_REQUIRE(level >= 1 && level <= (int)idx->levels.size(), MASK_ERR_ARG, "level out of range");
+  return idx->levels[level - 1];
+}
+
+}  // namespace
+
+// ============================================================================== C ABI
+extern "C" {
+
+int32_t mask_abi_version(void) { return MASK_ABI_VERSION; }
+
+const char* mask_last_error(void) { return g_err.c_str(); }
+
+int32_t mask_device_ok(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    return 0;
+  }
+  int dev = 0, major = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+  return major == 10 ? 1 : 0;
+}
+
+int32_t mask_comm_unique_id(uint8_t id_out[128]) {
+  return guarded([&] {
+    MASK_REQUIRE(id_out != nullptr, MASK_ERR_ARG, "id_out is NULL");
+    ncclUniqueId id;
+    MASK_NCCL(ncclGetUniqueId(&id));
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    std::memcpy(id_out, &id, 128);
+  });
+}
+
+int32_t mask_comm_init(const uint8_t id[128], int32_t world, int32_t rank, mask_comm** out) {
+  return guarded([&] {
+    MASK_REQUIRE(id != nullptr && out != nullptr, MASK_ERR_ARG, "NULL argument");
+    MASK_REQUIRE(world >= 1 && rank >= 0 && rank < world, MASK_ERR_ARG, "bad world/rank");
+    *out = nullptr;
+    ncclUniqueId uid;
+    std::memcpy(&uid, id, 128);
+    auto c = std::make_unique<mask_comm>();
+    c->world = world;
+    c->rank = rank;
+    MASK_NCCL(ncclCommInitRank(&c->comm, world, uid, rank));
+    *out = c.release();
+  });
+}
+
+void mask_comm_free(mask_comm* comm) {
+  if (!comm) return;
+  if (comm->comm) ncclCommDestroy(comm->comm);
+  delete comm;
+}
+
+int32_t mask_build(const mask_matrix* data, const mask_build_params* params, mask_comm* comm,
+                   void* stream, mask_index** out) {
+  return guarded([&] { build_impl(data, params, comm, as_stream(stream), out); });
+}
+
+int32_t mask_query(const mask_index* idx, const mask_matrix* queries, int32_t k_nn, int32_t beam,
+                   int64_t* ids_out, float* d2_out, void* stream) {
+  return guarded([&] {
+    MASK_REQUIRE(idx != nullptr, MASK_ERR_ARG, "index is NULL");
+    check_matrix(queries, "queries");
+    MASK_REQUIRE(k_nn >= 1 && k_nn <= 32, MASK_ERR_ARG, "k_nn must be in [1, 32]");
+    MASK_REQUIRE(beam >= 1 && beam <= 32, MASK_ERR_ARG, "beam must be in [1, 32]");
+    MASK_REQUIRE(queries->dim == idx->dim, MASK_ERR_ARG, "query dim differs from the index dim");
+    MASK_REQUIRE(queries->format == idx->format, MASK_ERR_UNSUPPORTED,
+                 "query format must match the index format");
+    MASK_REQUIRE(ids_out != nullptr && d2_out != nullptr, MASK_ERR_ARG, "NULL outputs");
+    cudaStream_t st = as_stream(stream);
+    const int64_t nq = queries->rows;
+    if (nq == 0) return;
+    QIndex qi{};
+    qi.L = (int)idx->levels.size();
+    qi.dim = idx->dim;
+    qi.X = idx->X;
+    qi.xrp = idx->rp;
+    qi.xcol = idx->col;
+    qi.xval = idx->val;
+    for (int l = 0; l < qi.L; ++l) {
+      qi.lv[l].P = idx->levels[l].P.p;
+      qi.lv[l].offsets = idx->levels[l].offsets.p;
+      qi.lv[l].members = idx->levels[l].members.p;
+      qi.lv[l].k = idx->levels[l].k;
+    }
+    const bool host = queries->memory == MASK_MEM_HOST;
+    DevBuf<float> qv;
+    DevBuf<int64_t> qrp;
+    DevBuf<int32_t> qcol;
+    DevBuf<int64_t> ids_d;
+    DevBuf<float> d2_d;
+    const float* Qv = queries->values;
+    const int64_t* Qrp = queries->row_ptr;
+    const int32_t* Qcol = queries->col_idx;
+    int64_t* ids = ids_out;
+    float* d2 = d2_out;
+    if (queries->format == MASK_CSR_F32) check_csr_structure(queries, st);
+    if (host) {
+      if (queries->format == MASK_DENSE_F32) {
+        qv.alloc((size_t)nq * queries->dim);
+        MASK_CUDA(cudaMemcpyAsync(qv.p, Qv, sizeof(float) * nq * queries->dim, cudaMemcpyHostToDevice, st));
+      } else {
+        qv.alloc(std::max<int64_t>(queries->nnz, 1));
+        qrp.alloc(nq + 1);
+        qcol.alloc(std::max<int64_t>(queries->nnz, 1));
+        MASK_CUDA(cudaMemcpyAsync(qrp.p, Qrp, sizeof(int64_t) * (nq + 1), cudaMemcpyHostToDevice, st));
+        if (queries->nnz) {
+          MASK_CUDA(cudaMemcpyAsync(qv.p, Qv, sizeof(float) * queries->nnz, cudaMemcpyHostToDevice, st));
+          MASK_CUDA(cudaMemcpyAsync(qcol.p, Qcol, sizeof(int32_t) * queries->nnz, cudaMemcpyHostToDevice, st));
+        }
+        Qrp = qrp.p;
+        Qcol = qcol.p;
+      }
+      Qv = qv.p;
+      ids_d.alloc((size_t)nq * k_nn);
+      d2_d.alloc((size_t)nq * k_nn);
+      ids = ids_d.p;
+      d2 = d2_d.p;
+    }
+    if (idx->format == MASK_DENSE_F32)
+      launch_query_dense(qi, Qv, nq, k_nn, beam, ids, d2, st);
+    else
+      launch_query_csr(qi, idx->cn2_flat.p, idx->cn2_off.p, Qrp, Qcol, Qv, nq, k_nn, beam, ids, d2, st);
+    if (host) {
+      MASK_CUDA(cudaMemcpyAsync(ids_out, ids, sizeof(int64_t) * nq * k_nn, cudaMemcpyDeviceToHost, st));
+      MASK_CUDA(cudaMemcpyAsync(d2_out, d2, sizeof(float) * nq * k_nn, cudaMemcpyDeviceToHost, st));
+    }
+    MASK_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+void mask_free(mask_index* idx) { delete idx; }
+
+int32_t mask_assign(const mask_matrix* data, const float* P, int64_t k, int32_t flags,
+                    int32_t* labels_out, float* d2_out, int64_t* n_flagged, void* stream) {
+  return guarded([&] {
+    check_matrix(data, "data");
+    MASK_REQUIRE(data->memory == MASK_MEM_DEVICE, MASK_ERR_UNSUPPORTED, "mask_assign takes device data");
+    MASK_REQUIRE(P != nullptr && labels_out != nullptr, MASK_ERR_ARG, "NULL argument");
+    MASK_REQUIRE(k >= 1, MASK_ERR_ARG, "k must be >= 1");
+    cudaStream_t st = as_stream(stream);
+    if (data->format == MASK_CSR_F32) check_csr_structure(data, st);
+    Input in;
+    in.format = data->format;
+    in.dim = data->dim;
+    in.n_local = in.n_global = data->rows;
+    in.X = data->values;
+    in.rp = data->row_ptr;
+    in.col = data->col_idx;
+    in.val = data->values;
+    in.nnz = data->nnz;
+    LloydWS ws;
+    DevBuf<float> best_tmp;
+    float* best = d2_out;
+    if (!best) {
+      best_tmp.alloc(std::max<int64_t>(data->rows, 1));
+      best = best_tmp.p;
+    }
+    HostStats hs;
+    const int64_t nf = assign_pass(in, P, k, flags, labels_out, best, ws, st, &hs);
+    if (n_flagged) *n_flagged = nf;
+    MASK_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+int32_t mask_update(const mask_matrix* data, const int32_t* labels, int64_t k, const float* P_in,
+                    float* P_out, int32_t* counts_out, double* max_disp, void* stream) {
+  return guarded([&] {
+    check_matrix(data, "data");
+    MASK_REQUIRE(data->memory == MASK_MEM_DEVICE, MASK_ERR_UNSUPPORTED, "mask_update takes device data");
+    MASK_REQUIRE(labels != nullptr && P_in != nullptr && P_out != nullptr, MASK_ERR_ARG, "NULL argument");
+    MASK_REQUIRE(k >= 1, MASK_ERR_ARG, "k must be >= 1");
+    cudaStream_t st = as_stream(stream);
+    const int d = data->dim;
+    DevBuf<float> S((size_t)k * d);
+    DevBuf<int32_t> counts(k);
+    DevBuf<uint32_t> fin(2);
+    MASK_CUDA(cudaMemsetAsync(S.p, 0, sizeof(float) * k * d, st));
+    MASK_CUDA(cudaMemsetAsync(counts.p, 0, sizeof(int32_t) * k, st));
+    MASK_CUDA(cudaMemsetAsync(fin.p, 0, sizeof(uint32_t) * 2, st));
+    if (P_out != P_in)
+      MASK_CUDA(cudaMemcpyAsync(P_out, P_in, sizeof(float) * k * d, cudaMemcpyDeviceToDevice, st));
+    if (data->format == MASK_CSR_F32)
+      launch_update_csr(data->row_ptr, data->col_idx, data->values, data->rows, d, labels, S.p, counts.p, st);
+    else
+      launch_update_dense(data->values, data->rows, d, labels, k, S.p, counts.p, st);
+    launch_finalize(P_out, S.p, counts.p, k, d, fin.p, 1, st);
+    if (counts_out)
+      MASK_CUDA(cudaMemcpyAsync(counts_out, counts.p, sizeof(int32_t) * k, cudaMemcpyDeviceToDevice, st));
+    uint32_t h[2] = {0, 0};
+    MASK_CUDA(cudaMemcpyAsync(h, fin.p, sizeof(h), cudaMemcpyDeviceToHost, st));
+    MASK_CUDA(cudaStreamSynchronize(st));
+    if (max_disp) {
+      float f;
+      std::memcpy(&f, &h[0], sizeof(float));
+      *max_disp = std::sqrt((double)f);
+    }
+  });
+}
+
+int64_t mask_kernel_launches(void) { return g_launches.load(); }
+
+int32_t mask_get_timing(const mask_index* idx, int32_t level, double* out, int32_t cap) {
+  int32_t written = 0;
+  const int32_t rc = guarded([&] {
+    const Level& L = level_of(idx, level);
+    MASK_REQUIRE(out != nullptr || cap == 0, MASK_ERR_ARG, "NULL output");
+    for (int c = 0; c < MASK_T_NCLASS && 2 * c + 1 < cap; ++c) {
+      out[2 * c] = L.t_ms[c];
+      out[2 * c + 1] = (double)L.t_count[c];
+      written = 2 * c + 2;
+    }
+  });
+  return rc == MASK_OK ? written : rc;
+}
+
+int32_t mask_num_levels(const mask_index* idx) { return idx ? (int32_t)idx->levels.size() : 0; }
+
+int32_t mask_level_info(const mask_index* idx, int32_t level, int64_t* n_items, int64_t* k,
+                        int32_t* dim, int32_t* passes, int32_t* updates) {
+  return guarded([&] {
+    const Level& L = level_of(idx, level);
+    if (n_items) *n_items = L.n_items;
+    if (k) *k = L.k;
+    if (dim) *dim = L.dim;
+    if (passes) *passes = (int32_t)L.J.size();
+    if (updates) *updates = L.updates;
+  });
+}
+
+int32_t mask_get_prototypes(const mask_index* idx, int32_t level, float* host_out) {
+  return guarded([&] {
+    const Level& L = level_of(idx, level);
+    MASK_REQUIRE(host_out != nullptr, MASK_ERR_ARG, "NULL output");
+    MASK_CUDA(cudaMemcpy(host_out, L.P.p, sizeof(float) * L.k * L.dim, cudaMemcpyDeviceToHost));
+  });
+}
+
+int32_t mask_get_labels(const mask_index* idx, int32_t level, int32_t* host_out) {
+  return guarded([&] {
+    const Level& L = level_of(idx, level);
+    MASK_REQUIRE(host_out != nullptr, MASK_ERR_ARG, "NULL output");
+    if (L.n_items)
+      MASK_CUDA(cudaMemcpy(host_out, L.labels.p, sizeof(int32_t) * L.n_items, cudaMemcpyDeviceToHost));
+  });
+}
+
+int32_t mask_get_children(const mask_index* idx, int32_t level, int64_t* host_offsets,
+                          int64_t* host_members) {
+  return guarded([&] {
+    const Level& L = level_of(idx, level);
+    MASK_REQUIRE(host_offsets != nullptr && host_members != nullptr, MASK_ERR_ARG, "NULL output");
+    MASK_CUDA(cudaMemcpy(host_offsets, L.offsets.p, sizeof(int64_t) * (L.k + 1), cudaMemcpyDeviceToHost));
+    std::vector<int32_t> m(L.n_items);
+    if (L.n_items)
+      MASK_CUDA(cudaMemcpy(m.data(), L.members.p, sizeof(int32_t) * L.n_items, cudaMemcpyDeviceToHost));
+    for (int64_t j = 0; j < L.k; ++j) std::sort(m.begin() + host_offsets[j], m.begin() + host_offsets[j + 1]);
+    for (int64_t i = 0; i < L.n_items; ++i) host_members[i] = m[i];
+  });
+}
+
+int32_t mask_get_trace(const mask_index* idx, int32_t level, double* J, int64_t* changed,
+                       int64_t* empties, int32_t cap) {
+  int32_t written = 0;
+  const int32_t rc = guarded([&] {
+    const Level& L = level_of(idx, level);
+    MASK_REQUIRE(cap >= 0, MASK_ERR_ARG, "cap < 0");
+    const int32_t np = (int32_t)std::min<size_t>(L.J.size(), (size_t)cap);
+    for (int32_t t = 0; t < np; ++t) {
+      if (J) J[t] = L.J[t];
+      if (changed) changed[t] = L.changed[t];
+      if (empties) empties[t] = t < (int32_t)L.empties.size() ? L.empties[t] : 0;
+    }
+    written = np;
+  });
+  return rc == MASK_OK ? written : rc;
+}
+
+}  // extern "C"

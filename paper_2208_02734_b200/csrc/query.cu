@@ -1,0 +1,365 @@
+// query.cu -- K9: batched approximate k-NN by multilevel descent (§3.3,
+// Algorithm 2; point/k-NN query prose P:846-884).
+//
+// One warp per query.  At the top level every prototype with children is a candidate; at
+// each lower level the candidates are the children of the b prototypes kept at the level
+// above (explicit child lists, D7; childless prototypes skipped); at the data layer the
+// candidates are the rows of the reached partition(s).  Every selection is a warp-level
+// bitonic top-K (K = beam for the levels, K = k_nn at the leaf) over chunks of 32
+// candidates with (d^2, id) ordering (D4): sort the chunk with a 32-lane bitonic network,
+// merge it into the running sorted top-32 (min against the reversed chunk, then a bitonic
+// merge), skipping chunks whose best candidate cannot enter the current top-K (ballot).
+// Distances are FP32 direct sums of squares.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "common.cuh"
+
+namespace mask {
+
+namespace {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int32_t PAD_ID = 0x7fffffff;
+
+__device__ __forceinline__ bool key_lt(float da, int32_t ia, float db, int32_t ib) {
+  return da < db || (da == db && ia < ib);
+}
+
+// Ascending bitonic sort of one (d, id) key per lane across the warp.
+__device__ __forceinline__ void warp_sort32(float& d, int32_t& id, int lane) {
+#pragma unroll
+  for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      const float od = __shfl_xor_sync(FULL, d, stride);
+      const int32_t oi = __shfl_xor_sync(FULL, id, stride);
+      const bool up = (lane & size) == 0 || size == 32;
+      const bool lower = (lane & stride) == 0;
+      const bool keep_min = (lower == up);
+      const bool other_less = key_lt(od, oi, d, id);
+      const bool take = keep_min ? other_less : key_lt(d, id, od, oi);
+      if (take) {
+        d = od;
+        id = oi;
+      }
+    }
+  }
+}
+
+// Bitonic merge of a bitonic warp sequence into ascending order.
+__device__ __forceinline__ void warp_merge32(float& d, int32_t& id, int lane) {
+#pragma unroll
+  for (int stride = 16; stride > 0; stride >>= 1) {
+    const float od = __shfl_xor_sync(FULL, d, stride);
+    const int32_t oi = __shfl_xor_sync(FULL, id, stride);
+    const bool lower = (lane & stride) == 0;
+    const bool take = lower ? key_lt(od, oi, d, id) : key_lt(d, id, od, oi);
+    if (take) {
+      d = od;
+      id = oi;
+    }
+  }
+}
+
+// Running top-K (K <= 32) held as a sorted warp vector: lane r holds the r-th best.
+struct WarpTopK {
+  float d;
+  int32_t id;
+  int K;
+  __device__ void reset(int k) {
+    K = k;
+    d = INFINITY;
+    id = PAD_ID;
+  }
+  // offer one candidate per lane (pass +inf / PAD_ID for none)
+  __device__ void offer(float cd, int32_t cid, int lane) {
+    const float kd = __shfl_sync(FULL, d, K - 1);
+    const int32_t ki = __shfl_sync(FULL, id, K - 1);
+    if (!__any_sync(FULL, key_lt(cd, cid, kd, ki))) return;
+    warp_sort32(cd, cid, lane);
+    const float rd = __shfl_sync(FULL, cd, 31 - lane);
+    const int32_t ri = __shfl_sync(FULL, cid, 31 - lane);
+    if (key_lt(rd, ri, d, id)) {
+      d = rd;
+      id = ri;
+    }
+    warp_merge32(d, id, lane);
+  }
+};
+
+__device__ __forceinline__ float dist_dense(const float* __restrict__ q, const float* __restrict__ x,
+                                            int d) {
+  float s = 0.f;
+  if ((d & 3) == 0 && ((uintptr_t)x & 15) == 0) {
+    const float4* x4 = reinterpret_cast<const float4*>(x);
+    const float4* q4 = reinterpret_cast<const float4*>(q);
+    for (int i = 0; i < (d >> 2); ++i) {
+      const float4 a = __ldg(x4 + i);
+      const float4 b = q4[i];
+      float t = b.x - a.x;
+      s = fmaf(t, t, s);
+      t = b.y - a.y;
+      s = fmaf(t, t, s);
+      t = b.z - a.z;
+      s = fmaf(t, t, s);
+      t = b.w - a.w;
+      s = fmaf(t, t, s);
+    }
+  } else {
+    for (int i = 0; i < d; ++i) {
+      const float t = q[i] - __ldg(x + i);
+      s = fmaf(t, t, s);
+    }
+  }
+  return s;
+}
+
+__device__ __forceinline__ bool has_children(const QLevel& L, int64_t j) {
+  return L.offsets[j + 1] > L.offsets[j];
+}
+
+constexpr int kWarpsPerBlock = 4;
+
+}  // namespace
+
+// Dense queries against a dense index.  Shared memory: one q vector (d floats) per warp.
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+    k_query_dense(QIndex qi, const float* __restrict__ Q, int64_t nq, int knn, int beam,
+                  int64_t* __restrict__ ids_out, float* __restrict__ d2_out) {
+  extern __shared__ __align__(16) float sq[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int d = qi.dim;
+  const int dpad = (d + 3) & ~3;
+  float* q = sq + w * dpad;
+  const int64_t nwarps = (int64_t)gridDim.x * kWarpsPerBlock;
+  for (int64_t qid = (int64_t)blockIdx.x * kWarpsPerBlock + w; qid < nq; qid += nwarps) {
+    __syncwarp();
+    for (int i = lane; i < d; i += 32) q[i] = Q[qid * d + i];
+    __syncwarp();
+    WarpTopK top;
+    // ---- top level: all prototypes with children
+    {
+      const QLevel& L = qi.lv[qi.L - 1];
+      top.reset(beam);
+      for (int64_t j0 = 0; j0 < L.k; j0 += 32) {
+        const int64_t j = j0 + lane;
+        float cd = INFINITY;
+        int32_t cid = PAD_ID;
+        if (j < L.k && has_children(L, j)) {
+          cd = dist_dense(q, L.P + j * d, d);
+          cid = (int32_t)j;
+        }
+        top.offer(cd, cid, lane);
+      }
+    }
+    // ---- levels L-1 .. 1: children of the kept prototypes
+    for (int l = qi.L - 2; l >= 0; --l) {
+      const QLevel& up = qi.lv[l + 1];
+      const QLevel& L = qi.lv[l];
+      const float sel_d = top.d;
+      const int32_t sel_id = top.id;
+      const int nsel = beam;
+      top.reset(beam);
+      for (int s = 0; s < nsel; ++s) {
+        const int32_t p = __shfl_sync(FULL, sel_id, s);
+        const float pd = __shfl_sync(FULL, sel_d, s);
+        if (p == PAD_ID || pd == INFINITY && p == PAD_ID) continue;
+        const int64_t m0 = up.offsets[p], m1 = up.offsets[p + 1];
+        for (int64_t m = m0; m < m1; m += 32) {
+          const int64_t mm = m + lane;
+          float cd = INFINITY;
+          int32_t cid = PAD_ID;
+          if (mm < m1) {
+            const int32_t j = up.members[mm];
+            if (has_children(L, j)) {
+              cd = dist_dense(q, L.P + (int64_t)j * d, d);
+              cid = j;
+            }
+          }
+          top.offer(cd, cid, lane);
+        }
+      }
+    }
+    // ---- data layer: rows of the reached partition(s)
+    {
+      const QLevel& L1 = qi.lv[0];
+      const float sel_d = top.d;
+      const int32_t sel_id = top.id;
+      (void)sel_d;
+      top.reset(knn);
+      for (int s = 0; s < beam; ++s) {
+        const int32_t p = __shfl_sync(FULL, sel_id, s);
+        if (p == PAD_ID) continue;
+        const int64_t m0 = L1.offsets[p], m1 = L1.offsets[p + 1];
+        for (int64_t m = m0; m < m1; m += 32) {
+          const int64_t mm = m + lane;
+          float cd = INFINITY;
+          int32_t cid = PAD_ID;
+          if (mm < m1) {
+            const int32_t i = L1.members[mm];
+            cd = dist_dense(q, qi.X + (int64_t)i * d, d);
+            cid = i;
+          }
+          top.offer(cd, cid, lane);
+        }
+      }
+    }
+    if (lane < knn) {
+      const bool pad = top.id == PAD_ID;
+      ids_out[qid * knn + lane] = pad ? -1 : (int64_t)top.id;
+      d2_out[qid * knn + lane] = pad ? INFINITY : top.d;
+    }
+  }
+}
+
+void launch_query_dense(const QIndex& qi, const float* Q, int64_t nq, int knn, int beam,
+                        int64_t* ids, float* d2, cudaStream_t st) {
+  if (nq <= 0) return;
+  const int dpad = (qi.dim + 3) & ~3;
+  const size_t smem = (size_t)kWarpsPerBlock * dpad * sizeof(float);
+  MASK_REQUIRE(smem <= 200 * 1024, MASK_ERR_UNSUPPORTED, "query: dim too large for dense queries");
+  if (smem > 48 * 1024)
+    MASK_CUDA(cudaFuncSetAttribute(k_query_dense, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int64_t blocks = (nq + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  const unsigned grid = (unsigned)(blocks < (int64_t)num_sms() * 16 ? blocks : (int64_t)num_sms() * 16);
+  k_query_dense<<<grid, kWarpsPerBlock * 32, smem, st>>>(qi, Q, nq, knn, beam, ids, d2);
+  MASK_LAUNCH_CHECK();
+}
+
+// ---------------------------------------------------------------------------------------
+// CSR queries against a CSR-data index (prototypes dense).  q's non-zeros are staged in
+// shared memory.  Prototype distance: ||c||^2 + sum_{p in nz(q)} (q_p^2 - 2 q_p c[col_p])
+// (D12); data-row distance: direct sum over the union of the two sorted supports.
+constexpr int kMaxQueryNnz = 1024;
+
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+    k_query_csr(QIndex qi, const float* __restrict__ cn2_flat, const int64_t* __restrict__ cn2_off,
+                const int64_t* __restrict__ qrp, const int32_t* __restrict__ qcol,
+                const float* __restrict__ qval, int64_t nq, int knn, int beam,
+                int64_t* __restrict__ ids_out, float* __restrict__ d2_out) {
+  __shared__ int32_t s_col[kWarpsPerBlock][kMaxQueryNnz];
+  __shared__ float s_val[kWarpsPerBlock][kMaxQueryNnz];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int d = qi.dim;
+  const int64_t nwarps = (int64_t)gridDim.x * kWarpsPerBlock;
+  for (int64_t qid = (int64_t)blockIdx.x * kWarpsPerBlock + w; qid < nq; qid += nwarps) {
+    const int64_t p0 = qrp[qid];
+    const int qn = (int)min64(qrp[qid + 1] - p0, kMaxQueryNnz);
+    __syncwarp();
+    for (int i = lane; i < qn; i += 32) {
+      s_col[w][i] = qcol[p0 + i];
+      s_val[w][i] = qval[p0 + i];
+    }
+    __syncwarp();
+    float qq = 0.f;
+    for (int i = 0; i < qn; ++i) qq = fmaf(s_val[w][i], s_val[w][i], qq);
+    auto proto_dist = [&](int l, int64_t j) {
+      const float* c = qi.lv[l].P + j * d;
+      float s = 0.f;
+      for (int i = 0; i < qn; ++i) s = fmaf(s_val[w][i], __ldg(c + s_col[w][i]), s);
+      return cn2_flat[cn2_off[l] + j] + qq - 2.f * s;
+    };
+    WarpTopK top;
+    {
+      const int l = qi.L - 1;
+      const QLevel& L = qi.lv[l];
+      top.reset(beam);
+      for (int64_t j0 = 0; j0 < L.k; j0 += 32) {
+        const int64_t j = j0 + lane;
+        float cd = INFINITY;
+        int32_t cid = PAD_ID;
+        if (j < L.k && has_children(L, j)) {
+          cd = proto_dist(l, j);
+          cid = (int32_t)j;
+        }
+        top.offer(cd, cid, lane);
+      }
+    }
+    for (int l = qi.L - 2; l >= 0; --l) {
+      const QLevel& up = qi.lv[l + 1];
+      const QLevel& L = qi.lv[l];
+      const int32_t sel_id = top.id;
+      top.reset(beam);
+      for (int s = 0; s < beam; ++s) {
+        const int32_t p = __shfl_sync(FULL, sel_id, s);
+        if (p == PAD_ID) continue;
+        const int64_t m0 = up.offsets[p], m1 = up.offsets[p + 1];
+        for (int64_t m = m0; m < m1; m += 32) {
+          const int64_t mm = m + lane;
+          float cd = INFINITY;
+          int32_t cid = PAD_ID;
+          if (mm < m1) {
+            const int32_t j = up.members[mm];
+            if (has_children(L, j)) {
+              cd = proto_dist(l, j);
+              cid = j;
+            }
+          }
+          top.offer(cd, cid, lane);
+        }
+      }
+    }
+    {
+      const QLevel& L1 = qi.lv[0];
+      const int32_t sel_id = top.id;
+      top.reset(knn);
+      for (int s = 0; s < beam; ++s) {
+        const int32_t p = __shfl_sync(FULL, sel_id, s);
+        if (p == PAD_ID) continue;
+        const int64_t m0 = L1.offsets[p], m1 = L1.offsets[p + 1];
+        for (int64_t m = m0; m < m1; m += 32) {
+          const int64_t mm = m + lane;
+          float cd = INFINITY;
+          int32_t cid = PAD_ID;
+          if (mm < m1) {
+            const int32_t i = L1.members[mm];
+            int64_t a = qi.xrp[i];
+            const int64_t ae = qi.xrp[i + 1];
+            int b = 0;
+            float s = 0.f;
+            while (a < ae || b < qn) {
+              float t;
+              const int32_t ca = a < ae ? __ldg(qi.xcol + a) : 0x7fffffff;
+              const int32_t cb = b < qn ? s_col[w][b] : 0x7fffffff;
+              if (ca < cb) {
+                t = __ldg(qi.xval + a);
+                ++a;
+              } else if (cb < ca) {
+                t = s_val[w][b];
+                ++b;
+              } else {
+                t = __ldg(qi.xval + a) - s_val[w][b];
+                ++a;
+                ++b;
+              }
+              s = fmaf(t, t, s);
+            }
+            cd = s;
+            cid = i;
+          }
+          top.offer(cd, cid, lane);
+        }
+      }
+    }
+    if (lane < knn) {
+      const bool pad = top.id == PAD_ID;
+      ids_out[qid * knn + lane] = pad ? -1 : (int64_t)top.id;
+      d2_out[qid * knn + lane] = pad ? INFINITY : top.d;
+    }
+  }
+}
+
+void launch_query_csr(const QIndex& qi, const float* cn2_flat, const int64_t* cn2_off,
+                      const int64_t* qrp, const int32_t* qcol, const float* qval, int64_t nq,
+                      int knn, int beam, int64_t* ids, float* d2, cudaStream_t st) {
+  if (nq <= 0) return;
+  const int64_t blocks = (nq + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  const unsigned grid = (unsigned)(blocks < (int64_t)num_sms() * 16 ? blocks : (int64_t)num_sms() * 16);
+  k_query_csr<<<grid, kWarpsPerBlock * 32, 0, st>>>(qi, cn2_flat, cn2_off, qrp, qcol, qval, nq, knn,
+                                                     beam, ids, d2);
+  MASK_LAUNCH_CHECK();
+}
+
+}  // namespace mask

@@ -1,0 +1,76 @@
+"""Parity criteria of BASELINE.json north_star, made operational.
+
+* Assignments: identical except rows whose oracle best and second-best squared distances
+  differ by less than 1e-5 relative (D10: (d2 - d1) < 1e-5 * d2 on FP64 squared distances);
+  for those exempt rows the oracle distance of the GPU's label must be <= d1 * (1 + 1e-5).
+* Prototypes: within 1e-4 relative L2 (Frobenius) error per level.
+* Queries: identical (d^2, id)-ordered result sets except queries whose oracle selections
+  had a competing candidate within 1e-5 relative (counted, not silently passed).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+import oracle
+
+TIE_REL = 1e-5
+PROTO_REL = 1e-4
+
+
+def check_assignment(Y, P, labels_gpu, d2_gpu=None, what=""):
+    """Compare GPU labels with the oracle's assignment of the same rows to the same P."""
+    Y = np.asarray(Y, np.float64)
+    P = np.asarray(P, np.float64)
+    lab, b1, b2 = oracle.assign(Y, P)
+    labels_gpu = np.asarray(labels_gpu).astype(np.int64)
+    assert labels_gpu.min() >= 0 and labels_gpu.max() < P.shape[0], f"{what}: label out of range"
+    exempt = (b2 - b1) < TIE_REL * b2
+    bad = (labels_gpu != lab) & ~exempt
+    assert not bad.any(), (f"{what}: {int(bad.sum())} non-exempt label mismatches of {len(lab)} "
+                           f"(first rows {np.nonzero(bad)[0][:5].tolist()})")
+    diff = labels_gpu != lab
+    if diff.any():
+        rows = np.nonzero(diff)[0]
+        dg = ((Y[rows] - P[labels_gpu[rows]]) ** 2).sum(axis=1)
+        assert np.all(dg <= b1[rows] * (1 + TIE_REL) + 1e-300), f"{what}: exempt row label not within window"
+    if d2_gpu is not None:
+        d2_gpu = np.asarray(d2_gpu, np.float64)
+        ref = ((Y - P[labels_gpu]) ** 2).sum(axis=1)
+        err = np.abs(d2_gpu - ref)
+        # FP32 value of a squared distance: 1e-5 of itself, plus (expanded form, tensor path)
+        # 1e-6 of the magnitudes ||x||^2 + ||c||^2 that cancel in ||x||^2 + ||c||^2 - 2 x.c
+        allow = 1e-5 * ref + 1e-6 * ((Y ** 2).sum(axis=1) + (P[labels_gpu] ** 2).sum(axis=1)) + 1e-30
+        assert np.all(err <= allow), f"{what}: d2 max err/allow {float((err / allow).max())}"
+    return int(diff.sum()), int(exempt.sum())
+
+
+def rel_l2(a, b) -> float:
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    den = np.linalg.norm(b)
+    return float(np.linalg.norm(a - b) / (den if den > 0 else 1.0))
+
+
+def check_prototypes(P_gpu, P_ref, what=""):
+    e = rel_l2(P_gpu, P_ref)
+    assert e <= PROTO_REL, f"{what}: prototype rel L2 error {e:.3e} > {PROTO_REL}"
+    return e
+
+
+def check_queries(ids_gpu, d2_gpu, ids_ref, d2_ref, gap_ref, what=""):
+    """Identical result lists except queries exempt by the oracle's tie window."""
+    ids_gpu = np.asarray(ids_gpu)
+    exempt = gap_ref < TIE_REL
+    same = np.all(ids_gpu == ids_ref, axis=1)
+    bad = ~same & ~exempt
+    assert not bad.any(), (f"{what}: {int(bad.sum())} non-exempt query mismatches of {len(same)} "
+                           f"(first {np.nonzero(bad)[0][:5].tolist()})")
+    ok = same
+    fin = np.isfinite(d2_ref[ok])
+    if fin.any():
+        a = np.asarray(d2_gpu, np.float64)[ok][fin]
+        b = d2_ref[ok][fin]
+        assert np.all(np.abs(a - b) <= 1e-4 * np.maximum(b, 1e-6) + 1e-6), f"{what}: d2 mismatch"
+    pad_gpu = ids_gpu < 0
+    assert np.all(np.isinf(np.asarray(d2_gpu)[pad_gpu])), f"{what}: padding must carry +inf"
+    return int((~same).sum()), int(exempt.sum())

@@ -1,0 +1,85 @@
+"""CPU checks of the C-ABI boundary: libmask.so loads without a GPU, exports every symbol
+include/mask.h declares, and fails loudly (no CPU fallback) when no GPU is present."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_2208_02734_b200 as mk
+from paper_2208_02734_b200 import _lib
+from paper_2208_02734_b200 import buildlib as buildmod
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _header_functions():
+    src = open(os.path.join(ROOT, "include", "mask.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    names = set(re.findall(r"\b(mask_[a-z_0-9]+)\s*\(", src))
+    return sorted(n for n in names if n not in {"mask_iter_cb"})
+
+
+@pytest.fixture(scope="module")
+def lib():
+    buildmod.build()
+    return _lib.load()
+
+
+def test_header_declares_the_north_star_calls():
+    fns = _header_functions()
+    for required in ("mask_build", "mask_query", "mask_free"):
+        assert required in fns
+
+
+def test_library_exports_every_declared_symbol(lib):
+    fns = _header_functions()
+    assert sorted(_lib.EXPORTS) == fns
+    for f in fns:
+        assert hasattr(lib, f), f
+
+
+def test_abi_version_and_no_gpu_is_an_error(lib):
+    assert lib.mask_abi_version() == 1
+    try:
+        import torch
+
+        has_gpu = torch.cuda.is_available()
+    except Exception:
+        has_gpu = False
+    if has_gpu:
+        pytest.skip("GPU present")
+    assert lib.mask_device_ok() == 0
+    with pytest.raises(mk.MaskError) as e:
+        mk.build(np.zeros((10, 2), np.float32), [3], 2, [np.array([0, 1, 2])])
+    assert e.value.code in (-4,)
+
+
+def test_argument_errors_before_touching_the_gpu(lib):
+    X = np.zeros((10, 2), np.float32)
+    with pytest.raises(mk.MaskError) as e:
+        mk.build(X, [11], 2, [np.arange(11)])  # k > n
+    assert e.value.code == -1
+    with pytest.raises(mk.MaskError) as e:
+        mk.build(X, [3], 2, [np.array([0, 0, 1])])  # duplicate init indices
+    assert e.value.code == -1
+    with pytest.raises(mk.MaskError) as e:
+        mk.build(X, [3], -1, [np.array([0, 1, 2])])  # T < 0
+    assert e.value.code == -1
+    with pytest.raises(mk.MaskError) as e:
+        mk.build(X, [3, 4], 2, [np.array([0, 1, 2]), np.array([0, 1, 2, 3])])  # k2 > k1
+    assert e.value.code == -1
+    # CSR structure errors
+    bad = mk.Csr(np.array([0, 2, 3], np.int64), np.array([3, 1, 0], np.int32), np.ones(3, np.float32), 5)
+    with pytest.raises(mk.MaskError) as e:
+        mk.build(bad, [1], 1, [np.array([0])])
+    assert e.value.code == -1
+
+
+def test_shard_ranges_partition_rows():
+    for n in (0, 1, 7, 100, 1_000_003):
+        for w in (1, 2, 3, 8):
+            spans = [mk.row_range(n, w, r) for r in range(w)]
+            assert spans[0][0] == 0 and spans[-1][1] == n
+            for (a, b), (c, d) in zip(spans, spans[1:]):
+                assert b == c and a <= b

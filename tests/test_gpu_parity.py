@@ -1,0 +1,294 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the FP64 oracle on the same seeded
+inputs, element by element, at sizes the oracle finishes in seconds (several tiles and a
+ragged tail), plus edge cases.  Marked `gpu` (run on a B200)."""
+import numpy as np
+import pytest
+
+import datagen
+import oracle
+from parity import check_assignment, check_prototypes, check_queries, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no GPU", allow_module_level=True)
+
+import paper_2208_02734_b200 as mk  # noqa: E402
+
+DEV = "cuda:0"
+
+
+def t(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+
+
+def test_native_library_is_the_one_loaded():
+    import paper_2208_02734_b200._lib as L
+
+    lib = L.load()
+    assert mk.device_ok(), "libmask reports no sm_100 device"
+    import os
+
+    maps = open("/proc/self/maps").read()
+    assert os.path.realpath(L.LIB_PATH) in maps
+
+
+# ------------------------------------------------------------------ assignment (K1/K2)
+ASSIGN_SHAPES = [
+    (1000, 2, 100), (1037, 3, 7), (4099, 16, 300), (500, 17, 33), (257, 64, 1), (300, 128, 300),
+    (2049, 8, 129), (777, 1, 5), (3000, 32, 64), (1500, 64, 513), (640, 96, 40), (130, 128, 257),
+]
+
+
+@pytest.mark.parametrize("n,d,k", ASSIGN_SHAPES)
+@pytest.mark.parametrize("flags", [0, mk.MASK_FORCE_SIMT])
+def test_assign_parity(n, d, k, flags):
+    X = datagen.blobs(100 + d, n, d, max(2, k // 4), spread=10.0)
+    P = X[datagen.init_indices(50 + d, 1, n, k)]
+    P = P + datagen.random_dense(7 + k, k, d, scale=0.1)  # prototypes that are not data rows
+    lab, d2, nf = mk.assign(t(X), t(P), flags=flags)
+    check_assignment(X, P, lab.cpu().numpy(), d2.cpu().numpy(), what=f"assign n={n} d={d} k={k}")
+
+
+def test_assign_exact_ties_take_lowest_ordinal():
+    X = np.array([[0.0, 0.0], [1.0, 1.0], [2.0, 2.0]] * 50, np.float32)
+    P = np.array([[5.0, 5.0], [1.0, 1.0], [1.0, 1.0], [0.0, 0.0], [0.0, 0.0]], np.float32)
+    for flags in (0, mk.MASK_FORCE_SIMT):
+        lab, d2, _ = mk.assign(t(X), t(P), flags=flags)
+        lab = lab.cpu().numpy()
+        assert np.all(lab[0::3] == 3) and np.all(lab[1::3] == 1) and np.all(lab[2::3] == 1)
+
+
+# ------------------------------------------------------------------ update (K5/K7)
+@pytest.mark.parametrize("n,d,k", [(5000, 2, 100), (4099, 16, 300), (1000, 17, 50), (3000, 64, 129), (700, 128, 33)])
+def test_update_parity(n, d, k):
+    X = datagen.blobs(200 + d, n, d, 7)
+    P_in = datagen.random_dense(300 + d, k, d)
+    rng = np.random.default_rng(n)
+    labels = rng.integers(0, max(1, k - 5), size=n).astype(np.int32)  # last clusters empty
+    P_out, counts, md = mk.update(t(X), t(labels), t(P_in))
+    P_ref, cnt_ref = oracle.means(X.astype(np.float64), labels, P_in.astype(np.float64))
+    assert np.array_equal(counts.cpu().numpy(), cnt_ref)
+    got = P_out.cpu().numpy()
+    check_prototypes(got, P_ref, what="update")
+    empty = cnt_ref == 0
+    assert np.array_equal(got[empty], P_in[empty])  # D5: empty keeps its prototype exactly
+    ref_md = np.sqrt(((P_ref - P_in) ** 2).sum(axis=1)).max()
+    assert md == pytest.approx(ref_md, rel=1e-4)
+
+
+# ------------------------------------------------------------------ build (levels + Lloyd)
+def _step_parity_build(X, levels, T, inits, flags=0, csr=None, tol=0.0):
+    """Build with the step-parity hook; check every pass's assignment and every update
+    against the oracle applied to the GPU's own P_t (SURVEY §8(c) step mode)."""
+    passes = {}
+
+    def cb(level, p, P, labels):
+        passes.setdefault(level, []).append((P, labels))
+
+    data = X if csr is None else csr
+    idx = mk.build(data, levels, T, inits, tol=tol, flags=flags, iter_cb=cb)
+    Y = None
+    for l in range(1, len(levels) + 1):
+        if l == 1:
+            if csr is None:
+                Y = X.astype(np.float64)
+            else:
+                rp, col, val = [a.cpu().numpy() if hasattr(a, "cpu") else a for a in (csr.row_ptr, csr.col, csr.val)]
+                Y = np.zeros((rp.size - 1, csr.dim))
+                for i in range(rp.size - 1):
+                    Y[i, col[rp[i]:rp[i + 1]]] = val[rp[i]:rp[i + 1]]
+        else:
+            Y = idx.prototypes(l - 1).astype(np.float64)
+        seq = passes[l]
+        # init prototypes = the seeded rows
+        np.testing.assert_array_equal(seq[0][0], Y[inits[l - 1]].astype(np.float32))
+        for p_i, (P, lab) in enumerate(seq):
+            check_assignment(Y, P, lab, what=f"level {l} pass {p_i}")
+            if p_i + 1 < len(seq):
+                P_next = seq[p_i + 1][0]
+                if not np.array_equal(P_next, P):  # an update happened between the passes
+                    P_ref, _ = oracle.means(Y, lab, P.astype(np.float64))
+                    check_prototypes(P_next, P_ref, what=f"level {l} update after pass {p_i}")
+        # stored labels = the final pass
+        np.testing.assert_array_equal(idx.labels(l), seq[-1][1])
+        np.testing.assert_array_equal(idx.prototypes(l), seq[-1][0])
+        # children = {i : labels[i] = j} ascending
+        off, mem = idx.children(l)
+        o_ref, m_ref = oracle.children(seq[-1][1], levels[l - 1])
+        np.testing.assert_array_equal(off, o_ref)
+        np.testing.assert_array_equal(mem, m_ref)
+        tr = idx.trace(l)
+        assert len(tr["J"]) == len(seq)
+    return idx, passes
+
+
+def _e2e_compare(idx, X, levels, T, inits, csr_dim=None, data=None):
+    ref = oracle.build_index(X if data is None else data, inits, T, csr_dim=csr_dim)
+    errs = []
+    for l in range(1, len(levels) + 1):
+        errs.append(check_prototypes(idx.prototypes(l), ref.levels[l - 1].P, what=f"e2e level {l}"))
+    return ref, errs
+
+
+def test_build_C1_full_step_and_e2e():
+    cfg = datagen.CONFIGS[1]
+    X = datagen.data(cfg)
+    inits = datagen.all_init_indices(cfg)
+    idx, passes = _step_parity_build(X, cfg.levels, cfg.iters, inits)
+    ref, errs = _e2e_compare(idx, X, cfg.levels, cfg.iters, inits)
+    # trace: J_t of the GPU vs the oracle's when the trajectories agree
+    trg = idx.trace(1)
+    if len(trg["J"]) == len(ref.levels[0].J):
+        np.testing.assert_allclose(trg["J"], ref.levels[0].J, rtol=1e-4)
+    # queries: oracle descends the GPU-built index
+    Q = datagen.queries(cfg)
+    _query_parity(idx, X, Q, cfg.levels, knn=cfg.knn, beam=1)
+    idx.free()
+
+
+def _query_parity(idx, X, Q, levels, knn, beam, Qdev=None, csr=False, dim=None):
+    L = len(levels)
+    P = [idx.prototypes(l).astype(np.float64) for l in range(1, L + 1)]
+    ch = [idx.children(l) for l in range(1, L + 1)]
+    ids_ref, d2_ref, gap = oracle.query(P, [c[0] for c in ch], [c[1] for c in ch], X, Q, knn, beam,
+                                        dim=dim, x_csr=csr, q_csr=csr)
+    qin = Qdev if Qdev is not None else t(Q)
+    ids, d2 = idx.query(qin, knn=knn, beam=beam)
+    ids = ids.cpu().numpy()
+    d2 = d2.cpu().numpy()
+    nd, ne = check_queries(ids, d2, ids_ref, d2_ref, gap, what=f"query beam={beam}")
+    # host-memory query path gives the same answer
+    if not csr:
+        ids_h, d2_h = idx.query(np.ascontiguousarray(Q, np.float32), knn=knn, beam=beam)
+        np.testing.assert_array_equal(ids_h, ids)
+    if not csr:
+        eids, _, _ = oracle.knn_exact(X, Q, knn)
+        ok = gap >= 1e-5
+        r_gpu = oracle.recall(ids[ok], eids[ok])
+        r_ref = oracle.recall(ids_ref[ok], eids[ok])
+        assert r_gpu == r_ref
+    return nd, ne
+
+
+@pytest.mark.parametrize("cid,div", [(2, 64), (3, 256), (5, 2048)])
+def test_build_scaled_replicas_step_and_queries(cid, div):
+    cfg = datagen.CONFIGS[cid].scaled(div)
+    X = datagen.data(cfg)
+    inits = datagen.all_init_indices(cfg)
+    T = min(cfg.iters, 8)
+    idx, _ = _step_parity_build(X, cfg.levels, T, inits)
+    Q = datagen.queries(cfg, count=200)
+    _query_parity(idx, X, Q, cfg.levels, knn=10, beam=1)
+    _query_parity(idx, X, Q, cfg.levels, knn=5, beam=3)
+    idx.free()
+
+
+def test_build_edge_cases():
+    X = datagen.blobs(300, 1001, 5, 9)
+    # k = n at level 1 with identity init: every point its own prototype, J = 0
+    idx = mk.build(t(X), [1001, 1], 3, [np.arange(1001), np.array([7])])
+    np.testing.assert_array_equal(idx.prototypes(1), X)
+    np.testing.assert_array_equal(idx.labels(1), np.arange(1001))
+    assert idx.trace(1)["J"][-1] == 0.0
+    # level 2 with k = 1: the mean of the level-1 prototypes
+    np.testing.assert_allclose(idx.prototypes(2)[0], X.astype(np.float64).mean(axis=0), rtol=1e-5, atol=1e-5)
+    # self-queries on the identity index return the point itself
+    ids, d2 = idx.query(t(X[:50]), knn=1)
+    np.testing.assert_array_equal(ids.cpu().numpy()[:, 0], np.arange(50))
+    idx.free()
+    # L = 1, k = 1: the leaf is the whole dataset -> exact k-NN, recall 1
+    idx = mk.build(t(X), [1], 2, [np.array([3])])
+    Q = datagen.blobs(301, 64, 5, 9)
+    ids, d2 = idx.query(t(Q), knn=10)
+    eids, ed2, gap = oracle.knn_exact(X, Q, 10)
+    ok = gap >= 1e-5
+    np.testing.assert_array_equal(ids.cpu().numpy()[ok], eids[ok])
+    idx.free()
+    # T = 0: labels are the plain assignment to the init rows
+    inits = [datagen.init_indices(5, 1, 1001, 40)]
+    idx = mk.build(t(X), [40], 0, inits)
+    check_assignment(X, X[inits[0]], idx.labels(1))
+    assert idx.level_info(1)["updates"] == 0
+    idx.free()
+    # a partition smaller than k_nn is padded with (-1, +inf)
+    idx = mk.build(t(X), [500], 3, [datagen.init_indices(6, 1, 1001, 500)])
+    ids, d2 = idx.query(t(X[:20]), knn=32)
+    ids = ids.cpu().numpy()
+    d2 = d2.cpu().numpy()
+    assert (ids < 0).any()
+    assert np.all(np.isinf(d2[ids < 0]))
+    idx.free()
+
+
+def test_empty_cluster_keeps_prototype():
+    # duplicated data rows -> duplicated init prototypes -> the higher copy gets no members
+    X = datagen.blobs(310, 2000, 3, 4)
+    X[1] = X[0]
+    inits = [np.array([0, 1] + list(range(2, 30)))]
+    idx, passes = _step_parity_build(X, [30], 5, inits)
+    tr = idx.trace(1)
+    assert tr["empties"][0] >= 1
+    np.testing.assert_array_equal(idx.prototypes(1)[1], X[1])
+    idx.free()
+
+
+def test_nonfinite_and_argument_errors():
+    X = datagen.blobs(320, 100, 4, 3)
+    X[5, 2] = np.nan
+    with pytest.raises(mk.MaskError) as e:
+        mk.build(t(X), [4], 2, [np.arange(4)], flags=mk.MASK_VALIDATE_FINITE)
+    assert e.value.code == -2
+    X[5, 2] = 0.0
+    idx = mk.build(t(X), [4], 2, [np.arange(4)])
+    with pytest.raises(mk.MaskError):
+        idx.query(t(X[:, :3]), knn=3)  # dim mismatch
+    with pytest.raises(mk.MaskError):
+        idx.query(t(X[:3]), knn=0)
+    with pytest.raises(mk.MaskError):
+        idx.query(t(X[:3]), knn=3, beam=0)
+    idx.free()
+
+
+def test_host_memory_build_matches_device_build():
+    cfg = datagen.CONFIGS[2].scaled(256)
+    X = datagen.data(cfg)
+    inits = datagen.all_init_indices(cfg)
+    a = mk.build(t(X), cfg.levels, 4, inits)
+    b = mk.build(X, cfg.levels, 4, inits)
+    for l in range(1, len(cfg.levels) + 1):
+        assert rel_l2(a.prototypes(l), b.prototypes(l)) < 1e-5
+    a.free()
+    b.free()
+
+
+# ------------------------------------------------------------------ sparse (K3/K6)
+def _csr_dev(rp, col, val, dim):
+    return mk.Csr(t(rp), t(col), t(val), dim)
+
+
+def test_sparse_assign_and_build_parity():
+    rp, col, val = datagen.random_csr(400, 3000, 600, 12)
+    dense = np.zeros((3000, 600))
+    for i in range(3000):
+        dense[i, col[rp[i]:rp[i + 1]]] = val[rp[i]:rp[i + 1]]
+    inits = [datagen.init_indices(401, 1, 3000, 64), datagen.init_indices(401, 2, 64, 8)]
+    csr = _csr_dev(rp, col, val, 600)
+    P = dense[inits[0]].astype(np.float32) + datagen.random_dense(3, 64, 600, scale=0.01)
+    lab, d2, _ = mk.assign(csr, t(P))
+    check_assignment(dense, P, lab.cpu().numpy(), d2.cpu().numpy(), what="csr assign")
+    idx, _ = _step_parity_build(None, [64, 8], 5, inits, csr=csr)
+    qrp, qcol, qval = datagen.random_csr(402, 100, 600, 12)
+    _query_parity(idx, (rp, col, val), (qrp, qcol, qval), [64, 8], knn=10, beam=1,
+                  Qdev=_csr_dev(qrp, qcol, qval, 600), csr=True, dim=600)
+    idx.free()
+
+
+def test_sparse_C4_shaped_replica():
+    cfg = datagen.CONFIGS[4].scaled(256)
+    rp, col, val = datagen.data(cfg)
+    inits = datagen.all_init_indices(cfg)
+    csr = _csr_dev(rp, col, val, cfg.dim)
+    idx, _ = _step_parity_build(None, cfg.levels, 4, inits, csr=csr)
+    idx.free()
