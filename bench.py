@@ -316,7 +316,7 @@ def main():
     lvl1 = idx.level_info(1)
     n1, k1, d = n_local, lvl1["k"], cfg.dim
     assign_avg_ms = kt["assign"] / max(kt["assign_n"], 1)
-    use_tc = (not args.force_simt) and d % 8 == 0 and d >= 8
+    use_tc = idx.timing(1)["assign_kernel"] == "K1-tcgen05-3xtf32"
     if use_tc:
         flops = 6.0 * n1 * k1 * d  # 3xTF32: three TF32 products per useful multiply-add
         peak = 0.5 * pk["bf16_tflops"]

@@ -209,7 +209,9 @@ int64_t mask_kernel_launches(void);
  * build stream around each launch (only when the build ran with MASK_TIME_KERNELS):
  * out[2*c] = total milliseconds, out[2*c+1] = number of launches, for kernel class
  * c = MASK_T_ASSIGN .. MASK_T_FINALIZE; cap = number of doubles out can hold (>= 2*c+2 for
- * class c to be written).  Returns the number of doubles written or < 0 on error. */
+ * class c to be written); out[2*MASK_T_NCLASS] (cap > 8) = the assignment kernel the level
+ * used (0 = K2 FP32 SIMT, 1 = K1 tcgen05 3xTF32, 2 = K3 CSR).  Returns the number of
+ * doubles written or < 0 on error. */
 int32_t mask_get_timing(const mask_index* idx, int32_t level, double* out, int32_t cap);
 
 #ifdef __cplusplus

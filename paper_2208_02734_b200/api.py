@@ -218,12 +218,14 @@ class Index:
 
     def timing(self, level: int) -> dict:
         """CUDA-event device times of the step kernels (build with MASK_TIME_KERNELS)."""
-        out = np.zeros(8, np.float64)
-        n = load().mask_get_timing(self.handle, level, out.ctypes.data, 8)
+        out = np.zeros(9, np.float64)
+        n = load().mask_get_timing(self.handle, level, out.ctypes.data, 9)
         if n < 0:
             check(n)
         names = ["assign", "fixup", "update", "finalize"]
-        return {nm: dict(ms=float(out[2 * i]), launches=int(out[2 * i + 1])) for i, nm in enumerate(names)}
+        res = {nm: dict(ms=float(out[2 * i]), launches=int(out[2 * i + 1])) for i, nm in enumerate(names)}
+        res["assign_kernel"] = {0: "K2-simt", 1: "K1-tcgen05-3xtf32", 2: "K3-csr"}.get(int(out[8]), "none")
+        return res
 
 
 def kernel_launches() -> int:

@@ -1,14 +1,458 @@
-// assign_tc.cu -- K1: tcgen05 3xTF32 dense assignment (placeholder until the kernel lands).
+// assign_tc.cu -- K1: dense assignment on the 5th-generation tensor cores (sm_100a).
+//
+// For a block of BM = 128 points x_i and every prototype c_j (PAPER.md P:897-898,
+// `euclideanDistance` + `searchPosMin`):
+//
+//     s_ij = ||c_j||^2 - 2 x_i . c_j        a_i = argmin_j s_ij  (lowest j on ties, D4)
+//
+// (||x_i||^2 is a row constant: it does not move the argmin and is added to the winner
+// only: d^2_i = s_i + ||x_i||^2.)  The contraction x . (-2c) runs as 3xTF32 on tcgen05.mma
+// kind::tf32 with FP32 accumulation in TMEM:
+//
+//     x = xb + xs, (-2c) = cb + cs  (xb = rn_tf32(x), xs = rn_tf32(x - xb), same for c)
+//     x.(-2c) ~= xs.cb + xb.cs + xb.cb        (representation error <= 2^-22 |x| per term)
+//
+// Data movement and roles (one CTA per 128-row block, 8 warps):
+//   warp 0   TMA producer: the 128 x d A block once (SWIZZLE_128B / 64B K-major chunks of
+//            CW fp32 columns), then the B operand (prototype tiles of BN rows, big and small
+//            parts) chunk by chunk through a STAGES-deep mbarrier ring;
+//   warp 1   MMA issuer (one thread): per K step of 8, three tcgen05.mma into the TMEM
+//            accumulator of the current tile; tcgen05.commit frees the smem stage and, after
+//            the last chunk of a tile, signals the epilogue; the accumulator is
+//            double-buffered (2 x BN TMEM columns) so tile t+1's MMAs overlap tile t's epilogue;
+//   warp 2   TMEM allocator;
+//   warps 4-7 split the A block in place into (xb, xs) once, then run the epilogue: each
+//            thread owns one row (TMEM lane), loads 32 accumulator columns at a time
+//            (tcgen05.ld 32x32b.x32), adds ||c_j||^2 and keeps the running best / second-best
+//            (value, index).  At the end: label, d^2 = s1 + ||x||^2, and a near-tie flag when
+//            s2 - s1 is within the worst-case 3xTF32 error bound (those rows are recomputed
+//            exactly by K4).
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <cmath>
+#include <cstdint>
+#include <mutex>
+
 #include "common.cuh"
 
 namespace mask {
 
-bool tc_supported(int64_t, int, int64_t) { return false; }
+namespace tc {
 
-void launch_assign_tc(const float*, int64_t, int, const float*, const float*, const float*,
-                      int64_t, const float*, int32_t*, float*, int32_t*, int32_t*, float,
-                      cudaStream_t) {
-  fail(MASK_ERR_UNSUPPORTED, "tensor-core assignment not built");
+constexpr int BM = 128;
+constexpr int kThreads = 256;
+constexpr int kEpiWarp0 = 4;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+      : "=r"(ok)
+      : "r"(addr), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
+// Bounded wait: a pipeline bug traps (kernel error) instead of hanging the GPU.
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t addr = smem_u32(bar);
+  uint64_t spins = 0;
+  while (!mbar_try_wait(addr, parity)) {
+    if (++spins > (1ull << 26)) __trap();
+  }
+}
+
+__device__ __forceinline__ void fence_barrier_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y)
+      : "memory");
+}
+
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+
+// UMMA shared-memory descriptor, K-major, swizzled (SWIZZLE_128B: layout 2, SBO 1024 B;
+// SWIZZLE_64B: layout 4, SBO 512 B); version 1 (sm_100), base offset 0.
+template <int CWB>
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr) {
+  constexpr uint64_t layout = CWB == 128 ? 2 : (CWB == 64 ? 4 : 6);
+  constexpr uint64_t sbo = 8 * CWB;  // 8 rows of one swizzle atom
+  uint64_t d = 0;
+  d |= (uint64_t)((addr >> 4) & 0x3FFF);
+  d |= (uint64_t)(16 >> 4) << 16;  // LBO (unused for swizzled K-major)
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;  // descriptor version (sm_100)
+  d |= layout << 61;
+  return d;
+}
+
+// Instruction descriptor: kind::tf32, D = F32, A/B = TF32, both K-major, M x N.
+template <int M, int N>
+__host__ __device__ constexpr uint32_t idesc_tf32() {
+  return (1u << 4)            // D format F32
+         | (2u << 7)          // A format TF32
+         | (2u << 10)         // B format TF32
+         | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(
+          d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+__device__ __forceinline__ float tf32_rn(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+template <int CW, int NKC, int BN, int STAGES>
+struct Cfg {
+  static constexpr int CWB = CW * 4;                  // bytes per row of one K chunk
+  static constexpr int A_CHUNK = BM * CWB;            // bytes of one A chunk
+  static constexpr int B_CHUNK = BN * CWB;            // bytes of one B chunk (one part)
+  static constexpr int A_BYTES = 2 * NKC * A_CHUNK;   // big + small
+  static constexpr int STAGE_BYTES = 2 * B_CHUNK;     // big + small
+  static constexpr int BAR_OFF = A_BYTES + STAGES * STAGE_BYTES;
+  static constexpr int NBARS = 2 * STAGES + 4 + 2;
+  static constexpr int SMEM = BAR_OFF + NBARS * 8 + 16 + 1024;  // + alignment slack
+  static constexpr int TMEM_COLS = 2 * BN <= 32 ? 32 : (2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512)));
+  static constexpr uint32_t IDESC = idesc_tf32<BM, BN>();
+};
+
+template <int CW, int NKC, int BN, int STAGES>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_assign_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmBb,
+                const __grid_constant__ CUtensorMap tmBs, const float* __restrict__ cn2,
+                const float* __restrict__ xn2, int64_t n, int d, int64_t k,
+                int32_t* __restrict__ labels, float* __restrict__ best, int32_t* __restrict__ flag_rows,
+                int32_t* __restrict__ flag_count, float err_coef) {
+  using C = Cfg<CW, NKC, BN, STAGES>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  float* A_big = reinterpret_cast<float*>(smem);
+  float* A_small = reinterpret_cast<float*>(smem + NKC * C::A_CHUNK);
+  uint8_t* Bst = smem + C::A_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + STAGES;
+  uint64_t* tfull = bars + 2 * STAGES;
+  uint64_t* tempty = bars + 2 * STAGES + 2;
+  uint64_t* a_full = bars + 2 * STAGES + 4;
+  uint64_t* a_ready = bars + 2 * STAGES + 5;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::NBARS);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t row0 = (int64_t)blockIdx.x * BM;
+  const int ntiles = (int)((k + BN - 1) / BN);
+  const int ksteps_last = ((d - (NKC - 1) * CW) + 7) / 8;  // K steps of 8 in the last chunk
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tmA);
+    prefetch_tmap(&tmBb);
+    prefetch_tmap(&tmBs);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 128);
+    }
+    mbar_init(a_full, 1);
+    mbar_init(a_ready, 128);
+    fence_barrier_init();
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(C::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      mbar_arrive_expect_tx(a_full, NKC * C::A_CHUNK);
+      for (int c = 0; c < NKC; ++c)
+        tma_load_2d(reinterpret_cast<uint8_t*>(A_big) + c * C::A_CHUNK, &tmA, a_full, c * CW, (int)row0);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = 0; t < ntiles; ++t) {
+        for (int c = 0; c < NKC; ++c) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* dst = Bst + stage * C::STAGE_BYTES;
+          mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
+          tma_load_2d(dst, &tmBb, &full[stage], c * CW, t * BN);
+          tma_load_2d(dst + C::B_CHUNK, &tmBs, &full[stage], c * CW, t * BN);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    mbar_wait(a_ready, 0);
+    tc_fence_after();
+    int stage = 0;
+    uint32_t phase = 0;
+    const uint32_t a_big_addr = smem_u32(A_big), a_small_addr = smem_u32(A_small);
+    for (int t = 0; t < ntiles; ++t) {
+      const int acc = t & 1;
+      mbar_wait(&tempty[acc], ((t >> 1) & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
+      for (int c = 0; c < NKC; ++c) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t bb = smem_u32(Bst + stage * C::STAGE_BYTES);
+          const uint32_t bs = bb + C::B_CHUNK;
+          const uint32_t ab = a_big_addr + c * C::A_CHUNK;
+          const uint32_t as = a_small_addr + c * C::A_CHUNK;
+          const int ks_n = (c == NKC - 1) ? ksteps_last : CW / 8;
+          for (int ks = 0; ks < ks_n; ++ks) {
+            const uint32_t off = ks * 32;  // 8 tf32 = 32 bytes along K inside the swizzle atom
+            const uint64_t dab = smem_desc<C::CWB>(ab + off), das = smem_desc<C::CWB>(as + off);
+            const uint64_t dbb = smem_desc<C::CWB>(bb + off), dbs = smem_desc<C::CWB>(bs + off);
+            mma_tf32(d_tmem, das, dbb, C::IDESC, (c | ks) != 0);
+            mma_tf32(d_tmem, dab, dbs, C::IDESC, 1u);
+            mma_tf32(d_tmem, dab, dbb, C::IDESC, 1u);
+          }
+          mma_commit(&empty[stage]);
+          if (c == NKC - 1) mma_commit(&tfull[acc]);
+        }
+        __syncwarp();
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else if (warp >= kEpiWarp0) {
+    // ------------------------------------------------------------ A split + epilogue
+    const int et = threadIdx.x - kEpiWarp0 * 32;  // 0..127
+    mbar_wait(a_full, 0);
+    {
+      const int total = NKC * BM * CW;
+      for (int e = et; e < total; e += 128) {
+        const float v = A_big[e];
+        const float b = tf32_rn(v);
+        A_big[e] = b;
+        A_small[e] = tf32_rn(v - b);
+      }
+    }
+    fence_proxy_async_smem();
+    mbar_arrive(a_ready);
+
+    const int q = warp - kEpiWarp0;  // TMEM lane quarter
+    const int64_t row = row0 + q * 32 + lane;
+    float b1 = INFINITY, b2 = INFINITY;
+    int32_t i1 = 0;
+    for (int t = 0; t < ntiles; ++t) {
+      const int acc = t & 1;
+      mbar_wait(&tfull[acc], (t >> 1) & 1);
+      tc_fence_after();
+      const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
+#pragma unroll 1
+      for (int cc = 0; cc < BN / 32; ++cc) {
+        uint32_t r[32];
+        tmem_ld32(tbase + cc * 32, r);
+        tmem_wait_ld();
+        const int j0 = t * BN + cc * 32;
+        const float4* c4 = reinterpret_cast<const float4*>(cn2 + j0);
+#pragma unroll
+        for (int i = 0; i < 32; i += 4) {
+          const float4 cv = __ldg(c4 + (i >> 2));
+          const float cvv[4] = {cv.x, cv.y, cv.z, cv.w};
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const float s = __uint_as_float(r[i + u]) + cvv[u];
+            const bool lt = s < b1;
+            b2 = fminf(b2, fmaxf(b1, s));
+            b1 = fminf(b1, s);
+            i1 = lt ? (j0 + i + u) : i1;
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+    }
+    bool flag = false;
+    if (row < n) {
+      const float xx = __ldg(xn2 + row);
+      labels[row] = i1;
+      best[row] = fmaxf(b1 + xx, 0.f);
+      const float thr = err_coef * (xx + __ldg(cn2 + i1));
+      flag = (b2 - b1) <= thr;
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, flag);
+    if (m) {
+      int base = 0;
+      if (lane == 0) base = atomicAdd(flag_count, __popc(m));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (flag) flag_rows[base + __popc(m & ((1u << lane) - 1))] = (int32_t)row;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(C::TMEM_COLS));
+  }
+}
+
+// ------------------------------------------------------------------ host side
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  MASK_REQUIRE(fn != nullptr, MASK_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  return fn;
+}
+
+// 2-D fp32 row-major [rows x cols] tensor map with a {box_cols x box_rows} box.
+CUtensorMap make_map(const float* base, int64_t rows, int cols, int box_cols, int box_rows) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * 4};
+  cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  const CUtensorMapSwizzle sw = box_cols * 4 == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                : box_cols * 4 == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                                     : CU_TENSOR_MAP_SWIZZLE_32B;
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box,
+                           estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  MASK_REQUIRE(r == CUDA_SUCCESS, MASK_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  return m;
+}
+
+template <int CW, int NKC, int BN, int STAGES>
+void launch_cfg(const float* X, int64_t n, int d, const float* Pb, const float* Ps, const float* cn2, int64_t k,
+                const float* xn2, int32_t* labels, float* best, int32_t* flag_rows, int32_t* flag_count,
+                float err_coef, cudaStream_t st) {
+  using C = Cfg<CW, NKC, BN, STAGES>;
+  static_assert(C::SMEM <= 232448, "shared memory budget");
+  const CUtensorMap tA = make_map(X, n, d, CW, BM);
+  const CUtensorMap tBb = make_map(Pb, k, d, CW, BN);
+  const CUtensorMap tBs = make_map(Ps, k, d, CW, BN);
+  auto kern = k_assign_tc<CW, NKC, BN, STAGES>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    MASK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    attr_set = true;
+  }
+  const unsigned grid = (unsigned)((n + BM - 1) / BM);
+  kern<<<grid, kThreads, C::SMEM, st>>>(tA, tBb, tBs, cn2, xn2, n, d, k, labels, best, flag_rows, flag_count,
+                                        err_coef);
+  MASK_LAUNCH_CHECK();
+}
+
+}  // namespace tc
+
+int tc_bn_for(int d) { return d <= 32 ? 256 : 128; }
+
+bool tc_supported(int64_t n, int d, int64_t k) {
+  (void)k;
+  if (const char* e = getenv("MASK_DISABLE_TC")) {
+    if (e[0] == '1') return false;
+  }
+  return n >= 1 && d >= 4 && d <= 128 && d % 4 == 0;
+}
+
+// Worst-case error coefficient of the 3xTF32 score s = ||c||^2 - 2x.c, doubled for a gap of
+// two scores: representation (<= 2^-20 |x||c| summed) + FP32 accumulation of 3*ceil(d/8)
+// partial sums (<= 3 ceil(d/8) 2^-24 sum|x_i c_i|), bounded with |x||c| <= (|x|^2+|c|^2)/2.
+float tc_err_coef(int d) {
+  const double ks = std::ceil(d / 8.0);
+  const double per = std::ldexp(1.0, -20) + 3.0 * ks * std::ldexp(1.0, -24) + std::ldexp(1.0, -23);
+  return (float)(2.0 * per);
+}
+
+void launch_assign_tc(const float* X, int64_t n, int d, const float* Pb, const float* Ps, const float* cn2,
+                      int64_t k, const float* xn2, int32_t* labels, float* best, int32_t* flag_rows,
+                      int32_t* flag_count, float tau_rel, cudaStream_t st) {
+  (void)tau_rel;
+  const float coef = tc_err_coef(d);
+  if (d <= 16)
+    tc::launch_cfg<16, 1, 256, 4>(X, n, d, Pb, Ps, cn2, k, xn2, labels, best, flag_rows, flag_count, coef, st);
+  else if (d <= 32)
+    tc::launch_cfg<32, 1, 256, 3>(X, n, d, Pb, Ps, cn2, k, xn2, labels, best, flag_rows, flag_count, coef, st);
+  else if (d <= 64)
+    tc::launch_cfg<32, 2, 128, 4>(X, n, d, Pb, Ps, cn2, k, xn2, labels, best, flag_rows, flag_count, coef, st);
+  else
+    tc::launch_cfg<32, 4, 128, 3>(X, n, d, Pb, Ps, cn2, k, xn2, labels, best, flag_rows, flag_count, coef, st);
 }
 
 }  // namespace mask

@@ -143,6 +143,7 @@ void launch_children(const int32_t* labels, int64_t n, int64_t k, int64_t* offse
                      int32_t* members, int32_t* cursor_ws, cudaStream_t st);
 // finite check: flag set to 1 if any non-finite value
 void launch_check_finite(const float* v, int64_t count, int32_t* flag, cudaStream_t st);
+void launch_fill(float* p, int64_t count, float v, cudaStream_t st);
 
 // K9: batched query descent.
 struct QLevel {

@@ -513,6 +513,17 @@ void launch_check_finite(const float* v, int64_t count, int32_t* flag, cudaStrea
   MASK_LAUNCH_CHECK();
 }
 
+__global__ void k_fill(float* p, int64_t count, float v) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+
+void launch_fill(float* p, int64_t count, float v, cudaStream_t st) {
+  if (count <= 0) return;
+  k_fill<<<grid_for(count, 256), 256, 0, st>>>(p, count, v);
+  MASK_LAUNCH_CHECK();
+}
+
 // PT[i * k + j] = P[j * d + i] (d x k), used by the sparse assignment.
 __global__ void k_transpose(const float* __restrict__ P, int64_t k, int d, float* __restrict__ PT) {
   __shared__ float tile[32][33];

@@ -138,6 +138,7 @@ struct Level {
   int updates = 0;
   double t_ms[MASK_T_NCLASS] = {0, 0, 0, 0};
   int64_t t_count[MASK_T_NCLASS] = {0, 0, 0, 0};
+  int assign_kernel = -1;  // 0 = K2 SIMT, 1 = K1 tcgen05 3xTF32, 2 = K3 CSR
 };
 
 // A level's input rows as seen by this rank.
@@ -231,6 +232,7 @@ struct LloydWS {
   DevBuf<float> Pb, Ps, cn2, xn2, PT;
   DevBuf<int32_t> flag_rows, flag_count;
   bool xn2_ready = false;
+  int kernel_id = -1;
 };
 
 // One assignment pass: labels_out[i] = argmin_j ||x_i - c_j||^2, best[i] = its d^2.
@@ -244,6 +246,7 @@ int64_t assign_pass(const Input& in, const float* P, int64_t k, int flags, int32
     if (!ws.cn2.p) ws.cn2.alloc(k);
     launch_transpose(P, k, d, ws.PT.p, st);
     launch_level_norms(P, k, d, ws.cn2.p, st);
+    ws.kernel_id = 2;
     if (tm) tm->t[MASK_T_ASSIGN].start(st);
     launch_assign_csr(in.rp, in.col, in.val, n, d, ws.PT.p, ws.cn2.p, k, labels_out, best, st);
     if (tm) tm->t[MASK_T_ASSIGN].stop(st);
@@ -252,17 +255,21 @@ int64_t assign_pass(const Input& in, const float* P, int64_t k, int flags, int32
   const bool use_tc = !(flags & MASK_FORCE_SIMT) && tc_supported(n, d, k) &&
                       ((uintptr_t)in.X % 16 == 0);
   if (!use_tc) {
+    ws.kernel_id = 0;
     if (tm) tm->t[MASK_T_ASSIGN].start(st);
     launch_assign_simt(in.X, n, d, P, k, labels_out, best, st);
     if (tm) tm->t[MASK_T_ASSIGN].stop(st);
     return 0;
   }
+  // ||c||^2 is padded with +inf to a whole number of 256-prototype tiles (K1 reads it unmasked)
+  const int64_t k_pad = (k + 255) / 256 * 256;
   if (!ws.Pb.p) {
     ws.Pb.alloc((size_t)k * d);
     ws.Ps.alloc((size_t)k * d);
-    ws.cn2.alloc(k);
+    ws.cn2.alloc(k_pad);
     ws.flag_rows.alloc(n);
     ws.flag_count.alloc(1);
+    launch_fill(ws.cn2.p + k, k_pad - k, INFINITY, st);
   }
   if (!ws.xn2_ready) {
     ws.xn2.alloc(n);
@@ -271,6 +278,7 @@ int64_t assign_pass(const Input& in, const float* P, int64_t k, int flags, int32
   }
   launch_prep_protos(P, k, d, ws.Pb.p, ws.Ps.p, ws.cn2.p, st);
   MASK_CUDA(cudaMemsetAsync(ws.flag_count.p, 0, sizeof(int32_t), st));
+  ws.kernel_id = 1;
   if (tm) tm->t[MASK_T_ASSIGN].start(st);
   launch_assign_tc(in.X, n, d, ws.Pb.p, ws.Ps.p, ws.cn2.p, k, ws.xn2.p, labels_out, best,
                    ws.flag_rows.p, ws.flag_count.p, 1e-5f, st);
@@ -411,6 +419,7 @@ void run_level(const Input& in, int64_t k, const int64_t* init_idx_host, const m
   L.updates = updates;
   L.labels = std::move(ws.lab_cur);
   L.n_items = n;
+  L.assign_kernel = ws.kernel_id;
   if (tm) {
     tm->collect();
     for (int c = 0; c < MASK_T_NCLASS; ++c) {
@@ -885,6 +894,10 @@ int32_t mask_get_timing(const mask_index* idx, int32_t level, double* out, int32
       out[2 * c] = L.t_ms[c];
       out[2 * c + 1] = (double)L.t_count[c];
       written = 2 * c + 2;
+    }
+    if (cap > 2 * MASK_T_NCLASS) {
+      out[2 * MASK_T_NCLASS] = (double)L.assign_kernel;
+      written = 2 * MASK_T_NCLASS + 1;
     }
   });
   return rc == MASK_OK ? written : rc;
