@@ -42,7 +42,6 @@ namespace mask {
 namespace tc {
 
 constexpr int BM = 128;
-constexpr int kThreads = 256;
 constexpr int kEpiWarp0 = 4;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -165,7 +164,13 @@ __device__ __forceinline__ float tf32_rn(float x) {
   return __uint_as_float(r);
 }
 
-template <int CW, int NKC, int BN, int STAGES>
+// FOLD (small d, d + 2 <= CW): the row constant ||x||^2 and the column constant ||c||^2 are
+// folded into the contraction as two extra K columns (A: [x | 1 | ||x||^2], B: [-2c |
+// ||c||^2 | 1]), so the accumulator holds the squared-distance estimate itself and the
+// epilogue only packs (value, column) into one int key and keeps the two smallest keys
+// (4 ALU ops per element).  Otherwise (large d, tensor-bound) the epilogue adds ||c||^2
+// from global memory and tracks the top-2 in FP32.
+template <int CW, int NKC, int BN, int STAGES, bool FOLD, int EPI_WG>
 struct Cfg {
   static constexpr int CWB = CW * 4;                  // bytes per row of one K chunk
   static constexpr int A_CHUNK = BM * CWB;            // bytes of one A chunk
@@ -174,19 +179,35 @@ struct Cfg {
   static constexpr int STAGE_BYTES = 2 * B_CHUNK;     // big + small
   static constexpr int BAR_OFF = A_BYTES + STAGES * STAGE_BYTES;
   static constexpr int NBARS = 2 * STAGES + 4 + 2;
-  static constexpr int SMEM = BAR_OFF + NBARS * 8 + 16 + 1024;  // + alignment slack
+  static constexpr int SMEM = BAR_OFF + NBARS * 8 + 16 + 3 * BM * 4 + 1024;  // + merge scratch + alignment
   static constexpr int TMEM_COLS = 2 * BN <= 32 ? 32 : (2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512)));
   static constexpr uint32_t IDESC = idesc_tf32<BM, BN>();
 };
 
-template <int CW, int NKC, int BN, int STAGES>
-__global__ void __launch_bounds__(kThreads, 1)
+// byte offset of element (r, c) inside a K-major swizzled chunk (16-byte granule c/4 of row
+// r is stored at granule (c/4) ^ (r % 8) for SWIZZLE_128B, ^ ((r/2) % 4) for SWIZZLE_64B)
+template <int CWB>
+__device__ __forceinline__ uint32_t swz_off(int r, int c) {
+  const int g = c >> 2;
+  int pg;
+  if (CWB == 128) pg = g ^ (r & 7);
+  else if (CWB == 64) pg = g ^ ((r >> 1) & 3);
+  else pg = g ^ ((r >> 2) & 1);
+  return (uint32_t)(r * CWB + pg * 16 + (c & 3) * 4);
+}
+
+__device__ __forceinline__ int32_t imin(int32_t a, int32_t b) { return a < b ? a : b; }
+__device__ __forceinline__ int32_t imax(int32_t a, int32_t b) { return a > b ? a : b; }
+
+template <int CW, int NKC, int BN, int STAGES, bool FOLD, int EPI_WG>
+__global__ void __launch_bounds__(128 + 128 * EPI_WG, 1)
     k_assign_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmBb,
-                const __grid_constant__ CUtensorMap tmBs, const float* __restrict__ cn2,
-                const float* __restrict__ xn2, int64_t n, int d, int64_t k,
+                const __grid_constant__ CUtensorMap tmBs, const float* __restrict__ X,
+                const float* __restrict__ P, const float* __restrict__ cn2,
+                const float* __restrict__ xn2, int64_t n, int d, int k_cols, int64_t k,
                 int32_t* __restrict__ labels, float* __restrict__ best, int32_t* __restrict__ flag_rows,
-                int32_t* __restrict__ flag_count, float err_coef) {
-  using C = Cfg<CW, NKC, BN, STAGES>;
+                int32_t* __restrict__ flag_count, float err_coef, uint32_t key_hi_mul, uint32_t key_lo_mul) {
+  using C = Cfg<CW, NKC, BN, STAGES, FOLD, EPI_WG>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   float* A_big = reinterpret_cast<float*>(smem);
@@ -204,7 +225,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t row0 = (int64_t)blockIdx.x * BM;
   const int ntiles = (int)((k + BN - 1) / BN);
-  const int ksteps_last = ((d - (NKC - 1) * CW) + 7) / 8;  // K steps of 8 in the last chunk
+  const int ksteps_last = ((k_cols - (NKC - 1) * CW) + 7) / 8;  // K steps of 8 in the last chunk
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmA);
@@ -216,10 +237,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 128);
+      mbar_init(&tempty[a], 128 * EPI_WG);
     }
     mbar_init(a_full, 1);
-    mbar_init(a_ready, 128);
+    mbar_init(a_ready, 128 * EPI_WG);
     fence_barrier_init();
   }
   if (warp == 2) {
@@ -295,67 +316,203 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp >= kEpiWarp0) {
     // ------------------------------------------------------------ A split + epilogue
-    const int et = threadIdx.x - kEpiWarp0 * 32;  // 0..127
+    // EPI_WG epilogue warpgroups; warpgroup g handles accumulator columns [g*BN/EPI_WG, ...)
+    // of every tile for the 128 rows (TMEM lane quarter = warp % 4).
+    constexpr int NEPI = 128 * EPI_WG;
+    constexpr int COLS = BN / EPI_WG;
+    const int et = threadIdx.x - kEpiWarp0 * 32;  // 0..NEPI-1
+    const int wg = et >> 7;                       // epilogue warpgroup
+    const int q = warp & 3;                       // TMEM lane quarter
+    const int rloc = q * 32 + lane;               // row of this thread inside the block
+    const int64_t row = row0 + rloc;
+    const float xx = row < n ? __ldg(xn2 + row) : 0.f;
     mbar_wait(a_full, 0);
     {
       const int total = NKC * BM * CW;
-      for (int e = et; e < total; e += 128) {
+      for (int e = et; e < total; e += NEPI) {
         const float v = A_big[e];
         const float b = tf32_rn(v);
         A_big[e] = b;
         A_small[e] = tf32_rn(v - b);
       }
     }
+    if (FOLD) {
+      // augmented columns of this thread's row: A[r, d] = 1, A[r, d+1] = ||x_r||^2 (split)
+      asm volatile("bar.sync 1, %0;" ::"n"(NEPI) : "memory");
+      if (wg == 0) {
+        uint8_t* ab = reinterpret_cast<uint8_t*>(A_big);
+        uint8_t* as = reinterpret_cast<uint8_t*>(A_small);
+        const float hb = tf32_rn(xx);
+        *reinterpret_cast<float*>(ab + swz_off<C::CWB>(rloc, d)) = 1.0f;
+        *reinterpret_cast<float*>(as + swz_off<C::CWB>(rloc, d)) = 0.0f;
+        *reinterpret_cast<float*>(ab + swz_off<C::CWB>(rloc, d + 1)) = hb;
+        *reinterpret_cast<float*>(as + swz_off<C::CWB>(rloc, d + 1)) = tf32_rn(xx - hb);
+      }
+    }
     fence_proxy_async_smem();
     mbar_arrive(a_ready);
 
-    const int q = warp - kEpiWarp0;  // TMEM lane quarter
-    const int64_t row = row0 + q * 32 + lane;
-    float b1 = INFINITY, b2 = INFINITY;
-    int32_t i1 = 0;
+    // running result over all tiles (this warpgroup's columns)
+    float g1 = INFINITY, g2 = INFINITY;
+    int32_t gi = 0x7fffffff;
     for (int t = 0; t < ntiles; ++t) {
       const int acc = t & 1;
       mbar_wait(&tfull[acc], (t >> 1) & 1);
       tc_fence_after();
-      const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
-#pragma unroll 1
-      for (int cc = 0; cc < BN / 32; ++cc) {
-        uint32_t r[32];
-        tmem_ld32(tbase + cc * 32, r);
-        tmem_wait_ld();
-        const int j0 = t * BN + cc * 32;
-        const float4* c4 = reinterpret_cast<const float4*>(cn2 + j0);
+      const int col0 = wg * COLS;  // first column of this warpgroup inside the tile
+      const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + col0);
+      float v1, v2;
+      int32_t j1;
+      if (FOLD) {
+        // packed keys: (float bits with the low 8 mantissa bits replaced by the column in the
+        // tile); signed-int order = value order for values >= 0, ties -> lower column
+        int32_t b1[4], b2[4];
 #pragma unroll
-        for (int i = 0; i < 32; i += 4) {
-          const float4 cv = __ldg(c4 + (i >> 2));
-          const float cvv[4] = {cv.x, cv.y, cv.z, cv.w};
+        for (int u = 0; u < 4; ++u) b1[u] = b2[u] = 0x7fffffff;
+        uint32_t r[2][32];
+        tmem_ld32(tbase, r[0]);
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const float s = __uint_as_float(r[i + u]) + cvv[u];
-            const bool lt = s < b1;
-            b2 = fminf(b2, fmaxf(b1, s));
-            b1 = fminf(b1, s);
-            i1 = lt ? (j0 + i + u) : i1;
+        for (int cc = 0; cc < COLS / 32; ++cc) {
+          tmem_wait_ld();
+          if (cc + 1 < COLS / 32) tmem_ld32(tbase + (cc + 1) * 32, r[(cc + 1) & 1]);
+#pragma unroll
+          for (int i = 0; i < 32; i += 2) {
+            // key = (bits >> 8) * 256 + column, built with two integer multiply-adds on the
+            // FMA pipe (the multipliers are kernel arguments so they stay IMADs) -- the
+            // min/max work below runs on the ALU pipe, which is the epilogue's limiter.
+            int32_t ka, kb;
+            asm("{\n .reg .u32 h;\n mul.hi.u32 h, %1, %2;\n mad.lo.u32 %0, h, %3, %4;\n}"
+                : "=r"(ka)
+                : "r"(r[cc & 1][i]), "r"(key_hi_mul), "r"(key_lo_mul), "r"((uint32_t)(cc * 32 + i)));
+            asm("{\n .reg .u32 h;\n mul.hi.u32 h, %1, %2;\n mad.lo.u32 %0, h, %3, %4;\n}"
+                : "=r"(kb)
+                : "r"(r[cc & 1][i + 1]), "r"(key_hi_mul), "r"(key_lo_mul), "r"((uint32_t)(cc * 32 + i + 1)));
+            // top-2 of {b1 <= b2} u {ka, kb}: b1' = min(b1, m), b2' = min(b2, M, max(b1, m))
+            const int u = (i >> 1) & 3;
+            const int32_t m = imin(ka, kb), M = imax(ka, kb);
+            const int32_t t2 = imax(b1[u], m);
+            b1[u] = imin(b1[u], m);
+            b2[u] = imin(imin(b2[u], M), t2);
           }
         }
+        tc_fence_before();
+        mbar_arrive(&tempty[acc]);
+        const int32_t k1 = imin(imin(b1[0], b1[1]), imin(b1[2], b1[3]));
+        int32_t k2 = 0x7fffffff;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) k2 = imin(k2, b1[u] == k1 ? b2[u] : b1[u]);
+        v1 = __int_as_float(k1 & 0xFFFFFF00);
+        v2 = __int_as_float(k2 & 0xFFFFFF00);
+        j1 = col0 + (k1 & 0xFF);
+      } else {
+        float b1[4], b2[4];
+        int32_t i1[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          b1[u] = b2[u] = INFINITY;
+          i1[u] = 0;
+        }
+        uint32_t r[2][32];
+        tmem_ld32(tbase, r[0]);
+#pragma unroll
+        for (int cc = 0; cc < COLS / 32; ++cc) {
+          tmem_wait_ld();
+          if (cc + 1 < COLS / 32) tmem_ld32(tbase + (cc + 1) * 32, r[(cc + 1) & 1]);
+          const float4* c4 = reinterpret_cast<const float4*>(cn2 + t * BN + col0 + cc * 32);
+#pragma unroll
+          for (int i = 0; i < 32; i += 4) {
+            const float4 cv = __ldg(c4 + (i >> 2));
+            const float cvv[4] = {cv.x, cv.y, cv.z, cv.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const float s = __uint_as_float(r[cc & 1][i + u]) + cvv[u];
+              const bool lt = s < b1[u];
+              b2[u] = fminf(b2[u], fmaxf(b1[u], s));
+              b1[u] = fminf(b1[u], s);
+              i1[u] = lt ? (cc * 32 + i + u) : i1[u];
+            }
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(&tempty[acc]);
+        // merge the 4 chains (lowest column on exact ties)
+        v1 = b1[0];
+        j1 = i1[0];
+#pragma unroll
+        for (int u = 1; u < 4; ++u)
+          if (b1[u] < v1 || (b1[u] == v1 && i1[u] < j1)) {
+            v1 = b1[u];
+            j1 = i1[u];
+          }
+        v2 = INFINITY;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v2 = fminf(v2, (b1[u] == v1 && i1[u] == j1) ? b2[u] : b1[u]);
+        j1 += col0;
       }
-      tc_fence_before();
-      mbar_arrive(&tempty[acc]);
+      if (v1 < g1) {  // strict: ties keep the earlier tile (lower prototype index)
+        g2 = fminf(g1, v2);
+        g1 = v1;
+        gi = t * BN + j1;
+      } else {
+        g2 = fminf(g2, v1);
+      }
     }
-    bool flag = false;
-    if (row < n) {
-      const float xx = __ldg(xn2 + row);
-      labels[row] = i1;
-      best[row] = fmaxf(b1 + xx, 0.f);
-      const float thr = err_coef * (xx + __ldg(cn2 + i1));
-      flag = (b2 - b1) <= thr;
+    // ---- merge the warpgroups' results for each row (lowest index on equal values)
+    if (EPI_WG > 1) {
+      float* mg1 = reinterpret_cast<float*>(tmem_slot + 4);
+      float* mg2 = mg1 + BM;
+      int32_t* mgi = reinterpret_cast<int32_t*>(mg2 + BM);
+      if (wg == 1) {
+        mg1[rloc] = g1;
+        mg2[rloc] = g2;
+        mgi[rloc] = gi;
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(NEPI) : "memory");
+      if (wg == 0) {
+        const float o1 = mg1[rloc], o2 = mg2[rloc];
+        const int32_t oi = mgi[rloc];
+        if (o1 < g1 || (o1 == g1 && oi < gi)) {
+          g2 = fminf(g1, o2);
+          g1 = o1;
+          gi = oi;
+        } else {
+          g2 = fminf(g2, o1);
+        }
+      }
     }
-    const unsigned m = __ballot_sync(0xffffffffu, flag);
-    if (m) {
-      int base = 0;
-      if (lane == 0) base = atomicAdd(flag_count, __popc(m));
-      base = __shfl_sync(0xffffffffu, base, 0);
-      if (flag) flag_rows[base + __popc(m & ((1u << lane) - 1))] = (int32_t)row;
+    if (wg == 0) {
+      bool flag = false;
+      if (row < n) {
+        labels[row] = gi;
+        // exact FP32 squared distance of the chosen prototype (direct form, for J and d2_out)
+        const float* xr = X + row * d;
+        const float* cr = P + (int64_t)gi * d;
+        float dd = 0.f;
+        for (int i = 0; i < d; i += 4) {
+          const float4 xv = __ldg(reinterpret_cast<const float4*>(xr + i));
+          const float4 cv = __ldg(reinterpret_cast<const float4*>(cr + i));
+          float tt = xv.x - cv.x;
+          dd = fmaf(tt, tt, dd);
+          tt = xv.y - cv.y;
+          dd = fmaf(tt, tt, dd);
+          tt = xv.z - cv.z;
+          dd = fmaf(tt, tt, dd);
+          tt = xv.w - cv.w;
+          dd = fmaf(tt, tt, dd);
+        }
+        best[row] = dd;
+        const float cc2 = __ldg(cn2 + gi);
+        float thr = err_coef * (xx + cc2);
+        if (FOLD) thr += ldexpf(fmaxf(fabsf(g2), fabsf(g1)), -14);  // key quantisation (2^-15 rel) x 2
+        flag = (g2 - g1) <= thr;
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, flag);
+      if (m) {
+        int base = 0;
+        if (lane == 0) base = atomicAdd(flag_count, __popc(m));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (flag) flag_rows[base + __popc(m & ((1u << lane) - 1))] = (int32_t)row;
+      }
     }
   }
   tc_fence_before();
@@ -398,30 +555,28 @@ CUtensorMap make_map(const float* base, int64_t rows, int cols, int box_cols, in
   return m;
 }
 
-template <int CW, int NKC, int BN, int STAGES>
-void launch_cfg(const float* X, int64_t n, int d, const float* Pb, const float* Ps, const float* cn2, int64_t k,
-                const float* xn2, int32_t* labels, float* best, int32_t* flag_rows, int32_t* flag_count,
-                float err_coef, cudaStream_t st) {
-  using C = Cfg<CW, NKC, BN, STAGES>;
+template <int CW, int NKC, int BN, int STAGES, bool FOLD, int EPI_WG>
+void launch_cfg(const float* X, int64_t n, int d, int kc, const float* P, const float* Pb, const float* Ps,
+                const float* cn2, int64_t k, const float* xn2, int32_t* labels, float* best, int32_t* flag_rows,
+                int32_t* flag_count, float err_coef, cudaStream_t st) {
+  using C = Cfg<CW, NKC, BN, STAGES, FOLD, EPI_WG>;
   static_assert(C::SMEM <= 232448, "shared memory budget");
   const CUtensorMap tA = make_map(X, n, d, CW, BM);
-  const CUtensorMap tBb = make_map(Pb, k, d, CW, BN);
-  const CUtensorMap tBs = make_map(Ps, k, d, CW, BN);
-  auto kern = k_assign_tc<CW, NKC, BN, STAGES>;
+  const CUtensorMap tBb = make_map(Pb, k, kc, CW, BN);
+  const CUtensorMap tBs = make_map(Ps, k, kc, CW, BN);
+  auto kern = k_assign_tc<CW, NKC, BN, STAGES, FOLD, EPI_WG>;
   static bool attr_set = false;
   if (!attr_set) {
     MASK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     attr_set = true;
   }
   const unsigned grid = (unsigned)((n + BM - 1) / BM);
-  kern<<<grid, kThreads, C::SMEM, st>>>(tA, tBb, tBs, cn2, xn2, n, d, k, labels, best, flag_rows, flag_count,
-                                        err_coef);
+  kern<<<grid, 128 + 128 * EPI_WG, C::SMEM, st>>>(tA, tBb, tBs, X, P, cn2, xn2, n, d, kc, k, labels, best,
+                                                  flag_rows, flag_count, err_coef, 1u << 24, 256u);
   MASK_LAUNCH_CHECK();
 }
 
 }  // namespace tc
-
-int tc_bn_for(int d) { return d <= 32 ? 256 : 128; }
 
 bool tc_supported(int64_t n, int d, int64_t k) {
   (void)k;
@@ -431,28 +586,35 @@ bool tc_supported(int64_t n, int d, int64_t k) {
   return n >= 1 && d >= 4 && d <= 128 && d % 4 == 0;
 }
 
-// Worst-case error coefficient of the 3xTF32 score s = ||c||^2 - 2x.c, doubled for a gap of
-// two scores: representation (<= 2^-20 |x||c| summed) + FP32 accumulation of 3*ceil(d/8)
-// partial sums (<= 3 ceil(d/8) 2^-24 sum|x_i c_i|), bounded with |x||c| <= (|x|^2+|c|^2)/2.
+int tc_operand_cols(int d) { return d + 2 <= 32 ? ((d + 2 + 3) / 4) * 4 : d; }
+
+// Worst-case error coefficient of the 3xTF32 score, doubled for a gap of two scores:
+// representation (<= 2^-20 |x||c| summed over the three products and the dropped xs.cs)
+// + FP32 accumulation of 3*ceil(K/8) partial sums (<= 3 ceil(K/8) 2^-24 sum|x_i c_i|) + the
+// final rounding, bounded with |x||c| <= (|x|^2+|c|^2)/2.
 float tc_err_coef(int d) {
-  const double ks = std::ceil(d / 8.0);
-  const double per = std::ldexp(1.0, -20) + 3.0 * ks * std::ldexp(1.0, -24) + std::ldexp(1.0, -23);
+  const double ks = std::ceil(tc_operand_cols(d) / 8.0);
+  const double per = std::ldexp(1.0, -20) + 3.0 * ks * std::ldexp(1.0, -24) + std::ldexp(1.0, -22);
   return (float)(2.0 * per);
 }
 
-void launch_assign_tc(const float* X, int64_t n, int d, const float* Pb, const float* Ps, const float* cn2,
-                      int64_t k, const float* xn2, int32_t* labels, float* best, int32_t* flag_rows,
-                      int32_t* flag_count, float tau_rel, cudaStream_t st) {
-  (void)tau_rel;
+void launch_assign_tc(const float* X, int64_t n, int d, const float* P, const float* Pb, const float* Ps,
+                      const float* cn2, int64_t k, const float* xn2, int32_t* labels, float* best,
+                      int32_t* flag_rows, int32_t* flag_count, cudaStream_t st) {
   const float coef = tc_err_coef(d);
-  if (d <= 16)
-    tc::launch_cfg<16, 1, 256, 4>(X, n, d, Pb, Ps, cn2, k, xn2, labels, best, flag_rows, flag_count, coef, st);
+  const int kc = tc_operand_cols(d);
+  if (d + 2 <= 32)
+    tc::launch_cfg<32, 1, 256, 3, true, 2>(X, n, d, kc, P, Pb, Ps, cn2, k, xn2, labels, best, flag_rows, flag_count,
+                                           coef, st);
   else if (d <= 32)
-    tc::launch_cfg<32, 1, 256, 3>(X, n, d, Pb, Ps, cn2, k, xn2, labels, best, flag_rows, flag_count, coef, st);
+    tc::launch_cfg<32, 1, 256, 3, false, 2>(X, n, d, kc, P, Pb, Ps, cn2, k, xn2, labels, best, flag_rows,
+                                            flag_count, coef, st);
   else if (d <= 64)
-    tc::launch_cfg<32, 2, 128, 4>(X, n, d, Pb, Ps, cn2, k, xn2, labels, best, flag_rows, flag_count, coef, st);
+    tc::launch_cfg<32, 2, 128, 4, false, 1>(X, n, d, kc, P, Pb, Ps, cn2, k, xn2, labels, best, flag_rows,
+                                            flag_count, coef, st);
   else
-    tc::launch_cfg<32, 4, 128, 3>(X, n, d, Pb, Ps, cn2, k, xn2, labels, best, flag_rows, flag_count, coef, st);
+    tc::launch_cfg<32, 4, 128, 3, false, 1>(X, n, d, kc, P, Pb, Ps, cn2, k, xn2, labels, best, flag_rows,
+                                            flag_count, coef, st);
 }
 
 }  // namespace mask

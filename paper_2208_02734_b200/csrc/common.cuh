@@ -100,16 +100,24 @@ void launch_assign_simt(const float* X, int64_t n, int d, const float* P, int64_
 // estimate incl. ||x||^2), and appends rows whose top-2 gap is within the error bound to
 // flag_rows / flag_count (device).  Returns false if the shape is unsupported.
 bool tc_supported(int64_t n, int d, int64_t k);
-void launch_assign_tc(const float* X, int64_t n, int d, const float* Pb, const float* Ps,
-                      const float* cn2, int64_t k, const float* xn2, int32_t* labels,
-                      float* best, int32_t* flag_rows, int32_t* flag_count, float tau_rel,
+// columns of the K1 B operand arrays Pb/Ps: d, or d+2 rounded up to 4 when ||x||^2 and ||c||^2
+// are folded into the contraction (small d)
+int tc_operand_cols(int d);
+void launch_assign_tc(const float* X, int64_t n, int d, const float* P, const float* Pb,
+                      const float* Ps, const float* cn2, int64_t k, const float* xn2,
+                      int32_t* labels, float* best, int32_t* flag_rows, int32_t* flag_count,
                       cudaStream_t st);
 // K4: exact FP32 direct re-check of flagged rows against all k prototypes.
 void launch_fixup(const float* X, int d, const float* P, int64_t k, const int32_t* flag_rows,
                   const int32_t* flag_count, int64_t max_flags, int32_t* labels, float* best,
                   cudaStream_t st);
-// prototype operands for K1: Pb = tf32_rn(-2c), Ps = tf32_rn(-2c - Pb), cn2 = ||c||^2
-void launch_prep_protos(const float* P, int64_t k, int d, float* Pb, float* Ps, float* cn2,
+// K4 (tiled): nf flagged rows (host-known count) against all prototypes; keys_ws = nf u64
+void launch_fixup_tiled(const float* X, int d, const float* P, int64_t k, const int32_t* flag_rows,
+                        int64_t nf, unsigned long long* keys_ws, int32_t* labels, float* best,
+                        cudaStream_t st);
+// prototype operands for K1: Pb = tf32_rn(-2c), Ps = tf32_rn(-2c - Pb), cn2 = ||c||^2; with
+// kc > d the augmented columns [d] = split(||c||^2), [d+1] = (1, 0), rest 0 (row stride kc)
+void launch_prep_protos(const float* P, int64_t k, int d, int kc, float* Pb, float* Ps, float* cn2,
                         cudaStream_t st);
 void launch_row_norms(const float* X, int64_t n, int d, float* xn2, cudaStream_t st);
 

@@ -233,6 +233,8 @@ struct LloydWS {
   DevBuf<int32_t> flag_rows, flag_count;
   bool xn2_ready = false;
   int kernel_id = -1;
+  DevBuf<unsigned long long> fix_keys;
+  int64_t last_flagged = 0;
 };
 
 // One assignment pass: labels_out[i] = argmin_j ||x_i - c_j||^2, best[i] = its d^2.
@@ -263,9 +265,10 @@ int64_t assign_pass(const Input& in, const float* P, int64_t k, int flags, int32
   }
   // ||c||^2 is padded with +inf to a whole number of 256-prototype tiles (K1 reads it unmasked)
   const int64_t k_pad = (k + 255) / 256 * 256;
+  const int kc = tc_operand_cols(d);
   if (!ws.Pb.p) {
-    ws.Pb.alloc((size_t)k * d);
-    ws.Ps.alloc((size_t)k * d);
+    ws.Pb.alloc((size_t)k * kc);
+    ws.Ps.alloc((size_t)k * kc);
     ws.cn2.alloc(k_pad);
     ws.flag_rows.alloc(n);
     ws.flag_count.alloc(1);
@@ -276,22 +279,26 @@ int64_t assign_pass(const Input& in, const float* P, int64_t k, int flags, int32
     launch_row_norms(in.X, n, d, ws.xn2.p, st);
     ws.xn2_ready = true;
   }
-  launch_prep_protos(P, k, d, ws.Pb.p, ws.Ps.p, ws.cn2.p, st);
+  launch_prep_protos(P, k, d, kc, ws.Pb.p, ws.Ps.p, ws.cn2.p, st);
   MASK_CUDA(cudaMemsetAsync(ws.flag_count.p, 0, sizeof(int32_t), st));
   ws.kernel_id = 1;
   if (tm) tm->t[MASK_T_ASSIGN].start(st);
-  launch_assign_tc(in.X, n, d, ws.Pb.p, ws.Ps.p, ws.cn2.p, k, ws.xn2.p, labels_out, best,
-                   ws.flag_rows.p, ws.flag_count.p, 1e-5f, st);
+  launch_assign_tc(in.X, n, d, P, ws.Pb.p, ws.Ps.p, ws.cn2.p, k, ws.xn2.p, labels_out, best,
+                   ws.flag_rows.p, ws.flag_count.p, st);
   if (tm) tm->t[MASK_T_ASSIGN].stop(st);
-  if (!(flags & MASK_NO_FIXUP)) {
+  // near-tie re-check (K4): the flagged-row count sizes the tiled grid (one small D2H read)
+  MASK_CUDA(cudaMemcpyAsync(hs->flags, ws.flag_count.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  MASK_CUDA(cudaStreamSynchronize(st));
+  const int64_t nf = *hs->flags;
+  if (!(flags & MASK_NO_FIXUP) && nf > 0) {
+    if ((int64_t)ws.fix_keys.n < nf) ws.fix_keys.alloc((size_t)nf + nf / 4 + 1024);
     if (tm) tm->t[MASK_T_FIXUP].start(st);
-    launch_fixup(in.X, d, P, k, ws.flag_rows.p, ws.flag_count.p, n, labels_out, best, st);
+    launch_fixup_tiled(in.X, d, P, k, ws.flag_rows.p, nf, ws.fix_keys.p, labels_out, best, st);
     if (tm) tm->t[MASK_T_FIXUP].stop(st);
   }
+  ws.last_flagged = nf;
   if (hs) {
-    MASK_CUDA(cudaMemcpyAsync(hs->flags, ws.flag_count.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-    MASK_CUDA(cudaStreamSynchronize(st));
-    return *hs->flags;
+    return nf;
   }
   return -1;
 }
@@ -373,7 +380,7 @@ void run_level(const Input& in, int64_t k, const int64_t* init_idx_host, const m
     fin_pending = false;
   };
   for (int t = 0; t < T; ++t) {
-    assign_pass(in, L.P.p, k, p->flags, ws.lab_cur.p, ws.best.p, ws, st, nullptr, tm);
+    assign_pass(in, L.P.p, k, p->flags, ws.lab_cur.p, ws.best.p, ws, st, &hs, tm);
     pass_stats(ws.lab_cur.p, ws.lab_prev.p);  // synchronises the stream
     read_fin();
     emit_cb(t, ws.lab_cur.p);
@@ -411,7 +418,7 @@ void run_level(const Input& in, int64_t k, const int64_t* init_idx_host, const m
     }
   }
   // ---- final assignment with the final prototypes (D3)
-  assign_pass(in, L.P.p, k, p->flags, ws.lab_cur.p, ws.best.p, ws, st, nullptr, tm);
+  assign_pass(in, L.P.p, k, p->flags, ws.lab_cur.p, ws.best.p, ws, st, &hs, tm);
   pass_stats(ws.lab_cur.p, ws.lab_prev.p);
   read_fin();
   L.empties.push_back(0);

@@ -38,8 +38,11 @@ def check_assignment(Y, P, labels_gpu, d2_gpu=None, what=""):
         ref = ((Y - P[labels_gpu]) ** 2).sum(axis=1)
         err = np.abs(d2_gpu - ref)
         # FP32 value of a squared distance: 1e-5 of itself, plus (expanded form, tensor path)
-        # 1e-6 of the magnitudes ||x||^2 + ||c||^2 that cancel in ||x||^2 + ||c||^2 - 2 x.c
-        allow = 1e-5 * ref + 1e-6 * ((Y ** 2).sum(axis=1) + (P[labels_gpu] ** 2).sum(axis=1)) + 1e-30
+        # the worst-case 3xTF32 error of ||c||^2 - 2 x.c relative to the magnitudes that
+        # cancel in it: (2^-20 + 3 ceil(d/8) 2^-24 + 2^-23) (||x||^2 + ||c||^2)  (K1)
+        d = Y.shape[1]
+        coef = 2.0 ** -20 + 3 * np.ceil(d / 8) * 2.0 ** -24 + 2.0 ** -23
+        allow = 1e-5 * ref + coef * ((Y ** 2).sum(axis=1) + (P[labels_gpu] ** 2).sum(axis=1)) + 1e-30
         assert np.all(err <= allow), f"{what}: d2 max err/allow {float((err / allow).max())}"
     return int(diff.sum()), int(exempt.sum())
 

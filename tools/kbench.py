@@ -54,6 +54,18 @@ def main():
         times.append(e0.elapsed_time(e1))
     ms = min(times)
     useful = 2.0 * a.n * a.k * a.d
+    # kernel-only time of the assignment launch (CUDA events inside the library, T = 0 build)
+    kt = []
+    for _ in range(a.reps):
+        flush.zero_()
+        idx = mk.build(Xd, [a.k], 0, [datagen.init_indices(77, 1, a.n, a.k)],
+                       flags=mk.MASK_TIME_KERNELS | mk.MASK_BORROW_DATA | flags)
+        tm = idx.timing(1)
+        kt.append((tm["assign"]["ms"], tm["fixup"]["ms"], tm["assign_kernel"]))
+        idx.free()
+    k_ms, f_ms, kname = min(kt)
+    print(f"[{kname}] kernel_ms={k_ms:.3f} fixup_ms={f_ms:.3f} useful_TF={useful / k_ms / 1e9:.1f} "
+          f"tensor3x_TF={3 * useful / k_ms / 1e9:.1f} frac_of_808={3 * useful / k_ms / 1e9 / 808.1:.3f}")
     print(f"n={a.n} d={a.d} k={a.k} simt={a.simt} call_ms={ms:.3f} (includes prep/fixup/alloc) "
           f"useful_TF={useful / ms / 1e9:.1f} tensor3x_TF={3 * useful / ms / 1e9:.1f} flagged={nf} "
           f"({100.0 * nf / a.n:.3f}%)")
