@@ -33,7 +33,10 @@
 
 #include <cmath>
 #include <cstdint>
+#include <algorithm>
+#include <cstdio>
 #include <mutex>
+#include <vector>
 
 #include "common.cuh"
 
@@ -164,83 +167,100 @@ __device__ __forceinline__ float tf32_rn(float x) {
   return __uint_as_float(r);
 }
 
-// FOLD (small d, d + 2 <= CW): the row constant ||x||^2 and the column constant ||c||^2 are
-// folded into the contraction as two extra K columns (A: [x | 1 | ||x||^2], B: [-2c |
-// ||c||^2 | 1]), so the accumulator holds the squared-distance estimate itself and the
-// epilogue only packs (value, column) into one int key and keeps the two smallest keys
-// (4 ALU ops per element).  Otherwise (large d, tensor-bound) the epilogue adds ||c||^2
-// from global memory and tracks the top-2 in FP32.
-template <int CW, int NKC, int BN, int STAGES, bool FOLD, int EPI_WG>
-struct Cfg {
-  static constexpr int CWB = CW * 4;                  // bytes per row of one K chunk
-  static constexpr int A_CHUNK = BM * CWB;            // bytes of one A chunk
-  static constexpr int B_CHUNK = BN * CWB;            // bytes of one B chunk (one part)
-  static constexpr int A_BYTES = 2 * NKC * A_CHUNK;   // big + small
-  static constexpr int STAGE_BYTES = 2 * B_CHUNK;     // big + small
-  static constexpr int BAR_OFF = A_BYTES + STAGES * STAGE_BYTES;
-  static constexpr int NBARS = 2 * STAGES + 4 + 2;
-  static constexpr int SMEM = BAR_OFF + NBARS * 8 + 16 + 3 * BM * 4 + 1024;  // + merge scratch + alignment
-  static constexpr int TMEM_COLS = 2 * BN <= 32 ? 32 : (2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512)));
-  static constexpr uint32_t IDESC = idesc_tf32<BM, BN>();
-};
-
-// byte offset of element (r, c) inside a K-major swizzled chunk (16-byte granule c/4 of row
-// r is stored at granule (c/4) ^ (r % 8) for SWIZZLE_128B, ^ ((r/2) % 4) for SWIZZLE_64B)
-template <int CWB>
-__device__ __forceinline__ uint32_t swz_off(int r, int c) {
-  const int g = c >> 2;
-  int pg;
-  if (CWB == 128) pg = g ^ (r & 7);
-  else if (CWB == 64) pg = g ^ ((r >> 1) & 3);
-  else pg = g ^ ((r >> 2) & 1);
-  return (uint32_t)(r * CWB + pg * 16 + (c & 3) * 4);
+__device__ __forceinline__ void mma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}" ::"r"(
+          d_tmem),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(accumulate)
+      : "memory");
 }
+
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&v)[8]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(taddr), "r"(v[0]),
+               "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 __device__ __forceinline__ int32_t imin(int32_t a, int32_t b) { return a < b ? a : b; }
 __device__ __forceinline__ int32_t imax(int32_t a, int32_t b) { return a > b ? a : b; }
 
-template <int CW, int NKC, int BN, int STAGES, bool FOLD, int EPI_WG>
+// development trace (MASK_TC_DEBUG bit 8): %globaltimer stamps of the first CTAs
+constexpr int kTraceCtas = 4096;
+__device__ long long g_tc_trace[8][kTraceCtas];
+__device__ __forceinline__ long long gtimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Kernel configuration.
+//   CW / NKC   K columns per smem chunk of B (32 fp32 = one 128-byte swizzle row) / chunks
+//   KA         K columns of the contraction (d, or d + 2 with FOLD), multiple of 8
+//   BN         prototypes per tile (MMA N);  NACC TMEM accumulator buffers
+//   FOLD       ||x||^2 and ||c||^2 folded into the contraction (small d), packed-key epilogue
+//   EPI_WG     epilogue warpgroups (each owns BN / EPI_WG accumulator columns of every tile)
+// TMEM: [NACC x BN accumulator columns][KA columns A_big][KA columns A_small]; A lives in TMEM
+// (lane = row, column = k), so the tensor core reads only B from shared memory.
+template <int CW, int NKC, int KA, int BN, int STAGES, int NACC, bool FOLD, int EPI_WG>
+struct Cfg {
+  static constexpr int CWB = CW * 4;
+  static constexpr int B_CHUNK = BN * CWB;
+  static constexpr int STAGE_BYTES = 2 * B_CHUNK;
+  static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
+  static constexpr int NBARS = 2 * STAGES + 2 * NACC + 1;
+  static constexpr int SMEM = BAR_OFF + NBARS * 8 + 16 + 1024;  // + alignment slack
+  static constexpr int A_COL = NACC * BN;
+  static constexpr int AS_COL = A_COL + KA;
+  static constexpr int NEED = AS_COL + KA;
+  static constexpr int TMEM_COLS = NEED <= 32 ? 32 : NEED <= 64 ? 64 : NEED <= 128 ? 128 : NEED <= 256 ? 256 : 512;
+  static constexpr uint32_t IDESC = idesc_tf32<BM, BN>();
+  static constexpr int NTHREADS = 128 + 128 * EPI_WG;
+  static_assert(NEED <= 512, "TMEM budget");
+  static_assert(KA % 8 == 0 && KA <= NKC * CW, "K layout");
+  static_assert(SMEM <= 232448, "shared memory budget");
+  static_assert(3 * BM * 4 * EPI_WG <= STAGES * STAGE_BYTES, "merge scratch");
+};
+
+template <int CW, int NKC, int KA, int BN, int STAGES, int NACC, bool FOLD, int EPI_WG>
 __global__ void __launch_bounds__(128 + 128 * EPI_WG, 1)
-    k_assign_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmBb,
-                const __grid_constant__ CUtensorMap tmBs, const float* __restrict__ X,
-                const float* __restrict__ P, const float* __restrict__ cn2,
-                const float* __restrict__ xn2, int64_t n, int d, int k_cols, int64_t k,
-                int32_t* __restrict__ labels, float* __restrict__ best, int32_t* __restrict__ flag_rows,
-                int32_t* __restrict__ flag_count, float err_coef, uint32_t key_hi_mul, uint32_t key_lo_mul) {
-  using C = Cfg<CW, NKC, BN, STAGES, FOLD, EPI_WG>;
+    k_assign_tc(const __grid_constant__ CUtensorMap tmBb, const __grid_constant__ CUtensorMap tmBs,
+                const float* __restrict__ X, const float* __restrict__ P, const float* __restrict__ cn2,
+                const float* __restrict__ xn2, int64_t n, int d, int64_t k, int32_t* __restrict__ labels,
+                float* __restrict__ best, int32_t* __restrict__ flag_rows, int32_t* __restrict__ flag_count,
+                float err_coef, uint32_t key_hi_mul, uint32_t key_lo_mul, int dbg) {
+  using C = Cfg<CW, NKC, KA, BN, STAGES, NACC, FOLD, EPI_WG>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  float* A_big = reinterpret_cast<float*>(smem);
-  float* A_small = reinterpret_cast<float*>(smem + NKC * C::A_CHUNK);
-  uint8_t* Bst = smem + C::A_BYTES;
+  uint8_t* Bst = smem;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
   uint64_t* full = bars;
   uint64_t* empty = bars + STAGES;
   uint64_t* tfull = bars + 2 * STAGES;
-  uint64_t* tempty = bars + 2 * STAGES + 2;
-  uint64_t* a_full = bars + 2 * STAGES + 4;
-  uint64_t* a_ready = bars + 2 * STAGES + 5;
+  uint64_t* tempty = bars + 2 * STAGES + NACC;
+  uint64_t* a_ready = bars + 2 * STAGES + 2 * NACC;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::NBARS);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t row0 = (int64_t)blockIdx.x * BM;
   const int ntiles = (int)((k + BN - 1) / BN);
-  const int ksteps_last = ((k_cols - (NKC - 1) * CW) + 7) / 8;  // K steps of 8 in the last chunk
+  const bool trace = (dbg & 8) && blockIdx.x < kTraceCtas;
+  if (trace && threadIdx.x == 0) g_tc_trace[0][blockIdx.x] = gtimer();
 
   if (warp == 0 && lane == 0) {
-    prefetch_tmap(&tmA);
     prefetch_tmap(&tmBb);
     prefetch_tmap(&tmBs);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    for (int a = 0; a < 2; ++a) {
+    for (int a = 0; a < NACC; ++a) {
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 128 * EPI_WG);
     }
-    mbar_init(a_full, 1);
-    mbar_init(a_ready, 128 * EPI_WG);
+    mbar_init(a_ready, 128);
     fence_barrier_init();
   }
   if (warp == 2) {
@@ -252,22 +272,24 @@ __global__ void __launch_bounds__(128 + 128 * EPI_WG, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (trace && threadIdx.x == 0) g_tc_trace[1][blockIdx.x] = gtimer();
 
   if (warp == 0) {
-    // ------------------------------------------------------------ TMA producer
+    // ------------------------------------------------------------ TMA producer (B only)
     if (lane == 0) {
-      mbar_arrive_expect_tx(a_full, NKC * C::A_CHUNK);
-      for (int c = 0; c < NKC; ++c)
-        tma_load_2d(reinterpret_cast<uint8_t*>(A_big) + c * C::A_CHUNK, &tmA, a_full, c * CW, (int)row0);
       int stage = 0;
       uint32_t phase = 0;
       for (int t = 0; t < ntiles; ++t) {
         for (int c = 0; c < NKC; ++c) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* dst = Bst + stage * C::STAGE_BYTES;
-          mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
-          tma_load_2d(dst, &tmBb, &full[stage], c * CW, t * BN);
-          tma_load_2d(dst + C::B_CHUNK, &tmBs, &full[stage], c * CW, t * BN);
+          if (dbg & 4) {  // ablation: no B traffic
+            mbar_arrive(&full[stage]);
+          } else {
+            mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
+            tma_load_2d(dst, &tmBb, &full[stage], c * CW, t * BN);
+            tma_load_2d(dst + C::B_CHUNK, &tmBs, &full[stage], c * CW, t * BN);
+          }
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -276,15 +298,14 @@ __global__ void __launch_bounds__(128 + 128 * EPI_WG, 1)
       }
     }
   } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer
+    // ------------------------------------------------------------ MMA issuer (A from TMEM)
     mbar_wait(a_ready, 0);
     tc_fence_after();
     int stage = 0;
     uint32_t phase = 0;
-    const uint32_t a_big_addr = smem_u32(A_big), a_small_addr = smem_u32(A_small);
     for (int t = 0; t < ntiles; ++t) {
-      const int acc = t & 1;
-      mbar_wait(&tempty[acc], ((t >> 1) & 1) ^ 1);
+      const int acc = t % NACC;
+      mbar_wait(&tempty[acc], ((t / NACC) & 1) ^ 1);
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
       for (int c = 0; c < NKC; ++c) {
@@ -293,16 +314,15 @@ __global__ void __launch_bounds__(128 + 128 * EPI_WG, 1)
         if (lane == 0) {
           const uint32_t bb = smem_u32(Bst + stage * C::STAGE_BYTES);
           const uint32_t bs = bb + C::B_CHUNK;
-          const uint32_t ab = a_big_addr + c * C::A_CHUNK;
-          const uint32_t as = a_small_addr + c * C::A_CHUNK;
-          const int ks_n = (c == NKC - 1) ? ksteps_last : CW / 8;
+          const int ks_n = (c == NKC - 1) ? (KA - (NKC - 1) * CW) / 8 : CW / 8;
           for (int ks = 0; ks < ks_n; ++ks) {
-            const uint32_t off = ks * 32;  // 8 tf32 = 32 bytes along K inside the swizzle atom
-            const uint64_t dab = smem_desc<C::CWB>(ab + off), das = smem_desc<C::CWB>(as + off);
-            const uint64_t dbb = smem_desc<C::CWB>(bb + off), dbs = smem_desc<C::CWB>(bs + off);
-            mma_tf32(d_tmem, das, dbb, C::IDESC, (c | ks) != 0);
-            mma_tf32(d_tmem, dab, dbs, C::IDESC, 1u);
-            mma_tf32(d_tmem, dab, dbb, C::IDESC, 1u);
+            if (dbg & 2) continue;  // ablation: no MMA
+            const uint32_t kcol = (uint32_t)(c * CW + ks * 8);
+            const uint32_t ab = tmem_base + C::A_COL + kcol, as = tmem_base + C::AS_COL + kcol;
+            const uint64_t dbb = smem_desc<C::CWB>(bb + ks * 32), dbs = smem_desc<C::CWB>(bs + ks * 32);
+            mma_tf32_ts(d_tmem, as, dbb, C::IDESC, (c | ks) != 0);
+            mma_tf32_ts(d_tmem, ab, dbs, C::IDESC, 1u);
+            mma_tf32_ts(d_tmem, ab, dbb, C::IDESC, 1u);
           }
           mma_commit(&empty[stage]);
           if (c == NKC - 1) mma_commit(&tfull[acc]);
@@ -315,71 +335,81 @@ __global__ void __launch_bounds__(128 + 128 * EPI_WG, 1)
       }
     }
   } else if (warp >= kEpiWarp0) {
-    // ------------------------------------------------------------ A split + epilogue
-    // EPI_WG epilogue warpgroups; warpgroup g handles accumulator columns [g*BN/EPI_WG, ...)
-    // of every tile for the 128 rows (TMEM lane quarter = warp % 4).
     constexpr int NEPI = 128 * EPI_WG;
     constexpr int COLS = BN / EPI_WG;
-    const int et = threadIdx.x - kEpiWarp0 * 32;  // 0..NEPI-1
-    const int wg = et >> 7;                       // epilogue warpgroup
-    const int q = warp & 3;                       // TMEM lane quarter
-    const int rloc = q * 32 + lane;               // row of this thread inside the block
+    static_assert(COLS % 32 == 0, "epilogue chunking");
+    const int et = threadIdx.x - kEpiWarp0 * 32;
+    const int wg = et >> 7;
+    const int q = warp & 3;          // TMEM lane quarter
+    const int rloc = q * 32 + lane;  // row of this thread inside the block
     const int64_t row = row0 + rloc;
     const float xx = row < n ? __ldg(xn2 + row) : 0.f;
-    mbar_wait(a_full, 0);
-    {
-      const int total = NKC * BM * CW;
-      for (int e = et; e < total; e += NEPI) {
-        const float v = A_big[e];
-        const float b = tf32_rn(v);
-        A_big[e] = b;
-        A_small[e] = tf32_rn(v - b);
+    const bool tr0 = trace && et == 0;
+    // ------------------------------------------------------------ A -> TMEM (warpgroup 0)
+    if (wg == 0) {
+      const float* xr = X + row * d;
+      const uint32_t lane_base = tmem_base + ((uint32_t)(q * 32) << 16);
+#pragma unroll 1
+      for (int g = 0; g < KA; g += 8) {
+        uint32_t vb[8], vs[8];
+#pragma unroll
+        for (int u = 0; u < 8; u += 4) {
+          const int col = g + u;
+          float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (row < n && col < d) v = __ldg(reinterpret_cast<const float4*>(xr + col));
+          const float e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+          for (int w = 0; w < 4; ++w) {
+            float x = e[w];
+            if (FOLD) {
+              if (col + w == d) x = 1.0f;         // pairs with ||c||^2 in B
+              else if (col + w == d + 1) x = xx;  // pairs with 1 in B
+            }
+            const float b = tf32_rn(x);
+            vb[u + w] = __float_as_uint(b);
+            vs[u + w] = __float_as_uint(tf32_rn(x - b));
+          }
+        }
+        tmem_st8(lane_base + C::A_COL + g, vb);
+        tmem_st8(lane_base + C::AS_COL + g, vs);
       }
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(a_ready);
     }
-    if (FOLD) {
-      // augmented columns of this thread's row: A[r, d] = 1, A[r, d+1] = ||x_r||^2 (split)
-      asm volatile("bar.sync 1, %0;" ::"n"(NEPI) : "memory");
-      if (wg == 0) {
-        uint8_t* ab = reinterpret_cast<uint8_t*>(A_big);
-        uint8_t* as = reinterpret_cast<uint8_t*>(A_small);
-        const float hb = tf32_rn(xx);
-        *reinterpret_cast<float*>(ab + swz_off<C::CWB>(rloc, d)) = 1.0f;
-        *reinterpret_cast<float*>(as + swz_off<C::CWB>(rloc, d)) = 0.0f;
-        *reinterpret_cast<float*>(ab + swz_off<C::CWB>(rloc, d + 1)) = hb;
-        *reinterpret_cast<float*>(as + swz_off<C::CWB>(rloc, d + 1)) = tf32_rn(xx - hb);
-      }
-    }
-    fence_proxy_async_smem();
-    mbar_arrive(a_ready);
+    if (tr0) g_tc_trace[2][blockIdx.x] = gtimer();
 
-    // running result over all tiles (this warpgroup's columns)
+    // ------------------------------------------------------------ epilogue
     float g1 = INFINITY, g2 = INFINITY;
     int32_t gi = 0x7fffffff;
     for (int t = 0; t < ntiles; ++t) {
-      const int acc = t & 1;
-      mbar_wait(&tfull[acc], (t >> 1) & 1);
+      const int acc = t % NACC;
+      mbar_wait(&tfull[acc], (t / NACC) & 1);
       tc_fence_after();
-      const int col0 = wg * COLS;  // first column of this warpgroup inside the tile
+      if (tr0 && t == 0) g_tc_trace[3][blockIdx.x] = gtimer();
+      if (tr0 && t == ntiles - 1) g_tc_trace[4][blockIdx.x] = gtimer();
+      const int col0 = wg * COLS;
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + col0);
       float v1, v2;
       int32_t j1;
+      const bool no_ld = dbg & 16;  // ablation: no TMEM loads
+      uint32_t r[2][32];
       if (FOLD) {
-        // packed keys: (float bits with the low 8 mantissa bits replaced by the column in the
-        // tile); signed-int order = value order for values >= 0, ties -> lower column
+        // packed keys: (float bits >> 8) * 256 + column (two IMADs on the FMA pipe); signed-int
+        // order = value order for values >= 0, ties -> lower column
         int32_t b1[4], b2[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) b1[u] = b2[u] = 0x7fffffff;
-        uint32_t r[2][32];
-        tmem_ld32(tbase, r[0]);
+        if (!no_ld) tmem_ld32(tbase, r[0]);
 #pragma unroll
         for (int cc = 0; cc < COLS / 32; ++cc) {
-          tmem_wait_ld();
-          if (cc + 1 < COLS / 32) tmem_ld32(tbase + (cc + 1) * 32, r[(cc + 1) & 1]);
+          if (!no_ld) {
+            tmem_wait_ld();
+            if (cc + 1 < COLS / 32) tmem_ld32(tbase + (cc + 1) * 32, r[(cc + 1) & 1]);
+          }
+          if (dbg & 1) continue;  // ablation: no epilogue arithmetic
 #pragma unroll
           for (int i = 0; i < 32; i += 2) {
-            // key = (bits >> 8) * 256 + column, built with two integer multiply-adds on the
-            // FMA pipe (the multipliers are kernel arguments so they stay IMADs) -- the
-            // min/max work below runs on the ALU pipe, which is the epilogue's limiter.
             int32_t ka, kb;
             asm("{\n .reg .u32 h;\n mul.hi.u32 h, %1, %2;\n mad.lo.u32 %0, h, %3, %4;\n}"
                 : "=r"(ka)
@@ -412,12 +442,14 @@ __global__ void __launch_bounds__(128 + 128 * EPI_WG, 1)
           b1[u] = b2[u] = INFINITY;
           i1[u] = 0;
         }
-        uint32_t r[2][32];
-        tmem_ld32(tbase, r[0]);
+        if (!no_ld) tmem_ld32(tbase, r[0]);
 #pragma unroll
         for (int cc = 0; cc < COLS / 32; ++cc) {
-          tmem_wait_ld();
-          if (cc + 1 < COLS / 32) tmem_ld32(tbase + (cc + 1) * 32, r[(cc + 1) & 1]);
+          if (!no_ld) {
+            tmem_wait_ld();
+            if (cc + 1 < COLS / 32) tmem_ld32(tbase + (cc + 1) * 32, r[(cc + 1) & 1]);
+          }
+          if (dbg & 1) continue;
           const float4* c4 = reinterpret_cast<const float4*>(cn2 + t * BN + col0 + cc * 32);
 #pragma unroll
           for (int i = 0; i < 32; i += 4) {
@@ -435,7 +467,6 @@ __global__ void __launch_bounds__(128 + 128 * EPI_WG, 1)
         }
         tc_fence_before();
         mbar_arrive(&tempty[acc]);
-        // merge the 4 chains (lowest column on exact ties)
         v1 = b1[0];
         j1 = i1[0];
 #pragma unroll
@@ -459,30 +490,37 @@ __global__ void __launch_bounds__(128 + 128 * EPI_WG, 1)
     }
     // ---- merge the warpgroups' results for each row (lowest index on equal values)
     if (EPI_WG > 1) {
-      float* mg1 = reinterpret_cast<float*>(tmem_slot + 4);
-      float* mg2 = mg1 + BM;
-      int32_t* mgi = reinterpret_cast<int32_t*>(mg2 + BM);
-      if (wg == 1) {
-        mg1[rloc] = g1;
-        mg2[rloc] = g2;
-        mgi[rloc] = gi;
+      // scratch [EPI_WG-1][BM] x {g1, g2, gi} in the B stage ring: every MMA (and so every
+      // TMA write) has completed once the last tile's accumulator was signalled full
+      float* mg1 = reinterpret_cast<float*>(Bst);
+      float* mg2 = mg1 + (EPI_WG - 1) * BM;
+      int32_t* mgi = reinterpret_cast<int32_t*>(mg2 + (EPI_WG - 1) * BM);
+      if (wg > 0) {
+        mg1[(wg - 1) * BM + rloc] = g1;
+        mg2[(wg - 1) * BM + rloc] = g2;
+        mgi[(wg - 1) * BM + rloc] = gi;
       }
       asm volatile("bar.sync 1, %0;" ::"n"(NEPI) : "memory");
       if (wg == 0) {
-        const float o1 = mg1[rloc], o2 = mg2[rloc];
-        const int32_t oi = mgi[rloc];
-        if (o1 < g1 || (o1 == g1 && oi < gi)) {
-          g2 = fminf(g1, o2);
-          g1 = o1;
-          gi = oi;
-        } else {
-          g2 = fminf(g2, o1);
+#pragma unroll
+        for (int w = 0; w < EPI_WG - 1; ++w) {
+          const float o1 = mg1[w * BM + rloc], o2 = mg2[w * BM + rloc];
+          const int32_t oi = mgi[w * BM + rloc];
+          if (o1 < g1 || (o1 == g1 && oi < gi)) {
+            g2 = fminf(g1, o2);
+            g1 = o1;
+            gi = oi;
+          } else {
+            g2 = fminf(g2, o1);
+          }
         }
       }
     }
+    if (tr0) g_tc_trace[5][blockIdx.x] = gtimer();
     if (wg == 0) {
       bool flag = false;
       if (row < n) {
+        if (dbg) gi = gi < 0 ? 0 : (gi >= k ? (int32_t)(k - 1) : gi);  // ablation runs: keep in range
         labels[row] = gi;
         // exact FP32 squared distance of the chosen prototype (direct form, for J and d2_out)
         const float* xr = X + row * d;
@@ -514,13 +552,41 @@ __global__ void __launch_bounds__(128 + 128 * EPI_WG, 1)
         if (flag) flag_rows[base + __popc(m & ((1u << lane) - 1))] = (int32_t)row;
       }
     }
+    if (tr0) g_tc_trace[6][blockIdx.x] = gtimer();
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   if (warp == 2) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(C::TMEM_COLS));
+    if (trace && lane == 0) g_tc_trace[7][blockIdx.x] = gtimer();
   }
+}
+
+// Host dump of the development trace: per-phase medians (us) over the traced CTAs.
+void dump_trace(int nctas) {
+  static long long h[8][kTraceCtas];
+  if (cudaDeviceSynchronize() != cudaSuccess) return;
+  if (cudaMemcpyFromSymbol(h, g_tc_trace, sizeof(h)) != cudaSuccess) return;
+  const int m = nctas < kTraceCtas ? nctas : kTraceCtas;
+  long long t0 = h[0][0], tend = 0;
+  for (int i = 0; i < m; ++i) {
+    t0 = h[0][i] < t0 ? h[0][i] : t0;
+    tend = h[7][i] > tend ? h[7][i] : tend;
+  }
+  const char* names[7] = {"setup", "A_to_tmem", "wait_first_tile", "tiles(all but last)", "last_tile+merge",
+                          "outputs", "teardown"};
+  fprintf(stderr, "[tc trace] %d CTAs span %.1f us; per-CTA phase medians (us):", m, (tend - t0) / 1e3);
+  for (int p = 0; p < 7; ++p) {
+    std::vector<long long> v;
+    for (int i = 0; i < m; ++i) v.push_back(h[p + 1][i] - h[p][i]);
+    std::sort(v.begin(), v.end());
+    fprintf(stderr, " %s=%.2f", names[p], v[v.size() / 2] / 1e3);
+  }
+  std::vector<long long> tot;
+  for (int i = 0; i < m; ++i) tot.push_back(h[7][i] - h[0][i]);
+  std::sort(tot.begin(), tot.end());
+  fprintf(stderr, " total=%.2f\n", tot[tot.size() / 2] / 1e3);
 }
 
 // ------------------------------------------------------------------ host side
@@ -555,25 +621,38 @@ CUtensorMap make_map(const float* base, int64_t rows, int cols, int box_cols, in
   return m;
 }
 
-template <int CW, int NKC, int BN, int STAGES, bool FOLD, int EPI_WG>
-void launch_cfg(const float* X, int64_t n, int d, int kc, const float* P, const float* Pb, const float* Ps,
-                const float* cn2, int64_t k, const float* xn2, int32_t* labels, float* best, int32_t* flag_rows,
-                int32_t* flag_count, float err_coef, cudaStream_t st) {
-  using C = Cfg<CW, NKC, BN, STAGES, FOLD, EPI_WG>;
-  static_assert(C::SMEM <= 232448, "shared memory budget");
-  const CUtensorMap tA = make_map(X, n, d, CW, BM);
-  const CUtensorMap tBb = make_map(Pb, k, kc, CW, BN);
-  const CUtensorMap tBs = make_map(Ps, k, kc, CW, BN);
-  auto kern = k_assign_tc<CW, NKC, BN, STAGES, FOLD, EPI_WG>;
+#ifndef MASK_TC_EPI_WG
+#define MASK_TC_EPI_WG 4
+#endif
+
+// development ablations (MASK_TC_DEBUG bits: 1 = no epilogue math, 2 = no MMA, 4 = no B loads,
+// 8 = phase trace, 16 = no TMEM loads)
+inline int tc_debug_mode() {
+  static int mode = [] {
+    const char* e = getenv("MASK_TC_DEBUG");
+    return e ? atoi(e) : 0;
+  }();
+  return mode;
+}
+
+template <int CW, int NKC, int KA, int BN, int STAGES, int NACC, bool FOLD, int EPI_WG>
+void launch_cfg(const float* X, int64_t n, int d, int kc, int64_t k_rows, const float* P, const float* Pb,
+                const float* Ps, const float* cn2, int64_t k, const float* xn2, int32_t* labels, float* best,
+                int32_t* flag_rows, int32_t* flag_count, float err_coef, cudaStream_t st) {
+  using C = Cfg<CW, NKC, KA, BN, STAGES, NACC, FOLD, EPI_WG>;
+  const CUtensorMap tBb = make_map(Pb, k_rows, kc, CW, BN);
+  const CUtensorMap tBs = make_map(Ps, k_rows, kc, CW, BN);
+  auto kern = k_assign_tc<CW, NKC, KA, BN, STAGES, NACC, FOLD, EPI_WG>;
   static bool attr_set = false;
   if (!attr_set) {
     MASK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     attr_set = true;
   }
   const unsigned grid = (unsigned)((n + BM - 1) / BM);
-  kern<<<grid, 128 + 128 * EPI_WG, C::SMEM, st>>>(tA, tBb, tBs, X, P, cn2, xn2, n, d, kc, k, labels, best,
-                                                  flag_rows, flag_count, err_coef, 1u << 24, 256u);
+  kern<<<grid, C::NTHREADS, C::SMEM, st>>>(tBb, tBs, X, P, cn2, xn2, n, d, k, labels, best, flag_rows, flag_count,
+                                           err_coef, 1u << 24, 256u, tc_debug_mode());
   MASK_LAUNCH_CHECK();
+  if (tc_debug_mode() & 8) dump_trace((int)grid);
 }
 
 }  // namespace tc
@@ -586,7 +665,11 @@ bool tc_supported(int64_t n, int d, int64_t k) {
   return n >= 1 && d >= 4 && d <= 128 && d % 4 == 0;
 }
 
-int tc_operand_cols(int d) { return d + 2 <= 32 ? ((d + 2 + 3) / 4) * 4 : d; }
+// B operand columns: d + 2 (||c||^2, 1) rounded up to 8 when folded (small d), else d rounded
+// up to 8 (zero columns beyond d)
+int tc_operand_cols(int d) { return d + 2 <= 32 ? ((d + 2 + 7) / 8) * 8 : ((d + 7) / 8) * 8; }
+// rows of the B operand arrays: padded to whole 256-prototype tiles (pad rows never win)
+int64_t tc_operand_rows(int64_t k) { return (k + 255) / 256 * 256 + 256; }
 
 // Worst-case error coefficient of the 3xTF32 score, doubled for a gap of two scores:
 // representation (<= 2^-20 |x||c| summed over the three products and the dropped xs.cs)
@@ -603,18 +686,24 @@ void launch_assign_tc(const float* X, int64_t n, int d, const float* P, const fl
                       int32_t* flag_rows, int32_t* flag_count, cudaStream_t st) {
   const float coef = tc_err_coef(d);
   const int kc = tc_operand_cols(d);
-  if (d + 2 <= 32)
-    tc::launch_cfg<32, 1, 256, 3, true, 2>(X, n, d, kc, P, Pb, Ps, cn2, k, xn2, labels, best, flag_rows, flag_count,
-                                           coef, st);
-  else if (d <= 32)
-    tc::launch_cfg<32, 1, 256, 3, false, 2>(X, n, d, kc, P, Pb, Ps, cn2, k, xn2, labels, best, flag_rows,
-                                            flag_count, coef, st);
+  const int64_t kr = tc_operand_rows(k);
+  // small d (FOLD): epilogue-bound; 192-prototype tiles, two TMEM accumulators (2 x 192 + 2 x
+  // KA columns), three epilogue warpgroups of 64 columns (best of the measured variants)
+  if (d + 2 <= 24)
+    tc::launch_cfg<32, 1, 24, 192, 4, 2, true, 3>(X, n, d, kc, kr, P, Pb, Ps, cn2, k, xn2, labels, best, flag_rows,
+                                                  flag_count, coef, st);
+  else if (d + 2 <= 32)
+    tc::launch_cfg<32, 1, 32, 192, 4, 2, true, 3>(X, n, d, kc, kr, P, Pb, Ps, cn2, k, xn2, labels, best, flag_rows,
+                                                  flag_count, coef, st);
   else if (d <= 64)
-    tc::launch_cfg<32, 2, 128, 4, false, 1>(X, n, d, kc, P, Pb, Ps, cn2, k, xn2, labels, best, flag_rows,
-                                            flag_count, coef, st);
+    tc::launch_cfg<32, 2, 64, 128, 6, 3, false, 2>(X, n, d, kc, kr, P, Pb, Ps, cn2, k, xn2, labels, best, flag_rows,
+                                                   flag_count, coef, st);
+  else if (d <= 96)
+    tc::launch_cfg<32, 3, 96, 128, 6, 2, false, 2>(X, n, d, kc, kr, P, Pb, Ps, cn2, k, xn2, labels, best, flag_rows,
+                                                   flag_count, coef, st);
   else
-    tc::launch_cfg<32, 4, 128, 3, false, 1>(X, n, d, kc, P, Pb, Ps, cn2, k, xn2, labels, best, flag_rows,
-                                            flag_count, coef, st);
+    tc::launch_cfg<32, 4, 128, 128, 6, 2, false, 2>(X, n, d, kc, kr, P, Pb, Ps, cn2, k, xn2, labels, best,
+                                                    flag_rows, flag_count, coef, st);
 }
 
 }  // namespace mask

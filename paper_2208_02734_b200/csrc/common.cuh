@@ -118,7 +118,9 @@ void launch_fixup_tiled(const float* X, int d, const float* P, int64_t k, const 
 // prototype operands for K1: Pb = tf32_rn(-2c), Ps = tf32_rn(-2c - Pb), cn2 = ||c||^2; with
 // kc > d the augmented columns [d] = split(||c||^2), [d+1] = (1, 0), rest 0 (row stride kc)
 void launch_prep_protos(const float* P, int64_t k, int d, int kc, float* Pb, float* Ps, float* cn2,
-                        cudaStream_t st);
+                        cudaStream_t st, int64_t k_rows, int fold);
+// rows of the K1 B operand arrays (k padded to whole 256-prototype tiles)
+int64_t tc_operand_rows(int64_t k);
 void launch_row_norms(const float* X, int64_t n, int d, float* xn2, cudaStream_t st);
 
 // K3: CSR rows x dense prototypes (sparse assignment).

@@ -299,8 +299,8 @@ __device__ __forceinline__ float tf32_rn(float x) {
 
 // One warp per prototype: Pb = tf32(-2c), Ps = tf32(-2c - Pb) (3xTF32 split of the B operand,
 // the factor -2 is exact), cn2 = ||c||^2 accumulated in FP64 then rounded.
-__global__ void k_prep_protos(const float* __restrict__ P, int64_t k, int d, int kc, float* __restrict__ Pb,
-                              float* __restrict__ Ps, float* __restrict__ cn2) {
+__global__ void k_prep_protos(const float* __restrict__ P, int64_t k, int64_t k_rows, int d, int kc, int fold,
+                              float* __restrict__ Pb, float* __restrict__ Ps, float* __restrict__ cn2) {
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t j = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); j < k; j += warps) {
@@ -318,25 +318,37 @@ __global__ void k_prep_protos(const float* __restrict__ P, int64_t k, int d, int
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     if (lane == 0 && cn2) cn2[j] = (float)s;
     if (Pb && kc > d) {
-      // augmented columns: [d] = ||c||^2 split (A side holds 1), [d+1] = 1 (A side ||x||^2)
+      // columns beyond d: with `fold` [d] = ||c||^2 split (A side holds 1), [d+1] = 1 (A side
+      // ||x||^2); otherwise zeros
       const float hb = tf32_rn((float)s);
       const float hs = tf32_rn((float)(s - (double)hb));
       for (int i = d + lane; i < kc; i += 32) {
-        Pb[j * kc + i] = i == d ? hb : (i == d + 1 ? 1.0f : 0.f);
-        Ps[j * kc + i] = i == d ? hs : 0.f;
+        Pb[j * kc + i] = !fold ? 0.f : (i == d ? hb : (i == d + 1 ? 1.0f : 0.f));
+        Ps[j * kc + i] = (fold && i == d) ? hs : 0.f;
       }
+    }
+  }
+  // pad rows [k, k_rows): never the nearest (folded: a huge ||c||^2; else ||c||^2 = +inf in cn2)
+  if (Pb) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < (k_rows - k) * kc;
+         e += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t j = k + e / kc;
+      const int i = (int)(e % kc);
+      Pb[j * kc + i] = (fold && i == d) ? 1e30f : 0.f;
+      Ps[j * kc + i] = 0.f;
     }
   }
 }
 
 void launch_prep_protos(const float* P, int64_t k, int d, int kc, float* Pb, float* Ps, float* cn2,
-                        cudaStream_t st) {
-  k_prep_protos<<<grid_for(k * 32, 256), 256, 0, st>>>(P, k, d, kc, Pb, Ps, cn2);
+                        cudaStream_t st, int64_t k_rows, int fold) {
+  if (k_rows < k) k_rows = k;
+  k_prep_protos<<<grid_for(k * 32, 256), 256, 0, st>>>(P, k, k_rows, d, kc, fold, Pb, Ps, cn2);
   MASK_LAUNCH_CHECK();
 }
 
 void launch_level_norms(const float* P, int64_t k, int d, float* cn2, cudaStream_t st) {
-  launch_prep_protos(P, k, d, d, nullptr, nullptr, cn2, st);
+  launch_prep_protos(P, k, d, d, nullptr, nullptr, cn2, st, k, 0);
 }
 
 __global__ void k_row_norms(const float* __restrict__ X, int64_t n, int d, float* __restrict__ xn2) {

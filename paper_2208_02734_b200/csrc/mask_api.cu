@@ -267,8 +267,8 @@ int64_t assign_pass(const Input& in, const float* P, int64_t k, int flags, int32
   const int64_t k_pad = (k + 255) / 256 * 256;
   const int kc = tc_operand_cols(d);
   if (!ws.Pb.p) {
-    ws.Pb.alloc((size_t)k * kc);
-    ws.Ps.alloc((size_t)k * kc);
+    ws.Pb.alloc((size_t)tc_operand_rows(k) * kc);
+    ws.Ps.alloc((size_t)tc_operand_rows(k) * kc);
     ws.cn2.alloc(k_pad);
     ws.flag_rows.alloc(n);
     ws.flag_count.alloc(1);
@@ -279,7 +279,7 @@ int64_t assign_pass(const Input& in, const float* P, int64_t k, int flags, int32
     launch_row_norms(in.X, n, d, ws.xn2.p, st);
     ws.xn2_ready = true;
   }
-  launch_prep_protos(P, k, d, kc, ws.Pb.p, ws.Ps.p, ws.cn2.p, st);
+  launch_prep_protos(P, k, d, kc, ws.Pb.p, ws.Ps.p, ws.cn2.p, st, tc_operand_rows(k), d + 2 <= 32 ? 1 : 0);
   MASK_CUDA(cudaMemsetAsync(ws.flag_count.p, 0, sizeof(int32_t), st));
   ws.kernel_id = 1;
   if (tm) tm->t[MASK_T_ASSIGN].start(st);
