@@ -43,7 +43,14 @@ void count_launch();
     if (!(cond)) ::mask::fail((code), std::string(msg)); \
   } while (0)
 
-// Owning device buffer (cudaMalloc/cudaFree).
+// Process-wide caching device allocator (mask_api.cu): blocks are rounded up to a size class
+// and recycled instead of cudaFree'd, so builds and queries do not synchronise the device on
+// allocation.  pool_trim() returns the cached blocks to the driver.
+void* pool_alloc(size_t bytes);
+void pool_free(void* p, size_t bytes);
+void pool_trim();
+
+// Owning device buffer (pool-backed).
 template <class T>
 struct DevBuf {
   T* p = nullptr;
@@ -61,10 +68,10 @@ struct DevBuf {
   void alloc(size_t count) {
     release();
     n = count;
-    if (count) MASK_CUDA(cudaMalloc(&p, count * sizeof(T)));
+    if (count) p = static_cast<T*>(pool_alloc(count * sizeof(T)));
   }
   void release() {
-    if (p) cudaFree(p);
+    if (p) pool_free(p, n * sizeof(T));
     p = nullptr;
     n = 0;
   }
@@ -111,6 +118,10 @@ void launch_assign_tc(const float* X, int64_t n, int d, const float* P, const fl
 void launch_fixup(const float* X, int d, const float* P, int64_t k, const int32_t* flag_rows,
                   const int32_t* flag_count, int64_t max_flags, int32_t* labels, float* best,
                   cudaStream_t st);
+// K4 (tiled, device-sized): the first min(*flag_count, cap) flagged rows; keys_ws = cap u64
+void launch_fixup_device(const float* X, int d, const float* P, int64_t k, const int32_t* flag_rows,
+                         const int32_t* flag_count, int64_t cap, unsigned long long* keys_ws, int32_t* labels,
+                         float* best, cudaStream_t st);
 // K4 (tiled): nf flagged rows (host-known count) against all prototypes; keys_ws = nf u64
 void launch_fixup_tiled(const float* X, int d, const float* P, int64_t k, const int32_t* flag_rows,
                         int64_t nf, unsigned long long* keys_ws, int32_t* labels, float* best,

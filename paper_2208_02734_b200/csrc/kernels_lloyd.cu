@@ -255,6 +255,128 @@ __global__ void __launch_bounds__(256) k_fixup_tiled(const float* __restrict__ X
   }
 }
 
+// Device-sized variant: the flagged count is read on the device (no host round trip); block
+// b walks work items (row block, prototype split) b, b + gridDim.x, ...  At most `cap` rows.
+__global__ void __launch_bounds__(256) k_fixup_dev(const float* __restrict__ X, int d,
+                                                   const float* __restrict__ P, int64_t k,
+                                                   const int32_t* __restrict__ flag_rows,
+                                                   const int32_t* __restrict__ flag_count, int64_t cap,
+                                                   int nsm, unsigned long long* __restrict__ keys) {
+  extern __shared__ float fsm[];
+  const int64_t nf = min64(*flag_count, cap);
+  if (nf <= 0) return;
+  const int dp = d + 1;
+  float* xs = fsm;
+  float* cs = fsm + FX_R * dp;
+  const int t = threadIdx.x;
+  const int rg = t & 7, pg = t >> 3;
+  const int64_t row_blocks = (nf + FX_R - 1) / FX_R;
+  const int64_t ntile = (k + FX_P - 1) / FX_P;
+  int64_t splits = (4LL * nsm + row_blocks - 1) / row_blocks;
+  splits = splits < 1 ? 1 : (splits > ntile ? ntile : splits);
+  const int64_t tps = (ntile + splits - 1) / splits;
+  splits = (ntile + tps - 1) / tps;
+  for (int64_t w = blockIdx.x; w < row_blocks * splits; w += gridDim.x) {
+    const int64_t f0 = (w / splits) * FX_R;
+    const int64_t t0 = (w % splits) * tps;
+    const int64_t t1 = min64(ntile, t0 + tps);
+    __syncthreads();
+    for (int e = t; e < FX_R * d; e += 256) {
+      const int r = e / d, c = e - r * d;
+      xs[r * dp + c] = (f0 + r < nf) ? X[(int64_t)flag_rows[f0 + r] * d + c] : 0.f;
+    }
+    float bv[4];
+    int64_t bj[4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      bv[a] = INFINITY;
+      bj[a] = INT64_MAX;
+    }
+    for (int64_t tile = t0; tile < t1; ++tile) {
+      const int64_t j0 = tile * FX_P;
+      __syncthreads();
+      for (int e = t; e < FX_P * d; e += 256) {
+        const int p = e / d, c = e - p * d;
+        cs[p * dp + c] = (j0 + p < k) ? P[(j0 + p) * d + c] : 0.f;
+      }
+      __syncthreads();
+      float acc[4][4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = 0.f;
+      for (int i = 0; i < d; ++i) {
+        float xv[4], cv[4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) xv[a] = xs[(rg * 4 + a) * dp + i];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) cv[b] = cs[(pg * 4 + b) * dp + i];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) {
+            const float df = xv[a] - cv[b];
+            acc[a][b] = fmaf(df, df, acc[a][b]);
+          }
+      }
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const int64_t j = j0 + pg * 4 + b;
+        if (j < k) {
+#pragma unroll
+          for (int a = 0; a < 4; ++a)
+            if (acc[a][b] < bv[a]) {
+              bv[a] = acc[a][b];
+              bj[a] = j;
+            }
+        }
+      }
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      const int64_t f = f0 + rg * 4 + a;
+      if (f < nf && bj[a] != INT64_MAX) {
+        const unsigned long long key =
+            ((unsigned long long)__float_as_uint(fmaxf(bv[a], 0.f)) << 32) | (unsigned long long)(uint32_t)bj[a];
+        atomicMin(keys + f, key);
+      }
+    }
+  }
+}
+
+__global__ void k_fixup_init(const int32_t* __restrict__ flag_count, int64_t cap, unsigned long long* keys) {
+  const int64_t nf = min64(*flag_count, cap);
+  for (int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; f < nf; f += (int64_t)gridDim.x * blockDim.x)
+    keys[f] = ~0ull;
+}
+
+__global__ void k_fixup_write_dev(const int32_t* __restrict__ flag_rows, const int32_t* __restrict__ flag_count,
+                                  int64_t cap, const unsigned long long* __restrict__ keys,
+                                  int32_t* __restrict__ labels, float* __restrict__ best) {
+  const int64_t nf = min64(*flag_count, cap);
+  for (int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; f < nf; f += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long key = keys[f];
+    const int32_t row = flag_rows[f];
+    labels[row] = (int32_t)(key & 0xffffffffu);
+    best[row] = __uint_as_float((uint32_t)(key >> 32));
+  }
+}
+
+void launch_fixup_device(const float* X, int d, const float* P, int64_t k, const int32_t* flag_rows,
+                         const int32_t* flag_count, int64_t cap, unsigned long long* keys_ws, int32_t* labels,
+                         float* best, cudaStream_t st) {
+  const size_t smem = (size_t)(FX_R + FX_P) * (d + 1) * sizeof(float);
+  MASK_REQUIRE(smem <= 200 * 1024, MASK_ERR_UNSUPPORTED, "fix-up: dim too large");
+  if (smem > 48 * 1024)
+    MASK_CUDA(cudaFuncSetAttribute(k_fixup_dev, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k_fixup_init<<<num_sms() * 2, 256, 0, st>>>(flag_count, cap, keys_ws);
+  MASK_LAUNCH_CHECK();
+  k_fixup_dev<<<num_sms() * 4, 256, smem, st>>>(X, d, P, k, flag_rows, flag_count, cap, num_sms(), keys_ws);
+  MASK_LAUNCH_CHECK();
+  k_fixup_write_dev<<<num_sms() * 2, 256, 0, st>>>(flag_rows, flag_count, cap, keys_ws, labels, best);
+  MASK_LAUNCH_CHECK();
+}
+
 __global__ void k_fixup_write(const int32_t* __restrict__ flag_rows, int64_t nf,
                               const unsigned long long* __restrict__ keys, int32_t* __restrict__ labels,
                               float* __restrict__ best) {

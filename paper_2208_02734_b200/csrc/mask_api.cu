@@ -17,6 +17,8 @@
 #include "common.cuh"
 
 #include <atomic>
+#include <map>
+#include <mutex>
 
 using namespace mask;
 
@@ -25,6 +27,54 @@ std::atomic<int64_t> g_launches{0};
 }
 
 void mask::count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+// ------------------------------------------------------------------ caching device allocator
+namespace {
+std::mutex g_pool_mu;
+std::multimap<size_t, void*> g_pool;  // size class -> free block
+size_t size_class(size_t bytes) {
+  if (bytes <= (1u << 20)) {  // small: next power of two >= 512 B
+    size_t c = 512;
+    while (c < bytes) c <<= 1;
+    return c;
+  }
+  return (bytes + (1u << 20) - 1) & ~size_t((1u << 20) - 1);  // large: whole MiB
+}
+}  // namespace
+
+void* mask::pool_alloc(size_t bytes) {
+  const size_t c = size_class(bytes);
+  {
+    std::lock_guard<std::mutex> g(g_pool_mu);
+    auto it = g_pool.find(c);
+    if (it != g_pool.end()) {
+      void* p = it->second;
+      g_pool.erase(it);
+      return p;
+    }
+  }
+  void* p = nullptr;
+  cudaError_t e = cudaMalloc(&p, c);
+  if (e == cudaErrorMemoryAllocation) {  // give the cache back and retry once
+    cudaGetLastError();
+    pool_trim();
+    e = cudaMalloc(&p, c);
+  }
+  MASK_CUDA(e);
+  return p;
+}
+
+void mask::pool_free(void* p, size_t bytes) {
+  if (!p) return;
+  std::lock_guard<std::mutex> g(g_pool_mu);
+  g_pool.emplace(size_class(bytes), p);
+}
+
+void mask::pool_trim() {
+  std::lock_guard<std::mutex> g(g_pool_mu);
+  for (auto& kv : g_pool) cudaFree(kv.second);
+  g_pool.clear();
+}
 
 namespace {
 
@@ -96,22 +146,20 @@ int32_t guarded(F&& f) {
       ::mask::fail(MASK_ERR_NCCL, std::string(#x) + ": " + ncclGetErrorString(r_));      \
   } while (0)
 
-// Pinned host scratch for per-pass statistics.
+// Pinned host scratch for per-pass statistics (one 64-byte block per thread, kept for the
+// life of the thread so builds do not pay a pinned allocation).
 struct HostStats {
   double* J = nullptr;
   unsigned long long* changed = nullptr;
   uint32_t* fin = nullptr;
   int32_t* flags = nullptr;
-  void* base = nullptr;
   HostStats() {
-    MASK_CUDA(cudaMallocHost(&base, 64));
+    thread_local void* base = nullptr;
+    if (!base) MASK_CUDA(cudaMallocHost(&base, 64));
     J = reinterpret_cast<double*>(base);
     changed = reinterpret_cast<unsigned long long*>(static_cast<char*>(base) + 8);
     fin = reinterpret_cast<uint32_t*>(static_cast<char*>(base) + 16);
     flags = reinterpret_cast<int32_t*>(static_cast<char*>(base) + 24);
-  }
-  ~HostStats() {
-    if (base) cudaFreeHost(base);
   }
 };
 
@@ -286,21 +334,16 @@ int64_t assign_pass(const Input& in, const float* P, int64_t k, int flags, int32
   launch_assign_tc(in.X, n, d, P, ws.Pb.p, ws.Ps.p, ws.cn2.p, k, ws.xn2.p, labels_out, best,
                    ws.flag_rows.p, ws.flag_count.p, st);
   if (tm) tm->t[MASK_T_ASSIGN].stop(st);
-  // near-tie re-check (K4): the flagged-row count sizes the tiled grid (one small D2H read)
-  MASK_CUDA(cudaMemcpyAsync(hs->flags, ws.flag_count.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-  MASK_CUDA(cudaStreamSynchronize(st));
-  const int64_t nf = *hs->flags;
-  if (!(flags & MASK_NO_FIXUP) && nf > 0) {
-    if ((int64_t)ws.fix_keys.n < nf) ws.fix_keys.alloc((size_t)nf + nf / 4 + 1024);
+  // near-tie re-check (K4), sized on the device from the flagged count (no host round trip);
+  // the count itself is read back with the pass statistics
+  if (!(flags & MASK_NO_FIXUP)) {
+    if ((int64_t)ws.fix_keys.n < n) ws.fix_keys.alloc((size_t)n);
     if (tm) tm->t[MASK_T_FIXUP].start(st);
-    launch_fixup_tiled(in.X, d, P, k, ws.flag_rows.p, nf, ws.fix_keys.p, labels_out, best, st);
+    launch_fixup_device(in.X, d, P, k, ws.flag_rows.p, ws.flag_count.p, n, ws.fix_keys.p, labels_out, best, st);
     if (tm) tm->t[MASK_T_FIXUP].stop(st);
   }
-  ws.last_flagged = nf;
-  if (hs) {
-    return nf;
-  }
-  return -1;
+  if (hs) MASK_CUDA(cudaMemcpyAsync(hs->flags, ws.flag_count.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  return -1;  // flagged count available in hs->flags after the next stream synchronisation
 }
 
 // Lloyd k-means for one level (SURVEY §8(c) pseudo-code; mirrors the oracle's order):
@@ -849,9 +892,10 @@ int32_t mask_assign(const mask_matrix* data, const float* P, int64_t k, int32_t 
       best = best_tmp.p;
     }
     HostStats hs;
-    const int64_t nf = assign_pass(in, P, k, flags, labels_out, best, ws, st, &hs);
-    if (n_flagged) *n_flagged = nf;
+    *hs.flags = 0;
+    assign_pass(in, P, k, flags, labels_out, best, ws, st, &hs);
     MASK_CUDA(cudaStreamSynchronize(st));
+    if (n_flagged) *n_flagged = *hs.flags;
   });
 }
 
