@@ -40,6 +40,11 @@
 
 #include "common.cuh"
 
+// independent top-2 chains per thread in the packed-key epilogue (ILP)
+#ifndef MASK_TC_CHAINS
+#define MASK_TC_CHAINS 4
+#endif
+
 namespace mask {
 
 namespace tc {
@@ -397,9 +402,10 @@ __global__ void __launch_bounds__(128 + 128 * EPI_WG, 1)
       if (FOLD) {
         // packed keys: (float bits >> 8) * 256 + column (two IMADs on the FMA pipe); signed-int
         // order = value order for values >= 0, ties -> lower column
-        int32_t b1[4], b2[4];
+        constexpr int NCH = MASK_TC_CHAINS;
+        int32_t b1[NCH], b2[NCH];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) b1[u] = b2[u] = 0x7fffffff;
+        for (int u = 0; u < NCH; ++u) b1[u] = b2[u] = 0x7fffffff;
         if (!no_ld) tmem_ld32(tbase, r[0]);
 #pragma unroll
         for (int cc = 0; cc < COLS / 32; ++cc) {
@@ -418,7 +424,7 @@ __global__ void __launch_bounds__(128 + 128 * EPI_WG, 1)
                 : "=r"(kb)
                 : "r"(r[cc & 1][i + 1]), "r"(key_hi_mul), "r"(key_lo_mul), "r"((uint32_t)(cc * 32 + i + 1)));
             // top-2 of {b1 <= b2} u {ka, kb}: b1' = min(b1, m), b2' = min(b2, M, max(b1, m))
-            const int u = (i >> 1) & 3;
+            const int u = (i >> 1) & (NCH - 1);
             const int32_t m = imin(ka, kb), M = imax(ka, kb);
             const int32_t t2 = imax(b1[u], m);
             b1[u] = imin(b1[u], m);
@@ -427,10 +433,12 @@ __global__ void __launch_bounds__(128 + 128 * EPI_WG, 1)
         }
         tc_fence_before();
         mbar_arrive(&tempty[acc]);
-        const int32_t k1 = imin(imin(b1[0], b1[1]), imin(b1[2], b1[3]));
+        int32_t k1 = b1[0];
+#pragma unroll
+        for (int u = 1; u < NCH; ++u) k1 = imin(k1, b1[u]);
         int32_t k2 = 0x7fffffff;
 #pragma unroll
-        for (int u = 0; u < 4; ++u) k2 = imin(k2, b1[u] == k1 ? b2[u] : b1[u]);
+        for (int u = 0; u < NCH; ++u) k2 = imin(k2, b1[u] == k1 ? b2[u] : b1[u]);
         v1 = __int_as_float(k1 & 0xFFFFFF00);
         v2 = __int_as_float(k2 & 0xFFFFFF00);
         j1 = col0 + (k1 & 0xFF);

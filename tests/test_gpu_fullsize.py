@@ -87,3 +87,55 @@ def test_C2_full_size_bench_configuration():
 
 def test_C3_full_size():
     _full_config(3, sample_rows=4096, checked=[0, 10, 20], n_queries=500)
+
+
+def test_C4_full_size_sparse():
+    """C4 at full size (1e6 CSR rows, d = 10,000, ~0.5 % non-zeros, k = 8192/256): step-mode
+    parity of sampled rows at checked passes, FP64 update checks, child lists, queries."""
+    cfg = datagen.CONFIGS[4]
+    rp, col, val = datagen.data(cfg)
+    inits = datagen.all_init_indices(cfg)
+    rng = np.random.default_rng(4)
+    rows = np.sort(rng.choice(cfg.n, 1024, replace=False))
+    seen = {}
+
+    def cb(level, p, P, labels):
+        if level == 1 and p in (0, 1, 7):
+            seen[p] = (P, labels)
+        elif level == 1:
+            seen[p] = (None, None)
+
+    dev = "cuda:0"
+    csr = mk.Csr(torch.from_numpy(rp).to(dev), torch.from_numpy(col).to(dev), torch.from_numpy(val).to(dev), cfg.dim)
+    T = 8
+    idx = mk.build(csr, cfg.levels, T, inits, flags=mk.MASK_BORROW_DATA, iter_cb=cb)
+    for p in (0, 1, 7):
+        if p not in seen or seen[p][0] is None:
+            continue
+        P, lab = seen[p]
+        sub_rp = np.concatenate([[0], np.cumsum(rp[rows + 1] - rp[rows])])
+        sub_col = np.concatenate([col[rp[r]:rp[r + 1]] for r in rows])
+        sub_val = np.concatenate([val[rp[r]:rp[r + 1]] for r in rows])
+        dense = np.zeros((len(rows), cfg.dim))
+        for i in range(len(rows)):
+            dense[i, sub_col[sub_rp[i]:sub_rp[i + 1]]] = sub_val[sub_rp[i]:sub_rp[i + 1]]
+        check_assignment(dense, P, lab[rows], what=f"C4 level 1 pass {p}")
+        if p == 0 and 1 in seen and seen[1][0] is not None:
+            S, cnt = oracle.cluster_sums_csr((rp, col, val), cfg.dim, lab, cfg.levels[0])
+            P_ref, _ = oracle.means_from_sums(S, cnt, P.astype(np.float64))
+            check_prototypes(seen[1][0], P_ref, what="C4 level 1 update after pass 0")
+    off, mem = idx.children(1)
+    o_ref, m_ref = oracle.children(idx.labels(1), cfg.levels[0])
+    np.testing.assert_array_equal(off, o_ref)
+    qrp, qcol, qval = datagen.queries(cfg, count=200)
+    ids, d2 = idx.query(mk.Csr(torch.from_numpy(qrp).to(dev), torch.from_numpy(qcol).to(dev),
+                               torch.from_numpy(qval).to(dev), cfg.dim), knn=cfg.knn)
+    L = len(cfg.levels)
+    P = [idx.prototypes(l).astype(np.float64) for l in range(1, L + 1)]
+    ch = [idx.children(l) for l in range(1, L + 1)]
+    rids, rd2, gap = oracle.query(P, [c[0] for c in ch], [c[1] for c in ch], (rp, col, val), (qrp, qcol, qval),
+                                  cfg.knn, 1, dim=cfg.dim, x_csr=True, q_csr=True)
+    check_queries(ids.cpu().numpy(), d2.cpu().numpy(), rids, rd2, gap, what="C4 queries")
+    tm = idx.timing(1)
+    print("C4 level-1 timing", tm)
+    idx.free()
