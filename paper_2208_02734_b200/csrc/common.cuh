@@ -100,6 +100,10 @@ inline int num_sms() {
 // (defined in the .cu files; all enqueue on `st` and never synchronise)
 
 // K2: FP32 SIMT assignment, direct (x - c)^2 sums; labels + squared distance of the winner.
+// K2b: blocked SIMT assignment for large d (dimension streamed through shared memory);
+// keys_ws = n u64 scratch
+void launch_assign_blocked(const float* X, int64_t n, int d, const float* P, int64_t k, unsigned long long* keys_ws,
+                           int32_t* labels, float* best, cudaStream_t st);
 void launch_assign_simt(const float* X, int64_t n, int d, const float* P, int64_t k,
                         int32_t* labels, float* best, cudaStream_t st);
 

@@ -255,19 +255,25 @@ __global__ void __launch_bounds__(256) k_fixup_tiled(const float* __restrict__ X
   }
 }
 
-// Device-sized variant: the flagged count is read on the device (no host round trip); block
-// b walks work items (row block, prototype split) b, b + gridDim.x, ...  At most `cap` rows.
-__global__ void __launch_bounds__(256) k_fixup_dev(const float* __restrict__ X, int d,
-                                                   const float* __restrict__ P, int64_t k,
-                                                   const int32_t* __restrict__ flag_rows,
-                                                   const int32_t* __restrict__ flag_count, int64_t cap,
-                                                   int nsm, unsigned long long* __restrict__ keys) {
-  extern __shared__ float fsm[];
-  const int64_t nf = min64(*flag_count, cap);
+// Blocked SIMT argmin (K4 re-check and the large-d assignment): rows = rows[0..count) (or the
+// identity when rows == nullptr), count = min(*count_dev, cap) (or cap when count_dev ==
+// nullptr), read on the device so no host round trip is needed.  Block b walks work items (32-row
+// block, prototype split) b, b + gridDim.x, ...; each item sweeps its 128-prototype tiles with
+// the dimension streamed through shared memory in chunks of FX_DK (thread = 4 rows x 4
+// prototypes, direct FP32 sums of squares); per row the best (d^2, j) is merged with a 64-bit
+// atomicMin on (d^2 bits << 32 | j).
+constexpr int FX_DK = 64;
+
+__global__ void __launch_bounds__(256) k_blocked_argmin(const float* __restrict__ X, int d,
+                                                        const float* __restrict__ P, int64_t k,
+                                                        const int32_t* __restrict__ rows,
+                                                        const int32_t* __restrict__ count_dev, int64_t cap,
+                                                        int nsm, unsigned long long* __restrict__ keys) {
+  __shared__ float xs[FX_R * (FX_DK + 1)];
+  __shared__ float cs[FX_P * (FX_DK + 1)];
+  const int64_t nf = count_dev ? min64(*count_dev, cap) : cap;
   if (nf <= 0) return;
-  const int dp = d + 1;
-  float* xs = fsm;
-  float* cs = fsm + FX_R * dp;
+  constexpr int dp = FX_DK + 1;
   const int t = threadIdx.x;
   const int rg = t & 7, pg = t >> 3;
   const int64_t row_blocks = (nf + FX_R - 1) / FX_R;
@@ -280,11 +286,6 @@ __global__ void __launch_bounds__(256) k_fixup_dev(const float* __restrict__ X, 
     const int64_t f0 = (w / splits) * FX_R;
     const int64_t t0 = (w % splits) * tps;
     const int64_t t1 = min64(ntile, t0 + tps);
-    __syncthreads();
-    for (int e = t; e < FX_R * d; e += 256) {
-      const int r = e / d, c = e - r * d;
-      xs[r * dp + c] = (f0 + r < nf) ? X[(int64_t)flag_rows[f0 + r] * d + c] : 0.f;
-    }
     float bv[4];
     int64_t bj[4];
 #pragma unroll
@@ -294,30 +295,39 @@ __global__ void __launch_bounds__(256) k_fixup_dev(const float* __restrict__ X, 
     }
     for (int64_t tile = t0; tile < t1; ++tile) {
       const int64_t j0 = tile * FX_P;
-      __syncthreads();
-      for (int e = t; e < FX_P * d; e += 256) {
-        const int p = e / d, c = e - p * d;
-        cs[p * dp + c] = (j0 + p < k) ? P[(j0 + p) * d + c] : 0.f;
-      }
-      __syncthreads();
       float acc[4][4];
 #pragma unroll
       for (int a = 0; a < 4; ++a)
 #pragma unroll
         for (int b = 0; b < 4; ++b) acc[a][b] = 0.f;
-      for (int i = 0; i < d; ++i) {
-        float xv[4], cv[4];
+      for (int k0 = 0; k0 < d; k0 += FX_DK) {
+        const int dk = d - k0 < FX_DK ? d - k0 : FX_DK;
+        __syncthreads();
+        for (int e = t; e < FX_R * dk; e += 256) {
+          const int r = e / dk, c = e - r * dk;
+          const int64_t f = f0 + r;
+          const int64_t row = f < nf ? (rows ? (int64_t)rows[f] : f) : -1;
+          xs[r * dp + c] = row >= 0 ? X[row * d + k0 + c] : 0.f;
+        }
+        for (int e = t; e < FX_P * dk; e += 256) {
+          const int p = e / dk, c = e - p * dk;
+          cs[p * dp + c] = (j0 + p < k) ? P[(j0 + p) * d + k0 + c] : 0.f;
+        }
+        __syncthreads();
+        for (int i = 0; i < dk; ++i) {
+          float xv[4], cv[4];
 #pragma unroll
-        for (int a = 0; a < 4; ++a) xv[a] = xs[(rg * 4 + a) * dp + i];
+          for (int a = 0; a < 4; ++a) xv[a] = xs[(rg * 4 + a) * dp + i];
 #pragma unroll
-        for (int b = 0; b < 4; ++b) cv[b] = cs[(pg * 4 + b) * dp + i];
+          for (int b = 0; b < 4; ++b) cv[b] = cs[(pg * 4 + b) * dp + i];
 #pragma unroll
-        for (int a = 0; a < 4; ++a)
+          for (int a = 0; a < 4; ++a)
 #pragma unroll
-          for (int b = 0; b < 4; ++b) {
-            const float df = xv[a] - cv[b];
-            acc[a][b] = fmaf(df, df, acc[a][b]);
-          }
+            for (int b = 0; b < 4; ++b) {
+              const float df = xv[a] - cv[b];
+              acc[a][b] = fmaf(df, df, acc[a][b]);
+            }
+        }
       }
 #pragma unroll
       for (int b = 0; b < 4; ++b) {
@@ -325,7 +335,7 @@ __global__ void __launch_bounds__(256) k_fixup_dev(const float* __restrict__ X, 
         if (j < k) {
 #pragma unroll
           for (int a = 0; a < 4; ++a)
-            if (acc[a][b] < bv[a]) {
+            if (acc[a][b] < bv[a]) {  // j increases with (tile, b) for this thread: keeps lowest j
               bv[a] = acc[a][b];
               bj[a] = j;
             }
@@ -344,37 +354,45 @@ __global__ void __launch_bounds__(256) k_fixup_dev(const float* __restrict__ X, 
   }
 }
 
-__global__ void k_fixup_init(const int32_t* __restrict__ flag_count, int64_t cap, unsigned long long* keys) {
-  const int64_t nf = min64(*flag_count, cap);
+__global__ void k_keys_init(const int32_t* __restrict__ count_dev, int64_t cap, unsigned long long* keys) {
+  const int64_t nf = count_dev ? min64(*count_dev, cap) : cap;
   for (int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; f < nf; f += (int64_t)gridDim.x * blockDim.x)
     keys[f] = ~0ull;
 }
 
-__global__ void k_fixup_write_dev(const int32_t* __restrict__ flag_rows, const int32_t* __restrict__ flag_count,
-                                  int64_t cap, const unsigned long long* __restrict__ keys,
-                                  int32_t* __restrict__ labels, float* __restrict__ best) {
-  const int64_t nf = min64(*flag_count, cap);
+__global__ void k_keys_write(const int32_t* __restrict__ rows, const int32_t* __restrict__ count_dev, int64_t cap,
+                             const unsigned long long* __restrict__ keys, int32_t* __restrict__ labels,
+                             float* __restrict__ best) {
+  const int64_t nf = count_dev ? min64(*count_dev, cap) : cap;
   for (int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; f < nf; f += (int64_t)gridDim.x * blockDim.x) {
     const unsigned long long key = keys[f];
-    const int32_t row = flag_rows[f];
+    const int64_t row = rows ? (int64_t)rows[f] : f;
     labels[row] = (int32_t)(key & 0xffffffffu);
-    best[row] = __uint_as_float((uint32_t)(key >> 32));
+    if (best) best[row] = __uint_as_float((uint32_t)(key >> 32));
   }
+}
+
+static void launch_blocked(const float* X, int d, const float* P, int64_t k, const int32_t* rows,
+                           const int32_t* count_dev, int64_t cap, unsigned long long* keys_ws, int32_t* labels,
+                           float* best, cudaStream_t st) {
+  k_keys_init<<<num_sms() * 2, 256, 0, st>>>(count_dev, cap, keys_ws);
+  MASK_LAUNCH_CHECK();
+  k_blocked_argmin<<<num_sms() * 4, 256, 0, st>>>(X, d, P, k, rows, count_dev, cap, num_sms(), keys_ws);
+  MASK_LAUNCH_CHECK();
+  k_keys_write<<<num_sms() * 2, 256, 0, st>>>(rows, count_dev, cap, keys_ws, labels, best);
+  MASK_LAUNCH_CHECK();
 }
 
 void launch_fixup_device(const float* X, int d, const float* P, int64_t k, const int32_t* flag_rows,
                          const int32_t* flag_count, int64_t cap, unsigned long long* keys_ws, int32_t* labels,
                          float* best, cudaStream_t st) {
-  const size_t smem = (size_t)(FX_R + FX_P) * (d + 1) * sizeof(float);
-  MASK_REQUIRE(smem <= 200 * 1024, MASK_ERR_UNSUPPORTED, "fix-up: dim too large");
-  if (smem > 48 * 1024)
-    MASK_CUDA(cudaFuncSetAttribute(k_fixup_dev, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k_fixup_init<<<num_sms() * 2, 256, 0, st>>>(flag_count, cap, keys_ws);
-  MASK_LAUNCH_CHECK();
-  k_fixup_dev<<<num_sms() * 4, 256, smem, st>>>(X, d, P, k, flag_rows, flag_count, cap, num_sms(), keys_ws);
-  MASK_LAUNCH_CHECK();
-  k_fixup_write_dev<<<num_sms() * 2, 256, 0, st>>>(flag_rows, flag_count, cap, keys_ws, labels, best);
-  MASK_LAUNCH_CHECK();
+  launch_blocked(X, d, P, k, flag_rows, flag_count, cap, keys_ws, labels, best, st);
+}
+
+void launch_assign_blocked(const float* X, int64_t n, int d, const float* P, int64_t k, unsigned long long* keys_ws,
+                           int32_t* labels, float* best, cudaStream_t st) {
+  if (n <= 0) return;
+  launch_blocked(X, d, P, k, nullptr, nullptr, n, keys_ws, labels, best, st);
 }
 
 __global__ void k_fixup_write(const int32_t* __restrict__ flag_rows, int64_t nf,

@@ -307,7 +307,12 @@ int64_t assign_pass(const Input& in, const float* P, int64_t k, int flags, int32
   if (!use_tc) {
     ws.kernel_id = 0;
     if (tm) tm->t[MASK_T_ASSIGN].start(st);
-    launch_assign_simt(in.X, n, d, P, k, labels_out, best, st);
+    if (d <= 64) {
+      launch_assign_simt(in.X, n, d, P, k, labels_out, best, st);
+    } else {  // large d: dimension-chunked blocked kernel
+      if ((int64_t)ws.fix_keys.n < n) ws.fix_keys.alloc((size_t)n);
+      launch_assign_blocked(in.X, n, d, P, k, ws.fix_keys.p, labels_out, best, st);
+    }
     if (tm) tm->t[MASK_T_ASSIGN].stop(st);
     return 0;
   }

@@ -65,6 +65,19 @@ def check_queries(ids_gpu, d2_gpu, ids_ref, d2_ref, gap_ref, what=""):
     ids_gpu = np.asarray(ids_gpu)
     exempt = gap_ref < TIE_REL
     same = np.all(ids_gpu == ids_ref, axis=1)
+    # the same result set whose order differs only inside groups of (near-)equal distances
+    # (adjacent oracle d^2 within 1e-5 relative: the (d^2, id) order of a tie is not decided by
+    # FP32 vs FP64 rounding) counts as identical
+    for q in np.nonzero(~same)[0]:
+        a, b = ids_gpu[q], ids_ref[q]
+        if set(a.tolist()) != set(b.tolist()):
+            continue
+        dref = {int(i): float(v) for i, v in zip(b, d2_ref[q]) if i >= 0}
+        da = np.array([dref[int(i)] for i in a if i >= 0])
+        pad_ok = np.all(a[len(da):] < 0)  # padding only at the tail
+        order_ok = pad_ok and np.all(np.diff(da) >= -TIE_REL * np.maximum(np.abs(da[1:]), 1e-30))
+        if order_ok:
+            same[q] = True
     bad = ~same & ~exempt
     assert not bad.any(), (f"{what}: {int(bad.sum())} non-exempt query mismatches of {len(same)} "
                            f"(first {np.nonzero(bad)[0][:5].tolist()})")
