@@ -147,6 +147,11 @@ void launch_transpose(const float* P, int64_t k, int d, float* PT, cudaStream_t 
 // K5/K6: cluster sums and counts (S, counts must be zeroed by the caller).
 void launch_update_dense(const float* X, int64_t n, int d, const int32_t* labels, int64_t k,
                          float* S, int32_t* counts, cudaStream_t st);
+// K5 (sorted): counting sort by label + warp-per-cluster segmented sums (d % 4 == 0);
+// counts must be zero on entry; workspaces: offsets k+1, cursor k, members n
+void launch_update_sorted(const float* X, int64_t n, int d, const int32_t* labels, int64_t k, float* S,
+                          int32_t* counts, int64_t* offsets_ws, int32_t* cursor_ws, int32_t* members_ws,
+                          cudaStream_t st);
 void launch_update_csr(const int64_t* row_ptr, const int32_t* col, const float* val, int64_t n,
                        int d, const int32_t* labels, float* S, int32_t* counts, cudaStream_t st);
 // K7: P_j <- S_j / n_j (keep if n_j == 0); zeroes S and counts; stats[0] = max disp^2 (as

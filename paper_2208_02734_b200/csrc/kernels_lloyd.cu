@@ -830,3 +830,117 @@ void launch_transpose(const float* P, int64_t k, int d, float* PT, cudaStream_t 
 }
 
 }  // namespace mask
+
+namespace mask {
+
+// ====================================================================== K5 (sorted variant)
+// Update by counting sort instead of float atomics: histogram of labels (= the counts) ->
+// exclusive scan -> scatter of row ids into per-cluster member lists -> one warp per cluster
+// sums its members' rows (float4 lanes, shuffle reduction) and writes S_j once.  Reads X once
+// (gathered rows), labels twice, member ids twice; no floating-point atomics.
+__global__ void k_segsum_v4(const float4* __restrict__ X4, int d4, const int64_t* __restrict__ offsets,
+                            const int32_t* __restrict__ members, int64_t k, float4* __restrict__ S4) {
+  const int lane = threadIdx.x & 31;
+  const int lpr = d4 < 32 ? d4 : 32;          // lanes per row (d4 <= 32 assumed by the caller's chunking)
+  const int rpi = 32 / lpr;                   // rows per warp iteration
+  const int sub = lane / lpr, c4 = lane - sub * lpr;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t j = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); j < k; j += warps) {
+    const int64_t m0 = offsets[j], m1 = offsets[j + 1];
+    for (int cb = 0; cb < d4; cb += lpr) {  // column blocks of 32 float4 for d > 128
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (sub < rpi && c4 + cb < d4) {
+        for (int64_t m = m0 + sub; m < m1; m += rpi) {
+          const float4 v = __ldg(X4 + (int64_t)members[m] * d4 + cb + c4);
+          acc.x += v.x;
+          acc.y += v.y;
+          acc.z += v.z;
+          acc.w += v.w;
+        }
+      }
+      for (int o = lpr; o < 32; o <<= 1) {  // reduce the rows of the warp that share c4
+        acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+        acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+        acc.z += __shfl_xor_sync(0xffffffffu, acc.z, o);
+        acc.w += __shfl_xor_sync(0xffffffffu, acc.w, o);
+      }
+      if (sub == 0 && c4 + cb < d4) S4[j * d4 + cb + c4] = acc;
+    }
+  }
+}
+
+__global__ void k_histogram2(const int32_t* __restrict__ labels, int64_t n, int32_t* __restrict__ cnt) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(cnt + labels[i], 1);
+}
+
+__global__ void __launch_bounds__(1024) k_scan_offsets2(const int32_t* __restrict__ cnt, int64_t k,
+                                                        int64_t* __restrict__ offsets,
+                                                        int32_t* __restrict__ cursor);
+__global__ void k_scatter_members2(const int32_t* __restrict__ labels, int64_t n, int32_t* __restrict__ cursor,
+                                   int32_t* __restrict__ members) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t pos = atomicAdd(cursor + labels[i], 1);
+    members[pos] = (int32_t)i;
+  }
+}
+
+void launch_update_sorted(const float* X, int64_t n, int d, const int32_t* labels, int64_t k, float* S,
+                          int32_t* counts, int64_t* offsets_ws, int32_t* cursor_ws, int32_t* members_ws,
+                          cudaStream_t st) {
+  if (n <= 0) return;
+  // counts must be zero on entry (the finalize kernel leaves them zeroed)
+  k_histogram2<<<grid_for(n, 256), 256, 0, st>>>(labels, n, counts);
+  MASK_LAUNCH_CHECK();
+  k_scan_offsets2<<<1, 1024, 0, st>>>(counts, k, offsets_ws, cursor_ws);
+  MASK_LAUNCH_CHECK();
+  k_scatter_members2<<<grid_for(n, 256), 256, 0, st>>>(labels, n, cursor_ws, members_ws);
+  MASK_LAUNCH_CHECK();
+  k_segsum_v4<<<grid_for(k * 32, 256), 256, 0, st>>>(reinterpret_cast<const float4*>(X), d / 4, offsets_ws,
+                                                     members_ws, k, reinterpret_cast<float4*>(S));
+  MASK_LAUNCH_CHECK();
+}
+
+__global__ void __launch_bounds__(1024) k_scan_offsets2(const int32_t* __restrict__ cnt, int64_t k,
+                                                        int64_t* __restrict__ offsets,
+                                                        int32_t* __restrict__ cursor) {
+  __shared__ int64_t warp_tot[32];
+  __shared__ int64_t carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int64_t base = 0; base < k; base += 1024) {
+    const int64_t j = base + threadIdx.x;
+    const int64_t v = j < k ? cnt[j] : 0;
+    int64_t incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    if (lane == 31) warp_tot[w] = incl;
+    __syncthreads();
+    if (w == 0) {
+      const int64_t t = warp_tot[lane];
+      int64_t ti = t;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int64_t u = __shfl_up_sync(0xffffffffu, ti, o);
+        if (lane >= o) ti += u;
+      }
+      warp_tot[lane] = ti - t;
+    }
+    __syncthreads();
+    const int64_t excl = carry + warp_tot[w] + incl - v;
+    if (j < k) {
+      offsets[j] = excl;
+      cursor[j] = (int32_t)excl;
+    }
+    __syncthreads();
+    if (threadIdx.x == 1023) carry = excl + v;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) offsets[k] = carry;
+}
+
+}  // namespace mask
