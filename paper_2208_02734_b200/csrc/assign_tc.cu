@@ -417,12 +417,18 @@ __global__ void __launch_bounds__(128 + 128 * EPI_WG, 1)
 #pragma unroll
           for (int i = 0; i < 32; i += 2) {
             int32_t ka, kb;
+#if !defined(MASK_TC_KEY_IMAD)
+            // key = (bits & ~0xFF) | column: one LOP3 (mask in a register, column immediate)
+            asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(ka) : "r"(r[cc & 1][i]), "r"(~(key_lo_mul - 1u)), "r"((uint32_t)(cc * 32 + i)));
+            asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(kb) : "r"(r[cc & 1][i + 1]), "r"(~(key_lo_mul - 1u)), "r"((uint32_t)(cc * 32 + i + 1)));
+#else
             asm("{\n .reg .u32 h;\n mul.hi.u32 h, %1, %2;\n mad.lo.u32 %0, h, %3, %4;\n}"
                 : "=r"(ka)
                 : "r"(r[cc & 1][i]), "r"(key_hi_mul), "r"(key_lo_mul), "r"((uint32_t)(cc * 32 + i)));
             asm("{\n .reg .u32 h;\n mul.hi.u32 h, %1, %2;\n mad.lo.u32 %0, h, %3, %4;\n}"
                 : "=r"(kb)
                 : "r"(r[cc & 1][i + 1]), "r"(key_hi_mul), "r"(key_lo_mul), "r"((uint32_t)(cc * 32 + i + 1)));
+#endif
             // top-2 of {b1 <= b2} u {ka, kb}: b1' = min(b1, m), b2' = min(b2, M, max(b1, m))
             const int u = (i >> 1) & (NCH - 1);
             const int32_t m = imin(ka, kb), M = imax(ka, kb);
