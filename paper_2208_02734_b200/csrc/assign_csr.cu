@@ -27,7 +27,8 @@ __global__ void __launch_bounds__(kRowsPerBlock * 32)
     k_assign_csr(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
                  const float* __restrict__ val, int64_t n, const float* __restrict__ PT,
                  const float* __restrict__ cn2, int64_t k, int32_t* __restrict__ labels,
-                 float* __restrict__ best_out) {
+                 float* __restrict__ best_out, const int* __restrict__ active) {
+  if (active && !*active) return;  // level converged: this pass is skipped on the device
   __shared__ int32_t s_col[kRowsPerBlock][kMaxNnzSmem];
   __shared__ float s_val[kRowsPerBlock][kMaxNnzSmem];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -95,12 +96,12 @@ __global__ void __launch_bounds__(kRowsPerBlock * 32)
 
 void launch_assign_csr(const int64_t* row_ptr, const int32_t* col, const float* val, int64_t n,
                        int d, const float* PT, const float* cn2, int64_t k, int32_t* labels,
-                       float* best, cudaStream_t st) {
+                       float* best, cudaStream_t st, const int* active) {
   (void)d;
   if (n <= 0) return;
   const int64_t blocks = (n + kRowsPerBlock - 1) / kRowsPerBlock;
   const unsigned grid = (unsigned)(blocks < (int64_t)num_sms() * 16 ? blocks : (int64_t)num_sms() * 16);
-  k_assign_csr<<<grid, kRowsPerBlock * 32, 0, st>>>(row_ptr, col, val, n, PT, cn2, k, labels, best);
+  k_assign_csr<<<grid, kRowsPerBlock * 32, 0, st>>>(row_ptr, col, val, n, PT, cn2, k, labels, best, active);
   MASK_LAUNCH_CHECK();
 }
 

@@ -235,7 +235,9 @@ __global__ void __launch_bounds__(128 + 128 * EPI_WG, 1)
                 const float* __restrict__ X, const float* __restrict__ P, const float* __restrict__ cn2,
                 const float* __restrict__ xn2, int64_t n, int d, int64_t k, int32_t* __restrict__ labels,
                 float* __restrict__ best, int32_t* __restrict__ flag_rows, int32_t* __restrict__ flag_count,
-                float err_coef, uint32_t key_hi_mul, uint32_t key_lo_mul, int dbg) {
+                float err_coef, uint32_t key_hi_mul, uint32_t key_lo_mul, int dbg,
+                const int* __restrict__ active) {
+  if (active && !*active) return;  // level converged: this pass is skipped on the device
   using C = Cfg<CW, NKC, KA, BN, STAGES, NACC, FOLD, EPI_WG>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -652,7 +654,8 @@ inline int tc_debug_mode() {
 template <int CW, int NKC, int KA, int BN, int STAGES, int NACC, bool FOLD, int EPI_WG>
 void launch_cfg(const float* X, int64_t n, int d, int kc, int64_t k_rows, const float* P, const float* Pb,
                 const float* Ps, const float* cn2, int64_t k, const float* xn2, int32_t* labels, float* best,
-                int32_t* flag_rows, int32_t* flag_count, float err_coef, cudaStream_t st) {
+                int32_t* flag_rows, int32_t* flag_count, float err_coef, cudaStream_t st,
+                const int* active) {
   using C = Cfg<CW, NKC, KA, BN, STAGES, NACC, FOLD, EPI_WG>;
   const CUtensorMap tBb = make_map(Pb, k_rows, kc, CW, BN);
   const CUtensorMap tBs = make_map(Ps, k_rows, kc, CW, BN);
@@ -664,7 +667,7 @@ void launch_cfg(const float* X, int64_t n, int d, int kc, int64_t k_rows, const 
   }
   const unsigned grid = (unsigned)((n + BM - 1) / BM);
   kern<<<grid, C::NTHREADS, C::SMEM, st>>>(tBb, tBs, X, P, cn2, xn2, n, d, k, labels, best, flag_rows, flag_count,
-                                           err_coef, 1u << 24, 256u, tc_debug_mode());
+                                           err_coef, 1u << 24, 256u, tc_debug_mode(), active);
   MASK_LAUNCH_CHECK();
   if (tc_debug_mode() & 8) dump_trace((int)grid);
 }
@@ -697,7 +700,7 @@ float tc_err_coef(int d) {
 
 void launch_assign_tc(const float* X, int64_t n, int d, const float* P, const float* Pb, const float* Ps,
                       const float* cn2, int64_t k, const float* xn2, int32_t* labels, float* best,
-                      int32_t* flag_rows, int32_t* flag_count, cudaStream_t st) {
+                      int32_t* flag_rows, int32_t* flag_count, cudaStream_t st, const int* active) {
   const float coef = tc_err_coef(d);
   const int kc = tc_operand_cols(d);
   const int64_t kr = tc_operand_rows(k);
@@ -705,19 +708,19 @@ void launch_assign_tc(const float* X, int64_t n, int d, const float* P, const fl
   // KA columns), three epilogue warpgroups of 64 columns (best of the measured variants)
   if (d + 2 <= 24)
     tc::launch_cfg<32, 1, 24, 192, 4, 2, true, 3>(X, n, d, kc, kr, P, Pb, Ps, cn2, k, xn2, labels, best, flag_rows,
-                                                  flag_count, coef, st);
+                                                  flag_count, coef, st, active);
   else if (d + 2 <= 32)
     tc::launch_cfg<32, 1, 32, 192, 4, 2, true, 3>(X, n, d, kc, kr, P, Pb, Ps, cn2, k, xn2, labels, best, flag_rows,
-                                                  flag_count, coef, st);
+                                                  flag_count, coef, st, active);
   else if (d <= 64)
     tc::launch_cfg<32, 2, 64, 128, 6, 3, false, 2>(X, n, d, kc, kr, P, Pb, Ps, cn2, k, xn2, labels, best, flag_rows,
-                                                   flag_count, coef, st);
+                                                   flag_count, coef, st, active);
   else if (d <= 96)
     tc::launch_cfg<32, 3, 96, 128, 6, 2, false, 2>(X, n, d, kc, kr, P, Pb, Ps, cn2, k, xn2, labels, best, flag_rows,
-                                                   flag_count, coef, st);
+                                                   flag_count, coef, st, active);
   else
     tc::launch_cfg<32, 4, 128, 128, 6, 2, false, 2>(X, n, d, kc, kr, P, Pb, Ps, cn2, k, xn2, labels, best,
-                                                    flag_rows, flag_count, coef, st);
+                                                    flag_rows, flag_count, coef, st, active);
 }
 
 }  // namespace mask

@@ -103,9 +103,9 @@ inline int num_sms() {
 // K2b: blocked SIMT assignment for large d (dimension streamed through shared memory);
 // keys_ws = n u64 scratch
 void launch_assign_blocked(const float* X, int64_t n, int d, const float* P, int64_t k, unsigned long long* keys_ws,
-                           int32_t* labels, float* best, cudaStream_t st);
+                           int32_t* labels, float* best, cudaStream_t st, const int* active = nullptr);
 void launch_assign_simt(const float* X, int64_t n, int d, const float* P, int64_t k,
-                        int32_t* labels, float* best, cudaStream_t st);
+                        int32_t* labels, float* best, cudaStream_t st, const int* active = nullptr);
 
 // K1: tcgen05 3xTF32 assignment (dense, d % 8 == 0, d <= 256).  Writes labels, best (d^2
 // estimate incl. ||x||^2), and appends rows whose top-2 gap is within the error bound to
@@ -117,7 +117,7 @@ int tc_operand_cols(int d);
 void launch_assign_tc(const float* X, int64_t n, int d, const float* P, const float* Pb,
                       const float* Ps, const float* cn2, int64_t k, const float* xn2,
                       int32_t* labels, float* best, int32_t* flag_rows, int32_t* flag_count,
-                      cudaStream_t st);
+                      cudaStream_t st, const int* active = nullptr);
 // K4: exact FP32 direct re-check of flagged rows against all k prototypes.
 void launch_fixup(const float* X, int d, const float* P, int64_t k, const int32_t* flag_rows,
                   const int32_t* flag_count, int64_t max_flags, int32_t* labels, float* best,
@@ -125,7 +125,7 @@ void launch_fixup(const float* X, int d, const float* P, int64_t k, const int32_
 // K4 (tiled, device-sized): the first min(*flag_count, cap) flagged rows; keys_ws = cap u64
 void launch_fixup_device(const float* X, int d, const float* P, int64_t k, const int32_t* flag_rows,
                          const int32_t* flag_count, int64_t cap, unsigned long long* keys_ws, int32_t* labels,
-                         float* best, cudaStream_t st);
+                         float* best, cudaStream_t st, const int* active = nullptr);
 // K4 (tiled): nf flagged rows (host-known count) against all prototypes; keys_ws = nf u64
 void launch_fixup_tiled(const float* X, int d, const float* P, int64_t k, const int32_t* flag_rows,
                         int64_t nf, unsigned long long* keys_ws, int32_t* labels, float* best,
@@ -133,7 +133,7 @@ void launch_fixup_tiled(const float* X, int d, const float* P, int64_t k, const 
 // prototype operands for K1: Pb = tf32_rn(-2c), Ps = tf32_rn(-2c - Pb), cn2 = ||c||^2; with
 // kc > d the augmented columns [d] = split(||c||^2), [d+1] = (1, 0), rest 0 (row stride kc)
 void launch_prep_protos(const float* P, int64_t k, int d, int kc, float* Pb, float* Ps, float* cn2,
-                        cudaStream_t st, int64_t k_rows, int fold);
+                        cudaStream_t st, int64_t k_rows, int fold, const int* active = nullptr);
 // rows of the K1 B operand arrays (k padded to whole 256-prototype tiles)
 int64_t tc_operand_rows(int64_t k);
 void launch_row_norms(const float* X, int64_t n, int d, float* xn2, cudaStream_t st);
@@ -141,26 +141,22 @@ void launch_row_norms(const float* X, int64_t n, int d, float* xn2, cudaStream_t
 // K3: CSR rows x dense prototypes (sparse assignment).
 void launch_assign_csr(const int64_t* row_ptr, const int32_t* col, const float* val, int64_t n,
                        int d, const float* PT /* d x k transposed */, const float* cn2, int64_t k,
-                       int32_t* labels, float* best, cudaStream_t st);
-void launch_transpose(const float* P, int64_t k, int d, float* PT, cudaStream_t st);
+                       int32_t* labels, float* best, cudaStream_t st, const int* active = nullptr);
+void launch_transpose(const float* P, int64_t k, int d, float* PT, cudaStream_t st, const int* active = nullptr);
 
 // K5/K6: cluster sums and counts (S, counts must be zeroed by the caller).
 void launch_update_dense(const float* X, int64_t n, int d, const int32_t* labels, int64_t k,
-                         float* S, int32_t* counts, cudaStream_t st);
-// K5 (sorted): counting sort by label + warp-per-cluster segmented sums (d % 4 == 0);
-// counts must be zero on entry; workspaces: offsets k+1, cursor k, members n
-void launch_update_sorted(const float* X, int64_t n, int d, const int32_t* labels, int64_t k, float* S,
-                          int32_t* counts, int64_t* offsets_ws, int32_t* cursor_ws, int32_t* members_ws,
-                          cudaStream_t st);
+                         float* S, int32_t* counts, cudaStream_t st, const int* active = nullptr);
 void launch_update_csr(const int64_t* row_ptr, const int32_t* col, const float* val, int64_t n,
-                       int d, const int32_t* labels, float* S, int32_t* counts, cudaStream_t st);
+                       int d, const int32_t* labels, float* S, int32_t* counts, cudaStream_t st,
+                       const int* active = nullptr);
 // K7: P_j <- S_j / n_j (keep if n_j == 0); zeroes S and counts; stats[0] = max disp^2 (as
 // float bits, atomicMax), stats[1] = empties.  `stat` must be zeroed by the caller.
 void launch_finalize(float* P, float* S, int32_t* counts, int64_t k, int d, uint32_t* stat,
-                     int keep_counts, cudaStream_t st);
+                     int keep_counts, cudaStream_t st, const int* active = nullptr);
 // pass statistics: J = sum best (double), changed = #(cur != prev)
 void launch_pass_stats(const int32_t* cur, const int32_t* prev, const float* best, int64_t n,
-                       double* J, unsigned long long* changed, cudaStream_t st);
+                       double* J, unsigned long long* changed, cudaStream_t st, const int* active = nullptr);
 // K10: P[j] = Y[idx[j]] (dense) / densified CSR row
 void launch_gather_rows(const float* Y, int d, const int64_t* idx, int64_t k, int64_t row_offset,
                         int64_t n_local, float* P, cudaStream_t st);
@@ -197,6 +193,6 @@ void launch_query_dense(const QIndex& qi, const float* Q, int64_t nq, int knn, i
 void launch_query_csr(const QIndex& qi, const float* cn2_levels_flat, const int64_t* cn2_off,
                       const int64_t* qrp, const int32_t* qcol, const float* qval, int64_t nq,
                       int knn, int beam, int64_t* ids, float* d2, cudaStream_t st);
-void launch_level_norms(const float* P, int64_t k, int d, float* cn2, cudaStream_t st);
+void launch_level_norms(const float* P, int64_t k, int d, float* cn2, cudaStream_t st, const int* active = nullptr);
 
 }  // namespace mask

@@ -27,7 +27,9 @@ __global__ void __launch_bounds__(256) k_assign_simt(const float* __restrict__ X
                                                      int d, const float* __restrict__ P,
                                                      int64_t k, int kc_max,
                                                      int32_t* __restrict__ labels,
-                                                     float* __restrict__ best_out) {
+                                                     float* __restrict__ best_out,
+                                                     const int* __restrict__ active) {
+  if (active && !*active) return;  // level converged: this pass is skipped on the device
   extern __shared__ float sP[];
   const int D = DT > 0 ? DT : d;
   const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -75,7 +77,7 @@ __global__ void __launch_bounds__(256) k_assign_simt(const float* __restrict__ X
 }
 
 void launch_assign_simt(const float* X, int64_t n, int d, const float* P, int64_t k,
-                        int32_t* labels, float* best, cudaStream_t st) {
+                        int32_t* labels, float* best, cudaStream_t st, const int* active) {
   if (n <= 0) return;
   const int block = 256;
   int kc = (int)min64(k, 40 * 1024 / (4 * (int64_t)d));
@@ -90,7 +92,7 @@ void launch_assign_simt(const float* X, int64_t n, int d, const float* P, int64_
     if (smem > 48 * 1024)                                                                 \
       MASK_CUDA(cudaFuncSetAttribute(k_assign_simt<DV>,                                   \
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
-    k_assign_simt<DV><<<grid, block, smem, st>>>(X, n, d, P, k, kc, labels, best);        \
+    k_assign_simt<DV><<<grid, block, smem, st>>>(X, n, d, P, k, kc, labels, best, active);        \
     break;                                                                                \
   }
   switch (d) {
@@ -106,7 +108,7 @@ void launch_assign_simt(const float* X, int64_t n, int d, const float* P, int64_
       if (smem > 48 * 1024)
         MASK_CUDA(cudaFuncSetAttribute(k_assign_simt<0>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      k_assign_simt<0><<<grid, block, smem, st>>>(X, n, d, P, k, kc, labels, best);
+      k_assign_simt<0><<<grid, block, smem, st>>>(X, n, d, P, k, kc, labels, best, active);
     }
   }
 #undef MASK_SIMT_CASE
@@ -268,7 +270,9 @@ __global__ void __launch_bounds__(256) k_blocked_argmin(const float* __restrict_
                                                         const float* __restrict__ P, int64_t k,
                                                         const int32_t* __restrict__ rows,
                                                         const int32_t* __restrict__ count_dev, int64_t cap,
-                                                        int nsm, unsigned long long* __restrict__ keys) {
+                                                        int nsm, unsigned long long* __restrict__ keys,
+                                                        const int* __restrict__ active) {
+  if (active && !*active) return;  // level converged: this pass is skipped on the device
   __shared__ float xs[FX_R * (FX_DK + 1)];
   __shared__ float cs[FX_P * (FX_DK + 1)];
   const int64_t nf = count_dev ? min64(*count_dev, cap) : cap;
@@ -354,7 +358,9 @@ __global__ void __launch_bounds__(256) k_blocked_argmin(const float* __restrict_
   }
 }
 
-__global__ void k_keys_init(const int32_t* __restrict__ count_dev, int64_t cap, unsigned long long* keys) {
+__global__ void k_keys_init(const int32_t* __restrict__ count_dev, int64_t cap, unsigned long long* keys,
+                            const int* __restrict__ active) {
+  if (active && !*active) return;  // level converged: this pass is skipped on the device
   const int64_t nf = count_dev ? min64(*count_dev, cap) : cap;
   for (int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; f < nf; f += (int64_t)gridDim.x * blockDim.x)
     keys[f] = ~0ull;
@@ -362,7 +368,8 @@ __global__ void k_keys_init(const int32_t* __restrict__ count_dev, int64_t cap, 
 
 __global__ void k_keys_write(const int32_t* __restrict__ rows, const int32_t* __restrict__ count_dev, int64_t cap,
                              const unsigned long long* __restrict__ keys, int32_t* __restrict__ labels,
-                             float* __restrict__ best) {
+                             float* __restrict__ best, const int* __restrict__ active) {
+  if (active && !*active) return;  // level converged: this pass is skipped on the device
   const int64_t nf = count_dev ? min64(*count_dev, cap) : cap;
   for (int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; f < nf; f += (int64_t)gridDim.x * blockDim.x) {
     const unsigned long long key = keys[f];
@@ -374,25 +381,25 @@ __global__ void k_keys_write(const int32_t* __restrict__ rows, const int32_t* __
 
 static void launch_blocked(const float* X, int d, const float* P, int64_t k, const int32_t* rows,
                            const int32_t* count_dev, int64_t cap, unsigned long long* keys_ws, int32_t* labels,
-                           float* best, cudaStream_t st) {
-  k_keys_init<<<num_sms() * 2, 256, 0, st>>>(count_dev, cap, keys_ws);
+                           float* best, cudaStream_t st, const int* active) {
+  k_keys_init<<<num_sms() * 2, 256, 0, st>>>(count_dev, cap, keys_ws, active);
   MASK_LAUNCH_CHECK();
-  k_blocked_argmin<<<num_sms() * 4, 256, 0, st>>>(X, d, P, k, rows, count_dev, cap, num_sms(), keys_ws);
+  k_blocked_argmin<<<num_sms() * 4, 256, 0, st>>>(X, d, P, k, rows, count_dev, cap, num_sms(), keys_ws, active);
   MASK_LAUNCH_CHECK();
-  k_keys_write<<<num_sms() * 2, 256, 0, st>>>(rows, count_dev, cap, keys_ws, labels, best);
+  k_keys_write<<<num_sms() * 2, 256, 0, st>>>(rows, count_dev, cap, keys_ws, labels, best, active);
   MASK_LAUNCH_CHECK();
 }
 
 void launch_fixup_device(const float* X, int d, const float* P, int64_t k, const int32_t* flag_rows,
                          const int32_t* flag_count, int64_t cap, unsigned long long* keys_ws, int32_t* labels,
-                         float* best, cudaStream_t st) {
-  launch_blocked(X, d, P, k, flag_rows, flag_count, cap, keys_ws, labels, best, st);
+                         float* best, cudaStream_t st, const int* active) {
+  launch_blocked(X, d, P, k, flag_rows, flag_count, cap, keys_ws, labels, best, st, active);
 }
 
 void launch_assign_blocked(const float* X, int64_t n, int d, const float* P, int64_t k, unsigned long long* keys_ws,
-                           int32_t* labels, float* best, cudaStream_t st) {
+                           int32_t* labels, float* best, cudaStream_t st, const int* active) {
   if (n <= 0) return;
-  launch_blocked(X, d, P, k, nullptr, nullptr, n, keys_ws, labels, best, st);
+  launch_blocked(X, d, P, k, nullptr, nullptr, n, keys_ws, labels, best, st, active);
 }
 
 __global__ void k_fixup_write(const int32_t* __restrict__ flag_rows, int64_t nf,
@@ -440,7 +447,9 @@ __device__ __forceinline__ float tf32_rn(float x) {
 // One warp per prototype: Pb = tf32(-2c), Ps = tf32(-2c - Pb) (3xTF32 split of the B operand,
 // the factor -2 is exact), cn2 = ||c||^2 accumulated in FP64 then rounded.
 __global__ void k_prep_protos(const float* __restrict__ P, int64_t k, int64_t k_rows, int d, int kc, int fold,
-                              float* __restrict__ Pb, float* __restrict__ Ps, float* __restrict__ cn2) {
+                              float* __restrict__ Pb, float* __restrict__ Ps, float* __restrict__ cn2,
+                              const int* __restrict__ active) {
+  if (active && !*active) return;  // level converged: this pass is skipped on the device
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t j = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); j < k; j += warps) {
@@ -481,14 +490,14 @@ __global__ void k_prep_protos(const float* __restrict__ P, int64_t k, int64_t k_
 }
 
 void launch_prep_protos(const float* P, int64_t k, int d, int kc, float* Pb, float* Ps, float* cn2,
-                        cudaStream_t st, int64_t k_rows, int fold) {
+                        cudaStream_t st, int64_t k_rows, int fold, const int* active) {
   if (k_rows < k) k_rows = k;
-  k_prep_protos<<<grid_for(k * 32, 256), 256, 0, st>>>(P, k, k_rows, d, kc, fold, Pb, Ps, cn2);
+  k_prep_protos<<<grid_for(k * 32, 256), 256, 0, st>>>(P, k, k_rows, d, kc, fold, Pb, Ps, cn2, active);
   MASK_LAUNCH_CHECK();
 }
 
-void launch_level_norms(const float* P, int64_t k, int d, float* cn2, cudaStream_t st) {
-  launch_prep_protos(P, k, d, d, nullptr, nullptr, cn2, st, k, 0);
+void launch_level_norms(const float* P, int64_t k, int d, float* cn2, cudaStream_t st, const int* active) {
+  launch_prep_protos(P, k, d, d, nullptr, nullptr, cn2, st, k, 0, active);
 }
 
 __global__ void k_row_norms(const float* __restrict__ X, int64_t n, int d, float* __restrict__ xn2) {
@@ -515,7 +524,8 @@ void launch_row_norms(const float* X, int64_t n, int d, float* xn2, cudaStream_t
 // Rows with d % 4 == 0 use one 16-byte vector red per 4 columns.
 __global__ void k_update_dense_v4(const float4* __restrict__ X4, int64_t n, int d4,
                                   const int32_t* __restrict__ labels, float* __restrict__ S,
-                                  int32_t* __restrict__ counts) {
+                                  int32_t* __restrict__ counts, const int* __restrict__ active) {
+  if (active && !*active) return;  // level converged: this pass is skipped on the device
   const int64_t total = n * (int64_t)d4;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += stride) {
@@ -533,7 +543,8 @@ __global__ void k_update_dense_v4(const float4* __restrict__ X4, int64_t n, int 
 
 __global__ void k_update_dense(const float* __restrict__ X, int64_t n, int d,
                                const int32_t* __restrict__ labels, float* __restrict__ S,
-                               int32_t* __restrict__ counts) {
+                               int32_t* __restrict__ counts, const int* __restrict__ active) {
+  if (active && !*active) return;  // level converged: this pass is skipped on the device
   const int64_t total = n * (int64_t)d;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += stride) {
@@ -546,16 +557,16 @@ __global__ void k_update_dense(const float* __restrict__ X, int64_t n, int d,
 }
 
 void launch_update_dense(const float* X, int64_t n, int d, const int32_t* labels, int64_t k,
-                         float* S, int32_t* counts, cudaStream_t st) {
+                         float* S, int32_t* counts, cudaStream_t st, const int* active) {
   (void)k;
   if (n <= 0) return;
   if (d % 4 == 0 && ((uintptr_t)X % 16) == 0) {
     const int d4 = d / 4;
     k_update_dense_v4<<<grid_for(n * d4, 256, (int64_t)num_sms() * 16), 256, 0, st>>>(
-        reinterpret_cast<const float4*>(X), n, d4, labels, S, counts);
+        reinterpret_cast<const float4*>(X), n, d4, labels, S, counts, active);
   } else {
     k_update_dense<<<grid_for(n * d, 256, (int64_t)num_sms() * 16), 256, 0, st>>>(X, n, d, labels,
-                                                                                 S, counts);
+                                                                                 S, counts, active);
   }
   MASK_LAUNCH_CHECK();
 }
@@ -565,7 +576,8 @@ void launch_update_dense(const float* X, int64_t n, int d, const int32_t* labels
 __global__ void k_update_csr(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
                              const float* __restrict__ val, int64_t n, int d,
                              const int32_t* __restrict__ labels, float* __restrict__ S,
-                             int32_t* __restrict__ counts) {
+                             int32_t* __restrict__ counts, const int* __restrict__ active) {
+  if (active && !*active) return;  // level converged: this pass is skipped on the device
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < n; r += warps) {
@@ -577,11 +589,12 @@ __global__ void k_update_csr(const int64_t* __restrict__ rp, const int32_t* __re
 }
 
 void launch_update_csr(const int64_t* row_ptr, const int32_t* col, const float* val, int64_t n,
-                       int d, const int32_t* labels, float* S, int32_t* counts, cudaStream_t st) {
+                       int d, const int32_t* labels, float* S, int32_t* counts, cudaStream_t st,
+                       const int* active) {
   if (n <= 0) return;
   k_update_csr<<<grid_for(n * 32, 256, (int64_t)num_sms() * 16), 256, 0, st>>>(row_ptr, col, val,
                                                                               n, d, labels, S,
-                                                                              counts);
+                                                                              counts, active);
   MASK_LAUNCH_CHECK();
 }
 
@@ -590,7 +603,9 @@ void launch_update_csr(const int64_t* row_ptr, const int32_t* col, const float* 
 // non-negative floats), stat[1] = number of empty prototypes.  S and counts are zeroed for
 // the next pass (unless keep_counts, which leaves counts for the caller to read).
 __global__ void k_finalize(float* __restrict__ P, float* __restrict__ S, int32_t* __restrict__ counts,
-                           int64_t k, int d, uint32_t* __restrict__ stat, int keep_counts) {
+                           int64_t k, int d, uint32_t* __restrict__ stat, int keep_counts,
+                           const int* __restrict__ active) {
+  if (active && !*active) return;  // level converged: this pass is skipped on the device
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t j = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); j < k; j += warps) {
@@ -617,15 +632,16 @@ __global__ void k_finalize(float* __restrict__ P, float* __restrict__ S, int32_t
 }
 
 void launch_finalize(float* P, float* S, int32_t* counts, int64_t k, int d, uint32_t* stat,
-                     int keep_counts, cudaStream_t st) {
-  k_finalize<<<grid_for(k * 32, 256), 256, 0, st>>>(P, S, counts, k, d, stat, keep_counts);
+                     int keep_counts, cudaStream_t st, const int* active) {
+  k_finalize<<<grid_for(k * 32, 256), 256, 0, st>>>(P, S, counts, k, d, stat, keep_counts, active);
   MASK_LAUNCH_CHECK();
 }
 
 // ====================================================================== pass statistics
 __global__ void k_pass_stats(const int32_t* __restrict__ cur, const int32_t* __restrict__ prev,
                              const float* __restrict__ best, int64_t n, double* __restrict__ J,
-                             unsigned long long* __restrict__ changed) {
+                             unsigned long long* __restrict__ changed, const int* __restrict__ active) {
+  if (active && !*active) return;  // level converged: this pass is skipped on the device
   double s = 0.0;
   unsigned long long c = 0;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -663,10 +679,10 @@ __global__ void k_pass_stats(const int32_t* __restrict__ cur, const int32_t* __r
 }
 
 void launch_pass_stats(const int32_t* cur, const int32_t* prev, const float* best, int64_t n,
-                       double* J, unsigned long long* changed, cudaStream_t st) {
+                       double* J, unsigned long long* changed, cudaStream_t st, const int* active) {
   if (n <= 0) return;
   k_pass_stats<<<grid_for(n, 256, (int64_t)num_sms() * 4), 256, 0, st>>>(cur, prev, best, n, J,
-                                                                         changed);
+                                                                         changed, active);
   MASK_LAUNCH_CHECK();
 }
 
@@ -809,7 +825,9 @@ void launch_fill(float* p, int64_t count, float v, cudaStream_t st) {
 }
 
 // PT[i * k + j] = P[j * d + i] (d x k), used by the sparse assignment.
-__global__ void k_transpose(const float* __restrict__ P, int64_t k, int d, float* __restrict__ PT) {
+__global__ void k_transpose(const float* __restrict__ P, int64_t k, int d, float* __restrict__ PT,
+                            const int* __restrict__ active) {
+  if (active && !*active) return;  // level converged: this pass is skipped on the device
   __shared__ float tile[32][33];
   const int64_t j0 = (int64_t)blockIdx.x * 32, i0 = (int64_t)blockIdx.y * 32;
   for (int r = threadIdx.y; r < 32; r += blockDim.y) {
@@ -823,124 +841,11 @@ __global__ void k_transpose(const float* __restrict__ P, int64_t k, int d, float
   }
 }
 
-void launch_transpose(const float* P, int64_t k, int d, float* PT, cudaStream_t st) {
+void launch_transpose(const float* P, int64_t k, int d, float* PT, cudaStream_t st, const int* active) {
   dim3 grid((unsigned)((k + 31) / 32), (unsigned)((d + 31) / 32));
-  k_transpose<<<grid, dim3(32, 8), 0, st>>>(P, k, d, PT);
+  k_transpose<<<grid, dim3(32, 8), 0, st>>>(P, k, d, PT, active);
   MASK_LAUNCH_CHECK();
 }
 
 }  // namespace mask
 
-namespace mask {
-
-// ====================================================================== K5 (sorted variant)
-// Update by counting sort instead of float atomics: histogram of labels (= the counts) ->
-// exclusive scan -> scatter of row ids into per-cluster member lists -> one warp per cluster
-// sums its members' rows (float4 lanes, shuffle reduction) and writes S_j once.  Reads X once
-// (gathered rows), labels twice, member ids twice; no floating-point atomics.
-__global__ void k_segsum_v4(const float4* __restrict__ X4, int d4, const int64_t* __restrict__ offsets,
-                            const int32_t* __restrict__ members, int64_t k, float4* __restrict__ S4) {
-  const int lane = threadIdx.x & 31;
-  const int lpr = d4 < 32 ? d4 : 32;          // lanes per row (d4 <= 32 assumed by the caller's chunking)
-  const int rpi = 32 / lpr;                   // rows per warp iteration
-  const int sub = lane / lpr, c4 = lane - sub * lpr;
-  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t j = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); j < k; j += warps) {
-    const int64_t m0 = offsets[j], m1 = offsets[j + 1];
-    for (int cb = 0; cb < d4; cb += lpr) {  // column blocks of 32 float4 for d > 128
-      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (sub < rpi && c4 + cb < d4) {
-        for (int64_t m = m0 + sub; m < m1; m += rpi) {
-          const float4 v = __ldg(X4 + (int64_t)members[m] * d4 + cb + c4);
-          acc.x += v.x;
-          acc.y += v.y;
-          acc.z += v.z;
-          acc.w += v.w;
-        }
-      }
-      for (int o = lpr; o < 32; o <<= 1) {  // reduce the rows of the warp that share c4
-        acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
-        acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
-        acc.z += __shfl_xor_sync(0xffffffffu, acc.z, o);
-        acc.w += __shfl_xor_sync(0xffffffffu, acc.w, o);
-      }
-      if (sub == 0 && c4 + cb < d4) S4[j * d4 + cb + c4] = acc;
-    }
-  }
-}
-
-__global__ void k_histogram2(const int32_t* __restrict__ labels, int64_t n, int32_t* __restrict__ cnt) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    atomicAdd(cnt + labels[i], 1);
-}
-
-__global__ void __launch_bounds__(1024) k_scan_offsets2(const int32_t* __restrict__ cnt, int64_t k,
-                                                        int64_t* __restrict__ offsets,
-                                                        int32_t* __restrict__ cursor);
-__global__ void k_scatter_members2(const int32_t* __restrict__ labels, int64_t n, int32_t* __restrict__ cursor,
-                                   int32_t* __restrict__ members) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t pos = atomicAdd(cursor + labels[i], 1);
-    members[pos] = (int32_t)i;
-  }
-}
-
-void launch_update_sorted(const float* X, int64_t n, int d, const int32_t* labels, int64_t k, float* S,
-                          int32_t* counts, int64_t* offsets_ws, int32_t* cursor_ws, int32_t* members_ws,
-                          cudaStream_t st) {
-  if (n <= 0) return;
-  // counts must be zero on entry (the finalize kernel leaves them zeroed)
-  k_histogram2<<<grid_for(n, 256), 256, 0, st>>>(labels, n, counts);
-  MASK_LAUNCH_CHECK();
-  k_scan_offsets2<<<1, 1024, 0, st>>>(counts, k, offsets_ws, cursor_ws);
-  MASK_LAUNCH_CHECK();
-  k_scatter_members2<<<grid_for(n, 256), 256, 0, st>>>(labels, n, cursor_ws, members_ws);
-  MASK_LAUNCH_CHECK();
-  k_segsum_v4<<<grid_for(k * 32, 256), 256, 0, st>>>(reinterpret_cast<const float4*>(X), d / 4, offsets_ws,
-                                                     members_ws, k, reinterpret_cast<float4*>(S));
-  MASK_LAUNCH_CHECK();
-}
-
-__global__ void __launch_bounds__(1024) k_scan_offsets2(const int32_t* __restrict__ cnt, int64_t k,
-                                                        int64_t* __restrict__ offsets,
-                                                        int32_t* __restrict__ cursor) {
-  __shared__ int64_t warp_tot[32];
-  __shared__ int64_t carry;
-  if (threadIdx.x == 0) carry = 0;
-  __syncthreads();
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (int64_t base = 0; base < k; base += 1024) {
-    const int64_t j = base + threadIdx.x;
-    const int64_t v = j < k ? cnt[j] : 0;
-    int64_t incl = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int64_t t = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += t;
-    }
-    if (lane == 31) warp_tot[w] = incl;
-    __syncthreads();
-    if (w == 0) {
-      const int64_t t = warp_tot[lane];
-      int64_t ti = t;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int64_t u = __shfl_up_sync(0xffffffffu, ti, o);
-        if (lane >= o) ti += u;
-      }
-      warp_tot[lane] = ti - t;
-    }
-    __syncthreads();
-    const int64_t excl = carry + warp_tot[w] + incl - v;
-    if (j < k) {
-      offsets[j] = excl;
-      cursor[j] = (int32_t)excl;
-    }
-    __syncthreads();
-    if (threadIdx.x == 1023) carry = excl + v;
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) offsets[k] = carry;
-}
-
-}  // namespace mask

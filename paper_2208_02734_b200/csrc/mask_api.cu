@@ -80,47 +80,6 @@ namespace {
 
 thread_local std::string g_err;
 
-// CUDA-event timer for one kernel class (MASK_TIME_KERNELS): start/stop recorded on the
-// build stream around the launch, read back at the next stream synchronisation.
-struct KTimer {
-  cudaEvent_t a = nullptr, b = nullptr;
-  bool pending = false;
-  double ms = 0.0;
-  int64_t count = 0;
-  ~KTimer() {
-    if (a) cudaEventDestroy(a);
-    if (b) cudaEventDestroy(b);
-  }
-  void start(cudaStream_t st) {
-    if (!a) {
-      MASK_CUDA(cudaEventCreate(&a));
-      MASK_CUDA(cudaEventCreate(&b));
-    }
-    collect();
-    MASK_CUDA(cudaEventRecord(a, st));
-  }
-  void stop(cudaStream_t st) {
-    MASK_CUDA(cudaEventRecord(b, st));
-    pending = true;
-  }
-  void collect() {
-    if (!pending) return;
-    MASK_CUDA(cudaEventSynchronize(b));
-    float t = 0.f;
-    MASK_CUDA(cudaEventElapsedTime(&t, a, b));
-    ms += t;
-    ++count;
-    pending = false;
-  }
-};
-
-struct Timers {
-  KTimer t[MASK_T_NCLASS];
-  void collect() {
-    for (auto& k : t) k.collect();
-  }
-};
-
 template <class F>
 int32_t guarded(F&& f) {
   try {
@@ -268,66 +227,74 @@ void check_csr_structure(const mask_matrix* m, cudaStream_t st) {
   }
 }
 
-// Update variant: float atomics (default; measured 1.5 TB/s on C2, 3.5 TB/s on C3) or
-// counting-sort + segmented sums (MASK_UPDATE=sorted; deterministic-order sums but slower:
-// 0.42 / 2.2 TB/s, its histogram/scatter counters contend instead).
-bool use_sorted_update(int d, const float* X) {
-  static const int mode = [] {
-    const char* e = getenv("MASK_UPDATE");
-    return (e && std::string(e) == "sorted") ? 1 : 0;
-  }();
-  return mode == 1 && d % 4 == 0 && ((uintptr_t)X % 16) == 0;
-}
-
 // Scratch of one level's Lloyd loop.
 struct LloydWS {
   DevBuf<int32_t> lab_prev, lab_cur;
   DevBuf<float> best;
   DevBuf<float> S;
   DevBuf<int32_t> counts;
-  DevBuf<double> J;
-  DevBuf<unsigned long long> changed;
-  DevBuf<uint32_t> fin;
   DevBuf<float> Pb, Ps, cn2, xn2, PT;
   DevBuf<int32_t> flag_rows, flag_count;
+  DevBuf<unsigned long long> fix_keys;
   bool xn2_ready = false;
   int kernel_id = -1;
-  DevBuf<int64_t> seg_offsets;  // sorted update workspaces
-  DevBuf<int32_t> seg_cursor, seg_members;
-  DevBuf<unsigned long long> fix_keys;
-  int64_t last_flagged = 0;
+};
+
+// CUDA-event pairs recorded around every launch of a kernel class during a level, read once
+// at the end of the level (no synchronisation inside the loop).  Only the first `executed`
+// pairs of a class count (passes skipped on the device after convergence are excluded).
+struct EventLog {
+  std::vector<cudaEvent_t> ev[MASK_T_NCLASS];
+  ~EventLog() {
+    for (auto& v : ev)
+      for (auto e : v) cudaEventDestroy(e);
+  }
+  void mark(int c, cudaStream_t st) {
+    cudaEvent_t e;
+    MASK_CUDA(cudaEventCreate(&e));
+    MASK_CUDA(cudaEventRecord(e, st));
+    ev[c].push_back(e);
+  }
+  // sum of the first `pairs` (start, stop) intervals of class c
+  double total_ms(int c, size_t pairs) const {
+    double ms = 0.0;
+    for (size_t i = 0; i + 1 < ev[c].size() && i / 2 < pairs; i += 2) {
+      float t = 0.f;
+      MASK_CUDA(cudaEventElapsedTime(&t, ev[c][i], ev[c][i + 1]));
+      ms += t;
+    }
+    return ms;
+  }
+  size_t pairs(int c) const { return ev[c].size() / 2; }
 };
 
 // One assignment pass: labels_out[i] = argmin_j ||x_i - c_j||^2, best[i] = its d^2.
-int64_t assign_pass(const Input& in, const float* P, int64_t k, int flags, int32_t* labels_out,
-                    float* best, LloydWS& ws, cudaStream_t st, HostStats* hs, Timers* tm = nullptr) {
+// `active` (device, may be NULL): the pass is a no-op on the device once the level converged.
+void assign_pass(const Input& in, const float* P, int64_t k, int flags, int32_t* labels_out, float* best,
+                 LloydWS& ws, cudaStream_t st, const int* active, EventLog* ev) {
   const int64_t n = in.n_local;
   const int d = in.dim;
-  if (n == 0) return 0;
+  if (n == 0) return;
   if (in.format == MASK_CSR_F32) {
     if (!ws.PT.p) ws.PT.alloc((size_t)k * d);
     if (!ws.cn2.p) ws.cn2.alloc(k);
-    launch_transpose(P, k, d, ws.PT.p, st);
-    launch_level_norms(P, k, d, ws.cn2.p, st);
+    launch_transpose(P, k, d, ws.PT.p, st, active);
+    launch_level_norms(P, k, d, ws.cn2.p, st, active);
     ws.kernel_id = 2;
-    if (tm) tm->t[MASK_T_ASSIGN].start(st);
-    launch_assign_csr(in.rp, in.col, in.val, n, d, ws.PT.p, ws.cn2.p, k, labels_out, best, st);
-    if (tm) tm->t[MASK_T_ASSIGN].stop(st);
-    return 0;
+    if (ev) ev->mark(MASK_T_ASSIGN, st);
+    launch_assign_csr(in.rp, in.col, in.val, n, d, ws.PT.p, ws.cn2.p, k, labels_out, best, st, active);
+    if (ev) ev->mark(MASK_T_ASSIGN, st);
+    return;
   }
-  const bool use_tc = !(flags & MASK_FORCE_SIMT) && tc_supported(n, d, k) &&
-                      ((uintptr_t)in.X % 16 == 0);
+  const bool use_tc = !(flags & MASK_FORCE_SIMT) && tc_supported(n, d, k) && ((uintptr_t)in.X % 16 == 0);
   if (!use_tc) {
     ws.kernel_id = 0;
-    if (tm) tm->t[MASK_T_ASSIGN].start(st);
-    if (d <= 64) {
-      launch_assign_simt(in.X, n, d, P, k, labels_out, best, st);
-    } else {  // large d: dimension-chunked blocked kernel
-      if ((int64_t)ws.fix_keys.n < n) ws.fix_keys.alloc((size_t)n);
-      launch_assign_blocked(in.X, n, d, P, k, ws.fix_keys.p, labels_out, best, st);
-    }
-    if (tm) tm->t[MASK_T_ASSIGN].stop(st);
-    return 0;
+    if (d > 64 && (int64_t)ws.fix_keys.n < n) ws.fix_keys.alloc((size_t)n);
+    if (ev) ev->mark(MASK_T_ASSIGN, st);
+    if (d <= 64) launch_assign_simt(in.X, n, d, P, k, labels_out, best, st, active);
+    else launch_assign_blocked(in.X, n, d, P, k, ws.fix_keys.p, labels_out, best, st, active);  // large d
+    if (ev) ev->mark(MASK_T_ASSIGN, st);
+    return;
   }
   // ||c||^2 is padded with +inf to a whole number of 256-prototype tiles (K1 reads it unmasked)
   const int64_t k_pad = (k + 255) / 256 * 256;
@@ -338,6 +305,7 @@ int64_t assign_pass(const Input& in, const float* P, int64_t k, int flags, int32
     ws.cn2.alloc(k_pad);
     ws.flag_rows.alloc(n);
     ws.flag_count.alloc(1);
+    ws.fix_keys.alloc((size_t)n);
     launch_fill(ws.cn2.p + k, k_pad - k, INFINITY, st);
   }
   if (!ws.xn2_ready) {
@@ -345,33 +313,59 @@ int64_t assign_pass(const Input& in, const float* P, int64_t k, int flags, int32
     launch_row_norms(in.X, n, d, ws.xn2.p, st);
     ws.xn2_ready = true;
   }
-  launch_prep_protos(P, k, d, kc, ws.Pb.p, ws.Ps.p, ws.cn2.p, st, tc_operand_rows(k), d + 2 <= 32 ? 1 : 0);
+  launch_prep_protos(P, k, d, kc, ws.Pb.p, ws.Ps.p, ws.cn2.p, st, tc_operand_rows(k), d + 2 <= 32 ? 1 : 0, active);
   MASK_CUDA(cudaMemsetAsync(ws.flag_count.p, 0, sizeof(int32_t), st));
   ws.kernel_id = 1;
-  if (tm) tm->t[MASK_T_ASSIGN].start(st);
-  launch_assign_tc(in.X, n, d, P, ws.Pb.p, ws.Ps.p, ws.cn2.p, k, ws.xn2.p, labels_out, best,
-                   ws.flag_rows.p, ws.flag_count.p, st);
-  if (tm) tm->t[MASK_T_ASSIGN].stop(st);
-  // near-tie re-check (K4), sized on the device from the flagged count (no host round trip);
-  // the count itself is read back with the pass statistics
+  if (ev) ev->mark(MASK_T_ASSIGN, st);
+  launch_assign_tc(in.X, n, d, P, ws.Pb.p, ws.Ps.p, ws.cn2.p, k, ws.xn2.p, labels_out, best, ws.flag_rows.p,
+                   ws.flag_count.p, st, active);
+  if (ev) ev->mark(MASK_T_ASSIGN, st);
+  // near-tie re-check (K4), sized on the device from the flagged count (no host round trip)
   if (!(flags & MASK_NO_FIXUP)) {
-    if ((int64_t)ws.fix_keys.n < n) ws.fix_keys.alloc((size_t)n);
-    if (tm) tm->t[MASK_T_FIXUP].start(st);
-    launch_fixup_device(in.X, d, P, k, ws.flag_rows.p, ws.flag_count.p, n, ws.fix_keys.p, labels_out, best, st);
-    if (tm) tm->t[MASK_T_FIXUP].stop(st);
+    if (ev) ev->mark(MASK_T_FIXUP, st);
+    launch_fixup_device(in.X, d, P, k, ws.flag_rows.p, ws.flag_count.p, n, ws.fix_keys.p, labels_out, best, st,
+                        active);
+    if (ev) ev->mark(MASK_T_FIXUP, st);
   }
-  if (hs) MASK_CUDA(cudaMemcpyAsync(hs->flags, ws.flag_count.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-  return -1;  // flagged count available in hs->flags after the next stream synchronisation
+}
+
+// ---- device-side loop control (one per level): ctrl[0] = active, ctrl[1] = loop passes run
+__global__ void k_after_stats(int* ctrl, const unsigned long long* changed, int t) {
+  if (!ctrl[0]) return;
+  if (t > 0 && changed[t] == 0) {  // no label changed: the update would be a no-op (stop)
+    ctrl[0] = 0;
+    ctrl[1] = t + 1;
+  }
+}
+__global__ void k_after_update(int* ctrl, const uint32_t* fin, int t, double tol, int T) {
+  if (!ctrl[0]) return;
+  const double disp = sqrt((double)__uint_as_float(fin[2 * t]));
+  if (tol > 0.0 && disp <= tol) {  // D3 tolerance stop
+    ctrl[0] = 0;
+    ctrl[1] = t + 1;
+  } else if (t == T - 1) {
+    ctrl[1] = T;
+  }
+}
+__global__ void k_copy_labels(int32_t* __restrict__ dst, const int32_t* __restrict__ src, int64_t n,
+                              const int* __restrict__ active) {
+  if (active && !*active) return;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = src[i];
 }
 
 // Lloyd k-means for one level (SURVEY §8(c) pseudo-code; mirrors the oracle's order):
 //   P <- init rows; for t < T: a <- assign(P); trace; stop if no label changed (t > 0);
 //   P <- means (empty keeps, D5); stop if tol > 0 and max displacement <= tol;
 //   final assignment -> labels.
+// The whole loop is enqueued at once: the stop tests run on the device (k_after_stats,
+// k_after_update) and later passes become no-ops, so the host synchronises once per level
+// (unless the test-only iteration callback needs host copies after every pass).
 void run_level(const Input& in, int64_t k, const int64_t* init_idx_host, const mask_build_params* p,
                mask_comm* comm, int level_no, cudaStream_t st, Level& L, HostStats& hs) {
   const int d = in.dim;
   const int64_t n = in.n_local;
+  const int T = p->max_iters;
   L.k = k;
   L.dim = d;
   L.P.alloc((size_t)k * d);
@@ -381,127 +375,148 @@ void run_level(const Input& in, int64_t k, const int64_t* init_idx_host, const m
   ws.best.alloc(std::max<int64_t>(n, 1));
   ws.S.alloc((size_t)k * d);
   ws.counts.alloc(k);
-  ws.J.alloc(1);
-  ws.changed.alloc(1);
-  ws.fin.alloc(2);
+  // per-pass statistics (slot T+1 = final pass) and loop control
+  DevBuf<double> Jd(T + 2);
+  DevBuf<unsigned long long> chd(T + 2);
+  DevBuf<uint32_t> fin(2 * (T + 2));
+  DevBuf<int> ctrl(4);
+  MASK_CUDA(cudaMemsetAsync(Jd.p, 0, sizeof(double) * (T + 2), st));
+  MASK_CUDA(cudaMemsetAsync(chd.p, 0, sizeof(unsigned long long) * (T + 2), st));
+  MASK_CUDA(cudaMemsetAsync(fin.p, 0, sizeof(uint32_t) * 2 * (T + 2), st));
+  const int ctrl_init[4] = {1, 0, 0, 0};
+  MASK_CUDA(cudaMemcpyAsync(ctrl.p, ctrl_init, sizeof(ctrl_init), cudaMemcpyHostToDevice, st));
   MASK_CUDA(cudaMemsetAsync(ws.S.p, 0, sizeof(float) * k * d, st));
   MASK_CUDA(cudaMemsetAsync(ws.counts.p, 0, sizeof(int32_t) * k, st));
   MASK_CUDA(cudaMemsetAsync(ws.lab_prev.p, 0xff, sizeof(int32_t) * std::max<int64_t>(n, 1), st));
+  const int* active = ctrl.p;
 
   // ---- seeded init (D2): gather the owned init rows, combine across ranks
-  {
-    DevBuf<int64_t> idx(k);
-    MASK_CUDA(cudaMemcpyAsync(idx.p, init_idx_host, sizeof(int64_t) * k, cudaMemcpyHostToDevice, st));
-    if (in.format == MASK_CSR_F32) {
-      MASK_CUDA(cudaMemsetAsync(L.P.p, 0, sizeof(float) * k * d, st));
-      launch_gather_csr_rows(in.rp, in.col, in.val, d, idx.p, k, in.row_offset, n, L.P.p, st);
-    } else {
-      launch_gather_rows(in.X, d, idx.p, k, in.row_offset, n, L.P.p, st);
-    }
-    if (comm) MASK_NCCL(ncclAllReduce(L.P.p, L.P.p, (size_t)k * d, ncclFloat, ncclSum, comm->comm, st));
-    MASK_CUDA(cudaStreamSynchronize(st));
+  DevBuf<int64_t> idx(k);
+  MASK_CUDA(cudaMemcpyAsync(idx.p, init_idx_host, sizeof(int64_t) * k, cudaMemcpyHostToDevice, st));
+  if (in.format == MASK_CSR_F32) {
+    MASK_CUDA(cudaMemsetAsync(L.P.p, 0, sizeof(float) * k * d, st));
+    launch_gather_csr_rows(in.rp, in.col, in.val, d, idx.p, k, in.row_offset, n, L.P.p, st);
+  } else {
+    launch_gather_rows(in.X, d, idx.p, k, in.row_offset, n, L.P.p, st);
   }
+  if (comm) MASK_NCCL(ncclAllReduce(L.P.p, L.P.p, (size_t)k * d, ncclFloat, ncclSum, comm->comm, st));
 
-  auto emit_cb = [&](int pass, const int32_t* labels_dev) {
-    if (!p->iter_cb) return;
+  std::unique_ptr<EventLog> ev((p->flags & MASK_TIME_KERNELS) ? new EventLog : nullptr);
+
+  // test-only step-parity hook: host copies of the P_t a pass used and the labels it produced
+  auto emit_cb = [&](int pass, const float* P_used, const int32_t* labels_dev) {
     std::vector<float> Ph((size_t)k * d);
     std::vector<int32_t> lh(n);
-    MASK_CUDA(cudaMemcpyAsync(Ph.data(), L.P.p, sizeof(float) * Ph.size(), cudaMemcpyDeviceToHost, st));
+    MASK_CUDA(cudaMemcpyAsync(Ph.data(), P_used, sizeof(float) * Ph.size(), cudaMemcpyDeviceToHost, st));
     if (n) MASK_CUDA(cudaMemcpyAsync(lh.data(), labels_dev, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st));
     MASK_CUDA(cudaStreamSynchronize(st));
     p->iter_cb(level_no, pass, Ph.data(), k, d, lh.data(), n, p->iter_cb_user);
   };
+  DevBuf<float> P_snap;  // P used by the pass (only kept for the callback)
+  if (p->iter_cb) P_snap.alloc((size_t)k * d);
 
-  // pass statistics (J_t, changed_t), combined over ranks; one 16-byte D2H read per pass
-  auto pass_stats = [&](const int32_t* cur, const int32_t* prev) {
-    MASK_CUDA(cudaMemsetAsync(ws.J.p, 0, sizeof(double), st));
-    MASK_CUDA(cudaMemsetAsync(ws.changed.p, 0, sizeof(unsigned long long), st));
-    launch_pass_stats(cur, prev, ws.best.p, n, ws.J.p, ws.changed.p, st);
+  // pass statistics into slot `slot`, combined over ranks (no host round trip)
+  auto pass_stats = [&](int slot, const int* act) {
+    launch_pass_stats(ws.lab_cur.p, ws.lab_prev.p, ws.best.p, n, Jd.p + slot, chd.p + slot, st, act);
     if (comm) {
       MASK_NCCL(ncclGroupStart());
-      MASK_NCCL(ncclAllReduce(ws.J.p, ws.J.p, 1, ncclDouble, ncclSum, comm->comm, st));
-      MASK_NCCL(ncclAllReduce(ws.changed.p, ws.changed.p, 1, ncclUint64, ncclSum, comm->comm, st));
+      MASK_NCCL(ncclAllReduce(Jd.p + slot, Jd.p + slot, 1, ncclDouble, ncclSum, comm->comm, st));
+      MASK_NCCL(ncclAllReduce(chd.p + slot, chd.p + slot, 1, ncclUint64, ncclSum, comm->comm, st));
       MASK_NCCL(ncclGroupEnd());
     }
-    MASK_CUDA(cudaMemcpyAsync(hs.J, ws.J.p, sizeof(double), cudaMemcpyDeviceToHost, st));
-    MASK_CUDA(cudaMemcpyAsync(hs.changed, ws.changed.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
-    MASK_CUDA(cudaStreamSynchronize(st));
-    L.J.push_back(*hs.J);
-    L.changed.push_back((int64_t)*hs.changed);
   };
 
-  const int T = p->max_iters;
-  int updates = 0;
-  Timers timers;
-  Timers* tm = (p->flags & MASK_TIME_KERNELS) ? &timers : nullptr;
-  bool fin_pending = false;  // empties of the last update not yet read back (tol == 0)
-  auto read_fin = [&]() {
-    if (!fin_pending) return;
-    L.empties.push_back((int64_t)hs.fin[1]);
-    fin_pending = false;
-  };
   for (int t = 0; t < T; ++t) {
-    assign_pass(in, L.P.p, k, p->flags, ws.lab_cur.p, ws.best.p, ws, st, &hs, tm);
-    pass_stats(ws.lab_cur.p, ws.lab_prev.p);  // synchronises the stream
-    read_fin();
-    emit_cb(t, ws.lab_cur.p);
-    if (t > 0 && L.changed.back() == 0) {
-      L.empties.push_back(0);
-      break;
+    if (p->iter_cb) MASK_CUDA(cudaMemcpyAsync(P_snap.p, L.P.p, sizeof(float) * k * d, cudaMemcpyDeviceToDevice, st));
+    assign_pass(in, L.P.p, k, p->flags, ws.lab_cur.p, ws.best.p, ws, st, active, ev.get());
+    pass_stats(t, active);
+    k_after_stats<<<1, 1, 0, st>>>(ctrl.p, chd.p, t);
+    MASK_LAUNCH_CHECK();
+    if (p->iter_cb) {  // host view of the control state (test-only path)
+      int h[4];
+      MASK_CUDA(cudaMemcpyAsync(h, ctrl.p, sizeof(h), cudaMemcpyDeviceToHost, st));
+      MASK_CUDA(cudaStreamSynchronize(st));
+      if (h[0] || h[1] == t + 1) emit_cb(t, P_snap.p, ws.lab_cur.p);
+      if (!h[0]) break;
     }
     // ---- update: S_j, n_j (K5/K6) -> allreduce (N1) -> P_j = S_j / n_j (K7)
-    if (tm) tm->t[MASK_T_UPDATE].start(st);
-    if (in.format == MASK_CSR_F32) {
-      launch_update_csr(in.rp, in.col, in.val, n, d, ws.lab_cur.p, ws.S.p, ws.counts.p, st);
-    } else if (use_sorted_update(d, in.X)) {
-      if (!ws.seg_members.p) {
-        ws.seg_offsets.alloc(k + 1);
-        ws.seg_cursor.alloc(k);
-        ws.seg_members.alloc(std::max<int64_t>(n, 1));
-      }
-      launch_update_sorted(in.X, n, d, ws.lab_cur.p, k, ws.S.p, ws.counts.p, ws.seg_offsets.p, ws.seg_cursor.p,
-                           ws.seg_members.p, st);
-    } else {
-      launch_update_dense(in.X, n, d, ws.lab_cur.p, k, ws.S.p, ws.counts.p, st);
-    }
-    if (tm) tm->t[MASK_T_UPDATE].stop(st);
+    if (ev) ev->mark(MASK_T_UPDATE, st);
+    if (in.format == MASK_CSR_F32)
+      launch_update_csr(in.rp, in.col, in.val, n, d, ws.lab_cur.p, ws.S.p, ws.counts.p, st, active);
+    else
+      launch_update_dense(in.X, n, d, ws.lab_cur.p, k, ws.S.p, ws.counts.p, st, active);
+    if (ev) ev->mark(MASK_T_UPDATE, st);
     if (comm) {
       MASK_NCCL(ncclGroupStart());
       MASK_NCCL(ncclAllReduce(ws.S.p, ws.S.p, (size_t)k * d, ncclFloat, ncclSum, comm->comm, st));
       MASK_NCCL(ncclAllReduce(ws.counts.p, ws.counts.p, (size_t)k, ncclInt32, ncclSum, comm->comm, st));
       MASK_NCCL(ncclGroupEnd());
     }
-    MASK_CUDA(cudaMemsetAsync(ws.fin.p, 0, sizeof(uint32_t) * 2, st));
-    if (tm) tm->t[MASK_T_FINALIZE].start(st);
-    launch_finalize(L.P.p, ws.S.p, ws.counts.p, k, d, ws.fin.p, 0, st);
-    if (tm) tm->t[MASK_T_FINALIZE].stop(st);
-    ++updates;
-    std::swap(ws.lab_prev, ws.lab_cur);
-    MASK_CUDA(cudaMemcpyAsync(hs.fin, ws.fin.p, sizeof(uint32_t) * 2, cudaMemcpyDeviceToHost, st));
-    fin_pending = true;
-    if (p->tol > 0.0) {
+    if (ev) ev->mark(MASK_T_FINALIZE, st);
+    launch_finalize(L.P.p, ws.S.p, ws.counts.p, k, d, fin.p + 2 * t, 0, st, active);
+    if (ev) ev->mark(MASK_T_FINALIZE, st);
+    k_copy_labels<<<grid_for(n, 256), 256, 0, st>>>(ws.lab_prev.p, ws.lab_cur.p, n, active);
+    MASK_LAUNCH_CHECK();
+    k_after_update<<<1, 1, 0, st>>>(ctrl.p, fin.p, t, p->tol, T);
+    MASK_LAUNCH_CHECK();
+    if (p->iter_cb) {
+      int h[4];
+      MASK_CUDA(cudaMemcpyAsync(h, ctrl.p, sizeof(h), cudaMemcpyDeviceToHost, st));
       MASK_CUDA(cudaStreamSynchronize(st));
-      float maxdisp2;
-      std::memcpy(&maxdisp2, &hs.fin[0], sizeof(float));
-      read_fin();
-      if (std::sqrt((double)maxdisp2) <= p->tol) break;
+      if (!h[0]) break;
     }
   }
-  // ---- final assignment with the final prototypes (D3)
-  assign_pass(in, L.P.p, k, p->flags, ws.lab_cur.p, ws.best.p, ws, st, &hs, tm);
-  pass_stats(ws.lab_cur.p, ws.lab_prev.p);
-  read_fin();
+  // ---- final assignment with the final prototypes (D3): always runs, stats into slot T+1
+  if (p->iter_cb) MASK_CUDA(cudaMemcpyAsync(P_snap.p, L.P.p, sizeof(float) * k * d, cudaMemcpyDeviceToDevice, st));
+  assign_pass(in, L.P.p, k, p->flags, ws.lab_cur.p, ws.best.p, ws, st, nullptr, ev.get());
+  pass_stats(T + 1, nullptr);
+
+  // ---- one read-back per level: control state and the per-pass trace
+  int h_ctrl[4];
+  std::vector<double> hJ(T + 2);
+  std::vector<unsigned long long> hch(T + 2);
+  std::vector<uint32_t> hfin(2 * (T + 2));
+  MASK_CUDA(cudaMemcpyAsync(h_ctrl, ctrl.p, sizeof(h_ctrl), cudaMemcpyDeviceToHost, st));
+  MASK_CUDA(cudaMemcpyAsync(hJ.data(), Jd.p, sizeof(double) * (T + 2), cudaMemcpyDeviceToHost, st));
+  MASK_CUDA(cudaMemcpyAsync(hch.data(), chd.p, sizeof(unsigned long long) * (T + 2), cudaMemcpyDeviceToHost, st));
+  MASK_CUDA(cudaMemcpyAsync(hfin.data(), fin.p, sizeof(uint32_t) * 2 * (T + 2), cudaMemcpyDeviceToHost, st));
+  MASK_CUDA(cudaStreamSynchronize(st));
+  const int loop_passes = T > 0 ? h_ctrl[1] : 0;  // assignment passes run inside the loop
+  int updates = 0;
+  for (int t = 0; t < loop_passes; ++t) {
+    L.J.push_back(hJ[t]);
+    L.changed.push_back((int64_t)hch[t]);
+    const bool updated = !(t > 0 && hch[t] == 0);  // a no-change pass stops before its update
+    L.empties.push_back(updated ? (int64_t)hfin[2 * t + 1] : 0);
+    updates += updated ? 1 : 0;
+  }
+  L.J.push_back(hJ[T + 1]);
+  L.changed.push_back((int64_t)hch[T + 1]);
   L.empties.push_back(0);
-  emit_cb((int)L.J.size() - 1, ws.lab_cur.p);
   L.updates = updates;
+  if (p->iter_cb) emit_cb(loop_passes, P_snap.p, ws.lab_cur.p);
   L.labels = std::move(ws.lab_cur);
   L.n_items = n;
   L.assign_kernel = ws.kernel_id;
-  if (tm) {
-    tm->collect();
+  if (ev) {
+    // loop launches of a class: one per executed pass (+ the final pass for assign/fixup)
+    const size_t run_assign = (size_t)loop_passes + 1, run_upd = (size_t)updates;
+    const size_t runs[MASK_T_NCLASS] = {run_assign, run_assign, run_upd, run_upd};
     for (int c = 0; c < MASK_T_NCLASS; ++c) {
-      L.t_ms[c] += tm->t[c].ms;
-      L.t_count[c] += tm->t[c].count;
+      const size_t np = ev->pairs(c);
+      if (!np) continue;
+      // the final pass's pair is the last one recorded; loop pairs are the first ones
+      size_t loop_pairs = (c <= MASK_T_FIXUP) ? std::min(np - 1, runs[c] - 1) : std::min(np, runs[c]);
+      double ms = ev->total_ms(c, loop_pairs);
+      int64_t cnt = (int64_t)loop_pairs;
+      if (c <= MASK_T_FIXUP) {  // add the final pass
+        float t = 0.f;
+        MASK_CUDA(cudaEventElapsedTime(&t, ev->ev[c][2 * (np - 1)], ev->ev[c][2 * (np - 1) + 1]));
+        ms += t;
+        cnt += 1;
+      }
+      L.t_ms[c] += ms;
+      L.t_count[c] += cnt;
     }
   }
 }
@@ -920,7 +935,9 @@ int32_t mask_assign(const mask_matrix* data, const float* P, int64_t k, int32_t 
     }
     HostStats hs;
     *hs.flags = 0;
-    assign_pass(in, P, k, flags, labels_out, best, ws, st, &hs);
+    assign_pass(in, P, k, flags, labels_out, best, ws, st, nullptr, nullptr);
+    if (ws.flag_count.p)
+      MASK_CUDA(cudaMemcpyAsync(hs.flags, ws.flag_count.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
     MASK_CUDA(cudaStreamSynchronize(st));
     if (n_flagged) *n_flagged = *hs.flags;
   });
