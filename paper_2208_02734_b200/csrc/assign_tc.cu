@@ -579,6 +579,312 @@ __global__ void __launch_bounds__(128 + 128 * EPI_WG, 1)
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// Persistent variant for the folded (small-d) case.  One CTA per SM walks row blocks
+// rb = blockIdx.x, blockIdx.x + gridDim.x, ...  A dedicated loader warpgroup stages the next
+// block's A (split, folded columns) into the second of two TMEM A buffers while the current
+// block's tiles run, so the per-block prologue (A load) and tail (merge, exact d^2, flags)
+// overlap the tensor-core work instead of idling the SM.  Warps: 0 TMA producer, 1 MMA issuer,
+// 2 TMEM allocator, 4-7 A loader, 8.. epilogue warpgroups.
+template <int KA, int BN, int STAGES, int NACC, int EPI_WG>
+struct PCfg {
+  static constexpr int CW = 32, CWB = 128;
+  static constexpr int B_CHUNK = BN * CWB;
+  static constexpr int STAGE_BYTES = 2 * B_CHUNK;
+  static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
+  static constexpr int NBARS = 2 * STAGES + 2 * NACC + 4;
+  static constexpr int SCRATCH_OFF = BAR_OFF + NBARS * 8 + 16;
+  static constexpr int SCRATCH_FLOATS = 2 * 3 * BM * (EPI_WG > 1 ? EPI_WG - 1 : 1);  // double-buffered
+  static constexpr int SMEM = SCRATCH_OFF + SCRATCH_FLOATS * 4 + 1024;
+  static constexpr int A_COL = NACC * BN;  // A buffer b: big at A_COL + 2*KA*b, small at + KA
+  static constexpr int NEED = A_COL + 4 * KA;
+  static constexpr int TMEM_COLS = NEED <= 256 ? 256 : 512;
+  static constexpr uint32_t IDESC = idesc_tf32<BM, BN>();
+  static constexpr int NTHREADS = 256 + 128 * EPI_WG;
+  static constexpr int EPI0 = 8;  // first epilogue warp
+  static_assert(NEED <= 512, "TMEM budget");
+  static_assert(KA % 8 == 0 && KA <= CW, "folded K fits one chunk");
+  static_assert(SMEM <= 232448, "shared memory budget");
+};
+
+template <int KA, int BN, int STAGES, int NACC, int EPI_WG>
+__global__ void __launch_bounds__(256 + 128 * EPI_WG, 1)
+    k_assign_tc_persist(const __grid_constant__ CUtensorMap tmBb, const __grid_constant__ CUtensorMap tmBs,
+                        const float* __restrict__ X, const float* __restrict__ P, const float* __restrict__ cn2,
+                        const float* __restrict__ xn2, int64_t n, int d, int64_t k, int32_t* __restrict__ labels,
+                        float* __restrict__ best, int32_t* __restrict__ flag_rows, int32_t* __restrict__ flag_count,
+                        float err_coef, uint32_t key_mask, const int* __restrict__ active) {
+  if (active && !*active) return;  // level converged: this pass is skipped on the device
+  using C = PCfg<KA, BN, STAGES, NACC, EPI_WG>;
+  constexpr int COLS = BN / EPI_WG;
+  static_assert(COLS % 32 == 0, "epilogue chunking");
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* Bst = smem;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + STAGES;
+  uint64_t* tfull = bars + 2 * STAGES;
+  uint64_t* tempty = bars + 2 * STAGES + NACC;
+  uint64_t* afull = bars + 2 * STAGES + 2 * NACC;
+  uint64_t* aempty = afull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::NBARS);
+  float* scratch = reinterpret_cast<float*>(smem + C::SCRATCH_OFF);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ntiles = (int)((k + BN - 1) / BN);
+  const int64_t nblocks = (n + BM - 1) / BM;
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tmBb);
+    prefetch_tmap(&tmBs);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < NACC; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 128 * EPI_WG);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&afull[a], 128);
+      mbar_init(&aempty[a], 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(C::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer (B)
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int64_t rb = blockIdx.x; rb < nblocks; rb += gridDim.x) {
+        for (int t = 0; t < ntiles; ++t) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* dst = Bst + stage * C::STAGE_BYTES;
+          mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
+          tma_load_2d(dst, &tmBb, &full[stage], 0, t * BN);
+          tma_load_2d(dst + C::B_CHUNK, &tmBs, &full[stage], 0, t * BN);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    int stage = 0;
+    uint32_t phase = 0;
+    int64_t g = 0;  // global tile counter of this CTA
+    int i = 0;      // block iteration of this CTA
+    for (int64_t rb = blockIdx.x; rb < nblocks; rb += gridDim.x, ++i) {
+      const int ab = i & 1;
+      mbar_wait(&afull[ab], (i >> 1) & 1);
+      tc_fence_after();
+      const uint32_t a_big = tmem_base + C::A_COL + 2 * KA * ab, a_small = a_big + KA;
+      for (int t = 0; t < ntiles; ++t, ++g) {
+        const int acc = (int)(g % NACC);
+        mbar_wait(&tempty[acc], ((g / NACC) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t bb = smem_u32(Bst + stage * C::STAGE_BYTES);
+          const uint32_t bs = bb + C::B_CHUNK;
+#pragma unroll
+          for (int ks = 0; ks < KA / 8; ++ks) {
+            const uint64_t dbb = smem_desc<C::CWB>(bb + ks * 32), dbs = smem_desc<C::CWB>(bs + ks * 32);
+            mma_tf32_ts(d_tmem, a_small + ks * 8, dbb, C::IDESC, ks != 0);
+            mma_tf32_ts(d_tmem, a_big + ks * 8, dbs, C::IDESC, 1u);
+            mma_tf32_ts(d_tmem, a_big + ks * 8, dbb, C::IDESC, 1u);
+          }
+          mma_commit(&empty[stage]);
+          mma_commit(&tfull[acc]);
+          if (t == ntiles - 1) mma_commit(&aempty[ab]);  // this block's A may be overwritten
+        }
+        __syncwarp();
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else if (warp >= 4 && warp < C::EPI0) {
+    // ------------------------------------------------------------ A loader (one thread per row)
+    const int q = warp & 3;
+    const int rloc = q * 32 + lane;
+    const uint32_t lane_base = tmem_base + ((uint32_t)(q * 32) << 16);
+    int i = 0;
+    for (int64_t rb = blockIdx.x; rb < nblocks; rb += gridDim.x, ++i) {
+      const int ab = i & 1;
+      mbar_wait(&aempty[ab], ((i >> 1) & 1) ^ 1);
+      tc_fence_after();
+      const int64_t row = rb * BM + rloc;
+      const float xx = row < n ? __ldg(xn2 + row) : 0.f;
+      const float* xr = X + row * d;
+      const uint32_t a_big = lane_base + C::A_COL + 2 * KA * ab, a_small = a_big + KA;
+#pragma unroll
+      for (int g8 = 0; g8 < KA; g8 += 8) {
+        uint32_t vb[8], vs[8];
+#pragma unroll
+        for (int u = 0; u < 8; u += 4) {
+          const int col = g8 + u;
+          float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (row < n && col < d) v = __ldg(reinterpret_cast<const float4*>(xr + col));
+          const float e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+          for (int w = 0; w < 4; ++w) {
+            float x = e[w];
+            if (col + w == d) x = 1.0f;         // pairs with ||c||^2 in B
+            else if (col + w == d + 1) x = xx;  // pairs with 1 in B
+            const float b = tf32_rn(x);
+            vb[u + w] = __float_as_uint(b);
+            vs[u + w] = __float_as_uint(tf32_rn(x - b));
+          }
+        }
+        tmem_st8(a_big + g8, vb);
+        tmem_st8(a_small + g8, vs);
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(&afull[ab]);
+    }
+  } else if (warp >= C::EPI0) {
+    // ------------------------------------------------------------ epilogue warpgroups
+    constexpr int NEPI = 128 * EPI_WG;
+    const int et = threadIdx.x - C::EPI0 * 32;
+    const int wg = et >> 7;
+    const int q = warp & 3;
+    const int rloc = q * 32 + lane;
+    int64_t g = 0;
+    int i = 0;
+    for (int64_t rb = blockIdx.x; rb < nblocks; rb += gridDim.x, ++i) {
+      const int64_t row = rb * BM + rloc;
+      float g1 = INFINITY, g2 = INFINITY;
+      int32_t gi = 0x7fffffff;
+      for (int t = 0; t < ntiles; ++t, ++g) {
+        const int acc = (int)(g % NACC);
+        mbar_wait(&tfull[acc], (g / NACC) & 1);
+        tc_fence_after();
+        const int col0 = wg * COLS;
+        const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + col0);
+        int32_t b1[MASK_TC_CHAINS], b2[MASK_TC_CHAINS];
+#pragma unroll
+        for (int u = 0; u < MASK_TC_CHAINS; ++u) b1[u] = b2[u] = 0x7fffffff;
+        uint32_t r[2][32];
+        tmem_ld32(tbase, r[0]);
+#pragma unroll
+        for (int cc = 0; cc < COLS / 32; ++cc) {
+          tmem_wait_ld();
+          if (cc + 1 < COLS / 32) tmem_ld32(tbase + (cc + 1) * 32, r[(cc + 1) & 1]);
+#pragma unroll
+          for (int e = 0; e < 32; e += 2) {
+            // key = (bits & ~0xFF) | column (one LOP3; mask in a register, column immediate)
+            int32_t ka, kb;
+            asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(ka) : "r"(r[cc & 1][e]), "r"(key_mask), "r"((uint32_t)(cc * 32 + e)));
+            asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(kb) : "r"(r[cc & 1][e + 1]), "r"(key_mask), "r"((uint32_t)(cc * 32 + e + 1)));
+            const int u = (e >> 1) & (MASK_TC_CHAINS - 1);
+            const int32_t m = imin(ka, kb), M = imax(ka, kb);
+            const int32_t t2 = imax(b1[u], m);
+            b1[u] = imin(b1[u], m);
+            b2[u] = imin(imin(b2[u], M), t2);
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(&tempty[acc]);
+        int32_t k1 = b1[0];
+#pragma unroll
+        for (int u = 1; u < MASK_TC_CHAINS; ++u) k1 = imin(k1, b1[u]);
+        int32_t k2 = 0x7fffffff;
+#pragma unroll
+        for (int u = 0; u < MASK_TC_CHAINS; ++u) k2 = imin(k2, b1[u] == k1 ? b2[u] : b1[u]);
+        const float v1 = __int_as_float(k1 & 0xFFFFFF00), v2 = __int_as_float(k2 & 0xFFFFFF00);
+        if (v1 < g1) {  // strict: ties keep the earlier tile (lower prototype index)
+          g2 = fminf(g1, v2);
+          g1 = v1;
+          gi = t * BN + col0 + (k1 & 0xFF);
+        } else {
+          g2 = fminf(g2, v1);
+        }
+      }
+      if (EPI_WG > 1) {  // merge the warpgroups' results (double-buffered scratch by block parity)
+        float* mg1 = scratch + (i & 1) * 3 * BM * (EPI_WG - 1);
+        float* mg2 = mg1 + (EPI_WG - 1) * BM;
+        int32_t* mgi = reinterpret_cast<int32_t*>(mg2 + (EPI_WG - 1) * BM);
+        if (wg > 0) {
+          mg1[(wg - 1) * BM + rloc] = g1;
+          mg2[(wg - 1) * BM + rloc] = g2;
+          mgi[(wg - 1) * BM + rloc] = gi;
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(NEPI) : "memory");
+        if (wg == 0) {
+#pragma unroll
+          for (int w = 0; w < EPI_WG - 1; ++w) {
+            const float o1 = mg1[w * BM + rloc], o2 = mg2[w * BM + rloc];
+            const int32_t oi = mgi[w * BM + rloc];
+            if (o1 < g1 || (o1 == g1 && oi < gi)) {
+              g2 = fminf(g1, o2);
+              g1 = o1;
+              gi = oi;
+            } else {
+              g2 = fminf(g2, o1);
+            }
+          }
+        }
+      }
+      if (wg == 0) {
+        bool flag = false;
+        if (row < n) {
+          labels[row] = gi;
+          const float* xr = X + row * d;
+          const float* cr = P + (int64_t)gi * d;
+          float dd = 0.f;
+          for (int c = 0; c < d; c += 4) {
+            const float4 xv = __ldg(reinterpret_cast<const float4*>(xr + c));
+            const float4 cv = __ldg(reinterpret_cast<const float4*>(cr + c));
+            float tt = xv.x - cv.x;
+            dd = fmaf(tt, tt, dd);
+            tt = xv.y - cv.y;
+            dd = fmaf(tt, tt, dd);
+            tt = xv.z - cv.z;
+            dd = fmaf(tt, tt, dd);
+            tt = xv.w - cv.w;
+            dd = fmaf(tt, tt, dd);
+          }
+          best[row] = dd;
+          const float xx = __ldg(xn2 + row);
+          const float thr = err_coef * (xx + __ldg(cn2 + gi)) + ldexpf(fmaxf(fabsf(g2), fabsf(g1)), -14);
+          flag = (g2 - g1) <= thr;
+        }
+        const unsigned msk = __ballot_sync(0xffffffffu, flag);
+        if (msk) {
+          int base = 0;
+          if (lane == 0) base = atomicAdd(flag_count, __popc(msk));
+          base = __shfl_sync(0xffffffffu, base, 0);
+          if (flag) flag_rows[base + __popc(msk & ((1u << lane) - 1))] = (int32_t)row;
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(C::TMEM_COLS));
+  }
+}
+
 // Host dump of the development trace: per-phase medians (us) over the traced CTAs.
 void dump_trace(int nctas) {
   static long long h[8][kTraceCtas];
@@ -672,6 +978,26 @@ void launch_cfg(const float* X, int64_t n, int d, int kc, int64_t k_rows, const 
   if (tc_debug_mode() & 8) dump_trace((int)grid);
 }
 
+template <int KA, int BN, int STAGES, int NACC, int EPI_WG>
+void launch_persist(const float* X, int64_t n, int d, int kc, int64_t k_rows, const float* P, const float* Pb,
+                    const float* Ps, const float* cn2, int64_t k, const float* xn2, int32_t* labels, float* best,
+                    int32_t* flag_rows, int32_t* flag_count, float err_coef, cudaStream_t st, const int* active) {
+  using C = PCfg<KA, BN, STAGES, NACC, EPI_WG>;
+  const CUtensorMap tBb = make_map(Pb, k_rows, kc, C::CW, BN);
+  const CUtensorMap tBs = make_map(Ps, k_rows, kc, C::CW, BN);
+  auto kern = k_assign_tc_persist<KA, BN, STAGES, NACC, EPI_WG>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    MASK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    attr_set = true;
+  }
+  const int64_t nblocks = (n + BM - 1) / BM;
+  const unsigned grid = (unsigned)(nblocks < num_sms() ? nblocks : num_sms());
+  kern<<<grid, C::NTHREADS, C::SMEM, st>>>(tBb, tBs, X, P, cn2, xn2, n, d, k, labels, best, flag_rows, flag_count,
+                                           err_coef, 0xFFFFFF00u, active);
+  MASK_LAUNCH_CHECK();
+}
+
 }  // namespace tc
 
 bool tc_supported(int64_t n, int d, int64_t k) {
@@ -706,7 +1032,20 @@ void launch_assign_tc(const float* X, int64_t n, int d, const float* P, const fl
   const int64_t kr = tc_operand_rows(k);
   // small d (FOLD): epilogue-bound; 192-prototype tiles, two TMEM accumulators (2 x 192 + 2 x
   // KA columns), three epilogue warpgroups of 64 columns (best of the measured variants)
-  if (d + 2 <= 24)
+  static const int persist = [] {
+    const char* e = getenv("MASK_TC_PERSIST");  // development switch (default: persistent)
+    return e ? atoi(e) : 1;
+  }();
+#ifndef MASK_TC_P_BN
+#define MASK_TC_P_BN 192
+#define MASK_TC_P_STAGES 4
+#define MASK_TC_P_NACC 2
+#define MASK_TC_P_EPI 3
+#endif
+  if (d + 2 <= 24 && persist)
+    tc::launch_persist<24, MASK_TC_P_BN, MASK_TC_P_STAGES, MASK_TC_P_NACC, MASK_TC_P_EPI>(
+        X, n, d, kc, kr, P, Pb, Ps, cn2, k, xn2, labels, best, flag_rows, flag_count, coef, st, active);
+  else if (d + 2 <= 24)
     tc::launch_cfg<32, 1, 24, 192, 4, 2, true, 3>(X, n, d, kc, kr, P, Pb, Ps, cn2, k, xn2, labels, best, flag_rows,
                                                   flag_count, coef, st, active);
   else if (d + 2 <= 32)
