@@ -69,6 +69,20 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
+// Consumer release by whole warps: each thread fences its own tcgen05 ops
+// (fence::before_thread_sync), the warp synchronises, and one elected lane arrives, so a
+// release costs one shared-memory arrive per warp instead of 32 (barrier counts are per warp).
+#if defined(MASK_TC_THREAD_ARRIVE)
+constexpr int kArrivePerWarp = 32;
+__device__ __forceinline__ void mbar_arrive_warp(uint64_t* bar) { mbar_arrive(bar); }
+#else
+constexpr int kArrivePerWarp = 1;
+__device__ __forceinline__ void mbar_arrive_warp(uint64_t* bar) {
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) mbar_arrive(bar);
+}
+#endif
+
 __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
   uint32_t ok;
   asm volatile(
@@ -79,12 +93,42 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
   return ok != 0;
 }
 
+// try_wait with a suspend-time hint: the waiting thread is parked by the hardware until the
+// phase completes (or the hint elapses) instead of re-issuing the test on the ALU pipe that the
+// epilogue warps are bound by
+__device__ __forceinline__ bool mbar_try_wait_hint(uint32_t addr, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n selp.u32 %0, 1, 0, p;\n}"
+      : "=r"(ok)
+      : "r"(addr), "r"(parity), "r"(1000000u)
+      : "memory");
+  return ok != 0;
+}
+
 // Bounded wait: a pipeline bug traps (kernel error) instead of hanging the GPU.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t addr = smem_u32(bar);
   uint64_t spins = 0;
+#if defined(MASK_TC_SPIN_WAIT)
   while (!mbar_try_wait(addr, parity)) {
+#else
+  while (!mbar_try_wait_hint(addr, parity)) {
+#endif
     if (++spins > (1ull << 26)) __trap();
+  }
+}
+
+// Wait off the critical path (the A loader, a whole block of tiles ahead): back off with
+// __nanosleep between tests so the spin does not take issue slots from the epilogue.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  const uint32_t addr = smem_u32(bar);
+  uint32_t spins = 0;
+  while (!mbar_try_wait(addr, parity)) {
+#if !defined(MASK_TC_SPIN_WAIT)
+    __nanosleep(200);
+#endif
+    if (++spins > (1u << 26)) __trap();
   }
 }
 
@@ -191,6 +235,47 @@ __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.
 
 __device__ __forceinline__ int32_t imin(int32_t a, int32_t b) { return a < b ? a : b; }
 __device__ __forceinline__ int32_t imax(int32_t a, int32_t b) { return a > b ? a : b; }
+__device__ __forceinline__ uint32_t umin(uint32_t a, uint32_t b) { return a < b ? a : b; }
+
+// Top-2 of one 32-column chunk of packed keys (bits & mask) | column, in two passes over the
+// registers instead of a running top-2 per element (K1 "epilogue"):
+//   pass 1: c1 = min_e key_e                                    (3-input mins: 1 ALU op / 2 keys)
+//   pass 2: c2 = c1 + 1 + min_e (key_e - c1 - 1) as unsigned    (the minimum itself wraps to
+//           0xFFFFFFFF; keys are distinct because they carry the column, so this is the
+//           second-smallest key exactly)
+// The subtraction is an IMAD (key * one + ~c1, `one` = 1 from a register the compiler cannot
+// fold) so it issues on the FMA pipe: the ALU pipe sees 1 LOP3 + 1 three-input min per key,
+// against 1 LOP3 + 2.5 min/max per key for the running top-2.
+__device__ __forceinline__ void chunk_top2(uint32_t* r, uint32_t mask, uint32_t colbase, uint32_t one, int32_t& c1,
+                                           int32_t& c2) {
+#pragma unroll
+  for (int e = 0; e < 32; ++e)
+    asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(r[e]) : "r"(r[e]), "r"(mask), "r"(colbase + (uint32_t)e));
+  int32_t m[11];
+#pragma unroll
+  for (int j = 0; j < 10; ++j)
+    m[j] = imin(imin((int32_t)r[3 * j], (int32_t)r[3 * j + 1]), (int32_t)r[3 * j + 2]);
+  m[10] = imin((int32_t)r[30], (int32_t)r[31]);
+  const int32_t a = imin(imin(m[0], m[1]), m[2]), b = imin(imin(m[3], m[4]), m[5]);
+  const int32_t c = imin(imin(m[6], m[7]), m[8]), dd = imin(m[9], m[10]);
+  c1 = imin(imin(a, b), imin(c, dd));
+  const uint32_t nc = ~(uint32_t)c1;  // -(c1 + 1)
+#pragma unroll
+  for (int e = 0; e < 32; ++e) asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r[e]) : "r"(r[e]), "r"(one), "r"(nc));
+  uint32_t w[11];
+#pragma unroll
+  for (int j = 0; j < 10; ++j) w[j] = umin(umin(r[3 * j], r[3 * j + 1]), r[3 * j + 2]);
+  w[10] = umin(r[30], r[31]);
+  const uint32_t ua = umin(umin(w[0], w[1]), w[2]), ub = umin(umin(w[3], w[4]), w[5]);
+  const uint32_t uc = umin(umin(w[6], w[7]), w[8]), ud = umin(w[9], w[10]);
+  c2 = (int32_t)(umin(umin(ua, ub), umin(uc, ud)) - nc);
+}
+
+// merge a chunk's (c1 < c2) into a running (b1 <= b2)
+__device__ __forceinline__ void merge_top2(int32_t& b1, int32_t& b2, int32_t c1, int32_t c2) {
+  b2 = imin(imin(b2, c2), imax(b1, c1));
+  b1 = imin(b1, c1);
+}
 
 // development trace (MASK_TC_DEBUG bit 8): %globaltimer stamps of the first CTAs
 constexpr int kTraceCtas = 4096;
@@ -265,9 +350,9 @@ __global__ void __launch_bounds__(128 + 128 * EPI_WG, 1)
     }
     for (int a = 0; a < NACC; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 128 * EPI_WG);
+      mbar_init(&tempty[a], 4 * EPI_WG * kArrivePerWarp);
     }
-    mbar_init(a_ready, 128);
+    mbar_init(a_ready, 4 * kArrivePerWarp);
     fence_barrier_init();
   }
   if (warp == 2) {
@@ -382,7 +467,7 @@ __global__ void __launch_bounds__(128 + 128 * EPI_WG, 1)
       }
       tmem_wait_st();
       tc_fence_before();
-      mbar_arrive(a_ready);
+      mbar_arrive_warp(a_ready);
     }
     if (tr0) g_tc_trace[2][blockIdx.x] = gtimer();
 
@@ -404,11 +489,27 @@ __global__ void __launch_bounds__(128 + 128 * EPI_WG, 1)
       if (FOLD) {
         // packed keys: (float bits >> 8) * 256 + column (two IMADs on the FMA pipe); signed-int
         // order = value order for values >= 0, ties -> lower column
+        if (!no_ld) tmem_ld32(tbase, r[0]);
+#if !defined(MASK_TC_TOP2_RUNNING) && !defined(MASK_TC_KEY_IMAD)
+        int32_t k1 = 0x7fffffff, k2 = 0x7fffffff;
+#pragma unroll
+        for (int cc = 0; cc < COLS / 32; ++cc) {
+          if (!no_ld) {
+            tmem_wait_ld();
+            if (cc + 1 < COLS / 32) tmem_ld32(tbase + (cc + 1) * 32, r[(cc + 1) & 1]);
+          }
+          if (dbg & 1) continue;  // ablation: no epilogue arithmetic
+          int32_t c1, c2;
+          chunk_top2(r[cc & 1], ~(key_lo_mul - 1u), (uint32_t)(cc * 32), key_lo_mul >> 8, c1, c2);
+          merge_top2(k1, k2, c1, c2);
+        }
+        tc_fence_before();
+        mbar_arrive_warp(&tempty[acc]);
+#else
         constexpr int NCH = MASK_TC_CHAINS;
         int32_t b1[NCH], b2[NCH];
 #pragma unroll
         for (int u = 0; u < NCH; ++u) b1[u] = b2[u] = 0x7fffffff;
-        if (!no_ld) tmem_ld32(tbase, r[0]);
 #pragma unroll
         for (int cc = 0; cc < COLS / 32; ++cc) {
           if (!no_ld) {
@@ -440,13 +541,14 @@ __global__ void __launch_bounds__(128 + 128 * EPI_WG, 1)
           }
         }
         tc_fence_before();
-        mbar_arrive(&tempty[acc]);
+        mbar_arrive_warp(&tempty[acc]);
         int32_t k1 = b1[0];
 #pragma unroll
         for (int u = 1; u < NCH; ++u) k1 = imin(k1, b1[u]);
         int32_t k2 = 0x7fffffff;
 #pragma unroll
         for (int u = 0; u < NCH; ++u) k2 = imin(k2, b1[u] == k1 ? b2[u] : b1[u]);
+#endif
         v1 = __int_as_float(k1 & 0xFFFFFF00);
         v2 = __int_as_float(k2 & 0xFFFFFF00);
         j1 = col0 + (k1 & 0xFF);
@@ -482,7 +584,7 @@ __global__ void __launch_bounds__(128 + 128 * EPI_WG, 1)
           }
         }
         tc_fence_before();
-        mbar_arrive(&tempty[acc]);
+        mbar_arrive_warp(&tempty[acc]);
         v1 = b1[0];
         j1 = i1[0];
 #pragma unroll
@@ -644,10 +746,10 @@ __global__ void __launch_bounds__(256 + 128 * EPI_WG, 1)
     }
     for (int a = 0; a < NACC; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 128 * EPI_WG);
+      mbar_init(&tempty[a], 4 * EPI_WG * kArrivePerWarp);
     }
     for (int a = 0; a < 2; ++a) {
-      mbar_init(&afull[a], 128);
+      mbar_init(&afull[a], 4 * kArrivePerWarp);
       mbar_init(&aempty[a], 1);
     }
     fence_barrier_init();
@@ -728,7 +830,7 @@ __global__ void __launch_bounds__(256 + 128 * EPI_WG, 1)
     int i = 0;
     for (int64_t rb = blockIdx.x; rb < nblocks; rb += gridDim.x, ++i) {
       const int ab = i & 1;
-      mbar_wait(&aempty[ab], ((i >> 1) & 1) ^ 1);
+      mbar_wait_sleep(&aempty[ab], ((i >> 1) & 1) ^ 1);
       tc_fence_after();
       const int64_t row = rb * BM + rloc;
       const float xx = row < n ? __ldg(xn2 + row) : 0.f;
@@ -758,7 +860,7 @@ __global__ void __launch_bounds__(256 + 128 * EPI_WG, 1)
       }
       tmem_wait_st();
       tc_fence_before();
-      mbar_arrive(&afull[ab]);
+      mbar_arrive_warp(&afull[ab]);
     }
   } else if (warp >= C::EPI0) {
     // ------------------------------------------------------------ epilogue warpgroups
@@ -779,11 +881,24 @@ __global__ void __launch_bounds__(256 + 128 * EPI_WG, 1)
         tc_fence_after();
         const int col0 = wg * COLS;
         const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + col0);
+        uint32_t r[2][32];
+        tmem_ld32(tbase, r[0]);
+#if !defined(MASK_TC_TOP2_RUNNING)
+        int32_t k1 = 0x7fffffff, k2 = 0x7fffffff;
+#pragma unroll
+        for (int cc = 0; cc < COLS / 32; ++cc) {
+          tmem_wait_ld();
+          if (cc + 1 < COLS / 32) tmem_ld32(tbase + (cc + 1) * 32, r[(cc + 1) & 1]);
+          int32_t c1, c2;
+          chunk_top2(r[cc & 1], key_mask, (uint32_t)(cc * 32), key_mask >> 31, c1, c2);
+          merge_top2(k1, k2, c1, c2);
+        }
+        tc_fence_before();
+        mbar_arrive_warp(&tempty[acc]);
+#else
         int32_t b1[MASK_TC_CHAINS], b2[MASK_TC_CHAINS];
 #pragma unroll
         for (int u = 0; u < MASK_TC_CHAINS; ++u) b1[u] = b2[u] = 0x7fffffff;
-        uint32_t r[2][32];
-        tmem_ld32(tbase, r[0]);
 #pragma unroll
         for (int cc = 0; cc < COLS / 32; ++cc) {
           tmem_wait_ld();
@@ -802,13 +917,14 @@ __global__ void __launch_bounds__(256 + 128 * EPI_WG, 1)
           }
         }
         tc_fence_before();
-        mbar_arrive(&tempty[acc]);
+        mbar_arrive_warp(&tempty[acc]);
         int32_t k1 = b1[0];
 #pragma unroll
         for (int u = 1; u < MASK_TC_CHAINS; ++u) k1 = imin(k1, b1[u]);
         int32_t k2 = 0x7fffffff;
 #pragma unroll
         for (int u = 0; u < MASK_TC_CHAINS; ++u) k2 = imin(k2, b1[u] == k1 ? b2[u] : b1[u]);
+#endif
         const float v1 = __int_as_float(k1 & 0xFFFFFF00), v2 = __int_as_float(k2 & 0xFFFFFF00);
         if (v1 < g1) {  // strict: ties keep the earlier tile (lower prototype index)
           g2 = fminf(g1, v2);
