@@ -62,7 +62,8 @@ enum {
   MASK_FORCE_SIMT = 1 << 2,      /* dense assignment on the FP32 SIMT kernel only (testing) */
   MASK_NO_FIXUP = 1 << 3,        /* disable the near-tie re-check of the tensor path (testing)*/
   MASK_SYNC_STATS = 1 << 4,      /* reserved: J/changed are read every pass (always on)       */
-  MASK_TIME_KERNELS = 1 << 5     /* record CUDA-event device times of the step kernels        */
+  MASK_TIME_KERNELS = 1 << 5,    /* record CUDA-event device times of the step kernels        */
+  MASK_NO_SORT = 1 << 6          /* small d: keep the data order in K1 (no per-pass label sort) */
 };
 
 /* kernel classes of mask_get_timing */

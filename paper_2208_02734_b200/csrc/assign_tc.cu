@@ -40,10 +40,6 @@
 
 #include "common.cuh"
 
-// independent top-2 chains per thread in the packed-key epilogue (ILP)
-#ifndef MASK_TC_CHAINS
-#define MASK_TC_CHAINS 4
-#endif
 
 namespace mask {
 
@@ -116,6 +112,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   while (!mbar_try_wait_hint(addr, parity)) {
 #endif
     if (++spins > (1ull << 26)) __trap();
+  }
+}
+
+// Wait on the MMA issuer's / TMA producer's critical path: plain try_wait polling (the
+// suspend-hinted form adds ~100 cycles of wake-up latency per wait, which the per-tile control
+// path of a short-K tile cannot hide behind the tensor core's instruction queue).
+__device__ __forceinline__ void mbar_wait_spin(uint64_t* bar, uint32_t parity) {
+  const uint32_t addr = smem_u32(bar);
+  uint32_t spins = 0;
+  while (!mbar_try_wait(addr, parity)) {
+    if (++spins > (1u << 28)) __trap();
   }
 }
 
@@ -280,6 +287,9 @@ __device__ __forceinline__ void merge_top2(int32_t& b1, int32_t& b2, int32_t c1,
 // development trace (MASK_TC_DEBUG bit 8): %globaltimer stamps of the first CTAs
 constexpr int kTraceCtas = 4096;
 __device__ long long g_tc_trace[8][kTraceCtas];
+constexpr int kPT = 512;
+__device__ long long g_pt[9][kPT];
+__device__ unsigned long long g_chunk_stats[4];  // debug bit 128: chunks seen / keyed
 __device__ __forceinline__ long long gtimer() {
   long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -320,7 +330,7 @@ __global__ void __launch_bounds__(128 + 128 * EPI_WG, 1)
                 const float* __restrict__ X, const float* __restrict__ P, const float* __restrict__ cn2,
                 const float* __restrict__ xn2, int64_t n, int d, int64_t k, int32_t* __restrict__ labels,
                 float* __restrict__ best, int32_t* __restrict__ flag_rows, int32_t* __restrict__ flag_count,
-                float err_coef, uint32_t key_hi_mul, uint32_t key_lo_mul, int dbg,
+                float err_coef, int dbg,
                 const int* __restrict__ active) {
   if (active && !*active) return;  // level converged: this pass is skipped on the device
   using C = Cfg<CW, NKC, KA, BN, STAGES, NACC, FOLD, EPI_WG>;
@@ -373,7 +383,7 @@ __global__ void __launch_bounds__(128 + 128 * EPI_WG, 1)
       uint32_t phase = 0;
       for (int t = 0; t < ntiles; ++t) {
         for (int c = 0; c < NKC; ++c) {
-          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_wait_spin(&empty[stage], phase ^ 1);
           uint8_t* dst = Bst + stage * C::STAGE_BYTES;
           if (dbg & 4) {  // ablation: no B traffic
             mbar_arrive(&full[stage]);
@@ -397,11 +407,11 @@ __global__ void __launch_bounds__(128 + 128 * EPI_WG, 1)
     uint32_t phase = 0;
     for (int t = 0; t < ntiles; ++t) {
       const int acc = t % NACC;
-      mbar_wait(&tempty[acc], ((t / NACC) & 1) ^ 1);
+      mbar_wait_spin(&tempty[acc], ((t / NACC) & 1) ^ 1);
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
       for (int c = 0; c < NKC; ++c) {
-        mbar_wait(&full[stage], phase);
+        mbar_wait_spin(&full[stage], phase);
         tc_fence_after();
         if (lane == 0) {
           const uint32_t bb = smem_u32(Bst + stage * C::STAGE_BYTES);
@@ -430,6 +440,7 @@ __global__ void __launch_bounds__(128 + 128 * EPI_WG, 1)
     constexpr int NEPI = 128 * EPI_WG;
     constexpr int COLS = BN / EPI_WG;
     static_assert(COLS % 32 == 0, "epilogue chunking");
+    static_assert(!FOLD, "small d runs the persistent kernel");
     const int et = threadIdx.x - kEpiWarp0 * 32;
     const int wg = et >> 7;
     const int q = warp & 3;          // TMEM lane quarter
@@ -452,11 +463,7 @@ __global__ void __launch_bounds__(128 + 128 * EPI_WG, 1)
           const float e[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
           for (int w = 0; w < 4; ++w) {
-            float x = e[w];
-            if (FOLD) {
-              if (col + w == d) x = 1.0f;         // pairs with ||c||^2 in B
-              else if (col + w == d + 1) x = xx;  // pairs with 1 in B
-            }
+            const float x = e[w];
             const float b = tf32_rn(x);
             vb[u + w] = __float_as_uint(b);
             vs[u + w] = __float_as_uint(tf32_rn(x - b));
@@ -486,73 +493,7 @@ __global__ void __launch_bounds__(128 + 128 * EPI_WG, 1)
       int32_t j1;
       const bool no_ld = dbg & 16;  // ablation: no TMEM loads
       uint32_t r[2][32];
-      if (FOLD) {
-        // packed keys: (float bits >> 8) * 256 + column (two IMADs on the FMA pipe); signed-int
-        // order = value order for values >= 0, ties -> lower column
-        if (!no_ld) tmem_ld32(tbase, r[0]);
-#if !defined(MASK_TC_TOP2_RUNNING) && !defined(MASK_TC_KEY_IMAD)
-        int32_t k1 = 0x7fffffff, k2 = 0x7fffffff;
-#pragma unroll
-        for (int cc = 0; cc < COLS / 32; ++cc) {
-          if (!no_ld) {
-            tmem_wait_ld();
-            if (cc + 1 < COLS / 32) tmem_ld32(tbase + (cc + 1) * 32, r[(cc + 1) & 1]);
-          }
-          if (dbg & 1) continue;  // ablation: no epilogue arithmetic
-          int32_t c1, c2;
-          chunk_top2(r[cc & 1], ~(key_lo_mul - 1u), (uint32_t)(cc * 32), key_lo_mul >> 8, c1, c2);
-          merge_top2(k1, k2, c1, c2);
-        }
-        tc_fence_before();
-        mbar_arrive_warp(&tempty[acc]);
-#else
-        constexpr int NCH = MASK_TC_CHAINS;
-        int32_t b1[NCH], b2[NCH];
-#pragma unroll
-        for (int u = 0; u < NCH; ++u) b1[u] = b2[u] = 0x7fffffff;
-#pragma unroll
-        for (int cc = 0; cc < COLS / 32; ++cc) {
-          if (!no_ld) {
-            tmem_wait_ld();
-            if (cc + 1 < COLS / 32) tmem_ld32(tbase + (cc + 1) * 32, r[(cc + 1) & 1]);
-          }
-          if (dbg & 1) continue;  // ablation: no epilogue arithmetic
-#pragma unroll
-          for (int i = 0; i < 32; i += 2) {
-            int32_t ka, kb;
-#if !defined(MASK_TC_KEY_IMAD)
-            // key = (bits & ~0xFF) | column: one LOP3 (mask in a register, column immediate)
-            asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(ka) : "r"(r[cc & 1][i]), "r"(~(key_lo_mul - 1u)), "r"((uint32_t)(cc * 32 + i)));
-            asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(kb) : "r"(r[cc & 1][i + 1]), "r"(~(key_lo_mul - 1u)), "r"((uint32_t)(cc * 32 + i + 1)));
-#else
-            asm("{\n .reg .u32 h;\n mul.hi.u32 h, %1, %2;\n mad.lo.u32 %0, h, %3, %4;\n}"
-                : "=r"(ka)
-                : "r"(r[cc & 1][i]), "r"(key_hi_mul), "r"(key_lo_mul), "r"((uint32_t)(cc * 32 + i)));
-            asm("{\n .reg .u32 h;\n mul.hi.u32 h, %1, %2;\n mad.lo.u32 %0, h, %3, %4;\n}"
-                : "=r"(kb)
-                : "r"(r[cc & 1][i + 1]), "r"(key_hi_mul), "r"(key_lo_mul), "r"((uint32_t)(cc * 32 + i + 1)));
-#endif
-            // top-2 of {b1 <= b2} u {ka, kb}: b1' = min(b1, m), b2' = min(b2, M, max(b1, m))
-            const int u = (i >> 1) & (NCH - 1);
-            const int32_t m = imin(ka, kb), M = imax(ka, kb);
-            const int32_t t2 = imax(b1[u], m);
-            b1[u] = imin(b1[u], m);
-            b2[u] = imin(imin(b2[u], M), t2);
-          }
-        }
-        tc_fence_before();
-        mbar_arrive_warp(&tempty[acc]);
-        int32_t k1 = b1[0];
-#pragma unroll
-        for (int u = 1; u < NCH; ++u) k1 = imin(k1, b1[u]);
-        int32_t k2 = 0x7fffffff;
-#pragma unroll
-        for (int u = 0; u < NCH; ++u) k2 = imin(k2, b1[u] == k1 ? b2[u] : b1[u]);
-#endif
-        v1 = __int_as_float(k1 & 0xFFFFFF00);
-        v2 = __int_as_float(k2 & 0xFFFFFF00);
-        j1 = col0 + (k1 & 0xFF);
-      } else {
+      {
         float b1[4], b2[4];
         int32_t i1[4];
 #pragma unroll
@@ -659,7 +600,6 @@ __global__ void __launch_bounds__(128 + 128 * EPI_WG, 1)
         best[row] = dd;
         const float cc2 = __ldg(cn2 + gi);
         float thr = err_coef * (xx + cc2);
-        if (FOLD) thr += ldexpf(fmaxf(fabsf(g2), fabsf(g1)), -14);  // key quantisation (2^-15 rel) x 2
         flag = (g2 - g1) <= thr;
       }
       const unsigned m = __ballot_sync(0xffffffffu, flag);
@@ -694,10 +634,12 @@ struct PCfg {
   static constexpr int B_CHUNK = BN * CWB;
   static constexpr int STAGE_BYTES = 2 * B_CHUNK;
   static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
-  static constexpr int NBARS = 2 * STAGES + 2 * NACC + 4;
+  static constexpr int NBARS = 2 * STAGES + 2 * NACC + 10;
   static constexpr int SCRATCH_OFF = BAR_OFF + NBARS * 8 + 16;
-  static constexpr int SCRATCH_FLOATS = 2 * 3 * BM * (EPI_WG > 1 ? EPI_WG - 1 : 1);  // double-buffered
-  static constexpr int SMEM = SCRATCH_OFF + SCRATCH_FLOATS * 4 + 1024;
+  // per-block results of each epilogue warpgroup {s1, s2, j1, j2} x BM, double-buffered
+  static constexpr int SCRATCH_FLOATS = 2 * 4 * BM * EPI_WG;
+  static constexpr int INFO_OFF = SCRATCH_OFF + SCRATCH_FLOATS * 4;  // [2][BM] rows, [2][BM] bounds
+  static constexpr int SMEM = INFO_OFF + 4 * BM * 4 + 1024;
   static constexpr int A_COL = NACC * BN;  // A buffer b: big at A_COL + 2*KA*b, small at + KA
   static constexpr int NEED = A_COL + 4 * KA;
   static constexpr int TMEM_COLS = NEED <= 256 ? 256 : 512;
@@ -715,11 +657,13 @@ __global__ void __launch_bounds__(256 + 128 * EPI_WG, 1)
                         const float* __restrict__ X, const float* __restrict__ P, const float* __restrict__ cn2,
                         const float* __restrict__ xn2, int64_t n, int d, int64_t k, int32_t* __restrict__ labels,
                         float* __restrict__ best, int32_t* __restrict__ flag_rows, int32_t* __restrict__ flag_count,
-                        float err_coef, uint32_t key_mask, const int* __restrict__ active) {
+                        float err_coef, uint32_t key_mask, const int* __restrict__ active,
+                        const int32_t* __restrict__ perm, const int32_t* __restrict__ prev_lab,
+                        int32_t* __restrict__ lab2, int dbg) {
   if (active && !*active) return;  // level converged: this pass is skipped on the device
   using C = PCfg<KA, BN, STAGES, NACC, EPI_WG>;
   constexpr int COLS = BN / EPI_WG;
-  static_assert(COLS % 32 == 0, "epilogue chunking");
+  static_assert(COLS % 32 == 0 && COLS / 32 <= 2, "epilogue chunking (two register buffers)");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* Bst = smem;
@@ -730,8 +674,13 @@ __global__ void __launch_bounds__(256 + 128 * EPI_WG, 1)
   uint64_t* tempty = bars + 2 * STAGES + NACC;
   uint64_t* afull = bars + 2 * STAGES + 2 * NACC;
   uint64_t* aempty = afull + 2;
+  uint64_t* iempty = afull + 4;  // block info (rows, bounds) consumed by the epilogue
+  uint64_t* rfull = afull + 6;   // epilogue results of a block ready for the tail
+  uint64_t* rempty = afull + 8;  // tail done with a result buffer
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::NBARS);
   float* scratch = reinterpret_cast<float*>(smem + C::SCRATCH_OFF);
+  int32_t* s_row = reinterpret_cast<int32_t*>(smem + C::INFO_OFF);
+  int32_t* s_ub = s_row + 2 * BM;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ntiles = (int)((k + BN - 1) / BN);
@@ -750,7 +699,10 @@ __global__ void __launch_bounds__(256 + 128 * EPI_WG, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&afull[a], 4 * kArrivePerWarp);
-      mbar_init(&aempty[a], 1);
+      mbar_init(&aempty[a], ntiles >= 2 ? 2 : 1);  // one commit per MMA issuer with tiles in the block
+      mbar_init(&iempty[a], 4 * EPI_WG * kArrivePerWarp);
+      mbar_init(&rfull[a], 4 * EPI_WG * kArrivePerWarp);
+      mbar_init(&rempty[a], 4 * kArrivePerWarp);
     }
     fence_barrier_init();
   }
@@ -769,13 +721,19 @@ __global__ void __launch_bounds__(256 + 128 * EPI_WG, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
+      int64_t gp = 0;
       for (int64_t rb = blockIdx.x; rb < nblocks; rb += gridDim.x) {
-        for (int t = 0; t < ntiles; ++t) {
-          mbar_wait(&empty[stage], phase ^ 1);
+        for (int t = 0; t < ntiles; ++t, ++gp) {
+          mbar_wait_spin(&empty[stage], phase ^ 1);
+          if ((dbg & 8) && blockIdx.x == 0 && gp < kPT) g_pt[8][gp] = clock64();
           uint8_t* dst = Bst + stage * C::STAGE_BYTES;
-          mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
-          tma_load_2d(dst, &tmBb, &full[stage], 0, t * BN);
-          tma_load_2d(dst + C::B_CHUNK, &tmBs, &full[stage], 0, t * BN);
+          if (dbg & 4) {  // ablation: no B traffic
+            mbar_arrive(&full[stage]);
+          } else {
+            mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
+            tma_load_2d(dst, &tmBb, &full[stage], 0, t * BN);
+            tma_load_2d(dst + C::B_CHUNK, &tmBs, &full[stage], 0, t * BN);
+          }
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -783,58 +741,181 @@ __global__ void __launch_bounds__(256 + 128 * EPI_WG, 1)
         }
       }
     }
-  } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer
-    int stage = 0;
-    uint32_t phase = 0;
-    int64_t g = 0;  // global tile counter of this CTA
-    int i = 0;      // block iteration of this CTA
-    for (int64_t rb = blockIdx.x; rb < nblocks; rb += gridDim.x, ++i) {
+  } else if (warp == 1 || warp == 3) {
+    // ------------------------------------------------------------ MMA issuers (two warps)
+    // Warp 1 issues the even tiles, warp 3 the odd ones (accumulator g % NACC): while
+    // one is blocked feeding the tensor core's instruction queue, the other has already passed
+    // its barrier waits, so the per-tile control path (commits, two waits) never drains the
+    // queue (a single issuer left the pipe idle ~35% of the time at d = 16).
+    static_assert((STAGES & (STAGES - 1)) == 0, "stage ring indexed by masking");
+    const int par = warp == 1 ? 0 : 1;
+    int64_t g0 = 0;  // first global tile of the block
+    int i = 0;       // block iteration of this CTA
+    for (int64_t rb = blockIdx.x; rb < nblocks; rb += gridDim.x, ++i, g0 += ntiles) {
+      const int first = (int)((g0 & 1) == par ? 0 : 1);  // this issuer's first tile of the block
+      if (first >= ntiles) continue;
+      const int last = first + (ntiles - 1 - first) / 2 * 2;
       const int ab = i & 1;
-      mbar_wait(&afull[ab], (i >> 1) & 1);
+      mbar_wait_spin(&afull[ab], (i >> 1) & 1);
       tc_fence_after();
       const uint32_t a_big = tmem_base + C::A_COL + 2 * KA * ab, a_small = a_big + KA;
-      for (int t = 0; t < ntiles; ++t, ++g) {
+      for (int t = first; t < ntiles; t += 2) {
+        const int64_t g = g0 + t;
+        const int stage = (int)(g & (STAGES - 1));
+        const uint32_t phase = (uint32_t)((g / STAGES) & 1);
         const int acc = (int)(g % NACC);
-        mbar_wait(&tempty[acc], ((g / NACC) & 1) ^ 1);
-        tc_fence_after();
         const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
-        mbar_wait(&full[stage], phase);
+        mbar_wait_spin(&tempty[acc], ((g / NACC) & 1) ^ 1);
         tc_fence_after();
+        const bool ptr = (dbg & 8) && blockIdx.x == 0 && lane == 0 && g < kPT;
+        if (ptr) g_pt[0][g] = clock64();
+        mbar_wait_spin(&full[stage], phase);
+        tc_fence_after();
+        if (ptr) g_pt[1][g] = clock64();
         if (lane == 0) {
           const uint32_t bb = smem_u32(Bst + stage * C::STAGE_BYTES);
           const uint32_t bs = bb + C::B_CHUNK;
 #pragma unroll
-          for (int ks = 0; ks < KA / 8; ++ks) {
+          for (int ks = 0; ks < KA / 8 - 1; ++ks) {
+            if (dbg & 2) break;  // ablation: no MMA
             const uint64_t dbb = smem_desc<C::CWB>(bb + ks * 32), dbs = smem_desc<C::CWB>(bs + ks * 32);
             mma_tf32_ts(d_tmem, a_small + ks * 8, dbb, C::IDESC, ks != 0);
             mma_tf32_ts(d_tmem, a_big + ks * 8, dbs, C::IDESC, 1u);
             mma_tf32_ts(d_tmem, a_big + ks * 8, dbb, C::IDESC, 1u);
           }
+          // fold step: ||c||^2 + ||x||^2 from exact 1-products of the split norms (one MMA)
+          constexpr int KF = KA / 8 - 1;
+          if (!(dbg & 2)) mma_tf32_ts(d_tmem, a_big + KF * 8, smem_desc<C::CWB>(bb + KF * 32), C::IDESC, 1u);
           mma_commit(&empty[stage]);
           mma_commit(&tfull[acc]);
-          if (t == ntiles - 1) mma_commit(&aempty[ab]);  // this block's A may be overwritten
+          // this issuer's MMAs on the block's A are done (aempty counts one arrive per issuer
+          // that has tiles in the block)
+          if (t == last) mma_commit(&aempty[ab]);
+          if (ptr) g_pt[7][g] = clock64();
         }
         __syncwarp();
-        if (++stage == STAGES) {
-          stage = 0;
-          phase ^= 1;
-        }
       }
     }
   } else if (warp >= 4 && warp < C::EPI0) {
     // ------------------------------------------------------------ A loader (one thread per row)
+    // Also publishes, per block, each row's index (through `perm`) and its pruning bound:
+    // with the previous pass's best and second-best prototypes a1 != a2, the exact FP32
+    // U = max(d^2(x, c_a1), d^2(x, c_a2)) bounds the true second-best distance, so the two
+    // smallest 3xTF32 scores are <= U + (score error) and any 32-column chunk whose raw
+    // minimum exceeds that bound holds neither (K1 "bound-pruned epilogue").
+    // The same warpgroup runs each block's tail one block later (merge of the epilogue
+    // warpgroups' top-2, labels, exact FP32 d^2 of the winner, near-tie flags), so the epilogue
+    // warpgroups go straight on to the next block's tiles.
     const int q = warp & 3;
     const int rloc = q * 32 + lane;
     const uint32_t lane_base = tmem_base + ((uint32_t)(q * 32) << 16);
+    auto tail = [&](int ib) {  // block iteration ib of this CTA
+      const int tb = ib & 1;
+      mbar_wait(&rfull[tb], (ib >> 1) & 1);
+      const float* r1 = scratch + tb * 4 * BM * EPI_WG;
+      const float* r2 = r1 + BM * EPI_WG;
+      const int32_t* ri = reinterpret_cast<const int32_t*>(r2 + BM * EPI_WG);
+      const int32_t* ri2 = ri + BM * EPI_WG;
+      float g1 = r1[rloc], g2 = r2[rloc];
+      int32_t gi = ri[rloc], gi2 = ri2[rloc];
+#pragma unroll
+      for (int w = 1; w < EPI_WG; ++w) {  // lowest index on equal values
+        const float o1 = r1[w * BM + rloc], o2 = r2[w * BM + rloc];
+        const int32_t oi = ri[w * BM + rloc], oi2 = ri2[w * BM + rloc];
+        if (o1 < g1 || (o1 == g1 && oi < gi)) {
+          if (g1 <= o2) {
+            g2 = g1;
+            gi2 = gi;
+          } else {
+            g2 = o2;
+            gi2 = oi2;
+          }
+          g1 = o1;
+          gi = oi;
+        } else if (o1 < g2) {
+          g2 = o1;
+          gi2 = oi;
+        }
+      }
+      const int64_t row = s_row[tb * BM + rloc];
+      mbar_arrive_warp(&rempty[tb]);
+      bool flag = false;
+      if (row < n) {
+        if (dbg) gi = gi < 0 ? 0 : (gi >= k ? (int32_t)(k - 1) : gi);  // ablation runs: keep in range
+        labels[row] = gi;
+        if (lab2) lab2[row] = gi2;
+        const float* xr = X + row * d;
+        const float* cr = P + (int64_t)gi * d;
+        float dd = 0.f;
+        for (int c = 0; c < d; c += 4) {
+          const float4 xv = __ldg(reinterpret_cast<const float4*>(xr + c));
+          const float4 cv = __ldg(reinterpret_cast<const float4*>(cr + c));
+          float tt = xv.x - cv.x;
+          dd = fmaf(tt, tt, dd);
+          tt = xv.y - cv.y;
+          dd = fmaf(tt, tt, dd);
+          tt = xv.z - cv.z;
+          dd = fmaf(tt, tt, dd);
+          tt = xv.w - cv.w;
+          dd = fmaf(tt, tt, dd);
+        }
+        best[row] = dd;
+        const float xx = __ldg(xn2 + row);
+        const float thr = err_coef * (xx + __ldg(cn2 + gi)) + ldexpf(fmaxf(fabsf(g2), fabsf(g1)), -14);
+        flag = (g2 - g1) <= thr;
+      }
+      const unsigned msk = __ballot_sync(0xffffffffu, flag);
+      if (msk) {
+        int base = 0;
+        if (lane == 0) base = atomicAdd(flag_count, __popc(msk));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (flag) flag_rows[base + __popc(msk & ((1u << lane) - 1))] = (int32_t)row;
+      }
+    };
     int i = 0;
     for (int64_t rb = blockIdx.x; rb < nblocks; rb += gridDim.x, ++i) {
       const int ab = i & 1;
       mbar_wait_sleep(&aempty[ab], ((i >> 1) & 1) ^ 1);
+      mbar_wait_sleep(&iempty[ab], ((i >> 1) & 1) ^ 1);
       tc_fence_after();
-      const int64_t row = rb * BM + rloc;
+      const bool ptr = (dbg & 8) && blockIdx.x == 0 && rloc == 0 && i < 512;
+      if (ptr) g_pt[5][i] = clock64();
+      const int64_t pos = rb * BM + rloc;
+      const int64_t row = pos < n ? (perm ? (int64_t)__ldg(perm + pos) : pos) : n;
       const float xx = row < n ? __ldg(xn2 + row) : 0.f;
       const float* xr = X + row * d;
+      constexpr int KX = KA - 8;  // x columns (d rounded up to 8); [KX, KA) is the fold step
+      float ub = INFINITY;
+      if (prev_lab && row < n) {
+        const int32_t a1 = __ldg(prev_lab + row), a2 = lab2[row];
+        if (a1 >= 0 && a1 < k && a2 >= 0 && a2 < k && a1 != a2) {
+          const float* c1 = P + (int64_t)a1 * d;
+          const float* c2 = P + (int64_t)a2 * d;
+          float s1 = 0.f, s2 = 0.f;
+          for (int c = 0; c < d; c += 4) {
+            const float4 xv = __ldg(reinterpret_cast<const float4*>(xr + c));
+            const float4 u = __ldg(reinterpret_cast<const float4*>(c1 + c));
+            const float4 w = __ldg(reinterpret_cast<const float4*>(c2 + c));
+            float t;
+            t = xv.x - u.x; s1 = fmaf(t, t, s1); t = xv.x - w.x; s2 = fmaf(t, t, s2);
+            t = xv.y - u.y; s1 = fmaf(t, t, s1); t = xv.y - w.y; s2 = fmaf(t, t, s2);
+            t = xv.z - u.z; s1 = fmaf(t, t, s1); t = xv.z - w.z; s2 = fmaf(t, t, s2);
+            t = xv.w - u.w; s1 = fmaf(t, t, s1); t = xv.w - w.w; s2 = fmaf(t, t, s2);
+          }
+          const float U = fmaxf(s1, s2);
+          // ||c_j|| <= ||x|| + sqrt(U) for every j with d^2 <= U; doubled error coefficient
+          const float cm = sqrtf(xx) + sqrtf(U);
+          ub = (U + 2.f * err_coef * (xx + cm * cm)) * (1.f + 0x1p-12f) + 0x1p-100f;
+        }
+      }
+      s_row[ab * BM + rloc] = (int32_t)row;
+      s_ub[ab * BM + rloc] = __float_as_int(ub);
+      if ((dbg & 32) && i >= 2) {  // ablation: keep the stale A block (no TMEM stores)
+        tc_fence_before();
+        mbar_arrive_warp(&afull[ab]);
+        tail(i - 1);
+        continue;
+      }
       const uint32_t a_big = lane_base + C::A_COL + 2 * KA * ab, a_small = a_big + KA;
 #pragma unroll
       for (int g8 = 0; g8 < KA; g8 += 8) {
@@ -847,150 +928,139 @@ __global__ void __launch_bounds__(256 + 128 * EPI_WG, 1)
           const float e[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
           for (int w = 0; w < 4; ++w) {
-            float x = e[w];
-            if (col + w == d) x = 1.0f;         // pairs with ||c||^2 in B
-            else if (col + w == d + 1) x = xx;  // pairs with 1 in B
-            const float b = tf32_rn(x);
+            const float b = tf32_rn(e[w]);
             vb[u + w] = __float_as_uint(b);
-            vs[u + w] = __float_as_uint(tf32_rn(x - b));
+            vs[u + w] = __float_as_uint(tf32_rn(e[w] - b));
           }
         }
+        if (g8 == KX) {  // fold step: [1, 1, xx_b, xx_s] . [cn2_b, cn2_s, 1, 1] (big parts only)
+          const float hb = tf32_rn(xx);
+          vb[0] = vb[1] = __float_as_uint(1.0f);
+          vb[2] = __float_as_uint(hb);
+          vb[3] = __float_as_uint(tf32_rn(xx - hb));
+          vb[4] = vb[5] = vb[6] = vb[7] = 0u;
+        }
         tmem_st8(a_big + g8, vb);
-        tmem_st8(a_small + g8, vs);
+        if (g8 < KX) tmem_st8(a_small + g8, vs);
       }
       tmem_wait_st();
       tc_fence_before();
       mbar_arrive_warp(&afull[ab]);
+      if (ptr) g_pt[6][i] = clock64();
+      if (i >= 1) tail(i - 1);
     }
+    if (i >= 1) tail(i - 1);
   } else if (warp >= C::EPI0) {
     // ------------------------------------------------------------ epilogue warpgroups
-    constexpr int NEPI = 128 * EPI_WG;
     const int et = threadIdx.x - C::EPI0 * 32;
     const int wg = et >> 7;
     const int q = warp & 3;
     const int rloc = q * 32 + lane;
     int64_t g = 0;
     int i = 0;
+    unsigned long long st_seen = 0, st_keyed = 0;
     for (int64_t rb = blockIdx.x; rb < nblocks; rb += gridDim.x, ++i) {
-      const int64_t row = rb * BM + rloc;
+      const int ab = i & 1;
+      mbar_wait(&afull[ab], (i >> 1) & 1);  // block info published with the A block
+      const int32_t ubk = s_ub[ab * BM + rloc];
+      mbar_arrive_warp(&iempty[ab]);
       float g1 = INFINITY, g2 = INFINITY;
-      int32_t gi = 0x7fffffff;
+      int32_t gi = 0x7fffffff, gi2 = -1;
       for (int t = 0; t < ntiles; ++t, ++g) {
         const int acc = (int)(g % NACC);
-        mbar_wait(&tfull[acc], (g / NACC) & 1);
+        // polled, not suspended: the accumulator round trip (MMA -> epilogue -> MMA) must fit in
+        // one tile of tensor-core work, and a suspended waiter wakes hundreds of cycles late
+        mbar_wait_spin(&tfull[acc], (g / NACC) & 1);
         tc_fence_after();
+        const bool ptr = (dbg & 8) && blockIdx.x == 0 && lane == 0 && q == 0 && g < 512;
+        if (ptr && wg == 0) g_pt[2][g] = clock64();
         const int col0 = wg * COLS;
         const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + col0);
         uint32_t r[2][32];
-        tmem_ld32(tbase, r[0]);
-#if !defined(MASK_TC_TOP2_RUNNING)
-        int32_t k1 = 0x7fffffff, k2 = 0x7fffffff;
+        if (dbg & 64) {  // ablation: no TMEM loads, no epilogue
+          tc_fence_before();
+          mbar_arrive_warp(&tempty[acc]);
+          if (ptr && wg == 0) g_pt[3][g] = clock64();
+          if (ptr && wg == EPI_WG - 1) g_pt[4][g] = clock64();
+          continue;
+        }
+        // all of this warpgroup's columns into registers, then release the accumulator before
+        // any arithmetic (the MMAs of tile g + NACC may start while this tile is reduced)
+#pragma unroll
+        for (int cc = 0; cc < COLS / 32; ++cc) tmem_ld32(tbase + cc * 32, r[cc]);
+        tmem_wait_ld();
+        tc_fence_before();
+        mbar_arrive_warp(&tempty[acc]);
+        if (ptr && wg == 0) g_pt[3][g] = clock64();
+        if (ptr && wg == EPI_WG - 1) g_pt[4][g] = clock64();
+        // running top-2 keys of this tile; k2 starts at the pruning bound (low byte 0xFF marks
+        // "no element": real keys carry a column < COLS in that byte)
+        int32_t k1 = 0x7fffffff;
+        int32_t k2 = imin(ubk, __float_as_int(g2)) | 0xFF;
 #pragma unroll
         for (int cc = 0; cc < COLS / 32; ++cc) {
-          tmem_wait_ld();
-          if (cc + 1 < COLS / 32) tmem_ld32(tbase + (cc + 1) * 32, r[(cc + 1) & 1]);
+          if (dbg & 1) {  // ablation: no epilogue arithmetic
+            if (cc == 0) k1 = (int32_t)r[0][0] & 0xFFFFFF00;
+            continue;
+          }
+#if !defined(MASK_TC_NO_PRUNE)
+          // pass 0: raw minimum of the chunk (3-input mins, 0.5 ALU op per key); the chunk is
+          // keyed and merged only if some row of the warp may have a key below its k2
+          const uint32_t* rr = r[cc & 1];
+          int32_t m[11];
+#pragma unroll
+          for (int j = 0; j < 10; ++j) m[j] = imin(imin((int32_t)rr[3 * j], (int32_t)rr[3 * j + 1]), (int32_t)rr[3 * j + 2]);
+          m[10] = imin((int32_t)rr[30], (int32_t)rr[31]);
+          const int32_t c0 = imin(imin(imin(m[0], m[1]), imin(m[2], m[3])),
+                                  imin(imin(imin(m[4], m[5]), imin(m[6], m[7])), imin(imin(m[8], m[9]), m[10])));
+          const bool need = __any_sync(0xffffffffu, c0 <= k2);
+          if (dbg & 128) {
+            ++st_seen;
+            st_keyed += need ? 1 : 0;
+          }
+          if (!need) continue;
+#endif
           int32_t c1, c2;
           chunk_top2(r[cc & 1], key_mask, (uint32_t)(cc * 32), key_mask >> 31, c1, c2);
           merge_top2(k1, k2, c1, c2);
         }
-        tc_fence_before();
-        mbar_arrive_warp(&tempty[acc]);
-#else
-        int32_t b1[MASK_TC_CHAINS], b2[MASK_TC_CHAINS];
-#pragma unroll
-        for (int u = 0; u < MASK_TC_CHAINS; ++u) b1[u] = b2[u] = 0x7fffffff;
-#pragma unroll
-        for (int cc = 0; cc < COLS / 32; ++cc) {
-          tmem_wait_ld();
-          if (cc + 1 < COLS / 32) tmem_ld32(tbase + (cc + 1) * 32, r[(cc + 1) & 1]);
-#pragma unroll
-          for (int e = 0; e < 32; e += 2) {
-            // key = (bits & ~0xFF) | column (one LOP3; mask in a register, column immediate)
-            int32_t ka, kb;
-            asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(ka) : "r"(r[cc & 1][e]), "r"(key_mask), "r"((uint32_t)(cc * 32 + e)));
-            asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(kb) : "r"(r[cc & 1][e + 1]), "r"(key_mask), "r"((uint32_t)(cc * 32 + e + 1)));
-            const int u = (e >> 1) & (MASK_TC_CHAINS - 1);
-            const int32_t m = imin(ka, kb), M = imax(ka, kb);
-            const int32_t t2 = imax(b1[u], m);
-            b1[u] = imin(b1[u], m);
-            b2[u] = imin(imin(b2[u], M), t2);
-          }
-        }
-        tc_fence_before();
-        mbar_arrive_warp(&tempty[acc]);
-        int32_t k1 = b1[0];
-#pragma unroll
-        for (int u = 1; u < MASK_TC_CHAINS; ++u) k1 = imin(k1, b1[u]);
-        int32_t k2 = 0x7fffffff;
-#pragma unroll
-        for (int u = 0; u < MASK_TC_CHAINS; ++u) k2 = imin(k2, b1[u] == k1 ? b2[u] : b1[u]);
-#endif
-        const float v1 = __int_as_float(k1 & 0xFFFFFF00), v2 = __int_as_float(k2 & 0xFFFFFF00);
-        if (v1 < g1) {  // strict: ties keep the earlier tile (lower prototype index)
-          g2 = fminf(g1, v2);
-          g1 = v1;
-          gi = t * BN + col0 + (k1 & 0xFF);
-        } else {
-          g2 = fminf(g2, v1);
-        }
-      }
-      if (EPI_WG > 1) {  // merge the warpgroups' results (double-buffered scratch by block parity)
-        float* mg1 = scratch + (i & 1) * 3 * BM * (EPI_WG - 1);
-        float* mg2 = mg1 + (EPI_WG - 1) * BM;
-        int32_t* mgi = reinterpret_cast<int32_t*>(mg2 + (EPI_WG - 1) * BM);
-        if (wg > 0) {
-          mg1[(wg - 1) * BM + rloc] = g1;
-          mg2[(wg - 1) * BM + rloc] = g2;
-          mgi[(wg - 1) * BM + rloc] = gi;
-        }
-        asm volatile("bar.sync 1, %0;" ::"n"(NEPI) : "memory");
-        if (wg == 0) {
-#pragma unroll
-          for (int w = 0; w < EPI_WG - 1; ++w) {
-            const float o1 = mg1[w * BM + rloc], o2 = mg2[w * BM + rloc];
-            const int32_t oi = mgi[w * BM + rloc];
-            if (o1 < g1 || (o1 == g1 && oi < gi)) {
-              g2 = fminf(g1, o2);
-              g1 = o1;
-              gi = oi;
+        if (k1 != 0x7fffffff) {
+          const float v1 = __int_as_float(k1 & 0xFFFFFF00);
+          const int32_t j1 = t * BN + col0 + (k1 & 0xFF);
+          const bool real2 = (k2 & 0xFF) != 0xFF;
+          const float v2 = real2 ? __int_as_float(k2 & 0xFFFFFF00) : INFINITY;
+          const int32_t j2 = real2 ? t * BN + col0 + (k2 & 0xFF) : -1;
+          if (v1 < g1) {  // strict: ties keep the earlier tile (lower prototype index)
+            if (g1 <= v2) {
+              g2 = g1;
+              gi2 = gi;
             } else {
-              g2 = fminf(g2, o1);
+              g2 = v2;
+              gi2 = j2;
             }
+            g1 = v1;
+            gi = j1;
+          } else if (v1 < g2) {
+            g2 = v1;
+            gi2 = j1;
           }
         }
       }
-      if (wg == 0) {
-        bool flag = false;
-        if (row < n) {
-          labels[row] = gi;
-          const float* xr = X + row * d;
-          const float* cr = P + (int64_t)gi * d;
-          float dd = 0.f;
-          for (int c = 0; c < d; c += 4) {
-            const float4 xv = __ldg(reinterpret_cast<const float4*>(xr + c));
-            const float4 cv = __ldg(reinterpret_cast<const float4*>(cr + c));
-            float tt = xv.x - cv.x;
-            dd = fmaf(tt, tt, dd);
-            tt = xv.y - cv.y;
-            dd = fmaf(tt, tt, dd);
-            tt = xv.z - cv.z;
-            dd = fmaf(tt, tt, dd);
-            tt = xv.w - cv.w;
-            dd = fmaf(tt, tt, dd);
-          }
-          best[row] = dd;
-          const float xx = __ldg(xn2 + row);
-          const float thr = err_coef * (xx + __ldg(cn2 + gi)) + ldexpf(fmaxf(fabsf(g2), fabsf(g1)), -14);
-          flag = (g2 - g1) <= thr;
-        }
-        const unsigned msk = __ballot_sync(0xffffffffu, flag);
-        if (msk) {
-          int base = 0;
-          if (lane == 0) base = atomicAdd(flag_count, __popc(msk));
-          base = __shfl_sync(0xffffffffu, base, 0);
-          if (flag) flag_rows[base + __popc(msk & ((1u << lane) - 1))] = (int32_t)row;
-        }
-      }
+      // hand this warpgroup's per-row top-2 to the tail (loader warpgroup)
+      mbar_wait(&rempty[ab], ((i >> 1) & 1) ^ 1);
+      float* r1 = scratch + ab * 4 * BM * EPI_WG;
+      float* r2 = r1 + BM * EPI_WG;
+      int32_t* ri = reinterpret_cast<int32_t*>(r2 + BM * EPI_WG);
+      int32_t* ri2 = ri + BM * EPI_WG;
+      r1[wg * BM + rloc] = g1;
+      r2[wg * BM + rloc] = g2;
+      ri[wg * BM + rloc] = gi;
+      ri2[wg * BM + rloc] = gi2;
+      mbar_arrive_warp(&rfull[ab]);
+    }
+    if ((dbg & 128) && lane == 0) {
+      atomicAdd(&g_chunk_stats[0], st_seen);
+      atomicAdd(&g_chunk_stats[1], st_keyed);
     }
   }
   tc_fence_before();
@@ -999,6 +1069,21 @@ __global__ void __launch_bounds__(256 + 128 * EPI_WG, 1)
   if (warp == 2) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(C::TMEM_COLS));
   }
+}
+
+// development trace of the persistent kernel (MASK_TC_DEBUG bit 8): clock64 stamps of CTA 0,
+// per tile g: [0] MMA issuer past tempty, [1] past full, [2] epilogue (wg0) past tfull,
+// [3] wg0 release, [4] last wg release; per block i: [5] loader start, [6] loader done
+void dump_ptrace() {
+  static long long h[9][kPT];
+  if (cudaDeviceSynchronize() != cudaSuccess) return;
+  if (cudaMemcpyFromSymbol(h, g_pt, sizeof(h)) != cudaSuccess) return;
+  fprintf(stderr, "[ptrace] tile: tma_issue tempty_ok full_ok issue_done | epi_start wg0_rel last_rel (cycles rel. to full_ok of the tile)\n");
+  for (int g = 40; g < 64; ++g)
+    fprintf(stderr, "  %3d: %6lld %6lld %6lld %6lld | %6lld %6lld %6lld | dfull %lld\n", g, h[8][g] - h[1][g], h[0][g] - h[1][g], 0ll,
+            h[7][g] - h[1][g], h[2][g] - h[1][g], h[3][g] - h[1][g], h[4][g] - h[1][g], h[1][g] - h[1][g - 1]);
+  for (int i = 1; i < 6; ++i)
+    fprintf(stderr, "  block %d loader start %lld dur %lld (rel. tile %d full_ok)\n", i, h[5][i] - h[1][0], h[6][i] - h[5][i], 0);
 }
 
 // Host dump of the development trace: per-phase medians (us) over the traced CTAs.
@@ -1043,9 +1128,11 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 // 2-D fp32 row-major [rows x cols] tensor map with a {box_cols x box_rows} box.
-CUtensorMap make_map(const float* base, int64_t rows, int cols, int box_cols, int box_rows) {
+// `width` <= cols limits the columns actually read (the rest of the box is zero-filled by the
+// TMA unit without memory traffic).
+CUtensorMap make_map(const float* base, int64_t rows, int cols, int box_cols, int box_rows, int width = 0) {
   CUtensorMap m;
-  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t dims[2] = {(cuuint64_t)(width > 0 ? width : cols), (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)cols * 4};
   cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
@@ -1089,7 +1176,7 @@ void launch_cfg(const float* X, int64_t n, int d, int kc, int64_t k_rows, const 
   }
   const unsigned grid = (unsigned)((n + BM - 1) / BM);
   kern<<<grid, C::NTHREADS, C::SMEM, st>>>(tBb, tBs, X, P, cn2, xn2, n, d, k, labels, best, flag_rows, flag_count,
-                                           err_coef, 1u << 24, 256u, tc_debug_mode(), active);
+                                           err_coef, tc_debug_mode(), active);
   MASK_LAUNCH_CHECK();
   if (tc_debug_mode() & 8) dump_trace((int)grid);
 }
@@ -1097,10 +1184,16 @@ void launch_cfg(const float* X, int64_t n, int d, int kc, int64_t k_rows, const 
 template <int KA, int BN, int STAGES, int NACC, int EPI_WG>
 void launch_persist(const float* X, int64_t n, int d, int kc, int64_t k_rows, const float* P, const float* Pb,
                     const float* Ps, const float* cn2, int64_t k, const float* xn2, int32_t* labels, float* best,
-                    int32_t* flag_rows, int32_t* flag_count, float err_coef, cudaStream_t st, const int* active) {
+                    int32_t* flag_rows, int32_t* flag_count, float err_coef, cudaStream_t st, const int* active,
+                    const int32_t* perm, const int32_t* prev_lab, int32_t* lab2) {
   using C = PCfg<KA, BN, STAGES, NACC, EPI_WG>;
   const CUtensorMap tBb = make_map(Pb, k_rows, kc, C::CW, BN);
+  // the small part is only read by the x steps (KA - 8 columns); the fold step uses Pb alone
+#if defined(MASK_TC_PS_TRIM)
+  const CUtensorMap tBs = make_map(Ps, k_rows, kc, C::CW, BN, KA - 8);
+#else
   const CUtensorMap tBs = make_map(Ps, k_rows, kc, C::CW, BN);
+#endif
   auto kern = k_assign_tc_persist<KA, BN, STAGES, NACC, EPI_WG>;
   static bool attr_set = false;
   if (!attr_set) {
@@ -1110,8 +1203,17 @@ void launch_persist(const float* X, int64_t n, int d, int kc, int64_t k_rows, co
   const int64_t nblocks = (n + BM - 1) / BM;
   const unsigned grid = (unsigned)(nblocks < num_sms() ? nblocks : num_sms());
   kern<<<grid, C::NTHREADS, C::SMEM, st>>>(tBb, tBs, X, P, cn2, xn2, n, d, k, labels, best, flag_rows, flag_count,
-                                           err_coef, 0xFFFFFF00u, active);
+                                           err_coef, 0xFFFFFF00u, active, perm, prev_lab, lab2, tc_debug_mode());
   MASK_LAUNCH_CHECK();
+  if (tc_debug_mode() & 8) dump_ptrace();
+  if (tc_debug_mode() & 128) {
+    unsigned long long h[4] = {0, 0, 0, 0};
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(h, g_chunk_stats, sizeof(h));
+    fprintf(stderr, "[chunks] seen %llu keyed %llu (%.1f%%)\n", h[0], h[1], 100.0 * h[1] / (h[0] ? h[0] : 1));
+    const unsigned long long z[4] = {0, 0, 0, 0};
+    cudaMemcpyToSymbol(g_chunk_stats, z, sizeof(z));
+  }
 }
 
 }  // namespace tc
@@ -1124,9 +1226,13 @@ bool tc_supported(int64_t n, int d, int64_t k) {
   return n >= 1 && d >= 4 && d <= 128 && d % 4 == 0;
 }
 
-// B operand columns: d + 2 (||c||^2, 1) rounded up to 8 when folded (small d), else d rounded
-// up to 8 (zero columns beyond d)
-int tc_operand_cols(int d) { return d + 2 <= 32 ? ((d + 2 + 7) / 8) * 8 : ((d + 7) / 8) * 8; }
+// B operand columns: d rounded up to 8 (zero columns beyond d), plus, for small d (d <= 24,
+// folded), one K step of 8 holding [||c||^2 big, ||c||^2 small, 1, 1, 0...]
+#if defined(MASK_TC_PAD32)
+int tc_operand_cols(int d) { return d <= 24 ? 32 : ((d + 7) / 8) * 8; }
+#else
+int tc_operand_cols(int d) { return ((d + 7) / 8) * 8 + (d <= 24 ? 8 : 0); }
+#endif
 // rows of the B operand arrays: padded to whole 256-prototype tiles (pad rows never win)
 int64_t tc_operand_rows(int64_t k) { return (k + 255) / 256 * 256 + 256; }
 
@@ -1142,31 +1248,36 @@ float tc_err_coef(int d) {
 
 void launch_assign_tc(const float* X, int64_t n, int d, const float* P, const float* Pb, const float* Ps,
                       const float* cn2, int64_t k, const float* xn2, int32_t* labels, float* best,
-                      int32_t* flag_rows, int32_t* flag_count, cudaStream_t st, const int* active) {
+                      int32_t* flag_rows, int32_t* flag_count, cudaStream_t st, const int* active,
+                      const int32_t* perm, const int32_t* prev_lab, int32_t* lab2) {
   const float coef = tc_err_coef(d);
   const int kc = tc_operand_cols(d);
   const int64_t kr = tc_operand_rows(k);
   // small d (FOLD): epilogue-bound; 192-prototype tiles, two TMEM accumulators (2 x 192 + 2 x
   // KA columns), three epilogue warpgroups of 64 columns (best of the measured variants)
-  static const int persist = [] {
-    const char* e = getenv("MASK_TC_PERSIST");  // development switch (default: persistent)
-    return e ? atoi(e) : 1;
-  }();
+  // small d (fold): epilogue-heavy; persistent CTAs, 192-prototype tiles, two TMEM
+  // accumulators, three epilogue warpgroups of 64 columns (best of the measured variants)
 #ifndef MASK_TC_P_BN
 #define MASK_TC_P_BN 192
 #define MASK_TC_P_STAGES 4
 #define MASK_TC_P_NACC 2
 #define MASK_TC_P_EPI 3
 #endif
-  if (d + 2 <= 24 && persist)
+  if (d <= 8)
+    tc::launch_persist<16, MASK_TC_P_BN, MASK_TC_P_STAGES, MASK_TC_P_NACC, MASK_TC_P_EPI>(
+        X, n, d, kc, kr, P, Pb, Ps, cn2, k, xn2, labels, best, flag_rows, flag_count, coef, st, active, perm,
+        prev_lab, lab2);
+  else if (d <= 16)
     tc::launch_persist<24, MASK_TC_P_BN, MASK_TC_P_STAGES, MASK_TC_P_NACC, MASK_TC_P_EPI>(
-        X, n, d, kc, kr, P, Pb, Ps, cn2, k, xn2, labels, best, flag_rows, flag_count, coef, st, active);
-  else if (d + 2 <= 24)
-    tc::launch_cfg<32, 1, 24, 192, 4, 2, true, 3>(X, n, d, kc, kr, P, Pb, Ps, cn2, k, xn2, labels, best, flag_rows,
-                                                  flag_count, coef, st, active);
-  else if (d + 2 <= 32)
-    tc::launch_cfg<32, 1, 32, 192, 4, 2, true, 3>(X, n, d, kc, kr, P, Pb, Ps, cn2, k, xn2, labels, best, flag_rows,
-                                                  flag_count, coef, st, active);
+        X, n, d, kc, kr, P, Pb, Ps, cn2, k, xn2, labels, best, flag_rows, flag_count, coef, st, active, perm,
+        prev_lab, lab2);
+  else if (d <= 24)
+    tc::launch_persist<32, MASK_TC_P_BN, MASK_TC_P_STAGES, MASK_TC_P_NACC, MASK_TC_P_EPI>(
+        X, n, d, kc, kr, P, Pb, Ps, cn2, k, xn2, labels, best, flag_rows, flag_count, coef, st, active, perm,
+        prev_lab, lab2);
+  else if (d <= 32)
+    tc::launch_cfg<32, 1, 32, 192, 4, 2, false, 3>(X, n, d, kc, kr, P, Pb, Ps, cn2, k, xn2, labels, best, flag_rows,
+                                                   flag_count, coef, st, active);
   else if (d <= 64)
     tc::launch_cfg<32, 2, 64, 128, 6, 3, false, 2>(X, n, d, kc, kr, P, Pb, Ps, cn2, k, xn2, labels, best, flag_rows,
                                                    flag_count, coef, st, active);

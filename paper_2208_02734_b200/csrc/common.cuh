@@ -117,7 +117,11 @@ int tc_operand_cols(int d);
 void launch_assign_tc(const float* X, int64_t n, int d, const float* P, const float* Pb,
                       const float* Ps, const float* cn2, int64_t k, const float* xn2,
                       int32_t* labels, float* best, int32_t* flag_rows, int32_t* flag_count,
-                      cudaStream_t st, const int* active = nullptr);
+                      cudaStream_t st, const int* active = nullptr, const int32_t* perm = nullptr,
+                      const int32_t* prev_lab = nullptr, int32_t* lab2 = nullptr);
+// Counting sort of rows by label: perm = rows of label 0, then 1, ...; cnt_ws = k int32.
+void launch_label_sort(const int32_t* labels, int64_t n, int64_t k, int32_t* perm, int32_t* cnt_ws,
+                       cudaStream_t st, const int* active = nullptr);
 // K4: exact FP32 direct re-check of flagged rows against all k prototypes.
 void launch_fixup(const float* X, int d, const float* P, int64_t k, const int32_t* flag_rows,
                   const int32_t* flag_count, int64_t max_flags, int32_t* labels, float* best,

@@ -467,13 +467,17 @@ __global__ void k_prep_protos(const float* __restrict__ P, int64_t k, int64_t k_
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     if (lane == 0 && cn2) cn2[j] = (float)s;
     if (Pb && kc > d) {
-      // columns beyond d: with `fold` [d] = ||c||^2 split (A side holds 1), [d+1] = 1 (A side
-      // ||x||^2); otherwise zeros
+      // columns beyond d: zeros, except with `fold` the K step F = d rounded up to 8 of the big part:
+      // [F] = ||c||^2 big, [F+1] = ||c||^2 small (A side: 1, 1), [F+2] = [F+3] = 1 (A side:
+      // ||x||^2 big, small)
       const float hb = tf32_rn((float)s);
       const float hs = tf32_rn((float)(s - (double)hb));
+      const int F = (d + 7) / 8 * 8;
       for (int i = d + lane; i < kc; i += 32) {
-        Pb[j * kc + i] = !fold ? 0.f : (i == d ? hb : (i == d + 1 ? 1.0f : 0.f));
-        Ps[j * kc + i] = (fold && i == d) ? hs : 0.f;
+        float v = 0.f;
+        if (fold && i >= F) v = i == F ? hb : (i == F + 1 ? hs : (i <= F + 3 ? 1.0f : 0.f));
+        Pb[j * kc + i] = v;
+        Ps[j * kc + i] = 0.f;
       }
     }
   }
@@ -483,7 +487,7 @@ __global__ void k_prep_protos(const float* __restrict__ P, int64_t k, int64_t k_
          e += (int64_t)gridDim.x * blockDim.x) {
       const int64_t j = k + e / kc;
       const int i = (int)(e % kc);
-      Pb[j * kc + i] = (fold && i == d) ? 1e30f : 0.f;
+      Pb[j * kc + i] = (fold && i == (d + 7) / 8 * 8) ? 1e30f : 0.f;
       Ps[j * kc + i] = 0.f;
     }
   }
@@ -797,6 +801,80 @@ void launch_children(const int32_t* labels, int64_t n, int64_t k, int64_t* offse
   k_scan_offsets<<<1, 1024, 0, st>>>(cursor_ws, k, offsets, cursor_ws);
   MASK_LAUNCH_CHECK();
   if (n > 0) k_scatter_members<<<grid_for(n, 256), 256, 0, st>>>(labels, n, cursor_ws, members);
+  MASK_LAUNCH_CHECK();
+}
+
+// Counting sort of row indices by label (K1 row order for warp-coherent pruning): perm lists
+// the rows of label 0, then label 1, ... (order inside a label unspecified).  Labels outside
+// [0, k) are skipped (their rows are appended by nobody: callers pass complete labelings).
+__global__ void k_sort_zero(int32_t* __restrict__ cnt, int64_t k, const int* __restrict__ active) {
+  if (active && !*active) return;
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < k; j += (int64_t)gridDim.x * blockDim.x)
+    cnt[j] = 0;
+}
+__global__ void k_sort_hist(const int32_t* __restrict__ labels, int64_t n, int64_t k, int32_t* __restrict__ cnt,
+                            const int* __restrict__ active) {
+  if (active && !*active) return;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t l = labels[i];
+    if (l >= 0 && l < k) atomicAdd(cnt + l, 1);
+  }
+}
+__global__ void __launch_bounds__(1024) k_sort_scan(int32_t* __restrict__ cnt, int64_t k, const int* __restrict__ active) {
+  if (active && !*active) return;
+  __shared__ int32_t warp_tot[32];
+  __shared__ int32_t carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int64_t base = 0; base < k; base += 1024) {
+    const int64_t j = base + threadIdx.x;
+    const int32_t v = j < k ? cnt[j] : 0;
+    int32_t incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    if (lane == 31) warp_tot[w] = incl;
+    __syncthreads();
+    if (w == 0) {
+      const int32_t t = warp_tot[lane];
+      int32_t ti = t;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int32_t u = __shfl_up_sync(0xffffffffu, ti, o);
+        if (lane >= o) ti += u;
+      }
+      warp_tot[lane] = ti - t;
+    }
+    __syncthreads();
+    const int32_t excl = carry + warp_tot[w] + incl - v;
+    if (j < k) cnt[j] = excl;  // becomes the scatter cursor
+    __syncthreads();
+    if (threadIdx.x == 1023) carry = excl + v;
+    __syncthreads();
+  }
+}
+__global__ void k_sort_scatter(const int32_t* __restrict__ labels, int64_t n, int64_t k, int32_t* __restrict__ cursor,
+                               int32_t* __restrict__ perm, const int* __restrict__ active) {
+  if (active && !*active) return;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t l = labels[i];
+    if (l >= 0 && l < k) perm[atomicAdd(cursor + l, 1)] = (int32_t)i;
+  }
+}
+
+void launch_label_sort(const int32_t* labels, int64_t n, int64_t k, int32_t* perm, int32_t* cnt_ws, cudaStream_t st,
+                       const int* active) {
+  if (n <= 0) return;
+  k_sort_zero<<<grid_for(k, 256), 256, 0, st>>>(cnt_ws, k, active);
+  MASK_LAUNCH_CHECK();
+  k_sort_hist<<<grid_for(n, 256), 256, 0, st>>>(labels, n, k, cnt_ws, active);
+  MASK_LAUNCH_CHECK();
+  k_sort_scan<<<1, 1024, 0, st>>>(cnt_ws, k, active);
+  MASK_LAUNCH_CHECK();
+  k_sort_scatter<<<grid_for(n, 256), 256, 0, st>>>(labels, n, k, cnt_ws, perm, active);
   MASK_LAUNCH_CHECK();
 }
 

@@ -230,6 +230,9 @@ void check_csr_structure(const mask_matrix* m, cudaStream_t st) {
 // Scratch of one level's Lloyd loop.
 struct LloydWS {
   DevBuf<int32_t> lab_prev, lab_cur;
+  DevBuf<int32_t> lab2;  // K1 second-best prototype of each row (pruning bound of the next pass)
+  DevBuf<int32_t> perm, sort_cnt;  // K1 row order: rows sorted by the previous pass's labels
+  bool have_prev = false;          // lab_prev holds a complete labeling (pass >= 1)
   DevBuf<float> best;
   DevBuf<float> S;
   DevBuf<int32_t> counts;
@@ -307,18 +310,31 @@ void assign_pass(const Input& in, const float* P, int64_t k, int flags, int32_t*
     ws.flag_count.alloc(1);
     ws.fix_keys.alloc((size_t)n);
     launch_fill(ws.cn2.p + k, k_pad - k, INFINITY, st);
+    ws.lab2.alloc(n);
+    MASK_CUDA(cudaMemsetAsync(ws.lab2.p, 0xff, sizeof(int32_t) * n, st));
   }
   if (!ws.xn2_ready) {
     ws.xn2.alloc(n);
     launch_row_norms(in.X, n, d, ws.xn2.p, st);
     ws.xn2_ready = true;
   }
-  launch_prep_protos(P, k, d, kc, ws.Pb.p, ws.Ps.p, ws.cn2.p, st, tc_operand_rows(k), d + 2 <= 32 ? 1 : 0, active);
+  launch_prep_protos(P, k, d, kc, ws.Pb.p, ws.Ps.p, ws.cn2.p, st, tc_operand_rows(k), d <= 24 ? 1 : 0, active);
   MASK_CUDA(cudaMemsetAsync(ws.flag_count.p, 0, sizeof(int32_t), st));
   ws.kernel_id = 1;
   if (ev) ev->mark(MASK_T_ASSIGN, st);
+  // small d (persistent K1): visit rows grouped by their previous label, so the rows of a warp
+  // share their nearest prototypes and the bound-pruned epilogue skips most chunks warp-wide
+  const int32_t* perm = nullptr;
+  if (ws.have_prev && d <= 24 && !(flags & MASK_NO_SORT)) {
+    if (!ws.perm.p) {
+      ws.perm.alloc(n);
+      ws.sort_cnt.alloc(k);
+    }
+    launch_label_sort(ws.lab_prev.p, n, k, ws.perm.p, ws.sort_cnt.p, st, active);
+    perm = ws.perm.p;
+  }
   launch_assign_tc(in.X, n, d, P, ws.Pb.p, ws.Ps.p, ws.cn2.p, k, ws.xn2.p, labels_out, best, ws.flag_rows.p,
-                   ws.flag_count.p, st, active);
+                   ws.flag_count.p, st, active, perm, ws.have_prev ? ws.lab_prev.p : nullptr, ws.lab2.p);
   if (ev) ev->mark(MASK_T_ASSIGN, st);
   // near-tie re-check (K4), sized on the device from the flagged count (no host round trip)
   if (!(flags & MASK_NO_FIXUP)) {
@@ -457,6 +473,7 @@ void run_level(const Input& in, int64_t k, const int64_t* init_idx_host, const m
     if (ev) ev->mark(MASK_T_FINALIZE, st);
     k_copy_labels<<<grid_for(n, 256), 256, 0, st>>>(ws.lab_prev.p, ws.lab_cur.p, n, active);
     MASK_LAUNCH_CHECK();
+    ws.have_prev = true;
     k_after_update<<<1, 1, 0, st>>>(ctrl.p, fin.p, t, p->tol, T);
     MASK_LAUNCH_CHECK();
     if (p->iter_cb) {
