@@ -118,24 +118,30 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 // Wait on the MMA issuer's / TMA producer's critical path: plain try_wait polling (the
 // suspend-hinted form adds ~100 cycles of wake-up latency per wait, which the per-tile control
 // path of a short-K tile cannot hide behind the tensor core's instruction queue).
+// Polls in unrolled groups of 16 so a waiting warp issues only try_wait + branch (no ALU
+// work competing with the epilogue's min trees); the bounded counter still traps on a hang.
 __device__ __forceinline__ void mbar_wait_spin(uint64_t* bar, uint32_t parity) {
   const uint32_t addr = smem_u32(bar);
   uint32_t spins = 0;
-  while (!mbar_try_wait(addr, parity)) {
-    if (++spins > (1u << 28)) __trap();
+  while (true) {
+#pragma unroll
+    for (int r = 0; r < 16; ++r)
+      if (mbar_try_wait(addr, parity)) return;
+    if (++spins > (1u << 24)) __trap();
   }
 }
 
 // Wait off the critical path (the A loader, a whole block of tiles ahead): back off with
 // __nanosleep between tests so the spin does not take issue slots from the epilogue.
+// Exponential back-off (64 ns .. 4 us) keeps a mostly idle warpgroup (the A loader / block
+// tail) from taking issue slots from the epilogue while it waits a block ahead.
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
   const uint32_t addr = smem_u32(bar);
-  uint32_t spins = 0;
+  uint32_t spins = 0, ns = 64;
   while (!mbar_try_wait(addr, parity)) {
-#if !defined(MASK_TC_SPIN_WAIT)
-    __nanosleep(200);
-#endif
-    if (++spins > (1u << 26)) __trap();
+    __nanosleep(ns);
+    ns = ns < 4096 ? 2 * ns : ns;
+    if (++spins > (1u << 24)) __trap();
   }
 }
 
@@ -289,6 +295,17 @@ constexpr int kTraceCtas = 4096;
 __device__ long long g_tc_trace[8][kTraceCtas];
 constexpr int kPT = 512;
 __device__ long long g_pt[9][kPT];
+// per-tile trace stamps (development builds with -DMASK_TC_TRACE only)
+#if defined(MASK_TC_TRACE)
+#define PT_STAMP(cond, row, idx) \
+  do {                           \
+    if (cond) g_pt[row][idx] = clock64(); \
+  } while (0)
+#else
+#define PT_STAMP(cond, row, idx) \
+  do {                           \
+  } while (0)
+#endif
 __device__ unsigned long long g_chunk_stats[4];  // debug bit 128: chunks seen / keyed
 __device__ __forceinline__ long long gtimer() {
   long long t;
@@ -725,7 +742,7 @@ __global__ void __launch_bounds__(256 + 128 * EPI_WG, 1)
       for (int64_t rb = blockIdx.x; rb < nblocks; rb += gridDim.x) {
         for (int t = 0; t < ntiles; ++t, ++gp) {
           mbar_wait_spin(&empty[stage], phase ^ 1);
-          if ((dbg & 8) && blockIdx.x == 0 && gp < kPT) g_pt[8][gp] = clock64();
+          PT_STAMP((dbg & 8) && blockIdx.x == 0 && gp < kPT, 8, gp);
           uint8_t* dst = Bst + stage * C::STAGE_BYTES;
           if (dbg & 4) {  // ablation: no B traffic
             mbar_arrive(&full[stage]);
@@ -749,7 +766,7 @@ __global__ void __launch_bounds__(256 + 128 * EPI_WG, 1)
     // queue (a single issuer left the pipe idle ~35% of the time at d = 16).
     static_assert((STAGES & (STAGES - 1)) == 0, "stage ring indexed by masking");
     const int par = warp == 1 ? 0 : 1;
-    int64_t g0 = 0;  // first global tile of the block
+    int g0 = 0;       // first global tile of the block
     int i = 0;       // block iteration of this CTA
     for (int64_t rb = blockIdx.x; rb < nblocks; rb += gridDim.x, ++i, g0 += ntiles) {
       const int first = (int)((g0 & 1) == par ? 0 : 1);  // this issuer's first tile of the block
@@ -760,7 +777,7 @@ __global__ void __launch_bounds__(256 + 128 * EPI_WG, 1)
       tc_fence_after();
       const uint32_t a_big = tmem_base + C::A_COL + 2 * KA * ab, a_small = a_big + KA;
       for (int t = first; t < ntiles; t += 2) {
-        const int64_t g = g0 + t;
+        const int g = g0 + t;
         const int stage = (int)(g & (STAGES - 1));
         const uint32_t phase = (uint32_t)((g / STAGES) & 1);
         const int acc = (int)(g % NACC);
@@ -768,10 +785,10 @@ __global__ void __launch_bounds__(256 + 128 * EPI_WG, 1)
         mbar_wait_spin(&tempty[acc], ((g / NACC) & 1) ^ 1);
         tc_fence_after();
         const bool ptr = (dbg & 8) && blockIdx.x == 0 && lane == 0 && g < kPT;
-        if (ptr) g_pt[0][g] = clock64();
+        PT_STAMP(ptr, 0, g);
         mbar_wait_spin(&full[stage], phase);
         tc_fence_after();
-        if (ptr) g_pt[1][g] = clock64();
+        PT_STAMP(ptr, 1, g);
         if (lane == 0) {
           const uint32_t bb = smem_u32(Bst + stage * C::STAGE_BYTES);
           const uint32_t bs = bb + C::B_CHUNK;
@@ -791,7 +808,7 @@ __global__ void __launch_bounds__(256 + 128 * EPI_WG, 1)
           // this issuer's MMAs on the block's A are done (aempty counts one arrive per issuer
           // that has tiles in the block)
           if (t == last) mma_commit(&aempty[ab]);
-          if (ptr) g_pt[7][g] = clock64();
+          PT_STAMP(ptr, 7, g);
         }
         __syncwarp();
       }
@@ -811,7 +828,7 @@ __global__ void __launch_bounds__(256 + 128 * EPI_WG, 1)
     const uint32_t lane_base = tmem_base + ((uint32_t)(q * 32) << 16);
     auto tail = [&](int ib) {  // block iteration ib of this CTA
       const int tb = ib & 1;
-      mbar_wait(&rfull[tb], (ib >> 1) & 1);
+      mbar_wait_sleep(&rfull[tb], (ib >> 1) & 1);
       const float* r1 = scratch + tb * 4 * BM * EPI_WG;
       const float* r2 = r1 + BM * EPI_WG;
       const int32_t* ri = reinterpret_cast<const int32_t*>(r2 + BM * EPI_WG);
@@ -879,7 +896,7 @@ __global__ void __launch_bounds__(256 + 128 * EPI_WG, 1)
       mbar_wait_sleep(&iempty[ab], ((i >> 1) & 1) ^ 1);
       tc_fence_after();
       const bool ptr = (dbg & 8) && blockIdx.x == 0 && rloc == 0 && i < 512;
-      if (ptr) g_pt[5][i] = clock64();
+      PT_STAMP(ptr, 5, i);
       const int64_t pos = rb * BM + rloc;
       const int64_t row = pos < n ? (perm ? (int64_t)__ldg(perm + pos) : pos) : n;
       const float xx = row < n ? __ldg(xn2 + row) : 0.f;
@@ -946,7 +963,7 @@ __global__ void __launch_bounds__(256 + 128 * EPI_WG, 1)
       tmem_wait_st();
       tc_fence_before();
       mbar_arrive_warp(&afull[ab]);
-      if (ptr) g_pt[6][i] = clock64();
+      PT_STAMP(ptr, 6, i);
       if (i >= 1) tail(i - 1);
     }
     if (i >= 1) tail(i - 1);
@@ -956,12 +973,12 @@ __global__ void __launch_bounds__(256 + 128 * EPI_WG, 1)
     const int wg = et >> 7;
     const int q = warp & 3;
     const int rloc = q * 32 + lane;
-    int64_t g = 0;
+    int g = 0;
     int i = 0;
     unsigned long long st_seen = 0, st_keyed = 0;
     for (int64_t rb = blockIdx.x; rb < nblocks; rb += gridDim.x, ++i) {
       const int ab = i & 1;
-      mbar_wait(&afull[ab], (i >> 1) & 1);  // block info published with the A block
+      mbar_wait_spin(&afull[ab], (i >> 1) & 1);  // block info published with the A block
       const int32_t ubk = s_ub[ab * BM + rloc];
       mbar_arrive_warp(&iempty[ab]);
       float g1 = INFINITY, g2 = INFINITY;
@@ -973,15 +990,15 @@ __global__ void __launch_bounds__(256 + 128 * EPI_WG, 1)
         mbar_wait_spin(&tfull[acc], (g / NACC) & 1);
         tc_fence_after();
         const bool ptr = (dbg & 8) && blockIdx.x == 0 && lane == 0 && q == 0 && g < 512;
-        if (ptr && wg == 0) g_pt[2][g] = clock64();
+        PT_STAMP(ptr && wg == 0, 2, g);
         const int col0 = wg * COLS;
         const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + col0);
         uint32_t r[2][32];
         if (dbg & 64) {  // ablation: no TMEM loads, no epilogue
           tc_fence_before();
           mbar_arrive_warp(&tempty[acc]);
-          if (ptr && wg == 0) g_pt[3][g] = clock64();
-          if (ptr && wg == EPI_WG - 1) g_pt[4][g] = clock64();
+          PT_STAMP(ptr && wg == 0, 3, g);
+          PT_STAMP(ptr && wg == EPI_WG - 1, 4, g);
           continue;
         }
         // all of this warpgroup's columns into registers, then release the accumulator before
@@ -991,8 +1008,8 @@ __global__ void __launch_bounds__(256 + 128 * EPI_WG, 1)
         tmem_wait_ld();
         tc_fence_before();
         mbar_arrive_warp(&tempty[acc]);
-        if (ptr && wg == 0) g_pt[3][g] = clock64();
-        if (ptr && wg == EPI_WG - 1) g_pt[4][g] = clock64();
+        PT_STAMP(ptr && wg == 0, 3, g);
+        PT_STAMP(ptr && wg == EPI_WG - 1, 4, g);
         // running top-2 keys of this tile; k2 starts at the pruning bound (low byte 0xFF marks
         // "no element": real keys carry a column < COLS in that byte)
         int32_t k1 = 0x7fffffff;
@@ -1018,7 +1035,7 @@ __global__ void __launch_bounds__(256 + 128 * EPI_WG, 1)
             ++st_seen;
             st_keyed += need ? 1 : 0;
           }
-          if (!need) continue;
+          if (!need || (dbg & 256)) continue;  // dbg 256 (ablation): never key
 #endif
           int32_t c1, c2;
           chunk_top2(r[cc & 1], key_mask, (uint32_t)(cc * 32), key_mask >> 31, c1, c2);
@@ -1047,7 +1064,7 @@ __global__ void __launch_bounds__(256 + 128 * EPI_WG, 1)
         }
       }
       // hand this warpgroup's per-row top-2 to the tail (loader warpgroup)
-      mbar_wait(&rempty[ab], ((i >> 1) & 1) ^ 1);
+      mbar_wait_spin(&rempty[ab], ((i >> 1) & 1) ^ 1);
       float* r1 = scratch + ab * 4 * BM * EPI_WG;
       float* r2 = r1 + BM * EPI_WG;
       int32_t* ri = reinterpret_cast<int32_t*>(r2 + BM * EPI_WG);
@@ -1084,6 +1101,9 @@ void dump_ptrace() {
             h[7][g] - h[1][g], h[2][g] - h[1][g], h[3][g] - h[1][g], h[4][g] - h[1][g], h[1][g] - h[1][g - 1]);
   for (int i = 1; i < 6; ++i)
     fprintf(stderr, "  block %d loader start %lld dur %lld (rel. tile %d full_ok)\n", i, h[5][i] - h[1][0], h[6][i] - h[5][i], 0);
+  fprintf(stderr, "  full_ok deltas tiles 1..%d:", kPT - 1);
+  for (int g = 1; g < 140; ++g) fprintf(stderr, "%s%lld", g % 22 == 0 ? " | " : " ", h[1][g] - h[1][g - 1]);
+  fprintf(stderr, "\n  total tiles 0..139: %lld cycles\n", h[1][139] - h[1][0]);
 }
 
 // Host dump of the development trace: per-phase medians (us) over the traced CTAs.
@@ -1226,13 +1246,11 @@ bool tc_supported(int64_t n, int d, int64_t k) {
   return n >= 1 && d >= 4 && d <= 128 && d % 4 == 0;
 }
 
-// B operand columns: d rounded up to 8 (zero columns beyond d), plus, for small d (d <= 24,
-// folded), one K step of 8 holding [||c||^2 big, ||c||^2 small, 1, 1, 0...]
-#if defined(MASK_TC_PAD32)
+// B operand columns: d rounded up to 8 (zero columns beyond d); small d (d <= 24, folded) holds
+// one more K step of 8 after the x columns, [||c||^2 big, ||c||^2 small, 1, 1, 0...]
+// Small d pads the rows to 32 columns (128 bytes): the TMA streams whole, aligned 128-byte
+// swizzle rows ~2.4x faster than 96-byte rows with an out-of-bounds tail (tools/tma_ubench.cu).
 int tc_operand_cols(int d) { return d <= 24 ? 32 : ((d + 7) / 8) * 8; }
-#else
-int tc_operand_cols(int d) { return ((d + 7) / 8) * 8 + (d <= 24 ? 8 : 0); }
-#endif
 // rows of the B operand arrays: padded to whole 256-prototype tiles (pad rows never win)
 int64_t tc_operand_rows(int64_t k) { return (k + 255) / 256 * 256 + 256; }
 
