@@ -149,8 +149,10 @@ void launch_assign_csr(const int64_t* row_ptr, const int32_t* col, const float* 
 void launch_transpose(const float* P, int64_t k, int d, float* PT, cudaStream_t st, const int* active = nullptr);
 
 // K5/K6: cluster sums and counts (S, counts must be zeroed by the caller).
+// perm (optional): rows sorted by these labels (launch_label_sort) -> run-accumulating kernel
 void launch_update_dense(const float* X, int64_t n, int d, const int32_t* labels, int64_t k,
-                         float* S, int32_t* counts, cudaStream_t st, const int* active = nullptr);
+                         float* S, int32_t* counts, cudaStream_t st, const int* active = nullptr,
+                         const int32_t* perm = nullptr);
 void launch_update_csr(const int64_t* row_ptr, const int32_t* col, const float* val, int64_t n,
                        int d, const int32_t* labels, float* S, int32_t* counts, cudaStream_t st,
                        const int* active = nullptr);

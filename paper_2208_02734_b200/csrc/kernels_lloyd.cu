@@ -560,11 +560,85 @@ __global__ void k_update_dense(const float* __restrict__ X, int64_t n, int d,
   }
 }
 
+// Rows visited in label-sorted order (perm from launch_label_sort of these labels, or of the
+// previous pass's: runs are then long but not perfect).  Each warp walks CH consecutive
+// positions; a row is covered by L = pow2 >= d/4 lanes (one float4 each), R = 32/L rows per
+// step.  Every lane group accumulates its run of equal labels in registers and flushes it with
+// one red.global.add.v4 per float4 when the label changes: a run of m rows costs d/4 vector
+// reds instead of m*d/4 (atomics were the limit of the element-parallel kernel).
+template <int L>
+__global__ void __launch_bounds__(256) k_update_runs(const float4* __restrict__ X4, const int32_t* __restrict__ perm,
+                                                      int64_t n, int d4, const int32_t* __restrict__ labels,
+                                                      float* __restrict__ S, int32_t* __restrict__ counts,
+                                                      const int* __restrict__ active) {
+  if (active && !*active) return;  // level converged: this pass is skipped on the device
+  constexpr int R = 32 / L, U = 4, CH = R * U * 4;  // 4 batches of U independent rows per lane group
+  const int lane = threadIdx.x & 31, slot = lane / L, c4 = lane % L;
+  const int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int64_t p0 = w * CH;
+  if (p0 >= n) return;
+  const int64_t p1 = p0 + CH < n ? p0 + CH : n;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  int32_t cur = -1, cnt = 0;
+  auto flush = [&]() {
+    if (c4 < d4)
+      asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(S + ((int64_t)cur * d4 + c4) * 4),
+                   "f"(acc.x), "f"(acc.y), "f"(acc.z), "f"(acc.w)
+                   : "memory");
+    if (c4 == 0) atomicAdd(counts + cur, cnt);
+  };
+  for (int64_t pb = p0 + slot; pb < p1; pb += R * U) {
+    // U independent rows in flight per lane group (perm -> label, row -> x) before reducing
+    int64_t row[U];
+    int32_t lab[U];
+    float4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t p = pb + (int64_t)u * R;
+      row[u] = p < p1 ? (perm ? (int64_t)__ldg(perm + p) : p) : -1;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      lab[u] = row[u] >= 0 ? __ldg(labels + row[u]) : -1;
+      v[u] = (row[u] >= 0 && c4 < d4) ? __ldg(X4 + row[u] * d4 + c4) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (lab[u] < 0) continue;
+      if (lab[u] != cur) {
+        if (cur >= 0) flush();
+        cur = lab[u];
+        acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        cnt = 0;
+      }
+      acc.x += v[u].x;
+      acc.y += v[u].y;
+      acc.z += v[u].z;
+      acc.w += v[u].w;
+      ++cnt;
+    }
+  }
+  if (cur >= 0) flush();
+}
+
 void launch_update_dense(const float* X, int64_t n, int d, const int32_t* labels, int64_t k,
-                         float* S, int32_t* counts, cudaStream_t st, const int* active) {
+                         float* S, int32_t* counts, cudaStream_t st, const int* active, const int32_t* perm) {
   (void)k;
   if (n <= 0) return;
-  if (d % 4 == 0 && ((uintptr_t)X % 16) == 0) {
+  if (perm && d % 4 == 0 && d <= 128 && ((uintptr_t)X % 16) == 0) {
+    const int d4 = d / 4;
+    const int L = d4 <= 1 ? 1 : d4 <= 2 ? 2 : d4 <= 4 ? 4 : d4 <= 8 ? 8 : d4 <= 16 ? 16 : 32;
+    const int64_t ch = (32 / L) * 16;  // positions per warp (k_update_runs CH)
+    const int64_t warps = (n + ch - 1) / ch;
+    const unsigned grid = (unsigned)((warps + 7) / 8);
+    const float4* X4 = reinterpret_cast<const float4*>(X);
+    if (d4 <= 1) k_update_runs<1><<<grid, 256, 0, st>>>(X4, perm, n, d4, labels, S, counts, active);
+    else if (d4 <= 2) k_update_runs<2><<<grid, 256, 0, st>>>(X4, perm, n, d4, labels, S, counts, active);
+    else if (d4 <= 4) k_update_runs<4><<<grid, 256, 0, st>>>(X4, perm, n, d4, labels, S, counts, active);
+    else if (d4 <= 8) k_update_runs<8><<<grid, 256, 0, st>>>(X4, perm, n, d4, labels, S, counts, active);
+    else if (d4 <= 16) k_update_runs<16><<<grid, 256, 0, st>>>(X4, perm, n, d4, labels, S, counts, active);
+    else k_update_runs<32><<<grid, 256, 0, st>>>(X4, perm, n, d4, labels, S, counts, active);
+  } else if (d % 4 == 0 && ((uintptr_t)X % 16) == 0) {
     const int d4 = d / 4;
     k_update_dense_v4<<<grid_for(n * d4, 256, (int64_t)num_sms() * 16), 256, 0, st>>>(
         reinterpret_cast<const float4*>(X), n, d4, labels, S, counts, active);

@@ -231,8 +231,9 @@ void check_csr_structure(const mask_matrix* m, cudaStream_t st) {
 struct LloydWS {
   DevBuf<int32_t> lab_prev, lab_cur;
   DevBuf<int32_t> lab2;  // K1 second-best prototype of each row (pruning bound of the next pass)
-  DevBuf<int32_t> perm, sort_cnt;  // K1 row order: rows sorted by the previous pass's labels
+  DevBuf<int32_t> perm, sort_cnt;  // rows sorted by the last pass's labels (update + next K1)
   bool have_prev = false;          // lab_prev holds a complete labeling (pass >= 1)
+  bool have_perm = false;          // perm is sorted by lab_prev's labels
   DevBuf<float> best;
   DevBuf<float> S;
   DevBuf<int32_t> counts;
@@ -322,17 +323,10 @@ void assign_pass(const Input& in, const float* P, int64_t k, int flags, int32_t*
   MASK_CUDA(cudaMemsetAsync(ws.flag_count.p, 0, sizeof(int32_t), st));
   ws.kernel_id = 1;
   if (ev) ev->mark(MASK_T_ASSIGN, st);
-  // small d (persistent K1): visit rows grouped by their previous label, so the rows of a warp
-  // share their nearest prototypes and the bound-pruned epilogue skips most chunks warp-wide
-  const int32_t* perm = nullptr;
-  if (ws.have_prev && d <= 24 && !(flags & MASK_NO_SORT)) {
-    if (!ws.perm.p) {
-      ws.perm.alloc(n);
-      ws.sort_cnt.alloc(k);
-    }
-    launch_label_sort(ws.lab_prev.p, n, k, ws.perm.p, ws.sort_cnt.p, st, active);
-    perm = ws.perm.p;
-  }
+  // small d (persistent K1): visit rows grouped by their previous label (perm, sorted after
+  // the previous pass), so the rows of a warp share their nearest prototypes and the
+  // bound-pruned epilogue skips most chunks warp-wide
+  const int32_t* perm = (ws.have_perm && !(flags & MASK_NO_SORT)) ? ws.perm.p : nullptr;
   launch_assign_tc(in.X, n, d, P, ws.Pb.p, ws.Ps.p, ws.cn2.p, k, ws.xn2.p, labels_out, best, ws.flag_rows.p,
                    ws.flag_count.p, st, active, perm, ws.have_prev ? ws.lab_prev.p : nullptr, ws.lab2.p);
   if (ev) ev->mark(MASK_T_ASSIGN, st);
@@ -455,12 +449,24 @@ void run_level(const Input& in, int64_t k, const int64_t* init_idx_host, const m
       if (h[0] || h[1] == t + 1) emit_cb(t, P_snap.p, ws.lab_cur.p);
       if (!h[0]) break;
     }
+    // ---- rows sorted by this pass's labels: run-accumulated update now, warp-coherent K1 rows
+    // in the next pass (its previous labels are these)
+    const bool sorted = in.format == MASK_DENSE_F32 && !(p->flags & MASK_NO_SORT) && n >= 4096;
+    if (sorted) {
+      if (!ws.perm.p) {
+        ws.perm.alloc(n);
+        ws.sort_cnt.alloc(k);
+      }
+      launch_label_sort(ws.lab_cur.p, n, k, ws.perm.p, ws.sort_cnt.p, st, active);
+      ws.have_perm = true;
+    }
     // ---- update: S_j, n_j (K5/K6) -> allreduce (N1) -> P_j = S_j / n_j (K7)
     if (ev) ev->mark(MASK_T_UPDATE, st);
     if (in.format == MASK_CSR_F32)
       launch_update_csr(in.rp, in.col, in.val, n, d, ws.lab_cur.p, ws.S.p, ws.counts.p, st, active);
     else
-      launch_update_dense(in.X, n, d, ws.lab_cur.p, k, ws.S.p, ws.counts.p, st, active);
+      launch_update_dense(in.X, n, d, ws.lab_cur.p, k, ws.S.p, ws.counts.p, st, active,
+                          sorted ? ws.perm.p : nullptr);
     if (ev) ev->mark(MASK_T_UPDATE, st);
     if (comm) {
       MASK_NCCL(ncclGroupStart());
