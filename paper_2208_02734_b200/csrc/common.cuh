@@ -120,8 +120,12 @@ void launch_assign_tc(const float* X, int64_t n, int d, const float* P, const fl
                       cudaStream_t st, const int* active = nullptr, const int32_t* perm = nullptr,
                       const int32_t* prev_lab = nullptr, int32_t* lab2 = nullptr);
 // Counting sort of rows by label: perm = rows of label 0, then 1, ...; cnt_ws = k int32.
-void launch_label_sort(const int32_t* labels, int64_t n, int64_t k, int32_t* perm, int32_t* cnt_ws,
-                       cudaStream_t st, const int* active = nullptr);
+// perm_old (optional): a previous sort, visited in its order (equal labels adjacent -> warp-
+// aggregated atomics); perm must not alias it.  copy_to (optional): copy_to[row] = labels[row].
+// cnt_zeroed: cnt_ws is already zero (the Lloyd loop's finalize zeroes it for the next sort).
+void launch_label_sort(const int32_t* labels, int64_t n, int64_t k, const int32_t* perm_old, int32_t* perm,
+                       int32_t* cnt_ws, int32_t* copy_to, cudaStream_t st, const int* active = nullptr,
+                       bool cnt_zeroed = false);
 // K4: exact FP32 direct re-check of flagged rows against all k prototypes.
 void launch_fixup(const float* X, int d, const float* P, int64_t k, const int32_t* flag_rows,
                   const int32_t* flag_count, int64_t max_flags, int32_t* labels, float* best,
@@ -136,8 +140,10 @@ void launch_fixup_tiled(const float* X, int d, const float* P, int64_t k, const 
                         cudaStream_t st);
 // prototype operands for K1: Pb = tf32_rn(-2c), Ps = tf32_rn(-2c - Pb), cn2 = ||c||^2; with
 // kc > d the augmented columns [d] = split(||c||^2), [d+1] = (1, 0), rest 0 (row stride kc)
+// flag_count (optional): reset to 0 (the list K1 appends near-tie rows to)
 void launch_prep_protos(const float* P, int64_t k, int d, int kc, float* Pb, float* Ps, float* cn2,
-                        cudaStream_t st, int64_t k_rows, int fold, const int* active = nullptr);
+                        cudaStream_t st, int64_t k_rows, int fold, const int* active = nullptr,
+                        int32_t* flag_count = nullptr);
 // rows of the K1 B operand arrays (k padded to whole 256-prototype tiles)
 int64_t tc_operand_rows(int64_t k);
 void launch_row_norms(const float* X, int64_t n, int d, float* xn2, cudaStream_t st);
@@ -156,13 +162,24 @@ void launch_update_dense(const float* X, int64_t n, int d, const int32_t* labels
 void launch_update_csr(const int64_t* row_ptr, const int32_t* col, const float* val, int64_t n,
                        int d, const int32_t* labels, float* S, int32_t* counts, cudaStream_t st,
                        const int* active = nullptr);
+// Device-side Lloyd loop control fused into the last block of a per-pass kernel:
+// ctrl = {active, passes run, stats ticket, finalize ticket}; t = pass, T = iteration cap.
+struct LoopCtl {
+  int* ctrl = nullptr;
+  int t = 0, T = 0;
+  double tol = 0.0;
+  int32_t* zero_cnt = nullptr;  // finalize: also zero these k counters (label sort)
+};
 // K7: P_j <- S_j / n_j (keep if n_j == 0); zeroes S and counts; stats[0] = max disp^2 (as
-// float bits, atomicMax), stats[1] = empties.  `stat` must be zeroed by the caller.
+// float bits, atomicMax), stats[1] = empties.  `stat` must be zeroed by the caller.  With
+// lc.ctrl: the tolerance stop / pass count of the loop (k_after_update's logic) in the last block.
 void launch_finalize(float* P, float* S, int32_t* counts, int64_t k, int d, uint32_t* stat,
-                     int keep_counts, cudaStream_t st, const int* active = nullptr);
-// pass statistics: J = sum best (double), changed = #(cur != prev)
+                     int keep_counts, cudaStream_t st, const int* active = nullptr, LoopCtl lc = LoopCtl());
+// pass statistics: J = sum best (double), changed = #(cur != prev).  With lc.ctrl: the
+// no-change stop test (k_after_stats's logic, single GPU) in the last block.
 void launch_pass_stats(const int32_t* cur, const int32_t* prev, const float* best, int64_t n,
-                       double* J, unsigned long long* changed, cudaStream_t st, const int* active = nullptr);
+                       double* J, unsigned long long* changed, cudaStream_t st, const int* active = nullptr,
+                       LoopCtl lc = LoopCtl());
 // K10: P[j] = Y[idx[j]] (dense) / densified CSR row
 void launch_gather_rows(const float* Y, int d, const int64_t* idx, int64_t k, int64_t row_offset,
                         int64_t n_local, float* P, cudaStream_t st);

@@ -448,8 +448,9 @@ __device__ __forceinline__ float tf32_rn(float x) {
 // the factor -2 is exact), cn2 = ||c||^2 accumulated in FP64 then rounded.
 __global__ void k_prep_protos(const float* __restrict__ P, int64_t k, int64_t k_rows, int d, int kc, int fold,
                               float* __restrict__ Pb, float* __restrict__ Ps, float* __restrict__ cn2,
-                              const int* __restrict__ active) {
+                              const int* __restrict__ active, int32_t* __restrict__ flag_count) {
   if (active && !*active) return;  // level converged: this pass is skipped on the device
+  if (flag_count && blockIdx.x == 0 && threadIdx.x == 0) *flag_count = 0;  // K1's near-tie list
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t j = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); j < k; j += warps) {
@@ -494,14 +495,15 @@ __global__ void k_prep_protos(const float* __restrict__ P, int64_t k, int64_t k_
 }
 
 void launch_prep_protos(const float* P, int64_t k, int d, int kc, float* Pb, float* Ps, float* cn2,
-                        cudaStream_t st, int64_t k_rows, int fold, const int* active) {
+                        cudaStream_t st, int64_t k_rows, int fold, const int* active, int32_t* flag_count) {
   if (k_rows < k) k_rows = k;
-  k_prep_protos<<<grid_for(k * 32, 256), 256, 0, st>>>(P, k, k_rows, d, kc, fold, Pb, Ps, cn2, active);
+  k_prep_protos<<<grid_for(k * 32, 256), 256, 0, st>>>(P, k, k_rows, d, kc, fold, Pb, Ps, cn2, active,
+                                                       flag_count);
   MASK_LAUNCH_CHECK();
 }
 
 void launch_level_norms(const float* P, int64_t k, int d, float* cn2, cudaStream_t st, const int* active) {
-  launch_prep_protos(P, k, d, d, nullptr, nullptr, cn2, st, k, 0, active);
+  launch_prep_protos(P, k, d, d, nullptr, nullptr, cn2, st, k, 0, active, nullptr);
 }
 
 __global__ void k_row_norms(const float* __restrict__ X, int64_t n, int d, float* __restrict__ xn2) {
@@ -680,13 +682,29 @@ void launch_update_csr(const int64_t* row_ptr, const int32_t* col, const float* 
 // Warp per prototype.  stat[0] = max over j of ||c_new - c_old||^2 (float bits, atomicMax on
 // non-negative floats), stat[1] = number of empty prototypes.  S and counts are zeroed for
 // the next pass (unless keep_counts, which leaves counts for the caller to read).
+// Last block of a grid (ticket counter, reset by that block): true in exactly one block,
+// after every block's earlier global writes/atomics are visible.
+__device__ __forceinline__ bool last_block_done(int* ticket) {
+  __shared__ int last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    last = atomicAdd(ticket, 1) == (int)gridDim.x - 1;
+    if (last) *ticket = 0;
+  }
+  __syncthreads();
+  if (last) __threadfence();
+  return last;
+}
+
 __global__ void k_finalize(float* __restrict__ P, float* __restrict__ S, int32_t* __restrict__ counts,
                            int64_t k, int d, uint32_t* __restrict__ stat, int keep_counts,
-                           const int* __restrict__ active) {
+                           const int* __restrict__ active, LoopCtl lc) {
   if (active && !*active) return;  // level converged: this pass is skipped on the device
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t j = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); j < k; j += warps) {
+    if (lc.zero_cnt && lane == 0) lc.zero_cnt[j] = 0;  // label-sort counts of the next pass
     const int32_t cnt = counts[j];
     float disp = 0.f;
     if (cnt > 0) {
@@ -707,18 +725,29 @@ __global__ void k_finalize(float* __restrict__ P, float* __restrict__ S, int32_t
       if (!keep_counts) counts[j] = 0;
     }
   }
+  // fused loop control (D3 tolerance stop / pass count), formerly a separate 1-thread kernel
+  if (lc.ctrl && last_block_done(lc.ctrl + 3) && threadIdx.x == 0) {
+    const double disp = sqrt((double)__uint_as_float(*(volatile uint32_t*)stat));
+    if (lc.tol > 0.0 && disp <= lc.tol) {
+      lc.ctrl[0] = 0;
+      lc.ctrl[1] = lc.t + 1;
+    } else if (lc.t == lc.T - 1) {
+      lc.ctrl[1] = lc.T;
+    }
+  }
 }
 
 void launch_finalize(float* P, float* S, int32_t* counts, int64_t k, int d, uint32_t* stat,
-                     int keep_counts, cudaStream_t st, const int* active) {
-  k_finalize<<<grid_for(k * 32, 256), 256, 0, st>>>(P, S, counts, k, d, stat, keep_counts, active);
+                     int keep_counts, cudaStream_t st, const int* active, LoopCtl lc) {
+  k_finalize<<<grid_for(k * 32, 256), 256, 0, st>>>(P, S, counts, k, d, stat, keep_counts, active, lc);
   MASK_LAUNCH_CHECK();
 }
 
 // ====================================================================== pass statistics
 __global__ void k_pass_stats(const int32_t* __restrict__ cur, const int32_t* __restrict__ prev,
                              const float* __restrict__ best, int64_t n, double* __restrict__ J,
-                             unsigned long long* __restrict__ changed, const int* __restrict__ active) {
+                             unsigned long long* __restrict__ changed, const int* __restrict__ active,
+                             LoopCtl lc) {
   if (active && !*active) return;  // level converged: this pass is skipped on the device
   double s = 0.0;
   unsigned long long c = 0;
@@ -754,13 +783,20 @@ __global__ void k_pass_stats(const int32_t* __restrict__ cur, const int32_t* __r
       atomicAdd(changed, c);
     }
   }
+  // fused stop test (single GPU): no label changed -> the update would be a no-op
+  if (lc.ctrl && last_block_done(lc.ctrl + 2) && threadIdx.x == 0) {
+    if (lc.t > 0 && *(volatile unsigned long long*)changed == 0) {
+      lc.ctrl[0] = 0;
+      lc.ctrl[1] = lc.t + 1;
+    }
+  }
 }
 
 void launch_pass_stats(const int32_t* cur, const int32_t* prev, const float* best, int64_t n,
-                       double* J, unsigned long long* changed, cudaStream_t st, const int* active) {
+                       double* J, unsigned long long* changed, cudaStream_t st, const int* active, LoopCtl lc) {
   if (n <= 0) return;
   k_pass_stats<<<grid_for(n, 256, (int64_t)num_sms() * 4), 256, 0, st>>>(cur, prev, best, n, J,
-                                                                         changed, active);
+                                                                         changed, active, lc);
   MASK_LAUNCH_CHECK();
 }
 
@@ -886,12 +922,27 @@ __global__ void k_sort_zero(int32_t* __restrict__ cnt, int64_t k, const int* __r
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < k; j += (int64_t)gridDim.x * blockDim.x)
     cnt[j] = 0;
 }
-__global__ void k_sort_hist(const int32_t* __restrict__ labels, int64_t n, int64_t k, int32_t* __restrict__ cnt,
+// Positions are visited in the previous pass's sorted order (perm_old, or identity), where
+// equal labels are mostly adjacent: a warp aggregates equal labels with __match_any_sync and
+// one lane does the atomic for the group, so the count / cursor atomics hit each label about
+// once per warp instead of once per row.  copy_to (optional) receives labels[row] (the
+// lab_prev <- lab_cur copy of the Lloyd loop, fused here).
+__global__ void k_sort_hist(const int32_t* __restrict__ labels, const int32_t* __restrict__ perm_old, int64_t n,
+                            int64_t k, int32_t* __restrict__ cnt, int32_t* __restrict__ copy_to,
                             const int* __restrict__ active) {
   if (active && !*active) return;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t l = labels[i];
-    if (l >= 0 && l < k) atomicAdd(cnt + l, 1);
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += stride) {
+    const int64_t p = base + threadIdx.x;
+    int32_t l = -1;
+    if (p < n) {
+      const int64_t row = perm_old ? (int64_t)__ldg(perm_old + p) : p;
+      l = labels[row];
+      if (copy_to) copy_to[row] = l;
+    }
+    const unsigned peers = __match_any_sync(0xffffffffu, l);
+    if (l >= 0 && l < k && lane == __ffs(peers) - 1) atomicAdd(cnt + l, __popc(peers));
   }
 }
 __global__ void __launch_bounds__(1024) k_sort_scan(int32_t* __restrict__ cnt, int64_t k, const int* __restrict__ active) {
@@ -930,25 +981,42 @@ __global__ void __launch_bounds__(1024) k_sort_scan(int32_t* __restrict__ cnt, i
     __syncthreads();
   }
 }
-__global__ void k_sort_scatter(const int32_t* __restrict__ labels, int64_t n, int64_t k, int32_t* __restrict__ cursor,
-                               int32_t* __restrict__ perm, const int* __restrict__ active) {
+__global__ void k_sort_scatter(const int32_t* __restrict__ labels, const int32_t* __restrict__ perm_old, int64_t n,
+                               int64_t k, int32_t* __restrict__ cursor, int32_t* __restrict__ perm,
+                               const int* __restrict__ active) {
   if (active && !*active) return;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t l = labels[i];
-    if (l >= 0 && l < k) perm[atomicAdd(cursor + l, 1)] = (int32_t)i;
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += stride) {
+    const int64_t p = base + threadIdx.x;
+    int32_t l = -1;
+    int64_t row = 0;
+    if (p < n) {
+      row = perm_old ? (int64_t)__ldg(perm_old + p) : p;
+      l = labels[row];
+    }
+    const unsigned peers = __match_any_sync(0xffffffffu, l);
+    const int leader = __ffs(peers) - 1;
+    int32_t pos = 0;
+    if (l >= 0 && l < k && lane == leader) pos = atomicAdd(cursor + l, __popc(peers));
+    pos = __shfl_sync(0xffffffffu, pos, leader);
+    if (l >= 0 && l < k) perm[pos + __popc(peers & ((1u << lane) - 1))] = (int32_t)row;
   }
 }
 
-void launch_label_sort(const int32_t* labels, int64_t n, int64_t k, int32_t* perm, int32_t* cnt_ws, cudaStream_t st,
-                       const int* active) {
+void launch_label_sort(const int32_t* labels, int64_t n, int64_t k, const int32_t* perm_old, int32_t* perm,
+                       int32_t* cnt_ws, int32_t* copy_to, cudaStream_t st, const int* active, bool cnt_zeroed) {
   if (n <= 0) return;
-  k_sort_zero<<<grid_for(k, 256), 256, 0, st>>>(cnt_ws, k, active);
-  MASK_LAUNCH_CHECK();
-  k_sort_hist<<<grid_for(n, 256), 256, 0, st>>>(labels, n, k, cnt_ws, active);
+  if (!cnt_zeroed) {
+    k_sort_zero<<<grid_for(k, 256), 256, 0, st>>>(cnt_ws, k, active);
+    MASK_LAUNCH_CHECK();
+  }
+  const unsigned grid = grid_for(n, 256, (int64_t)num_sms() * 8);
+  k_sort_hist<<<grid, 256, 0, st>>>(labels, perm_old, n, k, cnt_ws, copy_to, active);
   MASK_LAUNCH_CHECK();
   k_sort_scan<<<1, 1024, 0, st>>>(cnt_ws, k, active);
   MASK_LAUNCH_CHECK();
-  k_sort_scatter<<<grid_for(n, 256), 256, 0, st>>>(labels, n, k, cnt_ws, perm, active);
+  k_sort_scatter<<<grid, 256, 0, st>>>(labels, perm_old, n, k, cnt_ws, perm, active);
   MASK_LAUNCH_CHECK();
 }
 

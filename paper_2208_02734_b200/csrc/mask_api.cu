@@ -232,6 +232,7 @@ struct LloydWS {
   DevBuf<int32_t> lab_prev, lab_cur;
   DevBuf<int32_t> lab2;  // K1 second-best prototype of each row (pruning bound of the next pass)
   DevBuf<int32_t> perm, sort_cnt;  // rows sorted by the last pass's labels (update + next K1)
+  DevBuf<int32_t> perm_old;        // the sort before (visit order of the next sort)
   bool have_prev = false;          // lab_prev holds a complete labeling (pass >= 1)
   bool have_perm = false;          // perm is sorted by lab_prev's labels
   DevBuf<float> best;
@@ -319,8 +320,8 @@ void assign_pass(const Input& in, const float* P, int64_t k, int flags, int32_t*
     launch_row_norms(in.X, n, d, ws.xn2.p, st);
     ws.xn2_ready = true;
   }
-  launch_prep_protos(P, k, d, kc, ws.Pb.p, ws.Ps.p, ws.cn2.p, st, tc_operand_rows(k), d <= 24 ? 1 : 0, active);
-  MASK_CUDA(cudaMemsetAsync(ws.flag_count.p, 0, sizeof(int32_t), st));
+  launch_prep_protos(P, k, d, kc, ws.Pb.p, ws.Ps.p, ws.cn2.p, st, tc_operand_rows(k), d <= 24 ? 1 : 0, active,
+                     ws.flag_count.p);
   ws.kernel_id = 1;
   if (ev) ev->mark(MASK_T_ASSIGN, st);
   // small d (persistent K1): visit rows grouped by their previous label (perm, sorted after
@@ -347,16 +348,6 @@ __global__ void k_after_stats(int* ctrl, const unsigned long long* changed, int 
     ctrl[1] = t + 1;
   }
 }
-__global__ void k_after_update(int* ctrl, const uint32_t* fin, int t, double tol, int T) {
-  if (!ctrl[0]) return;
-  const double disp = sqrt((double)__uint_as_float(fin[2 * t]));
-  if (tol > 0.0 && disp <= tol) {  // D3 tolerance stop
-    ctrl[0] = 0;
-    ctrl[1] = t + 1;
-  } else if (t == T - 1) {
-    ctrl[1] = T;
-  }
-}
 __global__ void k_copy_labels(int32_t* __restrict__ dst, const int32_t* __restrict__ src, int64_t n,
                               const int* __restrict__ active) {
   if (active && !*active) return;
@@ -369,7 +360,7 @@ __global__ void k_copy_labels(int32_t* __restrict__ dst, const int32_t* __restri
 //   P <- means (empty keeps, D5); stop if tol > 0 and max displacement <= tol;
 //   final assignment -> labels.
 // The whole loop is enqueued at once: the stop tests run on the device (k_after_stats,
-// k_after_update) and later passes become no-ops, so the host synchronises once per level
+// the last blocks of k_pass_stats / k_finalize) and later passes become no-ops, so the host synchronises once per level
 // (unless the test-only iteration callback needs host copies after every pass).
 void run_level(const Input& in, int64_t k, const int64_t* init_idx_host, const mask_build_params* p,
                mask_comm* comm, int level_no, cudaStream_t st, Level& L, HostStats& hs) {
@@ -426,8 +417,8 @@ void run_level(const Input& in, int64_t k, const int64_t* init_idx_host, const m
   if (p->iter_cb) P_snap.alloc((size_t)k * d);
 
   // pass statistics into slot `slot`, combined over ranks (no host round trip)
-  auto pass_stats = [&](int slot, const int* act) {
-    launch_pass_stats(ws.lab_cur.p, ws.lab_prev.p, ws.best.p, n, Jd.p + slot, chd.p + slot, st, act);
+  auto pass_stats = [&](int slot, const int* act, LoopCtl lc) {
+    launch_pass_stats(ws.lab_cur.p, ws.lab_prev.p, ws.best.p, n, Jd.p + slot, chd.p + slot, st, act, lc);
     if (comm) {
       MASK_NCCL(ncclGroupStart());
       MASK_NCCL(ncclAllReduce(Jd.p + slot, Jd.p + slot, 1, ncclDouble, ncclSum, comm->comm, st));
@@ -439,9 +430,16 @@ void run_level(const Input& in, int64_t k, const int64_t* init_idx_host, const m
   for (int t = 0; t < T; ++t) {
     if (p->iter_cb) MASK_CUDA(cudaMemcpyAsync(P_snap.p, L.P.p, sizeof(float) * k * d, cudaMemcpyDeviceToDevice, st));
     assign_pass(in, L.P.p, k, p->flags, ws.lab_cur.p, ws.best.p, ws, st, active, ev.get());
-    pass_stats(t, active);
-    k_after_stats<<<1, 1, 0, st>>>(ctrl.p, chd.p, t);
-    MASK_LAUNCH_CHECK();
+    LoopCtl lc;
+    lc.t = t;
+    lc.T = T;
+    lc.tol = p->tol;
+    if (!comm) lc.ctrl = ctrl.p;  // single GPU: stop test fused into the stats kernel
+    pass_stats(t, active, lc);
+    if (comm) {  // the combined statistics decide (identically on every rank)
+      k_after_stats<<<1, 1, 0, st>>>(ctrl.p, chd.p, t);
+      MASK_LAUNCH_CHECK();
+    }
     if (p->iter_cb) {  // host view of the control state (test-only path)
       int h[4];
       MASK_CUDA(cudaMemcpyAsync(h, ctrl.p, sizeof(h), cudaMemcpyDeviceToHost, st));
@@ -452,12 +450,18 @@ void run_level(const Input& in, int64_t k, const int64_t* init_idx_host, const m
     // ---- rows sorted by this pass's labels: run-accumulated update now, warp-coherent K1 rows
     // in the next pass (its previous labels are these)
     const bool sorted = in.format == MASK_DENSE_F32 && !(p->flags & MASK_NO_SORT) && n >= 4096;
+    // (the sort also performs the lab_prev <- lab_cur copy; a skipped pass leaves the buffers
+    // swapped on the host, which only changes a row order: every consumer accepts any order)
     if (sorted) {
       if (!ws.perm.p) {
         ws.perm.alloc(n);
+        ws.perm_old.alloc(n);
         ws.sort_cnt.alloc(k);
+        MASK_CUDA(cudaMemsetAsync(ws.sort_cnt.p, 0, sizeof(int32_t) * k, st));
       }
-      launch_label_sort(ws.lab_cur.p, n, k, ws.perm.p, ws.sort_cnt.p, st, active);
+      std::swap(ws.perm, ws.perm_old);
+      launch_label_sort(ws.lab_cur.p, n, k, ws.have_perm ? ws.perm_old.p : nullptr, ws.perm.p, ws.sort_cnt.p,
+                        ws.lab_prev.p, st, active, /*cnt_zeroed=*/true);
       ws.have_perm = true;
     }
     // ---- update: S_j, n_j (K5/K6) -> allreduce (N1) -> P_j = S_j / n_j (K7)
@@ -475,13 +479,16 @@ void run_level(const Input& in, int64_t k, const int64_t* init_idx_host, const m
       MASK_NCCL(ncclGroupEnd());
     }
     if (ev) ev->mark(MASK_T_FINALIZE, st);
-    launch_finalize(L.P.p, ws.S.p, ws.counts.p, k, d, fin.p + 2 * t, 0, st, active);
+    LoopCtl lf = lc;
+    lf.ctrl = ctrl.p;  // tolerance stop / pass count (fin is identical on every rank)
+    lf.zero_cnt = sorted ? ws.sort_cnt.p : nullptr;
+    launch_finalize(L.P.p, ws.S.p, ws.counts.p, k, d, fin.p + 2 * t, 0, st, active, lf);
     if (ev) ev->mark(MASK_T_FINALIZE, st);
-    k_copy_labels<<<grid_for(n, 256), 256, 0, st>>>(ws.lab_prev.p, ws.lab_cur.p, n, active);
-    MASK_LAUNCH_CHECK();
+    if (!sorted) {
+      k_copy_labels<<<grid_for(n, 256), 256, 0, st>>>(ws.lab_prev.p, ws.lab_cur.p, n, active);
+      MASK_LAUNCH_CHECK();
+    }
     ws.have_prev = true;
-    k_after_update<<<1, 1, 0, st>>>(ctrl.p, fin.p, t, p->tol, T);
-    MASK_LAUNCH_CHECK();
     if (p->iter_cb) {
       int h[4];
       MASK_CUDA(cudaMemcpyAsync(h, ctrl.p, sizeof(h), cudaMemcpyDeviceToHost, st));
@@ -492,7 +499,7 @@ void run_level(const Input& in, int64_t k, const int64_t* init_idx_host, const m
   // ---- final assignment with the final prototypes (D3): always runs, stats into slot T+1
   if (p->iter_cb) MASK_CUDA(cudaMemcpyAsync(P_snap.p, L.P.p, sizeof(float) * k * d, cudaMemcpyDeviceToDevice, st));
   assign_pass(in, L.P.p, k, p->flags, ws.lab_cur.p, ws.best.p, ws, st, nullptr, ev.get());
-  pass_stats(T + 1, nullptr);
+  pass_stats(T + 1, nullptr, LoopCtl());
 
   // ---- one read-back per level: control state and the per-pass trace
   int h_ctrl[4];
