@@ -63,7 +63,8 @@ enum {
   MASK_NO_FIXUP = 1 << 3,        /* disable the near-tie re-check of the tensor path (testing)*/
   MASK_SYNC_STATS = 1 << 4,      /* reserved: J/changed are read every pass (always on)       */
   MASK_TIME_KERNELS = 1 << 5,    /* record CUDA-event device times of the step kernels        */
-  MASK_NO_SORT = 1 << 6          /* small d: keep the data order in K1 (no per-pass label sort) */
+  MASK_NO_SORT = 1 << 6,         /* small d: keep the data order in K1 (no per-pass label sort) */
+  MASK_NO_FUSED = 1 << 7         /* small levels: per-pass kernels instead of the fused loop    */
 };
 
 /* kernel classes of mask_get_timing */

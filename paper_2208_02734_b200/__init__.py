@@ -11,6 +11,7 @@ from ._lib import (
     MASK_BORROW_DATA,
     MASK_FORCE_SIMT,
     MASK_NO_FIXUP,
+    MASK_NO_FUSED,
     MASK_NO_SORT,
     MASK_TIME_KERNELS,
     MASK_VALIDATE_FINITE,
@@ -21,5 +22,5 @@ from .shard import query_range, row_range
 __all__ = [
     "Comm", "Csr", "Index", "assign", "build", "device_ok", "kernel_launches", "matrix", "update", "row_range",
     "query_range", "MaskError", "MASK_BORROW_DATA", "MASK_FORCE_SIMT", "MASK_NO_FIXUP",
-    "MASK_VALIDATE_FINITE", "MASK_TIME_KERNELS", "MASK_NO_SORT",
+    "MASK_VALIDATE_FINITE", "MASK_TIME_KERNELS", "MASK_NO_SORT", "MASK_NO_FUSED",
 ]

@@ -32,6 +32,7 @@ MASK_NO_FIXUP = 1 << 3
 MASK_SYNC_STATS = 1 << 4
 MASK_TIME_KERNELS = 1 << 5
 MASK_NO_SORT = 1 << 6
+MASK_NO_FUSED = 1 << 7
 T_ASSIGN, T_FIXUP, T_UPDATE, T_FINALIZE = 0, 1, 2, 3
 
 # every symbol include/mask.h declares (checked by tests/test_boundary.py)

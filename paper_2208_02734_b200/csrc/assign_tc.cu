@@ -304,6 +304,7 @@ __device__ long long g_pt[9][kPT];
 #else
 #define PT_STAMP(cond, row, idx) \
   do {                           \
+    (void)(cond);                \
   } while (0)
 #endif
 __device__ unsigned long long g_chunk_stats[4];  // debug bit 128: chunks seen / keyed

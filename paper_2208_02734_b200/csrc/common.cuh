@@ -126,6 +126,12 @@ void launch_assign_tc(const float* X, int64_t n, int d, const float* P, const fl
 void launch_label_sort(const int32_t* labels, int64_t n, int64_t k, const int32_t* perm_old, int32_t* perm,
                        int32_t* cnt_ws, int32_t* copy_to, cudaStream_t st, const int* active = nullptr,
                        bool cnt_zeroed = false);
+// K11: the whole Lloyd loop of a small dense level in one cooperative launch (same stats /
+// control words as run_level's multi-kernel loop; bar_ws = 2 unsigned).
+bool small_level_supported(int64_t n, int d, int64_t k);
+void launch_small_level(const float* Y, int64_t n, int d, int64_t k, float* P, int32_t* lab, int32_t* prev,
+                        float* best, float* S, int32_t* counts, double* J, unsigned long long* changed,
+                        uint32_t* fin, int* ctrl, unsigned* bar_ws, int T, double tol, cudaStream_t st);
 // K4: exact FP32 direct re-check of flagged rows against all k prototypes.
 void launch_fixup(const float* X, int d, const float* P, int64_t k, const int32_t* flag_rows,
                   const int32_t* flag_count, int64_t max_flags, int32_t* labels, float* best,

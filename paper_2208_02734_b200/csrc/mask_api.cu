@@ -145,7 +145,7 @@ struct Level {
   int updates = 0;
   double t_ms[MASK_T_NCLASS] = {0, 0, 0, 0};
   int64_t t_count[MASK_T_NCLASS] = {0, 0, 0, 0};
-  int assign_kernel = -1;  // 0 = K2 SIMT, 1 = K1 tcgen05 3xTF32, 2 = K3 CSR
+  int assign_kernel = -1;  // 0 = K2 SIMT, 1 = K1 tcgen05 3xTF32, 2 = K3 CSR, 3 = K11 fused small level
 };
 
 // A level's input rows as seen by this rank.
@@ -427,7 +427,18 @@ void run_level(const Input& in, int64_t k, const int64_t* init_idx_host, const m
     }
   };
 
-  for (int t = 0; t < T; ++t) {
+  // small dense level without a communicator or step hook: the whole loop in one launch (K11)
+  const bool fused = in.format == MASK_DENSE_F32 && !comm && !p->iter_cb && !(p->flags & MASK_FORCE_SIMT) &&
+                     !(p->flags & MASK_NO_FUSED) && small_level_supported(n, d, k);
+  if (fused) {
+    DevBuf<unsigned> bar(2);
+    if (ev) ev->mark(MASK_T_ASSIGN, st);
+    launch_small_level(in.X, n, d, k, L.P.p, ws.lab_cur.p, ws.lab_prev.p, ws.best.p, ws.S.p, ws.counts.p, Jd.p,
+                       chd.p, fin.p, ctrl.p, bar.p, T, p->tol, st);
+    if (ev) ev->mark(MASK_T_ASSIGN, st);
+    ws.kernel_id = 3;
+  }
+  for (int t = 0; t < T && !fused; ++t) {
     if (p->iter_cb) MASK_CUDA(cudaMemcpyAsync(P_snap.p, L.P.p, sizeof(float) * k * d, cudaMemcpyDeviceToDevice, st));
     assign_pass(in, L.P.p, k, p->flags, ws.lab_cur.p, ws.best.p, ws, st, active, ev.get());
     LoopCtl lc;
@@ -497,9 +508,11 @@ void run_level(const Input& in, int64_t k, const int64_t* init_idx_host, const m
     }
   }
   // ---- final assignment with the final prototypes (D3): always runs, stats into slot T+1
-  if (p->iter_cb) MASK_CUDA(cudaMemcpyAsync(P_snap.p, L.P.p, sizeof(float) * k * d, cudaMemcpyDeviceToDevice, st));
-  assign_pass(in, L.P.p, k, p->flags, ws.lab_cur.p, ws.best.p, ws, st, nullptr, ev.get());
-  pass_stats(T + 1, nullptr, LoopCtl());
+  if (!fused) {
+    if (p->iter_cb) MASK_CUDA(cudaMemcpyAsync(P_snap.p, L.P.p, sizeof(float) * k * d, cudaMemcpyDeviceToDevice, st));
+    assign_pass(in, L.P.p, k, p->flags, ws.lab_cur.p, ws.best.p, ws, st, nullptr, ev.get());
+    pass_stats(T + 1, nullptr, LoopCtl());
+  }
 
   // ---- one read-back per level: control state and the per-pass trace
   int h_ctrl[4];

@@ -172,6 +172,41 @@ def _query_parity(idx, X, Q, levels, knn, beam, Qdev=None, csr=False, dim=None):
     return nd, ne
 
 
+@pytest.mark.parametrize("cid,div,T", [(1, 1, 20), (2, 64, 25), (3, 512, 8)])
+def test_build_fused_small_levels_e2e(cid, div, T):
+    """Levels small enough for the fused single-launch Lloyd loop (K11; no step hook, so the
+    build takes that path): every level against the oracle end to end (prototypes, final
+    labels = nearest final prototype, child lists, J trace) and against the per-pass kernels."""
+    cfg = datagen.CONFIGS[cid].scaled(div) if div > 1 else datagen.CONFIGS[cid]
+    X = datagen.data(cfg)
+    inits = datagen.all_init_indices(cfg)
+    idx = mk.build(t(X), cfg.levels, T, inits, flags=mk.MASK_TIME_KERNELS)
+    fused_levels = [l for l in range(1, len(cfg.levels) + 1)
+                    if idx.timing(l)["assign_kernel"] == "K11-fused-small-level"]
+    assert fused_levels, "no level took the fused path"
+    ref = oracle.build_index(X, inits, T)
+    Y = X.astype(np.float64)
+    for l in range(1, len(cfg.levels) + 1):
+        P = idx.prototypes(l)
+        check_prototypes(P, ref.levels[l - 1].P, what=f"fused e2e level {l}")
+        lab = idx.labels(l)
+        check_assignment(Y, P, lab, what=f"fused final labels level {l}")
+        off, mem = idx.children(l)
+        o_ref, m_ref = oracle.children(lab, cfg.levels[l - 1])
+        np.testing.assert_array_equal(off, o_ref)
+        np.testing.assert_array_equal(mem, m_ref)
+        tr = idx.trace(l)
+        if len(tr["J"]) == len(ref.levels[l - 1].J):
+            np.testing.assert_allclose(tr["J"], ref.levels[l - 1].J, rtol=1e-4)
+        Y = P.astype(np.float64)
+    # the per-pass kernel loop reaches the same index
+    other = mk.build(t(X), cfg.levels, T, inits, flags=mk.MASK_NO_FUSED)
+    for l in range(1, len(cfg.levels) + 1):
+        assert rel_l2(idx.prototypes(l), other.prototypes(l)) <= 1e-4
+    other.free()
+    idx.free()
+
+
 @pytest.mark.parametrize("cid,div", [(2, 64), (3, 256), (5, 2048)])
 def test_build_scaled_replicas_step_and_queries(cid, div):
     cfg = datagen.CONFIGS[cid].scaled(div)
