@@ -124,6 +124,20 @@ def peaks():
             "source": "fallback"}
 
 
+def ncu_traffic(workload, kernel):
+    """DRAM bytes (read + write) per launch of the dominant kernel from the committed ncu
+    --set full capture (profiles/ncu_traffic.json, written by tools/ncu_summary.py --traffic),
+    or None when no capture of this workload / kernel class is recorded."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        rec = json.load(open(path)).get(workload)
+    except (OSError, ValueError):
+        return None
+    if not rec or not kernel.startswith(rec.get("kernel_class", "")):
+        return None
+    return rec["dram_bytes_per_launch"]
+
+
 def lloyd_distances(idx, n_levels):
     tot = 0
     per = []
@@ -346,7 +360,7 @@ def main():
                 "peak_basis": "FP32 SIMT = 148 SMs x 128 lanes x 2 flop x sm_max_mhz"}
     achieved = flops / (assign_avg_ms / 1000.0) / 1e12 if assign_avg_ms > 0 else 0.0
     roof.update({"achieved": achieved, "peak": peak, "frac": achieved / peak if peak else None,
-                 "traffic": None, "avg_launch_ms": assign_avg_ms,
+                 "traffic": ncu_traffic(cfg.name, roof["kernel"]), "avg_launch_ms": assign_avg_ms,
                  "share_of_step": kt["assign"] / total_ms if total_ms else None})
     upd_avg = kt["update"] / max(kt["update_n"], 1)
     upd_bytes = n1 * d * 4 + n1 * 4 + k1 * (d + 1) * 4

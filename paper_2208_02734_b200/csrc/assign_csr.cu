@@ -11,6 +11,7 @@
 // keeping a running (s, j) argmin; lowest j wins ties (D4).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "common.cuh"
@@ -92,6 +93,236 @@ __global__ void __launch_bounds__(kRowsPerBlock * 32)
       if (best_out) best_out[r] = fmaxf(b + xx, 0.f);
     }
   }
+}
+
+// ---------------------------------------------------------------------------------------------
+// K3 (chunk-major): the same scores with the loops swapped so the prototype working set is
+// shared.  Persistent CTAs (one per SM) each own a contiguous range of rows and sweep the
+// prototypes in 256-wide chunks; all CTAs work on the same chunk at about the same time, so the
+// chunk's slice of PT (d x 256 floats: 10 MB at C4) stays L2-resident instead of every row
+// streaming all of PT from HBM.  The HOT most frequent columns (Zipf-distributed features,
+// SURVEY §8(d) G4) have their chunk rows staged in shared memory once per CTA and chunk, so
+// most non-zeros read shared memory; the rest read L2.  Lane l covers prototypes
+// j0 + 8l .. 8l+7 (two 16-byte loads per non-zero).  A row's running argmin across chunks lives
+// in `state` (global, L2); the last chunk writes the label and d^2 = s + ||x||^2.
+constexpr int kPL = 8;          // prototypes per lane (8 FMAs per non-zero per warp visit)
+constexpr int kChunk = 32 * kPL;  // prototypes per chunk
+constexpr int kHot = 128;       // columns staged per chunk (kHot x kChunk floats = 128 KB)
+constexpr int kG = 4;           // non-zeros in flight per warp step (kG x kPL floats of loads)
+constexpr int kCsrWarps = 24;   // warps per CTA (85 registers each; measured best of 16/24/32 warps,
+                                // 8/16 prototypes per lane, 64/128 hot columns)
+
+// acc[u] += v * (kPL consecutive floats at p, 16-byte aligned)
+template <bool SMEM>
+__device__ __forceinline__ void load_pl(const float* p, float4 (&r)[kPL / 4]) {
+#pragma unroll
+  for (int i = 0; i < kPL / 4; ++i) r[i] = SMEM ? reinterpret_cast<const float4*>(p)[i] : __ldg(reinterpret_cast<const float4*>(p) + i);
+}
+__device__ __forceinline__ void fma_pl(float v, const float4 (&r)[kPL / 4], float (&acc)[kPL]) {
+#pragma unroll
+  for (int i = 0; i < kPL / 4; ++i) {
+    acc[4 * i + 0] = fmaf(v, r[i].x, acc[4 * i + 0]);
+    acc[4 * i + 1] = fmaf(v, r[i].y, acc[4 * i + 1]);
+    acc[4 * i + 2] = fmaf(v, r[i].z, acc[4 * i + 2]);
+    acc[4 * i + 3] = fmaf(v, r[i].w, acc[4 * i + 3]);
+  }
+}
+
+__global__ void __launch_bounds__(kCsrWarps * 32, 1)
+    k_assign_csr_chunked(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
+                         const float* __restrict__ val, int64_t n, int d, const float* __restrict__ PT,
+                         const float* __restrict__ cn2, int64_t k, const int16_t* __restrict__ colslot,
+                         const int32_t* __restrict__ hotcols, float2* __restrict__ state,
+                         int32_t* __restrict__ labels, float* __restrict__ best_out, const int* __restrict__ active) {
+  if (active && !*active) return;  // level converged: this pass is skipped on the device
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  float* hotPT = reinterpret_cast<float*>(smem_raw);                                       // [kHot][kChunk]
+  int16_t* slot = reinterpret_cast<int16_t*>(smem_raw + kHot * kChunk * sizeof(float));  // [d]
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int c = threadIdx.x; c < d; c += blockDim.x) slot[c] = colslot[c];
+  const int64_t r0 = n * blockIdx.x / gridDim.x, r1 = n * (blockIdx.x + 1) / gridDim.x;
+  const int nch = (int)((k + kChunk - 1) / kChunk);
+  const bool kvec = (k & 3) == 0;  // 16-byte aligned PT rows
+  for (int ch = 0; ch < nch; ++ch) {
+    const int64_t j0 = (int64_t)ch * kChunk;
+    __syncthreads();  // previous chunk's readers are done with hotPT
+    for (int e = threadIdx.x; e < kHot * (kChunk / 4); e += blockDim.x) {
+      const int h = e / (kChunk / 4), q = e - h * (kChunk / 4);
+      const int64_t j = j0 + 4 * q;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (hotcols[h] >= 0) {
+        const float* src = PT + (int64_t)hotcols[h] * k + j;
+        if (j + 3 < k && kvec) v = *reinterpret_cast<const float4*>(src);
+        else {
+          if (j < k) v.x = src[0];
+          if (j + 1 < k) v.y = src[1];
+          if (j + 2 < k) v.z = src[2];
+          if (j + 3 < k) v.w = src[3];
+        }
+      }
+      reinterpret_cast<float4*>(hotPT)[e] = v;
+    }
+    __syncthreads();
+    // this lane's kPL prototypes of the chunk: ||c||^2 (+inf beyond k: never chosen)
+    const int64_t jl = j0 + kPL * lane;
+    float cc[kPL];
+#pragma unroll
+    for (int u = 0; u < kPL; ++u) cc[u] = jl + u < k ? __ldg(cn2 + jl + u) : INFINITY;
+    const bool vec_ok = jl + kPL - 1 < k && kvec;
+    for (int64_t r = r0 + w; r < r1; r += kCsrWarps) {
+      const int64_t p0 = rp[r], p1 = rp[r + 1];
+      float acc[kPL];
+#pragma unroll
+      for (int u = 0; u < kPL; ++u) acc[u] = 0.f;
+      for (int64_t pb = p0; pb < p1; pb += 32) {
+        const int m = p1 - pb < 32 ? (int)(p1 - pb) : 32;
+        // each lane resolves one non-zero's hot slot in parallel; the warp then walks the tail
+        // (L2) non-zeros kG at a time with their loads issued before the FMAs, then the hot
+        // (shared-memory) ones
+        int32_t mc = 0, msl = -1;
+        float mv = 0.f;
+        if (lane < m) {
+          mc = __ldg(col + pb + lane);
+          mv = __ldg(val + pb + lane);
+          msl = slot[mc];
+        }
+        unsigned tail = __ballot_sync(0xffffffffu, lane < m && msl < 0);
+        unsigned hot = __ballot_sync(0xffffffffu, lane < m && msl >= 0);
+        while (tail) {
+          float vq[kG];
+          float4 rb[kG][kPL / 4];
+#pragma unroll
+          for (int i = 0; i < kG; ++i) {
+            const int q = tail ? __ffs(tail) - 1 : -1;
+            if (tail) tail &= tail - 1;
+            const int32_t cq = __shfl_sync(0xffffffffu, mc, q < 0 ? 0 : q);
+            vq[i] = q < 0 ? 0.f : __shfl_sync(0xffffffffu, mv, q < 0 ? 0 : q);
+            const float* g = PT + (int64_t)cq * k + jl;
+            if (q >= 0 && vec_ok) {
+              load_pl<false>(g, rb[i]);
+            } else {
+              float t[kPL];
+#pragma unroll
+              for (int u = 0; u < kPL; ++u) t[u] = (q >= 0 && jl + u < k) ? __ldg(g + u) : 0.f;
+#pragma unroll
+              for (int u = 0; u < kPL / 4; ++u) rb[i][u] = make_float4(t[4 * u], t[4 * u + 1], t[4 * u + 2], t[4 * u + 3]);
+            }
+          }
+#pragma unroll
+          for (int i = 0; i < kG; ++i) fma_pl(vq[i], rb[i], acc);
+        }
+        while (hot) {
+          float vq[kG];
+          float4 rb[kG][kPL / 4];
+#pragma unroll
+          for (int i = 0; i < kG; ++i) {
+            const int q = hot ? __ffs(hot) - 1 : -1;
+            if (hot) hot &= hot - 1;
+            const int sl = __shfl_sync(0xffffffffu, msl, q < 0 ? 0 : q);
+            vq[i] = q < 0 ? 0.f : __shfl_sync(0xffffffffu, mv, q < 0 ? 0 : q);
+            load_pl<true>(hotPT + (q < 0 ? 0 : sl) * kChunk + kPL * lane, rb[i]);
+          }
+#pragma unroll
+          for (int i = 0; i < kG; ++i) fma_pl(vq[i], rb[i], acc);
+        }
+      }
+      // lane argmin over its kPL (j increasing: strict < keeps the lowest j), then the warp's
+      float bv = INFINITY;
+      int32_t bj = 0x7fffffff;
+#pragma unroll
+      for (int u = 0; u < kPL; ++u) {
+        const float sv = fmaf(-2.f, acc[u], cc[u]);
+        if (sv < bv) {
+          bv = sv;
+          bj = (int32_t)(jl + u);
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int32_t oj = __shfl_xor_sync(0xffffffffu, bj, o);
+        if (ov < bv || (ov == bv && oj < bj)) {
+          bv = ov;
+          bj = oj;
+        }
+      }
+      if (ch > 0) {  // earlier chunks hold lower j: they win ties
+        const float2 st = state[r];
+        if (!(bv < st.x)) {
+          bv = st.x;
+          bj = __float_as_int(st.y);
+        }
+      }
+      if (ch + 1 < nch) {
+        if (lane == 0) state[r] = make_float2(bv, __int_as_float(bj));
+      } else {
+        float xx = 0.f;
+        for (int64_t p = p0 + lane; p < p1; p += 32) {
+          const float v = __ldg(val + p);
+          xx = fmaf(v, v, xx);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) xx += __shfl_xor_sync(0xffffffffu, xx, o);
+        if (lane == 0) {
+          labels[r] = bj;
+          if (best_out) best_out[r] = fmaxf(bv + xx, 0.f);
+        }
+      }
+    }
+  }
+}
+
+size_t csr_chunked_smem(int d) { return (size_t)kHot * kChunk * sizeof(float) + (size_t)d * sizeof(int16_t); }
+
+int csr_chunked_hot() { return kHot; }
+
+bool csr_chunked_supported(int d, int64_t k) {
+  (void)k;
+  return d <= 32767 && csr_chunked_smem(d) <= 227 * 1024;
+}
+
+void launch_assign_csr_chunked(const int64_t* row_ptr, const int32_t* col, const float* val, int64_t n, int d,
+                               const float* PT, const float* cn2, int64_t k, const int16_t* colslot,
+                               const int32_t* hotcols, float2* state, int32_t* labels, float* best, cudaStream_t st,
+                               const int* active) {
+  if (n <= 0) return;
+  const size_t smem = csr_chunked_smem(d);
+  static bool attr = false;
+  if (!attr) {
+    MASK_CUDA(cudaFuncSetAttribute(k_assign_csr_chunked, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    attr = true;
+  }
+  const int64_t grid = std::min<int64_t>(num_sms(), (n + kCsrWarps - 1) / kCsrWarps);
+  k_assign_csr_chunked<<<(unsigned)grid, kCsrWarps * 32, smem, st>>>(row_ptr, col, val, n, d, PT, cn2, k, colslot,
+                                                                    hotcols, state, labels, best, active);
+  MASK_LAUNCH_CHECK();
+}
+
+// Column statistics for the hot set: cnt[c] = non-zeros in column c (shared-memory histogram
+// per block when d fits, else global atomics).
+__global__ void k_col_hist(const int32_t* __restrict__ col, int64_t nnz, int d, int32_t* __restrict__ cnt) {
+  extern __shared__ int32_t h[];
+  const bool sm = d <= 12288;
+  if (sm)
+    for (int c = threadIdx.x; c < d; c += blockDim.x) h[c] = 0;
+  __syncthreads();
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < nnz; p += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t c = col[p];
+    if (sm) atomicAdd(h + c, 1);
+    else atomicAdd(cnt + c, 1);
+  }
+  __syncthreads();
+  if (sm)
+    for (int c = threadIdx.x; c < d; c += blockDim.x)
+      if (h[c]) atomicAdd(cnt + c, h[c]);
+}
+
+void launch_col_hist(const int32_t* col, int64_t nnz, int d, int32_t* cnt, cudaStream_t st) {
+  MASK_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * d, st));
+  if (nnz <= 0) return;
+  const size_t smem = d <= 12288 ? (size_t)d * sizeof(int32_t) : 0;
+  k_col_hist<<<grid_for(nnz, 256, (int64_t)num_sms() * 4), 256, smem, st>>>(col, nnz, d, cnt);
+  MASK_LAUNCH_CHECK();
 }
 
 void launch_assign_csr(const int64_t* row_ptr, const int32_t* col, const float* val, int64_t n,

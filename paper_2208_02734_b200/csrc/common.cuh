@@ -127,10 +127,10 @@ void launch_label_sort(const int32_t* labels, int64_t n, int64_t k, const int32_
                        int32_t* cnt_ws, int32_t* copy_to, cudaStream_t st, const int* active = nullptr,
                        bool cnt_zeroed = false);
 // K11: the whole Lloyd loop of a small dense level in one cooperative launch (same stats /
-// control words as run_level's multi-kernel loop; bar_ws = 2 unsigned).
+// control words as run_level's multi-kernel loop; bar_ws = 2 unsigned; S = k*d zeroed doubles).
 bool small_level_supported(int64_t n, int d, int64_t k);
 void launch_small_level(const float* Y, int64_t n, int d, int64_t k, float* P, int32_t* lab, int32_t* prev,
-                        float* best, float* S, int32_t* counts, double* J, unsigned long long* changed,
+                        float* best, double* S, int32_t* counts, double* J, unsigned long long* changed,
                         uint32_t* fin, int* ctrl, unsigned* bar_ws, int T, double tol, cudaStream_t st);
 // K4: exact FP32 direct re-check of flagged rows against all k prototypes.
 void launch_fixup(const float* X, int d, const float* P, int64_t k, const int32_t* flag_rows,
@@ -159,6 +159,16 @@ void launch_assign_csr(const int64_t* row_ptr, const int32_t* col, const float* 
                        int d, const float* PT /* d x k transposed */, const float* cn2, int64_t k,
                        int32_t* labels, float* best, cudaStream_t st, const int* active = nullptr);
 void launch_transpose(const float* P, int64_t k, int d, float* PT, cudaStream_t st, const int* active = nullptr);
+// K3 chunk-major: colslot[c] = hot slot of column c (< 128) or -1; hotcols[h] = column of slot
+// h (or -1); state = n float2 (running argmin across chunks).
+bool csr_chunked_supported(int d, int64_t k);
+int csr_chunked_hot();  // number of hot columns (slots) the kernel stages
+void launch_assign_csr_chunked(const int64_t* row_ptr, const int32_t* col, const float* val, int64_t n, int d,
+                               const float* PT, const float* cn2, int64_t k, const int16_t* colslot,
+                               const int32_t* hotcols, float2* state, int32_t* labels, float* best, cudaStream_t st,
+                               const int* active = nullptr);
+// per-column non-zero counts (d int32, zeroed here)
+void launch_col_hist(const int32_t* col, int64_t nnz, int d, int32_t* cnt, cudaStream_t st);
 
 // K5/K6: cluster sums and counts (S, counts must be zeroed by the caller).
 // perm (optional): rows sorted by these labels (launch_label_sort) -> run-accumulating kernel

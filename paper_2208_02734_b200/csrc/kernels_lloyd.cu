@@ -737,9 +737,73 @@ __global__ void k_finalize(float* __restrict__ P, float* __restrict__ S, int32_t
   }
 }
 
+// Wide rows (d >= 256, e.g. the dense C4 prototypes with d = 10,000): a block per prototype,
+// 16-byte vectors, so the k*d read-modify-write streams at HBM speed instead of a warp walking
+// d / 32 scalar iterations.
+__global__ void __launch_bounds__(256) k_finalize_wide(float* __restrict__ P, float* __restrict__ S,
+                                                       int32_t* __restrict__ counts, int64_t k, int d,
+                                                       uint32_t* __restrict__ stat, int keep_counts,
+                                                       const int* __restrict__ active, LoopCtl lc) {
+  if (active && !*active) return;  // level converged: this pass is skipped on the device
+  __shared__ float red[8];
+  for (int64_t j = blockIdx.x; j < k; j += gridDim.x) {
+    if (lc.zero_cnt && threadIdx.x == 0) lc.zero_cnt[j] = 0;
+    const int32_t cnt = counts[j];
+    float disp = 0.f;
+    if (cnt > 0) {
+      const float fc = (float)cnt;
+      float4* P4 = reinterpret_cast<float4*>(P + j * d);
+      float4* S4 = reinterpret_cast<float4*>(S + j * d);
+      for (int e = threadIdx.x; e < d / 4; e += blockDim.x) {
+        const float4 sv = S4[e], pv = P4[e];
+        float4 cv;
+        cv.x = __fdiv_rn(sv.x, fc);
+        cv.y = __fdiv_rn(sv.y, fc);
+        cv.z = __fdiv_rn(sv.z, fc);
+        cv.w = __fdiv_rn(sv.w, fc);
+        float t = cv.x - pv.x;
+        disp = fmaf(t, t, disp);
+        t = cv.y - pv.y;
+        disp = fmaf(t, t, disp);
+        t = cv.z - pv.z;
+        disp = fmaf(t, t, disp);
+        t = cv.w - pv.w;
+        disp = fmaf(t, t, disp);
+        P4[e] = cv;
+        S4[e] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) disp += __shfl_xor_sync(0xffffffffu, disp, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = disp;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      float tot = 0.f;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += red[w];
+      atomicMax(stat, __float_as_uint(tot));
+      if (cnt == 0) atomicAdd(stat + 1, 1u);
+      if (!keep_counts) counts[j] = 0;
+    }
+    __syncthreads();
+  }
+  if (lc.ctrl && last_block_done(lc.ctrl + 3) && threadIdx.x == 0) {
+    const double dsp = sqrt((double)__uint_as_float(*(volatile uint32_t*)stat));
+    if (lc.tol > 0.0 && dsp <= lc.tol) {
+      lc.ctrl[0] = 0;
+      lc.ctrl[1] = lc.t + 1;
+    } else if (lc.t == lc.T - 1) {
+      lc.ctrl[1] = lc.T;
+    }
+  }
+}
+
 void launch_finalize(float* P, float* S, int32_t* counts, int64_t k, int d, uint32_t* stat,
                      int keep_counts, cudaStream_t st, const int* active, LoopCtl lc) {
-  k_finalize<<<grid_for(k * 32, 256), 256, 0, st>>>(P, S, counts, k, d, stat, keep_counts, active, lc);
+  if (d >= 256 && d % 4 == 0 && ((uintptr_t)P % 16) == 0 && ((uintptr_t)S % 16) == 0)
+    k_finalize_wide<<<grid_for(k, 1, (int64_t)num_sms() * 8), 256, 0, st>>>(P, S, counts, k, d, stat, keep_counts,
+                                                                             active, lc);
+  else
+    k_finalize<<<grid_for(k * 32, 256), 256, 0, st>>>(P, S, counts, k, d, stat, keep_counts, active, lc);
   MASK_LAUNCH_CHECK();
 }
 

@@ -241,6 +241,9 @@ struct LloydWS {
   DevBuf<float> Pb, Ps, cn2, xn2, PT;
   DevBuf<int32_t> flag_rows, flag_count;
   DevBuf<unsigned long long> fix_keys;
+  DevBuf<int16_t> colslot;  // K3 chunk-major: hot slot of each column (-1 = read from L2)
+  DevBuf<int32_t> hotcols;  // the hot columns (most non-zeros)
+  DevBuf<float2> csr_state; // running argmin across prototype chunks
   bool xn2_ready = false;
   int kernel_id = -1;
 };
@@ -286,8 +289,40 @@ void assign_pass(const Input& in, const float* P, int64_t k, int flags, int32_t*
     launch_transpose(P, k, d, ws.PT.p, st, active);
     launch_level_norms(P, k, d, ws.cn2.p, st, active);
     ws.kernel_id = 2;
+    const bool chunked = csr_chunked_supported(d, k) && !(flags & MASK_FORCE_SIMT);
+    if (chunked && !ws.colslot.p) {
+      // hot set = the csr_chunked_hot() columns with the most non-zeros (one host round trip)
+      DevBuf<int32_t> cnt(d);
+      launch_col_hist(in.col, in.nnz, d, cnt.p, st);
+      std::vector<int32_t> hc(d);
+      MASK_CUDA(cudaMemcpyAsync(hc.data(), cnt.p, sizeof(int32_t) * d, cudaMemcpyDeviceToHost, st));
+      MASK_CUDA(cudaStreamSynchronize(st));
+      std::vector<int32_t> order(d);
+      for (int c = 0; c < d; ++c) order[c] = c;
+      const int H = csr_chunked_hot();
+      const int nh = std::min(H, d);
+      std::partial_sort(order.begin(), order.begin() + nh, order.end(),
+                        [&](int a, int b) { return hc[a] != hc[b] ? hc[a] > hc[b] : a < b; });
+      std::vector<int16_t> slot(d, (int16_t)-1);
+      std::vector<int32_t> hot(H, -1);
+      for (int h = 0; h < nh; ++h) {
+        if (hc[order[h]] == 0) break;
+        hot[h] = order[h];
+        slot[order[h]] = (int16_t)h;
+      }
+      ws.colslot.alloc(d);
+      ws.hotcols.alloc(H);
+      ws.csr_state.alloc(std::max<int64_t>(n, 1));
+      MASK_CUDA(cudaMemcpyAsync(ws.colslot.p, slot.data(), sizeof(int16_t) * d, cudaMemcpyHostToDevice, st));
+      MASK_CUDA(cudaMemcpyAsync(ws.hotcols.p, hot.data(), sizeof(int32_t) * H, cudaMemcpyHostToDevice, st));
+      MASK_CUDA(cudaStreamSynchronize(st));  // host vectors go out of scope
+    }
     if (ev) ev->mark(MASK_T_ASSIGN, st);
-    launch_assign_csr(in.rp, in.col, in.val, n, d, ws.PT.p, ws.cn2.p, k, labels_out, best, st, active);
+    if (chunked)
+      launch_assign_csr_chunked(in.rp, in.col, in.val, n, d, ws.PT.p, ws.cn2.p, k, ws.colslot.p, ws.hotcols.p,
+                                ws.csr_state.p, labels_out, best, st, active);
+    else
+      launch_assign_csr(in.rp, in.col, in.val, n, d, ws.PT.p, ws.cn2.p, k, labels_out, best, st, active);
     if (ev) ev->mark(MASK_T_ASSIGN, st);
     return;
   }
@@ -432,8 +467,10 @@ void run_level(const Input& in, int64_t k, const int64_t* init_idx_host, const m
                      !(p->flags & MASK_NO_FUSED) && small_level_supported(n, d, k);
   if (fused) {
     DevBuf<unsigned> bar(2);
+    DevBuf<double> S64((size_t)k * d);
+    MASK_CUDA(cudaMemsetAsync(S64.p, 0, sizeof(double) * k * d, st));
     if (ev) ev->mark(MASK_T_ASSIGN, st);
-    launch_small_level(in.X, n, d, k, L.P.p, ws.lab_cur.p, ws.lab_prev.p, ws.best.p, ws.S.p, ws.counts.p, Jd.p,
+    launch_small_level(in.X, n, d, k, L.P.p, ws.lab_cur.p, ws.lab_prev.p, ws.best.p, S64.p, ws.counts.p, Jd.p,
                        chd.p, fin.p, ctrl.p, bar.p, T, p->tol, st);
     if (ev) ev->mark(MASK_T_ASSIGN, st);
     ws.kernel_id = 3;

@@ -9,7 +9,7 @@
 //   for t < T:  a <- argmin_j ||y - c_j||^2 (FP32 direct, lowest j on ties, D4)  [P:897-898]
 //               J[t] = sum d^2, changed[t] = #(a != a_prev)
 //               stop if t > 0 and changed[t] == 0                               (D3)
-//               S_j, n_j <- sums / counts of the members; c_j <- S_j / n_j if n_j > 0 (D5)
+//               S_j, n_j <- sums (FP64) / counts of the members; c_j <- S_j / n_j if n_j > 0 (D5)
 //               fin[2t] = max_j ||c_j' - c_j||^2, fin[2t+1] = #empty; stop if tol > 0 and
 //               sqrt(fin[2t]) <= tol                                             (D3)
 //   final pass: a <- argmin (stats in slot T+1)
@@ -38,7 +38,7 @@ struct SmallArgs {
   int32_t* lab;
   int32_t* prev;
   float* best;
-  float* S;
+  double* S;  // FP64 sums: order-independent to ~1e-16, so the loop is reproducible run to run
   int32_t* counts;
   double* J;
   unsigned long long* changed;
@@ -178,8 +178,8 @@ __global__ void __launch_bounds__(256) k_small_level(SmallArgs a) {
     // ---- update: S_j, n_j
     for (int64_t i = tid; i < a.n; i += stride) {
       const int32_t j = __ldcg(a.lab + i);
-      float* Sj = a.S + (int64_t)j * a.d;
-      for (int e = 0; e < a.d; ++e) atomicAdd(Sj + e, __ldg(a.Y + i * a.d + e));
+      double* Sj = a.S + (int64_t)j * a.d;
+      for (int e = 0; e < a.d; ++e) atomicAdd(Sj + e, (double)__ldg(a.Y + i * a.d + e));
       atomicAdd(a.counts + j, 1);
       a.prev[i] = j;
     }
@@ -190,11 +190,11 @@ __global__ void __launch_bounds__(256) k_small_level(SmallArgs a) {
       float disp = 0.f;
       if (cnt > 0) {
         for (int e = lane; e < a.d; e += 32) {
-          const float cv = __fdiv_rn(__ldcg(a.S + j * a.d + e), (float)cnt);
+          const float cv = (float)(__ldcg(a.S + j * a.d + e) / (double)cnt);
           const float df = cv - a.P[j * a.d + e];
           disp = fmaf(df, df, disp);
           a.P[j * a.d + e] = cv;
-          a.S[j * a.d + e] = 0.f;
+          a.S[j * a.d + e] = 0.0;
         }
       }
 #pragma unroll
@@ -230,7 +230,7 @@ bool small_level_supported(int64_t n, int d, int64_t k) {
 }
 
 void launch_small_level(const float* Y, int64_t n, int d, int64_t k, float* P, int32_t* lab, int32_t* prev,
-                        float* best, float* S, int32_t* counts, double* J, unsigned long long* changed,
+                        float* best, double* S, int32_t* counts, double* J, unsigned long long* changed,
                         uint32_t* fin, int* ctrl, unsigned* bar_ws, int T, double tol, cudaStream_t st) {
   SmallArgs a{Y, n, d, k, P, lab, prev, best, S, counts, J, changed, fin, ctrl, bar_ws, T, tol};
   MASK_CUDA(cudaMemsetAsync(bar_ws, 0, 2 * sizeof(unsigned), st));

@@ -19,6 +19,21 @@ KEYS = [
 ]
 
 
+SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+
+
+def traffic(path):
+    """DRAM bytes (read + write) of the first kernel in a --set full report."""
+    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    hdr, units, vals = rows[0], rows[1], rows[2]
+    tot = 0.0
+    for key in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+        i = hdr.index(key)
+        tot += float(vals[i].replace(",", "")) * SCALE[units[i]]
+    return vals[hdr.index("Kernel Name")], tot
+
+
 def main(path):
     out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
@@ -33,6 +48,17 @@ def main(path):
 
 
 if __name__ == "__main__":
-    for p in sys.argv[1:]:
-        print(f"== {p}")
-        main(p)
+    # usage: ncu_summary.py REPORT...   |   ncu_summary.py --traffic WORKLOAD KERNEL_CLASS REPORT OUT.json
+    if sys.argv[1] == "--traffic":
+        import json, os
+        workload, kclass, rep, outp = sys.argv[2:6]
+        name, tot = traffic(rep)
+        db = json.load(open(outp)) if os.path.exists(outp) else {}
+        db[workload] = {"kernel_class": kclass, "kernel": name[:120], "dram_bytes_per_launch": tot,
+                        "capture": os.path.basename(rep)}
+        json.dump(db, open(outp, "w"), indent=1)
+        print(workload, kclass, tot)
+    else:
+        for p in sys.argv[1:]:
+            print(f"== {p}")
+            main(p)
