@@ -351,6 +351,9 @@ __global__ void __launch_bounds__(128 + 128 * EPI_WG, 1)
                 float err_coef, int dbg,
                 const int* __restrict__ active) {
   if (active && !*active) return;  // level converged: this pass is skipped on the device
+#if !defined(MASK_TC_ABLATE)
+  dbg = 0;  // development ablations / trace only in -DMASK_TC_ABLATE builds
+#endif
   using C = Cfg<CW, NKC, KA, BN, STAGES, NACC, FOLD, EPI_WG>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -417,18 +420,22 @@ __global__ void __launch_bounds__(128 + 128 * EPI_WG, 1)
         }
       }
     }
-  } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer (A from TMEM)
-    mbar_wait(a_ready, 0);
+  } else if (warp == 1 || warp == 3) {
+    // ------------------------------------------------------------ MMA issuers (A from TMEM)
+    // warp 1 issues the even tiles, warp 3 the odd ones (see the persistent kernel: the second
+    // issuer hides the per-tile control path behind the tensor core's short queue)
+    const int par = warp == 1 ? 0 : 1;
+    mbar_wait_spin(a_ready, 0);
     tc_fence_after();
-    int stage = 0;
-    uint32_t phase = 0;
-    for (int t = 0; t < ntiles; ++t) {
+    for (int t = par; t < ntiles; t += 2) {
       const int acc = t % NACC;
       mbar_wait_spin(&tempty[acc], ((t / NACC) & 1) ^ 1);
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
       for (int c = 0; c < NKC; ++c) {
+        const int gc = t * NKC + c;  // global chunk index: ring slot and phase
+        const int stage = gc % STAGES;
+        const uint32_t phase = (uint32_t)((gc / STAGES) & 1);
         mbar_wait_spin(&full[stage], phase);
         tc_fence_after();
         if (lane == 0) {
@@ -448,10 +455,6 @@ __global__ void __launch_bounds__(128 + 128 * EPI_WG, 1)
           if (c == NKC - 1) mma_commit(&tfull[acc]);
         }
         __syncwarp();
-        if (++stage == STAGES) {
-          stage = 0;
-          phase ^= 1;
-        }
       }
     }
   } else if (warp >= kEpiWarp0) {
@@ -501,7 +504,9 @@ __global__ void __launch_bounds__(128 + 128 * EPI_WG, 1)
     int32_t gi = 0x7fffffff;
     for (int t = 0; t < ntiles; ++t) {
       const int acc = t % NACC;
-      mbar_wait(&tfull[acc], (t / NACC) & 1);
+      // one polling warp per warpgroup, the others on a named barrier (as in the persistent kernel)
+      if (q == 0) mbar_wait_spin(&tfull[acc], (t / NACC) & 1);
+      asm volatile("bar.sync %0, 128;" ::"r"(2 + wg) : "memory");
       tc_fence_after();
       if (tr0 && t == 0) g_tc_trace[3][blockIdx.x] = gtimer();
       if (tr0 && t == ntiles - 1) g_tc_trace[4][blockIdx.x] = gtimer();
@@ -679,6 +684,9 @@ __global__ void __launch_bounds__(256 + 128 * EPI_WG, 1)
                         const int32_t* __restrict__ perm, const int32_t* __restrict__ prev_lab,
                         int32_t* __restrict__ lab2, int dbg) {
   if (active && !*active) return;  // level converged: this pass is skipped on the device
+#if !defined(MASK_TC_ABLATE)
+  dbg = 0;  // development ablations / counters only in -DMASK_TC_ABLATE builds (tools/build_variant.py)
+#endif
   using C = PCfg<KA, BN, STAGES, NACC, EPI_WG>;
   constexpr int COLS = BN / EPI_WG;
   static_assert(COLS % 32 == 0 && COLS / 32 <= 2, "epilogue chunking (two register buffers)");
@@ -987,8 +995,15 @@ __global__ void __launch_bounds__(256 + 128 * EPI_WG, 1)
       for (int t = 0; t < ntiles; ++t, ++g) {
         const int acc = (int)(g % NACC);
         // polled, not suspended: the accumulator round trip (MMA -> epilogue -> MMA) must fit in
-        // one tile of tensor-core work, and a suspended waiter wakes hundreds of cycles late
+        // one tile of tensor-core work, and a suspended waiter wakes hundreds of cycles late.
+        // One warp per warpgroup polls; the other three wait on a named barrier (no issue slots,
+        // no traffic on the barrier unit the MMA issuers' own waits go through).
+#if !defined(MASK_TC_ALL_POLL)
+        if (q == 0) mbar_wait_spin(&tfull[acc], (g / NACC) & 1);
+        asm volatile("bar.sync %0, 128;" ::"r"(2 + wg) : "memory");
+#else
         mbar_wait_spin(&tfull[acc], (g / NACC) & 1);
+#endif
         tc_fence_after();
         const bool ptr = (dbg & 8) && blockIdx.x == 0 && lane == 0 && q == 0 && g < 512;
         PT_STAMP(ptr && wg == 0, 2, g);

@@ -480,6 +480,55 @@ void run_tiles_epi() {
   cudaFree(sink);
 }
 
+// tcgen05.ld latency: one warp per lane quarter loads NLD x32 chunks and waits, repeatedly
+template <int NLD>
+__global__ void k_ldlat(int reps, long long* out, int* sink) {
+  __shared__ uint32_t tslot;
+  const int warp = threadIdx.x >> 5;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tslot)), "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = tslot + ((uint32_t)(warp * 32) << 16);
+  int acc = 0;
+  long long t0 = clock64();
+  for (int r = 0; r < reps; ++r) {
+    uint32_t v[NLD][32];
+#pragma unroll
+    for (int c = 0; c < NLD; ++c) tmem_ld32(tmem + c * 32 + (r & 3) * 64, v[c]);
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int c = 0; c < NLD; ++c) acc += (int)(v[c][0] ^ v[c][17] ^ v[c][31]);
+  }
+  long long t1 = clock64();
+  if (threadIdx.x == 0 && blockIdx.x == 0) out[0] = t1 - t0;
+  if (acc == 123456) sink[0] = acc;
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tslot), "r"(512));
+}
+
+template <int NLD>
+void run_ldlat() {
+  long long* d;
+  int* sink;
+  cudaMalloc(&d, 8);
+  cudaMalloc(&sink, 4);
+  const int reps = 4000;
+  k_ldlat<NLD><<<148, 128>>>(reps, d, sink);
+  k_ldlat<NLD><<<148, 128>>>(reps, d, sink);
+  cudaError_t e = cudaDeviceSynchronize();
+  long long h = 0;
+  cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
+  printf("tcgen05.ld %d x 32x32b.x32 + wait::ld: %6.1f cycles per round trip  (%s)\n", NLD, (double)h / reps,
+         cudaGetErrorString(e));
+  cudaFree(d);
+  cudaFree(sink);
+}
+
 template <int N, int MPT, int NACC>
 void run_tiles() {
   long long* d;
@@ -546,5 +595,8 @@ int main() {
   run_ctl<192, 2, 4, false, 2>();
   run_ctl<192, 2, 4, true, 2>();
   run_ctl<128, 2, 4, false, 2>();
+  run_ldlat<1>();
+  run_ldlat<2>();
+  run_ldlat<4>();
   return 0;
 }
