@@ -28,6 +28,8 @@ from __future__ import annotations
 import dataclasses
 from typing import List, Optional, Sequence, Tuple
 
+import os
+
 import numpy as np
 
 BLOCK_ROWS = 1 << 14
@@ -197,6 +199,46 @@ def _rows(cfg: Config, seed: int, n: int, start: int = 0):
         rps.append(np.array([off], dtype=np.int64))
         return np.concatenate(rps), np.concatenate(cs), np.concatenate(vs)
     return np.concatenate(out, axis=0) if out else np.zeros((0, cfg.dim), np.float32)
+
+
+def _fill_blocks(args):
+    """Worker of data_parallel: whole blocks [b0, b1) into the shared output array."""
+    name, shape, cid, b0, b1, n = args
+    from multiprocessing import shared_memory
+
+    cfg = CONFIGS[cid]
+    shm = shared_memory.SharedMemory(name=name)
+    try:
+        out = np.ndarray(shape, dtype=np.float32, buffer=shm.buf)
+        params = _mixture_params(cfg, 1000 + cid)
+        for b in range(b0, b1):
+            lo, hi = b * BLOCK_ROWS, min((b + 1) * BLOCK_ROWS, n)
+            out[lo:hi] = _dense_block(cfg, params, 1000 + cid, b, BLOCK_ROWS)[: hi - lo]
+    finally:
+        shm.close()
+    return b1 - b0
+
+
+def data_parallel(cfg: Config, workers: Optional[int] = None):
+    """All rows of a dense config, blocks generated by a process pool into shared memory.
+
+    Identical to ``data(cfg)`` (same per-block streams); for the 51 GB C5 set.  Returns
+    (array, shm): keep ``shm`` alive while the array is used, then ``shm.close(); shm.unlink()``."""
+    import multiprocessing as mp
+    from multiprocessing import shared_memory
+
+    assert not cfg.sparse
+    n = cfg.n
+    shape = (n, cfg.dim)
+    shm = shared_memory.SharedMemory(create=True, size=n * cfg.dim * 4)
+    nb = (n + BLOCK_ROWS - 1) // BLOCK_ROWS
+    workers = workers or os.cpu_count() or 1
+    step = max(1, (nb + 4 * workers - 1) // (4 * workers))
+    jobs = [(shm.name, shape, cfg.cid, b, min(b + step, nb), n) for b in range(0, nb, step)]
+    with mp.get_context("fork").Pool(workers) as pool:
+        done = sum(pool.map(_fill_blocks, jobs))
+    assert done == nb
+    return np.ndarray(shape, dtype=np.float32, buffer=shm.buf), shm
 
 
 def data(cfg: Config, start: int = 0, count: Optional[int] = None):

@@ -379,12 +379,147 @@ __global__ void k_keys_write(const int32_t* __restrict__ rows, const int32_t* __
   }
 }
 
+// Register-blocked exact argmin for d <= 256 (the K4 re-check at C3/C5 scale): a work item is
+// 32 rows x a prototype range; the 32 rows stay in shared memory for the whole range, each
+// 128-prototype tile is staged once, and a thread computes 4 rows x 4 prototypes with 16-byte
+// shared-memory loads along the dimension (4 dims per load): direct FP32 (x - c)^2 sums in
+// dimension order, the same arithmetic as the FP32 direct form of the oracle comparison.
+constexpr int RB_R = 32, RB_P = 128;
+
+__global__ void __launch_bounds__(256) k_rb_argmin(const float* __restrict__ X, int d, int d4p,
+                                                   const float* __restrict__ P, int64_t k,
+                                                   const int32_t* __restrict__ rows,
+                                                   const int32_t* __restrict__ count_dev, int64_t cap, int nsm,
+                                                   unsigned long long* __restrict__ keys,
+                                                   const int* __restrict__ active) {
+  if (active && !*active) return;  // level converged: this pass is skipped on the device
+  extern __shared__ float4 rsm[];
+  const int64_t nf = count_dev ? min64(*count_dev, cap) : cap;
+  if (nf <= 0) return;
+  // row stride d4p float4 (d/4 rounded up, +1 when even: conflict-free 16-byte column reads)
+  float4* xs = rsm;                  // [RB_R][d4p]
+  float4* cs = rsm + RB_R * d4p;     // [RB_P][d4p]
+  const int t = threadIdx.x;
+  const int rg = t & 7, pg = t >> 3;  // rows a*8+rg, prototypes b*32+pg (a, b < 4): interleaved so
+                                      // the 16-byte smem reads of a warp hit distinct banks
+  const int d4 = (d + 3) / 4;
+  const int64_t row_blocks = (nf + RB_R - 1) / RB_R;
+  const int64_t ntile = (k + RB_P - 1) / RB_P;
+  int64_t splits = (4LL * nsm + row_blocks - 1) / row_blocks;
+  splits = splits < 1 ? 1 : (splits > ntile ? ntile : splits);
+  const int64_t tps = (ntile + splits - 1) / splits;
+  splits = (ntile + tps - 1) / tps;
+  for (int64_t w = blockIdx.x; w < row_blocks * splits; w += gridDim.x) {
+    const int64_t f0 = (w / splits) * RB_R;
+    const int64_t t0 = (w % splits) * tps;
+    const int64_t t1 = min64(ntile, t0 + tps);
+    __syncthreads();
+    for (int e = t; e < RB_R * d4; e += 256) {
+      const int r = e / d4, c4 = e - r * d4;
+      const int64_t f = f0 + r;
+      const int64_t row = f < nf ? (rows ? (int64_t)rows[f] : f) : -1;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (row >= 0) {
+        const float* src = X + row * d + 4 * c4;
+        v.x = src[0];
+        if (4 * c4 + 1 < d) v.y = src[1];
+        if (4 * c4 + 2 < d) v.z = src[2];
+        if (4 * c4 + 3 < d) v.w = src[3];
+      }
+      xs[r * d4p + c4] = v;
+    }
+    float bv[4];
+    int64_t bj[4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      bv[a] = INFINITY;
+      bj[a] = INT64_MAX;
+    }
+    for (int64_t tile = t0; tile < t1; ++tile) {
+      const int64_t j0 = tile * RB_P;
+      __syncthreads();
+      for (int e = t; e < RB_P * d4; e += 256) {
+        const int pr = e / d4, c4 = e - pr * d4;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (j0 + pr < k) {
+          const float* src = P + (j0 + pr) * d + 4 * c4;
+          v.x = src[0];
+          if (4 * c4 + 1 < d) v.y = src[1];
+          if (4 * c4 + 2 < d) v.z = src[2];
+          if (4 * c4 + 3 < d) v.w = src[3];
+        }
+        cs[pr * d4p + c4] = v;
+      }
+      __syncthreads();
+      float acc[4][4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = 0.f;
+      for (int c4 = 0; c4 < d4; ++c4) {
+        float4 xv[4], cv[4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) xv[a] = xs[(a * 8 + rg) * d4p + c4];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) cv[b] = cs[(b * 32 + pg) * d4p + c4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) {  // dimensions in increasing order (zero padding adds 0)
+            float df = xv[a].x - cv[b].x;
+            acc[a][b] = fmaf(df, df, acc[a][b]);
+            df = xv[a].y - cv[b].y;
+            acc[a][b] = fmaf(df, df, acc[a][b]);
+            df = xv[a].z - cv[b].z;
+            acc[a][b] = fmaf(df, df, acc[a][b]);
+            df = xv[a].w - cv[b].w;
+            acc[a][b] = fmaf(df, df, acc[a][b]);
+          }
+      }
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const int64_t j = j0 + b * 32 + pg;
+        if (j < k) {
+#pragma unroll
+          for (int a = 0; a < 4; ++a)
+            if (acc[a][b] < bv[a]) {  // j increases with (tile, b) for this thread: keeps lowest j
+              bv[a] = acc[a][b];
+              bj[a] = j;
+            }
+        }
+      }
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      const int64_t f = f0 + a * 8 + rg;
+      if (f < nf && bj[a] != INT64_MAX) {
+        const unsigned long long key =
+            ((unsigned long long)__float_as_uint(fmaxf(bv[a], 0.f)) << 32) | (unsigned long long)(uint32_t)bj[a];
+        atomicMin(keys + f, key);
+      }
+    }
+  }
+}
+
 static void launch_blocked(const float* X, int d, const float* P, int64_t k, const int32_t* rows,
                            const int32_t* count_dev, int64_t cap, unsigned long long* keys_ws, int32_t* labels,
                            float* best, cudaStream_t st, const int* active) {
   k_keys_init<<<num_sms() * 2, 256, 0, st>>>(count_dev, cap, keys_ws, active);
   MASK_LAUNCH_CHECK();
-  k_blocked_argmin<<<num_sms() * 4, 256, 0, st>>>(X, d, P, k, rows, count_dev, cap, num_sms(), keys_ws, active);
+  const int d4 = (d + 3) / 4;
+  const int d4p = d4 | 1;  // odd float4 stride
+  const size_t rb_smem = (size_t)(RB_R + RB_P) * d4p * sizeof(float4);
+  if (d <= 256 && rb_smem <= 200 * 1024) {
+    static int attr_for = -1;
+    if (rb_smem > 48 * 1024 && attr_for < (int)rb_smem) {
+      MASK_CUDA(cudaFuncSetAttribute(k_rb_argmin, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      attr_for = 200 * 1024;
+    }
+    k_rb_argmin<<<num_sms() * 2, 256, rb_smem, st>>>(X, d, d4p, P, k, rows, count_dev, cap, num_sms(), keys_ws,
+                                                    active);
+  } else {
+    k_blocked_argmin<<<num_sms() * 4, 256, 0, st>>>(X, d, P, k, rows, count_dev, cap, num_sms(), keys_ws, active);
+  }
   MASK_LAUNCH_CHECK();
   k_keys_write<<<num_sms() * 2, 256, 0, st>>>(rows, count_dev, cap, keys_ws, labels, best, active);
   MASK_LAUNCH_CHECK();
