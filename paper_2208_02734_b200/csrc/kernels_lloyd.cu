@@ -403,6 +403,7 @@ __global__ void __launch_bounds__(256) k_rb_argmin(const float* __restrict__ X, 
   const int rg = t & 7, pg = t >> 3;  // rows a*8+rg, prototypes b*32+pg (a, b < 4): interleaved so
                                       // the 16-byte smem reads of a warp hit distinct banks
   const int d4 = (d + 3) / 4;
+  const bool vec = (d & 3) == 0 && ((uintptr_t)X & 15) == 0 && ((uintptr_t)P & 15) == 0;
   const int64_t row_blocks = (nf + RB_R - 1) / RB_R;
   const int64_t ntile = (k + RB_P - 1) / RB_P;
   int64_t splits = (4LL * nsm + row_blocks - 1) / row_blocks;
@@ -421,10 +422,14 @@ __global__ void __launch_bounds__(256) k_rb_argmin(const float* __restrict__ X, 
       float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
       if (row >= 0) {
         const float* src = X + row * d + 4 * c4;
-        v.x = src[0];
-        if (4 * c4 + 1 < d) v.y = src[1];
-        if (4 * c4 + 2 < d) v.z = src[2];
-        if (4 * c4 + 3 < d) v.w = src[3];
+        if (vec) {
+          v = __ldg(reinterpret_cast<const float4*>(src));
+        } else {
+          v.x = src[0];
+          if (4 * c4 + 1 < d) v.y = src[1];
+          if (4 * c4 + 2 < d) v.z = src[2];
+          if (4 * c4 + 3 < d) v.w = src[3];
+        }
       }
       xs[r * d4p + c4] = v;
     }
@@ -443,10 +448,14 @@ __global__ void __launch_bounds__(256) k_rb_argmin(const float* __restrict__ X, 
         float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
         if (j0 + pr < k) {
           const float* src = P + (j0 + pr) * d + 4 * c4;
-          v.x = src[0];
-          if (4 * c4 + 1 < d) v.y = src[1];
-          if (4 * c4 + 2 < d) v.z = src[2];
-          if (4 * c4 + 3 < d) v.w = src[3];
+          if (vec) {
+            v = __ldg(reinterpret_cast<const float4*>(src));
+          } else {
+            v.x = src[0];
+            if (4 * c4 + 1 < d) v.y = src[1];
+            if (4 * c4 + 2 < d) v.z = src[2];
+            if (4 * c4 + 3 < d) v.w = src[3];
+          }
         }
         cs[pr * d4p + c4] = v;
       }
