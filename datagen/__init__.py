@@ -241,6 +241,23 @@ def data_parallel(cfg: Config, workers: Optional[int] = None):
     return np.ndarray(shape, dtype=np.float32, buffer=shm.buf), shm
 
 
+def group_perm(seed: int, n: int) -> np.ndarray:
+    """The seeded random split order of the grouped construction's data layer (points
+    "randomly assigned" to groups): a permutation of range(n)."""
+    return _rng(seed, 0).permutation(n).astype(np.int64)
+
+
+def gaussian_clouds(seed: int, per_cloud: int, radius: float, sigma: float = 1.0, clouds: int = 8) -> np.ndarray:
+    """``clouds`` isotropic Gaussian clouds in R^2 (the paper's synthetic benchmark),
+    centres evenly spaced on a circle of ``radius``; radius >> sigma gives the no-overlap version
+    (centres and sigma are unspecified in the paper: flagged reading G6)."""
+    g = _rng(seed, 0)
+    ang = np.arange(clouds) * (2.0 * np.pi / clouds)
+    centres = radius * np.stack([np.cos(ang), np.sin(ang)], axis=1)
+    comp = np.repeat(np.arange(clouds), per_cloud)
+    return (centres[comp] + sigma * g.standard_normal((clouds * per_cloud, 2))).astype(np.float32)
+
+
 def data(cfg: Config, start: int = 0, count: Optional[int] = None):
     """Rows [start, start+count) of config ``cfg``'s dataset (dense fp32 n x d, or CSR triple)."""
     count = cfg.n - start if count is None else count

@@ -150,6 +150,36 @@ void mask_comm_free(mask_comm* comm); /* NULL-safe */
 int32_t mask_build(const mask_matrix* data, const mask_build_params* params, mask_comm* comm,
                    void* stream, mask_index** out);
 
+/* ---------------------------------------------------------------- grouped build
+ * The paper's own construction (Algorithm 1): the data
+ * layer's n rows are split, in `perm` order, into g_1 = floor(n / length_group) groups of
+ * balanced sizes (the last n mod g_1 groups hold one more row, G1); every group is
+ * clustered independently into n_centroids prototypes (Lloyd from the group's first
+ * n_centroids items, max_iters iterations, no-change stop, empty clusters keep; G3, D3-D5);
+ * the g_i * n_centroids prototypes (group-major) are the next layer's items, re-chunked
+ * contiguously (G2); layers continue while floor(n_i / length_group) >= 1 (the
+ * floor recurrence).  The index has the same shape as mask_build's (levels = centroid layers,
+ * labels = global prototype ids, explicit child lists), so mask_query / the getters apply
+ * (D7: descent over explicit children).  Dense data only, single GPU.
+ *   perm: optional host array of `rows` distinct indices (the seeded random split; NULL =
+ *         data order); borrowed for the call.
+ * Errors: MASK_ERR_ARG (n_centroids < 1 or >= length_group, rows < length_group, a group
+ * smaller than n_centroids, perm not a permutation), MASK_ERR_UNSUPPORTED (CSR data, depth >
+ * 16 layers, a group's working set > 200 KB of shared memory), MASK_ERR_CUDA. */
+typedef struct {
+  int32_t length_group; /* points per group (paper's lengthGroup) */
+  int32_t n_centroids;  /* prototypes per group (paper's nCentroids) */
+  int32_t max_iters;    /* Lloyd iterations per group (T >= 0) */
+  int32_t flags;        /* MASK_BORROW_DATA */
+  const int64_t* perm;  /* data-layer order (host, rows entries) or NULL */
+} mask_grouped_params;
+
+/* Depth (number of centroid layers) of the grouped construction for n points; writes the
+ * prototypes per layer to layer_k[0..min(depth, cap)) when non-NULL.  <0 on bad arguments. */
+int32_t mask_grouped_depth(int64_t n, int32_t length_group, int32_t n_centroids, int64_t* layer_k, int32_t cap);
+int32_t mask_build_grouped(const mask_matrix* data, const mask_grouped_params* params, void* stream,
+                           mask_index** out);
+
 /* ---------------------------------------------------------------- query
  * Batched approximate k-NN (Algorithm 2) of `queries` (same dim/format family
  * as the index: dense queries against a dense index, CSR queries against a CSR index).

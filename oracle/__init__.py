@@ -221,6 +221,62 @@ def build_index(X, init_idx: Sequence[np.ndarray], T: int, tol: float = 0.0, csr
     return Index(levels, offs, mems, dim)
 
 
+# ------------------------------------------------------------------ grouped construction
+def grouped_layer_sizes(n: int, length_group: int, n_centroids: int) -> List[Tuple[int, int]]:
+    """Algorithm 1's loop: ngroups <- n / lengthGroup (integer, floor), and while
+    ngroups >= 1 a layer of ngroups * nCentroids prototypes is built over n items, after which
+    n <- ngroups * nCentroids.  Returns [(n_items, ngroups)] per layer."""
+    if not 1 <= n_centroids < length_group:
+        raise ValueError("need 1 <= nCentroids < lengthGroup (the recurrence does not shrink otherwise)")
+    out = []
+    g = n // length_group
+    while g >= 1:
+        out.append((n, g))
+        n = g * n_centroids
+        g = n // length_group
+    return out
+
+
+def build_grouped(X, length_group: int, n_centroids: int, T: int, perm=None) -> Index:
+    """Grouped multilevel construction (Algorithm 1) with the readings of DESIGN.md
+    G1-G5: the data layer is taken in ``perm`` order, every layer is chunked into ngroups
+    balanced groups (sizes floor(n/g), the last n mod g groups one larger), each group is
+    clustered by ``lloyd`` from its first nCentroids items, prototypes are stored group-major
+    (global id = group * nCentroids + local id), and the next layer re-chunks them in order."""
+    Y = _f64(X)
+    levels, offs, mems = [], [], []
+    order = np.arange(Y.shape[0]) if perm is None else np.asarray(perm, np.int64)
+    for n, g in grouped_layer_sizes(Y.shape[0], length_group, n_centroids):
+        base, rem = divmod(n, g)
+        P = np.empty((g * n_centroids, Y.shape[1]), np.float64)
+        lab = np.empty(n, np.int32)
+        start = 0
+        for gi in range(g):
+            size = base + (1 if gi >= g - rem else 0)
+            items = order[start:start + size]
+            start += size
+            res = lloyd(Y[items], np.arange(n_centroids), T)
+            P[gi * n_centroids:(gi + 1) * n_centroids] = res.P
+            lab[items] = gi * n_centroids + res.labels
+        res_l = LevelResult(P, lab, np.zeros(0), np.zeros(0, np.int64), 0)
+        levels.append(res_l)
+        o, m = children(lab, P.shape[0])
+        offs.append(o)
+        mems.append(m)
+        Y = P
+        order = np.arange(P.shape[0])
+    return Index(levels, offs, mems, Y.shape[1])
+
+
+def exhaustive_error(index: Index, X) -> float:
+    """Fraction of the indexed points whose single-path (beam 1) descent over the explicit child
+    lists does not return the point itself as its nearest neighbour (point search of every
+    element; SPEC exhaustive_error)."""
+    X = _f64(X)
+    ids, _, _ = query(index.P, index.offsets, index.members, X, X, 1, 1)
+    return float(np.mean(ids[:, 0] != np.arange(X.shape[0])))
+
+
 # ------------------------------------------------------------------ queries
 def _ptr_array(arrs, ctype):
     return (C.POINTER(ctype) * len(arrs))(*[a.ctypes.data_as(C.POINTER(ctype)) for a in arrs])

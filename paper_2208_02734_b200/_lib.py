@@ -41,6 +41,7 @@ EXPORTS = [
     "mask_comm_free", "mask_build", "mask_query", "mask_free", "mask_assign", "mask_update",
     "mask_num_levels", "mask_level_info", "mask_get_prototypes", "mask_get_labels",
     "mask_get_children", "mask_get_trace", "mask_kernel_launches", "mask_get_timing",
+    "mask_grouped_depth", "mask_build_grouped",
 ]
 
 
@@ -76,6 +77,16 @@ class MaskBuildParams(C.Structure):
         ("flags", C.c_int32),
         ("iter_cb", ITER_CB),
         ("iter_cb_user", C.c_void_p),
+    ]
+
+
+class MaskGroupedParams(C.Structure):
+    _fields_ = [
+        ("length_group", C.c_int32),
+        ("n_centroids", C.c_int32),
+        ("max_iters", C.c_int32),
+        ("flags", C.c_int32),
+        ("perm", C.POINTER(C.c_int64)),
     ]
 
 
@@ -123,6 +134,8 @@ def load():
             "mask_get_trace": (i32, [P, i32, P, P, P, i32]),
             "mask_kernel_launches": (i64, []),
             "mask_get_timing": (i32, [P, i32, P, i32]),
+            "mask_grouped_depth": (i32, [i64, i32, i32, P, i32]),
+            "mask_build_grouped": (i32, [C.POINTER(MaskMatrix), C.POINTER(MaskGroupedParams), P, C.POINTER(P)]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)

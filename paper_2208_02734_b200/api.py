@@ -224,7 +224,7 @@ class Index:
             check(n)
         names = ["assign", "fixup", "update", "finalize"]
         res = {nm: dict(ms=float(out[2 * i]), launches=int(out[2 * i + 1])) for i, nm in enumerate(names)}
-        res["assign_kernel"] = {0: "K2-simt", 1: "K1-tcgen05-3xtf32", 2: "K3-csr", 3: "K11-fused-small-level"}.get(int(out[8]), "none")
+        res["assign_kernel"] = {0: "K2-simt", 1: "K1-tcgen05-3xtf32", 2: "K3-csr", 3: "K11-fused-small-level", 4: "K12-grouped"}.get(int(out[8]), "none")
         return res
 
 
@@ -270,6 +270,36 @@ def build(data, levels: Sequence[int], iters: int, init_idx: Sequence[np.ndarray
     check(rc)
     keep_all = keep if (flags & _lib.MASK_BORROW_DATA) else ()
     return Index(out.value, keep_all, m.dim, m.format == _lib.MASK_CSR_F32)
+
+
+def grouped_depth(n: int, length_group: int, n_centroids: int) -> Tuple[int, List[int]]:
+    """Depth and prototypes per layer of the grouped construction (floor recurrence)."""
+    cap = 64
+    out = (C.c_int64 * cap)()
+    depth = load().mask_grouped_depth(int(n), int(length_group), int(n_centroids), out, cap)
+    if depth < 0:
+        check(depth)
+    return depth, [int(out[i]) for i in range(min(depth, cap))]
+
+
+def build_grouped(data, length_group: int, n_centroids: int, iters: int, perm: Optional[np.ndarray] = None,
+                  flags: int = 0, stream=None) -> Index:
+    """mask_build_grouped: the paper's Algorithm 1 (groups of ``length_group`` items, each
+    clustered into ``n_centroids`` prototypes; ``perm`` = the seeded data-layer split order)."""
+    m, keep = matrix(data)
+    p = _lib.MaskGroupedParams()
+    p.length_group = int(length_group)
+    p.n_centroids = int(n_centroids)
+    p.max_iters = int(iters)
+    p.flags = int(flags)
+    perm_arr = None
+    if perm is not None:
+        perm_arr = np.ascontiguousarray(perm, dtype=np.int64)
+        p.perm = perm_arr.ctypes.data_as(C.POINTER(C.c_int64))
+    out = C.c_void_p()
+    check(load().mask_build_grouped(C.byref(m), C.byref(p), _stream(stream), C.byref(out)))
+    keep_all = keep if (flags & _lib.MASK_BORROW_DATA) else ()
+    return Index(out.value, keep_all, m.dim, False)
 
 
 def assign(data, P, flags: int = 0, stream=None):

@@ -132,6 +132,12 @@ bool small_level_supported(int64_t n, int d, int64_t k);
 void launch_small_level(const float* Y, int64_t n, int d, int64_t k, float* P, int32_t* lab, int32_t* prev,
                         float* best, double* S, int32_t* counts, double* J, unsigned long long* changed,
                         uint32_t* fin, int* ctrl, unsigned* bar_ws, int T, double tol, cudaStream_t st);
+// K12: one layer of the grouped construction (Algorithm 1): g groups of the n_items rows of Y
+// (through perm when given), nc prototypes each, T Lloyd iterations per group; P_out = g*nc x d
+// (group-major), labels[row] = global prototype id.
+size_t group_lloyd_smem(int64_t n_items, int64_t g, int nc, int d);
+void launch_group_lloyd(const float* Y, int d, const int64_t* perm, int64_t n_items, int64_t g, int nc, int T,
+                        float* P_out, int32_t* labels, cudaStream_t st);
 // K4: exact FP32 direct re-check of flagged rows against all k prototypes.
 void launch_fixup(const float* X, int d, const float* P, int64_t k, const int32_t* flag_rows,
                   const int32_t* flag_count, int64_t max_flags, int32_t* labels, float* best,

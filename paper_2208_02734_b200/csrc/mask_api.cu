@@ -850,6 +850,88 @@ void build_impl(const mask_matrix* data, const mask_build_params* p, mask_comm* 
   *out = idx.release();
 }
 
+// Grouped construction (Algorithm 1; G1-G5): layer sizes by the floor
+// recurrence g_i = floor(n_{i-1} / lengthGroup), n_i = g_i * nCentroids, while g_i >= 1.
+int grouped_layers(int64_t n, int64_t lg, int64_t nc, std::vector<std::pair<int64_t, int64_t>>* out) {
+  int depth = 0;
+  int64_t g = n / lg;
+  while (g >= 1) {
+    if (out) out->push_back({n, g});
+    ++depth;
+    n = g * nc;
+    g = n / lg;
+  }
+  return depth;
+}
+
+void build_grouped_impl(const mask_matrix* data, const mask_grouped_params* p, cudaStream_t st, mask_index** out) {
+  MASK_REQUIRE(out != nullptr, MASK_ERR_ARG, "out is NULL");
+  *out = nullptr;
+  check_matrix(data, "data");
+  MASK_REQUIRE(p != nullptr, MASK_ERR_ARG, "params is NULL");
+  MASK_REQUIRE(data->format == MASK_DENSE_F32, MASK_ERR_UNSUPPORTED, "grouped build takes dense data");
+  MASK_REQUIRE(data->n_global == data->rows && data->row_offset == 0, MASK_ERR_ARG,
+               "grouped build is single-GPU: n_global must equal rows");
+  MASK_REQUIRE(p->length_group >= 2 && p->n_centroids >= 1 && p->n_centroids < p->length_group, MASK_ERR_ARG,
+               "need 1 <= n_centroids < length_group (the layer sizes do not shrink otherwise)");
+  MASK_REQUIRE(p->max_iters >= 0, MASK_ERR_ARG, "max_iters must be >= 0");
+  const int64_t N = data->rows;
+  std::vector<std::pair<int64_t, int64_t>> layers;
+  grouped_layers(N, p->length_group, p->n_centroids, &layers);
+  MASK_REQUIRE(!layers.empty(), MASK_ERR_ARG, "fewer points than length_group: no centroid layer");
+  MASK_REQUIRE((int)layers.size() <= kMaxLevels, MASK_ERR_UNSUPPORTED, "grouped depth exceeds 16 layers");
+  for (const auto& lg : layers)
+    MASK_REQUIRE(lg.first / lg.second >= p->n_centroids, MASK_ERR_ARG,
+                 "a group holds fewer items than n_centroids");
+  const int d = data->dim;
+  auto idx = std::make_unique<mask_index>();
+  idx->dim = d;
+  idx->format = MASK_DENSE_F32;
+  idx->n_global = N;
+  const size_t cnt = (size_t)N * d;
+  const bool borrow = (p->flags & MASK_BORROW_DATA) && data->memory == MASK_MEM_DEVICE;
+  if (borrow) {
+    idx->X = data->values;
+  } else {
+    idx->own_X.alloc(std::max<size_t>(cnt, 1));
+    MASK_CUDA(cudaMemcpyAsync(idx->own_X.p, data->values, sizeof(float) * cnt,
+                              data->memory == MASK_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, st));
+    idx->X = idx->own_X.p;
+  }
+  DevBuf<int64_t> perm;
+  if (p->perm) {
+    std::vector<char> seen(N, 0);
+    for (int64_t i = 0; i < N; ++i) {
+      const int64_t v = p->perm[i];
+      MASK_REQUIRE(v >= 0 && v < N && !seen[v], MASK_ERR_ARG, "perm must be a permutation of [0, rows)");
+      seen[v] = 1;
+    }
+    perm.alloc(N);
+    MASK_CUDA(cudaMemcpyAsync(perm.p, p->perm, sizeof(int64_t) * N, cudaMemcpyHostToDevice, st));
+  }
+  idx->levels.resize(layers.size());
+  const float* Y = idx->X;
+  for (size_t l = 0; l < layers.size(); ++l) {
+    Level& L = idx->levels[l];
+    const int64_t n_items = layers[l].first, g = layers[l].second;
+    L.n_items = n_items;
+    L.k = g * p->n_centroids;
+    L.dim = d;
+    L.P.alloc((size_t)L.k * d);
+    L.labels.alloc(n_items);
+    L.assign_kernel = 4;
+    launch_group_lloyd(Y, d, l == 0 ? perm.p : nullptr, n_items, g, p->n_centroids, p->max_iters, L.P.p,
+                       L.labels.p, st);
+    L.offsets.alloc(L.k + 1);
+    L.members.alloc(std::max<int64_t>(n_items, 1));
+    DevBuf<int32_t> cursor(L.k);
+    launch_children(L.labels.p, n_items, L.k, L.offsets.p, L.members.p, cursor.p, st);
+    MASK_CUDA(cudaStreamSynchronize(st));  // cursor / perm scratch go out of scope
+    Y = L.P.p;
+  }
+  *out = idx.release();
+}
+
 const Level& level_of(const mask_index* idx, int level) {
   MASK_REQUIRE(idx != nullptr, MASK_ERR_ARG, "index is NULL");
   MASK_REQUIRE(level >= 1 && level <= (int)idx->levels.size(), MASK_ERR_ARG, "level out of range");
@@ -911,6 +993,19 @@ void mask_comm_free(mask_comm* comm) {
 int32_t mask_build(const mask_matrix* data, const mask_build_params* params, mask_comm* comm,
                    void* stream, mask_index** out) {
   return guarded([&] { build_impl(data, params, comm, as_stream(stream), out); });
+}
+
+int32_t mask_grouped_depth(int64_t n, int32_t length_group, int32_t n_centroids, int64_t* layer_k, int32_t cap) {
+  if (n < 0 || n_centroids < 1 || n_centroids >= length_group) return MASK_ERR_ARG;
+  std::vector<std::pair<int64_t, int64_t>> layers;
+  const int depth = grouped_layers(n, length_group, n_centroids, &layers);
+  for (int i = 0; i < depth && i < cap && layer_k; ++i) layer_k[i] = layers[i].second * n_centroids;
+  return depth;
+}
+
+int32_t mask_build_grouped(const mask_matrix* data, const mask_grouped_params* params, void* stream,
+                           mask_index** out) {
+  return guarded([&] { build_grouped_impl(data, params, as_stream(stream), out); });
 }
 
 int32_t mask_query(const mask_index* idx, const mask_matrix* queries, int32_t k_nn, int32_t beam,

@@ -322,3 +322,84 @@ def test_query_sparse_matches_densified():
 def test_recall_definition():
     assert oracle.recall(np.array([[1, 2, 3]]), np.array([[3, 2, 9]])) == pytest.approx(2 / 3)
     assert oracle.recall(np.array([[-1, -1]]), np.array([[0, 1]])) == 0.0
+
+
+# ------------------------------------------------------------------ grouped construction (NEXT-1)
+def _golden_grouped():
+    with open(os.path.join(GOLDEN, "paper_grouped_depth.json")) as f:
+        return json.load(f)
+
+
+def test_grouped_depth_matches_paper_tables():
+    # PAPER.md P:1457-1467 and P:1506-1516 (Tree depth column, 80,000 points)
+    g = _golden_grouped()
+    for row in g["depth_by_params"]:
+        layers = oracle.grouped_layer_sizes(g["n_points"], row["length_group"], row["n_centroids"])
+        assert len(layers) == row["tree_depth"], row
+
+
+def test_grouped_first_layer_of_the_1600_point_example():
+    # 1,600 points, lengthGroup 16, nCentroids 8 -> 100 groups, 800 centroids
+    ex = _golden_grouped()["first_layer_example"]
+    X = datagen.gaussian_clouds(1, ex["n_points"] // 8, 30.0)
+    idx = oracle.build_grouped(X, ex["length_group"], ex["n_centroids"], 5, datagen.group_perm(2, X.shape[0]))
+    assert oracle.grouped_layer_sizes(ex["n_points"], ex["length_group"], ex["n_centroids"])[0][1] == ex["groups"]
+    assert idx.levels[0].P.shape[0] == ex["first_layer_centroids"]
+    # top layer holds at most lengthGroup centroids ("less than or equal to")
+    assert idx.levels[-1].P.shape[0] <= ex["length_group"]
+
+
+def test_grouped_structure_and_per_group_clustering():
+    # SPEC index invariants: each group's child lists partition the group's chunk; every item is
+    # labelled with its nearest prototype of its own group (brute force, lowest ordinal on ties)
+    rng = np.random.default_rng(3)
+    X = rng.standard_normal((203, 3))
+    lg, nc = 20, 6
+    perm = datagen.group_perm(4, X.shape[0])
+    idx = oracle.build_grouped(X, lg, nc, 100, perm)
+    Y, order = X, perm
+    for lv, (n, g) in zip(idx.levels, oracle.grouped_layer_sizes(X.shape[0], lg, nc)):
+        base, rem = divmod(n, g)
+        start = 0
+        for gi in range(g):
+            size = base + (1 if gi >= g - rem else 0)
+            items = np.sort(order[start:start + size])
+            start += size
+            assert set(np.unique(lv.labels[items]) // nc) == {gi}
+            protos = lv.P[gi * nc:(gi + 1) * nc]
+            d = cdist(Y[items], protos, "sqeuclidean")
+            np.testing.assert_array_equal(lv.labels[items] - gi * nc, np.argmin(d, axis=1))
+            for c in range(nc):  # converged: non-empty prototypes are their members' means
+                mem = items[lv.labels[items] == gi * nc + c]
+                if mem.size:
+                    np.testing.assert_allclose(protos[c], Y[mem].mean(axis=0), rtol=1e-12, atol=1e-12)
+        Y, order = lv.P, np.arange(lv.P.shape[0])
+
+
+def test_grouped_single_centroid_groups_are_group_means():
+    # nCentroids = 1: each group's prototype is the mean of its chunk (closed form); 43 points in
+    # groups of 10 -> 4 groups of sizes 10, 11, 11, 11 (balanced split, remainder in the last groups)
+    rng = np.random.default_rng(5)
+    X = rng.standard_normal((43, 2))
+    perm = datagen.group_perm(6, 43)
+    idx = oracle.build_grouped(X, 10, 1, 3, perm)
+    assert len(idx.levels) == 1
+    chunks = [perm[0:10], perm[10:21], perm[21:32], perm[32:43]]
+    for gi, ch in enumerate(chunks):
+        np.testing.assert_allclose(idx.levels[0].P[gi], X[ch].mean(axis=0), rtol=1e-13)
+        assert np.all(idx.levels[0].labels[ch] == gi)
+    with pytest.raises(ValueError):
+        oracle.grouped_layer_sizes(100, 10, 10)
+
+
+def test_grouped_no_overlap_clouds_point_search_error_zero():
+    # X_GNO (8 well-separated clouds x 200 points, lengthGroup 16,
+    # nCentroids 8): "able to correctly find all points without errors" -> 0.0 %.  Read as the
+    # cloud-level error of the descent (G7): the point returned for every self-query
+    # lies in the query's own cloud.
+    X = datagen.gaussian_clouds(31, 200, 40.0, 1.0)
+    idx = oracle.build_grouped(X, 16, 8, 20, datagen.group_perm(32, X.shape[0]))
+    assert len(idx.levels) == 7  # P:1250-1251 "final depth of 8 layers" = 7 centroid layers + data
+    ids, _, _ = oracle.query(idx.P, idx.offsets, idx.members, X, X, 1, 1)
+    cloud = np.repeat(np.arange(8), 200)
+    assert np.mean(cloud[ids[:, 0]] != cloud) == 0.0
