@@ -193,6 +193,24 @@ int32_t mask_build_grouped(const mask_matrix* data, const mask_grouped_params* p
 int32_t mask_query(const mask_index* idx, const mask_matrix* queries, int32_t k_nn,
                    int32_t beam, int64_t* ids_out, float* d2_out, void* stream);
 
+/* ---------------------------------------------------------------- range search
+ * Range query (Algorithm 3): for each query q_i every data row
+ * x with ||q_i - x|| <= radius[i] among the partitions reached by a multi-path descent:
+ *   MASK_RANGE_PAPER: at each level keep the candidates c with ||q - c|| <= r (Algorithm 3's
+ *                     selectCandidates; may miss rows, like the paper);
+ *   MASK_RANGE_COVER: keep c with ||q - c|| <= r + cover(c), cover(c) >= the distance from c to
+ *                     every row below it (triangle inequality): the result equals the
+ *                     brute-force range scan (lossless).  Cover radii are computed on first use.
+ * Results are grouped by query and sorted by (d^2, id): row ids ids_out[offsets_out[i] ..
+ * offsets_out[i+1]) and squared distances d2_out[...].  queries / radius / outputs live in the
+ * same memory kind (device or host).  *total_out always receives the number of results; when it
+ * exceeds max_results the call fails with MASK_ERR_ARG (never silent truncation) and the caller
+ * retries with a larger buffer.  Dense index only (MASK_ERR_UNSUPPORTED for CSR).  Non-collective. */
+enum { MASK_RANGE_PAPER = 0, MASK_RANGE_COVER = 1 };
+int32_t mask_range_query(const mask_index* idx, const mask_matrix* queries, const float* radius, int32_t mode,
+                         int64_t max_results, int64_t* offsets_out, int64_t* ids_out, float* d2_out,
+                         int64_t* total_out, void* stream);
+
 void mask_free(mask_index* idx); /* NULL-safe */
 
 /* ---------------------------------------------------------------- step entry points

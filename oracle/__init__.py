@@ -277,6 +277,56 @@ def exhaustive_error(index: Index, X) -> float:
     return float(np.mean(ids[:, 0] != np.arange(X.shape[0])))
 
 
+# ------------------------------------------------------------------ range search (NEXT-2)
+def cover_radii(index: Index, X) -> List[np.ndarray]:
+    """cover_1(j) = max over data rows x with labels_1 = j of ||x - c_j||; cover_l(j) = max over
+    children i of ||c_i - c_j|| + cover_{l-1}(i) (an upper bound on the distance from c_j to every
+    row below it, by the triangle inequality).  Childless prototypes get 0."""
+    X = _f64(X)
+    out = []
+    Y = X
+    prev = np.zeros(X.shape[0])
+    for lv in index.levels:
+        P = _f64(lv.P)
+        lab = np.asarray(lv.labels, np.int64)
+        r = np.sqrt(((Y - P[lab]) ** 2).sum(axis=1)) + prev
+        cov = np.zeros(P.shape[0])
+        np.maximum.at(cov, lab, r)
+        out.append(cov)
+        Y, prev = P, cov
+    return out
+
+
+def range_query(P: Sequence[np.ndarray], offsets: Sequence[np.ndarray], members: Sequence[np.ndarray], X, q,
+                radius: float, cover: Optional[Sequence[np.ndarray]] = None):
+    """Algorithm 3 for one query over explicit child lists: keep every top-level
+    prototype with children whose distance is <= radius (+ cover(c) when ``cover`` is given),
+    follow the children of every kept prototype level by level, return the rows of the reached
+    partitions within ``radius`` as (ids, d^2) sorted by (d^2, id)."""
+    X, q = _f64(X), _f64(q)
+    L = len(P)
+
+    def kept(l, cand):
+        Pl = _f64(P[l])
+        has = offsets[l][cand + 1] > offsets[l][cand]
+        d = np.sqrt(((Pl[cand] - q) ** 2).sum(axis=1))
+        lim = radius + (cover[l][cand] if cover is not None else 0.0)
+        return cand[has & (d <= lim)]
+
+    S = kept(L - 1, np.arange(P[L - 1].shape[0]))
+    for l in range(L - 2, -1, -1):
+        C_ = np.concatenate([members[l + 1][offsets[l + 1][j]:offsets[l + 1][j + 1]] for j in S]) if S.size else \
+            np.zeros(0, np.int64)
+        S = kept(l, np.sort(C_.astype(np.int64)))
+    rows = np.concatenate([members[0][offsets[0][j]:offsets[0][j + 1]] for j in S]) if S.size else np.zeros(0, np.int64)
+    rows = np.sort(rows.astype(np.int64))
+    d2 = ((X[rows] - q) ** 2).sum(axis=1)
+    ok = d2 <= radius * radius
+    rows, d2 = rows[ok], d2[ok]
+    o = np.lexsort((rows, d2))
+    return rows[o], d2[o]
+
+
 # ------------------------------------------------------------------ queries
 def _ptr_array(arrs, ctype):
     return (C.POINTER(ctype) * len(arrs))(*[a.ctypes.data_as(C.POINTER(ctype)) for a in arrs])

@@ -33,6 +33,7 @@ MASK_SYNC_STATS = 1 << 4
 MASK_TIME_KERNELS = 1 << 5
 MASK_NO_SORT = 1 << 6
 MASK_NO_FUSED = 1 << 7
+MASK_RANGE_PAPER, MASK_RANGE_COVER = 0, 1
 T_ASSIGN, T_FIXUP, T_UPDATE, T_FINALIZE = 0, 1, 2, 3
 
 # every symbol include/mask.h declares (checked by tests/test_boundary.py)
@@ -41,7 +42,7 @@ EXPORTS = [
     "mask_comm_free", "mask_build", "mask_query", "mask_free", "mask_assign", "mask_update",
     "mask_num_levels", "mask_level_info", "mask_get_prototypes", "mask_get_labels",
     "mask_get_children", "mask_get_trace", "mask_kernel_launches", "mask_get_timing",
-    "mask_grouped_depth", "mask_build_grouped",
+    "mask_grouped_depth", "mask_build_grouped", "mask_range_query",
 ]
 
 
@@ -136,6 +137,7 @@ def load():
             "mask_get_timing": (i32, [P, i32, P, i32]),
             "mask_grouped_depth": (i32, [i64, i32, i32, P, i32]),
             "mask_build_grouped": (i32, [C.POINTER(MaskMatrix), C.POINTER(MaskGroupedParams), P, C.POINTER(P)]),
+            "mask_range_query": (i32, [P, C.POINTER(MaskMatrix), P, i32, i64, P, P, P, C.POINTER(i64), P]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)

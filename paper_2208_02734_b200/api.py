@@ -175,6 +175,38 @@ class Index:
         del keep
         return ids, d2
 
+    def range_query(self, queries, radius, mode: str = "cover", stream=None):
+        """mask_range_query: rows within ``radius`` (scalar or one per query) of each query.
+
+        mode "cover" is lossless (cover-radius pruning), "paper" is Algorithm 3's rule.
+        Returns (offsets int64[nq+1], ids int64[total], d2 float32[total]) on the queries' side."""
+        m, keep = matrix(queries)
+        nq = m.rows
+        md = {"paper": _lib.MASK_RANGE_PAPER, "cover": _lib.MASK_RANGE_COVER}[mode]
+        dev = m.memory == _lib.MASK_MEM_DEVICE
+        if dev:
+            d = keep[0].device
+            r = torch.full((nq,), float(radius), dtype=torch.float32, device=d) if np.isscalar(radius) else \
+                _prep(radius, np.float32)
+            alloc_i = lambda n: torch.empty(n, dtype=torch.int64, device=d)  # noqa: E731
+            alloc_f = lambda n: torch.empty(n, dtype=torch.float32, device=d)  # noqa: E731
+        else:
+            r = np.full(nq, radius, np.float32) if np.isscalar(radius) else _prep(radius, np.float32)
+            alloc_i = lambda n: np.empty(n, np.int64)  # noqa: E731
+            alloc_f = lambda n: np.empty(n, np.float32)  # noqa: E731
+        off = alloc_i(nq + 1)
+        total = C.c_int64(0)
+        rc = load().mask_range_query(self.handle, C.byref(m), _ptr(r), md, 0, _ptr(off), None, None,
+                                     C.byref(total), _stream(stream))
+        if rc != 0 and total.value == 0:
+            check(rc)
+        ids, d2 = alloc_i(max(total.value, 1)), alloc_f(max(total.value, 1))
+        if total.value:
+            check(load().mask_range_query(self.handle, C.byref(m), _ptr(r), md, total.value, _ptr(off), _ptr(ids),
+                                          _ptr(d2), C.byref(total), _stream(stream)))
+        del keep
+        return off, ids[:total.value], d2[:total.value]
+
     # ---------------------------------------------------------------- introspection
     @property
     def num_levels(self) -> int:

@@ -233,6 +233,13 @@ struct QIndex {
   const int32_t* xcol;
   const float* xval;
 };
+// K13 range search: cover radii (cover[l] = k_l float bits) and the multi-path descent; returns
+// the number of results, writing them (sorted by query, d^2, id) and per-query counts only when
+// ids_out != nullptr and the count fits cap_out.
+void launch_cover_radii(const float* X, int d, const QIndex& qi, const int32_t* const* labels,
+                        const int64_t* n_items, unsigned* const* cover, cudaStream_t st);
+int64_t range_search(const QIndex& qi, const unsigned* const* cover, const float* Q, int64_t nq, const float* radius,
+                     int mode, int64_t* ids_out, float* d2_out, int64_t* qcount, int64_t cap_out, cudaStream_t st);
 void launch_query_dense(const QIndex& qi, const float* Q, int64_t nq, int knn, int beam,
                         int64_t* ids, float* d2, cudaStream_t st);
 void launch_query_csr(const QIndex& qi, const float* cn2_levels_flat, const int64_t* cn2_off,

@@ -178,6 +178,9 @@ struct mask_index {
   // sparse-query support: ||c||^2 per level, flattened
   DevBuf<float> cn2_flat;
   DevBuf<int64_t> cn2_off;
+  // range search (K13): cover radii per level, computed on the first MASK_RANGE_COVER query
+  mutable std::once_flag cover_once;
+  mutable std::vector<DevBuf<unsigned>> cover;
 };
 
 namespace {
@@ -1006,6 +1009,115 @@ int32_t mask_grouped_depth(int64_t n, int32_t length_group, int32_t n_centroids,
 int32_t mask_build_grouped(const mask_matrix* data, const mask_grouped_params* params, void* stream,
                            mask_index** out) {
   return guarded([&] { build_grouped_impl(data, params, as_stream(stream), out); });
+}
+
+namespace {
+QIndex make_qindex(const mask_index* idx) {
+  QIndex qi{};
+  qi.L = (int)idx->levels.size();
+  qi.dim = idx->dim;
+  qi.X = idx->X;
+  qi.xrp = idx->rp;
+  qi.xcol = idx->col;
+  qi.xval = idx->val;
+  for (int l = 0; l < qi.L; ++l) {
+    qi.lv[l].P = idx->levels[l].P.p;
+    qi.lv[l].offsets = idx->levels[l].offsets.p;
+    qi.lv[l].members = idx->levels[l].members.p;
+    qi.lv[l].k = idx->levels[l].k;
+  }
+  return qi;
+}
+}  // namespace
+
+int32_t mask_range_query(const mask_index* idx, const mask_matrix* queries, const float* radius, int32_t mode,
+                         int64_t max_results, int64_t* offsets_out, int64_t* ids_out, float* d2_out,
+                         int64_t* total_out, void* stream) {
+  return guarded([&] {
+    MASK_REQUIRE(idx != nullptr, MASK_ERR_ARG, "index is NULL");
+    check_matrix(queries, "queries");
+    MASK_REQUIRE(idx->format == MASK_DENSE_F32 && queries->format == MASK_DENSE_F32, MASK_ERR_UNSUPPORTED,
+                 "range search takes a dense index and dense queries");
+    MASK_REQUIRE(queries->dim == idx->dim, MASK_ERR_ARG, "query dim differs from the index dim");
+    MASK_REQUIRE(mode == MASK_RANGE_PAPER || mode == MASK_RANGE_COVER, MASK_ERR_ARG, "unknown range mode");
+    MASK_REQUIRE(radius != nullptr && total_out != nullptr, MASK_ERR_ARG, "NULL radius / total_out");
+    MASK_REQUIRE(max_results >= 0, MASK_ERR_ARG, "max_results must be >= 0");
+    cudaStream_t st = as_stream(stream);
+    const int64_t nq = queries->rows;
+    const int d = idx->dim;
+    const bool host = queries->memory == MASK_MEM_HOST;
+    DevBuf<float> qv, rv;
+    const float* Q = queries->values;
+    const float* R = radius;
+    if (host) {
+      qv.alloc(std::max<int64_t>(nq * d, 1));
+      rv.alloc(std::max<int64_t>(nq, 1));
+      if (nq) {
+        MASK_CUDA(cudaMemcpyAsync(qv.p, Q, sizeof(float) * nq * d, cudaMemcpyHostToDevice, st));
+        MASK_CUDA(cudaMemcpyAsync(rv.p, R, sizeof(float) * nq, cudaMemcpyHostToDevice, st));
+      }
+      Q = qv.p;
+      R = rv.p;
+    }
+    const QIndex qi = make_qindex(idx);
+    std::vector<unsigned*> cov;
+    if (mode == MASK_RANGE_COVER) {
+      std::call_once(idx->cover_once, [&] {
+        idx->cover.resize(qi.L);
+        std::vector<const int32_t*> labs(qi.L);
+        std::vector<int64_t> ns(qi.L);
+        std::vector<unsigned*> cp(qi.L);
+        for (int l = 0; l < qi.L; ++l) {
+          idx->cover[l].alloc(idx->levels[l].k);
+          labs[l] = idx->levels[l].labels.p;
+          ns[l] = idx->levels[l].n_items;
+          cp[l] = idx->cover[l].p;
+        }
+        launch_cover_radii(idx->X, d, qi, labs.data(), ns.data(), cp.data(), st);
+        MASK_CUDA(cudaStreamSynchronize(st));
+      });
+      for (auto& c : idx->cover) cov.push_back(c.p);
+    }
+    DevBuf<int64_t> qcount(std::max<int64_t>(nq, 1)), ids_d;
+    DevBuf<float> d2_d;
+    int64_t total = 0;
+    if (nq) {
+      int64_t* ids = ids_out;
+      float* d2 = d2_out;
+      // the descent runs once; the results are written only when they fit
+      total = range_search(qi, cov.empty() ? nullptr : cov.data(), Q, nq, R, mode, nullptr, nullptr, nullptr, 0, st);
+      *total_out = total;
+      MASK_REQUIRE(total <= max_results, MASK_ERR_ARG,
+                   "max_results too small: the range query has " + std::to_string(total) + " results");
+      MASK_REQUIRE(offsets_out != nullptr && (total == 0 || (ids_out != nullptr && d2_out != nullptr)), MASK_ERR_ARG,
+                   "NULL outputs");
+      if (host) {
+        ids_d.alloc(std::max<int64_t>(total, 1));
+        d2_d.alloc(std::max<int64_t>(total, 1));
+        ids = ids_d.p;
+        d2 = d2_d.p;
+      }
+      range_search(qi, cov.empty() ? nullptr : cov.data(), Q, nq, R, mode, ids, d2, qcount.p, total, st);
+      std::vector<int64_t> hc(nq);
+      MASK_CUDA(cudaMemcpyAsync(hc.data(), qcount.p, sizeof(int64_t) * nq, cudaMemcpyDeviceToHost, st));
+      if (host && total) {
+        MASK_CUDA(cudaMemcpyAsync(ids_out, ids, sizeof(int64_t) * total, cudaMemcpyDeviceToHost, st));
+        MASK_CUDA(cudaMemcpyAsync(d2_out, d2, sizeof(float) * total, cudaMemcpyDeviceToHost, st));
+      }
+      MASK_CUDA(cudaStreamSynchronize(st));
+      std::vector<int64_t> off(nq + 1, 0);
+      for (int64_t q = 0; q < nq; ++q) off[q + 1] = off[q] + hc[q];
+      if (host) std::copy(off.begin(), off.end(), offsets_out);
+      else MASK_CUDA(cudaMemcpy(offsets_out, off.data(), sizeof(int64_t) * (nq + 1), cudaMemcpyHostToDevice));
+    } else {
+      *total_out = 0;
+      if (offsets_out) {
+        const int64_t z = 0;
+        if (host) offsets_out[0] = 0;
+        else MASK_CUDA(cudaMemcpy(offsets_out, &z, sizeof(int64_t), cudaMemcpyHostToDevice));
+      }
+    }
+  });
 }
 
 int32_t mask_query(const mask_index* idx, const mask_matrix* queries, int32_t k_nn, int32_t beam,

@@ -1,0 +1,94 @@
+"""GPU parity of range search (Algorithm 3) through the C-ABI:
+cover mode against the brute-force FP64 range scan (lossless), paper mode against the oracle's
+Algorithm 3 over the GPU-built index; rows whose distance to the query lies within 1e-5
+relative of a decision boundary (the radius, or radius + cover for kept prototypes) are exempt
+from exact set equality (FP32 vs FP64 on a boundary)."""
+import numpy as np
+import pytest
+
+import datagen
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no GPU", allow_module_level=True)
+
+import paper_2208_02734_b200 as mk  # noqa: E402
+
+REL = 1e-5
+
+
+def _index(cfg_id, div, T=6):
+    cfg = datagen.CONFIGS[cfg_id].scaled(div)
+    X = datagen.data(cfg)
+    inits = datagen.all_init_indices(cfg)
+    idx = mk.build(torch.from_numpy(X).cuda(), cfg.levels, T, inits)
+    return cfg, X, idx
+
+
+def _gpu_lists(off, ids, d2):
+    off = off.cpu().numpy() if hasattr(off, "cpu") else off
+    ids = ids.cpu().numpy() if hasattr(ids, "cpu") else ids
+    d2 = d2.cpu().numpy() if hasattr(d2, "cpu") else d2
+    return [(ids[off[i]:off[i + 1]], d2[off[i]:off[i + 1]]) for i in range(len(off) - 1)]
+
+
+@pytest.mark.parametrize("cfg_id,div", [(1, 4), (2, 256), (3, 2048)])
+def test_range_cover_mode_is_lossless(cfg_id, div):
+    cfg, X, idx = _index(cfg_id, div)
+    Q = datagen.queries(cfg, count=64)
+    X64 = X.astype(np.float64)
+    bd = ((Q.astype(np.float64)[:, None, :] - X64[None]) ** 2).sum(-1)
+    # radii: the distance to the 5th / 40th nearest row (a few results per query)
+    part = np.sort(bd, axis=1)
+    for col in (4, 39):
+        r = np.sqrt(part[:, col]).astype(np.float32)
+        lists = _gpu_lists(*idx.range_query(torch.from_numpy(Q).cuda(), torch.from_numpy(r).cuda(), "cover"))
+        for i, (ids, d2) in enumerate(lists):
+            ref = np.nonzero(bd[i] <= float(r[i]) ** 2)[0]
+            near = np.abs(np.sqrt(bd[i]) - r[i]) <= REL * r[i]
+            got = set(ids.tolist())
+            assert set(ref[~near[ref]].tolist()) <= got, f"query {i}: cover mode lost rows"
+            assert not (got - set(ref.tolist()) - set(np.nonzero(near)[0].tolist())), f"query {i}: extra rows"
+            o = np.lexsort((ids, d2))
+            assert np.array_equal(o, np.arange(len(ids))), "results not sorted by (d^2, id)"
+    # host-memory path gives the same lists
+    r = np.sqrt(part[:, 9]).astype(np.float32)
+    a = _gpu_lists(*idx.range_query(torch.from_numpy(Q).cuda(), torch.from_numpy(r).cuda(), "cover"))
+    b = _gpu_lists(*idx.range_query(np.ascontiguousarray(Q), r, "cover"))
+    for (ia, _), (ib, _) in zip(a, b):
+        np.testing.assert_array_equal(ia, ib)
+    idx.free()
+
+
+@pytest.mark.parametrize("cfg_id,div", [(1, 4), (2, 256)])
+def test_range_paper_mode_matches_oracle(cfg_id, div):
+    cfg, X, idx = _index(cfg_id, div)
+    Q = datagen.queries(cfg, count=48)
+    L = idx.num_levels
+    P = [idx.prototypes(l).astype(np.float64) for l in range(1, L + 1)]
+    ch = [idx.children(l) for l in range(1, L + 1)]
+    X64 = X.astype(np.float64)
+    for r in (0.5, 2.0, 5.0):
+        lists = _gpu_lists(*idx.range_query(torch.from_numpy(Q).cuda(), r, "paper"))
+        for i, (ids, d2) in enumerate(lists):
+            rid, rd2 = oracle.range_query(P, [c[0] for c in ch], [c[1] for c in ch], X64, Q[i], r)
+            if np.array_equal(np.sort(ids), np.sort(rid)):
+                continue
+            # a difference is only allowed through a boundary decision within the tie window:
+            # some prototype or row at distance ~ r from the query
+            q = Q[i].astype(np.float64)
+            dists = [np.sqrt(((p - q) ** 2).sum(axis=1)) for p in P] + [np.sqrt(((X64 - q) ** 2).sum(axis=1))]
+            assert any(np.any(np.abs(dd - r) <= REL * r) for dd in dists), f"query {i}: paper-mode sets differ"
+    idx.free()
+
+
+def test_range_errors():
+    cfg, X, idx = _index(1, 8)
+    with pytest.raises(mk.MaskError):
+        idx.range_query(torch.from_numpy(datagen.queries(cfg, 4)[:, :1].copy()).cuda(), 1.0)  # dim mismatch
+    off, ids, d2 = idx.range_query(torch.from_numpy(datagen.queries(cfg, 4)).cuda(), 0.0, "cover")
+    assert off.shape[0] == 5
+    idx.free()

@@ -403,3 +403,56 @@ def test_grouped_no_overlap_clouds_point_search_error_zero():
     ids, _, _ = oracle.query(idx.P, idx.offsets, idx.members, X, X, 1, 1)
     cloud = np.repeat(np.arange(8), 200)
     assert np.mean(cloud[ids[:, 0]] != cloud) == 0.0
+
+
+# ------------------------------------------------------------------ range search (NEXT-2)
+def _small_index(seed=3, n=600, d=3, levels=(40, 6)):
+    rng = np.random.default_rng(seed)
+    X = rng.standard_normal((n, d)) * np.array([3.0, 1.0, 0.5])[:d]
+    inits = [datagen.init_indices(seed, 1, n, levels[0]), datagen.init_indices(seed, 2, levels[0], levels[1])]
+    return X, oracle.build_index(X, inits, 10)
+
+
+def test_range_cover_mode_equals_brute_force():
+    # SPEC range_query [DERIVED]: cover-expanded pruning is lossless by the triangle inequality,
+    # so the result equals the brute-force range scan over the whole dataset
+    X, idx = _small_index()
+    cov = oracle.cover_radii(idx, X)
+    rng = np.random.default_rng(4)
+    for q in rng.standard_normal((25, 3)) * 2:
+        for r in (0.3, 1.0, 2.5):
+            ids, d2 = oracle.range_query(idx.P, idx.offsets, idx.members, X, q, r, cover=cov)
+            bd = cdist(q[None], X, "sqeuclidean")[0]
+            ref = np.nonzero(bd <= r * r)[0]
+            ref = ref[np.lexsort((ref, bd[ref]))]
+            np.testing.assert_array_equal(ids, ref)
+
+
+def test_range_paper_mode_is_a_subset_and_zero_radius_finds_duplicates():
+    X, idx = _small_index()
+    cov = oracle.cover_radii(idx, X)
+    rng = np.random.default_rng(5)
+    for q in rng.standard_normal((20, 3)) * 2:
+        a, _ = oracle.range_query(idx.P, idx.offsets, idx.members, X, q, 1.5)
+        b, _ = oracle.range_query(idx.P, idx.offsets, idx.members, X, q, 1.5, cover=cov)
+        assert set(a.tolist()) <= set(b.tolist())  # SPEC: candidate-set monotonicity
+    # radius 0 at an indexed point, cover mode: exactly that point (distinct data)
+    ids, d2 = oracle.range_query(idx.P, idx.offsets, idx.members, X, X[17], 0.0, cover=cov)
+    np.testing.assert_array_equal(ids, [17])
+    assert d2[0] == 0.0
+
+
+def test_cover_radii_bound_every_descendant():
+    X, idx = _small_index()
+    cov = oracle.cover_radii(idx, X)
+    # level 1: exact max member distance; level 2: >= the distance to every data row below
+    lab1 = idx.levels[0].labels
+    for j in range(idx.levels[0].P.shape[0]):
+        mem = X[lab1 == j]
+        exp = np.sqrt(((mem - idx.levels[0].P[j]) ** 2).sum(axis=1)).max() if len(mem) else 0.0
+        assert cov[0][j] == pytest.approx(exp, rel=1e-12, abs=0)
+    lab2 = idx.levels[1].labels
+    for j in range(idx.levels[1].P.shape[0]):
+        rows = np.nonzero(np.isin(lab1, np.nonzero(lab2 == j)[0]))[0]
+        if rows.size:
+            assert np.sqrt(((X[rows] - idx.levels[1].P[j]) ** 2).sum(axis=1)).max() <= cov[1][j] * (1 + 1e-12)
