@@ -211,6 +211,18 @@ int32_t mask_range_query(const mask_index* idx, const mask_matrix* queries, cons
                          int64_t max_results, int64_t* offsets_out, int64_t* ids_out, float* d2_out,
                          int64_t* total_out, void* stream);
 
+/* ---------------------------------------------------------------- insertion
+ * Dynamic insertion: each new point descends like a beam-1
+ * query (top level: nearest prototype with children; then the nearest of its children, ...)
+ * and joins the data partition of the level-1 prototype it reaches; prototypes are unchanged.
+ * New rows get ids n, n+1, ... (n = rows indexed so far); partition_out (optional, rows
+ * entries, same memory kind as `points`) receives the level-1 prototype of each.  A
+ * subsequent query with an inserted vector descends identically and finds it.  Mutates the
+ * index (single writer: no concurrent queries during the call); the index keeps its own copy
+ * of the grown data (a MASK_BORROW_DATA buffer is copied).  Dense single-GPU indexes only
+ * (MASK_ERR_UNSUPPORTED otherwise); MASK_ERR_ARG on a dim mismatch. */
+int32_t mask_insert(mask_index* idx, const mask_matrix* points, int64_t* partition_out, void* stream);
+
 void mask_free(mask_index* idx); /* NULL-safe */
 
 /* ---------------------------------------------------------------- step entry points

@@ -327,6 +327,29 @@ def range_query(P: Sequence[np.ndarray], offsets: Sequence[np.ndarray], members:
     return rows[o], d2[o]
 
 
+# ------------------------------------------------------------------ insertion (NEXT-4)
+def descend_leaf(P: Sequence[np.ndarray], offsets: Sequence[np.ndarray], members: Sequence[np.ndarray], q):
+    """The insertion procedure's path: at the top level the nearest prototype with
+    children, then the nearest of its children (with children), ... down to level 1.  Ties take
+    the lowest id (D4).  Returns (level-1 prototype, smallest relative gap of the decisions)."""
+    q = _f64(q)
+    L = len(P)
+
+    def pick(l, cand):
+        cand = np.asarray(cand, np.int64)
+        cand = cand[offsets[l][cand + 1] > offsets[l][cand]]
+        d = ((_f64(P[l])[cand] - q) ** 2).sum(axis=1)
+        o = np.lexsort((cand, d))
+        gap = (d[o[1]] - d[o[0]]) / d[o[1]] if len(o) > 1 and d[o[1]] > 0 else np.inf
+        return int(cand[o[0]]), gap
+
+    j, gap = pick(L - 1, np.arange(P[L - 1].shape[0]))
+    for l in range(L - 2, -1, -1):
+        j, g = pick(l, members[l + 1][offsets[l + 1][j]:offsets[l + 1][j + 1]])
+        gap = min(gap, g)
+    return j, gap
+
+
 # ------------------------------------------------------------------ queries
 def _ptr_array(arrs, ctype):
     return (C.POINTER(ctype) * len(arrs))(*[a.ctypes.data_as(C.POINTER(ctype)) for a in arrs])

@@ -42,7 +42,7 @@ EXPORTS = [
     "mask_comm_free", "mask_build", "mask_query", "mask_free", "mask_assign", "mask_update",
     "mask_num_levels", "mask_level_info", "mask_get_prototypes", "mask_get_labels",
     "mask_get_children", "mask_get_trace", "mask_kernel_launches", "mask_get_timing",
-    "mask_grouped_depth", "mask_build_grouped", "mask_range_query",
+    "mask_grouped_depth", "mask_build_grouped", "mask_range_query", "mask_insert",
 ]
 
 
@@ -138,6 +138,7 @@ def load():
             "mask_grouped_depth": (i32, [i64, i32, i32, P, i32]),
             "mask_build_grouped": (i32, [C.POINTER(MaskMatrix), C.POINTER(MaskGroupedParams), P, C.POINTER(P)]),
             "mask_range_query": (i32, [P, C.POINTER(MaskMatrix), P, i32, i64, P, P, P, C.POINTER(i64), P]),
+            "mask_insert": (i32, [P, C.POINTER(MaskMatrix), P, P]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)

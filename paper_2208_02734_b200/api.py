@@ -207,6 +207,18 @@ class Index:
         del keep
         return off, ids[:total.value], d2[:total.value]
 
+    def insert(self, points, stream=None):
+        """mask_insert: add ``points`` (dense) to the partitions their descent reaches; returns the
+        level-1 prototype of each (int64, on the points' side).  New row ids continue the index."""
+        m, keep = matrix(points)
+        if m.memory == _lib.MASK_MEM_DEVICE:
+            part = torch.empty(m.rows, dtype=torch.int64, device=keep[0].device)
+        else:
+            part = np.empty(m.rows, np.int64)
+        check(load().mask_insert(self.handle, C.byref(m), _ptr(part), _stream(stream)))
+        del keep
+        return part
+
     # ---------------------------------------------------------------- introspection
     @property
     def num_levels(self) -> int:

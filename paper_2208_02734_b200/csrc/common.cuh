@@ -173,6 +173,7 @@ void launch_assign_csr_chunked(const int64_t* row_ptr, const int32_t* col, const
                                const float* PT, const float* cn2, int64_t k, const int16_t* colslot,
                                const int32_t* hotcols, float2* state, int32_t* labels, float* best, cudaStream_t st,
                                const int* active = nullptr);
+void launch_i64_to_i32(const int64_t* a, int64_t n, int32_t* b, cudaStream_t st);
 // per-column non-zero counts (d int32, zeroed here)
 void launch_col_hist(const int32_t* col, int64_t nnz, int d, int32_t* cnt, cudaStream_t st);
 
@@ -240,8 +241,9 @@ void launch_cover_radii(const float* X, int d, const QIndex& qi, const int32_t* 
                         const int64_t* n_items, unsigned* const* cover, cudaStream_t st);
 int64_t range_search(const QIndex& qi, const unsigned* const* cover, const float* Q, int64_t nq, const float* radius,
                      int mode, int64_t* ids_out, float* d2_out, int64_t* qcount, int64_t cap_out, cudaStream_t st);
+// leaf_only: ids[q] = the level-1 prototype reached by the beam-1 descent (no data layer)
 void launch_query_dense(const QIndex& qi, const float* Q, int64_t nq, int knn, int beam,
-                        int64_t* ids, float* d2, cudaStream_t st);
+                        int64_t* ids, float* d2, cudaStream_t st, bool leaf_only = false);
 void launch_query_csr(const QIndex& qi, const float* cn2_levels_flat, const int64_t* cn2_off,
                       const int64_t* qrp, const int32_t* qcol, const float* qval, int64_t nq,
                       int knn, int beam, int64_t* ids, float* d2, cudaStream_t st);

@@ -1229,6 +1229,16 @@ void launch_label_sort(const int32_t* labels, int64_t n, int64_t k, const int32_
 }
 
 // ====================================================================== misc
+__global__ void k_i64_to_i32(const int64_t* __restrict__ a, int64_t n, int32_t* __restrict__ b) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    b[i] = (int32_t)a[i];
+}
+
+void launch_i64_to_i32(const int64_t* a, int64_t n, int32_t* b, cudaStream_t st) {
+  if (n <= 0) return;
+  k_i64_to_i32<<<grid_for(n, 256), 256, 0, st>>>(a, n, b);
+  MASK_LAUNCH_CHECK();
+}
 __global__ void k_check_finite(const float* __restrict__ v, int64_t count, int32_t* flag) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
        i += (int64_t)gridDim.x * blockDim.x)

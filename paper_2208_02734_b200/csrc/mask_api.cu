@@ -179,7 +179,9 @@ struct mask_index {
   DevBuf<float> cn2_flat;
   DevBuf<int64_t> cn2_off;
   // range search (K13): cover radii per level, computed on the first MASK_RANGE_COVER query
-  mutable std::once_flag cover_once;
+  // (and again after an insertion)
+  mutable std::mutex cover_mu;
+  mutable bool cover_valid = false;
   mutable std::vector<DevBuf<unsigned>> cover;
 };
 
@@ -1062,7 +1064,8 @@ int32_t mask_range_query(const mask_index* idx, const mask_matrix* queries, cons
     const QIndex qi = make_qindex(idx);
     std::vector<unsigned*> cov;
     if (mode == MASK_RANGE_COVER) {
-      std::call_once(idx->cover_once, [&] {
+      std::lock_guard<std::mutex> lock(idx->cover_mu);
+      if (!idx->cover_valid) {
         idx->cover.resize(qi.L);
         std::vector<const int32_t*> labs(qi.L);
         std::vector<int64_t> ns(qi.L);
@@ -1075,7 +1078,8 @@ int32_t mask_range_query(const mask_index* idx, const mask_matrix* queries, cons
         }
         launch_cover_radii(idx->X, d, qi, labs.data(), ns.data(), cp.data(), st);
         MASK_CUDA(cudaStreamSynchronize(st));
-      });
+        idx->cover_valid = true;
+      }
       for (auto& c : idx->cover) cov.push_back(c.p);
     }
     DevBuf<int64_t> qcount(std::max<int64_t>(nq, 1)), ids_d;
@@ -1117,6 +1121,54 @@ int32_t mask_range_query(const mask_index* idx, const mask_matrix* queries, cons
         else MASK_CUDA(cudaMemcpy(offsets_out, &z, sizeof(int64_t), cudaMemcpyHostToDevice));
       }
     }
+  });
+}
+
+int32_t mask_insert(mask_index* idx, const mask_matrix* points, int64_t* partition_out, void* stream) {
+  return guarded([&] {
+    MASK_REQUIRE(idx != nullptr, MASK_ERR_ARG, "index is NULL");
+    check_matrix(points, "points");
+    MASK_REQUIRE(idx->format == MASK_DENSE_F32 && points->format == MASK_DENSE_F32, MASK_ERR_UNSUPPORTED,
+                 "insertion takes a dense index and dense points");
+    MASK_REQUIRE(points->dim == idx->dim, MASK_ERR_ARG, "point dim differs from the index dim");
+    const int64_t m = points->rows;
+    if (m == 0) return;
+    cudaStream_t st = as_stream(stream);
+    const int d = idx->dim;
+    const int64_t n = idx->n_global;
+    Level& L1 = idx->levels[0];
+    // new rows appended to the index's own copy of the data (a borrowed buffer is copied first)
+    DevBuf<float> X2((size_t)(n + m) * d);
+    MASK_CUDA(cudaMemcpyAsync(X2.p, idx->X, sizeof(float) * n * d, cudaMemcpyDeviceToDevice, st));
+    MASK_CUDA(cudaMemcpyAsync(X2.p + n * d, points->values, sizeof(float) * m * d,
+                              points->memory == MASK_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice,
+                              st));
+    // the level-1 prototype each new point's descent reaches
+    const QIndex qi = make_qindex(idx);
+    DevBuf<int64_t> leaf(m);
+    launch_query_dense(qi, X2.p + n * d, m, 1, 1, leaf.p, nullptr, st, true);
+    DevBuf<int32_t> lab2(n + m);
+    MASK_CUDA(cudaMemcpyAsync(lab2.p, L1.labels.p, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, st));
+    launch_i64_to_i32(leaf.p, m, lab2.p + n, st);
+    DevBuf<int64_t> off(L1.k + 1);
+    DevBuf<int32_t> mem(n + m), cursor(L1.k);
+    launch_children(lab2.p, n + m, L1.k, off.p, mem.p, cursor.p, st);
+    if (partition_out) {
+      if (points->memory == MASK_MEM_HOST)
+        MASK_CUDA(cudaMemcpyAsync(partition_out, leaf.p, sizeof(int64_t) * m, cudaMemcpyDeviceToHost, st));
+      else
+        MASK_CUDA(cudaMemcpyAsync(partition_out, leaf.p, sizeof(int64_t) * m, cudaMemcpyDeviceToDevice, st));
+    }
+    MASK_CUDA(cudaStreamSynchronize(st));
+    idx->own_X = std::move(X2);
+    idx->X = idx->own_X.p;
+    idx->n_global = n + m;
+    L1.labels = std::move(lab2);
+    L1.offsets = std::move(off);
+    L1.members = std::move(mem);
+    L1.n_items = n + m;
+    std::lock_guard<std::mutex> lock(idx->cover_mu);
+    idx->cover_valid = false;
   });
 }
 

@@ -127,7 +127,7 @@ constexpr int kWarpsPerBlock = 4;
 // Dense queries against a dense index.  Shared memory: one q vector (d floats) per warp.
 __global__ void __launch_bounds__(kWarpsPerBlock * 32)
     k_query_dense(QIndex qi, const float* __restrict__ Q, int64_t nq, int knn, int beam,
-                  int64_t* __restrict__ ids_out, float* __restrict__ d2_out) {
+                  int64_t* __restrict__ ids_out, float* __restrict__ d2_out, int leaf_only) {
   extern __shared__ __align__(16) float sq[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int d = qi.dim;
@@ -182,6 +182,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
         }
       }
     }
+    if (leaf_only) {  // insertion: the level-1 prototype the descent reaches
+      if (lane == 0) ids_out[qid] = top.id == PAD_ID ? -1 : (int64_t)top.id;
+      continue;
+    }
     // ---- data layer: rows of the reached partition(s)
     {
       const QLevel& L1 = qi.lv[0];
@@ -215,7 +219,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
 }
 
 void launch_query_dense(const QIndex& qi, const float* Q, int64_t nq, int knn, int beam,
-                        int64_t* ids, float* d2, cudaStream_t st) {
+                        int64_t* ids, float* d2, cudaStream_t st, bool leaf_only) {
   if (nq <= 0) return;
   const int dpad = (qi.dim + 3) & ~3;
   const size_t smem = (size_t)kWarpsPerBlock * dpad * sizeof(float);
@@ -224,7 +228,7 @@ void launch_query_dense(const QIndex& qi, const float* Q, int64_t nq, int knn, i
     MASK_CUDA(cudaFuncSetAttribute(k_query_dense, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int64_t blocks = (nq + kWarpsPerBlock - 1) / kWarpsPerBlock;
   const unsigned grid = (unsigned)(blocks < (int64_t)num_sms() * 16 ? blocks : (int64_t)num_sms() * 16);
-  k_query_dense<<<grid, kWarpsPerBlock * 32, smem, st>>>(qi, Q, nq, knn, beam, ids, d2);
+  k_query_dense<<<grid, kWarpsPerBlock * 32, smem, st>>>(qi, Q, nq, knn, beam, ids, d2, leaf_only ? 1 : 0);
   MASK_LAUNCH_CHECK();
 }
 

@@ -456,3 +456,28 @@ def test_cover_radii_bound_every_descendant():
         rows = np.nonzero(np.isin(lab1, np.nonzero(lab2 == j)[0]))[0]
         if rows.size:
             assert np.sqrt(((X[rows] - idx.levels[1].P[j]) ** 2).sum(axis=1)).max() <= cov[1][j] * (1 + 1e-12)
+
+
+# ------------------------------------------------------------------ insertion (NEXT-4)
+def test_insertion_closure_and_descent_matches_query_path():
+    # P:963-982 + SPEC insert [TRIVIAL]: insert then point query of the same vector -> found, and
+    # the insertion path is the beam-1 query path (its partition holds the k-NN answer)
+    X, idx = _small_index(seed=6)
+    rng = np.random.default_rng(7)
+    new = rng.standard_normal((30, 3)) * 2
+    labels = [lv.labels.copy() for lv in idx.levels]
+    leafs = [oracle.descend_leaf(idx.P, idx.offsets, idx.members, q)[0] for q in new]
+    X2 = np.concatenate([X, new])
+    lab1 = np.concatenate([labels[0], np.array(leafs, np.int32)])
+    off1, mem1 = oracle.children(lab1, idx.levels[0].P.shape[0])
+    offs = [off1] + idx.offsets[1:]
+    mems = [mem1] + idx.members[1:]
+    ids, d2, _ = oracle.query(idx.P, offs, mems, X2, new, 1, 1)
+    np.testing.assert_array_equal(ids[:, 0], np.arange(X.shape[0], X2.shape[0]))
+    assert np.all(d2[:, 0] == 0.0)
+    # the leaf reached is the partition a beam-1 k-NN query of a pre-existing row scans
+    for i in rng.choice(X.shape[0], 20, replace=False):
+        j, _ = oracle.descend_leaf(idx.P, idx.offsets, idx.members, X[i])
+        rows = idx.members[0][idx.offsets[0][j]:idx.offsets[0][j + 1]]
+        got, _, _ = oracle.query(idx.P, idx.offsets, idx.members, X, X[i:i + 1], 1, 1)
+        assert got[0, 0] in rows
