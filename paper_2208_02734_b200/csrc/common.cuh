@@ -138,18 +138,11 @@ void launch_small_level(const float* Y, int64_t n, int d, int64_t k, float* P, i
 size_t group_lloyd_smem(int64_t n_items, int64_t g, int nc, int d);
 void launch_group_lloyd(const float* Y, int d, const int64_t* perm, int64_t n_items, int64_t g, int nc, int T,
                         float* P_out, int32_t* labels, cudaStream_t st);
-// K4: exact FP32 direct re-check of flagged rows against all k prototypes.
-void launch_fixup(const float* X, int d, const float* P, int64_t k, const int32_t* flag_rows,
-                  const int32_t* flag_count, int64_t max_flags, int32_t* labels, float* best,
-                  cudaStream_t st);
-// K4 (tiled, device-sized): the first min(*flag_count, cap) flagged rows; keys_ws = cap u64
+// K4: exact FP32 direct re-check of the flagged rows against all k prototypes, sized on the
+// device from the flagged count (no host round trip); keys_ws = cap u64.
 void launch_fixup_device(const float* X, int d, const float* P, int64_t k, const int32_t* flag_rows,
                          const int32_t* flag_count, int64_t cap, unsigned long long* keys_ws, int32_t* labels,
                          float* best, cudaStream_t st, const int* active = nullptr);
-// K4 (tiled): nf flagged rows (host-known count) against all prototypes; keys_ws = nf u64
-void launch_fixup_tiled(const float* X, int d, const float* P, int64_t k, const int32_t* flag_rows,
-                        int64_t nf, unsigned long long* keys_ws, int32_t* labels, float* best,
-                        cudaStream_t st);
 // prototype operands for K1: Pb = tf32_rn(-2c), Ps = tf32_rn(-2c - Pb), cn2 = ||c||^2; with
 // kc > d the augmented columns [d] = split(||c||^2), [d+1] = (1, 0), rest 0 (row stride kc)
 // flag_count (optional): reset to 0 (the list K1 appends near-tie rows to)

@@ -116,145 +116,8 @@ void launch_assign_simt(const float* X, int64_t n, int d, const float* P, int64_
 }
 
 // ====================================================================== K4 near-tie re-check
-// One warp per flagged row: lanes sweep the prototypes (j = lane, lane+32, ...) with the
-// direct FP32 form, then a warp (d^2, j) argmin.  Rewrites labels[row] and best[row].
-__global__ void __launch_bounds__(256) k_fixup(const float* __restrict__ X, int d,
-                                               const float* __restrict__ P, int64_t k,
-                                               const int32_t* __restrict__ flag_rows,
-                                               const int32_t* __restrict__ flag_count,
-                                               int64_t max_flags, int32_t* __restrict__ labels,
-                                               float* __restrict__ best) {
-  const int lane = threadIdx.x & 31;
-  const int64_t nf = min64(*flag_count, max_flags);
-  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t f = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); f < nf;
-       f += warps) {
-    const int64_t row = flag_rows[f];
-    const float* x = X + row * d;
-    float b = INFINITY;
-    int64_t a = INT64_MAX;
-    for (int64_t j = lane; j < k; j += 32) {
-      const float* c = P + j * d;
-      float s = 0.f;
-      for (int i = 0; i < d; ++i) {
-        float t = __ldg(x + i) - __ldg(c + i);
-        s = fmaf(t, t, s);
-      }
-      if (s < b) {
-        b = s;
-        a = j;
-      }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      float ob = __shfl_xor_sync(0xffffffffu, b, o);
-      int64_t oa = __shfl_xor_sync(0xffffffffu, a, o);
-      if (ob < b || (ob == b && oa < a)) {
-        b = ob;
-        a = oa;
-      }
-    }
-    if (lane == 0) {
-      labels[row] = (int32_t)a;
-      best[row] = b;
-    }
-  }
-}
-
-void launch_fixup(const float* X, int d, const float* P, int64_t k, const int32_t* flag_rows,
-                  const int32_t* flag_count, int64_t max_flags, int32_t* labels, float* best,
-                  cudaStream_t st) {
-  k_fixup<<<num_sms() * 4, 256, 0, st>>>(X, d, P, k, flag_rows, flag_count, max_flags, labels,
-                                         best);
-  MASK_LAUNCH_CHECK();
-}
-
-// ---------------------------------------------------------------------- K4 (tiled)
-// Flagged rows x all prototypes, direct FP32 sums of squares, register-blocked like a small
-// SIMT GEMM: a block takes 32 flagged rows (smem) and sweeps its share of the prototypes in
-// tiles of 128 (smem); thread (rg, pg) accumulates 4 rows x 4 prototypes.  Per row the best
-// (d^2, j) of the block is merged into a 64-bit key (float bits << 32 | j) with atomicMin, so
-// the smallest distance wins and the lowest index breaks exact ties (D4); d^2 >= 0 keeps the
-// float bit order monotone.
 namespace {
 constexpr int FX_R = 32, FX_P = 128;
-}
-
-__global__ void __launch_bounds__(256) k_fixup_tiled(const float* __restrict__ X, int d,
-                                                     const float* __restrict__ P, int64_t k,
-                                                     const int32_t* __restrict__ flag_rows, int64_t nf,
-                                                     int64_t tiles_per_split,
-                                                     unsigned long long* __restrict__ keys) {
-  extern __shared__ float fsm[];
-  const int dp = d + 1;  // padded row stride (bank-conflict free)
-  float* xs = fsm;
-  float* cs = fsm + FX_R * dp;
-  const int t = threadIdx.x;
-  const int rg = t & 7, pg = t >> 3;  // 8 row groups x 32 prototype groups, 4 x 4 each
-  const int64_t f0 = (int64_t)blockIdx.x * FX_R;
-  for (int e = t; e < FX_R * d; e += 256) {
-    const int r = e / d, c = e - r * d;
-    xs[r * dp + c] = (f0 + r < nf) ? X[(int64_t)flag_rows[f0 + r] * d + c] : 0.f;
-  }
-  float bv[4];
-  int64_t bj[4];
-#pragma unroll
-  for (int a = 0; a < 4; ++a) {
-    bv[a] = INFINITY;
-    bj[a] = INT64_MAX;
-  }
-  const int64_t ntile = (k + FX_P - 1) / FX_P;
-  const int64_t t0 = (int64_t)blockIdx.y * tiles_per_split;
-  const int64_t t1 = min64(ntile, t0 + tiles_per_split);
-  for (int64_t tile = t0; tile < t1; ++tile) {
-    const int64_t j0 = tile * FX_P;
-    __syncthreads();
-    for (int e = t; e < FX_P * d; e += 256) {
-      const int p = e / d, c = e - p * d;
-      cs[p * dp + c] = (j0 + p < k) ? P[(j0 + p) * d + c] : 0.f;
-    }
-    __syncthreads();
-    float acc[4][4];
-#pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-      for (int b = 0; b < 4; ++b) acc[a][b] = 0.f;
-    for (int i = 0; i < d; ++i) {
-      float xv[4], cv[4];
-#pragma unroll
-      for (int a = 0; a < 4; ++a) xv[a] = xs[(rg * 4 + a) * dp + i];
-#pragma unroll
-      for (int b = 0; b < 4; ++b) cv[b] = cs[(pg * 4 + b) * dp + i];
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          const float df = xv[a] - cv[b];
-          acc[a][b] = fmaf(df, df, acc[a][b]);
-        }
-    }
-#pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      const int64_t j = j0 + pg * 4 + b;
-      if (j < k) {
-#pragma unroll
-        for (int a = 0; a < 4; ++a)
-          if (acc[a][b] < bv[a]) {  // j increases with (tile, b) for this thread: keeps lowest j
-            bv[a] = acc[a][b];
-            bj[a] = j;
-          }
-      }
-    }
-  }
-#pragma unroll
-  for (int a = 0; a < 4; ++a) {
-    const int64_t f = f0 + rg * 4 + a;
-    if (f < nf && bj[a] != INT64_MAX) {
-      const unsigned long long key =
-          ((unsigned long long)__float_as_uint(fmaxf(bv[a], 0.f)) << 32) | (unsigned long long)(uint32_t)bj[a];
-      atomicMin(keys + f, key);
-    }
-  }
 }
 
 // Blocked SIMT argmin (K4 re-check and the large-d assignment): rows = rows[0..count) (or the
@@ -544,41 +407,6 @@ void launch_assign_blocked(const float* X, int64_t n, int d, const float* P, int
                            int32_t* labels, float* best, cudaStream_t st, const int* active) {
   if (n <= 0) return;
   launch_blocked(X, d, P, k, nullptr, nullptr, n, keys_ws, labels, best, st, active);
-}
-
-__global__ void k_fixup_write(const int32_t* __restrict__ flag_rows, int64_t nf,
-                              const unsigned long long* __restrict__ keys, int32_t* __restrict__ labels,
-                              float* __restrict__ best) {
-  for (int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; f < nf; f += (int64_t)gridDim.x * blockDim.x) {
-    const unsigned long long key = keys[f];
-    const int32_t row = flag_rows[f];
-    labels[row] = (int32_t)(key & 0xffffffffu);
-    best[row] = __uint_as_float((uint32_t)(key >> 32));
-  }
-}
-
-void launch_fixup_tiled(const float* X, int d, const float* P, int64_t k, const int32_t* flag_rows,
-                        int64_t nf, unsigned long long* keys_ws, int32_t* labels, float* best,
-                        cudaStream_t st) {
-  if (nf <= 0) return;
-  MASK_CUDA(cudaMemsetAsync(keys_ws, 0xff, sizeof(unsigned long long) * nf, st));
-  const int64_t row_blocks = (nf + FX_R - 1) / FX_R;
-  const int64_t ntile = (k + FX_P - 1) / FX_P;
-  int64_t splits = (4LL * num_sms() + row_blocks - 1) / row_blocks;
-  if (splits > ntile) splits = ntile;
-  if (splits > 65535) splits = 65535;
-  if (splits < 1) splits = 1;
-  const int64_t tps = (ntile + splits - 1) / splits;
-  splits = (ntile + tps - 1) / tps;
-  const size_t smem = (size_t)(FX_R + FX_P) * (d + 1) * sizeof(float);
-  MASK_REQUIRE(smem <= 200 * 1024, MASK_ERR_UNSUPPORTED, "fix-up: dim too large");
-  if (smem > 48 * 1024)
-    MASK_CUDA(cudaFuncSetAttribute(k_fixup_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  dim3 grid((unsigned)row_blocks, (unsigned)splits);
-  k_fixup_tiled<<<grid, 256, smem, st>>>(X, d, P, k, flag_rows, nf, tps, keys_ws);
-  MASK_LAUNCH_CHECK();
-  k_fixup_write<<<grid_for(nf, 256), 256, 0, st>>>(flag_rows, nf, keys_ws, labels, best);
-  MASK_LAUNCH_CHECK();
 }
 
 // ====================================================================== operand prep
