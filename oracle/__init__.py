@@ -350,6 +350,85 @@ def descend_leaf(P: Sequence[np.ndarray], offsets: Sequence[np.ndarray], members
     return j, gap
 
 
+# ------------------------------------------------------------------ distributed mode (NEXT-3)
+def top_registry(index_P_top, offsets_top) -> np.ndarray:
+    """What a node registers with the coordinator (§3.4, "just the top level
+    centroids from each node need to be recorded"): its top-level prototypes, keeping those
+    with children (reading C2: a childless prototype represents no data)."""
+    P = _f64(index_P_top)
+    o = np.asarray(offsets_top, np.int64)
+    return P[o[1:] > o[:-1]]
+
+
+def route(tops: Sequence[np.ndarray], q, epsilon: float) -> Tuple[List[int], float]:
+    """§3.4: the nodes "that have centroids whose distance to the target query
+    object is lower than a given threshold epsilon" -- node n is routed iff some registered
+    top centroid c of n has ||q - c|| < epsilon (strict; reading C1), epsilon = inf routes to
+    every node ("searching in all nodes in parallel").  Returns (routed node ids ascending,
+    smallest relative gap |d_min^2 - epsilon^2| / epsilon^2 over the nodes, inf if none)."""
+    q = _f64(q)
+    nodes, gap = [], np.inf
+    for n, T in enumerate(tops):
+        if np.isinf(epsilon):
+            nodes.append(n)
+            continue
+        T = _f64(T)
+        if T.shape[0] == 0:
+            continue
+        dmin2 = ((T - q) ** 2).sum(axis=1).min()
+        e2 = float(epsilon) * float(epsilon)
+        if dmin2 < e2:
+            nodes.append(n)
+        if e2 > 0:
+            gap = min(gap, abs(dmin2 - e2) / e2)
+    return nodes, gap
+
+
+def merge(results: Sequence[Tuple[np.ndarray, np.ndarray]], routed: Sequence[int], knn: int):
+    """The coordinator's merge ("searching in all nodes in parallel"): the knn best
+    of the routed nodes' local answers by (d^2, node, id) (reading C3); ids are global;
+    padded with (-1, +inf).  ``results[n]`` = (ids, d2) of node n for this query."""
+    cand = []
+    for n in routed:
+        ids, d2 = results[n]
+        cand += [(float(d), n, int(i)) for i, d in zip(ids, d2) if i >= 0]
+    cand.sort()
+    cand = cand[:knn]
+    ids = np.full(knn, -1, np.int64)
+    d2 = np.full(knn, np.inf)
+    for r, (d, _, i) in enumerate(cand):
+        ids[r], d2[r] = i, d
+    return ids, d2
+
+
+def cluster_query(nodes: Sequence[dict], Q, knn: int, beam: int, epsilon: float):
+    """§3.4 distributed k-NN for a batch: route each query against the registry, run the
+    descent (``query``) on each routed node's own index, merge.  ``nodes[n]`` = dict(P, offsets,
+    members, X, id_base) of node n's independent index (node-local row ids; global id =
+    id_base + local id).  Returns ids, d2 (nq x knn), routed (nq x n_nodes bool), gap (per
+    query: the smallest relative gap of the routing decisions and of the descents)."""
+    Q = _f64(Q)
+    nq, W = Q.shape[0], len(nodes)
+    tops = [top_registry(nd["P"][-1], nd["offsets"][-1]) for nd in nodes]
+    routed = np.zeros((nq, W), bool)
+    rgap = np.full(nq, np.inf)
+    for i in range(nq):
+        rs, rgap[i] = route(tops, Q[i], epsilon)
+        routed[i, rs] = True
+    local = []
+    qgap = np.full(nq, np.inf)
+    for n, nd in enumerate(nodes):
+        ids, d2, g = query(nd["P"], nd["offsets"], nd["members"], nd["X"], Q, knn, beam)
+        ids = np.where(ids >= 0, ids + int(nd["id_base"]), -1)
+        local.append((ids, d2))
+        qgap = np.where(routed[:, n], np.minimum(qgap, g), qgap)
+    out_i = np.empty((nq, knn), np.int64)
+    out_d = np.empty((nq, knn))
+    for i in range(nq):
+        out_i[i], out_d[i] = merge([(l[0][i], l[1][i]) for l in local], np.nonzero(routed[i])[0], knn)
+    return out_i, out_d, routed, np.minimum(rgap, qgap)
+
+
 # ------------------------------------------------------------------ queries
 def _ptr_array(arrs, ctype):
     return (C.POINTER(ctype) * len(arrs))(*[a.ctypes.data_as(C.POINTER(ctype)) for a in arrs])

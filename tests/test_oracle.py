@@ -481,3 +481,97 @@ def test_insertion_closure_and_descent_matches_query_path():
         rows = idx.members[0][idx.offsets[0][j]:idx.offsets[0][j + 1]]
         got, _, _ = oracle.query(idx.P, idx.offsets, idx.members, X, X[i:i + 1], 1, 1)
         assert got[0, 0] in rows
+
+
+# ------------------------------------------------------------------ distributed mode (NEXT-3)
+def _node_indexes(X, W, levels=(12, 3), seed=41, T=6):
+    """W independent indexes over contiguous row ranges of X (global id = range start + local)."""
+    n = X.shape[0]
+    nodes = []
+    for r in range(W):
+        lo, hi = r * n // W, (r + 1) * n // W
+        Xl = X[lo:hi]
+        inits = [datagen.init_indices(seed + r, 1, hi - lo, levels[0]),
+                 datagen.init_indices(seed + r, 2, levels[0], levels[1])]
+        idx = oracle.build_index(Xl, inits, T)
+        nodes.append(dict(P=idx.P, offsets=idx.offsets, members=idx.members, X=Xl, id_base=lo))
+    return nodes
+
+
+def test_route_matches_library_distances_and_limits():
+    # §3.4 P:1032-1034: routed(q) = {n : min_c ||q - c|| < eps}; checked against scipy's cdist,
+    # eps = inf -> every node, eps = 0 -> no node (strict, reading C1), monotone in eps
+    rng = np.random.default_rng(7)
+    tops = [rng.standard_normal((m, 3)) * 4 for m in (5, 1, 9)]
+    tops.append(np.zeros((0, 3)))  # a node that registered nothing
+    Q = rng.standard_normal((60, 3)) * 4
+    R = np.concatenate(tops[:3])
+    owner = np.repeat(np.arange(3), [5, 1, 9])
+    D = cdist(Q, R)
+    for eps in (0.5, 2.0, 3.7, 8.0):
+        for i, q in enumerate(Q):
+            got, _ = oracle.route(tops, q, eps)
+            assert got == sorted(set(owner[D[i] < eps].tolist()))
+    for q in Q[:10]:
+        assert oracle.route(tops, q, np.inf)[0] == [0, 1, 2, 3]
+        assert oracle.route(tops, q, 0.0)[0] == []
+        prev = set()
+        for eps in np.linspace(0, 12, 25):
+            cur = set(oracle.route(tops, q, eps)[0])
+            assert prev <= cur
+            prev = cur
+    # strict: a query exactly on a centroid is not routed at eps = 0 but is at any eps > 0
+    assert oracle.route(tops, tops[1][0], 0.0)[0] == []
+    assert 1 in oracle.route(tops, tops[1][0], 1e-9)[0]
+
+
+def test_route_node_exclusive_region():
+    # SPEC route [DERIVED]: node n holds cloud n only (clouds 40 apart, sigma 1); a query near
+    # cloud n's centre with eps = half the centre spacing reaches exactly node n
+    X = datagen.gaussian_clouds(5, 150, radius=40.0, sigma=1.0, clouds=4).astype(np.float64)
+    nodes = _node_indexes(X, 4, levels=(10, 2))
+    tops = [oracle.top_registry(nd["P"][-1], nd["offsets"][-1]) for nd in nodes]
+    centres = 40.0 * np.stack([np.cos(np.arange(4) * np.pi / 2), np.sin(np.arange(4) * np.pi / 2)], 1)
+    spacing = 40.0 * np.sqrt(2.0)
+    rng = np.random.default_rng(3)
+    for n in range(4):
+        for _ in range(5):
+            q = centres[n] + rng.standard_normal(2) * 0.5
+            assert oracle.route(tops, q, spacing / 2)[0] == [n]
+
+
+def test_cluster_broadcast_with_wide_beam_is_exact_knn():
+    # eps = inf and beam >= every k_l: each node's descent scans all its rows, so the merged
+    # answer is the exact k-NN of the union with global ids (brute force, ties by (d^2, id))
+    X = datagen.blobs(21, 600, 3, 6).astype(np.float64)
+    Q = datagen.blobs(22, 30, 3, 6).astype(np.float64)
+    nodes = _node_indexes(X, 3)
+    ids, d2, routed, _ = oracle.cluster_query(nodes, Q, 7, beam=12, epsilon=np.inf)
+    assert routed.all()
+    eids, ed2, _ = oracle.knn_exact(X, Q, 7)
+    np.testing.assert_array_equal(ids, eids)
+    np.testing.assert_allclose(d2, ed2, rtol=1e-13)
+
+
+def test_cluster_single_node_and_tight_epsilon():
+    X = datagen.blobs(23, 500, 2, 5).astype(np.float64)
+    Q = datagen.blobs(24, 40, 2, 5).astype(np.float64)
+    # one node: the cluster answer is that node's own descent (no merge)
+    one = _node_indexes(X, 1)
+    ids, d2, _, _ = oracle.cluster_query(one, Q, 5, 1, np.inf)
+    ids0, d20, _ = oracle.query(one[0]["P"], one[0]["offsets"], one[0]["members"], X, Q, 5, 1)
+    np.testing.assert_array_equal(ids, ids0)
+    # a tight eps routes fewer nodes: results are drawn only from the routed nodes, queries
+    # with no routed node get the padding, and recall cannot exceed the broadcast's
+    nodes = _node_indexes(X, 4)
+    ids_all, _, _, _ = oracle.cluster_query(nodes, Q, 5, 1, np.inf)
+    ids_t, d2_t, routed, _ = oracle.cluster_query(nodes, Q, 5, 1, 0.6)
+    assert routed.sum() < routed.size
+    lo = np.array([nd["id_base"] for nd in nodes] + [X.shape[0]])
+    for i in range(len(Q)):
+        own = np.searchsorted(lo, ids_t[i][ids_t[i] >= 0], side="right") - 1
+        assert set(own.tolist()) <= set(np.nonzero(routed[i])[0].tolist())
+        if not routed[i].any():
+            assert (ids_t[i] == -1).all() and np.isinf(d2_t[i]).all()
+    eids, _, _ = oracle.knn_exact(X, Q, 5)
+    assert oracle.recall(ids_t, eids) <= oracle.recall(ids_all, eids)
