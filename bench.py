@@ -80,6 +80,13 @@ class ClockSampler:
             if len(parts) >= 9:
                 self.rows.append(parts)
 
+    def wait_rows(self, n, timeout):
+        """Block until ``n`` samples exist (nvidia-smi needs ~0.1-0.5 s to start): short timed
+        regions (C1: a few ms) are then bracketed by a sample right before and right after."""
+        t0 = time.time()
+        while self.proc and len(self.rows) < n and time.time() - t0 < timeout:
+            time.sleep(0.01)
+
     def stop(self):
         if self.proc:
             self.proc.terminate()
@@ -138,6 +145,44 @@ def ncu_traffic(workload, kernel):
     return rec["dram_bytes_per_launch"]
 
 
+def _csr_rows(trip, lo, hi):
+    rp, col, val = trip
+    return (rp[lo:hi + 1] - rp[lo], col[rp[lo]:rp[hi]], val[rp[lo]:rp[hi]])
+
+
+def _nbytes(a):
+    return sum(x.nbytes for x in a) if isinstance(a, tuple) else a.nbytes
+
+
+def _densify(trip, dim):
+    rp, col, val = trip
+    Y = np.zeros((rp.size - 1, dim))
+    for i in range(rp.size - 1):
+        Y[i, col[rp[i]:rp[i + 1]]] = val[rp[i]:rp[i + 1]]
+    return Y
+
+
+def _oracle_pass(cfg, X_all, rows, P):
+    """One FP64 oracle Lloyd pass (assignment + update) over the first ``rows`` rows of X_all."""
+    import oracle
+
+    if cfg.sparse:
+        Y = _csr_rows(X_all, 0, rows)
+        lab, _, _ = oracle.assign_csr(Y, cfg.dim, P)
+        S, cnt = oracle.cluster_sums_csr(Y, cfg.dim, lab, P.shape[0])
+        oracle.means_from_sums(S, cnt, P)
+        return
+    Y = X_all[:rows].astype(np.float64)
+    lab, _, _ = oracle.assign(Y, P)
+    oracle.means(Y, lab, P)
+
+
+def _init_protos(cfg, X_all, init):
+    if cfg.sparse:
+        return np.stack([_densify(_csr_rows(X_all, int(i), int(i) + 1), cfg.dim)[0] for i in init])
+    return X_all[init].astype(np.float64)
+
+
 def lloyd_distances(idx, n_levels):
     tot = 0
     per = []
@@ -158,26 +203,22 @@ def run_reference(args, rank, world):
 
     cfg = datagen.CONFIGS[args.config]
     k = cfg.levels[0]
-    P = datagen.data(cfg, 0, cfg.n)[datagen.init_indices(cfg.cid, 1, cfg.n, k)].astype(np.float64)
+    X_all = datagen.data(cfg) if cfg.sparse else datagen.data(cfg, 0, cfg.n)
+    P = _init_protos(cfg, X_all, datagen.init_indices(cfg.cid, 1, cfg.n, k))
     cores = oracle.num_threads()
     # rows per step: ~3 s of one oracle Lloyd pass (assignment + update) on the box's cores
-    probe = datagen.data(cfg, 0, 4096).astype(np.float64)
-    t0 = time.perf_counter()
-    oracle.assign(probe, P)
-    rate = 4096 * k / max(time.perf_counter() - t0, 1e-6)
-    rows = int(min(cfg.n, max(4096, 3.0 * rate / k)))
-    Y = datagen.data(cfg, 0, rows).astype(np.float64)
-    t0 = time.perf_counter()
-    lab, _, _ = oracle.assign(Y, P)
-    dt = time.perf_counter() - t0
-    if dt < 2.0 and rows < cfg.n:  # the small probe under-estimates the rate
+    rows = min(cfg.n, 4096)
+    for _ in range(4):
+        t0 = time.perf_counter()
+        _oracle_pass(cfg, X_all, rows, P)
+        dt = time.perf_counter() - t0
+        if dt >= 2.0 or rows >= cfg.n:
+            break
         rows = int(min(cfg.n, rows * 3.0 / max(dt, 1e-3)))
-        Y = datagen.data(cfg, 0, rows).astype(np.float64)
     times = []
     for s in range(args.warmup + args.steps):
         t0 = time.perf_counter()
-        lab, _, _ = oracle.assign(Y, P)
-        oracle.means(Y, lab, P)
+        _oracle_pass(cfg, X_all, rows, P)
         dt = time.perf_counter() - t0
         if s >= args.warmup:
             times.append(dt)
@@ -194,22 +235,16 @@ def run_reference(args, rank, world):
     }), flush=True)
 
 
-def cpu_baseline(cfg, P0):
-    """Oracle timed on the host cores on a bounded sample (~10-20 s): level-1 assignment rows."""
+def cpu_baseline(cfg, X_all, init):
+    """Oracle timed on the host cores on a bounded sample (~10 s): level-1 Lloyd passes."""
     import oracle
 
-    k = P0.shape[0]
-    Pd = P0.astype(np.float64)
-    probe = datagen.data(cfg, 0, 2048).astype(np.float64)
-    t0 = time.perf_counter()
-    oracle.assign(probe, Pd)
-    rate = 2048 * k / max(time.perf_counter() - t0, 1e-6)
-    rows = int(min(cfg.n, max(2048, 10.0 * rate / k)))
-    for _ in range(3):  # the small probe under-estimates the rate: re-size until the sample is ~10 s
-        Y = datagen.data(cfg, 0, rows).astype(np.float64)
+    Pd = _init_protos(cfg, X_all, init)
+    k = Pd.shape[0]
+    rows = min(cfg.n, 2048)
+    for _ in range(5):  # re-size until the sample is ~10 s (a small probe under-estimates the rate)
         t0 = time.perf_counter()
-        lab, _, _ = oracle.assign(Y, Pd)
-        oracle.means(Y, lab, Pd)
+        _oracle_pass(cfg, X_all, rows, Pd)
         dt = time.perf_counter() - t0
         if dt >= 7.0 or rows >= cfg.n:
             break
@@ -217,8 +252,7 @@ def cpu_baseline(cfg, P0):
     reps = 1
     while dt < 7.0:  # the whole level-1 pass is short: repeat it (the oracle as it stands, re-run)
         t0 = time.perf_counter()
-        lab, _, _ = oracle.assign(Y, Pd)
-        oracle.means(Y, lab, Pd)
+        _oracle_pass(cfg, X_all, rows, Pd)
         dt += time.perf_counter() - t0
         reps += 1
     return {"value": reps * rows * k / dt, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
@@ -269,9 +303,22 @@ def main():
         inits.append(datagen.init_indices(cfg.cid, l, prev, kk))
         prev = kk
     qlo, qhi = mk.query_range(cfg.n_queries * world, world, rank)
-    Q_host = datagen.queries(cfg, count=cfg.n_queries * world)[qlo:qhi]
-    X = torch.from_numpy(X_host).to(dev)
-    Q = torch.from_numpy(np.ascontiguousarray(Q_host)).to(dev)
+    Q_host = datagen.queries(cfg, count=cfg.n_queries * world)
+    if not cfg.sparse:
+        Q_host = Q_host[qlo:qhi]
+    csr = cfg.sparse
+    if csr:  # C4: CSR rows and CSR queries (row_ptr int64, col int32, val fp32)
+        def to_dev(trip):
+            rp, col, val = trip
+            return mk.Csr(torch.from_numpy(rp).to(dev), torch.from_numpy(col).to(dev), torch.from_numpy(val).to(dev),
+                          cfg.dim)
+
+        X = to_dev(X_host)
+        Q_host = _csr_rows(Q_host, qlo, qhi)
+        Q = to_dev(Q_host)
+    else:
+        X = torch.from_numpy(X_host).to(dev)
+        Q = torch.from_numpy(np.ascontiguousarray(Q_host)).to(dev)
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
     flags = mk.MASK_TIME_KERNELS | (mk.MASK_FORCE_SIMT if args.force_simt else 0)
     if world == 1:
@@ -296,6 +343,7 @@ def main():
     sampler = ClockSampler(local) if rank == 0 else None
     if sampler:
         sampler.start()
+        sampler.wait_rows(1, 5.0)
     launches0 = mk.kernel_launches()
     step_ms = []
     kt = {"assign": 0.0, "assign_n": 0, "update": 0.0, "update_n": 0}
@@ -330,6 +378,7 @@ def main():
             idx.free()
     launches = mk.kernel_launches() - launches0
     if sampler:
+        sampler.wait_rows(len(sampler.rows) + 1, 1.0)
         sampler.stop()
     total_ms = sum(step_ms)
     if world > 1:
@@ -347,8 +396,14 @@ def main():
     lvl1 = idx.level_info(1)
     n1, k1, d = n_local, lvl1["k"], cfg.dim
     assign_avg_ms = kt["assign"] / max(kt["assign_n"], 1)
-    use_tc = idx.timing(1)["assign_kernel"] == "K1-tcgen05-3xtf32"
-    if use_tc:
+    akern = idx.timing(1)["assign_kernel"]
+    use_tc = akern == "K1-tcgen05-3xtf32"
+    if akern == "K3-csr":
+        flops = 2.0 * X_host[0][-1] * k1  # one FMA per (non-zero, prototype): the sparse contraction
+        peak = 148 * 128 * 2 * pk["sm_max_mhz"] * 1e6 / 1e12
+        roof = {"bound": "alu", "kernel": "K3 CSR assignment (level 1)", "unit": "TFLOP/s",
+                "peak_basis": "FP32 FMA = 148 SMs x 128 lanes x 2 flop x sm_max_mhz (DESIGN.md K3)"}
+    elif use_tc:
         flops = 6.0 * n1 * k1 * d  # 3xTF32: three TF32 products per useful multiply-add
         peak = 0.5 * pk["bf16_tflops"]
         roof = {"bound": "tensor", "kernel": "K1 tcgen05 3xTF32 assignment (level 1)", "unit": "TFLOP/s",
@@ -363,8 +418,11 @@ def main():
                  "traffic": ncu_traffic(cfg.name, roof["kernel"]), "avg_launch_ms": assign_avg_ms,
                  "share_of_step": kt["assign"] / total_ms if total_ms else None})
     upd_avg = kt["update"] / max(kt["update_n"], 1)
-    upd_bytes = n1 * d * 4 + n1 * 4 + k1 * (d + 1) * 4
-    upd = {"kernel": "K5 update (sums+counts)", "avg_launch_ms": upd_avg,
+    if csr:  # K6: CSR rows + labels read, k x d sums + counts written
+        upd_bytes = int(X_host[0][-1]) * 8 + (n1 + 1) * 8 + n1 * 4 + k1 * (d + 1) * 4
+    else:
+        upd_bytes = n1 * d * 4 + n1 * 4 + k1 * (d + 1) * 4
+    upd = {"kernel": "K6 CSR update (sums+counts)" if csr else "K5 update (sums+counts)", "avg_launch_ms": upd_avg,
            "achieved_gbs": upd_bytes / (upd_avg / 1000.0) / 1e9 if upd_avg > 0 else None,
            "peak_gbs": pk["hbm_gbs"]}
     if upd["achieved_gbs"]:
@@ -377,7 +435,8 @@ def main():
             import oracle
 
             m = 200
-            eids, _, gap = oracle.knn_exact(X_host, Q_host[:m], cfg.knn)
+            Qs = _csr_rows(Q_host, 0, m) if csr else Q_host[:m]
+            eids, _, gap = oracle.knn_exact(X_host, Qs, cfg.knn, csr=csr)
             recall = oracle.recall(ids[:m].cpu().numpy(), eids)
         except Exception as e:  # the recall sample is a report, not the timed value
             recall = f"unavailable: {e}"
@@ -385,8 +444,12 @@ def main():
     # ---- e2e through the C-ABI with HOST buffers (H2D/D2H copies inside the call)
     e2e = None
     if not args.no_e2e and world == 1:
-        Xp = torch.from_numpy(X_host).pin_memory().numpy()
-        Qp = torch.from_numpy(np.ascontiguousarray(Q_host)).pin_memory().numpy()
+        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()  # noqa: E731
+        if csr:
+            Xp = mk.Csr(*[pin(a) for a in X_host], cfg.dim)
+            Qp = mk.Csr(*[pin(a) for a in Q_host], cfg.dim)
+        else:
+            Xp, Qp = pin(X_host), pin(Q_host)
         h_ms = []
         for s in range(2):
             flush.zero_()
@@ -399,14 +462,13 @@ def main():
             dh, _ = lloyd_distances(idx_h, len(cfg.levels))
             idx_h.free()
         e2e = {"value": dh / (min(h_ms) / 1000.0), "unit": UNIT, "ms_per_step": min(h_ms),
-               "h2d_bytes_per_step": int(X_host.nbytes + Q_host.nbytes),
+               "h2d_bytes_per_step": int(_nbytes(X_host) + _nbytes(Q_host)),
                "d2h_bytes_per_step": int(ids_h.nbytes + d2_h.nbytes)}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            P0 = X_host[inits[0]]
-            cpu = cpu_baseline(cfg, P0)
+            cpu = cpu_baseline(cfg, X_host, inits[0])
         except Exception as e:
             cpu = {"value": None, "unit": UNIT, "cores": None, "kind": "oracle", "sample": f"failed: {e}"}
 

@@ -223,6 +223,46 @@ int32_t mask_range_query(const mask_index* idx, const mask_matrix* queries, cons
  * (MASK_ERR_UNSUPPORTED otherwise); MASK_ERR_ARG on a dim mismatch. */
 int32_t mask_insert(mask_index* idx, const mask_matrix* points, int64_t* partition_out, void* stream);
 
+/* ---------------------------------------------------------------- distributed mode
+ * The paper's §3.4 "Indexing distributed datasets": every
+ * node (one GPU, one process) builds its own index over its own rows with comm = NULL (zero
+ * collectives: mask_collective_count() does not move); "just the top level centroids from
+ * each node need to be recorded" by the coordinator; a query is answered either
+ * by all nodes or only by the "nodes that have centroids whose distance to the target query
+ * object is lower than a given threshold epsilon"; the answers are merged.
+ *
+ * mask_top_prototypes: the index's top-level prototypes that have children (reading C2), in
+ * id order, into host_out (count x dim fp32, caller-allocated with room for k_L rows; may be
+ * NULL to query the count); *count_out = their number.
+ *
+ * mask_route: routed_out[q * n_nodes + n] = 1 iff some registry row c with node_of[c] = n has
+ * ||q - c||^2 < epsilon^2 (strict, reading C1; FP32), else 0; epsilon = +inf routes every
+ * query to every node; epsilon = 0 to none.  registry: device n_registry x dim fp32
+ * (row-major), node_of: device int32 in [0, n_nodes), queries: device (dense or CSR, dim =
+ * the registry's), routed_out: device uint8 nq x n_nodes.  MASK_ERR_ARG on n_nodes < 1,
+ * epsilon < 0 or NULL pointers; MASK_ERR_UNSUPPORTED for host queries.
+ *
+ * mask_query_routed: mask_query (device queries and outputs only) answering query q only if
+ * routed[q * routed_stride] != 0 -- the rest get (-1, +inf) padding -- and reporting global
+ * ids id_base + local row id.  A node passes routed_out + its node number and stride n_nodes.
+ *
+ * mask_merge: the coordinator's merge: ids / d2 hold n_nodes blocks of nq x k_nn answers
+ * (node-major; each row sorted by (d^2, id), padded with (-1, +inf)); writes the k_nn best per
+ * query by (d^2, node, id) (reading C3) to ids_out / d2_out (nq x k_nn), padded with (-1, +inf).
+ * All device buffers.  MASK_ERR_ARG on n_nodes outside [1, 64] or k_nn outside [1, 32].
+ *
+ * mask_collective_count: the number of NCCL calls the library has issued in this process (the
+ * zero-communication counter of the independent per-node build). */
+int32_t mask_top_prototypes(const mask_index* idx, float* host_out, int64_t* count_out);
+int32_t mask_route(const float* registry, const int32_t* node_of, int64_t n_registry, int32_t n_nodes,
+                   const mask_matrix* queries, double epsilon, uint8_t* routed_out, void* stream);
+int32_t mask_query_routed(const mask_index* idx, const mask_matrix* queries, const uint8_t* routed,
+                          int64_t routed_stride, int64_t id_base, int32_t k_nn, int32_t beam, int64_t* ids_out,
+                          float* d2_out, void* stream);
+int32_t mask_merge(const int64_t* ids, const float* d2, int32_t n_nodes, int64_t nq, int32_t k_nn, int64_t* ids_out,
+                   float* d2_out, void* stream);
+int64_t mask_collective_count(void);
+
 void mask_free(mask_index* idx); /* NULL-safe */
 
 /* ---------------------------------------------------------------- step entry points

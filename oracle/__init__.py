@@ -401,24 +401,31 @@ def merge(results: Sequence[Tuple[np.ndarray, np.ndarray]], routed: Sequence[int
     return ids, d2
 
 
-def cluster_query(nodes: Sequence[dict], Q, knn: int, beam: int, epsilon: float):
+def cluster_query(nodes: Sequence[dict], Q, knn: int, beam: int, epsilon: float, csr_dim: Optional[int] = None):
     """§3.4 distributed k-NN for a batch: route each query against the registry, run the
     descent (``query``) on each routed node's own index, merge.  ``nodes[n]`` = dict(P, offsets,
     members, X, id_base) of node n's independent index (node-local row ids; global id =
     id_base + local id).  Returns ids, d2 (nq x knn), routed (nq x n_nodes bool), gap (per
     query: the smallest relative gap of the routing decisions and of the descents)."""
-    Q = _f64(Q)
-    nq, W = Q.shape[0], len(nodes)
+    if csr_dim is not None:  # CSR data and queries: route on the densified query vectors
+        rp, col, val = _csr(Q)
+        Qv = np.zeros((rp.size - 1, csr_dim))
+        for i in range(rp.size - 1):
+            Qv[i, col[rp[i]:rp[i + 1]]] = val[rp[i]:rp[i + 1]]
+    else:
+        Q = Qv = _f64(Q)
+    nq, W = Qv.shape[0], len(nodes)
     tops = [top_registry(nd["P"][-1], nd["offsets"][-1]) for nd in nodes]
     routed = np.zeros((nq, W), bool)
     rgap = np.full(nq, np.inf)
     for i in range(nq):
-        rs, rgap[i] = route(tops, Q[i], epsilon)
+        rs, rgap[i] = route(tops, Qv[i], epsilon)
         routed[i, rs] = True
     local = []
     qgap = np.full(nq, np.inf)
     for n, nd in enumerate(nodes):
-        ids, d2, g = query(nd["P"], nd["offsets"], nd["members"], nd["X"], Q, knn, beam)
+        ids, d2, g = query(nd["P"], nd["offsets"], nd["members"], nd["X"], Q, knn, beam, dim=csr_dim,
+                           x_csr=csr_dim is not None, q_csr=csr_dim is not None)
         ids = np.where(ids >= 0, ids + int(nd["id_base"]), -1)
         local.append((ids, d2))
         qgap = np.where(routed[:, n], np.minimum(qgap, g), qgap)

@@ -6,8 +6,8 @@ compute lives in ``libmask.so`` (hand-written sm_100a CUDA behind the C-ABI of
 sharding helpers.  Importing it does not require a GPU; calling it does (no CPU fallback).
 """
 from . import _lib
-from .api import (Comm, Csr, Index, assign, build, build_grouped, device_ok, grouped_depth, kernel_launches, matrix,
-                  update)
+from .api import (Comm, Csr, Index, assign, build, build_grouped, collective_count, device_ok, grouped_depth,
+                  kernel_launches, matrix, merge, route, update)
 from ._lib import (
     MASK_BORROW_DATA,
     MASK_FORCE_SIMT,
@@ -21,7 +21,8 @@ from ._lib import (
 from .shard import query_range, row_range
 
 __all__ = [
-    "Comm", "Csr", "Index", "assign", "build", "build_grouped", "grouped_depth", "device_ok", "kernel_launches", "matrix", "update", "row_range",
+    "Comm", "Csr", "Index", "assign", "build", "build_grouped", "grouped_depth", "device_ok", "kernel_launches", "matrix",
+    "update", "route", "merge", "collective_count", "row_range",
     "query_range", "MaskError", "MASK_BORROW_DATA", "MASK_FORCE_SIMT", "MASK_NO_FIXUP",
     "MASK_VALIDATE_FINITE", "MASK_TIME_KERNELS", "MASK_NO_SORT", "MASK_NO_FUSED",
 ]

@@ -43,6 +43,7 @@ EXPORTS = [
     "mask_num_levels", "mask_level_info", "mask_get_prototypes", "mask_get_labels",
     "mask_get_children", "mask_get_trace", "mask_kernel_launches", "mask_get_timing",
     "mask_grouped_depth", "mask_build_grouped", "mask_range_query", "mask_insert",
+    "mask_top_prototypes", "mask_route", "mask_query_routed", "mask_merge", "mask_collective_count",
 ]
 
 
@@ -139,6 +140,11 @@ def load():
             "mask_build_grouped": (i32, [C.POINTER(MaskMatrix), C.POINTER(MaskGroupedParams), P, C.POINTER(P)]),
             "mask_range_query": (i32, [P, C.POINTER(MaskMatrix), P, i32, i64, P, P, P, C.POINTER(i64), P]),
             "mask_insert": (i32, [P, C.POINTER(MaskMatrix), P, P]),
+            "mask_top_prototypes": (i32, [P, P, C.POINTER(i64)]),
+            "mask_route": (i32, [P, P, i64, i32, C.POINTER(MaskMatrix), C.c_double, P, P]),
+            "mask_query_routed": (i32, [P, C.POINTER(MaskMatrix), P, i64, i64, i32, i32, P, P, P]),
+            "mask_merge": (i32, [P, P, i32, i64, i32, P, P, P]),
+            "mask_collective_count": (i64, []),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)

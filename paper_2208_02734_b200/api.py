@@ -219,6 +219,28 @@ class Index:
         del keep
         return part
 
+    def query_routed(self, queries, routed, node: int, id_base: int, knn: int = 10, beam: int = 1, stream=None):
+        """mask_query_routed (§3.4): answer only the queries with routed[q, node] != 0 (the rest
+        are padded), reporting global ids id_base + local id.  Device tensors only."""
+        m, keep = matrix(queries)
+        nq = m.rows
+        dev = keep[0].device
+        ids = torch.empty((nq, knn), dtype=torch.int64, device=dev)
+        d2 = torch.empty((nq, knn), dtype=torch.float32, device=dev)
+        W = int(routed.shape[1]) if nq else 1
+        check(load().mask_query_routed(self.handle, C.byref(m), _ptr(routed) + int(node), W, int(id_base), knn, beam,
+                                       _ptr(ids), _ptr(d2), _stream(stream)))
+        del keep
+        return ids, d2
+
+    def top_prototypes(self) -> np.ndarray:
+        """mask_top_prototypes: the top-level prototypes with children (what a node registers)."""
+        cnt = C.c_int64(0)
+        check(load().mask_top_prototypes(self.handle, None, C.byref(cnt)))
+        out = np.empty((max(cnt.value, 1), self.dim), np.float32)
+        check(load().mask_top_prototypes(self.handle, out.ctypes.data, C.byref(cnt)))
+        return out[:cnt.value]
+
     # ---------------------------------------------------------------- introspection
     @property
     def num_levels(self) -> int:
@@ -373,6 +395,36 @@ def update(data, labels, P_in, stream=None):
                              _ptr(counts), C.byref(md), _stream(stream)))
     del keep
     return P_out, counts, float(md.value)
+
+
+def route(registry, node_of, n_nodes: int, queries, epsilon: float, stream=None):
+    """mask_route (§3.4): uint8 (nq x n_nodes) device tensor, 1 where some registered centroid
+    of the node is closer than epsilon (strict); epsilon = inf routes everywhere."""
+    registry = _prep(registry, np.float32)
+    node_of = _prep(node_of, np.int32)
+    m, keep = matrix(queries)
+    routed = torch.empty((m.rows, int(n_nodes)), dtype=torch.uint8, device=registry.device)
+    check(load().mask_route(_ptr(registry), _ptr(node_of), int(registry.shape[0]), int(n_nodes), C.byref(m),
+                            float(epsilon), _ptr(routed), _stream(stream)))
+    del keep
+    return routed
+
+
+def merge(ids, d2, stream=None):
+    """mask_merge (§3.4): ids / d2 of shape (n_nodes, nq, k) -> the k best per query by
+    (d^2, node, id), shapes (nq, k)."""
+    ids = _prep(ids, np.int64)
+    d2 = _prep(d2, np.float32)
+    W, nq, k = ids.shape
+    oi = torch.empty((nq, k), dtype=torch.int64, device=ids.device)
+    od = torch.empty((nq, k), dtype=torch.float32, device=ids.device)
+    check(load().mask_merge(_ptr(ids), _ptr(d2), int(W), int(nq), int(k), _ptr(oi), _ptr(od), _stream(stream)))
+    return oi, od
+
+
+def collective_count() -> int:
+    """NCCL calls libmask has issued in this process (the §3.4 zero-communication counter)."""
+    return int(load().mask_collective_count())
 
 
 def device_ok() -> bool:

@@ -102,9 +102,10 @@ __global__ void __launch_bounds__(kRowsPerBlock * 32)
 // chunk's slice of PT (d x 256 floats: 10 MB at C4) stays L2-resident instead of every row
 // streaming all of PT from HBM.  The HOT most frequent columns (Zipf-distributed features,
 // SURVEY §8(d) G4) have their chunk rows staged in shared memory once per CTA and chunk, so
-// most non-zeros read shared memory; the rest read L2.  Lane l covers prototypes
-// j0 + 8l .. 8l+7 (two 16-byte loads per non-zero).  A row's running argmin across chunks lives
+// most non-zeros read shared memory; the rest read L2 (two 16-byte loads per lane and
+// non-zero).  A row's running argmin across chunks lives
 // in `state` (global, L2); the last chunk writes the label and d^2 = s + ||x||^2.
+// (Lane l covers prototypes j0 + 128 i + 4 l + (0..3): conflict-free 16-byte loads.)
 constexpr int kPL = 8;          // prototypes per lane (8 FMAs per non-zero per warp visit)
 constexpr int kChunk = 32 * kPL;  // prototypes per chunk
 constexpr int kHot = 128;       // columns staged per chunk (kHot x kChunk floats = 128 KB)
@@ -112,11 +113,16 @@ constexpr int kG = 4;           // non-zeros in flight per warp step (kG x kPL f
 constexpr int kCsrWarps = 24;   // warps per CTA (85 registers each; measured best of 16/24/32 warps,
                                 // 8/16 prototypes per lane, 64/128 hot columns)
 
-// acc[u] += v * (kPL consecutive floats at p, 16-byte aligned)
+// Lane l covers the chunk's prototypes 128 i + 4 l + (0..3), i < kPL / 4: each float4 load of
+// the warp reads 512 contiguous bytes (4 wavefronts; a 32-byte lane stride would need 8)
+__device__ __forceinline__ int pl_off(int u, int lane) { return (u >> 2) * 128 + 4 * lane + (u & 3); }
+
+// r[i] = the 4 floats at p + 128 i (p = chunk base + 4 lane, 16-byte aligned)
 template <bool SMEM>
 __device__ __forceinline__ void load_pl(const float* p, float4 (&r)[kPL / 4]) {
 #pragma unroll
-  for (int i = 0; i < kPL / 4; ++i) r[i] = SMEM ? reinterpret_cast<const float4*>(p)[i] : __ldg(reinterpret_cast<const float4*>(p) + i);
+  for (int i = 0; i < kPL / 4; ++i)
+    r[i] = SMEM ? *reinterpret_cast<const float4*>(p + 128 * i) : __ldg(reinterpret_cast<const float4*>(p + 128 * i));
 }
 __device__ __forceinline__ void fma_pl(float v, const float4 (&r)[kPL / 4], float (&acc)[kPL]) {
 #pragma unroll
@@ -164,11 +170,13 @@ __global__ void __launch_bounds__(kCsrWarps * 32, 1)
     }
     __syncthreads();
     // this lane's kPL prototypes of the chunk: ||c||^2 (+inf beyond k: never chosen)
-    const int64_t jl = j0 + kPL * lane;
     float cc[kPL];
 #pragma unroll
-    for (int u = 0; u < kPL; ++u) cc[u] = jl + u < k ? __ldg(cn2 + jl + u) : INFINITY;
-    const bool vec_ok = jl + kPL - 1 < k && kvec;
+    for (int u = 0; u < kPL; ++u) {
+      const int64_t j = j0 + pl_off(u, lane);
+      cc[u] = j < k ? __ldg(cn2 + j) : INFINITY;
+    }
+    const bool vec_ok = j0 + pl_off(kPL - 1, lane) < k && kvec;
     for (int64_t r = r0 + w; r < r1; r += kCsrWarps) {
       const int64_t p0 = rp[r], p1 = rp[r + 1];
       float acc[kPL];
@@ -197,13 +205,13 @@ __global__ void __launch_bounds__(kCsrWarps * 32, 1)
             if (tail) tail &= tail - 1;
             const int32_t cq = __shfl_sync(0xffffffffu, mc, q < 0 ? 0 : q);
             vq[i] = q < 0 ? 0.f : __shfl_sync(0xffffffffu, mv, q < 0 ? 0 : q);
-            const float* g = PT + (int64_t)cq * k + jl;
+            const float* g = PT + (int64_t)cq * k + j0;
             if (q >= 0 && vec_ok) {
-              load_pl<false>(g, rb[i]);
+              load_pl<false>(g + 4 * lane, rb[i]);
             } else {
               float t[kPL];
 #pragma unroll
-              for (int u = 0; u < kPL; ++u) t[u] = (q >= 0 && jl + u < k) ? __ldg(g + u) : 0.f;
+              for (int u = 0; u < kPL; ++u) t[u] = (q >= 0 && j0 + pl_off(u, lane) < k) ? __ldg(g + pl_off(u, lane)) : 0.f;
 #pragma unroll
               for (int u = 0; u < kPL / 4; ++u) rb[i][u] = make_float4(t[4 * u], t[4 * u + 1], t[4 * u + 2], t[4 * u + 3]);
             }
@@ -220,7 +228,7 @@ __global__ void __launch_bounds__(kCsrWarps * 32, 1)
             if (hot) hot &= hot - 1;
             const int sl = __shfl_sync(0xffffffffu, msl, q < 0 ? 0 : q);
             vq[i] = q < 0 ? 0.f : __shfl_sync(0xffffffffu, mv, q < 0 ? 0 : q);
-            load_pl<true>(hotPT + (q < 0 ? 0 : sl) * kChunk + kPL * lane, rb[i]);
+            load_pl<true>(hotPT + (q < 0 ? 0 : sl) * kChunk + 4 * lane, rb[i]);
           }
 #pragma unroll
           for (int i = 0; i < kG; ++i) fma_pl(vq[i], rb[i], acc);
@@ -234,7 +242,7 @@ __global__ void __launch_bounds__(kCsrWarps * 32, 1)
         const float sv = fmaf(-2.f, acc[u], cc[u]);
         if (sv < bv) {
           bv = sv;
-          bj = (int32_t)(jl + u);
+          bj = (int32_t)(j0 + pl_off(u, lane));
         }
       }
 #pragma unroll

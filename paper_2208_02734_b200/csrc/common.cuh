@@ -226,6 +226,11 @@ struct QIndex {
   const int64_t* xrp;       // CSR data
   const int32_t* xcol;
   const float* xval;
+  // §3.4 distributed mode (K14): when `routed` is set, query q is answered only if
+  // routed[q * rstride] != 0 (else padded); result ids are id_base + local row id
+  const uint8_t* routed = nullptr;
+  int64_t rstride = 0;
+  int64_t id_base = 0;
 };
 // K13 range search: cover radii (cover[l] = k_l float bits) and the multi-path descent; returns
 // the number of results, writing them (sorted by query, d^2, id) and per-query counts only when
@@ -241,5 +246,14 @@ void launch_query_csr(const QIndex& qi, const float* cn2_levels_flat, const int6
                       const int64_t* qrp, const int32_t* qcol, const float* qval, int64_t nq,
                       int knn, int beam, int64_t* ids, float* d2, cudaStream_t st);
 void launch_level_norms(const float* P, int64_t k, int d, float* cn2, cudaStream_t st, const int* active = nullptr);
+// K14 distributed mode (§3.4): routing of queries to nodes by the registered top-level
+// prototypes, and the (d^2, node, id) merge of the nodes' answers
+void launch_route_dense(const float* reg, const int32_t* node_of, int64_t R, int W, const float* Q, int64_t nq, int d,
+                        float eps2, bool all, uint8_t* routed, cudaStream_t st);
+void launch_route_csr(const float* reg, float* reg_n2 /* R floats of workspace */, const int32_t* node_of, int64_t R, int W, int d,
+                      const int64_t* qrp, const int32_t* qcol, const float* qval, int64_t nq, float eps2, bool all,
+                      uint8_t* routed, cudaStream_t st);
+void launch_merge(const int64_t* ids, const float* d2, int W, int64_t nq, int k, int64_t* ids_out, float* d2_out,
+                  cudaStream_t st);
 
 }  // namespace mask

@@ -8,6 +8,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -24,6 +25,7 @@ using namespace mask;
 
 namespace {
 std::atomic<int64_t> g_launches{0};
+std::atomic<int64_t> g_nccl_calls{0};  // every NCCL call the library issues (mask_collective_count)
 }
 
 void mask::count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
@@ -100,6 +102,7 @@ int32_t guarded(F&& f) {
 
 #define MASK_NCCL(x)                                                                     \
   do {                                                                                   \
+    g_nccl_calls.fetch_add(1, std::memory_order_relaxed);                               \
     ncclResult_t r_ = (x);                                                               \
     if (r_ != ncclSuccess)                                                               \
       ::mask::fail(MASK_ERR_NCCL, std::string(#x) + ": " + ncclGetErrorString(r_));      \
@@ -1172,8 +1175,10 @@ int32_t mask_insert(mask_index* idx, const mask_matrix* points, int64_t* partiti
   });
 }
 
-int32_t mask_query(const mask_index* idx, const mask_matrix* queries, int32_t k_nn, int32_t beam,
-                   int64_t* ids_out, float* d2_out, void* stream) {
+namespace {
+int32_t query_impl(const mask_index* idx, const mask_matrix* queries, int32_t k_nn, int32_t beam,
+                   int64_t* ids_out, float* d2_out, void* stream, const uint8_t* routed, int64_t rstride,
+                   int64_t id_base) {
   return guarded([&] {
     MASK_REQUIRE(idx != nullptr, MASK_ERR_ARG, "index is NULL");
     check_matrix(queries, "queries");
@@ -1233,6 +1238,9 @@ int32_t mask_query(const mask_index* idx, const mask_matrix* queries, int32_t k_
       ids = ids_d.p;
       d2 = d2_d.p;
     }
+    qi.routed = routed;
+    qi.rstride = rstride;
+    qi.id_base = id_base;
     if (idx->format == MASK_DENSE_F32)
       launch_query_dense(qi, Qv, nq, k_nn, beam, ids, d2, st);
     else
@@ -1244,6 +1252,84 @@ int32_t mask_query(const mask_index* idx, const mask_matrix* queries, int32_t k_
     MASK_CUDA(cudaStreamSynchronize(st));
   });
 }
+}  // namespace
+
+int32_t mask_query(const mask_index* idx, const mask_matrix* queries, int32_t k_nn, int32_t beam,
+                   int64_t* ids_out, float* d2_out, void* stream) {
+  return query_impl(idx, queries, k_nn, beam, ids_out, d2_out, stream, nullptr, 0, 0);
+}
+
+// ---------------------------------------------------------------- §3.4 distributed mode (K14)
+int32_t mask_query_routed(const mask_index* idx, const mask_matrix* queries, const uint8_t* routed,
+                          int64_t routed_stride, int64_t id_base, int32_t k_nn, int32_t beam, int64_t* ids_out,
+                          float* d2_out, void* stream) {
+  if (queries && queries->memory != MASK_MEM_DEVICE)
+    return guarded([&] { MASK_REQUIRE(false, MASK_ERR_UNSUPPORTED, "mask_query_routed takes device queries"); });
+  if (!routed || routed_stride < 1)
+    return guarded([&] { MASK_REQUIRE(false, MASK_ERR_ARG, "routed must be non-NULL with stride >= 1"); });
+  return query_impl(idx, queries, k_nn, beam, ids_out, d2_out, stream, routed, routed_stride, id_base);
+}
+
+int32_t mask_top_prototypes(const mask_index* idx, float* host_out, int64_t* count_out) {
+  return guarded([&] {
+    MASK_REQUIRE(idx != nullptr && count_out != nullptr, MASK_ERR_ARG, "NULL argument");
+    const auto& top = idx->levels.back();
+    const int64_t k = top.k, d = idx->dim;
+    std::vector<int64_t> off(k + 1);
+    std::vector<float> P((size_t)k * d);
+    MASK_CUDA(cudaMemcpy(off.data(), top.offsets.p, sizeof(int64_t) * (k + 1), cudaMemcpyDeviceToHost));
+    MASK_CUDA(cudaMemcpy(P.data(), top.P.p, sizeof(float) * k * d, cudaMemcpyDeviceToHost));
+    int64_t c = 0;
+    for (int64_t j = 0; j < k; ++j) {
+      if (off[j + 1] == off[j]) continue;  // childless: represents no data (reading C2)
+      if (host_out) std::memcpy(host_out + c * d, P.data() + j * d, sizeof(float) * d);
+      ++c;
+    }
+    *count_out = c;
+  });
+}
+
+int32_t mask_route(const float* registry, const int32_t* node_of, int64_t n_registry, int32_t n_nodes,
+                   const mask_matrix* queries, double epsilon, uint8_t* routed_out, void* stream) {
+  return guarded([&] {
+    check_matrix(queries, "queries");
+    MASK_REQUIRE(queries->memory == MASK_MEM_DEVICE, MASK_ERR_UNSUPPORTED, "mask_route takes device queries");
+    MASK_REQUIRE(n_nodes >= 1 && n_registry >= 0, MASK_ERR_ARG, "n_nodes must be >= 1, n_registry >= 0");
+    MASK_REQUIRE(n_registry == 0 || (registry != nullptr && node_of != nullptr), MASK_ERR_ARG, "NULL registry");
+    MASK_REQUIRE(epsilon >= 0.0, MASK_ERR_ARG, "epsilon must be >= 0");
+    cudaStream_t st = as_stream(stream);
+    const int64_t nq = queries->rows;
+    if (nq == 0) return;
+    MASK_REQUIRE(routed_out != nullptr, MASK_ERR_ARG, "NULL output");
+    const bool all = std::isinf(epsilon);
+    const float eps2 = all ? INFINITY : (float)(epsilon * epsilon);
+    if (queries->format == MASK_DENSE_F32) {
+      launch_route_dense(registry, node_of, n_registry, n_nodes, queries->values, nq, queries->dim, eps2, all,
+                         routed_out, st);
+    } else {
+      check_csr_structure(queries, st);
+      DevBuf<float> n2;
+      n2.alloc(std::max<int64_t>(n_registry, 1));
+      launch_route_csr(registry, n2.p, node_of, n_registry, n_nodes, queries->dim, queries->row_ptr,
+                       queries->col_idx, queries->values, nq, eps2, all, routed_out, st);
+      MASK_CUDA(cudaStreamSynchronize(st));
+    }
+    MASK_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+int32_t mask_merge(const int64_t* ids, const float* d2, int32_t n_nodes, int64_t nq, int32_t k_nn, int64_t* ids_out,
+                   float* d2_out, void* stream) {
+  return guarded([&] {
+    MASK_REQUIRE(k_nn >= 1 && k_nn <= 32 && nq >= 0, MASK_ERR_ARG, "k_nn must be in [1, 32], nq >= 0");
+    MASK_REQUIRE(nq == 0 || (ids && d2 && ids_out && d2_out), MASK_ERR_ARG, "NULL argument");
+    cudaStream_t st = as_stream(stream);
+    launch_merge(ids, d2, n_nodes, nq, k_nn, ids_out, d2_out, st);
+    MASK_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+int64_t mask_collective_count(void) { return g_nccl_calls.load(); }
 
 void mask_free(mask_index* idx) { delete idx; }
 

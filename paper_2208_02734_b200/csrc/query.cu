@@ -135,6 +135,13 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
   float* q = sq + w * dpad;
   const int64_t nwarps = (int64_t)gridDim.x * kWarpsPerBlock;
   for (int64_t qid = (int64_t)blockIdx.x * kWarpsPerBlock + w; qid < nq; qid += nwarps) {
+    if (qi.routed && !qi.routed[qid * qi.rstride]) {  // §3.4: not routed to this node
+      if (lane < knn) {
+        ids_out[qid * knn + lane] = -1;
+        if (d2_out) d2_out[qid * knn + lane] = INFINITY;
+      }
+      continue;
+    }
     __syncwarp();
     for (int i = lane; i < d; i += 32) q[i] = Q[qid * d + i];
     __syncwarp();
@@ -212,7 +219,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
     }
     if (lane < knn) {
       const bool pad = top.id == PAD_ID;
-      ids_out[qid * knn + lane] = pad ? -1 : (int64_t)top.id;
+      ids_out[qid * knn + lane] = pad ? -1 : qi.id_base + (int64_t)top.id;
       d2_out[qid * knn + lane] = pad ? INFINITY : top.d;
     }
   }
@@ -249,6 +256,13 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
   const int d = qi.dim;
   const int64_t nwarps = (int64_t)gridDim.x * kWarpsPerBlock;
   for (int64_t qid = (int64_t)blockIdx.x * kWarpsPerBlock + w; qid < nq; qid += nwarps) {
+    if (qi.routed && !qi.routed[qid * qi.rstride]) {  // §3.4: not routed to this node
+      if (lane < knn) {
+        ids_out[qid * knn + lane] = -1;
+        d2_out[qid * knn + lane] = INFINITY;
+      }
+      continue;
+    }
     const int64_t p0 = qrp[qid];
     const int qn = (int)min64(qrp[qid + 1] - p0, kMaxQueryNnz);
     __syncwarp();
@@ -349,7 +363,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
     }
     if (lane < knn) {
       const bool pad = top.id == PAD_ID;
-      ids_out[qid * knn + lane] = pad ? -1 : (int64_t)top.id;
+      ids_out[qid * knn + lane] = pad ? -1 : qi.id_base + (int64_t)top.id;
       d2_out[qid * knn + lane] = pad ? INFINITY : top.d;
     }
   }

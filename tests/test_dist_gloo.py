@@ -85,3 +85,61 @@ def test_data_parallel_lloyd_and_query_sharding_gloo(tmp_path):
     port = _free_port()
     mp.spawn(_worker, args=(2, port, str(tmp_path)), nprocs=2, join=True)
     assert (tmp_path / "ok").exists()
+
+
+def _cluster_worker(rank, world, port, out_dir):
+    """§3.4 distributed mode host plumbing: each rank is a node with its own index
+    (the oracle's, built from its rows only), the registry / query / answer exchanges of
+    paper_2208_02734_b200.cluster, and the merge, against the single-process oracle."""
+    from paper_2208_02734_b200.cluster import gather_queries, gather_registry, return_answers
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        X = datagen.gaussian_clouds(61, 120, radius=15.0, sigma=1.0).astype(np.float64)
+        X = X[datagen.group_perm(61, X.shape[0])]
+        n = X.shape[0]
+        bounds = [(r * n // world, (r + 1) * n // world) for r in range(world)]
+        levels = [(12, 3), (10, 5)]  # different top sizes per node: ragged registry
+        nodes = []
+        for r, (lo, hi) in enumerate(bounds):
+            k1, k2 = levels[r]
+            idx = oracle.build_index(X[lo:hi], [datagen.init_indices(62 + r, 1, hi - lo, k1),
+                                                datagen.init_indices(62 + r, 2, k1, k2)], 6)
+            nodes.append(dict(P=idx.P, offsets=idx.offsets, members=idx.members, X=X[lo:hi], id_base=lo))
+        me = nodes[rank]
+        top = oracle.top_registry(me["P"][-1], me["offsets"][-1]).astype(np.float32)
+        tops, bases = gather_registry(top, bounds[rank][1] - bounds[rank][0], 2)
+        assert bases == [lo for lo, _ in bounds]
+        for nd, tp in zip(nodes, tops):
+            np.testing.assert_array_equal(tp, oracle.top_registry(nd["P"][-1], nd["offsets"][-1]).astype(np.float32))
+        Q = datagen.gaussian_clouds(63, 5, radius=15.0, sigma=1.0).astype(np.float32)  # 40 queries
+        qlo, qhi = query_range(len(Q), world, rank)
+        Qall, counts = gather_queries(torch.from_numpy(Q[qlo:qhi]))
+        assert np.array_equal(Qall.numpy(), Q)
+        for eps in (np.inf, 4.0):
+            # this node answers the queries routed to it (the rest padded), global ids
+            ids, d2, _ = oracle.query(me["P"], me["offsets"], me["members"], me["X"], Qall.numpy(), 5, 1)
+            ids = np.where(ids >= 0, ids + me["id_base"], -1)
+            for i in range(len(Q)):
+                if rank not in oracle.route(tops, Qall.numpy()[i], eps)[0]:
+                    ids[i], d2[i] = -1, np.inf
+            ai, ad = return_answers(torch.from_numpy(ids), torch.from_numpy(d2), counts)
+            assert ai.shape == (world, qhi - qlo, 5)
+            got = [oracle.merge([(ai[n, i].numpy(), ad[n, i].numpy()) for n in range(world)], range(world), 5)
+                   for i in range(qhi - qlo)]
+            ref_i, ref_d, _, _ = oracle.cluster_query(nodes, Q, 5, 1, eps)
+            np.testing.assert_array_equal(np.stack([g[0] for g in got]), ref_i[qlo:qhi])
+            np.testing.assert_array_equal(np.stack([g[1] for g in got]), ref_d[qlo:qhi])
+        dist.barrier()
+        if rank == 0:
+            open(os.path.join(out_dir, "ok"), "w").write("ok")
+    finally:
+        dist.destroy_process_group()
+
+
+def test_distributed_mode_exchanges_gloo(tmp_path):
+    oracle.build()
+    port = _free_port()
+    mp.spawn(_cluster_worker, args=(2, port, str(tmp_path)), nprocs=2, join=True)
+    assert (tmp_path / "ok").exists()
