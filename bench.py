@@ -398,7 +398,13 @@ def main():
     assign_avg_ms = kt["assign"] / max(kt["assign_n"], 1)
     akern = idx.timing(1)["assign_kernel"]
     use_tc = akern == "K1-tcgen05-3xtf32"
-    if akern == "K3-csr":
+    if akern == "K11-fused-small-level":  # one launch runs the whole level: all its passes
+        flops = 3.0 * n1 * k1 * d * lvl1["passes"]
+        peak = 148 * 128 * 2 * pk["sm_max_mhz"] * 1e6 / 1e12
+        roof = {"bound": "alu", "kernel": "K11 fused small level (level 1, all passes in one launch)",
+                "unit": "TFLOP/s", "peak_basis": "FP32 SIMT = 148 SMs x 128 lanes x 2 flop x sm_max_mhz; "
+                "latency-bound (grid barriers between passes), DESIGN.md K11"}
+    elif akern == "K3-csr":
         flops = 2.0 * X_host[0][-1] * k1  # one FMA per (non-zero, prototype): the sparse contraction
         peak = 148 * 128 * 2 * pk["sm_max_mhz"] * 1e6 / 1e12
         roof = {"bound": "alu", "kernel": "K3 CSR assignment (level 1)", "unit": "TFLOP/s",

@@ -36,14 +36,23 @@ i64p = np.ctypeslib.ndpointer(dtype=np.int64, flags="C_CONTIGUOUS")
 i32p = np.ctypeslib.ndpointer(dtype=np.int32, flags="C_CONTIGUOUS")
 
 
+# MASK_ORACLE_SANITIZE=1: an ASan + UBSan build (run python with LD_PRELOAD=$(gcc
+# -print-file-name=libasan.so) ASAN_OPTIONS=detect_leaks=0; SURVEY §4 T4 for the host code)
+_SANITIZE = os.environ.get("MASK_ORACLE_SANITIZE") == "1"
+if _SANITIZE:
+    _LIB_PATH = os.path.join(_HERE, "_build", "liboracle_asan.so")
+
+
 def build(force: bool = False) -> str:
     """Compile mask_oracle.c -> oracle/_build/liboracle.so (gcc -O2 -fopenmp, IEEE FP)."""
     os.makedirs(os.path.dirname(_LIB_PATH), exist_ok=True)
     if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(_SRC):
         tmp = _LIB_PATH + f".tmp{os.getpid()}"
+        san = ["-fsanitize=address,undefined", "-fno-omit-frame-pointer", "-fno-sanitize-recover=all"] \
+            if _SANITIZE else []
         subprocess.check_call(
             ["gcc", "-O2", "-std=c11", "-fPIC", "-shared", "-fopenmp", "-fno-fast-math",
-             "-ffp-contract=off", "-o", tmp, _SRC, "-lm"]
+             "-ffp-contract=off", *san, "-o", tmp, _SRC, "-lm"]
         )
         os.replace(tmp, _LIB_PATH)
     return _LIB_PATH

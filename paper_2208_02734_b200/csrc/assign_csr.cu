@@ -113,6 +113,13 @@ constexpr int kG = 4;           // non-zeros in flight per warp step (kG x kPL f
 constexpr int kCsrWarps = 24;   // warps per CTA (85 registers each; measured best of 16/24/32 warps,
                                 // 8/16 prototypes per lane, 64/128 hot columns)
 
+// one staged non-zero: element offset of its P^T row (tail: col * k; hot: slot * kChunk), value
+struct __align__(16) NzEntry {
+  int64_t off;
+  float v;
+  float pad;
+};
+
 // Lane l covers the chunk's prototypes 128 i + 4 l + (0..3), i < kPL / 4: each float4 load of
 // the warp reads 512 contiguous bytes (4 wavefronts; a 32-byte lane stride would need 8)
 __device__ __forceinline__ int pl_off(int u, int lane) { return (u >> 2) * 128 + 4 * lane + (u & 3); }
@@ -143,8 +150,11 @@ __global__ void __launch_bounds__(kCsrWarps * 32, 1)
   if (active && !*active) return;  // level converged: this pass is skipped on the device
   extern __shared__ __align__(16) uint8_t smem_raw[];
   float* hotPT = reinterpret_cast<float*>(smem_raw);                                       // [kHot][kChunk]
-  int16_t* slot = reinterpret_cast<int16_t*>(smem_raw + kHot * kChunk * sizeof(float));  // [d]
+  NzEntry* lists = reinterpret_cast<NzEntry*>(smem_raw + kHot * kChunk * sizeof(float));  // [warps][2][32]
+  int16_t* slot = reinterpret_cast<int16_t*>(lists + kCsrWarps * 64);                      // [d]
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  NzEntry* lt_list = lists + w * 64;
+  NzEntry* hot_list = lt_list + 32;
   for (int c = threadIdx.x; c < d; c += blockDim.x) slot[c] = colslot[c];
   const int64_t r0 = n * blockIdx.x / gridDim.x, r1 = n * (blockIdx.x + 1) / gridDim.x;
   const int nch = (int)((k + kChunk - 1) / kChunk);
@@ -184,54 +194,64 @@ __global__ void __launch_bounds__(kCsrWarps * 32, 1)
       for (int u = 0; u < kPL; ++u) acc[u] = 0.f;
       for (int64_t pb = p0; pb < p1; pb += 32) {
         const int m = p1 - pb < 32 ? (int)(p1 - pb) : 32;
-        // each lane resolves one non-zero's hot slot in parallel; the warp then walks the tail
-        // (L2) non-zeros kG at a time with their loads issued before the FMAs, then the hot
-        // (shared-memory) ones
-        int32_t mc = 0, msl = -1;
+        // each lane resolves one non-zero's hot slot; the warp compacts the block into a tail
+        // (L2) list and a hot (shared-memory) list of {element offset, value}, padded to a
+        // multiple of kG with zero entries, then walks each list kG entries at a time: one
+        // broadcast 16-byte LDS per entry, both loads issued before the FMAs
+        int32_t msl = -1;
+        int64_t moff = 0;
         float mv = 0.f;
         if (lane < m) {
-          mc = __ldg(col + pb + lane);
+          const int32_t mc = __ldg(col + pb + lane);
           mv = __ldg(val + pb + lane);
           msl = slot[mc];
+          moff = msl >= 0 ? (int64_t)msl * kChunk : (int64_t)mc * k;
         }
-        unsigned tail = __ballot_sync(0xffffffffu, lane < m && msl < 0);
-        unsigned hot = __ballot_sync(0xffffffffu, lane < m && msl >= 0);
-        while (tail) {
+        const unsigned lt = (1u << lane) - 1u;
+        const unsigned tb = __ballot_sync(0xffffffffu, lane < m && msl < 0);
+        const unsigned hb = __ballot_sync(0xffffffffu, lane < m && msl >= 0);
+        const int nt = __popc(tb), nh = __popc(hb);
+        __syncwarp();  // the previous block's readers are done with the lists
+        if (lane < m) {
+          NzEntry* dst = msl < 0 ? lt_list + __popc(tb & lt) : hot_list + __popc(hb & lt);
+          *dst = NzEntry{moff, mv, 0.f};
+        }
+        const int ntp = (nt + kG - 1) / kG * kG, nhp = (nh + kG - 1) / kG * kG;
+        if (lane >= nt && lane < ntp) lt_list[lane] = NzEntry{0, 0.f, 0.f};
+        if (lane >= nh && lane < nhp) hot_list[lane] = NzEntry{0, 0.f, 0.f};
+        __syncwarp();
+        for (int i = 0; i < ntp; i += kG) {
           float vq[kG];
           float4 rb[kG][kPL / 4];
 #pragma unroll
-          for (int i = 0; i < kG; ++i) {
-            const int q = tail ? __ffs(tail) - 1 : -1;
-            if (tail) tail &= tail - 1;
-            const int32_t cq = __shfl_sync(0xffffffffu, mc, q < 0 ? 0 : q);
-            vq[i] = q < 0 ? 0.f : __shfl_sync(0xffffffffu, mv, q < 0 ? 0 : q);
-            const float* g = PT + (int64_t)cq * k + j0;
-            if (q >= 0 && vec_ok) {
-              load_pl<false>(g + 4 * lane, rb[i]);
+          for (int g = 0; g < kG; ++g) {
+            const NzEntry e = lt_list[i + g];
+            vq[g] = e.v;
+            const float* src = PT + e.off + j0;
+            if (vec_ok) {
+              load_pl<false>(src + 4 * lane, rb[g]);
             } else {
-              float t[kPL];
+              float tt[kPL];
 #pragma unroll
-              for (int u = 0; u < kPL; ++u) t[u] = (q >= 0 && j0 + pl_off(u, lane) < k) ? __ldg(g + pl_off(u, lane)) : 0.f;
+              for (int u = 0; u < kPL; ++u) tt[u] = j0 + pl_off(u, lane) < k ? __ldg(src + pl_off(u, lane)) : 0.f;
 #pragma unroll
-              for (int u = 0; u < kPL / 4; ++u) rb[i][u] = make_float4(t[4 * u], t[4 * u + 1], t[4 * u + 2], t[4 * u + 3]);
+              for (int u = 0; u < kPL / 4; ++u) rb[g][u] = make_float4(tt[4 * u], tt[4 * u + 1], tt[4 * u + 2], tt[4 * u + 3]);
             }
           }
 #pragma unroll
-          for (int i = 0; i < kG; ++i) fma_pl(vq[i], rb[i], acc);
+          for (int g = 0; g < kG; ++g) fma_pl(vq[g], rb[g], acc);
         }
-        while (hot) {
+        for (int i = 0; i < nhp; i += kG) {
           float vq[kG];
           float4 rb[kG][kPL / 4];
 #pragma unroll
-          for (int i = 0; i < kG; ++i) {
-            const int q = hot ? __ffs(hot) - 1 : -1;
-            if (hot) hot &= hot - 1;
-            const int sl = __shfl_sync(0xffffffffu, msl, q < 0 ? 0 : q);
-            vq[i] = q < 0 ? 0.f : __shfl_sync(0xffffffffu, mv, q < 0 ? 0 : q);
-            load_pl<true>(hotPT + (q < 0 ? 0 : sl) * kChunk + 4 * lane, rb[i]);
+          for (int g = 0; g < kG; ++g) {
+            const NzEntry e = hot_list[i + g];
+            vq[g] = e.v;
+            load_pl<true>(hotPT + e.off + 4 * lane, rb[g]);
           }
 #pragma unroll
-          for (int i = 0; i < kG; ++i) fma_pl(vq[i], rb[i], acc);
+          for (int g = 0; g < kG; ++g) fma_pl(vq[g], rb[g], acc);
         }
       }
       // lane argmin over its kPL (j increasing: strict < keeps the lowest j), then the warp's
@@ -280,7 +300,9 @@ __global__ void __launch_bounds__(kCsrWarps * 32, 1)
   }
 }
 
-size_t csr_chunked_smem(int d) { return (size_t)kHot * kChunk * sizeof(float) + (size_t)d * sizeof(int16_t); }
+size_t csr_chunked_smem(int d) {
+  return (size_t)kHot * kChunk * sizeof(float) + (size_t)kCsrWarps * 64 * sizeof(NzEntry) + (size_t)d * sizeof(int16_t);
+}
 
 int csr_chunked_hot() { return kHot; }
 

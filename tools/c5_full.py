@@ -33,6 +33,9 @@ def main():
     ap.add_argument("--T", type=int, default=1)
     ap.add_argument("--rows", type=int, default=4096)
     ap.add_argument("--clusters", type=int, default=256)
+    ap.add_argument("--clean", action="store_true",
+                    help="time one clean build (no step hook, no checks) and the 1e6-query batch")
+    ap.add_argument("--recall-sample", type=int, default=20)
     a = ap.parse_args()
     cfg = datagen.CONFIGS[5]
     t0 = time.time()
@@ -43,6 +46,12 @@ def main():
     Xd = torch.from_numpy(X).to("cuda:0")
     torch.cuda.synchronize()
     print(f"H2D {X.nbytes / 1e9:.1f} GB in {time.time() - t0:.1f} s", flush=True)
+    if a.clean:
+        clean(a, cfg, X, Xd, inits)
+        del Xd
+        shm.close()
+        shm.unlink()
+        return
     seen = {}
 
     def cb(level, p, P, labels):
@@ -102,6 +111,42 @@ def main():
     shm.close()
     shm.unlink()
     print("C5 full-size checks passed")
+
+
+def clean(a, cfg, X, Xd, inits):
+    """One production build (CUDA events around mask_build) + the batched query over 1e6 queries."""
+    st = torch.cuda.current_stream()
+    e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+    e0.record(st)
+    idx = mk.build(Xd, cfg.levels, a.T, inits, flags=mk.MASK_BORROW_DATA | mk.MASK_TIME_KERNELS, stream=st)
+    e1.record(st)
+    torch.cuda.synchronize()
+    build_s = e0.elapsed_time(e1) / 1e3
+    tot = 0
+    for lv in range(1, len(cfg.levels) + 1):
+        info = idx.level_info(lv)
+        tm = idx.timing(lv)
+        tot += info["passes"] * info["n_items"] * info["k"]
+        print(f"level {lv}: {info['passes']} passes ({tm['assign_kernel']}), assign {tm['assign']['ms'] / 1e3:.2f} s, "
+              f"fix-up {tm['fixup']['ms'] / 1e3:.2f} s, update {tm['update']['ms'] / 1e3:.3f} s", flush=True)
+    print(f"C5 build (T={a.T}): {build_s:.1f} s, {tot:.3e} distances, {tot / build_s:.3e} distances/s", flush=True)
+    Q = datagen.queries(cfg)
+    Qd = torch.from_numpy(Q).to("cuda:0")
+    ms = []
+    for _ in range(3):
+        e1.record(st)
+        ids, d2 = idx.query(Qd, knn=cfg.knn, beam=1, stream=st)
+        e2.record(st)
+        torch.cuda.synchronize()
+        ms.append(e1.elapsed_time(e2))
+    qms = min(ms)
+    m = a.recall_sample
+    t0 = time.time()
+    eids, _, _ = oracle.knn_exact(X, Q[:m], cfg.knn)
+    rec = oracle.recall(ids[:m].cpu().numpy(), eids)
+    print(f"query: {Q.shape[0]} queries in {qms:.1f} ms = {Q.shape[0] / qms * 1e3:.3e} QPS, recall@{cfg.knn} "
+          f"{rec:.3f} on {m} queries (exact k-NN on the host {time.time() - t0:.0f} s)", flush=True)
+    idx.free()
 
 
 if __name__ == "__main__":
