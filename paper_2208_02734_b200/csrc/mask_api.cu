@@ -703,9 +703,13 @@ void build_impl(const mask_matrix* data, const mask_build_params* p, mask_comm* 
   DevBuf<int64_t> loc_rp;
   DevBuf<int32_t> loc_col;
   const bool borrow = (p->flags & MASK_BORROW_DATA) && data->memory == MASK_MEM_DEVICE && !comm;
+  // world > 1 gathers every rank's rows into the index's own copy at the end of level 1, so the
+  // shard is read in place; a single GPU (with or without a one-rank communicator) keeps the
+  // data it was given, so it copies unless the caller lends it (MASK_BORROW_DATA)
+  const bool in_place = borrow || (comm && world > 1);
   if (data->format == MASK_DENSE_F32) {
     const size_t cnt = (size_t)data->rows * d;
-    if (data->memory == MASK_MEM_DEVICE && (borrow || comm)) {
+    if (data->memory == MASK_MEM_DEVICE && in_place) {
       in.X = data->values;
     } else {
       loc_X.alloc(std::max<size_t>(cnt, 1));
@@ -714,7 +718,7 @@ void build_impl(const mask_matrix* data, const mask_build_params* p, mask_comm* 
       in.X = loc_X.p;
     }
   } else {
-    if (data->memory == MASK_MEM_DEVICE && (borrow || comm)) {
+    if (data->memory == MASK_MEM_DEVICE && in_place) {
       in.rp = data->row_ptr;
       in.col = data->col_idx;
       in.val = data->values;
