@@ -175,6 +175,11 @@ void launch_col_hist(const int32_t* col, int64_t nnz, int d, int32_t* cnt, cudaS
 void launch_update_dense(const float* X, int64_t n, int d, const int32_t* labels, int64_t k,
                          float* S, int32_t* counts, cudaStream_t st, const int* active = nullptr,
                          const int32_t* perm = nullptr);
+// K6 over rows sorted by label (perm, end = per-label end offsets from launch_label_sort)
+bool csr_sorted_update_supported(int d);
+void launch_update_csr_sorted(const int64_t* row_ptr, const int32_t* col, const float* val, int d,
+                              const int32_t* perm, const int32_t* labels, const int32_t* end, int64_t n, int64_t k,
+                              float* S, int32_t* counts, cudaStream_t st, const int* active);
 void launch_update_csr(const int64_t* row_ptr, const int32_t* col, const float* val, int64_t n,
                        int d, const int32_t* labels, float* S, int32_t* counts, cudaStream_t st,
                        const int* active = nullptr);

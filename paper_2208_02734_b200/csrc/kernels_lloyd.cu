@@ -650,6 +650,111 @@ void launch_update_csr(const int64_t* row_ptr, const int32_t* col, const float* 
   MASK_LAUNCH_CHECK();
 }
 
+// K6 over label-sorted rows.  The sorted row order (perm) is cut into segments of kSegRows
+// positions; a CTA takes a segment and, for every cluster j present in it (rows perm[start ..
+// stop) with label j), accumulates those rows into a dense d-float shared-memory row with
+// shared atomics, then flushes it: a cluster wholly inside the segment is written to S_j with
+// plain coalesced stores (n_j = its row count), a cluster cut by a segment boundary adds its
+// non-zero entries with global atomics.  No k x d atomics sweep, S is written about once per
+// pass, and a huge cluster is spread over many CTAs.  S and the counts arrive zeroed
+// (previous finalize / level start).  end[j] = the label sort's scatter cursor = end offset of
+// label j in perm.
+constexpr int kSegRows = 256;
+
+__global__ void __launch_bounds__(256) k_update_csr_sorted(const int64_t* __restrict__ rp,
+                                                           const int32_t* __restrict__ col,
+                                                           const float* __restrict__ val, int d,
+                                                           const int32_t* __restrict__ perm,
+                                                           const int32_t* __restrict__ labels,
+                                                           const int32_t* __restrict__ end, int64_t n, int64_t k,
+                                                           float* __restrict__ S, int32_t* __restrict__ counts,
+                                                           const int* __restrict__ active) {
+  if (active && !*active) return;  // level converged: this pass is skipped on the device
+  extern __shared__ __align__(16) float acc[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const bool vec = (d & 3) == 0;
+  const int64_t nseg = (n + kSegRows - 1) / kSegRows;
+  for (int64_t sg = blockIdx.x; sg < nseg; sg += gridDim.x) {
+    const int32_t q0 = (int32_t)(sg * kSegRows), q1 = (int32_t)min64(n, (sg + 1) * kSegRows);
+    const int32_t j0 = labels[perm[q0]], j1 = labels[perm[q1 - 1]];
+    for (int32_t j = j0; j <= j1; ++j) {
+      const int32_t cs = j ? end[j - 1] : 0, ce = end[j];
+      const int32_t a = cs > q0 ? cs : q0, b = ce < q1 ? ce : q1;
+      if (b <= a) continue;  // empty cluster (uniform across the CTA)
+      for (int c = threadIdx.x; c < d; c += blockDim.x) acc[c] = 0.f;
+      __syncthreads();
+      // a warp takes 4 rows at a time and issues all their loads (2 non-zeros per lane and
+      // row) before the shared atomics: perm -> row_ptr -> (col, val) is a latency chain
+      constexpr int RW = 4;
+      for (int32_t qa = a + w * RW; qa < b; qa += nw * RW) {
+        int64_t r0 = 0, r1 = 0;
+        if (lane < RW && qa + lane < b) {
+          const int64_t r = perm[qa + lane];
+          r0 = rp[r];
+          r1 = rp[r + 1];
+        }
+        int32_t cq[RW][2];
+        float vq[RW][2];
+#pragma unroll
+        for (int u = 0; u < RW; ++u) {
+          const int64_t s0 = __shfl_sync(0xffffffffu, r0, u), s1 = __shfl_sync(0xffffffffu, r1, u);
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int64_t pp = s0 + h * 32 + lane;
+            cq[u][h] = pp < s1 ? __ldg(col + pp) : -1;
+            vq[u][h] = pp < s1 ? __ldg(val + pp) : 0.f;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < RW; ++u) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+            if (cq[u][h] >= 0) atomicAdd(acc + cq[u][h], vq[u][h]);
+          const int64_t s0 = __shfl_sync(0xffffffffu, r0, u), s1 = __shfl_sync(0xffffffffu, r1, u);
+          for (int64_t pp = s0 + 64 + lane; pp < s1; pp += 32) atomicAdd(acc + __ldg(col + pp), __ldg(val + pp));
+        }
+      }
+      __syncthreads();
+      float* Sj = S + (int64_t)j * d;
+      if (a == cs && b == ce) {  // the whole cluster: plain stores
+        if (vec) {
+          for (int c = threadIdx.x; c < d / 4; c += blockDim.x)
+            reinterpret_cast<float4*>(Sj)[c] = reinterpret_cast<const float4*>(acc)[c];
+        } else {
+          for (int c = threadIdx.x; c < d; c += blockDim.x) Sj[c] = acc[c];
+        }
+        if (threadIdx.x == 0) counts[j] = b - a;
+      } else {  // a piece of a cluster that other segments share
+        for (int c = threadIdx.x; c < d; c += blockDim.x) {
+          const float v = acc[c];
+          if (v != 0.f) atomicAdd(Sj + c, v);
+        }
+        if (threadIdx.x == 0) atomicAdd(counts + j, b - a);
+      }
+      __syncthreads();  // acc is reused by the next cluster
+    }
+  }
+}
+
+bool csr_sorted_update_supported(int d) { return (size_t)d * sizeof(float) <= 200 * 1024; }
+
+void launch_update_csr_sorted(const int64_t* row_ptr, const int32_t* col, const float* val, int d,
+                              const int32_t* perm, const int32_t* labels, const int32_t* end, int64_t n, int64_t k,
+                              float* S, int32_t* counts, cudaStream_t st, const int* active) {
+  if (k <= 0 || n <= 0) return;
+  const size_t smem = (size_t)d * sizeof(float);
+  static size_t attr_for = 0;
+  if (smem > 48 * 1024 && attr_for < smem) {
+    MASK_CUDA(cudaFuncSetAttribute(k_update_csr_sorted, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr_for = 200 * 1024;
+  }
+  const int per_sm = smem > 0 ? (int)std::max<size_t>(1, std::min<size_t>(8, (200 * 1024) / std::max<size_t>(smem, 1))) : 8;
+  const int64_t grid = std::min<int64_t>((n + kSegRows - 1) / kSegRows, (int64_t)num_sms() * per_sm);
+  k_update_csr_sorted<<<(unsigned)grid, 256, smem, st>>>(row_ptr, col, val, d, perm, labels, end, n, k, S, counts,
+                                                         active);
+  MASK_LAUNCH_CHECK();
+}
+
 // ====================================================================== K7 finalize
 // Warp per prototype.  stat[0] = max over j of ||c_new - c_old||^2 (float bits, atomicMax on
 // non-negative floats), stat[1] = number of empty prototypes.  S and counts are zeroed for

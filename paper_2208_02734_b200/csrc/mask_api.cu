@@ -505,7 +505,8 @@ void run_level(const Input& in, int64_t k, const int64_t* init_idx_host, const m
     }
     // ---- rows sorted by this pass's labels: run-accumulated update now, warp-coherent K1 rows
     // in the next pass (its previous labels are these)
-    const bool sorted = in.format == MASK_DENSE_F32 && !(p->flags & MASK_NO_SORT) && n >= 4096;
+    const bool sorted = !(p->flags & MASK_NO_SORT) && n >= 4096 &&
+                        (in.format == MASK_DENSE_F32 || csr_sorted_update_supported(d));
     // (the sort also performs the lab_prev <- lab_cur copy; a skipped pass leaves the buffers
     // swapped on the host, which only changes a row order: every consumer accepts any order)
     if (sorted) {
@@ -522,7 +523,10 @@ void run_level(const Input& in, int64_t k, const int64_t* init_idx_host, const m
     }
     // ---- update: S_j, n_j (K5/K6) -> allreduce (N1) -> P_j = S_j / n_j (K7)
     if (ev) ev->mark(MASK_T_UPDATE, st);
-    if (in.format == MASK_CSR_F32)
+    if (in.format == MASK_CSR_F32 && sorted)
+      launch_update_csr_sorted(in.rp, in.col, in.val, d, ws.perm.p, ws.lab_cur.p, ws.sort_cnt.p, n, k, ws.S.p,
+                               ws.counts.p, st, active);
+    else if (in.format == MASK_CSR_F32)
       launch_update_csr(in.rp, in.col, in.val, n, d, ws.lab_cur.p, ws.S.p, ws.counts.p, st, active);
     else
       launch_update_dense(in.X, n, d, ws.lab_cur.p, k, ws.S.p, ws.counts.p, st, active,
