@@ -47,9 +47,14 @@ struct SmallArgs {
   unsigned* bar;  // [0] arrivals, [1] generation (zeroed before the launch)
   int T;
   double tol;
+  int tpr;  // threads per row in the assignment phase (power of two <= 32)
 };
 
 __device__ __forceinline__ void grid_barrier(unsigned* bar) {
+  if (gridDim.x == 1) {  // one block: the block barrier orders its global-memory traffic
+    __syncthreads();
+    return;
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
     volatile unsigned* gen = bar + 1;
@@ -109,10 +114,10 @@ constexpr int kSmallSmemFloats = 11264;  // prototypes staged in shared memory u
 // (P changes inside the kernel, so no read-only-cache loads)
 template <int D, bool STAGED>
 __device__ __forceinline__ void row_argmin(const float (&x)[D], const float* C, int64_t k, int d, float& bv,
-                                           int32_t& bj) {
+                                           int32_t& bj, int j0 = 0, int jstep = 1) {
   bv = INFINITY;
-  bj = 0;
-  for (int64_t j = 0; j < k; ++j) {
+  bj = 0x7fffffff;
+  for (int64_t j = j0; j < k; j += jstep) {
     const float* cj = C + j * d;
     float acc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
@@ -141,18 +146,40 @@ __device__ void assign_all(const SmallArgs& a, int slot, float* sP) {
   __syncthreads();
   double s = 0.0;
   unsigned long long c = 0;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += stride) {
-    float x[D];
+  // a.tpr consecutive lanes per row (power of two <= 32): lane h of a row scans prototypes
+  // h, h + tpr, ... (lowest index on ties within its subset), then the lanes combine by
+  // (value, index) -- the same argmin with more threads on the prototypes
+  const int S = a.tpr;
+  const int lane = threadIdx.x & 31, h = lane & (S - 1);
+  const int64_t total = a.n * S;
+  const int64_t warp0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) - lane;
+  for (int64_t base = warp0; base < total; base += stride) {
+    const int64_t t = base + lane;
+    const bool valid = t < total;
+    const int64_t i = valid ? t / S : 0;
+    float bv = INFINITY;
+    int32_t bj = 0x7fffffff;
+    if (valid) {
+      float x[D];
 #pragma unroll
-    for (int e = 0; e < D; ++e) x[e] = e < a.d ? __ldg(a.Y + i * a.d + e) : 0.f;
-    float bv;
-    int32_t bj;
-    if (staged) row_argmin<D, true>(x, sP, a.k, a.d, bv, bj);
-    else row_argmin<D, false>(x, a.P, a.k, a.d, bv, bj);
-    a.lab[i] = bj;
-    a.best[i] = bv;
-    s += (double)bv;
-    c += (bj != __ldcg(a.prev + i)) ? 1ull : 0ull;
+      for (int e = 0; e < D; ++e) x[e] = e < a.d ? __ldg(a.Y + i * a.d + e) : 0.f;
+      if (staged) row_argmin<D, true>(x, sP, a.k, a.d, bv, bj, h, S);
+      else row_argmin<D, false>(x, a.P, a.k, a.d, bv, bj, h, S);
+    }
+    for (int o = 1; o < S; o <<= 1) {
+      const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int32_t oj = __shfl_xor_sync(0xffffffffu, bj, o);
+      if (ov < bv || (ov == bv && oj < bj)) {
+        bv = ov;
+        bj = oj;
+      }
+    }
+    if (valid && h == 0) {
+      a.lab[i] = bj;
+      a.best[i] = bv;
+      s += (double)bv;
+      c += (bj != __ldcg(a.prev + i)) ? 1ull : 0ull;
+    }
   }
   block_stats(s, c, a.J + slot, a.changed + slot);
 }
@@ -232,7 +259,7 @@ bool small_level_supported(int64_t n, int d, int64_t k) {
 void launch_small_level(const float* Y, int64_t n, int d, int64_t k, float* P, int32_t* lab, int32_t* prev,
                         float* best, double* S, int32_t* counts, double* J, unsigned long long* changed,
                         uint32_t* fin, int* ctrl, unsigned* bar_ws, int T, double tol, cudaStream_t st) {
-  SmallArgs a{Y, n, d, k, P, lab, prev, best, S, counts, J, changed, fin, ctrl, bar_ws, T, tol};
+  SmallArgs a{Y, n, d, k, P, lab, prev, best, S, counts, J, changed, fin, ctrl, bar_ws, T, tol, 1};
   MASK_CUDA(cudaMemsetAsync(bar_ws, 0, 2 * sizeof(unsigned), st));
   void* fn;
   if (d <= 4) fn = (void*)k_small_level<4>;
@@ -245,6 +272,15 @@ void launch_small_level(const float* Y, int64_t n, int d, int64_t k, float* P, i
   MASK_REQUIRE(per_sm >= 1, MASK_ERR_CUDA, "small-level kernel cannot be resident");
   // enough blocks for the rows (and the prototypes in the finalize phase), all co-resident
   int64_t want = (std::max<int64_t>(n, k * 32) + 255) / 256;
+  // a tiny level (C2 level 3: 256 items, 16 prototypes) runs in one block: block barriers
+  // instead of grid barriers, its work is a few hundred distances per thread
+  if (n <= 1024 && k <= 64) want = 1;
+  // spread each row's prototype scan over tpr lanes until ~16K threads work on the assignment
+  // (C2 level 2: 4,096 rows x 256 prototypes -> 4 lanes per row, 64 blocks)
+  if (want > 1) {
+    while (a.tpr < 32 && n * a.tpr * 2 <= 16384 && a.tpr * 2 <= k) a.tpr *= 2;
+    want = std::max<int64_t>(want, (n * a.tpr + 255) / 256);
+  }
   const int64_t cap = (int64_t)per_sm * num_sms();
   const int grid = (int)std::max<int64_t>(1, std::min(want, cap));
   void* args[] = {&a};

@@ -16,4 +16,6 @@ ncu --set full --clock-control none --import-source on -k regex:k_assign_tc -s 1
   -o $O/${R}_k1_c3 python tools/prof_build.py --cfg 3 --n 1000000 --iters 1 > $O/${R}_ncu_k1c3.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:k_assign_csr_chunked -s 1 -c 1 \
   -o $O/${R}_k3_c4 python tools/c4bench.py 1 > $O/${R}_ncu_k3.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:k_update_csr_sorted -s 1 -c 1 \
+  -o $O/${R}_k6_c4 python tools/c4bench.py 1 > $O/${R}_ncu_k6.log 2>&1
 ls -la $O/${R}_*
