@@ -11,6 +11,9 @@
 // k-means prototype = mean of members, levels P:631-638.
 #include <cuda_runtime.h>
 
+#include <map>
+#include <mutex>
+
 #include <cfloat>
 #include <cstdint>
 
@@ -269,7 +272,8 @@ __global__ void __launch_bounds__(256) k_rb_argmin(const float* __restrict__ X, 
   const bool vec = (d & 3) == 0 && ((uintptr_t)X & 15) == 0 && ((uintptr_t)P & 15) == 0;
   const int64_t row_blocks = (nf + RB_R - 1) / RB_R;
   const int64_t ntile = (k + RB_P - 1) / RB_P;
-  int64_t splits = (4LL * nsm + row_blocks - 1) / row_blocks;
+  // enough (row block, prototype range) items to fill every resident CTA (nsm = the grid)
+  int64_t splits = ((int64_t)nsm + row_blocks - 1) / row_blocks;
   splits = splits < 1 ? 1 : (splits > ntile ? ntile : splits);
   const int64_t tps = (ntile + splits - 1) / splits;
   splits = (ntile + tps - 1) / tps;
@@ -387,8 +391,23 @@ static void launch_blocked(const float* X, int d, const float* P, int64_t k, con
       MASK_CUDA(cudaFuncSetAttribute(k_rb_argmin, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
       attr_for = 200 * 1024;
     }
-    k_rb_argmin<<<num_sms() * 2, 256, rb_smem, st>>>(X, d, d4p, P, k, rows, count_dev, cap, num_sms(), keys_ws,
-                                                    active);
+    // one wave of resident CTAs (the flagged count is only known on the device: small counts
+    // split the prototypes finely so every CTA gets one short item)
+    static std::map<size_t, int> occ_cache;
+    int occ = 0;
+    {
+      static std::mutex mu;
+      std::lock_guard<std::mutex> lock(mu);
+      auto it = occ_cache.find(rb_smem);
+      if (it == occ_cache.end()) {
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_rb_argmin, 256, rb_smem) != cudaSuccess) occ = 2;
+        (void)cudaGetLastError();
+        it = occ_cache.emplace(rb_smem, std::max(1, std::min(occ, 8))).first;
+      }
+      occ = it->second;
+    }
+    const int grid = num_sms() * occ;
+    k_rb_argmin<<<grid, 256, rb_smem, st>>>(X, d, d4p, P, k, rows, count_dev, cap, grid, keys_ws, active);
   } else {
     k_blocked_argmin<<<num_sms() * 4, 256, 0, st>>>(X, d, P, k, rows, count_dev, cap, num_sms(), keys_ws, active);
   }
