@@ -83,3 +83,35 @@ def test_shard_ranges_partition_rows():
             assert spans[0][0] == 0 and spans[-1][1] == n
             for (a, b), (c, d) in zip(spans, spans[1:]):
                 assert b == c and a <= b
+
+
+def _build_c_example(tmp_path):
+    import shutil
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    pkg = os.path.join(root, "paper_2208_02734_b200")
+    if shutil.which("gcc") is None:
+        pytest.skip("no gcc")
+    exe = str(tmp_path / "abi_example")
+    subprocess.check_call(["gcc", "-std=c11", "-O1", "-I", os.path.join(root, "include"),
+                           os.path.join(root, "tests", "c", "abi_example.c"), "-L", pkg, "-lmask", "-lm",
+                           f"-Wl,-rpath,{pkg}", "-o", exe])
+    return exe
+
+
+def test_plain_c_caller_links_and_reports_no_gpu(tmp_path, lib):
+    # include/mask.h is usable from C alone; without a GPU every device call fails loudly
+    import subprocess
+    exe = _build_c_example(tmp_path)
+    if lib.mask_device_ok():
+        pytest.skip("GPU present: covered by test_plain_c_caller_on_gpu")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0 and "C_ABI_NO_GPU_OK" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.gpu
+def test_plain_c_caller_on_gpu(tmp_path, lib):
+    import subprocess
+    exe = _build_c_example(tmp_path)
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "C_ABI_OK" in r.stdout, r.stdout + r.stderr
