@@ -1,0 +1,7 @@
+import sys, torch
+sys.path.insert(0, "/root/repo")
+import datagen, paper_2208_02734_b200 as mk
+cfg = datagen.CONFIGS[2]
+X = torch.from_numpy(datagen.data(cfg)).cuda()
+idx = mk.build(X, cfg.levels, cfg.iters, datagen.all_init_indices(cfg), flags=mk.MASK_BORROW_DATA)
+print(idx.trace(1)["changed"].tolist())
