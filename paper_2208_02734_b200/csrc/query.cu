@@ -93,19 +93,44 @@ __device__ __forceinline__ float dist_dense(const float* __restrict__ q, const f
                                             int d) {
   float s = 0.f;
   if ((d & 3) == 0 && ((uintptr_t)x & 15) == 0) {
+    // the row's 16-byte loads are issued QB at a time before their arithmetic: the descent is
+    // bound by the latency of these gathers (one candidate row per lane)
+    constexpr int QB = 8;
     const float4* x4 = reinterpret_cast<const float4*>(x);
     const float4* q4 = reinterpret_cast<const float4*>(q);
-    for (int i = 0; i < (d >> 2); ++i) {
-      const float4 a = __ldg(x4 + i);
-      const float4 b = q4[i];
-      float t = b.x - a.x;
-      s = fmaf(t, t, s);
-      t = b.y - a.y;
-      s = fmaf(t, t, s);
-      t = b.z - a.z;
-      s = fmaf(t, t, s);
-      t = b.w - a.w;
-      s = fmaf(t, t, s);
+    const int d4 = d >> 2;
+    if (d4 <= 4) {  // short rows: the plain loop (its loads are already all in flight)
+      for (int i = 0; i < d4; ++i) {
+        const float4 a = __ldg(x4 + i);
+        const float4 b = q4[i];
+        float t = b.x - a.x;
+        s = fmaf(t, t, s);
+        t = b.y - a.y;
+        s = fmaf(t, t, s);
+        t = b.z - a.z;
+        s = fmaf(t, t, s);
+        t = b.w - a.w;
+        s = fmaf(t, t, s);
+      }
+      return s;
+    }
+    for (int i0 = 0; i0 < d4; i0 += QB) {
+      float4 a[QB];
+#pragma unroll
+      for (int u = 0; u < QB; ++u) a[u] = i0 + u < d4 ? __ldg(x4 + i0 + u) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int u = 0; u < QB; ++u) {
+        if (i0 + u >= d4) break;
+        const float4 b = q4[i0 + u];
+        float t = b.x - a[u].x;
+        s = fmaf(t, t, s);
+        t = b.y - a[u].y;
+        s = fmaf(t, t, s);
+        t = b.z - a[u].z;
+        s = fmaf(t, t, s);
+        t = b.w - a[u].w;
+        s = fmaf(t, t, s);
+      }
     }
   } else {
     for (int i = 0; i < d; ++i) {
