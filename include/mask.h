@@ -109,9 +109,11 @@ typedef struct {
   const int64_t* k;               /* host, k[0..L-1] bottom first; 1 <= k[l] <= n_l where
                                      n_0 = n_global, n_l = k[l-1]                          */
   double tol;                     /* >= 0; > 0 also stops when max_j |c_j'-c_j| <= tol     */
-  uint64_t seed;                  /* reserved (init indices are passed explicitly)         */
-  const int64_t* const* init_idx; /* host; init_idx[l] = k[l] distinct indices into the
-                                     level-l input (global row ids for level 1) (D2)       */
+  uint64_t seed;                  /* init sampling seed, used for every level whose
+                                     init_idx (or init_idx[l]) is NULL (mask_seeded_init)  */
+  const int64_t* const* init_idx; /* host, optional; init_idx[l] = k[l] distinct indices
+                                     into the level-l input (global row ids for level 1)
+                                     (D2); NULL -> drawn from `seed`                       */
   int32_t empty_policy;           /* MASK_EMPTY_KEEP                                       */
   int32_t flags;                  /* MASK_* flags above                                    */
   mask_iter_cb iter_cb;           /* NULL in production                                    */
@@ -262,6 +264,17 @@ int32_t mask_query_routed(const mask_index* idx, const mask_matrix* queries, con
 int32_t mask_merge(const int64_t* ids, const float* d2, int32_t n_nodes, int64_t nq, int32_t k_nn, int64_t* ids_out,
                    float* d2_out, void* stream);
 int64_t mask_collective_count(void);
+
+/* ---------------------------------------------------------------- seeded initialisation
+ * The init indices mask_build draws when init_idx is NULL (D2: k distinct indices, uniform
+ * without replacement): Floyd's algorithm -- for j = n-k .. n-1: t = u(j+1); take t unless
+ * already taken, else j -- with u(m) = next() mod m and next() the SplitMix64 sequence
+ * state += 0x9E3779B97F4A7C15; z = state; z = (z ^ z>>30) * 0xBF58476D1CE4E5B9;
+ * z = (z ^ z>>27) * 0x94D049BB133111EB; return z ^ z>>31, started from state = seed + level *
+ * 0x9E3779B97F4A7C15 (level 1 = the data level).  out[0..k) = the indices in the order they
+ * are taken (prototype j starts at item out[j]).  Host only; MASK_ERR_ARG unless 1 <= k <= n,
+ * level >= 1, out != NULL. */
+int32_t mask_seeded_init(uint64_t seed, int32_t level, int64_t n, int64_t k, int64_t* out);
 
 void mask_free(mask_index* idx); /* NULL-safe */
 

@@ -158,6 +158,32 @@ def means(Y, labels, P_old):
     return means_from_sums(S, cnt, P_old)[0], cnt
 
 
+# ------------------------------------------------------------------ seeded initialisation
+_M64 = (1 << 64) - 1
+
+
+def seeded_init(seed: int, level: int, n: int, k: int) -> np.ndarray:
+    """D2's k distinct init indices in [0, n) when the caller passes none (include/mask.h
+    mask_seeded_init, the same documented generator written out here): Floyd's algorithm --
+    for j = n-k .. n-1 take t = u(j+1) unless already taken, else j -- with u(m) = next() mod m
+    over the SplitMix64 sequence started at seed + level * 0x9E3779B97F4A7C15."""
+    if not (1 <= k <= n) or level < 1:
+        raise ValueError("need 1 <= k <= n and level >= 1")
+    state = (seed + level * 0x9E3779B97F4A7C15) & _M64
+    taken, out = set(), []
+    for j in range(n - k, n):
+        state = (state + 0x9E3779B97F4A7C15) & _M64
+        z = state
+        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & _M64
+        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & _M64
+        z = z ^ (z >> 31)
+        t = z % (j + 1)
+        v = j if t in taken else t
+        taken.add(v)
+        out.append(v)
+    return np.array(out, np.int64)
+
+
 # ------------------------------------------------------------------ Lloyd / build
 class LevelResult:
     def __init__(self, P, labels, J, changed, updates):

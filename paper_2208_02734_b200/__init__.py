@@ -7,7 +7,7 @@ sharding helpers.  Importing it does not require a GPU; calling it does (no CPU 
 """
 from . import _lib
 from .api import (Comm, Csr, Index, assign, build, build_grouped, collective_count, device_ok, grouped_depth,
-                  kernel_launches, matrix, merge, route, update)
+                  kernel_launches, matrix, merge, route, seeded_init, update)
 from ._lib import (
     MASK_BORROW_DATA,
     MASK_FORCE_SIMT,
@@ -22,7 +22,7 @@ from .shard import query_range, row_range
 
 __all__ = [
     "Comm", "Csr", "Index", "assign", "build", "build_grouped", "grouped_depth", "device_ok", "kernel_launches", "matrix",
-    "update", "route", "merge", "collective_count", "row_range",
+    "update", "route", "merge", "collective_count", "seeded_init", "row_range",
     "query_range", "MaskError", "MASK_BORROW_DATA", "MASK_FORCE_SIMT", "MASK_NO_FIXUP",
     "MASK_VALIDATE_FINITE", "MASK_TIME_KERNELS", "MASK_NO_SORT", "MASK_NO_FUSED",
 ]

@@ -299,27 +299,31 @@ def kernel_launches() -> int:
     return int(load().mask_kernel_launches())
 
 
-def build(data, levels: Sequence[int], iters: int, init_idx: Sequence[np.ndarray], tol: float = 0.0,
-          flags: int = 0, comm: Optional[Comm] = None, iter_cb: Optional[Callable] = None, stream=None,
-          n_global: Optional[int] = None, row_offset: int = 0) -> Index:
+def build(data, levels: Sequence[int], iters: int, init_idx: Optional[Sequence[np.ndarray]] = None,
+          tol: float = 0.0, flags: int = 0, comm: Optional[Comm] = None, iter_cb: Optional[Callable] = None,
+          stream=None, n_global: Optional[int] = None, row_offset: int = 0, seed: int = 0) -> Index:
     """mask_build: multilevel index over ``data`` (this rank's shard when ``comm`` is given).
 
-    iter_cb(level, pass, P (k x dim float32 numpy), labels (int32 numpy)) is the test-only
-    step-parity hook."""
+    init_idx: one array of distinct indices per level, or None to let the library draw them
+    from ``seed`` (mask_seeded_init).  iter_cb(level, pass, P (k x dim float32 numpy), labels
+    (int32 numpy)) is the test-only step-parity hook."""
     m, keep = matrix(data, n_global=n_global, row_offset=row_offset)
     L = len(levels)
     ks = (C.c_int64 * L)(*[int(k) for k in levels])
-    idx_arrays = [np.ascontiguousarray(a, dtype=np.int64) for a in init_idx]
-    if len(idx_arrays) != L:
-        raise ValueError("one init index array per level")
-    ptrs = (C.POINTER(C.c_int64) * L)(*[a.ctypes.data_as(C.POINTER(C.c_int64)) for a in idx_arrays])
+    ptrs = None
+    if init_idx is not None:
+        idx_arrays = [np.ascontiguousarray(a, dtype=np.int64) for a in init_idx]
+        if len(idx_arrays) != L:
+            raise ValueError("one init index array per level")
+        ptrs = (C.POINTER(C.c_int64) * L)(*[a.ctypes.data_as(C.POINTER(C.c_int64)) for a in idx_arrays])
     p = MaskBuildParams()
     p.num_levels = L
     p.max_iters = int(iters)
     p.k = ks
     p.tol = float(tol)
-    p.seed = 0
-    p.init_idx = ptrs
+    p.seed = int(seed) & 0xFFFFFFFFFFFFFFFF
+    if ptrs is not None:
+        p.init_idx = ptrs
     p.empty_policy = _lib.MASK_EMPTY_KEEP
     p.flags = int(flags)
     cb_ref = None
@@ -336,6 +340,13 @@ def build(data, levels: Sequence[int], iters: int, init_idx: Sequence[np.ndarray
     check(rc)
     keep_all = keep if (flags & _lib.MASK_BORROW_DATA) else ()
     return Index(out.value, keep_all, m.dim, m.format == _lib.MASK_CSR_F32)
+
+
+def seeded_init(seed: int, level: int, n: int, k: int) -> np.ndarray:
+    """mask_seeded_init: the k distinct init indices mask_build draws from ``seed`` for a level."""
+    out = np.empty(max(int(k), 1), np.int64)
+    check(load().mask_seeded_init(int(seed) & 0xFFFFFFFFFFFFFFFF, int(level), int(n), int(k), out.ctypes.data))
+    return out[:int(k)]
 
 
 def grouped_depth(n: int, length_group: int, n_centroids: int) -> Tuple[int, List[int]]:

@@ -655,7 +655,7 @@ void build_impl(const mask_matrix* data, const mask_build_params* p, mask_comm* 
                "num_levels must be in [1, 16]");
   MASK_REQUIRE(p->max_iters >= 0, MASK_ERR_ARG, "max_iters must be >= 0");
   MASK_REQUIRE(p->tol >= 0.0, MASK_ERR_ARG, "tol must be >= 0");
-  MASK_REQUIRE(p->k != nullptr && p->init_idx != nullptr, MASK_ERR_ARG, "k / init_idx are NULL");
+  MASK_REQUIRE(p->k != nullptr, MASK_ERR_ARG, "k is NULL");
   MASK_REQUIRE(p->empty_policy == MASK_EMPTY_KEEP, MASK_ERR_UNSUPPORTED, "only MASK_EMPTY_KEEP");
   const int world = comm ? comm->world : 1;
   const int rank = comm ? comm->rank : 0;
@@ -669,17 +669,27 @@ void build_impl(const mask_matrix* data, const mask_build_params* p, mask_comm* 
   const int64_t N = data->n_global;
   MASK_REQUIRE(N >= 1, MASK_ERR_ARG, "empty dataset");
   int64_t n_prev = N;
+  // init indices per level: the caller's, or drawn from `seed` (mask_seeded_init) when
+  // init_idx (or init_idx[l]) is NULL -- identical on every rank
+  std::vector<std::vector<int64_t>> drawn((size_t)p->num_levels);
+  std::vector<const int64_t*> inits((size_t)p->num_levels);
   for (int l = 0; l < p->num_levels; ++l) {
     const int64_t k = p->k[l];
     MASK_REQUIRE(k >= 1 && k <= n_prev, MASK_ERR_ARG,
                  "k[" + std::to_string(l) + "] must be in [1, n_items of the level]");
-    MASK_REQUIRE(p->init_idx[l] != nullptr, MASK_ERR_ARG, "init_idx[l] is NULL");
-    std::unordered_set<int64_t> seen;
-    seen.reserve((size_t)k * 2);
-    for (int64_t j = 0; j < k; ++j) {
-      const int64_t v = p->init_idx[l][j];
-      MASK_REQUIRE(v >= 0 && v < n_prev, MASK_ERR_ARG, "init index out of range");
-      MASK_REQUIRE(seen.insert(v).second, MASK_ERR_ARG, "init indices must be distinct");
+    if (p->init_idx && p->init_idx[l]) {
+      inits[l] = p->init_idx[l];
+      std::unordered_set<int64_t> seen;
+      seen.reserve((size_t)k * 2);
+      for (int64_t j = 0; j < k; ++j) {
+        const int64_t v = inits[l][j];
+        MASK_REQUIRE(v >= 0 && v < n_prev, MASK_ERR_ARG, "init index out of range");
+        MASK_REQUIRE(seen.insert(v).second, MASK_ERR_ARG, "init indices must be distinct");
+      }
+    } else {
+      drawn[l].resize((size_t)k);
+      mask_seeded_init(p->seed, l + 1, n_prev, k, drawn[l].data());
+      inits[l] = drawn[l].data();
     }
     n_prev = k;
   }
@@ -763,7 +773,7 @@ void build_impl(const mask_matrix* data, const mask_build_params* p, mask_comm* 
   HostStats hs;
   idx->levels.resize(p->num_levels);
   // ---- level 1: the (sharded) data
-  run_level(in, p->k[0], p->init_idx[0], p, comm, 1, st, idx->levels[0], hs);
+  run_level(in, p->k[0], inits[0], p, comm, 1, st, idx->levels[0], hs);
 
   // ---- end of level 1: every rank gets all labels (and all data rows for leaf scans)
   if (comm && world > 1) {
@@ -831,7 +841,7 @@ void build_impl(const mask_matrix* data, const mask_build_params* p, mask_comm* 
     up.n_local = up.n_global = prev.k;
     up.row_offset = 0;
     up.X = prev.P.p;
-    run_level(up, p->k[l], p->init_idx[l], p, nullptr, l + 1, st, idx->levels[l], hs);
+    run_level(up, p->k[l], inits[l], p, nullptr, l + 1, st, idx->levels[l], hs);
     if (comm && world > 1) {
       Level& L = idx->levels[l];
       MASK_NCCL(ncclGroupStart());
@@ -1338,6 +1348,30 @@ int32_t mask_merge(const int64_t* ids, const float* d2, int32_t n_nodes, int64_t
 }
 
 int64_t mask_collective_count(void) { return g_nccl_calls.load(); }
+
+// Seeded init (D2; mask.h): Floyd's sampling of k distinct indices in [0, n), driven by a
+// SplitMix64 stream keyed by (seed, level); the order is the insertion order.
+int32_t mask_seeded_init(uint64_t seed, int32_t level, int64_t n, int64_t k, int64_t* out) {
+  if (n < 1 || k < 1 || k > n || out == nullptr || level < 1) return MASK_ERR_ARG;
+  uint64_t state = seed + (uint64_t)level * 0x9E3779B97F4A7C15ull;
+  auto next = [&]() {
+    state += 0x9E3779B97F4A7C15ull;
+    uint64_t z = state;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+  };
+  std::unordered_set<int64_t> chosen;
+  chosen.reserve((size_t)k * 2);
+  int64_t c = 0;
+  for (int64_t j = n - k; j < n; ++j) {
+    const int64_t t = (int64_t)(next() % (uint64_t)(j + 1));
+    const int64_t v = chosen.count(t) ? j : t;
+    chosen.insert(v);
+    out[c++] = v;
+  }
+  return MASK_OK;
+}
 
 void mask_free(mask_index* idx) { delete idx; }
 

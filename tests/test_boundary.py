@@ -115,3 +115,13 @@ def test_plain_c_caller_on_gpu(tmp_path, lib):
     exe = _build_c_example(tmp_path)
     r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and "C_ABI_OK" in r.stdout, r.stdout + r.stderr
+
+
+def test_seeded_init_matches_the_oracle_generator(lib):
+    # mask_seeded_init is host code: the library and the oracle implement the documented
+    # generator independently and must agree index for index
+    import oracle
+    for seed, level, n, k in ((0, 1, 100, 10), (12345, 2, 4096, 256), (2**63 + 7, 3, 50, 50), (99, 1, 10**6, 4096)):
+        np.testing.assert_array_equal(mk.seeded_init(seed, level, n, k), oracle.seeded_init(seed, level, n, k))
+    with pytest.raises(mk.MaskError):
+        mk.seeded_init(1, 1, 5, 6)

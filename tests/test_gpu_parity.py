@@ -334,3 +334,29 @@ def test_sparse_C4_shaped_replica():
     csr = _csr_dev(rp, col, val, cfg.dim)
     idx, _ = _step_parity_build(None, cfg.levels, 4, inits, csr=csr)
     idx.free()
+
+
+def test_seeded_init_when_no_indices_are_given():
+    # init_idx = NULL: mask_build draws D2's indices from `seed` (mask_seeded_init); with T = 0
+    # every level's prototypes are exactly the drawn rows of its input
+    cfg = datagen.CONFIGS[2].scaled(256)
+    X = datagen.data(cfg)
+    seed = 20221004
+    idx = mk.build(t(X), cfg.levels, 0, None, seed=seed)
+    Y = X
+    for l, k in enumerate(cfg.levels, start=1):
+        sel = oracle.seeded_init(seed, l, Y.shape[0], k)
+        P = idx.prototypes(l)
+        np.testing.assert_array_equal(P, Y[sel])
+        Y = P
+    idx.free()
+    # a Lloyd build from the seed equals the build from the same indices passed explicitly
+    inits = [oracle.seeded_init(seed, 1, X.shape[0], cfg.levels[0])]
+    for l in range(1, len(cfg.levels)):
+        inits.append(oracle.seeded_init(seed, l + 1, cfg.levels[l - 1], cfg.levels[l]))
+    a = mk.build(t(X), cfg.levels, 4, None, seed=seed)
+    b = mk.build(t(X), cfg.levels, 4, inits)
+    for l in range(1, len(cfg.levels) + 1):
+        assert rel_l2(a.prototypes(l), b.prototypes(l)) < 1e-5
+    a.free()
+    b.free()

@@ -575,3 +575,35 @@ def test_cluster_single_node_and_tight_epsilon():
             assert (ids_t[i] == -1).all() and np.isinf(d2_t[i]).all()
     eids, _, _ = oracle.knn_exact(X, Q, 5)
     assert oracle.recall(ids_t, eids) <= oracle.recall(ids_all, eids)
+
+
+# ------------------------------------------------------------------ seeded initialisation (D2)
+def test_seeded_init_is_a_uniform_sample_without_replacement():
+    # k distinct indices in range; k = n gives every index; the first SplitMix64 outputs of the
+    # published reference seed 0 (state increments from 0) pin the generator itself
+    for (n, k) in ((10, 10), (1000, 5), (57, 56), (1, 1)):
+        v = oracle.seeded_init(3, 1, n, k)
+        assert len(v) == k and len(set(v.tolist())) == k and v.min() >= 0 and v.max() < n
+    assert sorted(oracle.seeded_init(9, 2, 40, 40).tolist()) == list(range(40))
+    # SplitMix64 from state 0: 0xE220A8397B1DCDAF, 0x6E789E6AA1B965F4 (Steele et al.'s sequence)
+    import oracle as o
+    state, outs = 0, []
+    for _ in range(2):
+        state = (state + 0x9E3779B97F4A7C15) & o._M64
+        z = state
+        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & o._M64
+        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & o._M64
+        outs.append(z ^ (z >> 31))
+    assert outs == [0xE220A8397B1DCDAF, 0x6E789E6AA1B965F4]
+    # level 1 with seed = -level * golden starts from state 0: its first draw is u(n-k+1) of
+    # the first output above
+    n, k = 1000, 3
+    seed = (-1 * 0x9E3779B97F4A7C15) & o._M64
+    assert oracle.seeded_init(seed, 1, n, k)[0] == 0xE220A8397B1DCDAF % (n - k + 1)
+    # uniformity: each index of [0, 20) is chosen with probability k/n = 1/4 over many seeds
+    cnt = np.zeros(20)
+    for s in range(4000):
+        cnt[oracle.seeded_init(s, 1, 20, 5)] += 1
+    p = 5 / 20
+    sd = np.sqrt(4000 * p * (1 - p))
+    assert np.all(np.abs(cnt - 4000 * p) < 5 * sd), cnt
