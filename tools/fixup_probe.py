@@ -1,5 +1,7 @@
+"""C2 near-tie re-check probe: K4 time per build (CUDA events) and, for every level-1 pass of a
+build, the number of rows K1 flags when the same prototypes are re-assigned (mask_assign)."""
 import sys, numpy as np, torch
-sys.path.insert(0, "/root/repo")
+sys.path.insert(0, __import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.abspath(__file__))))
 import datagen, paper_2208_02734_b200 as mk
 cfg = datagen.CONFIGS[2]
 X = torch.from_numpy(datagen.data(cfg)).cuda()

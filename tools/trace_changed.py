@@ -1,5 +1,6 @@
+"""Per-pass changed-label counts of the C2 level-1 Lloyd loop (mask_get_trace)."""
 import sys, torch
-sys.path.insert(0, "/root/repo")
+sys.path.insert(0, __import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.abspath(__file__))))
 import datagen, paper_2208_02734_b200 as mk
 cfg = datagen.CONFIGS[2]
 X = torch.from_numpy(datagen.data(cfg)).cuda()
