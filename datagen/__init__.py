@@ -247,6 +247,13 @@ def group_perm(seed: int, n: int) -> np.ndarray:
     return _rng(seed, 0).permutation(n).astype(np.int64)
 
 
+def relocation_keys(base_seed: int, iteration: int, n: int) -> np.ndarray:
+    """Random order keys of relocation iteration ``iteration`` (the rebuild seed policy
+    seed = base_seed + iteration, SPEC DESIGN DECISIONS): a permutation rank per point, used to
+    order the points inside each target group before the rebuild (no method arithmetic)."""
+    return _rng(base_seed + iteration, 7).permutation(n).astype(np.int64)
+
+
 def gaussian_clouds(seed: int, per_cloud: int, radius: float, sigma: float = 1.0, clouds: int = 8) -> np.ndarray:
     """``clouds`` isotropic Gaussian clouds in R^2 (the paper's synthetic benchmark),
     centres evenly spaced on a circle of ``radius``; radius >> sigma gives the no-overlap version

@@ -312,6 +312,47 @@ def exhaustive_error(index: Index, X) -> float:
     return float(np.mean(ids[:, 0] != np.arange(X.shape[0])))
 
 
+def relocation_order(order, n_groups: int, found, reached_group, keys) -> np.ndarray:
+    """One relocation step (§5.1: "when the point search reaches a partition at
+    the bottom of the tree and the target element is not found in that group, ... the target
+    point is reassigned to that partition"; reading G8): a point keeps its current data-layer
+    group when its search found it, else it moves to the group of the partition its search
+    reached; the new data-layer order lists the target groups in order, the points of a group
+    by their seeded key (the rebuild seed policy), and the rebuild splits it into the same
+    number of balanced groups."""
+    order = np.asarray(order, np.int64)
+    n = order.size
+    base, rem = divmod(n, n_groups)
+    sizes = np.full(n_groups, base, np.int64)
+    sizes[n_groups - rem:] += 1
+    cur = np.empty(n, np.int64)
+    cur[order] = np.repeat(np.arange(n_groups), sizes)
+    target = np.where(np.asarray(found, bool), cur, np.asarray(reached_group, np.int64))
+    return np.lexsort((np.asarray(keys, np.int64), target)).astype(np.int64)
+
+
+def relocate_and_rebuild(X, length_group: int, n_centroids: int, T: int, perm, iterations: int,
+                         base_seed: int, keys_fn):
+    """§5.1 relocation loop (Table 1): build, exhaustive point search, relocate the
+    points not found, rebuild; returns the error rate after each build (entry 0 = the first
+    build).  keys_fn(base_seed, i, n) gives iteration i's order keys (an input, datagen)."""
+    Xd = _f64(X)
+    n = Xd.shape[0]
+    g = grouped_layer_sizes(n, length_group, n_centroids)[0][1]
+    order = np.asarray(perm, np.int64)
+    errors = []
+    for i in range(iterations + 1):
+        idx = build_grouped(Xd, length_group, n_centroids, T, perm=order)
+        ids, _, _ = query(idx.P, idx.offsets, idx.members, Xd, Xd, 1, 1)
+        found = ids[:, 0] == np.arange(n)
+        errors.append(float(np.mean(~found)))
+        if i == iterations:
+            break
+        reached = idx.levels[0].labels[ids[:, 0]] // n_centroids  # the returned row's partition
+        order = relocation_order(order, g, found, reached, keys_fn(base_seed, i + 1, n))
+    return errors
+
+
 # ------------------------------------------------------------------ range search (NEXT-2)
 def cover_radii(index: Index, X) -> List[np.ndarray]:
     """cover_1(j) = max over data rows x with labels_1 = j of ||x - c_j||; cover_l(j) = max over

@@ -85,3 +85,41 @@ def test_grouped_argument_errors():
         mk.build_grouped(X, 200, 5, 5)  # fewer points than a group
     with pytest.raises(mk.MaskError):
         mk.build_grouped(X, 10, 5, 5, np.zeros(100, np.int64))  # not a permutation
+
+
+def test_relocation_and_rebuild_parity():
+    # §5.1 relocation loop (NEXT-4): every build is Algorithm 1 over the loop's order (same
+    # checks as above), every point search agrees with the oracle's descent over that index
+    # (tie window), and every next order is the oracle's relocation step applied to the
+    # search results (independent implementations of reading G8)
+    from paper_2208_02734_b200.relocate import relocate_and_rebuild
+    lg, nc = 16, 8
+    X = datagen.gaussian_clouds(11, 200, 12.0, 2.0)
+    n = X.shape[0]
+    perm = datagen.group_perm(11, n)
+    g = oracle.grouped_layer_sizes(n, lg, nc)[0][1]
+    recs = []
+
+    def hook(i, order, idx, found, reached):
+        _check_layers(idx, X, lg, nc, order)
+        L = idx.num_levels
+        ch = [idx.children(l) for l in range(1, L + 1)]
+        ids, _, gap = oracle.query([idx.prototypes(l) for l in range(1, L + 1)], [c[0] for c in ch],
+                                   [c[1] for c in ch], X, X, 1, 1)
+        f_ref = ids[:, 0] == np.arange(n)
+        bad = (f_ref != found) & (gap >= TIE_REL)
+        assert not bad.any(), f"iteration {i}: {int(bad.sum())} point searches differ"
+        agree = f_ref == found
+        r_ref = idx.labels(1)[ids[:, 0]] // nc
+        assert np.array_equal(r_ref[agree & ~found], reached[agree & ~found])
+        recs.append((order.copy(), found.copy(), reached.copy()))
+
+    keys = lambda i, m: datagen.relocation_keys(77, i, m)  # noqa: E731
+    errs = relocate_and_rebuild(torch.from_numpy(X).cuda(), lg, nc, 30, perm, 3, keys, hook=hook)
+    assert len(errs) == 4 and len(recs) == 4
+    for i, (order, found, reached) in enumerate(recs):
+        assert errs[i] == float(np.mean(~found))
+        if i + 1 < len(recs):
+            np.testing.assert_array_equal(recs[i + 1][0], oracle.relocation_order(order, g, found, reached,
+                                                                                  keys(i + 1, n)))
+    assert min(errs[1:]) < errs[0]  # relocation helps (Table 1's trend)
