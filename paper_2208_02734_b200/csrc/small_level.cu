@@ -112,12 +112,13 @@ constexpr int kSmallSmemFloats = 11264;  // prototypes staged in shared memory u
 
 // row-vs-all-prototypes argmin; C is shared memory (STAGED) or global memory read through L2
 // (P changes inside the kernel, so no read-only-cache loads)
-template <int D, bool STAGED>
+template <int D, bool STAGED, bool STRIDED = false>
 __device__ __forceinline__ void row_argmin(const float (&x)[D], const float* C, int64_t k, int d, float& bv,
                                            int32_t& bj, int j0 = 0, int jstep = 1) {
   bv = INFINITY;
   bj = 0x7fffffff;
-  for (int64_t j = j0; j < k; j += jstep) {
+  if (!STRIDED) j0 = 0, jstep = 1;  // compile-time unit stride for the one-lane-per-row case
+  for (int64_t j = j0; j < k; j += (STRIDED ? jstep : 1)) {
     const float* cj = C + j * d;
     float acc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
@@ -163,8 +164,13 @@ __device__ void assign_all(const SmallArgs& a, int slot, float* sP) {
       float x[D];
 #pragma unroll
       for (int e = 0; e < D; ++e) x[e] = e < a.d ? __ldg(a.Y + i * a.d + e) : 0.f;
-      if (staged) row_argmin<D, true>(x, sP, a.k, a.d, bv, bj, h, S);
-      else row_argmin<D, false>(x, a.P, a.k, a.d, bv, bj, h, S);
+      if (S == 1) {
+        if (staged) row_argmin<D, true>(x, sP, a.k, a.d, bv, bj);
+        else row_argmin<D, false>(x, a.P, a.k, a.d, bv, bj);
+      } else {
+        if (staged) row_argmin<D, true, true>(x, sP, a.k, a.d, bv, bj, h, S);
+        else row_argmin<D, false, true>(x, a.P, a.k, a.d, bv, bj, h, S);
+      }
     }
     for (int o = 1; o < S; o <<= 1) {
       const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
@@ -272,9 +278,6 @@ void launch_small_level(const float* Y, int64_t n, int d, int64_t k, float* P, i
   MASK_REQUIRE(per_sm >= 1, MASK_ERR_CUDA, "small-level kernel cannot be resident");
   // enough blocks for the rows (and the prototypes in the finalize phase), all co-resident
   int64_t want = (std::max<int64_t>(n, k * 32) + 255) / 256;
-  // a tiny level (C2 level 3: 256 items, 16 prototypes) runs in one block: block barriers
-  // instead of grid barriers, its work is a few hundred distances per thread
-  if (n <= 1024 && k <= 64) want = 1;
   // spread each row's prototype scan over tpr lanes until ~16K threads work on the assignment
   // (C2 level 2: 4,096 rows x 256 prototypes -> 4 lanes per row, 64 blocks)
   if (want > 1) {
