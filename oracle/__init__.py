@@ -316,8 +316,8 @@ def relocation_order(order, n_groups: int, found, reached_group, keys) -> np.nda
     """One relocation step (§5.1: "when the point search reaches a partition at
     the bottom of the tree and the target element is not found in that group, ... the target
     point is reassigned to that partition"; reading G8): a point keeps its current data-layer
-    group when its search found it, else it moves to the group of the partition its search
-    reached; the new data-layer order lists the target groups in order, the points of a group
+    group when its search found it (or reached no partition: reached_group < 0), else it moves
+    to the group of the partition its search reached; the new data-layer order lists the target groups in order, the points of a group
     by their seeded key (the rebuild seed policy), and the rebuild splits it into the same
     number of balanced groups."""
     order = np.asarray(order, np.int64)
@@ -327,7 +327,9 @@ def relocation_order(order, n_groups: int, found, reached_group, keys) -> np.nda
     sizes[n_groups - rem:] += 1
     cur = np.empty(n, np.int64)
     cur[order] = np.repeat(np.arange(n_groups), sizes)
-    target = np.where(np.asarray(found, bool), cur, np.asarray(reached_group, np.int64))
+    reached_group = np.asarray(reached_group, np.int64)
+    # a search that dead-ends (no partition reached: reached_group < 0) leaves the point in place
+    target = np.where(np.asarray(found, bool) | (reached_group < 0), cur, reached_group)
     return np.lexsort((np.asarray(keys, np.int64), target)).astype(np.int64)
 
 
@@ -348,7 +350,9 @@ def relocate_and_rebuild(X, length_group: int, n_centroids: int, T: int, perm, i
         errors.append(float(np.mean(~found)))
         if i == iterations:
             break
-        reached = idx.levels[0].labels[ids[:, 0]] // n_centroids  # the returned row's partition
+        # the returned row's partition (-1: the descent dead-ended in a prototype whose children
+        # are all childless, so nothing was returned)
+        reached = np.where(ids[:, 0] >= 0, idx.levels[0].labels[np.maximum(ids[:, 0], 0)] // n_centroids, -1)
         order = relocation_order(order, g, found, reached, keys_fn(base_seed, i + 1, n))
     return errors
 

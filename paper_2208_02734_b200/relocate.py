@@ -59,7 +59,8 @@ def relocate_and_rebuild(X, length_group: int, n_centroids: int, iters: int, per
         idx.free()
         if i == iterations:
             break
-        target = np.where(found, _groups_of(order, n_groups), reached)
+        # found points, and searches that reached no partition (reached < 0), stay in place
+        target = np.where(found | (reached < 0), _groups_of(order, n_groups), reached)
         keys = np.asarray(keys_fn(i + 1, n), np.int64)
         order = np.lexsort((keys, target)).astype(np.int64)
     return errors
