@@ -147,8 +147,10 @@ void mask_comm_free(mask_comm* comm); /* NULL-safe */
  * (J_t, changed_t); and a copy of the data for leaf scans (all n_global rows on every rank
  * after the build), unless MASK_BORROW_DATA is set with device data on one GPU, in which
  * case the caller keeps `data` alive and unchanged until mask_free.
- * Errors: MASK_ERR_ARG (L < 1, k[l] out of range, bad init indices, bad CSR, dim < 1),
- * MASK_ERR_NONFINITE, MASK_ERR_OOM, MASK_ERR_CUDA, MASK_ERR_NCCL. *out is NULL on error. */
+ * Errors: MASK_ERR_ARG (L < 1, k[l] out of range, bad init indices, bad CSR, dim < 1, or --
+ * with a communicator -- ranks disagreeing on the parameters / init indices, checked with one
+ * allreduce of a hash), MASK_ERR_NONFINITE, MASK_ERR_OOM, MASK_ERR_CUDA, MASK_ERR_NCCL.  *out
+ * is NULL on error. */
 int32_t mask_build(const mask_matrix* data, const mask_build_params* params, mask_comm* comm,
                    void* stream, mask_index** out);
 

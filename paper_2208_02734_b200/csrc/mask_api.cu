@@ -698,6 +698,33 @@ void build_impl(const mask_matrix* data, const mask_build_params* p, mask_comm* 
   MASK_CUDA(cudaGetDeviceCount(&ndev));
   MASK_REQUIRE(ndev > 0, MASK_ERR_CUDA, "no CUDA device");
   if (data->format == MASK_CSR_F32 && data->memory == MASK_MEM_DEVICE) check_csr_structure(data, st);
+  if (comm && world > 1) {
+    // every rank must build the same index: a hash of the parameters and init indices, its
+    // max and min over the ranks must agree (MASK_ERR_ARG on every rank otherwise)
+    uint64_t h = 1469598103934665603ull;
+    auto mix = [&](uint64_t v) { h = (h ^ v) * 1099511628211ull; };
+    mix((uint64_t)p->num_levels);
+    mix((uint64_t)p->max_iters);
+    uint64_t tb;
+    std::memcpy(&tb, &p->tol, sizeof(tb));
+    mix(tb);
+    mix((uint64_t)p->flags);
+    mix((uint64_t)data->dim);
+    mix((uint64_t)data->format);
+    mix((uint64_t)data->n_global);
+    for (int l = 0; l < p->num_levels; ++l) {
+      mix((uint64_t)p->k[l]);
+      for (int64_t j = 0; j < p->k[l]; ++j) mix((uint64_t)inits[l][j]);
+    }
+    const int64_t hv[2] = {(int64_t)(h >> 1), -(int64_t)(h >> 1)};  // max of both = (max h, -min h)
+    DevBuf<int64_t> hd(2);
+    MASK_CUDA(cudaMemcpyAsync(hd.p, hv, sizeof(hv), cudaMemcpyHostToDevice, st));
+    MASK_NCCL(ncclAllReduce(hd.p, hd.p, 2, ncclInt64, ncclMax, comm->comm, st));
+    int64_t hr[2];
+    MASK_CUDA(cudaMemcpyAsync(hr, hd.p, sizeof(hr), cudaMemcpyDeviceToHost, st));
+    MASK_CUDA(cudaStreamSynchronize(st));
+    MASK_REQUIRE(hr[0] == -hr[1], MASK_ERR_ARG, "ranks disagree on the build parameters or init indices");
+  }
 
   auto idx = std::make_unique<mask_index>();
   idx->dim = data->dim;
