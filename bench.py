@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--force-simt", action="store_true")
+    ap.add_argument("--force-comm", action="store_true",
+                    help="build through an NCCL communicator even on one rank (exercises the multi-GPU path)")
     return ap.parse_args()
 
 
@@ -282,7 +284,7 @@ def main():
     if rank == 0:
         buildlib.build()
     comm = None
-    if world > 1:
+    if world > 1 or args.force_comm:  # --force-comm: the NCCL build path on one rank (testing)
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=dev)
@@ -499,7 +501,7 @@ def main():
     idx.free()
     if comm:
         comm.free()
-    if world > 1:
+    if world > 1 or args.force_comm:
         torch.distributed.destroy_process_group()
 
 
