@@ -64,7 +64,9 @@ enum {
   MASK_SYNC_STATS = 1 << 4,      /* reserved: J/changed are read every pass (always on)       */
   MASK_TIME_KERNELS = 1 << 5,    /* record CUDA-event device times of the step kernels        */
   MASK_NO_SORT = 1 << 6,         /* small d: keep the data order in K1 (no per-pass label sort) */
-  MASK_NO_FUSED = 1 << 7         /* small levels: per-pass kernels instead of the fused loop    */
+  MASK_NO_FUSED = 1 << 7,        /* small levels: per-pass kernels instead of the fused loop    */
+  MASK_TIME_ASSIGN = 1 << 8      /* like MASK_TIME_KERNELS for the assignment class only (one
+                                    event pair per pass: the cheapest live kernel timing)      */
 };
 
 /* kernel classes of mask_get_timing */

@@ -14,6 +14,7 @@ from ._lib import (
     MASK_NO_FIXUP,
     MASK_NO_FUSED,
     MASK_NO_SORT,
+    MASK_TIME_ASSIGN,
     MASK_TIME_KERNELS,
     MASK_VALIDATE_FINITE,
     MaskError,
@@ -24,5 +25,5 @@ __all__ = [
     "Comm", "Csr", "Index", "assign", "build", "build_grouped", "grouped_depth", "device_ok", "kernel_launches", "matrix",
     "update", "route", "merge", "collective_count", "seeded_init", "row_range",
     "query_range", "MaskError", "MASK_BORROW_DATA", "MASK_FORCE_SIMT", "MASK_NO_FIXUP",
-    "MASK_VALIDATE_FINITE", "MASK_TIME_KERNELS", "MASK_NO_SORT", "MASK_NO_FUSED",
+    "MASK_VALIDATE_FINITE", "MASK_TIME_KERNELS", "MASK_TIME_ASSIGN", "MASK_NO_SORT", "MASK_NO_FUSED",
 ]

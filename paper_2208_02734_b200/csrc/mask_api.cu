@@ -261,11 +261,14 @@ struct LloydWS {
 // pairs of a class count (passes skipped on the device after convergence are excluded).
 struct EventLog {
   std::vector<cudaEvent_t> ev[MASK_T_NCLASS];
+  unsigned classes;  // bit c: class c is timed (MASK_TIME_ASSIGN: the assignment class only)
+  explicit EventLog(unsigned cls) : classes(cls) {}
   ~EventLog() {
     for (auto& v : ev)
       for (auto e : v) cudaEventDestroy(e);
   }
   void mark(int c, cudaStream_t st) {
+    if (!(classes & (1u << c))) return;
     cudaEvent_t e;
     MASK_CUDA(cudaEventCreate(&e));
     MASK_CUDA(cudaEventRecord(e, st));
@@ -445,7 +448,11 @@ void run_level(const Input& in, int64_t k, const int64_t* init_idx_host, const m
   }
   if (comm) MASK_NCCL(ncclAllReduce(L.P.p, L.P.p, (size_t)k * d, ncclFloat, ncclSum, comm->comm, st));
 
-  std::unique_ptr<EventLog> ev((p->flags & MASK_TIME_KERNELS) ? new EventLog : nullptr);
+  // every event pair costs a few microseconds of device time per pass (~5 % of a C2 build for
+  // all four classes), so MASK_TIME_ASSIGN times the assignment kernel alone
+  const unsigned ev_classes = (p->flags & MASK_TIME_KERNELS) ? (1u << MASK_T_NCLASS) - 1u
+                              : (p->flags & MASK_TIME_ASSIGN) ? (1u << MASK_T_ASSIGN) : 0u;
+  std::unique_ptr<EventLog> ev(ev_classes ? new EventLog(ev_classes) : nullptr);
 
   // test-only step-parity hook: host copies of the P_t a pass used and the labels it produced
   auto emit_cb = [&](int pass, const float* P_used, const int32_t* labels_dev) {
