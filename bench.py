@@ -329,11 +329,14 @@ def main():
     if world == 1:
         flags |= mk.MASK_BORROW_DATA
     stream = torch.cuda.current_stream(dev)
+    nq_local = (Q.rows if csr else int(Q.shape[0]))
+    qout = (torch.empty((nq_local, cfg.knn), dtype=torch.int64, device=dev),
+            torch.empty((nq_local, cfg.knn), dtype=torch.float32, device=dev))  # result buffers, reused
 
     def step():
         idx = mk.build(X, cfg.levels, cfg.iters, inits, flags=flags, comm=comm, n_global=n_global,
                        row_offset=rank * n_local, stream=stream)
-        ids, d2 = idx.query(Q, knn=cfg.knn, beam=1, stream=stream)
+        ids, d2 = idx.query(Q, knn=cfg.knn, beam=1, stream=stream, out=qout)
         return idx, ids, d2
 
     def barrier():
@@ -366,7 +369,7 @@ def main():
         idx = mk.build(X, cfg.levels, cfg.iters, inits, flags=flags, comm=comm, n_global=n_global,
                        row_offset=rank * n_local, stream=stream)
         e1.record(stream)
-        ids, d2 = idx.query(Q, knn=cfg.knn, beam=1, stream=stream)
+        ids, d2 = idx.query(Q, knn=cfg.knn, beam=1, stream=stream, out=qout)
         e2.record(stream)
         barrier()
         step_ms.append(e0.elapsed_time(e2))
