@@ -280,6 +280,11 @@ int64_t mask_collective_count(void);
  * level >= 1, out != NULL. */
 int32_t mask_seeded_init(uint64_t seed, int32_t level, int64_t n, int64_t k, int64_t* out);
 
+/* Test hook (failure-path tests): the nth next device allocation of the library (0 = the next
+ * one) fails as if the device were out of memory, so the call making it returns MASK_ERR_OOM
+ * and releases what it had allocated; -1 disarms it.  Not for production use. */
+void mask_debug_fail_alloc(int64_t nth);
+
 void mask_free(mask_index* idx); /* NULL-safe */
 
 /* ---------------------------------------------------------------- step entry points

@@ -45,7 +45,7 @@ EXPORTS = [
     "mask_get_children", "mask_get_trace", "mask_kernel_launches", "mask_get_timing",
     "mask_grouped_depth", "mask_build_grouped", "mask_range_query", "mask_insert",
     "mask_top_prototypes", "mask_route", "mask_query_routed", "mask_merge", "mask_collective_count",
-    "mask_seeded_init",
+    "mask_seeded_init", "mask_debug_fail_alloc",
 ]
 
 
@@ -148,6 +148,7 @@ def load():
             "mask_merge": (i32, [P, P, i32, i64, i32, P, P, P]),
             "mask_collective_count": (i64, []),
             "mask_seeded_init": (i32, [C.c_uint64, i32, i64, i64, P]),
+            "mask_debug_fail_alloc": (None, [i64]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)

@@ -6,8 +6,10 @@
 // lists, the query entry point (Algorithm 2) and introspection.
 #include <cuda_runtime.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cmath>
 #include <cstring>
 #include <memory>
@@ -44,7 +46,13 @@ size_t size_class(size_t bytes) {
 }
 }  // namespace
 
+namespace {
+std::atomic<int64_t> g_fail_alloc{-1};  // test hook: the n-th next device allocation fails
+}
+
 void* mask::pool_alloc(size_t bytes) {
+  if (g_fail_alloc.load(std::memory_order_relaxed) >= 0 && g_fail_alloc.fetch_sub(1) == 0)
+    ::mask::fail(MASK_ERR_OOM, "injected device allocation failure (mask_debug_fail_alloc)");
   const size_t c = size_class(bytes);
   {
     std::lock_guard<std::mutex> g(g_pool_mu);
@@ -99,6 +107,12 @@ int32_t guarded(F&& f) {
     return MASK_ERR_CUDA;
   }
 }
+
+// NVTX ranges around the API calls and levels (free when no profiler is attached)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 #define MASK_NCCL(x)                                                                     \
   do {                                                                                   \
@@ -408,8 +422,25 @@ __global__ void k_copy_labels(int32_t* __restrict__ dst, const int32_t* __restri
 // The whole loop is enqueued at once: the stop tests run on the device (k_after_stats,
 // the last blocks of k_pass_stats / k_finalize) and later passes become no-ops, so the host synchronises once per level
 // (unless the test-only iteration callback needs host copies after every pass).
+// After a host synchronisation of a communicator build: a failed or hung peer surfaces as an
+// asynchronous NCCL error; abort the communicator (every later collective returns at once) and
+// fail the call with MASK_ERR_NCCL instead of waiting forever.
+void check_comm(mask_comm* comm) {
+  if (!comm) return;
+  ncclResult_t ar = ncclSuccess;
+  const ncclResult_t r = ncclCommGetAsyncError(comm->comm, &ar);
+  if (r != ncclSuccess || ar != ncclSuccess) {
+    ncclCommAbort(comm->comm);
+    comm->comm = nullptr;
+    ::mask::fail(MASK_ERR_NCCL, std::string("NCCL asynchronous error: ") + ncclGetErrorString(r != ncclSuccess ? r : ar));
+  }
+}
+
 void run_level(const Input& in, int64_t k, const int64_t* init_idx_host, const mask_build_params* p,
                mask_comm* comm, int level_no, cudaStream_t st, Level& L, HostStats& hs) {
+  char nv[32];
+  std::snprintf(nv, sizeof(nv), "mask level %d", level_no);
+  NvtxRange range(nv);
   const int d = in.dim;
   const int64_t n = in.n_local;
   const int T = p->max_iters;
@@ -580,6 +611,7 @@ void run_level(const Input& in, int64_t k, const int64_t* init_idx_host, const m
   MASK_CUDA(cudaMemcpyAsync(hch.data(), chd.p, sizeof(unsigned long long) * (T + 2), cudaMemcpyDeviceToHost, st));
   MASK_CUDA(cudaMemcpyAsync(hfin.data(), fin.p, sizeof(uint32_t) * 2 * (T + 2), cudaMemcpyDeviceToHost, st));
   MASK_CUDA(cudaStreamSynchronize(st));
+  check_comm(comm);
   const int loop_passes = T > 0 ? h_ctrl[1] : 0;  // assignment passes run inside the loop
   int updates = 0;
   for (int t = 0; t < loop_passes; ++t) {
@@ -1052,7 +1084,11 @@ void mask_comm_free(mask_comm* comm) {
 
 int32_t mask_build(const mask_matrix* data, const mask_build_params* params, mask_comm* comm,
                    void* stream, mask_index** out) {
-  return guarded([&] { build_impl(data, params, comm, as_stream(stream), out); });
+  NvtxRange range("mask_build");
+  return guarded([&] {
+    MASK_REQUIRE(!comm || comm->comm, MASK_ERR_NCCL, "communicator was aborted after an earlier NCCL error");
+    build_impl(data, params, comm, as_stream(stream), out);
+  });
 }
 
 int32_t mask_grouped_depth(int64_t n, int32_t length_group, int32_t n_centroids, int64_t* layer_k, int32_t cap) {
@@ -1308,6 +1344,7 @@ int32_t query_impl(const mask_index* idx, const mask_matrix* queries, int32_t k_
 
 int32_t mask_query(const mask_index* idx, const mask_matrix* queries, int32_t k_nn, int32_t beam,
                    int64_t* ids_out, float* d2_out, void* stream) {
+  NvtxRange range("mask_query");
   return query_impl(idx, queries, k_nn, beam, ids_out, d2_out, stream, nullptr, 0, 0);
 }
 
@@ -1382,6 +1419,8 @@ int32_t mask_merge(const int64_t* ids, const float* d2, int32_t n_nodes, int64_t
 }
 
 int64_t mask_collective_count(void) { return g_nccl_calls.load(); }
+
+void mask_debug_fail_alloc(int64_t nth) { g_fail_alloc.store(nth); }
 
 // Seeded init (D2; mask.h): Floyd's sampling of k distinct indices in [0, n), driven by a
 // SplitMix64 stream keyed by (seed, level); the order is the insertion order.

@@ -25,6 +25,10 @@
 
 #include "common.cuh"
 
+#ifndef MASK_K11_THREADS
+#define MASK_K11_THREADS 16384  // assignment threads the lanes-per-row split aims for
+#endif
+
 namespace mask {
 
 namespace {
@@ -281,7 +285,7 @@ void launch_small_level(const float* Y, int64_t n, int d, int64_t k, float* P, i
   // spread each row's prototype scan over tpr lanes until ~16K threads work on the assignment
   // (C2 level 2: 4,096 rows x 256 prototypes -> 4 lanes per row, 64 blocks)
   if (want > 1) {
-    while (a.tpr < 32 && n * a.tpr * 2 <= 16384 && a.tpr * 2 <= k) a.tpr *= 2;
+    while (a.tpr < 32 && n * a.tpr * 2 <= MASK_K11_THREADS && a.tpr * 2 <= k) a.tpr *= 2;
     want = std::max<int64_t>(want, (n * a.tpr + 255) / 256);
   }
   const int64_t cap = (int64_t)per_sm * num_sms();

@@ -98,3 +98,34 @@ def test_concurrent_queries_from_threads_and_streams():
     for (a, b), (c, d) in zip(out, seq):
         assert torch.equal(a, c) and torch.equal(b, d)
     idx.free()
+
+
+def test_injected_allocation_failures_are_reported_and_recovered():
+    # failure mapping: a device allocation failing in the middle of a build or a
+    # query returns MASK_ERR_OOM with a message, frees what the call had taken, and the
+    # library keeps working afterwards (same results as an undisturbed build)
+    lib = mk._lib.load()
+    cfg = datagen.CONFIGS[2].scaled(256)
+    X = datagen.data(cfg)
+    inits = datagen.all_init_indices(cfg)
+    ref = mk.build(t(X), cfg.levels, 3, inits)
+    for nth in (0, 5, 40):
+        lib.mask_debug_fail_alloc(nth)
+        with pytest.raises(mk.MaskError) as e:
+            mk.build(t(X), cfg.levels, 3, inits)
+        assert e.value.code == -3 and "injected" in str(e.value)
+    lib.mask_debug_fail_alloc(-1)
+    Qh = np.ascontiguousarray(datagen.queries(cfg, count=50))
+    lib.mask_debug_fail_alloc(0)
+    with pytest.raises(mk.MaskError) as e:
+        ref.query(Qh, knn=5)  # host queries: the staging buffer allocation fails
+    assert e.value.code == -3
+    lib.mask_debug_fail_alloc(-1)
+    again = mk.build(t(X), cfg.levels, 3, inits)
+    for lv in range(1, len(cfg.levels) + 1):  # FP32 atomics: equal up to the summation order
+        Pa, Pb = again.prototypes(lv), ref.prototypes(lv)
+        assert np.linalg.norm(Pa - Pb) <= 1e-5 * np.linalg.norm(Pb)
+    a, _ = ref.query(Qh, knn=5)
+    assert a.shape == (50, 5) and (a >= 0).any()
+    again.free()
+    ref.free()
