@@ -149,7 +149,52 @@ constexpr int kWarpsPerBlock = 4;
 
 }  // namespace
 
+// Distances of the warp's 32 candidates (lane L owns candidate id cid, PAD_ID = none), LPC lanes
+// per candidate: at step s the lane group g = L / LPC evaluates candidate s * (32 / LPC) + g with
+// one 16-byte load per lane per 4 * LPC dimensions, reduces over its LPC lanes, and the owner
+// lane picks its value up.  Fewer L1 wavefronts per byte than one row per lane but more
+// instructions: used for wide beams (many candidates per query), LPC = 1 otherwise.
+template <int LPC>
+__device__ __forceinline__ float coop_dist(const float* __restrict__ q, const float* __restrict__ base, int d,
+                                           int32_t cid, int lane) {
+  if constexpr (LPC == 1) {
+    return cid == PAD_ID ? INFINITY : dist_dense(q, base + (int64_t)cid * d, d);
+  } else {
+    constexpr int G = 32 / LPC;
+    const int g = lane / LPC, e = lane % LPC;
+    const int d4 = d >> 2;
+    float mine = INFINITY;
+#pragma unroll
+    for (int s = 0; s < LPC; ++s) {
+      const int32_t id = __shfl_sync(FULL, cid, s * G + g);
+      float acc = 0.f;
+      if (id != PAD_ID) {
+        const float4* x4 = reinterpret_cast<const float4*>(base + (int64_t)id * d);
+        const float4* q4 = reinterpret_cast<const float4*>(q);
+        for (int c = e; c < d4; c += LPC) {
+          const float4 xv = __ldg(x4 + c);
+          const float4 qv = q4[c];
+          float t = qv.x - xv.x;
+          acc = fmaf(t, t, acc);
+          t = qv.y - xv.y;
+          acc = fmaf(t, t, acc);
+          t = qv.z - xv.z;
+          acc = fmaf(t, t, acc);
+          t = qv.w - xv.w;
+          acc = fmaf(t, t, acc);
+        }
+      }
+#pragma unroll
+      for (int o = LPC / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(FULL, acc, o);
+      const float v = __shfl_sync(FULL, acc, (lane % G) * LPC);
+      if (lane / G == s) mine = v;
+    }
+    return cid == PAD_ID ? INFINITY : mine;
+  }
+}
+
 // Dense queries against a dense index.  Shared memory: one q vector (d floats) per warp.
+template <int LPC>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32)
     k_query_dense(QIndex qi, const float* __restrict__ Q, int64_t nq, int knn, int beam,
                   int64_t* __restrict__ ids_out, float* __restrict__ d2_out, int leaf_only) {
@@ -177,13 +222,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
       top.reset(beam);
       for (int64_t j0 = 0; j0 < L.k; j0 += 32) {
         const int64_t j = j0 + lane;
-        float cd = INFINITY;
-        int32_t cid = PAD_ID;
-        if (j < L.k && has_children(L, j)) {
-          cd = dist_dense(q, L.P + j * d, d);
-          cid = (int32_t)j;
-        }
-        top.offer(cd, cid, lane);
+        const int32_t cid = (j < L.k && has_children(L, j)) ? (int32_t)j : PAD_ID;
+        top.offer(coop_dist<LPC>(q, L.P, d, cid, lane), cid, lane);
       }
     }
     // ---- levels L-1 .. 1: children of the kept prototypes
@@ -201,16 +241,12 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
         const int64_t m0 = up.offsets[p], m1 = up.offsets[p + 1];
         for (int64_t m = m0; m < m1; m += 32) {
           const int64_t mm = m + lane;
-          float cd = INFINITY;
           int32_t cid = PAD_ID;
           if (mm < m1) {
             const int32_t j = up.members[mm];
-            if (has_children(L, j)) {
-              cd = dist_dense(q, L.P + (int64_t)j * d, d);
-              cid = j;
-            }
+            if (has_children(L, j)) cid = j;
           }
-          top.offer(cd, cid, lane);
+          top.offer(coop_dist<LPC>(q, L.P, d, cid, lane), cid, lane);
         }
       }
     }
@@ -231,14 +267,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
         const int64_t m0 = L1.offsets[p], m1 = L1.offsets[p + 1];
         for (int64_t m = m0; m < m1; m += 32) {
           const int64_t mm = m + lane;
-          float cd = INFINITY;
-          int32_t cid = PAD_ID;
-          if (mm < m1) {
-            const int32_t i = L1.members[mm];
-            cd = dist_dense(q, qi.X + (int64_t)i * d, d);
-            cid = i;
-          }
-          top.offer(cd, cid, lane);
+          const int32_t cid = mm < m1 ? (int32_t)L1.members[mm] : PAD_ID;
+          top.offer(coop_dist<LPC>(q, qi.X, d, cid, lane), cid, lane);
         }
       }
     }
@@ -256,11 +286,21 @@ void launch_query_dense(const QIndex& qi, const float* Q, int64_t nq, int knn, i
   const int dpad = (qi.dim + 3) & ~3;
   const size_t smem = (size_t)kWarpsPerBlock * dpad * sizeof(float);
   MASK_REQUIRE(smem <= 200 * 1024, MASK_ERR_UNSUPPORTED, "query: dim too large for dense queries");
-  if (smem > 48 * 1024)
-    MASK_CUDA(cudaFuncSetAttribute(k_query_dense, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  // wide beams (>= 8 prototypes kept per level) visit many candidates per query: 8 lanes per
+  // candidate row there (C3: beam 16 57 -> 47 ms, beam 32 110 -> 77 ms), one lane per row otherwise
+  const bool coop = (qi.dim & 3) == 0 && qi.dim >= 32 && beam >= 8 && ((uintptr_t)qi.X & 15) == 0;
   const int64_t blocks = (nq + kWarpsPerBlock - 1) / kWarpsPerBlock;
   const unsigned grid = (unsigned)(blocks < (int64_t)num_sms() * 16 ? blocks : (int64_t)num_sms() * 16);
-  k_query_dense<<<grid, kWarpsPerBlock * 32, smem, st>>>(qi, Q, nq, knn, beam, ids, d2, leaf_only ? 1 : 0);
+  const int lo = leaf_only ? 1 : 0;
+  if (coop) {
+    if (smem > 48 * 1024)
+      MASK_CUDA(cudaFuncSetAttribute(k_query_dense<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_query_dense<8><<<grid, kWarpsPerBlock * 32, smem, st>>>(qi, Q, nq, knn, beam, ids, d2, lo);
+  } else {
+    if (smem > 48 * 1024)
+      MASK_CUDA(cudaFuncSetAttribute(k_query_dense<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_query_dense<1><<<grid, kWarpsPerBlock * 32, smem, st>>>(qi, Q, nq, knn, beam, ids, d2, lo);
+  }
   MASK_LAUNCH_CHECK();
 }
 
