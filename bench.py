@@ -46,6 +46,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--force-simt", action="store_true")
+    ap.add_argument("--beam", type=int, default=1, help="prototypes kept per level in the query (1 = Algorithm 2)")
+    ap.add_argument("--knn", type=int, default=None, help="neighbours per query (default: the config's)")
+    ap.add_argument("--iters", type=int, default=None, help="Lloyd iterations T (default: the config's)")
     ap.add_argument("--force-comm", action="store_true",
                     help="build through an NCCL communicator even on one rank (exercises the multi-GPU path)")
     return ap.parse_args()
@@ -295,6 +298,11 @@ def main():
         comm = mk.Comm.from_process_group()
 
     cfg = datagen.CONFIGS[args.config]
+    if args.knn is not None or args.iters is not None:  # optional overrides, reported in `config`
+        import dataclasses
+        cfg = dataclasses.replace(cfg, knn=args.knn if args.knn is not None else cfg.knn,
+                                  iters=args.iters if args.iters is not None else cfg.iters)
+    beam = args.beam
     # weak scaling: rank r owns rows [r*n, (r+1)*n) of the block-seeded generator
     n_local = cfg.n
     n_global = n_local * world
@@ -336,7 +344,7 @@ def main():
     def step():
         idx = mk.build(X, cfg.levels, cfg.iters, inits, flags=flags, comm=comm, n_global=n_global,
                        row_offset=rank * n_local, stream=stream)
-        ids, d2 = idx.query(Q, knn=cfg.knn, beam=1, stream=stream, out=qout)
+        ids, d2 = idx.query(Q, knn=cfg.knn, beam=beam, stream=stream, out=qout)
         return idx, ids, d2
 
     def barrier():
@@ -369,7 +377,7 @@ def main():
         idx = mk.build(X, cfg.levels, cfg.iters, inits, flags=flags, comm=comm, n_global=n_global,
                        row_offset=rank * n_local, stream=stream)
         e1.record(stream)
-        ids, d2 = idx.query(Q, knn=cfg.knn, beam=1, stream=stream, out=qout)
+        ids, d2 = idx.query(Q, knn=cfg.knn, beam=beam, stream=stream, out=qout)
         e2.record(stream)
         barrier()
         step_ms.append(e0.elapsed_time(e2))
@@ -479,7 +487,7 @@ def main():
             torch.cuda.synchronize(dev)
             t0 = time.perf_counter()
             idx_h = mk.build(Xp, cfg.levels, cfg.iters, inits, stream=stream)
-            ids_h, d2_h = idx_h.query(Qp, knn=cfg.knn, beam=1, stream=stream)
+            ids_h, d2_h = idx_h.query(Qp, knn=cfg.knn, beam=beam, stream=stream)
             torch.cuda.synchronize(dev)
             if s > 0:
                 h_ms.append((time.perf_counter() - t0) * 1000.0)
@@ -504,7 +512,7 @@ def main():
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": cfg.name, "n_per_gpu": n_local, "n_global": n_global, "dim": cfg.dim,
                        "levels": list(cfg.levels), "iters": cfg.iters, "queries": cfg.n_queries * world,
-                       "knn": cfg.knn, "beam": 1, "parallelism": f"dp{world}" if world > 1 else "single",
+                       "knn": cfg.knn, "beam": beam, "parallelism": f"dp{world}" if world > 1 else "single",
                        "l2": "flushed between timed steps (512 MiB write)"},
             "per_level_distances": per_level, "build_ms": statistics.mean(build_ms),
             "query_ms": statistics.mean(query_ms),
