@@ -65,8 +65,10 @@ enum {
   MASK_TIME_KERNELS = 1 << 5,    /* record CUDA-event device times of the step kernels        */
   MASK_NO_SORT = 1 << 6,         /* small d: keep the data order in K1 (no per-pass label sort) */
   MASK_NO_FUSED = 1 << 7,        /* small levels: per-pass kernels instead of the fused loop    */
-  MASK_TIME_ASSIGN = 1 << 8      /* like MASK_TIME_KERNELS for the assignment class only (one
+  MASK_TIME_ASSIGN = 1 << 8,     /* like MASK_TIME_KERNELS for the assignment class only (one
                                     event pair per pass: the cheapest live kernel timing)      */
+  MASK_NO_PARTITION_COPY = 1 << 9 /* dense: skip the partition-ordered copy of the rows that
+                                    mask_query's leaf scans read (saves n*dim floats)          */
 };
 
 /* kernel classes of mask_get_timing */

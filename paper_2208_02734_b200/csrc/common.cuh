@@ -236,7 +236,12 @@ struct QIndex {
   const uint8_t* routed = nullptr;
   int64_t rstride = 0;
   int64_t id_base = 0;
+  // dense data rows in level-1 partition order (Xp[pos] = X[members_1[pos]]), or nullptr: leaf
+  // scans then read contiguous rows at addresses known before the member ids arrive
+  const float* Xp = nullptr;
 };
+// Xp[pos * d ...] = X[members[pos] * d ...] for pos < n (the partition-ordered copy of the rows)
+void launch_gather_partition(const float* X, int d, const int32_t* members, int64_t n, float* Xp, cudaStream_t st);
 // K13 range search: cover radii (cover[l] = k_l float bits) and the multi-path descent; returns
 // the number of results, writing them (sorted by query, d^2, id) and per-query counts only when
 // ids_out != nullptr and the count fits cap_out.

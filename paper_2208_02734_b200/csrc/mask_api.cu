@@ -189,6 +189,7 @@ struct mask_index {
   const int32_t* col = nullptr;
   const float* val = nullptr;
   DevBuf<float> own_X, own_val;
+  DevBuf<float> Xpart;  // dense rows in level-1 partition order (leaf scans of mask_query)
   DevBuf<int64_t> own_rp;
   DevBuf<int32_t> own_col;
   std::vector<Level> levels;
@@ -924,6 +925,12 @@ void build_impl(const mask_matrix* data, const mask_build_params* p, mask_comm* 
     launch_children(L.labels.p, L.n_items, L.k, L.offsets.p, L.members.p, cursor.p, st);
     MASK_CUDA(cudaStreamSynchronize(st));
   }
+  // ---- dense rows in level-1 partition order for the leaf scans (one gather, n x d floats)
+  if (idx->format == MASK_DENSE_F32 && !(p->flags & MASK_NO_PARTITION_COPY)) {
+    idx->Xpart.alloc((size_t)N * d);
+    launch_gather_partition(idx->X, d, idx->levels[0].members.p, N, idx->Xpart.p, st);
+    MASK_CUDA(cudaStreamSynchronize(st));
+  }
   if (idx->format == MASK_CSR_F32) {
     // ||c||^2 per level for sparse queries
     int64_t tot = 0;
@@ -1258,6 +1265,12 @@ int32_t mask_insert(mask_index* idx, const mask_matrix* points, int64_t* partiti
     L1.offsets = std::move(off);
     L1.members = std::move(mem);
     L1.n_items = n + m;
+    if (idx->Xpart.p) {  // the partitions changed: re-gather the partition-ordered rows
+      DevBuf<float> xp((size_t)(n + m) * d);
+      launch_gather_partition(idx->X, d, L1.members.p, n + m, xp.p, st);
+      MASK_CUDA(cudaStreamSynchronize(st));
+      idx->Xpart = std::move(xp);
+    }
     std::lock_guard<std::mutex> lock(idx->cover_mu);
     idx->cover_valid = false;
   });
@@ -1329,6 +1342,7 @@ int32_t query_impl(const mask_index* idx, const mask_matrix* queries, int32_t k_
     qi.routed = routed;
     qi.rstride = rstride;
     qi.id_base = id_base;
+    qi.Xp = idx->Xpart.p;
     if (idx->format == MASK_DENSE_F32)
       launch_query_dense(qi, Qv, nq, k_nn, beam, ids, d2, st);
     else

@@ -268,7 +268,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
         for (int64_t m = m0; m < m1; m += 32) {
           const int64_t mm = m + lane;
           const int32_t cid = mm < m1 ? (int32_t)L1.members[mm] : PAD_ID;
-          top.offer(coop_dist<LPC>(q, qi.X, d, cid, lane), cid, lane);
+          // partition-ordered rows: the row address is the position itself (no wait on the id)
+          const float cd = qi.Xp ? coop_dist<LPC>(q, qi.Xp, d, mm < m1 ? (int32_t)mm : PAD_ID, lane)
+                                 : coop_dist<LPC>(q, qi.X, d, cid, lane);
+          top.offer(cd, cid, lane);
         }
       }
     }
@@ -278,6 +281,21 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
       d2_out[qid * knn + lane] = pad ? INFINITY : top.d;
     }
   }
+}
+
+__global__ void k_gather_partition(const float* __restrict__ X, int d, const int32_t* __restrict__ members, int64_t n,
+                                   float* __restrict__ Xp) {
+  const int64_t total = n * d;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t pos = e / d;
+    Xp[e] = __ldg(X + (int64_t)members[pos] * d + (e - pos * d));
+  }
+}
+
+void launch_gather_partition(const float* X, int d, const int32_t* members, int64_t n, float* Xp, cudaStream_t st) {
+  if (n <= 0) return;
+  k_gather_partition<<<grid_for(n * d, 256, (int64_t)num_sms() * 32), 256, 0, st>>>(X, d, members, n, Xp);
+  MASK_LAUNCH_CHECK();
 }
 
 void launch_query_dense(const QIndex& qi, const float* Q, int64_t nq, int knn, int beam,
