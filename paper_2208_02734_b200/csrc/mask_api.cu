@@ -921,15 +921,15 @@ void build_impl(const mask_matrix* data, const mask_build_params* p, mask_comm* 
   for (auto& L : idx->levels) {
     L.offsets.alloc(L.k + 1);
     L.members.alloc(std::max<int64_t>(L.n_items, 1));
+    // (the cursor block may return to the pool at once: the pool hands it only to later work
+    // on this stream, which runs after these kernels)
     DevBuf<int32_t> cursor(L.k);
     launch_children(L.labels.p, L.n_items, L.k, L.offsets.p, L.members.p, cursor.p, st);
-    MASK_CUDA(cudaStreamSynchronize(st));
   }
   // ---- dense rows in level-1 partition order for the leaf scans (one gather, n x d floats)
   if (idx->format == MASK_DENSE_F32 && !(p->flags & MASK_NO_PARTITION_COPY)) {
     idx->Xpart.alloc((size_t)N * d);
     launch_gather_partition(idx->X, d, idx->levels[0].members.p, N, idx->Xpart.p, st);
-    MASK_CUDA(cudaStreamSynchronize(st));
   }
   if (idx->format == MASK_CSR_F32) {
     // ||c||^2 per level for sparse queries
