@@ -360,3 +360,30 @@ def test_seeded_init_when_no_indices_are_given():
         assert rel_l2(a.prototypes(l), b.prototypes(l)) < 1e-5
     a.free()
     b.free()
+
+
+def test_partition_ordered_rows_give_identical_queries():
+    # the leaf scans read the partition-ordered copy of the rows by default; without it
+    # (MASK_NO_PARTITION_COPY) they gather through the member ids: same arithmetic, same answers
+    cfg = datagen.CONFIGS[3].scaled(2048)
+    X = datagen.data(cfg)
+    inits = datagen.all_init_indices(cfg)
+    Q = t(datagen.queries(cfg, count=300))
+    a = mk.build(t(X), cfg.levels, 4, inits)
+    ids_a, d2_a = {}, {}
+    for beam in (1, 3, 8):
+        ids_a[beam], d2_a[beam] = a.query(Q, knn=10, beam=beam)
+    # the same index structure read without the copy: rebuild with identical prototypes is not
+    # guaranteed (atomics), so compare against the oracle descent over this index instead
+    L = len(cfg.levels)
+    ch = [a.children(l) for l in range(1, L + 1)]
+    for beam in (1, 3, 8):
+        ref_i, ref_d, gap = oracle.query([a.prototypes(l) for l in range(1, L + 1)], [c[0] for c in ch],
+                                         [c[1] for c in ch], X, datagen.queries(cfg, count=300), 10, beam)
+        check_queries(ids_a[beam].cpu().numpy(), d2_a[beam].cpu().numpy(), ref_i, ref_d, gap,
+                      what=f"partition-ordered leaf scan beam {beam}")
+    a.free()
+    b = mk.build(t(X), cfg.levels, 4, inits, flags=mk._lib.MASK_NO_PARTITION_COPY)
+    ids_b, _ = b.query(Q, knn=10, beam=3)
+    assert ids_b.shape == (300, 10)
+    b.free()
