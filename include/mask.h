@@ -327,6 +327,10 @@ int32_t mask_get_children(const mask_index* idx, int32_t level, int64_t* host_of
  * of passes written (<= cap) or < 0 on error. */
 int32_t mask_get_trace(const mask_index* idx, int32_t level, double* J, int64_t* changed,
                        int64_t* empties, int32_t cap);
+/* per assignment pass, like mask_get_trace: dmax_t = max_j ||c_j' - c_j|| of the update that
+ * followed it (the tolerance-stop quantity, D3; 0 when no update followed).  Returns the number
+ * of passes written or < 0 on error. */
+int32_t mask_get_displacement(const mask_index* idx, int32_t level, double* dmax, int32_t cap);
 
 /* ---------------------------------------------------------------- diagnostics
  * Cumulative number of CUDA kernel launches issued by this library in this process. */

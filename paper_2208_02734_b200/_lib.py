@@ -46,7 +46,7 @@ EXPORTS = [
     "mask_get_children", "mask_get_trace", "mask_kernel_launches", "mask_get_timing",
     "mask_grouped_depth", "mask_build_grouped", "mask_range_query", "mask_insert",
     "mask_top_prototypes", "mask_route", "mask_query_routed", "mask_merge", "mask_collective_count",
-    "mask_seeded_init", "mask_debug_fail_alloc",
+    "mask_seeded_init", "mask_debug_fail_alloc", "mask_get_displacement",
 ]
 
 
@@ -150,6 +150,7 @@ def load():
             "mask_collective_count": (i64, []),
             "mask_seeded_init": (i32, [C.c_uint64, i32, i64, i64, P]),
             "mask_debug_fail_alloc": (None, [i64]),
+            "mask_get_displacement": (i32, [P, i32, P, i32]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)

@@ -280,7 +280,11 @@ class Index:
         n = load().mask_get_trace(self.handle, level, J.ctypes.data, ch.ctypes.data, em.ctypes.data, cap)
         if n < 0:
             check(n)
-        return dict(J=J[:n], changed=ch[:n], empties=em[:n])
+        dm = np.zeros(cap, np.float64)
+        m = load().mask_get_displacement(self.handle, level, dm.ctypes.data, cap)
+        if m < 0:
+            check(m)
+        return dict(J=J[:n], changed=ch[:n], empties=em[:n], dmax=dm[:m])
 
     def timing(self, level: int) -> dict:
         """CUDA-event device times of the step kernels (build with MASK_TIME_KERNELS)."""

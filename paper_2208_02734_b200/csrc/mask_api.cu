@@ -159,6 +159,7 @@ struct Level {
   DevBuf<int32_t> members;    // n_items
   std::vector<double> J;
   std::vector<int64_t> changed, empties;
+  std::vector<double> dmax;  // per pass: max_j ||c_j' - c_j|| of the update that followed
   int updates = 0;
   double t_ms[MASK_T_NCLASS] = {0, 0, 0, 0};
   int64_t t_count[MASK_T_NCLASS] = {0, 0, 0, 0};
@@ -620,11 +621,15 @@ void run_level(const Input& in, int64_t k, const int64_t* init_idx_host, const m
     L.changed.push_back((int64_t)hch[t]);
     const bool updated = !(t > 0 && hch[t] == 0);  // a no-change pass stops before its update
     L.empties.push_back(updated ? (int64_t)hfin[2 * t + 1] : 0);
+    float d2max;
+    std::memcpy(&d2max, &hfin[2 * t], sizeof(d2max));
+    L.dmax.push_back(updated ? std::sqrt((double)d2max) : 0.0);
     updates += updated ? 1 : 0;
   }
   L.J.push_back(hJ[T + 1]);
   L.changed.push_back((int64_t)hch[T + 1]);
   L.empties.push_back(0);
+  L.dmax.push_back(0.0);
   L.updates = updates;
   if (p->iter_cb) emit_cb(loop_passes, P_snap.p, ws.lab_cur.p);
   L.labels = std::move(ws.lab_cur);
@@ -1609,6 +1614,18 @@ int32_t mask_get_trace(const mask_index* idx, int32_t level, double* J, int64_t*
       if (changed) changed[t] = L.changed[t];
       if (empties) empties[t] = t < (int32_t)L.empties.size() ? L.empties[t] : 0;
     }
+    written = np;
+  });
+  return rc == MASK_OK ? written : rc;
+}
+
+int32_t mask_get_displacement(const mask_index* idx, int32_t level, double* dmax, int32_t cap) {
+  int32_t written = 0;
+  const int32_t rc = guarded([&] {
+    const Level& L = level_of(idx, level);
+    MASK_REQUIRE(cap >= 0 && dmax != nullptr, MASK_ERR_ARG, "cap < 0 or NULL output");
+    const int32_t np = (int32_t)std::min<size_t>(L.dmax.size(), (size_t)cap);
+    for (int32_t t = 0; t < np; ++t) dmax[t] = L.dmax[t];
     written = np;
   });
   return rc == MASK_OK ? written : rc;

@@ -387,3 +387,22 @@ def test_partition_ordered_rows_give_identical_queries():
     ids_b, _ = b.query(Q, knn=10, beam=3)
     assert ids_b.shape == (300, 10)
     b.free()
+
+
+def test_displacement_trace_matches_the_prototype_steps():
+    # mask_get_displacement: dmax_t = max_j ||c_j^(t+1) - c_j^(t)|| (the tolerance-stop
+    # quantity, D3), checked against the prototypes the step hook exported for every pass
+    cfg = datagen.CONFIGS[2].scaled(256)
+    X = datagen.data(cfg)
+    seen = {}
+    idx = mk.build(t(X), cfg.levels, 6, datagen.all_init_indices(cfg),
+                   iter_cb=lambda l, p, P, lab: seen.__setitem__((l, p), P.astype(np.float64)))
+    for lv in range(1, len(cfg.levels) + 1):
+        tr = idx.trace(lv)
+        passes = sorted(p for (l, p) in seen if l == lv)
+        assert len(tr["dmax"]) == len(tr["J"]) == len(passes)
+        for p in passes[:-1]:
+            ref = np.sqrt(((seen[(lv, p + 1)] - seen[(lv, p)]) ** 2).sum(axis=1)).max()
+            assert abs(tr["dmax"][p] - ref) <= 1e-5 * ref + 1e-6, (lv, p, tr["dmax"][p], ref)
+        assert tr["dmax"][passes[-1]] == 0.0
+    idx.free()
