@@ -406,3 +406,15 @@ def test_displacement_trace_matches_the_prototype_steps():
             assert abs(tr["dmax"][p] - ref) <= 1e-5 * ref + 1e-6, (lv, p, tr["dmax"][p], ref)
         assert tr["dmax"][passes[-1]] == 0.0
     idx.free()
+
+
+@pytest.mark.parametrize("knn,beam", [(32, 32), (1, 32), (32, 1), (17, 5)])
+def test_query_limits_match_the_oracle(knn, beam):
+    # the largest k_nn and beam the ABI accepts (32 each), ragged values, over a 3-level index
+    # with small partitions (answers padded where a partition holds fewer than k_nn rows)
+    cfg = datagen.CONFIGS[3].scaled(4096)
+    X = datagen.data(cfg)
+    idx = mk.build(t(X), cfg.levels, 5, datagen.all_init_indices(cfg))
+    Q = datagen.queries(cfg, count=120)
+    _query_parity(idx, X, Q, cfg.levels, knn=knn, beam=beam)
+    idx.free()
