@@ -183,3 +183,25 @@ def test_dist_cluster_nccl_single_rank():
                         "--master-addr", "127.0.0.1", "--master-port", str(port),
                         os.path.join(here, "_dist_cluster_main.py")], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "DIST_CLUSTER_OK" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
+
+
+def test_merge_at_the_node_limit():
+    # 64 nodes (the K14 merge limit) with random sorted answers: (d^2, node, id) merge = a
+    # host sort of the union
+    rng = np.random.default_rng(5)
+    W, nq, k = 64, 40, 7
+    d2 = np.sort(rng.integers(0, 30, size=(W, nq, k)).astype(np.float32), axis=2)
+    ids = rng.integers(0, 10**6, size=(W, nq, k)).astype(np.int64)
+    ids[:, :, -1] = np.where(rng.random((W, nq)) < 0.3, -1, ids[:, :, -1])
+    d2 = np.where(ids < 0, np.inf, d2).astype(np.float32)
+    for n in range(W):  # every node's answer sorted by (d^2, id), padding last (the contract)
+        for q in range(nq):
+            o = np.lexsort((np.where(ids[n, q] < 0, np.iinfo(np.int64).max, ids[n, q]), d2[n, q]))
+            ids[n, q], d2[n, q] = ids[n, q][o], d2[n, q][o]
+    mi, md = mk.merge(t(ids), t(d2))
+    mi, md = mi.cpu().numpy(), md.cpu().numpy()
+    for q in range(nq):
+        cand = sorted((float(d2[n, q, r]), n, int(ids[n, q, r])) for n in range(W) for r in range(k) if ids[n, q, r] >= 0)
+        ref = cand[:k]
+        assert [c[2] for c in ref] == mi[q][:len(ref)].tolist()
+        assert np.allclose([c[0] for c in ref], md[q][:len(ref)])

@@ -418,3 +418,14 @@ def test_query_limits_match_the_oracle(knn, beam):
     Q = datagen.queries(cfg, count=120)
     _query_parity(idx, X, Q, cfg.levels, knn=knn, beam=beam)
     idx.free()
+
+
+def test_sparse_queries_with_a_beam():
+    rp, col, val = datagen.random_csr(410, 2500, 700, 14)
+    inits = [datagen.init_indices(411, 1, 2500, 48), datagen.init_indices(411, 2, 48, 6)]
+    idx = mk.build(_csr_dev(rp, col, val, 700), [48, 6], 5, inits)
+    qrp, qcol, qval = datagen.random_csr(412, 80, 700, 14)
+    for beam in (2, 6):
+        _query_parity(idx, (rp, col, val), (qrp, qcol, qval), [48, 6], knn=10, beam=beam,
+                      Qdev=_csr_dev(qrp, qcol, qval, 700), csr=True, dim=700)
+    idx.free()
