@@ -36,6 +36,7 @@ def main():
     ap.add_argument("--clean", action="store_true",
                     help="time one clean build (no step hook, no checks) and the 1e6-query batch")
     ap.add_argument("--recall-sample", type=int, default=20)
+    ap.add_argument("--beams", default="1", help="--clean: beam widths of the query batch")
     a = ap.parse_args()
     cfg = datagen.CONFIGS[5]
     t0 = time.time()
@@ -132,20 +133,22 @@ def clean(a, cfg, X, Xd, inits):
     print(f"C5 build (T={a.T}): {build_s:.1f} s, {tot:.3e} distances, {tot / build_s:.3e} distances/s", flush=True)
     Q = datagen.queries(cfg)
     Qd = torch.from_numpy(Q).to("cuda:0")
-    ms = []
-    for _ in range(3):
-        e1.record(st)
-        ids, d2 = idx.query(Qd, knn=cfg.knn, beam=1, stream=st)
-        e2.record(st)
-        torch.cuda.synchronize()
-        ms.append(e1.elapsed_time(e2))
-    qms = min(ms)
     m = a.recall_sample
     t0 = time.time()
     eids, _, _ = oracle.knn_exact(X, Q[:m], cfg.knn)
-    rec = oracle.recall(ids[:m].cpu().numpy(), eids)
-    print(f"query: {Q.shape[0]} queries in {qms:.1f} ms = {Q.shape[0] / qms * 1e3:.3e} QPS, recall@{cfg.knn} "
-          f"{rec:.3f} on {m} queries (exact k-NN on the host {time.time() - t0:.0f} s)", flush=True)
+    print(f"exact k-NN of {m} queries on the host: {time.time() - t0:.0f} s", flush=True)
+    for beam in [int(b) for b in a.beams.split(",")]:
+        ms = []
+        for _ in range(3):
+            e1.record(st)
+            ids, d2 = idx.query(Qd, knn=cfg.knn, beam=beam, stream=st)
+            e2.record(st)
+            torch.cuda.synchronize()
+            ms.append(e1.elapsed_time(e2))
+        qms = min(ms)
+        rec = oracle.recall(ids[:m].cpu().numpy(), eids)
+        print(f"query beam {beam}: {Q.shape[0]} queries in {qms:.1f} ms = {Q.shape[0] / qms * 1e3:.3e} QPS, "
+              f"recall@{cfg.knn} {rec:.3f} on {m} queries", flush=True)
     idx.free()
 
 
