@@ -1,0 +1,46 @@
+"""§5.1 relocation and rebuild on one B200 (Table 1's experiment): the
+error rate after the first grouped build and after each relocation rebuild, with the time of
+each iteration (build + exhaustive point search), for overlapping and separated clouds.
+
+    python tools/relocation_bench.py [--iterations 8]
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import datagen  # noqa: E402
+from paper_2208_02734_b200.relocate import relocate_and_rebuild  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--iterations", type=int, default=8)
+    a = ap.parse_args()
+    for name, per, R, sig in (("GRO-like overlap", 200, 12.0, 2.0), ("GNO-like separated", 200, 40.0, 1.0),
+                              ("overlap, 80k points", 10000, 12.0, 2.0)):
+        X = datagen.gaussian_clouds(5, per, radius=R, sigma=sig)
+        perm = datagen.group_perm(5, X.shape[0])
+        Xd = torch.from_numpy(X).cuda()
+        times = []
+
+        def hook(i, order, idx, found, reached):
+            torch.cuda.synchronize()
+            times.append(time.time())
+
+        t0 = time.time()
+        errs = relocate_and_rebuild(Xd, 16, 8, 10, perm, a.iterations,
+                                    lambda i, n: datagen.relocation_keys(100, i, n), hook=hook)
+        per_iter = [round(b - a_, 4) for a_, b in zip([t0] + times[:-1], times)]
+        print(json.dumps({"data": name, "points": int(X.shape[0]), "length_group": 16, "n_centroids": 8,
+                          "error_rate_per_iteration": [round(e, 4) for e in errs],
+                          "best_iteration": int(min(range(len(errs)), key=errs.__getitem__)),
+                          "seconds_per_iteration": per_iter}), flush=True)
+
+
+if __name__ == "__main__":
+    main()
