@@ -67,8 +67,13 @@ enum {
   MASK_NO_FUSED = 1 << 7,        /* small levels: per-pass kernels instead of the fused loop    */
   MASK_TIME_ASSIGN = 1 << 8,     /* like MASK_TIME_KERNELS for the assignment class only (one
                                     event pair per pass: the cheapest live kernel timing)      */
-  MASK_NO_PARTITION_COPY = 1 << 9 /* dense: skip the partition-ordered copy of the rows that
+  MASK_NO_PARTITION_COPY = 1 << 9, /* dense: skip the partition-ordered copy of the rows that
                                     mask_query's leaf scans read (saves n*dim floats)          */
+  MASK_TRACE_PASSES = 1 << 10    /* keep, per level, the prototypes every assignment pass used
+                                    and the labels it produced, on the device, read back with
+                                    mask_get_pass (parity tests of the production path: unlike
+                                    iter_cb it changes no kernel choice and adds no host sync;
+                                    costs (T+1) x (n_items + k*dim) words per level)          */
 };
 
 /* kernel classes of mask_get_timing */
@@ -331,6 +336,13 @@ int32_t mask_get_trace(const mask_index* idx, int32_t level, double* J, int64_t*
  * followed it (the tolerance-stop quantity, D3; 0 when no update followed).  Returns the number
  * of passes written or < 0 on error. */
 int32_t mask_get_displacement(const mask_index* idx, int32_t level, double* dmax, int32_t cap);
+
+/* per assignment pass of a build made with MASK_TRACE_PASSES (pass = 0 .. passes-1 as in
+ * mask_level_info, the last one being the final assignment): P_host (k x dim fp32, may be NULL)
+ * receives the prototypes the pass used and labels_host (may be NULL) the labels it produced
+ * for this rank's items of the level.  MASK_ERR_ARG on a bad level / pass, MASK_ERR_UNSUPPORTED
+ * when the build did not keep the trace. */
+int32_t mask_get_pass(const mask_index* idx, int32_t level, int32_t pass, float* P_host, int32_t* labels_host);
 
 /* ---------------------------------------------------------------- diagnostics
  * Cumulative number of CUDA kernel launches issued by this library in this process. */

@@ -81,6 +81,9 @@ def lib():
             L.orc_lloyd.argtypes = [C.c_int64, C.c_int, dp] + lloyd_args
             L.orc_lloyd_csr.restype = C.c_int
             L.orc_lloyd_csr.argtypes = [C.c_int64, C.c_int, i64p, i32p, dp] + lloyd_args
+            L.orc_lloyd_trace.restype = C.c_int
+            L.orc_lloyd_trace.argtypes = [C.c_int64, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p] + \
+                lloyd_args + [dp, i32p]
             _lib = L
         return _lib
 
@@ -186,16 +189,22 @@ def seeded_init(seed: int, level: int, n: int, k: int) -> np.ndarray:
 
 # ------------------------------------------------------------------ Lloyd / build
 class LevelResult:
-    def __init__(self, P, labels, J, changed, updates):
+    def __init__(self, P, labels, J, changed, updates, passes=None):
         self.P = P
         self.labels = labels
         self.J = J
         self.changed = changed
         self.updates = updates
+        self.passes = passes  # trace=True: [(P_t used by pass t, labels_t), ...] incl. the final pass
 
 
-def lloyd(Y, init_idx, T: int, tol: float = 0.0, csr_dim: Optional[int] = None) -> LevelResult:
-    """One level: Lloyd from Y[init_idx], T iterations, then a final assignment."""
+def lloyd(Y, init_idx, T: int, tol: float = 0.0, csr_dim: Optional[int] = None, trace: bool = False) -> LevelResult:
+    """One level: Lloyd from Y[init_idx], T iterations, then a final assignment.
+
+    trace=True also records, per assignment pass, the prototypes it used and its labels
+    (an output copy only: the arithmetic is the same code path)."""
+    if trace:
+        return _lloyd_trace(Y, init_idx, T, tol, csr_dim)
     init_idx = np.ascontiguousarray(init_idx, np.int64)
     k = init_idx.size
     J = np.zeros(T + 1, np.float64)
@@ -214,6 +223,32 @@ def lloyd(Y, init_idx, T: int, tol: float = 0.0, csr_dim: Optional[int] = None) 
         lab = np.empty(n, np.int32)
         passes = lib().orc_lloyd_csr(n, d, rp, col, val, k, init_idx, T, tol, P, lab, J, ch, C.byref(upd))
     return LevelResult(P, lab, J[:passes], ch[:passes], upd.value)
+
+
+def _lloyd_trace(Y, init_idx, T, tol, csr_dim):
+    init_idx = np.ascontiguousarray(init_idx, np.int64)
+    k = init_idx.size
+    J = np.zeros(T + 1, np.float64)
+    ch = np.zeros(T + 1, np.int64)
+    upd = C.c_int(0)
+    if csr_dim is None:
+        Y = _f64(Y)
+        n, d = Y.shape
+        args = (Y.ctypes.data, None, None, None)
+        keep = (Y,)
+    else:
+        rp, col, val = _csr(Y)
+        n, d = rp.size - 1, csr_dim
+        args = (None, rp.ctypes.data, col.ctypes.data, val.ctypes.data)
+        keep = (rp, col, val)
+    P = np.empty((k, d), np.float64)
+    lab = np.empty(n, np.int32)
+    Pp = np.empty((T + 1, k, d), np.float64)
+    Lp = np.empty((T + 1, max(n, 1)), np.int32)
+    passes = lib().orc_lloyd_trace(n, d, *args, k, init_idx, T, tol, P, lab, J, ch, C.byref(upd), Pp, Lp)
+    del keep
+    seq = [(Pp[t], Lp[t, :n]) for t in range(passes)]
+    return LevelResult(P, lab, J[:passes], ch[:passes], upd.value, passes=seq)
 
 
 def children(labels, k: int) -> Tuple[np.ndarray, np.ndarray]:
@@ -240,13 +275,14 @@ class Index:
         return [lv.P for lv in self.levels]
 
 
-def build_index(X, init_idx: Sequence[np.ndarray], T: int, tol: float = 0.0, csr_dim: Optional[int] = None) -> Index:
+def build_index(X, init_idx: Sequence[np.ndarray], T: int, tol: float = 0.0, csr_dim: Optional[int] = None,
+                trace: bool = False) -> Index:
     """Bottom-up levels: level 1 clusters X, level l+1 clusters P_l (D1, D6)."""
     levels, offs, mems = [], [], []
     Y = X
     dim = csr_dim
     for l, idx in enumerate(init_idx):
-        res = lloyd(Y, idx, T, tol, csr_dim=csr_dim if l == 0 else None)
+        res = lloyd(Y, idx, T, tol, csr_dim=csr_dim if l == 0 else None, trace=trace)
         levels.append(res)
         o, m = children(res.labels, res.P.shape[0])
         offs.append(o)

@@ -220,7 +220,7 @@ static int lloyd_impl(int64_t n, int d, const double* Y, const int64_t* row_ptr,
                       const int32_t* col, const double* val, int64_t k,
                       const int64_t* init_idx, int T, double tol, double* P_out,
                       int32_t* labels_out, double* J_trace, int64_t* changed_trace,
-                      int* updates_run) {
+                      int* updates_run, double* P_pass, int32_t* lab_pass) {
   double* P = P_out;
   double* P_new = (double*)malloc(sizeof(double) * (size_t)(k * d));
   double* S = (double*)malloc(sizeof(double) * (size_t)(k * d));
@@ -244,6 +244,9 @@ static int lloyd_impl(int64_t n, int d, const double* Y, const int64_t* row_ptr,
   for (int t = 0; t < T; ++t) {
     if (Y) orc_assign(n, d, Y, k, P, a, best, NULL);
     else orc_assign_csr(n, d, row_ptr, col, val, k, P, a, best, NULL);
+    /* optional per-pass record (output only): the prototypes this pass used, its labels */
+    if (P_pass) memcpy(P_pass + (size_t)passes * (size_t)(k * d), P, sizeof(double) * (size_t)(k * d));
+    if (lab_pass) memcpy(lab_pass + (size_t)passes * (size_t)n, a, sizeof(int32_t) * (size_t)n);
     double J = 0.0;
     int64_t changed = 0;
     for (int64_t i = 0; i < n; ++i) {
@@ -266,6 +269,8 @@ static int lloyd_impl(int64_t n, int d, const double* Y, const int64_t* row_ptr,
   /* final assignment with the final prototypes */
   if (Y) orc_assign(n, d, Y, k, P, labels_out, best, NULL);
   else orc_assign_csr(n, d, row_ptr, col, val, k, P, labels_out, best, NULL);
+  if (P_pass) memcpy(P_pass + (size_t)passes * (size_t)(k * d), P, sizeof(double) * (size_t)(k * d));
+  if (lab_pass) memcpy(lab_pass + (size_t)passes * (size_t)n, labels_out, sizeof(int32_t) * (size_t)n);
   {
     double J = 0.0;
     int64_t changed = 0;
@@ -291,7 +296,18 @@ int orc_lloyd(int64_t n, int d, const double* Y, int64_t k, const int64_t* init_
               double tol, double* P_out, int32_t* labels_out, double* J_trace,
               int64_t* changed_trace, int* updates_run) {
   return lloyd_impl(n, d, Y, NULL, NULL, NULL, k, init_idx, T, tol, P_out, labels_out, J_trace,
-                    changed_trace, updates_run);
+                    changed_trace, updates_run, NULL, NULL);
+}
+
+/* orc_lloyd / orc_lloyd_csr with a per-pass record: P_pass ((T+1) x k x d) receives the
+ * prototypes each assignment pass used, lab_pass ((T+1) x n) the labels it produced (pass
+ * index = position in J_trace; the final assignment is the last one).  Either may be NULL. */
+int orc_lloyd_trace(int64_t n, int d, const double* Y, const int64_t* row_ptr, const int32_t* col,
+                    const double* val, int64_t k, const int64_t* init_idx, int T, double tol,
+                    double* P_out, int32_t* labels_out, double* J_trace, int64_t* changed_trace,
+                    int* updates_run, double* P_pass, int32_t* lab_pass) {
+  return lloyd_impl(n, d, Y, row_ptr, col, val, k, init_idx, T, tol, P_out, labels_out, J_trace,
+                    changed_trace, updates_run, P_pass, lab_pass);
 }
 
 int orc_lloyd_csr(int64_t n, int d, const int64_t* row_ptr, const int32_t* col,
@@ -299,7 +315,7 @@ int orc_lloyd_csr(int64_t n, int d, const int64_t* row_ptr, const int32_t* col,
                   double* P_out, int32_t* labels_out, double* J_trace, int64_t* changed_trace,
                   int* updates_run) {
   return lloyd_impl(n, d, NULL, row_ptr, col, val, k, init_idx, T, tol, P_out, labels_out,
-                    J_trace, changed_trace, updates_run);
+                    J_trace, changed_trace, updates_run, NULL, NULL);
 }
 
 /* ------------------------------------------------------------------ query */

@@ -16,6 +16,7 @@ from ._lib import (
     MASK_NO_SORT,
     MASK_TIME_ASSIGN,
     MASK_TIME_KERNELS,
+    MASK_TRACE_PASSES,
     MASK_VALIDATE_FINITE,
     MaskError,
 )
@@ -26,4 +27,5 @@ __all__ = [
     "update", "route", "merge", "collective_count", "seeded_init", "row_range",
     "query_range", "MaskError", "MASK_BORROW_DATA", "MASK_FORCE_SIMT", "MASK_NO_FIXUP",
     "MASK_VALIDATE_FINITE", "MASK_TIME_KERNELS", "MASK_TIME_ASSIGN", "MASK_NO_SORT", "MASK_NO_FUSED",
+    "MASK_TRACE_PASSES",
 ]

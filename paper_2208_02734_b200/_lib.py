@@ -35,6 +35,7 @@ MASK_NO_SORT = 1 << 6
 MASK_NO_FUSED = 1 << 7
 MASK_TIME_ASSIGN = 1 << 8
 MASK_NO_PARTITION_COPY = 1 << 9
+MASK_TRACE_PASSES = 1 << 10
 MASK_RANGE_PAPER, MASK_RANGE_COVER = 0, 1
 T_ASSIGN, T_FIXUP, T_UPDATE, T_FINALIZE = 0, 1, 2, 3
 
@@ -46,7 +47,7 @@ EXPORTS = [
     "mask_get_children", "mask_get_trace", "mask_kernel_launches", "mask_get_timing",
     "mask_grouped_depth", "mask_build_grouped", "mask_range_query", "mask_insert",
     "mask_top_prototypes", "mask_route", "mask_query_routed", "mask_merge", "mask_collective_count",
-    "mask_seeded_init", "mask_debug_fail_alloc", "mask_get_displacement",
+    "mask_seeded_init", "mask_debug_fail_alloc", "mask_get_displacement", "mask_get_pass",
 ]
 
 
@@ -151,6 +152,7 @@ def load():
             "mask_seeded_init": (i32, [C.c_uint64, i32, i64, i64, P]),
             "mask_debug_fail_alloc": (None, [i64]),
             "mask_get_displacement": (i32, [P, i32, P, i32]),
+            "mask_get_pass": (i32, [P, i32, i32, P, P]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)

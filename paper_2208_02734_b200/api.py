@@ -286,6 +286,18 @@ class Index:
             check(m)
         return dict(J=J[:n], changed=ch[:n], empties=em[:n], dmax=dm[:m])
 
+    def pass_trace(self, level: int, pass_: int) -> Tuple[np.ndarray, np.ndarray]:
+        """mask_get_pass (build with MASK_TRACE_PASSES): (P used by the pass, labels it produced)."""
+        info = self.level_info(level)
+        P = np.empty((info["k"], info["dim"]), np.float32)
+        lab = np.empty(max(info["n_items"], 1), np.int32)
+        check(load().mask_get_pass(self.handle, level, int(pass_), P.ctypes.data, lab.ctypes.data))
+        return P, lab[: info["n_items"]]
+
+    def passes(self, level: int) -> List[Tuple[np.ndarray, np.ndarray]]:
+        """Every assignment pass of a level (MASK_TRACE_PASSES builds): [(P_t, labels_t), ...]."""
+        return [self.pass_trace(level, t) for t in range(self.level_info(level)["passes"])]
+
     def timing(self, level: int) -> dict:
         """CUDA-event device times of the step kernels (build with MASK_TIME_KERNELS)."""
         out = np.zeros(9, np.float64)

@@ -131,7 +131,8 @@ void launch_label_sort(const int32_t* labels, int64_t n, int64_t k, const int32_
 bool small_level_supported(int64_t n, int d, int64_t k);
 void launch_small_level(const float* Y, int64_t n, int d, int64_t k, float* P, int32_t* lab, int32_t* prev,
                         float* best, double* S, int32_t* counts, double* J, unsigned long long* changed,
-                        uint32_t* fin, int* ctrl, unsigned* bar_ws, int T, double tol, cudaStream_t st);
+                        uint32_t* fin, int* ctrl, unsigned* bar_ws, int T, double tol, cudaStream_t st,
+                        float* P_trace = nullptr, int32_t* lab_trace = nullptr);
 // K12: one layer of the grouped construction (Algorithm 1): g groups of the n_items rows of Y
 // (through perm when given), nc prototypes each, T Lloyd iterations per group; P_out = g*nc x d
 // (group-major), labels[row] = global prototype id.

@@ -33,9 +33,23 @@ std::atomic<int64_t> g_nccl_calls{0};  // every NCCL call the library issues (ma
 void mask::count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 // ------------------------------------------------------------------ caching device allocator
+// Blocks are recycled instead of cudaFree'd.  A block released while an API call's stream may
+// still be using it (a DevBuf leaving scope right after the launches that read it) carries an
+// event recorded on that stream at release: the same stream may take it again at once (stream
+// order), any other stream or thread only after the event has completed.  Blocks released
+// outside an API call (mask_free: nothing is in flight by the synchronous call contract) carry
+// no event.
 namespace {
 std::mutex g_pool_mu;
-std::multimap<size_t, void*> g_pool;  // size class -> free block
+struct FreeBlock {
+  void* p;
+  cudaStream_t st;  // stream whose pending work may still use the block (when ev != nullptr)
+  cudaEvent_t ev;   // recorded on st at release, or nullptr
+};
+std::multimap<size_t, FreeBlock> g_pool;  // size class -> free block
+std::vector<cudaEvent_t> g_event_cache;   // completed events for reuse (under g_pool_mu)
+thread_local bool g_have_stream = false;  // inside an API call that named its stream
+thread_local cudaStream_t g_cur_stream = nullptr;
 size_t size_class(size_t bytes) {
   if (bytes <= (1u << 20)) {  // small: next power of two >= 512 B
     size_t c = 512;
@@ -56,16 +70,25 @@ void* mask::pool_alloc(size_t bytes) {
   const size_t c = size_class(bytes);
   {
     std::lock_guard<std::mutex> g(g_pool_mu);
-    auto it = g_pool.find(c);
-    if (it != g_pool.end()) {
-      void* p = it->second;
+    auto range = g_pool.equal_range(c);
+    for (auto it = range.first; it != range.second; ++it) {
+      FreeBlock& b = it->second;
+      bool ready = b.ev == nullptr || (g_have_stream && b.st == g_cur_stream);
+      if (!ready) {
+        const cudaError_t q = cudaEventQuery(b.ev);
+        if (q == cudaErrorNotReady) continue;
+        cudaGetLastError();  // (an error here resurfaces at the caller's next CUDA call)
+        ready = true;
+      }
+      void* p = b.p;
+      if (b.ev) g_event_cache.push_back(b.ev);  // re-recorded before any later wait on it
       g_pool.erase(it);
       return p;
     }
   }
   void* p = nullptr;
   cudaError_t e = cudaMalloc(&p, c);
-  if (e == cudaErrorMemoryAllocation) {  // give the cache back and retry once
+  if (e == cudaErrorMemoryAllocation) {  // give the idle cache back and retry once
     cudaGetLastError();
     pool_trim();
     e = cudaMalloc(&p, c);
@@ -77,21 +100,61 @@ void* mask::pool_alloc(size_t bytes) {
 void mask::pool_free(void* p, size_t bytes) {
   if (!p) return;
   std::lock_guard<std::mutex> g(g_pool_mu);
-  g_pool.emplace(size_class(bytes), p);
+  FreeBlock b{p, g_cur_stream, nullptr};
+  if (g_have_stream) {
+    cudaEvent_t ev = nullptr;
+    if (!g_event_cache.empty()) {
+      ev = g_event_cache.back();
+      g_event_cache.pop_back();
+    } else if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) {
+      cudaGetLastError();
+      ev = nullptr;
+    }
+    if (ev && cudaEventRecord(ev, g_cur_stream) == cudaSuccess) {
+      b.ev = ev;
+    } else {  // no event: wait for the stream instead of handing out a block in use
+      cudaGetLastError();
+      if (ev) g_event_cache.push_back(ev);
+      cudaStreamSynchronize(g_cur_stream);
+      cudaGetLastError();
+    }
+  }
+  g_pool.emplace(size_class(bytes), b);
 }
 
 void mask::pool_trim() {
   std::lock_guard<std::mutex> g(g_pool_mu);
-  for (auto& kv : g_pool) cudaFree(kv.second);
-  g_pool.clear();
+  for (auto it = g_pool.begin(); it != g_pool.end();) {
+    FreeBlock& b = it->second;
+    if (b.ev && cudaEventQuery(b.ev) == cudaErrorNotReady) {  // still in use by a stream
+      ++it;
+      continue;
+    }
+    cudaGetLastError();
+    if (b.ev) g_event_cache.push_back(b.ev);
+    cudaFree(b.p);
+    it = g_pool.erase(it);
+  }
 }
 
 namespace {
 
 thread_local std::string g_err;
 
+// the stream the pool orders this thread's releases on (set by as_stream inside a call)
+struct StreamCtx {  // saved / restored so a nested entry point leaves the caller's context intact
+  bool have = g_have_stream;
+  cudaStream_t st = g_cur_stream;
+  StreamCtx() { g_have_stream = false; }
+  ~StreamCtx() {
+    g_have_stream = have;
+    g_cur_stream = st;
+  }
+};
+
 template <class F>
 int32_t guarded(F&& f) {
+  StreamCtx sc;
   try {
     g_err.clear();
     f();
@@ -164,6 +227,12 @@ struct Level {
   double t_ms[MASK_T_NCLASS] = {0, 0, 0, 0};
   int64_t t_count[MASK_T_NCLASS] = {0, 0, 0, 0};
   int assign_kernel = -1;  // 0 = K2 SIMT, 1 = K1 tcgen05 3xTF32, 2 = K3 CSR, 3 = K11 fused small level
+  // MASK_TRACE_PASSES: slot t < T = loop pass t, slot T = the final pass (T + 1 slots)
+  DevBuf<float> P_trace;        // (T+1) x k x dim
+  DevBuf<int32_t> lab_trace;    // (T+1) x n_items (this rank's items)
+  int trace_T = -1;             // T of the traced build (-1: no trace)
+  int trace_loop_passes = 0;    // loop passes run (the final pass follows them)
+  int64_t trace_n = 0;          // items per label slot
 };
 
 // A level's input rows as seen by this rank.
@@ -206,7 +275,12 @@ struct mask_index {
 
 namespace {
 
-cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+// The call's stream; also the stream the caching pool orders this thread's releases on.
+cudaStream_t as_stream(void* s) {
+  g_cur_stream = reinterpret_cast<cudaStream_t>(s);
+  g_have_stream = true;
+  return g_cur_stream;
+}
 
 void check_matrix(const mask_matrix* m, const char* what) {
   MASK_REQUIRE(m != nullptr, MASK_ERR_ARG, std::string(what) + ": NULL matrix");
@@ -469,6 +543,23 @@ void run_level(const Input& in, int64_t k, const int64_t* init_idx_host, const m
   MASK_CUDA(cudaMemsetAsync(ws.counts.p, 0, sizeof(int32_t) * k, st));
   MASK_CUDA(cudaMemsetAsync(ws.lab_prev.p, 0xff, sizeof(int32_t) * std::max<int64_t>(n, 1), st));
   const int* active = ctrl.p;
+  const bool tracing = (p->flags & MASK_TRACE_PASSES) != 0;
+  if (tracing) {
+    L.P_trace.alloc((size_t)(T + 1) * k * d);
+    L.lab_trace.alloc((size_t)(T + 1) * std::max<int64_t>(n, 1));
+    L.trace_T = T;
+    L.trace_n = n;
+  }
+  auto trace_P = [&](int slot) {
+    if (tracing)
+      MASK_CUDA(cudaMemcpyAsync(L.P_trace.p + (size_t)slot * k * d, L.P.p, sizeof(float) * k * d,
+                                cudaMemcpyDeviceToDevice, st));
+  };
+  auto trace_labels = [&](int slot) {
+    if (tracing && n)
+      MASK_CUDA(cudaMemcpyAsync(L.lab_trace.p + (size_t)slot * n, ws.lab_cur.p, sizeof(int32_t) * n,
+                                cudaMemcpyDeviceToDevice, st));
+  };
 
   // ---- seeded init (D2): gather the owned init rows, combine across ranks
   DevBuf<int64_t> idx(k);
@@ -519,13 +610,16 @@ void run_level(const Input& in, int64_t k, const int64_t* init_idx_host, const m
     MASK_CUDA(cudaMemsetAsync(S64.p, 0, sizeof(double) * k * d, st));
     if (ev) ev->mark(MASK_T_ASSIGN, st);
     launch_small_level(in.X, n, d, k, L.P.p, ws.lab_cur.p, ws.lab_prev.p, ws.best.p, S64.p, ws.counts.p, Jd.p,
-                       chd.p, fin.p, ctrl.p, bar.p, T, p->tol, st);
+                       chd.p, fin.p, ctrl.p, bar.p, T, p->tol, st, tracing ? L.P_trace.p : nullptr,
+                       tracing ? L.lab_trace.p : nullptr);
     if (ev) ev->mark(MASK_T_ASSIGN, st);
     ws.kernel_id = 3;
   }
   for (int t = 0; t < T && !fused; ++t) {
     if (p->iter_cb) MASK_CUDA(cudaMemcpyAsync(P_snap.p, L.P.p, sizeof(float) * k * d, cudaMemcpyDeviceToDevice, st));
+    trace_P(t);  // (passes skipped on the device after convergence fill slots never read back)
     assign_pass(in, L.P.p, k, p->flags, ws.lab_cur.p, ws.best.p, ws, st, active, ev.get());
+    trace_labels(t);
     LoopCtl lc;
     lc.t = t;
     lc.T = T;
@@ -599,7 +693,9 @@ void run_level(const Input& in, int64_t k, const int64_t* init_idx_host, const m
   // ---- final assignment with the final prototypes (D3): always runs, stats into slot T+1
   if (!fused) {
     if (p->iter_cb) MASK_CUDA(cudaMemcpyAsync(P_snap.p, L.P.p, sizeof(float) * k * d, cudaMemcpyDeviceToDevice, st));
+    trace_P(T);
     assign_pass(in, L.P.p, k, p->flags, ws.lab_cur.p, ws.best.p, ws, st, nullptr, ev.get());
+    trace_labels(T);
     pass_stats(T + 1, nullptr, LoopCtl());
   }
 
@@ -631,6 +727,7 @@ void run_level(const Input& in, int64_t k, const int64_t* init_idx_host, const m
   L.empties.push_back(0);
   L.dmax.push_back(0.0);
   L.updates = updates;
+  L.trace_loop_passes = loop_passes;
   if (p->iter_cb) emit_cb(loop_passes, P_snap.p, ws.lab_cur.p);
   L.labels = std::move(ws.lab_cur);
   L.n_items = n;
@@ -926,8 +1023,6 @@ void build_impl(const mask_matrix* data, const mask_build_params* p, mask_comm* 
   for (auto& L : idx->levels) {
     L.offsets.alloc(L.k + 1);
     L.members.alloc(std::max<int64_t>(L.n_items, 1));
-    // (the cursor block may return to the pool at once: the pool hands it only to later work
-    // on this stream, which runs after these kernels)
     DevBuf<int32_t> cursor(L.k);
     launch_children(L.labels.p, L.n_items, L.k, L.offsets.p, L.members.p, cursor.p, st);
   }
@@ -1617,6 +1712,21 @@ int32_t mask_get_trace(const mask_index* idx, int32_t level, double* J, int64_t*
     written = np;
   });
   return rc == MASK_OK ? written : rc;
+}
+
+int32_t mask_get_pass(const mask_index* idx, int32_t level, int32_t pass, float* P_host, int32_t* labels_host) {
+  return guarded([&] {
+    const Level& L = level_of(idx, level);
+    MASK_REQUIRE(L.trace_T >= 0 && L.P_trace.p, MASK_ERR_UNSUPPORTED, "the build did not keep a pass trace (MASK_TRACE_PASSES)");
+    MASK_REQUIRE(pass >= 0 && pass <= L.trace_loop_passes, MASK_ERR_ARG, "pass out of range");
+    const int slot = pass < L.trace_loop_passes ? pass : L.trace_T;
+    if (P_host)
+      MASK_CUDA(cudaMemcpy(P_host, L.P_trace.p + (size_t)slot * L.k * L.dim, sizeof(float) * L.k * L.dim,
+                           cudaMemcpyDeviceToHost));
+    const int64_t n = L.trace_n;
+    if (labels_host && n)
+      MASK_CUDA(cudaMemcpy(labels_host, L.lab_trace.p + (size_t)slot * n, sizeof(int32_t) * n, cudaMemcpyDeviceToHost));
+  });
 }
 
 int32_t mask_get_displacement(const mask_index* idx, int32_t level, double* dmax, int32_t cap) {

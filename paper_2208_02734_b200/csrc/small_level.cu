@@ -42,7 +42,7 @@ struct SmallArgs {
   int32_t* lab;
   int32_t* prev;
   float* best;
-  double* S;  // FP64 sums: order-independent to ~1e-16, so the loop is reproducible run to run
+  double* S;  // FP64 sums (atomics: the summation order varies, the FP32 mean practically never)
   int32_t* counts;
   double* J;
   unsigned long long* changed;
@@ -52,6 +52,8 @@ struct SmallArgs {
   int T;
   double tol;
   int tpr;  // threads per row in the assignment phase (power of two <= 32)
+  float* P_trace;      // MASK_TRACE_PASSES: (T+1) x k x d prototypes per pass, or nullptr
+  int32_t* lab_trace;  // (T+1) x n labels per pass (slot T = the final pass)
 };
 
 __device__ __forceinline__ void grid_barrier(unsigned* bar) {
@@ -143,9 +145,12 @@ __device__ __forceinline__ void row_argmin(const float (&x)[D], const float* C, 
 // assignment of every row (thread per row, row in registers, prototypes broadcast from shared
 // memory when they fit in 44 KB)
 template <int D>
-__device__ void assign_all(const SmallArgs& a, int slot, float* sP) {
+__device__ void assign_all(const SmallArgs& a, int slot, float* sP, int tslot) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const bool staged = a.k * a.d <= kSmallSmemFloats;
+  if (a.P_trace)  // P is read-only until the next grid barrier
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < a.k * a.d; e += stride)
+      a.P_trace[(int64_t)tslot * a.k * a.d + e] = __ldcg(a.P + e);
   if (staged)
     for (int64_t e = threadIdx.x; e < a.k * a.d; e += blockDim.x) sP[e] = __ldcg(a.P + e);
   __syncthreads();
@@ -186,6 +191,7 @@ __device__ void assign_all(const SmallArgs& a, int slot, float* sP) {
     }
     if (valid && h == 0) {
       a.lab[i] = bj;
+      if (a.lab_trace) a.lab_trace[(int64_t)tslot * a.n + i] = bj;
       a.best[i] = bv;
       s += (double)bv;
       c += (bj != __ldcg(a.prev + i)) ? 1ull : 0ull;
@@ -203,7 +209,7 @@ __global__ void __launch_bounds__(256) k_small_level(SmallArgs a) {
   const int64_t warps = stride >> 5, wid = tid >> 5;
   int t = 0;
   for (; t < a.T; ++t) {
-    assign_all<D>(a, t, sP);
+    assign_all<D>(a, t, sP, t);
     grid_barrier(a.bar);
     if (t > 0 && *(volatile unsigned long long*)(a.changed + t) == 0) {  // no label changed: stop
       if (tid == 0) {
@@ -254,7 +260,7 @@ __global__ void __launch_bounds__(256) k_small_level(SmallArgs a) {
     if (t == a.T - 1 && tid == 0) a.ctrl[1] = a.T;
   }
   // ---- final assignment with the final prototypes (stats slot T+1)
-  assign_all<D>(a, a.T + 1, sP);
+  assign_all<D>(a, a.T + 1, sP, a.T);
 }
 
 }  // namespace
@@ -268,8 +274,9 @@ bool small_level_supported(int64_t n, int d, int64_t k) {
 
 void launch_small_level(const float* Y, int64_t n, int d, int64_t k, float* P, int32_t* lab, int32_t* prev,
                         float* best, double* S, int32_t* counts, double* J, unsigned long long* changed,
-                        uint32_t* fin, int* ctrl, unsigned* bar_ws, int T, double tol, cudaStream_t st) {
-  SmallArgs a{Y, n, d, k, P, lab, prev, best, S, counts, J, changed, fin, ctrl, bar_ws, T, tol, 1};
+                        uint32_t* fin, int* ctrl, unsigned* bar_ws, int T, double tol, cudaStream_t st,
+                        float* P_trace, int32_t* lab_trace) {
+  SmallArgs a{Y, n, d, k, P, lab, prev, best, S, counts, J, changed, fin, ctrl, bar_ws, T, tol, 1, P_trace, lab_trace};
   MASK_CUDA(cudaMemsetAsync(bar_ws, 0, 2 * sizeof(unsigned), st));
   void* fn;
   if (d <= 4) fn = (void*)k_small_level<4>;

@@ -172,45 +172,39 @@ def _query_parity(idx, X, Q, levels, knn, beam, Qdev=None, csr=False, dim=None):
     return nd, ne
 
 
-@pytest.mark.parametrize("cid,div,T", [(1, 1, 6), (2, 64, 6), (3, 2048, 5)])
+@pytest.mark.parametrize("cid,div,T", [(1, 1, 20), (2, 64, 25), (3, 2048, 20)])
 def test_build_fused_small_levels_step(cid, div, T):
-    """Levels small enough for the fused single-launch Lloyd loop (K11) have no step hook, so
-    step mode is rebuilt from builds with T = 0, 1, 2, ...: the fused loop is deterministic
-    (FP64 sums), so the build with T = t runs exactly the first t passes of the one with
-    T = t + 1.  Checked per t against the oracle: final labels = nearest prototype of P_t (tie
-    window), P_{t+1} = member means of those labels (1e-4), child lists; J of the final pass."""
+    """Levels small enough for the fused single-launch Lloyd loop (K11) in step mode over the
+    pass trace of the production build (MASK_TRACE_PASSES; no iteration callback, so K11 runs):
+    every pass's labels = nearest prototype of the P_t it used (tie window), every update =
+    FP64 member means of those labels (1e-4), J of the final pass, child lists."""
     cfg = datagen.CONFIGS[cid].scaled(div) if div > 1 else datagen.CONFIGS[cid]
     X = datagen.data(cfg)
     inits = datagen.all_init_indices(cfg)
-    prev = None
-    for t_iters in range(T + 1):
-        idx = mk.build(t(X), cfg.levels, t_iters, inits, flags=mk.MASK_TIME_KERNELS)
-        assert all(idx.timing(l)["assign_kernel"] == "K11-fused-small-level"
-                   for l in range(1, len(cfg.levels) + 1)), "expected the fused path on every level"
-        cur = []
-        Y = X.astype(np.float64)
-        for l in range(1, len(cfg.levels) + 1):
-            P = idx.prototypes(l)
-            lab = idx.labels(l)
-            check_assignment(Y, P, lab, what=f"T={t_iters} level {l} labels")
-            if t_iters == 0:
-                np.testing.assert_array_equal(P, Y[inits[l - 1]].astype(np.float32))
-            elif l == 1:  # level 1's input does not depend on T
-                P_prev, lab_prev = prev[0]
-                P_ref, _ = oracle.means(Y, lab_prev, P_prev.astype(np.float64))
-                if not np.array_equal(P, P_prev):  # an update happened (not stopped early)
-                    check_prototypes(P, P_ref, what=f"T={t_iters} level 1 update")
-            off, mem = idx.children(l)
-            o_ref, m_ref = oracle.children(lab, cfg.levels[l - 1])
-            np.testing.assert_array_equal(off, o_ref)
-            np.testing.assert_array_equal(mem, m_ref)
-            tr = idx.trace(l)
-            d2 = ((Y - P.astype(np.float64)[lab]) ** 2).sum()
-            assert tr["J"][-1] == pytest.approx(d2, rel=1e-5)
-            cur.append((P, lab))
-            Y = P.astype(np.float64)
-        prev = cur
-        idx.free()
+    idx = mk.build(t(X), cfg.levels, T, inits, flags=mk.MASK_TIME_KERNELS | mk.MASK_TRACE_PASSES)
+    Y = X.astype(np.float64)
+    for l in range(1, len(cfg.levels) + 1):
+        assert idx.timing(l)["assign_kernel"] == "K11-fused-small-level", f"level {l}: expected K11"
+        seq = idx.passes(l)
+        np.testing.assert_array_equal(seq[0][0], Y[inits[l - 1]].astype(np.float32))
+        for p_i, (P, lab) in enumerate(seq):
+            check_assignment(Y, P, lab, what=f"level {l} pass {p_i}")
+            if p_i + 1 < len(seq) and not np.array_equal(seq[p_i + 1][0], P):
+                P_ref, _ = oracle.means(Y, lab, P.astype(np.float64))
+                check_prototypes(seq[p_i + 1][0], P_ref, what=f"level {l} update after pass {p_i}")
+        P, lab = seq[-1]
+        np.testing.assert_array_equal(idx.labels(l), lab)
+        np.testing.assert_array_equal(idx.prototypes(l), P)
+        off, mem = idx.children(l)
+        o_ref, m_ref = oracle.children(lab, cfg.levels[l - 1])
+        np.testing.assert_array_equal(off, o_ref)
+        np.testing.assert_array_equal(mem, m_ref)
+        tr = idx.trace(l)
+        assert len(tr["J"]) == len(seq)
+        d2 = ((Y - P.astype(np.float64)[lab]) ** 2).sum()
+        assert tr["J"][-1] == pytest.approx(d2, rel=1e-5)
+        Y = P.astype(np.float64)
+    idx.free()
 
 
 @pytest.mark.parametrize("cid,div", [(2, 64), (3, 256), (5, 2048)])
