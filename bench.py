@@ -5,9 +5,11 @@ over the config's query set, on seeded synthetic data resident in HBM.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl mask|reference]
 
-N > 1 is launched with torch.distributed.run (one rank per GPU, NCCL): rows are sharded
-(weak scaling: every rank owns one config-sized block of rows of the same block-seeded
-generator) and mask_build combines the per-iteration partial sums with one NCCL allreduce.
+N > 1 is launched with torch.distributed.run (one rank per GPU, NCCL): the config's rows are
+sharded (strong scaling: rank r owns rows shard.row_range(n, N, r) of the same block-seeded
+generator, so every N builds the identical index) and mask_build combines each Lloyd
+iteration's partial sums, counts and statistics with ONE NCCL allreduce; the query batch is
+sharded by rank.  Default workload: C3 (BASELINE configs[2], listed at 1/2/4/8 GPUs).
 
 Prints ONE JSON line on rank 0 (contract in DESIGN.md "Measurement").  Metric: Lloyd
 point·prototype distances/s = (sum over levels and assignment passes of n_items * k_l)
@@ -41,7 +43,7 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--impl", default="mask", choices=["mask", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -51,6 +53,7 @@ def parse():
     ap.add_argument("--iters", type=int, default=None, help="Lloyd iterations T (default: the config's)")
     ap.add_argument("--force-comm", action="store_true",
                     help="build through an NCCL communicator even on one rank (exercises the multi-GPU path)")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the QPS@recall beam sweep")
     return ap.parse_args()
 
 
@@ -303,17 +306,14 @@ def main():
         cfg = dataclasses.replace(cfg, knn=args.knn if args.knn is not None else cfg.knn,
                                   iters=args.iters if args.iters is not None else cfg.iters)
     beam = args.beam
-    # weak scaling: rank r owns rows [r*n, (r+1)*n) of the block-seeded generator
-    n_local = cfg.n
-    n_global = n_local * world
-    X_host = datagen.data(cfg, rank * n_local, n_local)
-    inits = []
-    prev = n_global
-    for l, kk in enumerate(cfg.levels, start=1):
-        inits.append(datagen.init_indices(cfg.cid, l, prev, kk))
-        prev = kk
-    qlo, qhi = mk.query_range(cfg.n_queries * world, world, rank)
-    Q_host = datagen.queries(cfg, count=cfg.n_queries * world)
+    # strong scaling: rank r owns rows [lo, hi) of the config's block-seeded generator
+    lo, hi = mk.row_range(cfg.n, world, rank)
+    n_local = hi - lo
+    n_global = cfg.n
+    X_host = datagen.data(cfg, lo, n_local)
+    inits = datagen.all_init_indices(cfg)
+    qlo, qhi = mk.query_range(cfg.n_queries, world, rank)
+    Q_host = datagen.queries(cfg)
     if not cfg.sparse:
         Q_host = Q_host[qlo:qhi]
     csr = cfg.sparse
@@ -343,7 +343,7 @@ def main():
 
     def step():
         idx = mk.build(X, cfg.levels, cfg.iters, inits, flags=flags, comm=comm, n_global=n_global,
-                       row_offset=rank * n_local, stream=stream)
+                       row_offset=lo, stream=stream)
         ids, d2 = idx.query(Q, knn=cfg.knn, beam=beam, stream=stream, out=qout)
         return idx, ids, d2
 
@@ -375,7 +375,7 @@ def main():
         e2 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         idx = mk.build(X, cfg.levels, cfg.iters, inits, flags=flags, comm=comm, n_global=n_global,
-                       row_offset=rank * n_local, stream=stream)
+                       row_offset=lo, stream=stream)
         e1.record(stream)
         ids, d2 = idx.query(Q, knn=cfg.knn, beam=beam, stream=stream, out=qout)
         e2.record(stream)
@@ -397,21 +397,26 @@ def main():
     # update kernel (K5/K6) times: two extra builds with every kernel class timed (untimed region)
     for _ in range(2):
         idx_u = mk.build(X, cfg.levels, cfg.iters, inits, flags=(flags & ~mk.MASK_TIME_ASSIGN) | mk.MASK_TIME_KERNELS,
-                         comm=comm, n_global=n_global, row_offset=rank * n_local, stream=stream)
+                         comm=comm, n_global=n_global, row_offset=lo, stream=stream)
         tu = idx_u.timing(1)
         kt["update"] += tu["update"]["ms"]
         kt["update_n"] += tu["update"]["launches"]
         idx_u.free()
 
     total_ms = sum(step_ms)
-    if world > 1:
-        t = torch.tensor([total_ms, float(dist_total)], dtype=torch.float64, device=dev)
-        tmax = t.clone()
-        torch.distributed.all_reduce(tmax[:1], op=torch.distributed.ReduceOp.MAX)
-        total_ms = float(tmax[0])
-        dist_all = torch.tensor([float(dist_total)], dtype=torch.float64, device=dev)
-        # level-1 passes count every global row once per rank's view (n_items = n_global) -> no sum
-        dist_total = float(dist_all[0])
+
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([float(v)], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        return float(t[0])
+
+    # every rank's index covers all n_global rows (level 1 n_items = n_global after the gather),
+    # so dist_total already counts the whole job's work; the time is the slowest rank's
+    total_ms = max_over_ranks(total_ms)
+    build_mean = max_over_ranks(statistics.mean(build_ms))
+    query_mean = max_over_ranks(statistics.mean(query_ms))
     value = dist_total / (total_ms / 1000.0)
 
     # ---- roofline of the dominant kernel (level-1 assignment), measured live above

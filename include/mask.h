@@ -142,10 +142,31 @@ int32_t mask_device_ok(void);
 /* ---------------------------------------------------------------- multi-GPU
  * One process per GPU.  Rank 0 calls mask_comm_unique_id, the caller broadcasts the 128
  * bytes over its own process group, then every rank calls mask_comm_init (collective).
- * The communicator is used by mask_build (one allreduce of [sums | counts] per Lloyd
- * iteration, BASELINE.json north_star) and must outlive the builds that use it. */
+ * The communicator is used by mask_build (ONE allreduce per Lloyd iteration of the packed
+ * [sums | counts | J | changed], BASELINE.json north_star) and must outlive the builds that
+ * use it. */
 int32_t mask_comm_unique_id(uint8_t id_out[128]);
 int32_t mask_comm_init(const uint8_t id[128], int32_t world, int32_t rank, mask_comm** out);
+
+/* Host transport (testing): a communicator whose collectives are carried out by the caller's
+ * `fn` on host buffers, so every world > 1 branch of mask_build can run with several processes
+ * sharing one GPU (the library drains its stream, stages the buffer through host memory,
+ * calls fn, copies the result back).  fn(kind, buf, send, count, dtype, arg, user) is called
+ * in the same order on every rank and returns 0 on success:
+ *   MASK_COLL_ALLREDUCE: buf (count elements) <- elementwise sum (arg = MASK_COLL_SUM) or max
+ *                        (MASK_COLL_MAX) over the ranks, in place;
+ *   MASK_COLL_BROADCAST: buf (count elements) <- rank `arg`'s buf;
+ *   MASK_COLL_ALLGATHER: buf (world * count elements) <- every rank's send (count elements),
+ *                        rank-major.
+ * dtype: MASK_COLL_F32 / F64 / I32 / I64 / U64.  A non-zero return fails the call with
+ * MASK_ERR_NCCL and marks the communicator unusable.  Performance runs use mask_comm_init. */
+enum { MASK_COLL_ALLREDUCE = 0, MASK_COLL_BROADCAST = 1, MASK_COLL_ALLGATHER = 2 };
+enum { MASK_COLL_F32 = 0, MASK_COLL_F64 = 1, MASK_COLL_I32 = 2, MASK_COLL_I64 = 3, MASK_COLL_U64 = 4 };
+enum { MASK_COLL_SUM = 0, MASK_COLL_MAX = 1 };
+typedef int32_t (*mask_host_collective_fn)(int32_t kind, void* buf, const void* send, int64_t count,
+                                           int32_t dtype, int32_t arg, void* user);
+int32_t mask_comm_init_host(int32_t world, int32_t rank, mask_host_collective_fn fn, void* user,
+                            mask_comm** out);
 void mask_comm_free(mask_comm* comm); /* NULL-safe */
 
 /* ---------------------------------------------------------------- build

@@ -48,6 +48,7 @@ EXPORTS = [
     "mask_grouped_depth", "mask_build_grouped", "mask_range_query", "mask_insert",
     "mask_top_prototypes", "mask_route", "mask_query_routed", "mask_merge", "mask_collective_count",
     "mask_seeded_init", "mask_debug_fail_alloc", "mask_get_displacement", "mask_get_pass",
+    "mask_comm_init_host",
 ]
 
 
@@ -66,6 +67,10 @@ class MaskMatrix(C.Structure):
         ("nnz", C.c_int64),
     ]
 
+
+HOST_COLL = C.CFUNCTYPE(C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_void_p)
+MASK_COLL_ALLREDUCE, MASK_COLL_BROADCAST, MASK_COLL_ALLGATHER = 0, 1, 2
+MASK_COLL_SUM, MASK_COLL_MAX = 0, 1
 
 ITER_CB = C.CFUNCTYPE(None, C.c_int32, C.c_int32, C.POINTER(C.c_float), C.c_int64, C.c_int32,
                       C.POINTER(C.c_int32), C.c_int64, C.c_void_p)
@@ -153,6 +158,7 @@ def load():
             "mask_debug_fail_alloc": (None, [i64]),
             "mask_get_displacement": (i32, [P, i32, P, i32]),
             "mask_get_pass": (i32, [P, i32, i32, P, P]),
+            "mask_comm_init_host": (i32, [i32, i32, HOST_COLL, P, C.POINTER(P)]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)

@@ -132,10 +132,62 @@ class Comm:
         dist.broadcast_object_list(obj, src=0)
         return cls.init(obj[0], world, rank)
 
+    @classmethod
+    def host(cls, group=None) -> "Comm":
+        """Host-transport communicator (mask_comm_init_host): libmask's collectives are carried
+        out by torch.distributed on host buffers of ``group`` (e.g. gloo), so several ranks can
+        share one GPU in tests.  Performance runs use ``from_process_group`` (NCCL)."""
+        import torch.distributed as dist
+
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        fn = _lib.HOST_COLL(lambda *a: host_collective(*a, group=group))
+        out = C.c_void_p()
+        check(load().mask_comm_init_host(world, rank, fn, None, C.byref(out)))
+        c = cls(out.value, world, rank)
+        c._fn = fn  # the C function pointer must outlive the communicator
+        return c
+
     def free(self) -> None:
         if self.handle:
             load().mask_comm_free(self.handle)
             self.handle = None
+
+
+_COLL_NP = {0: np.float32, 1: np.float64, 2: np.int32, 3: np.int64, 4: np.int64}  # u64 sums as int64 bits
+
+
+def host_collective(kind, buf, send, count, dtype, arg, user=None, group=None) -> int:
+    """The host transport of mask_comm_init_host over torch.distributed (argument marshalling:
+    the buffers are wrapped, not copied; the reduction is the process group's)."""
+    try:
+        import torch.distributed as dist
+
+        count = int(count)
+        if count == 0:
+            return 0
+        npdt = np.dtype(_COLL_NP[int(dtype)])
+        world = dist.get_world_size(group)
+
+        def view(addr, n):
+            return torch.from_numpy(np.frombuffer((C.c_char * (n * npdt.itemsize)).from_address(addr), dtype=npdt))
+
+        if kind == _lib.MASK_COLL_ALLREDUCE:
+            op = dist.ReduceOp.MAX if arg == _lib.MASK_COLL_MAX else dist.ReduceOp.SUM
+            dist.all_reduce(view(buf, count), op=op, group=group)
+        elif kind == _lib.MASK_COLL_BROADCAST:
+            src = int(arg) if group is None else dist.get_global_rank(group, int(arg))
+            dist.broadcast(view(buf, count), src=src, group=group)
+        elif kind == _lib.MASK_COLL_ALLGATHER:
+            out = view(buf, count * world)
+            dist.all_gather(list(out.split(count)), view(send, count).clone(), group=group)
+        else:
+            return 2
+        return 0
+    except Exception:  # reported to the library as a failed collective (MASK_ERR_NCCL)
+        import traceback
+
+        traceback.print_exc()
+        return 1
 
 
 class Index:

@@ -205,10 +205,106 @@ struct HostStats {
 }  // namespace
 
 struct mask_comm {
-  ncclComm_t comm = nullptr;
+  ncclComm_t comm = nullptr;           // NCCL transport (one GPU per rank)
+  mask_host_collective_fn host = nullptr;  // host transport (mask_comm_init_host), or nullptr
+  void* host_user = nullptr;
+  bool host_failed = false;
   int world = 1;
   int rank = 0;
+  bool usable() const { return host ? !host_failed : comm != nullptr; }
 };
+
+namespace {
+
+// ---- collectives over either transport.  NCCL: enqueued on the build stream (the path every
+// GPU count runs).  Host transport (mask_comm_init_host, the multi-rank tests on one GPU): the
+// stream is drained, the buffer staged through host memory, the caller's function exchanges
+// it, and the result is copied back -- the same call sequence, so every world > 1 branch of
+// mask_build runs.
+enum CollType { kF32 = MASK_COLL_F32, kF64 = MASK_COLL_F64, kI32 = MASK_COLL_I32, kI64 = MASK_COLL_I64,
+                kU64 = MASK_COLL_U64 };
+size_t coll_size(CollType t) { return (t == kF32 || t == kI32) ? 4 : 8; }
+ncclDataType_t coll_nccl(CollType t) {
+  switch (t) {
+    case kF32: return ncclFloat;
+    case kF64: return ncclDouble;
+    case kI32: return ncclInt32;
+    case kI64: return ncclInt64;
+    default: return ncclUint64;
+  }
+}
+
+void host_call(mask_comm* c, int kind, void* buf, const void* send, size_t count, CollType t, int arg) {
+  g_nccl_calls.fetch_add(1, std::memory_order_relaxed);
+  const int32_t r = c->host(kind, buf, send, (int64_t)count, (int32_t)t, arg, c->host_user);
+  if (r != 0) {
+    c->host_failed = true;
+    ::mask::fail(MASK_ERR_NCCL, "host collective failed (code " + std::to_string(r) + ")");
+  }
+}
+
+void coll_allreduce(mask_comm* c, void* dev, size_t count, CollType t, bool max_op, cudaStream_t st) {
+  if (!c->host) {
+    MASK_NCCL(ncclAllReduce(dev, dev, count, coll_nccl(t), max_op ? ncclMax : ncclSum, c->comm, st));
+    return;
+  }
+  std::vector<char> h(count * coll_size(t));
+  MASK_CUDA(cudaMemcpyAsync(h.data(), dev, h.size(), cudaMemcpyDeviceToHost, st));
+  MASK_CUDA(cudaStreamSynchronize(st));
+  host_call(c, MASK_COLL_ALLREDUCE, h.data(), nullptr, count, t, max_op ? MASK_COLL_MAX : MASK_COLL_SUM);
+  MASK_CUDA(cudaMemcpyAsync(dev, h.data(), h.size(), cudaMemcpyHostToDevice, st));
+  MASK_CUDA(cudaStreamSynchronize(st));
+}
+
+// recv <- root's send (send is read on the root only; may alias recv)
+void coll_broadcast(mask_comm* c, const void* send, void* recv, size_t count, CollType t, int root, cudaStream_t st) {
+  if (!c->host) {
+    MASK_NCCL(ncclBroadcast(send, recv, count, coll_nccl(t), root, c->comm, st));
+    return;
+  }
+  std::vector<char> h(count * coll_size(t));
+  if (c->rank == root && count) {
+    MASK_CUDA(cudaMemcpyAsync(h.data(), send, h.size(), cudaMemcpyDeviceToHost, st));
+    MASK_CUDA(cudaStreamSynchronize(st));
+  }
+  host_call(c, MASK_COLL_BROADCAST, h.data(), nullptr, count, t, root);
+  if (count) {
+    MASK_CUDA(cudaMemcpyAsync(recv, h.data(), h.size(), cudaMemcpyHostToDevice, st));
+    MASK_CUDA(cudaStreamSynchronize(st));
+  }
+}
+
+// recv[r * count ...] <- rank r's send (count elements each)
+void coll_allgather(mask_comm* c, const void* send, void* recv, size_t count, CollType t, cudaStream_t st) {
+  if (!c->host) {
+    MASK_NCCL(ncclAllGather(send, recv, count, coll_nccl(t), c->comm, st));
+    return;
+  }
+  std::vector<char> hs(count * coll_size(t)), hr(count * coll_size(t) * c->world);
+  MASK_CUDA(cudaMemcpyAsync(hs.data(), send, hs.size(), cudaMemcpyDeviceToHost, st));
+  MASK_CUDA(cudaStreamSynchronize(st));
+  host_call(c, MASK_COLL_ALLGATHER, hr.data(), hs.data(), count, t, 0);
+  MASK_CUDA(cudaMemcpyAsync(recv, hr.data(), hr.size(), cudaMemcpyHostToDevice, st));
+  MASK_CUDA(cudaStreamSynchronize(st));
+}
+
+// ncclGroupStart/End around a batch of collectives (no-op for the host transport, whose
+// calls complete one by one in the same order on every rank)
+struct CollGroup {
+  mask_comm* c;
+  explicit CollGroup(mask_comm* cm) : c(cm) {
+    if (!c->host) MASK_NCCL(ncclGroupStart());
+  }
+  void end() {
+    if (c && !c->host) MASK_NCCL(ncclGroupEnd());
+    c = nullptr;
+  }
+  ~CollGroup() {
+    if (c && !c->host) ncclGroupEnd();  // unwinding: close the group, error already raised
+  }
+};
+
+}  // namespace
 
 namespace {
 
@@ -476,13 +572,54 @@ void assign_pass(const Input& in, const float* P, int64_t k, int flags, int32_t*
   }
 }
 
-// ---- device-side loop control (one per level): ctrl[0] = active, ctrl[1] = loop passes run
-__global__ void k_after_stats(int* ctrl, const unsigned long long* changed, int t) {
-  if (!ctrl[0]) return;
-  if (t > 0 && changed[t] == 0) {  // no label changed: the update would be a no-op (stop)
-    ctrl[0] = 0;
-    ctrl[1] = t + 1;
+// ---- N1 packing: one fp32 allreduce per pass carries the sums, the counts and the pass stats.
+// An integer v is sent as (v >> 12, v & 4095): each half's sum over the ranks stays below 2^24
+// (n < 2^36 rows, < 4096 ranks), so the fp32 sums are exact.  J (double) as hi + lo floats.
+__global__ void k_pack_pass(const int32_t* __restrict__ counts, int64_t k, const double* __restrict__ J,
+                            const unsigned long long* __restrict__ ch, float* __restrict__ tail,
+                            const int* __restrict__ active) {
+  if (active && !*active) return;
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < k; j += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t c = counts[j];
+    tail[j] = (float)(c >> 12);
+    tail[k + j] = (float)(c & 4095);
   }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    const double v = *J;
+    const float hi = (float)v;
+    tail[2 * k] = hi;
+    tail[2 * k + 1] = (float)(v - (double)hi);
+    const unsigned long long c = *ch;
+    tail[2 * k + 2] = (float)(c >> 12);
+    tail[2 * k + 3] = (float)(c & 4095ull);
+  }
+}
+// inverse of k_pack_pass on the combined buffer; with ctrl: the no-change stop test of pass t
+__global__ void k_unpack_pass(const float* __restrict__ tail, int64_t k, int32_t* __restrict__ counts,
+                              double* __restrict__ J, unsigned long long* __restrict__ ch, int* ctrl, int t,
+                              const int* __restrict__ active) {
+  if (active && !*active) return;
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < k; j += (int64_t)gridDim.x * blockDim.x)
+    counts[j] = (int32_t)tail[j] * 4096 + (int32_t)tail[k + j];
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    *J = (double)tail[2 * k] + (double)tail[2 * k + 1];
+    const unsigned long long c = (unsigned long long)tail[2 * k + 2] * 4096ull + (unsigned long long)tail[2 * k + 3];
+    *ch = c;
+    if (ctrl && t > 0 && c == 0) {  // no label changed anywhere: stop before the update (D3)
+      ctrl[0] = 0;
+      ctrl[1] = t + 1;
+    }
+  }
+}
+void launch_pack_pass(const int32_t* counts, int64_t k, const double* J, const unsigned long long* ch, float* tail,
+                      cudaStream_t st, const int* active) {
+  k_pack_pass<<<grid_for(std::max<int64_t>(k, 1), 256), 256, 0, st>>>(counts, k, J, ch, tail, active);
+  MASK_LAUNCH_CHECK();
+}
+void launch_unpack_pass(const float* tail, int64_t k, int32_t* counts, double* J, unsigned long long* ch, int* ctrl,
+                        int t, cudaStream_t st, const int* active) {
+  k_unpack_pass<<<grid_for(std::max<int64_t>(k, 1), 256), 256, 0, st>>>(tail, k, counts, J, ch, ctrl, t, active);
+  MASK_LAUNCH_CHECK();
 }
 __global__ void k_copy_labels(int32_t* __restrict__ dst, const int32_t* __restrict__ src, int64_t n,
                               const int* __restrict__ active) {
@@ -495,14 +632,14 @@ __global__ void k_copy_labels(int32_t* __restrict__ dst, const int32_t* __restri
 //   P <- init rows; for t < T: a <- assign(P); trace; stop if no label changed (t > 0);
 //   P <- means (empty keeps, D5); stop if tol > 0 and max displacement <= tol;
 //   final assignment -> labels.
-// The whole loop is enqueued at once: the stop tests run on the device (k_after_stats,
-// the last blocks of k_pass_stats / k_finalize) and later passes become no-ops, so the host synchronises once per level
+// The whole loop is enqueued at once: the stop tests run on the device (k_unpack_pass with a
+// communicator, the last blocks of k_pass_stats / k_finalize) and later passes become no-ops, so the host synchronises once per level
 // (unless the test-only iteration callback needs host copies after every pass).
 // After a host synchronisation of a communicator build: a failed or hung peer surfaces as an
 // asynchronous NCCL error; abort the communicator (every later collective returns at once) and
 // fail the call with MASK_ERR_NCCL instead of waiting forever.
 void check_comm(mask_comm* comm) {
-  if (!comm) return;
+  if (!comm || comm->host) return;
   ncclResult_t ar = ncclSuccess;
   const ncclResult_t r = ncclCommGetAsyncError(comm->comm, &ar);
   if (r != ncclSuccess || ar != ncclSuccess) {
@@ -527,7 +664,7 @@ void run_level(const Input& in, int64_t k, const int64_t* init_idx_host, const m
   ws.lab_prev.alloc(std::max<int64_t>(n, 1));
   ws.lab_cur.alloc(std::max<int64_t>(n, 1));
   ws.best.alloc(std::max<int64_t>(n, 1));
-  ws.S.alloc((size_t)k * d);
+  ws.S.alloc((size_t)k * d + (comm ? 2 * (size_t)k + 8 : 0));  // + the packed tail (N1)
   ws.counts.alloc(k);
   // per-pass statistics (slot T+1 = final pass) and loop control
   DevBuf<double> Jd(T + 2);
@@ -570,7 +707,7 @@ void run_level(const Input& in, int64_t k, const int64_t* init_idx_host, const m
   } else {
     launch_gather_rows(in.X, d, idx.p, k, in.row_offset, n, L.P.p, st);
   }
-  if (comm) MASK_NCCL(ncclAllReduce(L.P.p, L.P.p, (size_t)k * d, ncclFloat, ncclSum, comm->comm, st));
+  if (comm) coll_allreduce(comm, L.P.p, (size_t)k * d, kF32, false, st);
 
   // every event pair costs a few microseconds of device time per pass (~5 % of a C2 build for
   // all four classes), so MASK_TIME_ASSIGN times the assignment kernel alone
@@ -590,15 +727,24 @@ void run_level(const Input& in, int64_t k, const int64_t* init_idx_host, const m
   DevBuf<float> P_snap;  // P used by the pass (only kept for the callback)
   if (p->iter_cb) P_snap.alloc((size_t)k * d);
 
-  // pass statistics into slot `slot`, combined over ranks (no host round trip)
+  // pass statistics into slot `slot` (this rank's rows; with a communicator they are combined
+  // in the pass's single allreduce below, or -- final pass -- in one small allreduce)
   auto pass_stats = [&](int slot, const int* act, LoopCtl lc) {
     launch_pass_stats(ws.lab_cur.p, ws.lab_prev.p, ws.best.p, n, Jd.p + slot, chd.p + slot, st, act, lc);
-    if (comm) {
-      MASK_NCCL(ncclGroupStart());
-      MASK_NCCL(ncclAllReduce(Jd.p + slot, Jd.p + slot, 1, ncclDouble, ncclSum, comm->comm, st));
-      MASK_NCCL(ncclAllReduce(chd.p + slot, chd.p + slot, 1, ncclUint64, ncclSum, comm->comm, st));
-      MASK_NCCL(ncclGroupEnd());
-    }
+  };
+  // multi-GPU combine (N1): ONE allreduce per Lloyd iteration of the packed fp32 buffer
+  // [S (k x d) | counts split hi/lo (2k) | J hi/lo | changed hi/lo] (BASELINE north_star
+  // "combined with a single NCCL allreduce"); the integer parts are split into 12-bit low
+  // halves and the rest so every fp32 partial sum stays exact
+  const size_t pack_tail = (size_t)k * d;
+  auto combine = [&](int slot, int t, bool with_sums, const int* act) {
+    // with sums: the whole buffer; stats only (final pass, S no longer needed): its first 4 floats
+    float* tail = ws.S.p + (with_sums ? pack_tail : 0);
+    const int64_t kk = with_sums ? k : 0;
+    launch_pack_pass(ws.counts.p, kk, Jd.p + slot, chd.p + slot, tail, st, act);
+    const size_t count = with_sums ? pack_tail + 2 * (size_t)k + 4 : 4;
+    coll_allreduce(comm, ws.S.p, count, kF32, false, st);
+    launch_unpack_pass(tail, kk, ws.counts.p, Jd.p + slot, chd.p + slot, with_sums ? ctrl.p : nullptr, t, st, act);
   };
 
   // small dense level without a communicator or step hook: the whole loop in one launch (K11)
@@ -626,10 +772,6 @@ void run_level(const Input& in, int64_t k, const int64_t* init_idx_host, const m
     lc.tol = p->tol;
     if (!comm) lc.ctrl = ctrl.p;  // single GPU: stop test fused into the stats kernel
     pass_stats(t, active, lc);
-    if (comm) {  // the combined statistics decide (identically on every rank)
-      k_after_stats<<<1, 1, 0, st>>>(ctrl.p, chd.p, t);
-      MASK_LAUNCH_CHECK();
-    }
     if (p->iter_cb) {  // host view of the control state (test-only path)
       int h[4];
       MASK_CUDA(cudaMemcpyAsync(h, ctrl.p, sizeof(h), cudaMemcpyDeviceToHost, st));
@@ -666,12 +808,9 @@ void run_level(const Input& in, int64_t k, const int64_t* init_idx_host, const m
       launch_update_dense(in.X, n, d, ws.lab_cur.p, k, ws.S.p, ws.counts.p, st, active,
                           sorted ? ws.perm.p : nullptr);
     if (ev) ev->mark(MASK_T_UPDATE, st);
-    if (comm) {
-      MASK_NCCL(ncclGroupStart());
-      MASK_NCCL(ncclAllReduce(ws.S.p, ws.S.p, (size_t)k * d, ncclFloat, ncclSum, comm->comm, st));
-      MASK_NCCL(ncclAllReduce(ws.counts.p, ws.counts.p, (size_t)k, ncclInt32, ncclSum, comm->comm, st));
-      MASK_NCCL(ncclGroupEnd());
-    }
+    // the combined statistics decide the no-change stop identically on every rank (the update
+    // of a pass that changed no label is then not applied: K7 is skipped, as in the oracle)
+    if (comm) combine(t, t, true, active);
     if (ev) ev->mark(MASK_T_FINALIZE, st);
     LoopCtl lf = lc;
     lf.ctrl = ctrl.p;  // tolerance stop / pass count (fin is identical on every rank)
@@ -697,6 +836,7 @@ void run_level(const Input& in, int64_t k, const int64_t* init_idx_host, const m
     assign_pass(in, L.P.p, k, p->flags, ws.lab_cur.p, ws.best.p, ws, st, nullptr, ev.get());
     trace_labels(T);
     pass_stats(T + 1, nullptr, LoopCtl());
+    if (comm) combine(T + 1, T + 1, false, nullptr);
   }
 
   // ---- one read-back per level: control state and the per-pass trace
@@ -755,27 +895,27 @@ void run_level(const Input& in, int64_t k, const int64_t* init_idx_host, const m
   }
 }
 
-// Gather per-rank row blocks into one n_global buffer on every rank (ncclBroadcast per root).
+// Gather per-rank row blocks into one n_global buffer on every rank (a broadcast per root).
 template <class T>
 void allgather_rows(mask_comm* comm, const T* local, int64_t local_count, T* global,
-                    const std::vector<int64_t>& counts, cudaStream_t st, ncclDataType_t ty) {
+                    const std::vector<int64_t>& counts, cudaStream_t st, CollType ty) {
   (void)local_count;
   int64_t off = 0;
-  MASK_NCCL(ncclGroupStart());
+  CollGroup g(comm);
   for (int r = 0; r < comm->world; ++r) {
     if (counts[r] > 0)
-      MASK_NCCL(ncclBroadcast(r == comm->rank ? (const void*)local : (const void*)(global + off),
-                              global + off, (size_t)counts[r], ty, r, comm->comm, st));
+      coll_broadcast(comm, r == comm->rank ? (const void*)local : (const void*)(global + off), global + off,
+                     (size_t)counts[r], ty, r, st);
     off += counts[r];
   }
-  MASK_NCCL(ncclGroupEnd());
+  g.end();
 }
 
 std::vector<int64_t> allgather_scalar(mask_comm* comm, int64_t v, cudaStream_t st) {
   DevBuf<int64_t> buf(comm->world);
   DevBuf<int64_t> mine(1);
   MASK_CUDA(cudaMemcpyAsync(mine.p, &v, sizeof(int64_t), cudaMemcpyHostToDevice, st));
-  MASK_NCCL(ncclAllGather(mine.p, buf.p, 1, ncclInt64, comm->comm, st));
+  coll_allgather(comm, mine.p, buf.p, 1, kI64, st);
   std::vector<int64_t> out(comm->world);
   MASK_CUDA(cudaMemcpyAsync(out.data(), buf.p, sizeof(int64_t) * comm->world, cudaMemcpyDeviceToHost, st));
   MASK_CUDA(cudaStreamSynchronize(st));
@@ -861,7 +1001,7 @@ void build_impl(const mask_matrix* data, const mask_build_params* p, mask_comm* 
     const int64_t hv[2] = {(int64_t)(h >> 1), -(int64_t)(h >> 1)};  // max of both = (max h, -min h)
     DevBuf<int64_t> hd(2);
     MASK_CUDA(cudaMemcpyAsync(hd.p, hv, sizeof(hv), cudaMemcpyHostToDevice, st));
-    MASK_NCCL(ncclAllReduce(hd.p, hd.p, 2, ncclInt64, ncclMax, comm->comm, st));
+    coll_allreduce(comm, hd.p, 2, kI64, true, st);
     int64_t hr[2];
     MASK_CUDA(cudaMemcpyAsync(hr, hd.p, sizeof(hr), cudaMemcpyDeviceToHost, st));
     MASK_CUDA(cudaStreamSynchronize(st));
@@ -932,7 +1072,7 @@ void build_impl(const mask_matrix* data, const mask_build_params* p, mask_comm* 
       // every rank must agree on the outcome
       DevBuf<int32_t> f2(1);
       MASK_CUDA(cudaMemcpyAsync(f2.p, &h, sizeof(int32_t), cudaMemcpyHostToDevice, st));
-      MASK_NCCL(ncclAllReduce(f2.p, f2.p, 1, ncclInt32, ncclMax, comm->comm, st));
+      coll_allreduce(comm, f2.p, 1, kI32, true, st);
       MASK_CUDA(cudaMemcpyAsync(&h, f2.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
       MASK_CUDA(cudaStreamSynchronize(st));
     }
@@ -949,14 +1089,14 @@ void build_impl(const mask_matrix* data, const mask_build_params* p, mask_comm* 
     const auto counts = allgather_scalar(comm, data->rows, st);
     Level& L1 = idx->levels[0];
     DevBuf<int32_t> glab(N);
-    allgather_rows<int32_t>(comm, L1.labels.p, data->rows, glab.p, counts, st, ncclInt32);
+    allgather_rows<int32_t>(comm, L1.labels.p, data->rows, glab.p, counts, st, kI32);
     L1.labels = std::move(glab);
     L1.n_items = N;
     if (data->format == MASK_DENSE_F32) {
       idx->own_X.alloc((size_t)N * d);
       std::vector<int64_t> ecounts(world);
       for (int r = 0; r < world; ++r) ecounts[r] = counts[r] * d;
-      allgather_rows<float>(comm, in.X, data->rows * d, idx->own_X.p, ecounts, st, ncclFloat);
+      allgather_rows<float>(comm, in.X, data->rows * d, idx->own_X.p, ecounts, st, kF32);
       idx->X = idx->own_X.p;
     } else {
       const auto nnzs = allgather_scalar(comm, data->nnz, st);
@@ -967,8 +1107,8 @@ void build_impl(const mask_matrix* data, const mask_build_params* p, mask_comm* 
       idx->own_col.alloc(std::max<int64_t>(total, 1));
       idx->own_val.alloc(std::max<int64_t>(total, 1));
       idx->own_rp.alloc(N + 1);
-      allgather_rows<int32_t>(comm, in.col, data->nnz, idx->own_col.p, nnzs, st, ncclInt32);
-      allgather_rows<float>(comm, in.val, data->nnz, idx->own_val.p, nnzs, st, ncclFloat);
+      allgather_rows<int32_t>(comm, in.col, data->nnz, idx->own_col.p, nnzs, st, kI32);
+      allgather_rows<float>(comm, in.val, data->nnz, idx->own_val.p, nnzs, st, kF32);
       // row_ptr: each rank contributes rows entries rebased by its nnz offset
       DevBuf<int64_t> rp_loc(std::max<int64_t>(data->rows, 1));
       if (data->rows) {
@@ -976,7 +1116,7 @@ void build_impl(const mask_matrix* data, const mask_build_params* p, mask_comm* 
         k_add_offset<<<grid_for(data->rows, 256), 256, 0, st>>>(rp_loc.p, data->rows, nnz_off[rank]);
         MASK_LAUNCH_CHECK();
       }
-      allgather_rows<int64_t>(comm, rp_loc.p, data->rows, idx->own_rp.p, counts, st, ncclInt64);
+      allgather_rows<int64_t>(comm, rp_loc.p, data->rows, idx->own_rp.p, counts, st, kI64);
       MASK_CUDA(cudaMemcpyAsync(idx->own_rp.p + N, &total, sizeof(int64_t), cudaMemcpyHostToDevice, st));
       idx->rp = idx->own_rp.p;
       idx->col = idx->own_col.p;
@@ -1013,10 +1153,10 @@ void build_impl(const mask_matrix* data, const mask_build_params* p, mask_comm* 
     run_level(up, p->k[l], inits[l], p, nullptr, l + 1, st, idx->levels[l], hs);
     if (comm && world > 1) {
       Level& L = idx->levels[l];
-      MASK_NCCL(ncclGroupStart());
-      MASK_NCCL(ncclBroadcast(L.P.p, L.P.p, (size_t)L.k * d, ncclFloat, 0, comm->comm, st));
-      MASK_NCCL(ncclBroadcast(L.labels.p, L.labels.p, (size_t)L.n_items, ncclInt32, 0, comm->comm, st));
-      MASK_NCCL(ncclGroupEnd());
+      CollGroup g(comm);
+      coll_broadcast(comm, L.P.p, L.P.p, (size_t)L.k * d, kF32, 0, st);
+      coll_broadcast(comm, L.labels.p, L.labels.p, (size_t)L.n_items, kI32, 0, st);
+      g.end();
     }
   }
   // ---- child lists (K8) for every level
@@ -1183,6 +1323,19 @@ int32_t mask_comm_init(const uint8_t id[128], int32_t world, int32_t rank, mask_
   });
 }
 
+int32_t mask_comm_init_host(int32_t world, int32_t rank, mask_host_collective_fn fn, void* user, mask_comm** out) {
+  return guarded([&] {
+    MASK_REQUIRE(fn != nullptr && out != nullptr, MASK_ERR_ARG, "NULL argument");
+    MASK_REQUIRE(world >= 1 && rank >= 0 && rank < world, MASK_ERR_ARG, "bad world/rank");
+    auto c = std::make_unique<mask_comm>();
+    c->world = world;
+    c->rank = rank;
+    c->host = fn;
+    c->host_user = user;
+    *out = c.release();
+  });
+}
+
 void mask_comm_free(mask_comm* comm) {
   if (!comm) return;
   if (comm->comm) ncclCommDestroy(comm->comm);
@@ -1193,7 +1346,7 @@ int32_t mask_build(const mask_matrix* data, const mask_build_params* params, mas
                    void* stream, mask_index** out) {
   NvtxRange range("mask_build");
   return guarded([&] {
-    MASK_REQUIRE(!comm || comm->comm, MASK_ERR_NCCL, "communicator was aborted after an earlier NCCL error");
+    MASK_REQUIRE(!comm || comm->usable(), MASK_ERR_NCCL, "communicator was aborted after an earlier NCCL error");
     build_impl(data, params, comm, as_stream(stream), out);
   });
 }

@@ -347,19 +347,25 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
       continue;
     }
     const int64_t p0 = qrp[qid];
-    const int qn = (int)min64(qrp[qid + 1] - p0, kMaxQueryNnz);
+    const int64_t qn = qrp[qid + 1] - p0;
+    // the query's non-zeros: staged in shared memory up to kMaxQueryNnz, else read in place
+    // from global memory (any length; never truncated)
+    const bool staged = qn <= kMaxQueryNnz;
+    const int32_t* qc = staged ? s_col[w] : qcol + p0;
+    const float* qv = staged ? s_val[w] : qval + p0;
     __syncwarp();
-    for (int i = lane; i < qn; i += 32) {
-      s_col[w][i] = qcol[p0 + i];
-      s_val[w][i] = qval[p0 + i];
-    }
+    if (staged)
+      for (int i = lane; i < qn; i += 32) {
+        s_col[w][i] = qcol[p0 + i];
+        s_val[w][i] = qval[p0 + i];
+      }
     __syncwarp();
     float qq = 0.f;
-    for (int i = 0; i < qn; ++i) qq = fmaf(s_val[w][i], s_val[w][i], qq);
+    for (int64_t i = 0; i < qn; ++i) qq = fmaf(qv[i], qv[i], qq);
     auto proto_dist = [&](int l, int64_t j) {
       const float* c = qi.lv[l].P + j * d;
       float s = 0.f;
-      for (int i = 0; i < qn; ++i) s = fmaf(s_val[w][i], __ldg(c + s_col[w][i]), s);
+      for (int64_t i = 0; i < qn; ++i) s = fmaf(qv[i], __ldg(c + qc[i]), s);
       return cn2_flat[cn2_off[l] + j] + qq - 2.f * s;
     };
     WarpTopK top;
@@ -418,20 +424,20 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
             const int32_t i = L1.members[mm];
             int64_t a = qi.xrp[i];
             const int64_t ae = qi.xrp[i + 1];
-            int b = 0;
+            int64_t b = 0;
             float s = 0.f;
             while (a < ae || b < qn) {
               float t;
               const int32_t ca = a < ae ? __ldg(qi.xcol + a) : 0x7fffffff;
-              const int32_t cb = b < qn ? s_col[w][b] : 0x7fffffff;
+              const int32_t cb = b < qn ? qc[b] : 0x7fffffff;
               if (ca < cb) {
                 t = __ldg(qi.xval + a);
                 ++a;
               } else if (cb < ca) {
-                t = s_val[w][b];
+                t = qv[b];
                 ++b;
               } else {
-                t = __ldg(qi.xval + a) - s_val[w][b];
+                t = __ldg(qi.xval + a) - qv[b];
                 ++a;
                 ++b;
               }

@@ -143,3 +143,49 @@ def test_distributed_mode_exchanges_gloo(tmp_path):
     port = _free_port()
     mp.spawn(_cluster_worker, args=(2, port, str(tmp_path)), nprocs=2, join=True)
     assert (tmp_path / "ok").exists()
+
+
+def _host_coll_worker(rank, world, port, out_dir):
+    """The host transport of libmask's communicator (api.host_collective, the function
+    mask_comm_init_host calls) over gloo: every kind and dtype the library issues."""
+    import ctypes as C
+
+    from paper_2208_02734_b200 import _lib
+    from paper_2208_02734_b200.api import host_collective
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        for dt, code in [(np.float32, 0),
+                         (np.float64, 1), (np.int32, 2), (np.int64, 3), (np.uint64, 4)]:
+            a = (np.arange(6) + 10 * rank).astype(dt)
+            assert host_collective(_lib.MASK_COLL_ALLREDUCE, a.ctypes.data, None, a.size, code, _lib.MASK_COLL_SUM) == 0
+            np.testing.assert_array_equal(a, sum((np.arange(6) + 10 * r) for r in range(world)).astype(dt))
+            b = (np.arange(4) * (rank + 1)).astype(dt)
+            assert host_collective(_lib.MASK_COLL_ALLREDUCE, b.ctypes.data, None, b.size, code, _lib.MASK_COLL_MAX) == 0
+            np.testing.assert_array_equal(b, (np.arange(4) * world).astype(dt))
+            c = np.full(5, rank + 7, dt)
+            assert host_collective(_lib.MASK_COLL_BROADCAST, c.ctypes.data, None, c.size, code, world - 1) == 0
+            np.testing.assert_array_equal(c, np.full(5, world - 1 + 7, dt))
+            s = np.full(3, rank, dt)
+            g = np.zeros(3 * world, dt)
+            assert host_collective(_lib.MASK_COLL_ALLGATHER, g.ctypes.data, s.ctypes.data, 3, code, 0) == 0
+            np.testing.assert_array_equal(g, np.repeat(np.arange(world), 3).astype(dt))
+        # u64 sums beyond 2^63 keep their bits (summed as int64 two's complement)
+        u = np.array([2 ** 63 + rank], np.uint64)
+        assert host_collective(_lib.MASK_COLL_ALLREDUCE, u.ctypes.data, None, 1, 4, _lib.MASK_COLL_SUM) == 0
+        assert int(u[0]) == (world * 2 ** 63 + sum(range(world))) % 2 ** 64
+        # an unknown kind is reported as a failure (the library turns it into MASK_ERR_NCCL)
+        z = np.zeros(1, np.float32)
+        assert host_collective(9, z.ctypes.data, None, 1, 0, 0) != 0
+        open(os.path.join(out_dir, f"ok{rank}"), "w").write("ok")
+    finally:
+        dist.destroy_process_group()
+
+
+def test_host_collective_transport_gloo(tmp_path):
+    world = 2
+    mp.spawn(_host_coll_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    for r in range(world):
+        assert (tmp_path / f"ok{r}").exists()

@@ -423,3 +423,23 @@ def test_sparse_queries_with_a_beam():
         _query_parity(idx, (rp, col, val), (qrp, qcol, qval), [48, 6], knn=10, beam=beam,
                       Qdev=_csr_dev(qrp, qcol, qval, 700), csr=True, dim=700)
     idx.free()
+
+
+def test_sparse_queries_longer_than_the_staged_limit():
+    """CSR queries with more non-zeros than the kernel stages in shared memory (1024) are
+    answered in full from global memory: identical to the oracle descent (no truncation)."""
+    d = 6000
+    rp, col, val = datagen.random_csr(420, 2000, d, 20)
+    inits = [datagen.init_indices(421, 1, 2000, 40), datagen.init_indices(421, 2, 40, 5)]
+    idx = mk.build(_csr_dev(rp, col, val, d), [40, 5], 5, inits)
+    # 30 queries: a mix of 1500- and 3000-non-zero rows plus short ones
+    parts = [datagen.random_csr(422, 10, d, 1500), datagen.random_csr(423, 10, d, 3000),
+             datagen.random_csr(424, 10, d, 20)]
+    qrp = np.concatenate([[0]] + [p[0][1:] + sum(q[0][-1] for q in parts[:i]) for i, p in enumerate(parts)])
+    qcol = np.concatenate([p[1] for p in parts])
+    qval = np.concatenate([p[2] for p in parts])
+    assert np.diff(qrp).max() > 1024
+    for beam in (1, 3):
+        _query_parity(idx, (rp, col, val), (qrp.astype(np.int64), qcol, qval), [40, 5], knn=10, beam=beam,
+                      Qdev=_csr_dev(qrp.astype(np.int64), qcol, qval, d), csr=True, dim=d)
+    idx.free()
