@@ -64,6 +64,7 @@ def lib():
         if _lib is None:
             L = C.CDLL(build())
             L.orc_num_threads.restype = C.c_int
+            L.orc_set_num_threads.argtypes = [C.c_int]
             L.orc_dist2.restype = C.c_double
             L.orc_dist2.argtypes = [C.c_int, dp, dp]
             L.orc_dist2_csr_dense.restype = C.c_double
@@ -90,6 +91,11 @@ def lib():
 
 def num_threads() -> int:
     return int(lib().orc_num_threads())
+
+
+def set_num_threads(t: int) -> None:
+    """OpenMP threads of the oracle's parallel loops (rows / queries split across threads)."""
+    lib().orc_set_num_threads(int(t))
 
 
 def _f64(a) -> np.ndarray:

@@ -53,6 +53,15 @@ int orc_num_threads(void) {
 #endif
 }
 
+/* threads of the later parallel loops (timing the single-core rate of the CPU baseline) */
+void orc_set_num_threads(int t) {
+#ifdef _OPENMP
+  if (t >= 1) omp_set_num_threads(t);
+#else
+  (void)t;
+#endif
+}
+
 /* ------------------------------------------------------------------ distances */
 
 /* Squared Euclidean distance, direct form (D9). */
