@@ -361,8 +361,10 @@ int32_t mask_get_displacement(const mask_index* idx, int32_t level, double* dmax
 /* per assignment pass of a build made with MASK_TRACE_PASSES (pass = 0 .. passes-1 as in
  * mask_level_info, the last one being the final assignment): P_host (k x dim fp32, may be NULL)
  * receives the prototypes the pass used and labels_host (may be NULL) the labels it produced
- * for this rank's items of the level.  MASK_ERR_ARG on a bad level / pass, MASK_ERR_UNSUPPORTED
- * when the build did not keep the trace. */
+ * for this rank's items of the level (labels_host needs room for n_items of mask_level_info).
+ * Returns the number of labels written (this rank's items: the shard's rows at level 1 of a
+ * multi-GPU build) or < 0: MASK_ERR_ARG on a bad level / pass, MASK_ERR_UNSUPPORTED when the
+ * build did not keep the trace. */
 int32_t mask_get_pass(const mask_index* idx, int32_t level, int32_t pass, float* P_host, int32_t* labels_host);
 
 /* ---------------------------------------------------------------- diagnostics

@@ -343,8 +343,10 @@ class Index:
         info = self.level_info(level)
         P = np.empty((info["k"], info["dim"]), np.float32)
         lab = np.empty(max(info["n_items"], 1), np.int32)
-        check(load().mask_get_pass(self.handle, level, int(pass_), P.ctypes.data, lab.ctypes.data))
-        return P, lab[: info["n_items"]]
+        n = load().mask_get_pass(self.handle, level, int(pass_), P.ctypes.data, lab.ctypes.data)
+        if n < 0:
+            check(n)
+        return P, lab[:n]
 
     def passes(self, level: int) -> List[Tuple[np.ndarray, np.ndarray]]:
         """Every assignment pass of a level (MASK_TRACE_PASSES builds): [(P_t, labels_t), ...]."""

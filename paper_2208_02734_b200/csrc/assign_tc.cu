@@ -651,9 +651,15 @@ __global__ void __launch_bounds__(128 + 128 * EPI_WG, 1)
 // block's tiles run, so the per-block prologue (A load) and tail (merge, exact d^2, flags)
 // overlap the tensor-core work instead of idling the SM.  Warps: 0 TMA producer, 1 MMA issuer,
 // 2 TMEM allocator, 4-7 A loader, 8.. epilogue warpgroups.
-template <int KA, int BN, int STAGES, int NACC, int EPI_WG>
+//   FOLD  ||x||^2 + ||c||^2 enter the accumulator through one extra K step (small d); else the
+//         epilogue adds them (two FADDs per score on the otherwise idle FMA pipe)
+//   ABUF  TMEM A buffers (2: the next block's A is staged while the current block runs; 1 for
+//         large d, where a block's thousands of tiles dwarf the A reload)
+//   NKC   128-byte K chunks per prototype tile (B stage = one chunk of the big and small parts)
+template <int KA, int BN, int STAGES, int NACC, int EPI_WG, bool FOLD = true, int ABUF = 2>
 struct PCfg {
   static constexpr int CW = 32, CWB = 128;
+  static constexpr int NKC = (KA + CW - 1) / CW;
   static constexpr int B_CHUNK = BN * CWB;
   static constexpr int STAGE_BYTES = 2 * B_CHUNK;
   static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
@@ -661,20 +667,23 @@ struct PCfg {
   static constexpr int SCRATCH_OFF = BAR_OFF + NBARS * 8 + 16;
   // per-block results of each epilogue warpgroup {s1, s2, j1, j2} x BM, double-buffered
   static constexpr int SCRATCH_FLOATS = 2 * 4 * BM * EPI_WG;
-  static constexpr int INFO_OFF = SCRATCH_OFF + SCRATCH_FLOATS * 4;  // [2][BM] rows, [2][BM] bounds
-  static constexpr int SMEM = INFO_OFF + 4 * BM * 4 + 1024;
+  static constexpr int INFO_OFF = SCRATCH_OFF + SCRATCH_FLOATS * 4;  // [2][BM] rows, bounds, ||x||^2
+  static constexpr int SMEM = INFO_OFF + 6 * BM * 4 + 1024;
   static constexpr int A_COL = NACC * BN;  // A buffer b: big at A_COL + 2*KA*b, small at + KA
-  static constexpr int NEED = A_COL + 4 * KA;
+  static constexpr int NEED = A_COL + 2 * ABUF * KA;
   static constexpr int TMEM_COLS = NEED <= 256 ? 256 : 512;
   static constexpr uint32_t IDESC = idesc_tf32<BM, BN>();
   static constexpr int NTHREADS = 256 + 128 * EPI_WG;
   static constexpr int EPI0 = 8;  // first epilogue warp
+  static constexpr int XSTEPS = FOLD ? KA / 8 - 1 : KA / 8;  // K steps of x (three MMAs each)
   static_assert(NEED <= 512, "TMEM budget");
-  static_assert(KA % 8 == 0 && KA <= CW, "folded K fits one chunk");
+  static_assert(KA % 8 == 0 && KA <= NKC * CW, "K layout");
+  static_assert(!FOLD || KA <= CW, "folded K fits one chunk");
+  static_assert(ABUF == 1 || ABUF == 2, "A buffers");
   static_assert(SMEM <= 232448, "shared memory budget");
 };
 
-template <int KA, int BN, int STAGES, int NACC, int EPI_WG>
+template <int KA, int BN, int STAGES, int NACC, int EPI_WG, bool FOLD, int ABUF>
 __global__ void __launch_bounds__(256 + 128 * EPI_WG, 1)
     k_assign_tc_persist(const __grid_constant__ CUtensorMap tmBb, const __grid_constant__ CUtensorMap tmBs,
                         const float* __restrict__ X, const float* __restrict__ P, const float* __restrict__ cn2,
@@ -687,7 +696,7 @@ __global__ void __launch_bounds__(256 + 128 * EPI_WG, 1)
 #if !defined(MASK_TC_ABLATE)
   dbg = 0;  // development ablations / counters only in -DMASK_TC_ABLATE builds (tools/build_variant.py)
 #endif
-  using C = PCfg<KA, BN, STAGES, NACC, EPI_WG>;
+  using C = PCfg<KA, BN, STAGES, NACC, EPI_WG, FOLD, ABUF>;
   constexpr int COLS = BN / EPI_WG;
   static_assert(COLS % 32 == 0 && COLS / 32 <= 2, "epilogue chunking (two register buffers)");
   extern __shared__ uint8_t smem_raw[];
@@ -707,6 +716,7 @@ __global__ void __launch_bounds__(256 + 128 * EPI_WG, 1)
   float* scratch = reinterpret_cast<float*>(smem + C::SCRATCH_OFF);
   int32_t* s_row = reinterpret_cast<int32_t*>(smem + C::INFO_OFF);
   int32_t* s_ub = s_row + 2 * BM;
+  float* s_xx = reinterpret_cast<float*>(s_ub + 2 * BM);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ntiles = (int)((k + BN - 1) / BN);
@@ -750,19 +760,21 @@ __global__ void __launch_bounds__(256 + 128 * EPI_WG, 1)
       int64_t gp = 0;
       for (int64_t rb = blockIdx.x; rb < nblocks; rb += gridDim.x) {
         for (int t = 0; t < ntiles; ++t, ++gp) {
-          mbar_wait_spin(&empty[stage], phase ^ 1);
-          PT_STAMP((dbg & 8) && blockIdx.x == 0 && gp < kPT, 8, gp);
-          uint8_t* dst = Bst + stage * C::STAGE_BYTES;
-          if (dbg & 4) {  // ablation: no B traffic
-            mbar_arrive(&full[stage]);
-          } else {
-            mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
-            tma_load_2d(dst, &tmBb, &full[stage], 0, t * BN);
-            tma_load_2d(dst + C::B_CHUNK, &tmBs, &full[stage], 0, t * BN);
-          }
-          if (++stage == STAGES) {
-            stage = 0;
-            phase ^= 1;
+          for (int c = 0; c < C::NKC; ++c) {
+            mbar_wait_spin(&empty[stage], phase ^ 1);
+            PT_STAMP((dbg & 8) && blockIdx.x == 0 && gp < kPT && c == 0, 8, gp);
+            uint8_t* dst = Bst + stage * C::STAGE_BYTES;
+            if (dbg & 4) {  // ablation: no B traffic
+              mbar_arrive(&full[stage]);
+            } else {
+              mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
+              tma_load_2d(dst, &tmBb, &full[stage], c * C::CW, t * BN);
+              tma_load_2d(dst + C::B_CHUNK, &tmBs, &full[stage], c * C::CW, t * BN);
+            }
+            if (++stage == STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
           }
         }
       }
@@ -773,7 +785,6 @@ __global__ void __launch_bounds__(256 + 128 * EPI_WG, 1)
     // one is blocked feeding the tensor core's instruction queue, the other has already passed
     // its barrier waits, so the per-tile control path (commits, two waits) never drains the
     // queue (a single issuer left the pipe idle ~35% of the time at d = 16).
-    static_assert((STAGES & (STAGES - 1)) == 0, "stage ring indexed by masking");
     const int par = warp == 1 ? 0 : 1;
     int g0 = 0;       // first global tile of the block
     int i = 0;       // block iteration of this CTA
@@ -781,45 +792,55 @@ __global__ void __launch_bounds__(256 + 128 * EPI_WG, 1)
       const int first = (int)((g0 & 1) == par ? 0 : 1);  // this issuer's first tile of the block
       if (first >= ntiles) continue;
       const int last = first + (ntiles - 1 - first) / 2 * 2;
-      const int ab = i & 1;
-      mbar_wait_spin(&afull[ab], (i >> 1) & 1);
+      const int ab = i % ABUF;
+      mbar_wait_spin(&afull[ab], (i / ABUF) & 1);
       tc_fence_after();
       const uint32_t a_big = tmem_base + C::A_COL + 2 * KA * ab, a_small = a_big + KA;
       for (int t = first; t < ntiles; t += 2) {
         const int g = g0 + t;
-        const int stage = (int)(g & (STAGES - 1));
-        const uint32_t phase = (uint32_t)((g / STAGES) & 1);
         const int acc = (int)(g % NACC);
         const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
         mbar_wait_spin(&tempty[acc], ((g / NACC) & 1) ^ 1);
         tc_fence_after();
         const bool ptr = (dbg & 8) && blockIdx.x == 0 && lane == 0 && g < kPT;
         PT_STAMP(ptr, 0, g);
-        mbar_wait_spin(&full[stage], phase);
-        tc_fence_after();
-        PT_STAMP(ptr, 1, g);
-        if (lane == 0) {
-          const uint32_t bb = smem_u32(Bst + stage * C::STAGE_BYTES);
-          const uint32_t bs = bb + C::B_CHUNK;
 #pragma unroll
-          for (int ks = 0; ks < KA / 8 - 1; ++ks) {
-            if (dbg & 2) break;  // ablation: no MMA
-            const uint64_t dbb = smem_desc<C::CWB>(bb + ks * 32), dbs = smem_desc<C::CWB>(bs + ks * 32);
-            mma_tf32_ts(d_tmem, a_small + ks * 8, dbb, C::IDESC, ks != 0);
-            mma_tf32_ts(d_tmem, a_big + ks * 8, dbs, C::IDESC, 1u);
-            mma_tf32_ts(d_tmem, a_big + ks * 8, dbb, C::IDESC, 1u);
+        for (int c = 0; c < C::NKC; ++c) {
+          const int64_t gc = (int64_t)g * C::NKC + c;  // global chunk: ring slot and phase
+          const int stage = (int)(gc % STAGES);
+          const uint32_t phase = (uint32_t)((gc / STAGES) & 1);
+          mbar_wait_spin(&full[stage], phase);
+          tc_fence_after();
+          if (c == 0) PT_STAMP(ptr, 1, g);
+          if (lane == 0) {
+            const uint32_t bb = smem_u32(Bst + stage * C::STAGE_BYTES);
+            const uint32_t bs = bb + C::B_CHUNK;
+#pragma unroll
+            for (int ks = 0; ks < 4; ++ks) {
+              const int s8 = c * 4 + ks;  // global K step
+              if (s8 >= KA / 8 || (dbg & 2)) break;  // (dbg 2, ablation: no MMA)
+              const uint64_t dbb = smem_desc<C::CWB>(bb + ks * 32);
+              if (s8 < C::XSTEPS) {
+                const uint64_t dbs = smem_desc<C::CWB>(bs + ks * 32);
+                mma_tf32_ts(d_tmem, a_small + s8 * 8, dbb, C::IDESC, s8 != 0);
+                mma_tf32_ts(d_tmem, a_big + s8 * 8, dbs, C::IDESC, 1u);
+                mma_tf32_ts(d_tmem, a_big + s8 * 8, dbb, C::IDESC, 1u);
+              } else {
+                // fold step: ||c||^2 + ||x||^2 from exact 1-products of the split norms (one MMA)
+                mma_tf32_ts(d_tmem, a_big + s8 * 8, dbb, C::IDESC, 1u);
+              }
+            }
+            mma_commit(&empty[stage]);
+            if (c == C::NKC - 1) {
+              mma_commit(&tfull[acc]);
+              // this issuer's MMAs on the block's A are done (aempty counts one arrive per issuer
+              // that has tiles in the block)
+              if (t == last) mma_commit(&aempty[ab]);
+            }
           }
-          // fold step: ||c||^2 + ||x||^2 from exact 1-products of the split norms (one MMA)
-          constexpr int KF = KA / 8 - 1;
-          if (!(dbg & 2)) mma_tf32_ts(d_tmem, a_big + KF * 8, smem_desc<C::CWB>(bb + KF * 32), C::IDESC, 1u);
-          mma_commit(&empty[stage]);
-          mma_commit(&tfull[acc]);
-          // this issuer's MMAs on the block's A are done (aempty counts one arrive per issuer
-          // that has tiles in the block)
-          if (t == last) mma_commit(&aempty[ab]);
-          PT_STAMP(ptr, 7, g);
+          __syncwarp();
         }
-        __syncwarp();
+        PT_STAMP(ptr, 7, g);
       }
     }
   } else if (warp >= 4 && warp < C::EPI0) {
@@ -900,9 +921,10 @@ __global__ void __launch_bounds__(256 + 128 * EPI_WG, 1)
     };
     int i = 0;
     for (int64_t rb = blockIdx.x; rb < nblocks; rb += gridDim.x, ++i) {
-      const int ab = i & 1;
-      mbar_wait_sleep(&aempty[ab], ((i >> 1) & 1) ^ 1);
-      mbar_wait_sleep(&iempty[ab], ((i >> 1) & 1) ^ 1);
+      const int ab = i % ABUF;  // TMEM A buffer
+      const int ib = i & 1;     // block info slot
+      mbar_wait_sleep(&aempty[ab], ((i / ABUF) & 1) ^ 1);
+      mbar_wait_sleep(&iempty[ib], ((i >> 1) & 1) ^ 1);
       tc_fence_after();
       const bool ptr = (dbg & 8) && blockIdx.x == 0 && rloc == 0 && i < 512;
       PT_STAMP(ptr, 5, i);
@@ -910,7 +932,7 @@ __global__ void __launch_bounds__(256 + 128 * EPI_WG, 1)
       const int64_t row = pos < n ? (perm ? (int64_t)__ldg(perm + pos) : pos) : n;
       const float xx = row < n ? __ldg(xn2 + row) : 0.f;
       const float* xr = X + row * d;
-      constexpr int KX = KA - 8;  // x columns (d rounded up to 8); [KX, KA) is the fold step
+      constexpr int KX = FOLD ? KA - 8 : KA;  // x columns (d rounded up to 8); [KX, KA) is the fold step
       float ub = INFINITY;
       if (prev_lab && row < n) {
         const int32_t a1 = __ldg(prev_lab + row), a2 = lab2[row];
@@ -934,8 +956,9 @@ __global__ void __launch_bounds__(256 + 128 * EPI_WG, 1)
           ub = (U + 2.f * err_coef * (xx + cm * cm)) * (1.f + 0x1p-12f) + 0x1p-100f;
         }
       }
-      s_row[ab * BM + rloc] = (int32_t)row;
-      s_ub[ab * BM + rloc] = __float_as_int(ub);
+      s_row[ib * BM + rloc] = (int32_t)row;
+      s_ub[ib * BM + rloc] = __float_as_int(ub);
+      s_xx[ib * BM + rloc] = xx;
       if ((dbg & 32) && i >= 2) {  // ablation: keep the stale A block (no TMEM stores)
         tc_fence_before();
         mbar_arrive_warp(&afull[ab]);
@@ -959,7 +982,7 @@ __global__ void __launch_bounds__(256 + 128 * EPI_WG, 1)
             vs[u + w] = __float_as_uint(tf32_rn(e[w] - b));
           }
         }
-        if (g8 == KX) {  // fold step: [1, 1, xx_b, xx_s] . [cn2_b, cn2_s, 1, 1] (big parts only)
+        if (FOLD && g8 == KX) {  // fold step: [1, 1, xx_b, xx_s] . [cn2_b, cn2_s, 1, 1] (big parts only)
           const float hb = tf32_rn(xx);
           vb[0] = vb[1] = __float_as_uint(1.0f);
           vb[2] = __float_as_uint(hb);
@@ -986,10 +1009,11 @@ __global__ void __launch_bounds__(256 + 128 * EPI_WG, 1)
     int i = 0;
     unsigned long long st_seen = 0, st_keyed = 0;
     for (int64_t rb = blockIdx.x; rb < nblocks; rb += gridDim.x, ++i) {
-      const int ab = i & 1;
-      mbar_wait_spin(&afull[ab], (i >> 1) & 1);  // block info published with the A block
-      const int32_t ubk = s_ub[ab * BM + rloc];
-      mbar_arrive_warp(&iempty[ab]);
+      const int ab = i % ABUF, ib = i & 1;
+      mbar_wait_spin(&afull[ab], (i / ABUF) & 1);  // block info published with the A block
+      const int32_t ubk = s_ub[ib * BM + rloc];
+      const float xx = FOLD ? 0.f : s_xx[ib * BM + rloc];
+      mbar_arrive_warp(&iempty[ib]);
       float g1 = INFINITY, g2 = INFINITY;
       int32_t gi = 0x7fffffff, gi2 = -1;
       for (int t = 0; t < ntiles; ++t, ++g) {
@@ -1028,6 +1052,22 @@ __global__ void __launch_bounds__(256 + 128 * EPI_WG, 1)
         PT_STAMP(ptr && wg == EPI_WG - 1, 4, g);
         // running top-2 keys of this tile; k2 starts at the pruning bound (low byte 0xFF marks
         // "no element": real keys carry a column < COLS in that byte)
+        if (!FOLD) {
+          // the d^2 estimate: accumulator (-2 x.c) + ||c_j||^2 + ||x||^2 (FMA pipe; cn2 is padded
+          // with +inf beyond k, so pad columns never win)
+#pragma unroll
+          for (int cc = 0; cc < COLS / 32; ++cc) {
+            const float4* c4 = reinterpret_cast<const float4*>(cn2 + (int64_t)t * BN + col0 + cc * 32);
+#pragma unroll
+            for (int e4 = 0; e4 < 8; ++e4) {
+              const float4 cv = __ldg(c4 + e4);
+              r[cc][4 * e4 + 0] = __float_as_uint((__uint_as_float(r[cc][4 * e4 + 0]) + cv.x) + xx);
+              r[cc][4 * e4 + 1] = __float_as_uint((__uint_as_float(r[cc][4 * e4 + 1]) + cv.y) + xx);
+              r[cc][4 * e4 + 2] = __float_as_uint((__uint_as_float(r[cc][4 * e4 + 2]) + cv.z) + xx);
+              r[cc][4 * e4 + 3] = __float_as_uint((__uint_as_float(r[cc][4 * e4 + 3]) + cv.w) + xx);
+            }
+          }
+        }
         int32_t k1 = 0x7fffffff;
         int32_t k2 = imin(ubk, __float_as_int(g2)) | 0xFF;
 #pragma unroll
@@ -1080,8 +1120,8 @@ __global__ void __launch_bounds__(256 + 128 * EPI_WG, 1)
         }
       }
       // hand this warpgroup's per-row top-2 to the tail (loader warpgroup)
-      mbar_wait_spin(&rempty[ab], ((i >> 1) & 1) ^ 1);
-      float* r1 = scratch + ab * 4 * BM * EPI_WG;
+      mbar_wait_spin(&rempty[ib], ((i >> 1) & 1) ^ 1);
+      float* r1 = scratch + ib * 4 * BM * EPI_WG;
       float* r2 = r1 + BM * EPI_WG;
       int32_t* ri = reinterpret_cast<int32_t*>(r2 + BM * EPI_WG);
       int32_t* ri2 = ri + BM * EPI_WG;
@@ -1089,7 +1129,7 @@ __global__ void __launch_bounds__(256 + 128 * EPI_WG, 1)
       r2[wg * BM + rloc] = g2;
       ri[wg * BM + rloc] = gi;
       ri2[wg * BM + rloc] = gi2;
-      mbar_arrive_warp(&rfull[ab]);
+      mbar_arrive_warp(&rfull[ib]);
     }
     if ((dbg & 128) && lane == 0) {
       atomicAdd(&g_chunk_stats[0], st_seen);
@@ -1217,20 +1257,20 @@ void launch_cfg(const float* X, int64_t n, int d, int kc, int64_t k_rows, const 
   if (tc_debug_mode() & 8) dump_trace((int)grid);
 }
 
-template <int KA, int BN, int STAGES, int NACC, int EPI_WG>
+template <int KA, int BN, int STAGES, int NACC, int EPI_WG, bool FOLD = true, int ABUF = 2>
 void launch_persist(const float* X, int64_t n, int d, int kc, int64_t k_rows, const float* P, const float* Pb,
                     const float* Ps, const float* cn2, int64_t k, const float* xn2, int32_t* labels, float* best,
                     int32_t* flag_rows, int32_t* flag_count, float err_coef, cudaStream_t st, const int* active,
                     const int32_t* perm, const int32_t* prev_lab, int32_t* lab2) {
-  using C = PCfg<KA, BN, STAGES, NACC, EPI_WG>;
+  using C = PCfg<KA, BN, STAGES, NACC, EPI_WG, FOLD, ABUF>;
   const CUtensorMap tBb = make_map(Pb, k_rows, kc, C::CW, BN);
   // the small part is only read by the x steps (KA - 8 columns); the fold step uses Pb alone
 #if defined(MASK_TC_PS_TRIM)
-  const CUtensorMap tBs = make_map(Ps, k_rows, kc, C::CW, BN, KA - 8);
+  const CUtensorMap tBs = make_map(Ps, k_rows, kc, C::CW, BN, FOLD ? KA - 8 : 0);
 #else
   const CUtensorMap tBs = make_map(Ps, k_rows, kc, C::CW, BN);
 #endif
-  auto kern = k_assign_tc_persist<KA, BN, STAGES, NACC, EPI_WG>;
+  auto kern = k_assign_tc_persist<KA, BN, STAGES, NACC, EPI_WG, FOLD, ABUF>;
   static bool attr_set = false;
   if (!attr_set) {
     MASK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
@@ -1274,6 +1314,14 @@ int64_t tc_operand_rows(int64_t k) { return (k + 255) / 256 * 256 + 256; }
 // representation (<= 2^-20 |x||c| summed over the three products and the dropped xs.cs)
 // + FP32 accumulation of 3*ceil(K/8) partial sums (<= 3 ceil(K/8) 2^-24 sum|x_i c_i|) + the
 // final rounding, bounded with |x||c| <= (|x|^2+|c|^2)/2.
+bool tc_legacy_large_d() {
+  static const bool v = [] {
+    const char* e = getenv("MASK_TC_LEGACY");
+    return e && e[0] == '1';
+  }();
+  return v;
+}
+
 float tc_err_coef(int d) {
   const double ks = std::ceil(tc_operand_cols(d) / 8.0);
   const double per = std::ldexp(1.0, -20) + 3.0 * ks * std::ldexp(1.0, -24) + std::ldexp(1.0, -22);
@@ -1309,18 +1357,38 @@ void launch_assign_tc(const float* X, int64_t n, int d, const float* P, const fl
     tc::launch_persist<32, MASK_TC_P_BN, MASK_TC_P_STAGES, MASK_TC_P_NACC, MASK_TC_P_EPI>(
         X, n, d, kc, kr, P, Pb, Ps, cn2, k, xn2, labels, best, flag_rows, flag_count, coef, st, active, perm,
         prev_lab, lab2);
-  else if (d <= 32)
-    tc::launch_cfg<32, 1, 32, 192, 4, 2, false, 3>(X, n, d, kc, kr, P, Pb, Ps, cn2, k, xn2, labels, best, flag_rows,
-                                                   flag_count, coef, st, active);
-  else if (d <= 64)
-    tc::launch_cfg<32, 2, 64, 128, 6, 3, false, 2>(X, n, d, kc, kr, P, Pb, Ps, cn2, k, xn2, labels, best, flag_rows,
-                                                   flag_count, coef, st, active);
-  else if (d <= 96)
-    tc::launch_cfg<32, 3, 96, 128, 6, 2, false, 2>(X, n, d, kc, kr, P, Pb, Ps, cn2, k, xn2, labels, best, flag_rows,
-                                                   flag_count, coef, st, active);
-  else
-    tc::launch_cfg<32, 4, 128, 128, 6, 2, false, 2>(X, n, d, kc, kr, P, Pb, Ps, cn2, k, xn2, labels, best,
-                                                    flag_rows, flag_count, coef, st, active);
+  else if (tc_legacy_large_d()) {  // MASK_TC_LEGACY=1: the round-1 one-CTA-per-block kernel (A/B runs)
+    if (d <= 32)
+      tc::launch_cfg<32, 1, 32, 192, 4, 2, false, 3>(X, n, d, kc, kr, P, Pb, Ps, cn2, k, xn2, labels, best, flag_rows,
+                                                     flag_count, coef, st, active);
+    else if (d <= 64)
+      tc::launch_cfg<32, 2, 64, 128, 6, 3, false, 2>(X, n, d, kc, kr, P, Pb, Ps, cn2, k, xn2, labels, best, flag_rows,
+                                                     flag_count, coef, st, active);
+    else if (d <= 96)
+      tc::launch_cfg<32, 3, 96, 128, 6, 2, false, 2>(X, n, d, kc, kr, P, Pb, Ps, cn2, k, xn2, labels, best, flag_rows,
+                                                     flag_count, coef, st, active);
+    else
+      tc::launch_cfg<32, 4, 128, 128, 6, 2, false, 2>(X, n, d, kc, kr, P, Pb, Ps, cn2, k, xn2, labels, best,
+                                                      flag_rows, flag_count, coef, st, active);
+  } else {
+    // d > 24: the persistent kernel without the fold step (||c||^2 + ||x||^2 added by the
+    // epilogue, two more roundings: + 2^-21 (||x||^2 + ||c||^2) on the gap bound), the same
+    // raw-minimum / bound-pruned epilogue and label-sorted rows as small d.  K = d rounded up
+    // to a whole 32-column chunk (zero columns add exact zeros)
+    const float c2 = coef + std::ldexp(1.0f, -21);
+    if (d <= 32)
+      tc::launch_persist<32, 192, 4, 2, 3, false, 2>(X, n, d, kc, kr, P, Pb, Ps, cn2, k, xn2, labels, best,
+                                                     flag_rows, flag_count, c2, st, active, perm, prev_lab, lab2);
+    else if (d <= 64)
+      tc::launch_persist<64, 128, 6, 2, 2, false, 2>(X, n, d, kc, kr, P, Pb, Ps, cn2, k, xn2, labels, best,
+                                                     flag_rows, flag_count, c2, st, active, perm, prev_lab, lab2);
+    else if (d <= 96)
+      tc::launch_persist<96, 128, 6, 2, 2, false, 1>(X, n, d, kc, kr, P, Pb, Ps, cn2, k, xn2, labels, best,
+                                                     flag_rows, flag_count, c2, st, active, perm, prev_lab, lab2);
+    else
+      tc::launch_persist<128, 128, 6, 2, 2, false, 1>(X, n, d, kc, kr, P, Pb, Ps, cn2, k, xn2, labels, best,
+                                                      flag_rows, flag_count, c2, st, active, perm, prev_lab, lab2);
+  }
 }
 
 }  // namespace mask

@@ -539,11 +539,11 @@ void assign_pass(const Input& in, const float* P, int64_t k, int flags, int32_t*
   if (!ws.Pb.p) {
     ws.Pb.alloc((size_t)tc_operand_rows(k) * kc);
     ws.Ps.alloc((size_t)tc_operand_rows(k) * kc);
-    ws.cn2.alloc(k_pad);
+    ws.cn2.alloc(tc_operand_rows(k));  // +inf beyond k: the epilogue reads whole tiles
     ws.flag_rows.alloc(n);
     ws.flag_count.alloc(1);
     ws.fix_keys.alloc((size_t)n);
-    launch_fill(ws.cn2.p + k, k_pad - k, INFINITY, st);
+    launch_fill(ws.cn2.p + k, tc_operand_rows(k) - k, INFINITY, st);
     ws.lab2.alloc(n);
     MASK_CUDA(cudaMemsetAsync(ws.lab2.p, 0xff, sizeof(int32_t) * n, st));
   }
@@ -1868,7 +1868,8 @@ int32_t mask_get_trace(const mask_index* idx, int32_t level, double* J, int64_t*
 }
 
 int32_t mask_get_pass(const mask_index* idx, int32_t level, int32_t pass, float* P_host, int32_t* labels_host) {
-  return guarded([&] {
+  int32_t written = 0;
+  const int32_t rc = guarded([&] {
     const Level& L = level_of(idx, level);
     MASK_REQUIRE(L.trace_T >= 0 && L.P_trace.p, MASK_ERR_UNSUPPORTED, "the build did not keep a pass trace (MASK_TRACE_PASSES)");
     MASK_REQUIRE(pass >= 0 && pass <= L.trace_loop_passes, MASK_ERR_ARG, "pass out of range");
@@ -1879,7 +1880,9 @@ int32_t mask_get_pass(const mask_index* idx, int32_t level, int32_t pass, float*
     const int64_t n = L.trace_n;
     if (labels_host && n)
       MASK_CUDA(cudaMemcpy(labels_host, L.lab_trace.p + (size_t)slot * n, sizeof(int32_t) * n, cudaMemcpyDeviceToHost));
+    written = (int32_t)n;
   });
+  return rc == MASK_OK ? written : rc;
 }
 
 int32_t mask_get_displacement(const mask_index* idx, int32_t level, double* dmax, int32_t cap) {
