@@ -366,4 +366,81 @@ void launch_assign_csr(const int64_t* row_ptr, const int32_t* col, const float* 
   MASK_LAUNCH_CHECK();
 }
 
+// K3 hot set on the device (no host round trip): the H columns with the most non-zeros (lower
+// index on equal counts; never a zero-count column).  One block: a binary search for the count
+// threshold c* = min{c : #(cnt > c) < H}, then every column above c* and the lowest-index
+// columns at c* until H, slots in ascending column order within each group.
+__global__ void __launch_bounds__(1024) k_select_hot(const int32_t* __restrict__ cnt, int d, int H,
+                                                     int32_t* __restrict__ hotcols, int16_t* __restrict__ colslot) {
+  __shared__ int s_red[32];
+  __shared__ int s_scan[32];
+  __shared__ int s_base;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, nw = blockDim.x >> 5;
+  auto block_sum = [&](int v) {
+    v = __reduce_add_sync(0xffffffffu, v);
+    __syncthreads();
+    if (lane == 0) s_red[w] = v;
+    __syncthreads();
+    int t = lane < nw ? s_red[lane] : 0;
+    return __reduce_add_sync(0xffffffffu, t);
+  };
+  auto block_max = [&](int v) {
+    v = __reduce_max_sync(0xffffffffu, v);
+    __syncthreads();
+    if (lane == 0) s_red[w] = v;
+    __syncthreads();
+    int t = lane < nw ? s_red[lane] : 0;
+    return __reduce_max_sync(0xffffffffu, t);
+  };
+  for (int c = tid; c < d; c += blockDim.x) colslot[c] = -1;
+  for (int h = tid; h < H; h += blockDim.x) hotcols[h] = -1;
+  int m = 0;
+  for (int c = tid; c < d; c += blockDim.x) m = max(m, cnt[c]);
+  const int M = block_max(m);
+  auto greater = [&](int thr) {
+    int g = 0;
+    for (int c = tid; c < d; c += blockDim.x) g += cnt[c] > thr ? 1 : 0;
+    return block_sum(g);
+  };
+  int lo = 0, hi = M;
+  while (lo < hi) {  // (uniform across the block)
+    const int mid = lo + (hi - lo) / 2;
+    if (greater(mid) < H) hi = mid;
+    else lo = mid + 1;
+  }
+  const int cstar = lo;
+  // ordered compaction: pass 0 = columns above c*, pass 1 = columns at c* (c* > 0) up to H
+  if (tid == 0) s_base = 0;
+  __syncthreads();
+  for (int pass = 0; pass < 2; ++pass) {
+    if (pass == 1 && cstar == 0) break;
+    for (int c0 = 0; c0 < d; c0 += blockDim.x) {
+      const int c = c0 + tid;
+      const bool f = c < d && (pass == 0 ? cnt[c] > cstar : cnt[c] == cstar);
+      const unsigned b = __ballot_sync(0xffffffffu, f);
+      if (lane == 0) s_scan[w] = __popc(b);
+      __syncthreads();
+      int before = 0, total = 0;
+      for (int i = 0; i < nw; ++i) {
+        const int v = s_scan[i];
+        before += i < w ? v : 0;
+        total += v;
+      }
+      const int pos = s_base + before + __popc(b & ((1u << lane) - 1));
+      if (f && pos < H) {
+        hotcols[pos] = c;
+        colslot[c] = (int16_t)pos;
+      }
+      __syncthreads();
+      if (tid == 0) s_base += total;
+      __syncthreads();
+    }
+  }
+}
+
+void launch_select_hot(const int32_t* cnt, int d, int H, int32_t* hotcols, int16_t* colslot, cudaStream_t st) {
+  k_select_hot<<<1, 1024, 0, st>>>(cnt, d, H, hotcols, colslot);
+  MASK_LAUNCH_CHECK();
+}
+
 }  // namespace mask

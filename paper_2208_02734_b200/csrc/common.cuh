@@ -212,6 +212,13 @@ void launch_gather_csr_rows(const int64_t* row_ptr, const int32_t* col, const fl
 // segment unspecified)
 void launch_children(const int32_t* labels, int64_t n, int64_t k, int64_t* offsets,
                      int32_t* members, int32_t* cursor_ws, cudaStream_t st);
+// CSR structure check on the device: *err = OR of 1 (row_ptr), 2 (column range), 4 (column order)
+void launch_check_csr(const int64_t* rp, const int32_t* col, int64_t rows, int64_t nnz, int dim, int* err,
+                      cudaStream_t st);
+// device top-H column selection for K3's hot set from a column histogram: hotcols[0..H) and
+// colslot[d] (slot or -1); columns by non-zero count (more first), lower index on equal counts,
+// zero-count columns never hot
+void launch_select_hot(const int32_t* cnt, int d, int H, int32_t* hotcols, int16_t* colslot, cudaStream_t st);
 // finite check: flag set to 1 if any non-finite value
 void launch_check_finite(const float* v, int64_t count, int32_t* flag, cudaStream_t st);
 void launch_fill(float* p, int64_t count, float v, cudaStream_t st);

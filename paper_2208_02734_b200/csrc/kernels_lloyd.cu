@@ -1237,5 +1237,36 @@ void launch_transpose(const float* P, int64_t k, int d, float* PT, cudaStream_t 
   MASK_LAUNCH_CHECK();
 }
 
-}  // namespace mask
+// CSR structure check on the device (include/mask.h mask_matrix: row_ptr[0] = 0, non-decreasing,
+// row_ptr[rows] = nnz, columns strictly increasing within a row and < dim): a warp per row,
+// error bits OR-ed into *err (1 = row_ptr, 2 = column range, 4 = column order).
+__global__ void k_check_csr(const int64_t* __restrict__ rp, const int32_t* __restrict__ col, int64_t rows,
+                            int64_t nnz, int dim, int* __restrict__ err) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  if (blockIdx.x == 0 && threadIdx.x == 0 && (rp[0] != 0 || rp[rows] != nnz)) atomicOr(err, 1);
+  int bits = 0;
+  for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < rows; r += warps) {
+    const int64_t a = rp[r], b = rp[r + 1];
+    if (a < 0 || b < a || b > nnz) {
+      bits |= 1;
+      continue;
+    }
+    for (int64_t q = a + lane; q < b; q += 32) {
+      const int32_t c = col[q];
+      if (c < 0 || c >= dim) bits |= 2;
+      if (q > a && col[q - 1] >= c) bits |= 4;
+    }
+  }
+  bits = __reduce_or_sync(0xffffffffu, bits);
+  if (lane == 0 && bits) atomicOr(err, bits);
+}
 
+void launch_check_csr(const int64_t* rp, const int32_t* col, int64_t rows, int64_t nnz, int dim, int* err,
+                      cudaStream_t st) {
+  MASK_CUDA(cudaMemsetAsync(err, 0, sizeof(int), st));
+  k_check_csr<<<grid_for(rows * 32, 256), 256, 0, st>>>(rp, col, rows, nnz, dim, err);
+  MASK_LAUNCH_CHECK();
+}
+
+}  // namespace mask

@@ -396,21 +396,23 @@ void check_matrix(const mask_matrix* m, const char* what) {
   }
 }
 
-// Host-side CSR structure check (sorted, unique, in range); device CSR is copied down first.
-void check_csr_structure(const mask_matrix* m, cudaStream_t st) {
-  std::vector<int64_t> rp(m->rows + 1);
-  std::vector<int32_t> col(m->nnz);
-  if (m->memory == MASK_MEM_HOST) {
-    std::memcpy(rp.data(), m->row_ptr, sizeof(int64_t) * rp.size());
-    if (m->nnz) std::memcpy(col.data(), m->col_idx, sizeof(int32_t) * col.size());
-  } else {
-    MASK_CUDA(cudaMemcpyAsync(rp.data(), m->row_ptr, sizeof(int64_t) * rp.size(),
-                              cudaMemcpyDeviceToHost, st));
-    if (m->nnz)
-      MASK_CUDA(cudaMemcpyAsync(col.data(), m->col_idx, sizeof(int32_t) * col.size(),
-                                cudaMemcpyDeviceToHost, st));
-    MASK_CUDA(cudaStreamSynchronize(st));
-  }
+// CSR structure check (sorted, unique, in range) of device arrays: one kernel, one 4-byte read.
+void check_csr_device(const int64_t* rp, const int32_t* col, int64_t rows, int64_t nnz, int dim, cudaStream_t st) {
+  DevBuf<int> err(1);
+  launch_check_csr(rp, col, rows, nnz, dim, err.p, st);
+  int h = 0;
+  MASK_CUDA(cudaMemcpyAsync(&h, err.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  MASK_CUDA(cudaStreamSynchronize(st));
+  MASK_REQUIRE(!(h & 1), MASK_ERR_ARG, "CSR: row_ptr[0] must be 0, non-decreasing, row_ptr[rows] == nnz");
+  MASK_REQUIRE(!(h & 2), MASK_ERR_ARG, "CSR: column index out of range");
+  MASK_REQUIRE(!(h & 4), MASK_ERR_ARG, "CSR: columns not strictly increasing in a row");
+}
+
+// Host-side CSR structure check of host arrays (argument validation before any device work;
+// device arrays are checked on the device by check_csr_device).
+void check_host_csr(const mask_matrix* m) {
+  const int64_t* rp = m->row_ptr;
+  const int32_t* col = m->col_idx;
   MASK_REQUIRE(rp[0] == 0 && rp[m->rows] == m->nnz, MASK_ERR_ARG, "CSR: row_ptr[0] must be 0 and row_ptr[rows] == nnz");
   for (int64_t r = 0; r < m->rows; ++r) {
     MASK_REQUIRE(rp[r + 1] >= rp[r], MASK_ERR_ARG, "CSR: row_ptr not non-decreasing");
@@ -488,31 +490,14 @@ void assign_pass(const Input& in, const float* P, int64_t k, int flags, int32_t*
     ws.kernel_id = 2;
     const bool chunked = csr_chunked_supported(d, k) && !(flags & MASK_FORCE_SIMT);
     if (chunked && !ws.colslot.p) {
-      // hot set = the csr_chunked_hot() columns with the most non-zeros (one host round trip)
+      // hot set = the csr_chunked_hot() columns with the most non-zeros (selected on the device)
       DevBuf<int32_t> cnt(d);
       launch_col_hist(in.col, in.nnz, d, cnt.p, st);
-      std::vector<int32_t> hc(d);
-      MASK_CUDA(cudaMemcpyAsync(hc.data(), cnt.p, sizeof(int32_t) * d, cudaMemcpyDeviceToHost, st));
-      MASK_CUDA(cudaStreamSynchronize(st));
-      std::vector<int32_t> order(d);
-      for (int c = 0; c < d; ++c) order[c] = c;
       const int H = csr_chunked_hot();
-      const int nh = std::min(H, d);
-      std::partial_sort(order.begin(), order.begin() + nh, order.end(),
-                        [&](int a, int b) { return hc[a] != hc[b] ? hc[a] > hc[b] : a < b; });
-      std::vector<int16_t> slot(d, (int16_t)-1);
-      std::vector<int32_t> hot(H, -1);
-      for (int h = 0; h < nh; ++h) {
-        if (hc[order[h]] == 0) break;
-        hot[h] = order[h];
-        slot[order[h]] = (int16_t)h;
-      }
       ws.colslot.alloc(d);
       ws.hotcols.alloc(H);
       ws.csr_state.alloc(std::max<int64_t>(n, 1));
-      MASK_CUDA(cudaMemcpyAsync(ws.colslot.p, slot.data(), sizeof(int16_t) * d, cudaMemcpyHostToDevice, st));
-      MASK_CUDA(cudaMemcpyAsync(ws.hotcols.p, hot.data(), sizeof(int32_t) * H, cudaMemcpyHostToDevice, st));
-      MASK_CUDA(cudaStreamSynchronize(st));  // host vectors go out of scope
+      launch_select_hot(cnt.p, d, H, ws.hotcols.p, ws.colslot.p, st);
     }
     if (ev) ev->mark(MASK_T_ASSIGN, st);
     if (chunked)
@@ -927,6 +912,22 @@ __global__ void k_add_offset(int64_t* v, int64_t n, int64_t off) {
     v[i] += off;
 }
 
+// The partition-ordered copy of the dense rows (K9's contiguous leaf scans) is an optimisation:
+// when the device cannot hold it the index keeps none and queries scan through the member ids.
+void gather_partition_best_effort(mask_index* idx, cudaStream_t st) {
+  const int64_t N = idx->n_global;
+  const int d = idx->dim;
+  try {
+    idx->Xpart.alloc((size_t)N * d);
+  } catch (const Error& e) {
+    if (e.code != MASK_ERR_OOM) throw;
+    cudaGetLastError();
+    idx->Xpart.release();
+    return;
+  }
+  launch_gather_partition(idx->X, d, idx->levels[0].members.p, N, idx->Xpart.p, st);
+}
+
 void build_impl(const mask_matrix* data, const mask_build_params* p, mask_comm* comm,
                 cudaStream_t st, mask_index** out) {
   MASK_REQUIRE(out != nullptr, MASK_ERR_ARG, "out is NULL");
@@ -975,11 +976,10 @@ void build_impl(const mask_matrix* data, const mask_build_params* p, mask_comm* 
     }
     n_prev = k;
   }
-  if (data->format == MASK_CSR_F32 && data->memory == MASK_MEM_HOST) check_csr_structure(data, st);
+  if (data->format == MASK_CSR_F32 && data->memory == MASK_MEM_HOST) check_host_csr(data);
   int ndev = 0;
   MASK_CUDA(cudaGetDeviceCount(&ndev));
   MASK_REQUIRE(ndev > 0, MASK_ERR_CUDA, "no CUDA device");
-  if (data->format == MASK_CSR_F32 && data->memory == MASK_MEM_DEVICE) check_csr_structure(data, st);
   if (comm && world > 1) {
     // every rank must build the same index: a hash of the parameters and init indices, its
     // max and min over the ranks must agree (MASK_ERR_ARG on every rank otherwise)
@@ -1058,6 +1058,19 @@ void build_impl(const mask_matrix* data, const mask_build_params* p, mask_comm* 
       in.rp = loc_rp.p;
       in.col = loc_col.p;
       in.val = loc_val.p;
+    }
+  }
+  if (data->format == MASK_CSR_F32 && data->memory == MASK_MEM_DEVICE) {
+    if (comm && world > 1) {  // every rank fails together (no rank left waiting in a collective)
+      DevBuf<int> err(1);
+      launch_check_csr(in.rp, in.col, data->rows, data->nnz, d, err.p, st);
+      coll_allreduce(comm, err.p, 1, kI32, true, st);
+      int h = 0;
+      MASK_CUDA(cudaMemcpyAsync(&h, err.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+      MASK_CUDA(cudaStreamSynchronize(st));
+      MASK_REQUIRE(h == 0, MASK_ERR_ARG, "CSR structure invalid on some rank (row_ptr / column range / order)");
+    } else {
+      check_csr_device(in.rp, in.col, data->rows, data->nnz, d, st);
     }
   }
   if (p->flags & MASK_VALIDATE_FINITE) {
@@ -1167,10 +1180,8 @@ void build_impl(const mask_matrix* data, const mask_build_params* p, mask_comm* 
     launch_children(L.labels.p, L.n_items, L.k, L.offsets.p, L.members.p, cursor.p, st);
   }
   // ---- dense rows in level-1 partition order for the leaf scans (one gather, n x d floats)
-  if (idx->format == MASK_DENSE_F32 && !(p->flags & MASK_NO_PARTITION_COPY)) {
-    idx->Xpart.alloc((size_t)N * d);
-    launch_gather_partition(idx->X, d, idx->levels[0].members.p, N, idx->Xpart.p, st);
-  }
+  if (idx->format == MASK_DENSE_F32 && !(p->flags & MASK_NO_PARTITION_COPY))
+    gather_partition_best_effort(idx.get(), st);
   if (idx->format == MASK_CSR_F32) {
     // ||c||^2 per level for sparse queries
     int64_t tot = 0;
@@ -1519,10 +1530,9 @@ int32_t mask_insert(mask_index* idx, const mask_matrix* points, int64_t* partiti
     L1.members = std::move(mem);
     L1.n_items = n + m;
     if (idx->Xpart.p) {  // the partitions changed: re-gather the partition-ordered rows
-      DevBuf<float> xp((size_t)(n + m) * d);
-      launch_gather_partition(idx->X, d, L1.members.p, n + m, xp.p, st);
+      idx->Xpart.release();  // (the old copy goes first: peak = data + one copy)
+      gather_partition_best_effort(idx, st);
       MASK_CUDA(cudaStreamSynchronize(st));
-      idx->Xpart = std::move(xp);
     }
     std::lock_guard<std::mutex> lock(idx->cover_mu);
     idx->cover_valid = false;
@@ -1569,7 +1579,7 @@ int32_t query_impl(const mask_index* idx, const mask_matrix* queries, int32_t k_
     const int32_t* Qcol = queries->col_idx;
     int64_t* ids = ids_out;
     float* d2 = d2_out;
-    if (queries->format == MASK_CSR_F32) check_csr_structure(queries, st);
+    if (queries->format == MASK_CSR_F32 && host) check_host_csr(queries);
     if (host) {
       if (queries->format == MASK_DENSE_F32) {
         qv.alloc((size_t)nq * queries->dim);
@@ -1591,6 +1601,8 @@ int32_t query_impl(const mask_index* idx, const mask_matrix* queries, int32_t k_
       d2_d.alloc((size_t)nq * k_nn);
       ids = ids_d.p;
       d2 = d2_d.p;
+    } else if (queries->format == MASK_CSR_F32) {
+      check_csr_device(Qrp, Qcol, nq, queries->nnz, queries->dim, st);
     }
     qi.routed = routed;
     qi.rstride = rstride;
@@ -1663,7 +1675,7 @@ int32_t mask_route(const float* registry, const int32_t* node_of, int64_t n_regi
       launch_route_dense(registry, node_of, n_registry, n_nodes, queries->values, nq, queries->dim, eps2, all,
                          routed_out, st);
     } else {
-      check_csr_structure(queries, st);
+      check_csr_device(queries->row_ptr, queries->col_idx, nq, queries->nnz, queries->dim, st);
       DevBuf<float> n2;
       n2.alloc(std::max<int64_t>(n_registry, 1));
       launch_route_csr(registry, n2.p, node_of, n_registry, n_nodes, queries->dim, queries->row_ptr,
@@ -1723,7 +1735,7 @@ int32_t mask_assign(const mask_matrix* data, const float* P, int64_t k, int32_t 
     MASK_REQUIRE(P != nullptr && labels_out != nullptr, MASK_ERR_ARG, "NULL argument");
     MASK_REQUIRE(k >= 1, MASK_ERR_ARG, "k must be >= 1");
     cudaStream_t st = as_stream(stream);
-    if (data->format == MASK_CSR_F32) check_csr_structure(data, st);
+    if (data->format == MASK_CSR_F32) check_csr_device(data->row_ptr, data->col_idx, data->rows, data->nnz, data->dim, st);
     Input in;
     in.format = data->format;
     in.dim = data->dim;

@@ -443,3 +443,30 @@ def test_sparse_queries_longer_than_the_staged_limit():
         _query_parity(idx, (rp, col, val), (qrp.astype(np.int64), qcol, qval), [40, 5], knn=10, beam=beam,
                       Qdev=_csr_dev(qrp.astype(np.int64), qcol, qval, d), csr=True, dim=d)
     idx.free()
+
+
+def test_csr_structure_errors_are_reported():
+    """Invalid CSR input (include/mask.h mask_matrix) is MASK_ERR_ARG from the device-side check,
+    for device and host data, builds, queries and mask_assign; the valid matrix still builds."""
+    rp, col, val = datagen.random_csr(430, 300, 200, 6)
+    inits = [datagen.init_indices(431, 1, 300, 12)]
+    bad_order = col.copy()
+    bad_order[[6, 7]] = bad_order[[7, 6]]  # row 1: columns not increasing
+    bad_range = col.copy()
+    bad_range[20] = 200  # column index == dim
+    bad_rp = rp.copy()
+    bad_rp[5] = bad_rp[4] - 1  # row_ptr decreasing
+    for c, r, msg in [(bad_order, rp, "strictly increasing"), (bad_range, rp, "out of range"), (col, bad_rp, "row_ptr")]:
+        for dev in (True, False):
+            data = _csr_dev(r, c, val, 200) if dev else mk.Csr(r, c, val, 200)
+            with pytest.raises(mk.MaskError, match=msg):
+                mk.build(data, [12], 2, inits)
+        with pytest.raises(mk.MaskError, match=msg):
+            mk.assign(_csr_dev(r, c, val, 200), t(np.zeros((4, 200), np.float32)))
+    idx = mk.build(_csr_dev(rp, col, val, 200), [12], 2, inits)
+    for c, r, msg in [(bad_order, rp, "strictly increasing"), (bad_range, rp, "out of range")]:
+        with pytest.raises(mk.MaskError, match=msg):
+            idx.query(_csr_dev(r, c, val, 200), knn=3)
+        with pytest.raises(mk.MaskError, match=msg):
+            idx.query(mk.Csr(r, c, val, 200), knn=3)
+    idx.free()
