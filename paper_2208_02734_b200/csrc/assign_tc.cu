@@ -790,11 +790,13 @@ __global__ void __launch_bounds__(256 + 128 * EPI_WG, 1)
     int i = 0;       // block iteration of this CTA
     for (int64_t rb = blockIdx.x; rb < nblocks; rb += gridDim.x, ++i, g0 += ntiles) {
       const int first = (int)((g0 & 1) == par ? 0 : 1);  // this issuer's first tile of the block
-      if (first >= ntiles) continue;
-      const int last = first + (ntiles - 1 - first) / 2 * 2;
       const int ab = i % ABUF;
+      // every block's afull phase is consumed, also by an issuer without tiles in it (k <= BN):
+      // with one A buffer a skipped phase would let the next parity wait pass a phase early
       mbar_wait_spin(&afull[ab], (i / ABUF) & 1);
       tc_fence_after();
+      if (first >= ntiles) continue;
+      const int last = first + (ntiles - 1 - first) / 2 * 2;
       const uint32_t a_big = tmem_base + C::A_COL + 2 * KA * ab, a_small = a_big + KA;
       for (int t = first; t < ntiles; t += 2) {
         const int g = g0 + t;

@@ -38,6 +38,9 @@ def test_native_library_is_the_one_loaded():
 ASSIGN_SHAPES = [
     (1000, 2, 100), (1037, 3, 7), (4099, 16, 300), (500, 17, 33), (257, 64, 1), (300, 128, 300),
     (2049, 8, 129), (777, 1, 5), (3000, 32, 64), (1500, 64, 513), (640, 96, 40), (300, 128, 257),
+    # one prototype tile, many row blocks (one TMEM A buffer for d > 64): every issuer keeps
+    # the per-block A phases in step
+    (5000, 128, 100), (3000, 96, 128), (4100, 64, 128), (2000, 40, 192),
 ]
 
 
