@@ -349,7 +349,7 @@ __global__ void __launch_bounds__(128 + 128 * EPI_WG, 1)
                 const float* __restrict__ xn2, int64_t n, int d, int64_t k, int32_t* __restrict__ labels,
                 float* __restrict__ best, int32_t* __restrict__ flag_rows, int32_t* __restrict__ flag_count,
                 float err_coef, int dbg,
-                const int* __restrict__ active) {
+                const int* __restrict__ active, int2* __restrict__ flag_pair) {
   if (active && !*active) return;  // level converged: this pass is skipped on the device
 #if !defined(MASK_TC_ABLATE)
   dbg = 0;  // development ablations / trace only in -DMASK_TC_ABLATE builds
@@ -630,7 +630,11 @@ __global__ void __launch_bounds__(128 + 128 * EPI_WG, 1)
         int base = 0;
         if (lane == 0) base = atomicAdd(flag_count, __popc(m));
         base = __shfl_sync(0xffffffffu, base, 0);
-        if (flag) flag_rows[base + __popc(m & ((1u << lane) - 1))] = (int32_t)row;
+        if (flag) {
+          const int pos = base + __popc(m & ((1u << lane) - 1));
+          flag_rows[pos] = (int32_t)row;
+          if (flag_pair) flag_pair[pos] = make_int2(gi, -1);  // (no third bound: full re-check)
+        }
       }
     }
     if (tr0) g_tc_trace[6][blockIdx.x] = gtimer();
@@ -665,8 +669,8 @@ struct PCfg {
   static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
   static constexpr int NBARS = 2 * STAGES + 2 * NACC + 10;
   static constexpr int SCRATCH_OFF = BAR_OFF + NBARS * 8 + 16;
-  // per-block results of each epilogue warpgroup {s1, s2, j1, j2} x BM, double-buffered
-  static constexpr int SCRATCH_FLOATS = 2 * 4 * BM * EPI_WG;
+  // per-block results of each epilogue warpgroup {s1, s2, j1, j2, s3lb} x BM, double-buffered
+  static constexpr int SCRATCH_FLOATS = 2 * 5 * BM * EPI_WG;
   static constexpr int INFO_OFF = SCRATCH_OFF + SCRATCH_FLOATS * 4;  // [2][BM] rows, bounds, ||x||^2
   static constexpr int SMEM = INFO_OFF + 6 * BM * 4 + 1024;
   static constexpr int A_COL = NACC * BN;  // A buffer b: big at A_COL + 2*KA*b, small at + KA
@@ -691,7 +695,7 @@ __global__ void __launch_bounds__(256 + 128 * EPI_WG, 1)
                         float* __restrict__ best, int32_t* __restrict__ flag_rows, int32_t* __restrict__ flag_count,
                         float err_coef, uint32_t key_mask, const int* __restrict__ active,
                         const int32_t* __restrict__ perm, const int32_t* __restrict__ prev_lab,
-                        int32_t* __restrict__ lab2, int dbg) {
+                        int32_t* __restrict__ lab2, int2* __restrict__ flag_pair, int dbg) {
   if (active && !*active) return;  // level converged: this pass is skipped on the device
 #if !defined(MASK_TC_ABLATE)
   dbg = 0;  // development ablations / counters only in -DMASK_TC_ABLATE builds (tools/build_variant.py)
@@ -861,16 +865,19 @@ __global__ void __launch_bounds__(256 + 128 * EPI_WG, 1)
     auto tail = [&](int ib) {  // block iteration ib of this CTA
       const int tb = ib & 1;
       mbar_wait_sleep(&rfull[tb], (ib >> 1) & 1);
-      const float* r1 = scratch + tb * 4 * BM * EPI_WG;
+      const float* r1 = scratch + tb * 5 * BM * EPI_WG;
       const float* r2 = r1 + BM * EPI_WG;
       const int32_t* ri = reinterpret_cast<const int32_t*>(r2 + BM * EPI_WG);
       const int32_t* ri2 = ri + BM * EPI_WG;
-      float g1 = r1[rloc], g2 = r2[rloc];
+      const float* r3 = reinterpret_cast<const float*>(ri2 + BM * EPI_WG);
+      float g1 = r1[rloc], g2 = r2[rloc], g3 = r3[rloc];
       int32_t gi = ri[rloc], gi2 = ri2[rloc];
 #pragma unroll
       for (int w = 1; w < EPI_WG; ++w) {  // lowest index on equal values
-        const float o1 = r1[w * BM + rloc], o2 = r2[w * BM + rloc];
+        const float o1 = r1[w * BM + rloc], o2 = r2[w * BM + rloc], o3 = r3[w * BM + rloc];
         const int32_t oi = ri[w * BM + rloc], oi2 = ri2[w * BM + rloc];
+        // third-smallest lower bound of the union (merge path of two sorted triples)
+        g3 = fminf(fminf(g3, o3), fminf(fmaxf(g1, o2), fmaxf(g2, o1)));
         if (o1 < g1 || (o1 == g1 && oi < gi)) {
           if (g1 <= o2) {
             g2 = g1;
@@ -888,7 +895,7 @@ __global__ void __launch_bounds__(256 + 128 * EPI_WG, 1)
       }
       const int64_t row = s_row[tb * BM + rloc];
       mbar_arrive_warp(&rempty[tb]);
-      bool flag = false;
+      bool flag = false, pair = false;
       if (row < n) {
         if (dbg) gi = gi < 0 ? 0 : (gi >= k ? (int32_t)(k - 1) : gi);  // ablation runs: keep in range
         labels[row] = gi;
@@ -912,13 +919,21 @@ __global__ void __launch_bounds__(256 + 128 * EPI_WG, 1)
         const float xx = __ldg(xn2 + row);
         const float thr = err_coef * (xx + __ldg(cn2 + gi)) + ldexpf(fmaxf(fabsf(g2), fabsf(g1)), -14);
         flag = (g2 - g1) <= thr;
+        // a flagged row whose every other score (lower bound g3: keyed chunks' third-smallest,
+        // skipped chunks' minima) lies beyond twice the window has exactly two candidates:
+        // K4 decides between them exactly, no re-scan
+        pair = flag && gi2 >= 0 && gi2 < k && gi2 != gi && (g3 - g1) > 2.f * thr;
       }
       const unsigned msk = __ballot_sync(0xffffffffu, flag);
       if (msk) {
         int base = 0;
         if (lane == 0) base = atomicAdd(flag_count, __popc(msk));
         base = __shfl_sync(0xffffffffu, base, 0);
-        if (flag) flag_rows[base + __popc(msk & ((1u << lane) - 1))] = (int32_t)row;
+        if (flag) {
+          const int pos = base + __popc(msk & ((1u << lane) - 1));
+          flag_rows[pos] = (int32_t)row;
+          if (flag_pair) flag_pair[pos] = make_int2(gi, pair ? gi2 : -1);
+        }
       }
     };
     int i = 0;
@@ -1016,8 +1031,9 @@ __global__ void __launch_bounds__(256 + 128 * EPI_WG, 1)
       const int32_t ubk = s_ub[ib * BM + rloc];
       const float xx = FOLD ? 0.f : s_xx[ib * BM + rloc];
       mbar_arrive_warp(&iempty[ib]);
-      float g1 = INFINITY, g2 = INFINITY;
+      float g1 = INFINITY, g2 = INFINITY, g3 = INFINITY;  // g3: lower bound of the third-smallest
       int32_t gi = 0x7fffffff, gi2 = -1;
+      int32_t smin = 0x7fffffff;  // smallest raw key of the chunks this row skipped
       for (int t = 0; t < ntiles; ++t, ++g) {
         const int acc = (int)(g % NACC);
         // polled, not suspended: the accumulator round trip (MMA -> epilogue -> MMA) must fit in
@@ -1072,6 +1088,9 @@ __global__ void __launch_bounds__(256 + 128 * EPI_WG, 1)
         }
         int32_t k1 = 0x7fffffff;
         int32_t k2 = imin(ubk, __float_as_int(g2)) | 0xFF;
+        // the tile's keyed elements alone (no bound marker): second smallest t2 and a lower bound t3
+        // of the third (a chunk's exact top-2 (c1, c2) stands for (c1, c2, >= c2))
+        int32_t t2 = 0x7fffffff, t3 = 0x7fffffff;
 #pragma unroll
         for (int cc = 0; cc < COLS / 32; ++cc) {
           if (dbg & 1) {  // ablation: no epilogue arithmetic
@@ -1093,11 +1112,22 @@ __global__ void __launch_bounds__(256 + 128 * EPI_WG, 1)
             ++st_seen;
             st_keyed += need ? 1 : 0;
           }
-          if (!need || (dbg & 256)) continue;  // dbg 256 (ablation): never key
+          if (!need || (dbg & 256)) {  // dbg 256 (ablation): never key
+            smin = imin(smin, c0);
+            continue;
+          }
 #endif
           int32_t c1, c2;
           chunk_top2(r[cc & 1], key_mask, (uint32_t)(cc * 32), key_mask >> 31, c1, c2);
+          t3 = imin(imin(t3, c2), imax(t2, c1));  // merge path of sorted triples (old t2, old k1)
+          t2 = imin(imin(t2, c2), imax(k1, c1));
           merge_top2(k1, k2, c1, c2);
+        }
+        {  // lower bound of the block's third-smallest so far (merge path with the running top-2)
+          const float v1 = k1 != 0x7fffffff ? __int_as_float(k1 & 0xFFFFFF00) : INFINITY;
+          const float v2 = t2 != 0x7fffffff ? __int_as_float(t2 & 0xFFFFFF00) : INFINITY;
+          const float v3 = t3 != 0x7fffffff ? __int_as_float(t3 & 0xFFFFFF00) : INFINITY;
+          g3 = fminf(fminf(g3, v3), fminf(fmaxf(g1, v2), fmaxf(g2, v1)));
         }
         if (k1 != 0x7fffffff) {
           const float v1 = __int_as_float(k1 & 0xFFFFFF00);
@@ -1123,14 +1153,19 @@ __global__ void __launch_bounds__(256 + 128 * EPI_WG, 1)
       }
       // hand this warpgroup's per-row top-2 to the tail (loader warpgroup)
       mbar_wait_spin(&rempty[ib], ((i >> 1) & 1) ^ 1);
-      float* r1 = scratch + ib * 4 * BM * EPI_WG;
+      float* r1 = scratch + ib * 5 * BM * EPI_WG;
       float* r2 = r1 + BM * EPI_WG;
       int32_t* ri = reinterpret_cast<int32_t*>(r2 + BM * EPI_WG);
       int32_t* ri2 = ri + BM * EPI_WG;
+      float* r3 = reinterpret_cast<float*>(ri2 + BM * EPI_WG);
       r1[wg * BM + rloc] = g1;
       r2[wg * BM + rloc] = g2;
       ri[wg * BM + rloc] = gi;
       ri2[wg * BM + rloc] = gi2;
+      // raw keys order as floats only when non-negative: a negative skipped minimum (a d^2 estimate
+      // below 0, i.e. a row on a prototype) gives no bound
+      const float sm = __int_as_float(smin);
+      r3[wg * BM + rloc] = fminf(g3, smin == 0x7fffffff ? INFINITY : (sm < 0.f ? -INFINITY : sm));
       mbar_arrive_warp(&rfull[ib]);
     }
     if ((dbg & 128) && lane == 0) {
@@ -1242,7 +1277,7 @@ template <int CW, int NKC, int KA, int BN, int STAGES, int NACC, bool FOLD, int 
 void launch_cfg(const float* X, int64_t n, int d, int kc, int64_t k_rows, const float* P, const float* Pb,
                 const float* Ps, const float* cn2, int64_t k, const float* xn2, int32_t* labels, float* best,
                 int32_t* flag_rows, int32_t* flag_count, float err_coef, cudaStream_t st,
-                const int* active) {
+                const int* active, int2* flag_pair) {
   using C = Cfg<CW, NKC, KA, BN, STAGES, NACC, FOLD, EPI_WG>;
   const CUtensorMap tBb = make_map(Pb, k_rows, kc, CW, BN);
   const CUtensorMap tBs = make_map(Ps, k_rows, kc, CW, BN);
@@ -1254,7 +1289,7 @@ void launch_cfg(const float* X, int64_t n, int d, int kc, int64_t k_rows, const 
   }
   const unsigned grid = (unsigned)((n + BM - 1) / BM);
   kern<<<grid, C::NTHREADS, C::SMEM, st>>>(tBb, tBs, X, P, cn2, xn2, n, d, k, labels, best, flag_rows, flag_count,
-                                           err_coef, tc_debug_mode(), active);
+                                           err_coef, tc_debug_mode(), active, flag_pair);
   MASK_LAUNCH_CHECK();
   if (tc_debug_mode() & 8) dump_trace((int)grid);
 }
@@ -1263,7 +1298,7 @@ template <int KA, int BN, int STAGES, int NACC, int EPI_WG, bool FOLD = true, in
 void launch_persist(const float* X, int64_t n, int d, int kc, int64_t k_rows, const float* P, const float* Pb,
                     const float* Ps, const float* cn2, int64_t k, const float* xn2, int32_t* labels, float* best,
                     int32_t* flag_rows, int32_t* flag_count, float err_coef, cudaStream_t st, const int* active,
-                    const int32_t* perm, const int32_t* prev_lab, int32_t* lab2) {
+                    const int32_t* perm, const int32_t* prev_lab, int32_t* lab2, int2* flag_pair) {
   using C = PCfg<KA, BN, STAGES, NACC, EPI_WG, FOLD, ABUF>;
   const CUtensorMap tBb = make_map(Pb, k_rows, kc, C::CW, BN);
   // the small part is only read by the x steps (KA - 8 columns); the fold step uses Pb alone
@@ -1281,7 +1316,8 @@ void launch_persist(const float* X, int64_t n, int d, int kc, int64_t k_rows, co
   const int64_t nblocks = (n + BM - 1) / BM;
   const unsigned grid = (unsigned)(nblocks < num_sms() ? nblocks : num_sms());
   kern<<<grid, C::NTHREADS, C::SMEM, st>>>(tBb, tBs, X, P, cn2, xn2, n, d, k, labels, best, flag_rows, flag_count,
-                                           err_coef, 0xFFFFFF00u, active, perm, prev_lab, lab2, tc_debug_mode());
+                                           err_coef, 0xFFFFFF00u, active, perm, prev_lab, lab2, flag_pair,
+                                           tc_debug_mode());
   MASK_LAUNCH_CHECK();
   if (tc_debug_mode() & 8) dump_ptrace();
   if (tc_debug_mode() & 128) {
@@ -1333,7 +1369,7 @@ float tc_err_coef(int d) {
 void launch_assign_tc(const float* X, int64_t n, int d, const float* P, const float* Pb, const float* Ps,
                       const float* cn2, int64_t k, const float* xn2, int32_t* labels, float* best,
                       int32_t* flag_rows, int32_t* flag_count, cudaStream_t st, const int* active,
-                      const int32_t* perm, const int32_t* prev_lab, int32_t* lab2) {
+                      const int32_t* perm, const int32_t* prev_lab, int32_t* lab2, int2* flag_pair) {
   const float coef = tc_err_coef(d);
   const int kc = tc_operand_cols(d);
   const int64_t kr = tc_operand_rows(k);
@@ -1350,28 +1386,28 @@ void launch_assign_tc(const float* X, int64_t n, int d, const float* P, const fl
   if (d <= 8)
     tc::launch_persist<16, MASK_TC_P_BN, MASK_TC_P_STAGES, MASK_TC_P_NACC, MASK_TC_P_EPI>(
         X, n, d, kc, kr, P, Pb, Ps, cn2, k, xn2, labels, best, flag_rows, flag_count, coef, st, active, perm,
-        prev_lab, lab2);
+        prev_lab, lab2, flag_pair);
   else if (d <= 16)
     tc::launch_persist<24, MASK_TC_P_BN, MASK_TC_P_STAGES, MASK_TC_P_NACC, MASK_TC_P_EPI>(
         X, n, d, kc, kr, P, Pb, Ps, cn2, k, xn2, labels, best, flag_rows, flag_count, coef, st, active, perm,
-        prev_lab, lab2);
+        prev_lab, lab2, flag_pair);
   else if (d <= 24)
     tc::launch_persist<32, MASK_TC_P_BN, MASK_TC_P_STAGES, MASK_TC_P_NACC, MASK_TC_P_EPI>(
         X, n, d, kc, kr, P, Pb, Ps, cn2, k, xn2, labels, best, flag_rows, flag_count, coef, st, active, perm,
-        prev_lab, lab2);
+        prev_lab, lab2, flag_pair);
   else if (tc_legacy_large_d()) {  // MASK_TC_LEGACY=1: the round-1 one-CTA-per-block kernel (A/B runs)
     if (d <= 32)
       tc::launch_cfg<32, 1, 32, 192, 4, 2, false, 3>(X, n, d, kc, kr, P, Pb, Ps, cn2, k, xn2, labels, best, flag_rows,
-                                                     flag_count, coef, st, active);
+                                                     flag_count, coef, st, active, flag_pair);
     else if (d <= 64)
       tc::launch_cfg<32, 2, 64, 128, 6, 3, false, 2>(X, n, d, kc, kr, P, Pb, Ps, cn2, k, xn2, labels, best, flag_rows,
-                                                     flag_count, coef, st, active);
+                                                     flag_count, coef, st, active, flag_pair);
     else if (d <= 96)
       tc::launch_cfg<32, 3, 96, 128, 6, 2, false, 2>(X, n, d, kc, kr, P, Pb, Ps, cn2, k, xn2, labels, best, flag_rows,
-                                                     flag_count, coef, st, active);
+                                                     flag_count, coef, st, active, flag_pair);
     else
       tc::launch_cfg<32, 4, 128, 128, 6, 2, false, 2>(X, n, d, kc, kr, P, Pb, Ps, cn2, k, xn2, labels, best,
-                                                      flag_rows, flag_count, coef, st, active);
+                                                      flag_rows, flag_count, coef, st, active, flag_pair);
   } else {
     // d > 24: the persistent kernel without the fold step (||c||^2 + ||x||^2 added by the
     // epilogue, two more roundings: + 2^-21 (||x||^2 + ||c||^2) on the gap bound), the same
@@ -1380,16 +1416,20 @@ void launch_assign_tc(const float* X, int64_t n, int d, const float* P, const fl
     const float c2 = coef + std::ldexp(1.0f, -21);
     if (d <= 32)
       tc::launch_persist<32, 192, 4, 2, 3, false, 2>(X, n, d, kc, kr, P, Pb, Ps, cn2, k, xn2, labels, best,
-                                                     flag_rows, flag_count, c2, st, active, perm, prev_lab, lab2);
+                                                     flag_rows, flag_count, c2, st, active, perm, prev_lab, lab2,
+                                                     flag_pair);
     else if (d <= 64)
       tc::launch_persist<64, 128, 6, 2, 2, false, 2>(X, n, d, kc, kr, P, Pb, Ps, cn2, k, xn2, labels, best,
-                                                     flag_rows, flag_count, c2, st, active, perm, prev_lab, lab2);
+                                                     flag_rows, flag_count, c2, st, active, perm, prev_lab, lab2,
+                                                     flag_pair);
     else if (d <= 96)
       tc::launch_persist<96, 128, 6, 2, 2, false, 1>(X, n, d, kc, kr, P, Pb, Ps, cn2, k, xn2, labels, best,
-                                                     flag_rows, flag_count, c2, st, active, perm, prev_lab, lab2);
+                                                     flag_rows, flag_count, c2, st, active, perm, prev_lab, lab2,
+                                                     flag_pair);
     else
       tc::launch_persist<128, 128, 6, 2, 2, false, 1>(X, n, d, kc, kr, P, Pb, Ps, cn2, k, xn2, labels, best,
-                                                      flag_rows, flag_count, c2, st, active, perm, prev_lab, lab2);
+                                                      flag_rows, flag_count, c2, st, active, perm, prev_lab, lab2,
+                                                     flag_pair);
   }
 }
 

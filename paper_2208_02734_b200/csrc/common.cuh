@@ -118,7 +118,7 @@ void launch_assign_tc(const float* X, int64_t n, int d, const float* P, const fl
                       const float* Ps, const float* cn2, int64_t k, const float* xn2,
                       int32_t* labels, float* best, int32_t* flag_rows, int32_t* flag_count,
                       cudaStream_t st, const int* active = nullptr, const int32_t* perm = nullptr,
-                      const int32_t* prev_lab = nullptr, int32_t* lab2 = nullptr);
+                      const int32_t* prev_lab = nullptr, int32_t* lab2 = nullptr, int2* flag_pair = nullptr);
 // Counting sort of rows by label: perm = rows of label 0, then 1, ...; cnt_ws = k int32.
 // perm_old (optional): a previous sort, visited in its order (equal labels adjacent -> warp-
 // aggregated atomics); perm must not alias it.  copy_to (optional): copy_to[row] = labels[row].
@@ -141,9 +141,13 @@ void launch_group_lloyd(const float* Y, int d, const int64_t* perm, int64_t n_it
                         float* P_out, int32_t* labels, cudaStream_t st);
 // K4: exact FP32 direct re-check of the flagged rows against all k prototypes, sized on the
 // device from the flagged count (no host round trip); keys_ws = cap u64.
+// flag_pair (optional): per flagged row (j1, j2): j2 >= 0 -> the only two candidates, decided
+// exactly (FP64 direct distances, lower index on ties); j2 < 0 -> full re-check, through the
+// compacted list rescan_rows / rescan_count (n int32 / 1 int32 workspace)
 void launch_fixup_device(const float* X, int d, const float* P, int64_t k, const int32_t* flag_rows,
                          const int32_t* flag_count, int64_t cap, unsigned long long* keys_ws, int32_t* labels,
-                         float* best, cudaStream_t st, const int* active = nullptr);
+                         float* best, cudaStream_t st, const int* active = nullptr, const int2* flag_pair = nullptr,
+                         int32_t* rescan_rows = nullptr, int32_t* rescan_count = nullptr);
 // prototype operands for K1: Pb = tf32_rn(-2c), Ps = tf32_rn(-2c - Pb), cn2 = ||c||^2; with
 // kc > d the augmented columns [d] = split(||c||^2), [d+1] = (1, 0), rest 0 (row stride kc)
 // flag_count (optional): reset to 0 (the list K1 appends near-tie rows to)

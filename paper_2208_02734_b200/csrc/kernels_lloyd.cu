@@ -416,10 +416,53 @@ static void launch_blocked(const float* X, int d, const float* P, int64_t k, con
   MASK_LAUNCH_CHECK();
 }
 
+// Two-candidate re-check: the exact decision between the only two prototypes a flagged row can
+// take (K4): FP64 direct sums of squares in dimension order (separately rounded
+// products and sums, as the oracle's FP64 loop), smaller distance, then lower index (D4).
+// Rows without a pair are appended to the full re-check list.
+__global__ void k_fix_pairs(const float* __restrict__ X, int d, const float* __restrict__ P,
+                            const int32_t* __restrict__ flag_rows, const int2* __restrict__ flag_pair,
+                            const int32_t* __restrict__ flag_count, int64_t cap, int32_t* __restrict__ labels,
+                            float* __restrict__ best, int32_t* __restrict__ rescan_rows,
+                            int32_t* __restrict__ rescan_count, const int* __restrict__ active) {
+  if (active && !*active) return;
+  const int64_t nf = min64(*flag_count, cap);
+  for (int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; f < nf; f += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t row = flag_rows[f];
+    const int2 jp = flag_pair[f];
+    if (jp.y < 0) {
+      rescan_rows[atomicAdd(rescan_count, 1)] = row;
+      continue;
+    }
+    const float* x = X + (int64_t)row * d;
+    const float* c1 = P + (int64_t)jp.x * d;
+    const float* c2 = P + (int64_t)jp.y * d;
+    double s1 = 0.0, s2 = 0.0;
+    for (int i = 0; i < d; ++i) {
+      const double xi = (double)x[i];
+      const double t1 = xi - (double)c1[i], t2 = xi - (double)c2[i];
+      s1 = __dadd_rn(s1, __dmul_rn(t1, t1));
+      s2 = __dadd_rn(s2, __dmul_rn(t2, t2));
+    }
+    const bool first = s1 < s2 || (s1 == s2 && jp.x < jp.y);
+    labels[row] = first ? jp.x : jp.y;
+    best[row] = (float)(first ? s1 : s2);
+  }
+}
+
 void launch_fixup_device(const float* X, int d, const float* P, int64_t k, const int32_t* flag_rows,
                          const int32_t* flag_count, int64_t cap, unsigned long long* keys_ws, int32_t* labels,
-                         float* best, cudaStream_t st, const int* active) {
-  launch_blocked(X, d, P, k, flag_rows, flag_count, cap, keys_ws, labels, best, st, active);
+                         float* best, cudaStream_t st, const int* active, const int2* flag_pair,
+                         int32_t* rescan_rows, int32_t* rescan_count) {
+  if (!flag_pair) {
+    launch_blocked(X, d, P, k, flag_rows, flag_count, cap, keys_ws, labels, best, st, active);
+    return;
+  }
+  MASK_CUDA(cudaMemsetAsync(rescan_count, 0, sizeof(int32_t), st));
+  k_fix_pairs<<<num_sms() * 4, 256, 0, st>>>(X, d, P, flag_rows, flag_pair, flag_count, cap, labels, best,
+                                             rescan_rows, rescan_count, active);
+  MASK_LAUNCH_CHECK();
+  launch_blocked(X, d, P, k, rescan_rows, rescan_count, cap, keys_ws, labels, best, st, active);
 }
 
 void launch_assign_blocked(const float* X, int64_t n, int d, const float* P, int64_t k, unsigned long long* keys_ws,

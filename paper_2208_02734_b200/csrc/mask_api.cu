@@ -436,6 +436,8 @@ struct LloydWS {
   DevBuf<int32_t> counts;
   DevBuf<float> Pb, Ps, cn2, xn2, PT;
   DevBuf<int32_t> flag_rows, flag_count;
+  DevBuf<int2> flag_pair;                     // K1 -> K4: the two candidates of a flagged row
+  DevBuf<int32_t> rescan_rows, rescan_count;  // K4: flagged rows that need the full re-check
   DevBuf<unsigned long long> fix_keys;
   DevBuf<int16_t> colslot;  // K3 chunk-major: hot slot of each column (-1 = read from L2)
   DevBuf<int32_t> hotcols;  // the hot columns (most non-zeros)
@@ -526,6 +528,9 @@ void assign_pass(const Input& in, const float* P, int64_t k, int flags, int32_t*
     ws.Ps.alloc((size_t)tc_operand_rows(k) * kc);
     ws.cn2.alloc(tc_operand_rows(k));  // +inf beyond k: the epilogue reads whole tiles
     ws.flag_rows.alloc(n);
+    ws.flag_pair.alloc(n);
+    ws.rescan_rows.alloc(n);
+    ws.rescan_count.alloc(1);
     ws.flag_count.alloc(1);
     ws.fix_keys.alloc((size_t)n);
     launch_fill(ws.cn2.p + k, tc_operand_rows(k) - k, INFINITY, st);
@@ -546,13 +551,14 @@ void assign_pass(const Input& in, const float* P, int64_t k, int flags, int32_t*
   // bound-pruned epilogue skips most chunks warp-wide
   const int32_t* perm = (ws.have_perm && !(flags & MASK_NO_SORT)) ? ws.perm.p : nullptr;
   launch_assign_tc(in.X, n, d, P, ws.Pb.p, ws.Ps.p, ws.cn2.p, k, ws.xn2.p, labels_out, best, ws.flag_rows.p,
-                   ws.flag_count.p, st, active, perm, ws.have_prev ? ws.lab_prev.p : nullptr, ws.lab2.p);
+                   ws.flag_count.p, st, active, perm, ws.have_prev ? ws.lab_prev.p : nullptr, ws.lab2.p,
+                   ws.flag_pair.p);
   if (ev) ev->mark(MASK_T_ASSIGN, st);
   // near-tie re-check (K4), sized on the device from the flagged count (no host round trip)
   if (!(flags & MASK_NO_FIXUP)) {
     if (ev) ev->mark(MASK_T_FIXUP, st);
     launch_fixup_device(in.X, d, P, k, ws.flag_rows.p, ws.flag_count.p, n, ws.fix_keys.p, labels_out, best, st,
-                        active);
+                        active, ws.flag_pair.p, ws.rescan_rows.p, ws.rescan_count.p);
     if (ev) ev->mark(MASK_T_FIXUP, st);
   }
 }

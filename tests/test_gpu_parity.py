@@ -473,3 +473,26 @@ def test_csr_structure_errors_are_reported():
         with pytest.raises(mk.MaskError, match=msg):
             idx.query(mk.Csr(r, c, val, 200), knn=3)
     idx.free()
+
+
+@pytest.mark.parametrize("d", [16, 32, 64, 128])
+def test_near_ties_are_decided_exactly(d):
+    """Rows placed on the bisector of two prototypes (midpoint + noise orthogonal to their
+    difference): the 3xTF32 scores cannot order them, K1 flags them with their two candidates and
+    K4 decides between the two in FP64 (the oracle's arithmetic): every label then equals the
+    oracle's argmin (lowest index on exact ties), with no tie-window exemption."""
+    rng = np.random.default_rng(d)
+    k, n = 300, 4096
+    P = (rng.standard_normal((k, d)) * 4.0).astype(np.float32)
+    a = rng.integers(0, k, n)
+    b = (a + 1 + rng.integers(0, k - 1, n)) % k
+    diff = P[a].astype(np.float64) - P[b]
+    z = rng.standard_normal((n, d))
+    z -= (z * diff).sum(1, keepdims=True) / (diff * diff).sum(1, keepdims=True) * diff
+    X = ((P[a].astype(np.float64) + P[b]) / 2 + 0.05 * z).astype(np.float32)
+    lab, d2, nf = mk.assign(t(X), t(P))
+    ref, b1, b2 = oracle.assign(X.astype(np.float64), P.astype(np.float64))
+    assert nf > n // 4, f"expected most rows flagged, got {nf}"
+    got = lab.cpu().numpy()
+    bad = np.nonzero(got != ref)[0]
+    assert bad.size == 0, f"{bad.size} labels differ from the oracle (rows {bad[:5].tolist()})"
