@@ -472,6 +472,54 @@ def descend_leaf(P: Sequence[np.ndarray], offsets: Sequence[np.ndarray], members
     return j, gap
 
 
+def split_partitions(P: Sequence[np.ndarray], labels: Sequence[np.ndarray], X, threshold: int, T: int, seed: int):
+    """Partition split and local rebuild ("if one partition grows beyond a certain
+    threshold, it can be split in smaller data groups and reconstruct just the local part of the
+    index covering that specific region, without affecting the rest of the structure";
+    DESIGN.md reading S1).
+
+    For every level-1 prototype j in ascending order whose partition holds n_j > threshold rows:
+    its rows in ascending id order are clustered by Lloyd (``lloyd``, T iterations + the final
+    assignment) into s = ceil(n_j / threshold) groups from the init rows
+    ``seeded_init(seed + j, 1, n_j, s)``; group 0 keeps id j, groups 1..s-1 get the next new
+    level-1 ids (k_1, k_1 + 1, ... in order of j, then group); the new prototypes' level-2 label is
+    j's (same parent); prototypes and labels of every other partition and of every upper level
+    are unchanged.  Partitions created here are not split again in the same call.
+
+    P, labels: per level (bottom first) as the index holds them (labels[0] over the data rows,
+    labels[l] over level-l prototypes).  Returns (P, labels, split_js) with P[0], labels[0] and
+    (if present) labels[1] updated."""
+    P = [np.array(p, np.float64) for p in P]
+    labels = [np.array(lb, np.int64) for lb in labels]
+    X = _f64(X)
+    k1 = P[0].shape[0]
+    counts = np.bincount(labels[0], minlength=k1)
+    new_rows, new_parent, split = [], [], []
+    nxt = k1
+    for j in range(k1):
+        nj = int(counts[j])
+        if nj <= threshold:
+            continue
+        rows = np.nonzero(labels[0] == j)[0]  # ascending row ids
+        s = -(-nj // threshold)
+        init = seeded_init((seed + j) & _M64, 1, nj, s)
+        res = lloyd(X[rows], init, T)
+        P[0][j] = res.P[0]
+        for g in range(1, s):
+            new_rows.append(res.P[g])
+            if len(labels) > 1:
+                new_parent.append(labels[1][j])
+        lab = np.where(res.labels == 0, j, nxt + res.labels.astype(np.int64) - 1)
+        labels[0][rows] = lab
+        nxt += s - 1
+        split.append(j)
+    if new_rows:
+        P[0] = np.vstack([P[0], np.array(new_rows)])
+        if len(labels) > 1:
+            labels[1] = np.concatenate([labels[1], np.array(new_parent, np.int64)])
+    return P, labels, split
+
+
 # ------------------------------------------------------------------ distributed mode (NEXT-3)
 def top_registry(index_P_top, offsets_top) -> np.ndarray:
     """What a node registers with the coordinator (§3.4, "just the top level

@@ -647,3 +647,69 @@ def test_relocation_lowers_the_self_miss_rate():
     perm = datagen.group_perm(5, X.shape[0])
     e = oracle.relocate_and_rebuild(X, 16, 8, 10, perm, 4, 100, datagen.relocation_keys)
     assert len(e) == 5 and min(e[1:]) < e[0]
+
+
+# ------------------------------------------------------------------ NEXT-4 partition split (reading S1)
+def test_split_partitions_worked_example():
+    """Hand-derived: a partition {0, 1, 2, 100, 101, 102} on a line with threshold 3 splits into
+    s = 2 groups; whatever the two seeded init rows are, Lloyd separates the two clusters (an
+    init inside one cluster pulls the far cluster to the other prototype at the first update:
+    e.g. init (0, 1): {0} | {1, 2, 100, 101, 102} -> prototypes (0, 61.2) -> {0,1,2} | {100,101,102}),
+    so the prototypes are 1 and 101; the other partition {50} and the level-2 labels stay."""
+    X = np.array([[0.0], [1.0], [2.0], [100.0], [101.0], [102.0], [50.0]])
+    P = [np.array([[51.0], [50.0]]), np.array([[40.0]])]
+    labels = [np.array([0, 0, 0, 0, 0, 0, 1]), np.array([0, 0])]
+    for seed in range(5):
+        P2, L2, split = oracle.split_partitions(P, labels, X, threshold=3, T=5, seed=seed)
+        assert split == [0]
+        assert P2[0].shape == (3, 1) and P2[0][1, 0] == 50.0
+        assert sorted([P2[0][0, 0], P2[0][2, 0]]) == [1.0, 101.0]
+        a, b = L2[0][:3], L2[0][3:6]
+        assert len(set(a)) == 1 and len(set(b)) == 1 and {a[0], b[0]} == {0, 2}
+        assert P2[0][a[0], 0] == 1.0 and P2[0][b[0], 0] == 101.0
+        assert L2[0][6] == 1
+        np.testing.assert_array_equal(L2[1], [0, 0, 0])  # the new prototype's parent = j's parent
+        np.testing.assert_array_equal(P2[1], P[1])
+
+
+def test_split_partitions_invariants():
+    """Random data: the split partitions' rows are exactly covered by the new groups, every new
+    prototype is the mean of its members (numpy), every member sits at its nearest new prototype
+    (scipy cdist), other partitions and upper levels are untouched, and s = ceil(n_j / threshold)."""
+    from scipy.spatial.distance import cdist
+
+    X = datagen.blobs(77, 3000, 5, 12)
+    k1 = 12
+    labels0 = oracle.assign(X, X[datagen.init_indices(78, 1, 3000, k1)])[0].astype(np.int64)
+    P1 = np.stack([X[labels0 == j].mean(axis=0) for j in range(k1)])
+    labels1 = np.arange(k1) % 3
+    P2l = np.stack([P1[labels1 == j].mean(axis=0) for j in range(3)])
+    thr = 300
+    counts = np.bincount(labels0, minlength=k1)
+    P2, L2, split = oracle.split_partitions([P1, P2l], [labels0, labels1], X, threshold=thr, T=8, seed=9)
+    assert split == [j for j in range(k1) if counts[j] > thr] and split
+    n_new = sum(-(-int(counts[j]) // thr) - 1 for j in split)
+    assert P2[0].shape[0] == k1 + n_new and L2[1].shape[0] == k1 + n_new
+    np.testing.assert_array_equal(P2[1], P2l)
+    nxt = k1
+    for j in range(k1):
+        rows = np.nonzero(labels0 == j)[0]
+        if j not in split:
+            np.testing.assert_array_equal(P2[0][j], P1[j])
+            np.testing.assert_array_equal(L2[0][rows], j)
+            continue
+        s = -(-int(counts[j]) // thr)
+        ids = [j] + list(range(nxt, nxt + s - 1))
+        nxt += s - 1
+        assert set(L2[0][rows].tolist()) <= set(ids)
+        for g in ids:
+            mem = rows[L2[0][rows] == g]
+            if mem.size:
+                np.testing.assert_allclose(P2[0][g], X[mem].astype(np.float64).mean(axis=0), rtol=1e-12, atol=1e-12)
+            assert L2[1][g] == labels1[j]
+        D = cdist(X[rows].astype(np.float64), P2[0][ids], "sqeuclidean")
+        near = np.array(ids)[D.argmin(axis=1)]
+        np.testing.assert_array_equal(L2[0][rows], near)
+    # nothing above the threshold: nothing changes
+    P3, L3, sp3 = oracle.split_partitions([P1, P2l], [labels0, labels1], X, threshold=int(counts.max()), T=8, seed=9)
+    assert sp3 == [] and np.array_equal(P3[0], P1) and np.array_equal(L3[0], labels0)
