@@ -257,6 +257,30 @@ int32_t mask_range_query(const mask_index* idx, const mask_matrix* queries, cons
  * (MASK_ERR_UNSUPPORTED otherwise); MASK_ERR_ARG on a dim mismatch. */
 int32_t mask_insert(mask_index* idx, const mask_matrix* points, int64_t* partition_out, void* stream);
 
+/* ---------------------------------------------------------------- partition split
+ * Partition split and local rebuild ("if one partition grows beyond a certain
+ * threshold, it can be split in smaller data groups and reconstruct just the local part of the
+ * index covering that specific region, without affecting the rest of the structure"; SURVEY
+ * §8(f) NEXT-4; reading S1).  For every level-1 prototype j, in ascending order,
+ * whose partition holds n_j > threshold rows: its rows in ascending id order are clustered by
+ * the library's Lloyd loop (max_iters iterations + the final assignment, empty groups keep,
+ * lowest index on ties) into s = ceil(n_j / threshold) groups from the init rows
+ * mask_seeded_init(seed + j, 1, n_j, s); group 0 keeps id j, groups 1..s-1 take the next new
+ * level-1 ids (k_1, k_1 + 1, ... in order of j, then group); each new prototype's level-2
+ * parent is j's; every other prototype, label and upper level is unchanged (so the descent
+ * reaches the new partitions through j's parent).  Partitions created by the call are not
+ * split again in it.  Mutates the index (single writer); level 1 then has k_1 + (new ids)
+ * prototypes (mask_level_info); a MASK_TRACE_PASSES trace of level 1 is dropped.  Dense
+ * single-GPU indexes only (MASK_ERR_UNSUPPORTED otherwise); MASK_ERR_ARG on threshold < 1 or
+ * max_iters < 0.  *n_split_out (optional) = the number of partitions split. */
+typedef struct {
+  int64_t threshold; /* split partitions with more rows than this (>= 1)                    */
+  int32_t max_iters; /* Lloyd iterations of each local k-means (>= 0)                      */
+  int32_t flags;     /* MASK_FORCE_SIMT / MASK_NO_FUSED for the local Lloyd loop (else 0)   */
+  uint64_t seed;     /* local init seed (partition j draws from seed + j)                   */
+} mask_split_params;
+int32_t mask_split(mask_index* idx, const mask_split_params* params, int64_t* n_split_out, void* stream);
+
 /* ---------------------------------------------------------------- distributed mode
  * The paper's §3.4 "Indexing distributed datasets": every
  * node (one GPU, one process) builds its own index over its own rows with comm = NULL (zero

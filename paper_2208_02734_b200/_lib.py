@@ -48,7 +48,7 @@ EXPORTS = [
     "mask_grouped_depth", "mask_build_grouped", "mask_range_query", "mask_insert",
     "mask_top_prototypes", "mask_route", "mask_query_routed", "mask_merge", "mask_collective_count",
     "mask_seeded_init", "mask_debug_fail_alloc", "mask_get_displacement", "mask_get_pass",
-    "mask_comm_init_host",
+    "mask_comm_init_host", "mask_split",
 ]
 
 
@@ -88,6 +88,15 @@ class MaskBuildParams(C.Structure):
         ("flags", C.c_int32),
         ("iter_cb", ITER_CB),
         ("iter_cb_user", C.c_void_p),
+    ]
+
+
+class MaskSplitParams(C.Structure):
+    _fields_ = [
+        ("threshold", C.c_int64),
+        ("max_iters", C.c_int32),
+        ("flags", C.c_int32),
+        ("seed", C.c_uint64),
     ]
 
 
@@ -159,6 +168,7 @@ def load():
             "mask_get_displacement": (i32, [P, i32, P, i32]),
             "mask_get_pass": (i32, [P, i32, i32, P, P]),
             "mask_comm_init_host": (i32, [i32, i32, HOST_COLL, P, C.POINTER(P)]),
+            "mask_split": (i32, [P, C.POINTER(MaskSplitParams), C.POINTER(i64), P]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)

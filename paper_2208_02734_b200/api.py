@@ -271,6 +271,19 @@ class Index:
         del keep
         return part
 
+    def split(self, threshold: int, iters: int, seed: int = 0, flags: int = 0, stream=None) -> int:
+        """mask_split: split every level-1 partition with more than ``threshold`` rows
+        by a local Lloyd k-means and rebuild the local part of the index; returns the number of
+        partitions split."""
+        p = _lib.MaskSplitParams()
+        p.threshold = int(threshold)
+        p.max_iters = int(iters)
+        p.flags = int(flags)
+        p.seed = int(seed) & 0xFFFFFFFFFFFFFFFF
+        out = C.c_int64(0)
+        check(load().mask_split(self.handle, C.byref(p), C.byref(out), _stream(stream)))
+        return int(out.value)
+
     def query_routed(self, queries, routed, node: int, id_base: int, knn: int = 10, beam: int = 1, stream=None):
         """mask_query_routed (§3.4): answer only the queries with routed[q, node] != 0 (the rest
         are padded), reporting global ids id_base + local id.  Device tensors only."""

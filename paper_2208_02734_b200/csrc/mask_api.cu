@@ -1546,6 +1546,129 @@ int32_t mask_insert(mask_index* idx, const mask_matrix* points, int64_t* partiti
 }
 
 namespace {
+__global__ void k_relabel_split(const int64_t* __restrict__ rows, const int32_t* __restrict__ loc, int64_t m,
+                                int32_t j, int32_t base, int32_t* __restrict__ labels) {
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < m; r += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t g = loc[r];
+    labels[rows[r]] = g == 0 ? j : base + g - 1;
+  }
+}
+
+// Partition split + local rebuild (mask.h mask_split, reading S1).
+void split_impl(mask_index* idx, const mask_split_params* p, int64_t* n_split_out, cudaStream_t st) {
+  MASK_REQUIRE(idx != nullptr && p != nullptr, MASK_ERR_ARG, "NULL argument");
+  MASK_REQUIRE(idx->format == MASK_DENSE_F32, MASK_ERR_UNSUPPORTED, "partition split takes a dense index");
+  MASK_REQUIRE(p->threshold >= 1 && p->max_iters >= 0, MASK_ERR_ARG, "threshold must be >= 1 and max_iters >= 0");
+  Level& L1 = idx->levels[0];
+  const int64_t n = L1.n_items, k1 = L1.k;
+  const int d = idx->dim;
+  std::vector<int32_t> lab(n);
+  if (n) MASK_CUDA(cudaMemcpyAsync(lab.data(), L1.labels.p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st));
+  MASK_CUDA(cudaStreamSynchronize(st));
+  std::vector<int64_t> cnt(k1, 0);
+  for (int64_t i = 0; i < n; ++i) ++cnt[lab[i]];
+  std::vector<int64_t> todo;
+  int64_t extra = 0;
+  for (int64_t j = 0; j < k1; ++j)
+    if (cnt[j] > p->threshold) {
+      todo.push_back(j);
+      extra += (cnt[j] + p->threshold - 1) / p->threshold - 1;
+    }
+  if (n_split_out) *n_split_out = (int64_t)todo.size();
+  if (todo.empty()) return;
+  MASK_REQUIRE(k1 + extra < (int64_t(1) << 31), MASK_ERR_UNSUPPORTED, "too many prototypes after the split");
+  // rows of each split partition in ascending id order
+  std::vector<std::vector<int64_t>> rows(todo.size());
+  {
+    std::vector<int64_t> slot(k1, -1);
+    for (size_t t = 0; t < todo.size(); ++t) {
+      slot[todo[t]] = (int64_t)t;
+      rows[t].reserve((size_t)cnt[todo[t]]);
+    }
+    for (int64_t i = 0; i < n; ++i)
+      if (slot[lab[i]] >= 0) rows[slot[lab[i]]].push_back(i);
+  }
+  const int64_t k1n = k1 + extra;
+  DevBuf<float> P1((size_t)k1n * d);
+  MASK_CUDA(cudaMemcpyAsync(P1.p, L1.P.p, sizeof(float) * k1 * d, cudaMemcpyDeviceToDevice, st));
+  std::vector<int32_t> parents;  // level-2 labels of the new ids
+  std::vector<int32_t> lab2;
+  const bool upper = idx->levels.size() >= 2;
+  if (upper) {
+    lab2.resize(k1);
+    MASK_CUDA(cudaMemcpyAsync(lab2.data(), idx->levels[1].labels.p, sizeof(int32_t) * k1, cudaMemcpyDeviceToHost, st));
+    MASK_CUDA(cudaStreamSynchronize(st));
+  }
+  mask_build_params bp{};
+  bp.num_levels = 1;
+  bp.max_iters = p->max_iters;
+  bp.tol = 0.0;
+  bp.flags = p->flags & (MASK_FORCE_SIMT | MASK_NO_FUSED | MASK_NO_SORT | MASK_NO_FIXUP);
+  HostStats hs;
+  int64_t nxt = k1;
+  for (size_t t = 0; t < todo.size(); ++t) {
+    const int64_t j = todo[t];
+    const int64_t nj = (int64_t)rows[t].size();
+    const int64_t sgrp = (nj + p->threshold - 1) / p->threshold;
+    DevBuf<int64_t> rdev(nj);
+    MASK_CUDA(cudaMemcpyAsync(rdev.p, rows[t].data(), sizeof(int64_t) * nj, cudaMemcpyHostToDevice, st));
+    DevBuf<float> Y((size_t)nj * d);
+    launch_gather_rows(idx->X, d, rdev.p, nj, 0, n, Y.p, st);
+    std::vector<int64_t> init((size_t)sgrp);
+    MASK_REQUIRE(mask_seeded_init(p->seed + (uint64_t)j, 1, nj, sgrp, init.data()) == MASK_OK, MASK_ERR_ARG,
+                 "seeded init failed");
+    Input in;
+    in.format = MASK_DENSE_F32;
+    in.dim = d;
+    in.n_local = in.n_global = nj;
+    in.X = Y.p;
+    Level Lj;
+    run_level(in, sgrp, init.data(), &bp, nullptr, 1, st, Lj, hs);
+    // group 0 -> prototype j, groups 1.. -> new ids nxt, nxt + 1, ...
+    MASK_CUDA(cudaMemcpyAsync(P1.p + j * d, Lj.P.p, sizeof(float) * d, cudaMemcpyDeviceToDevice, st));
+    if (sgrp > 1)
+      MASK_CUDA(cudaMemcpyAsync(P1.p + nxt * d, Lj.P.p + d, sizeof(float) * (sgrp - 1) * d, cudaMemcpyDeviceToDevice,
+                                st));
+    k_relabel_split<<<grid_for(nj, 256), 256, 0, st>>>(rdev.p, Lj.labels.p, nj, (int32_t)j, (int32_t)nxt, L1.labels.p);
+    MASK_LAUNCH_CHECK();
+    if (upper)
+      for (int64_t g = 1; g < sgrp; ++g) parents.push_back(lab2[j]);
+    nxt += sgrp - 1;
+    MASK_CUDA(cudaStreamSynchronize(st));  // Y / rdev / Lj leave scope
+  }
+  L1.P = std::move(P1);
+  L1.k = k1n;
+  L1.offsets.alloc(k1n + 1);
+  {
+    DevBuf<int32_t> cursor(k1n);
+    launch_children(L1.labels.p, n, k1n, L1.offsets.p, L1.members.p, cursor.p, st);
+  }
+  L1.P_trace.release();
+  L1.lab_trace.release();
+  L1.trace_T = -1;
+  if (upper) {
+    Level& L2 = idx->levels[1];
+    DevBuf<int32_t> l2((size_t)k1n);
+    MASK_CUDA(cudaMemcpyAsync(l2.p, L2.labels.p, sizeof(int32_t) * k1, cudaMemcpyDeviceToDevice, st));
+    MASK_CUDA(cudaMemcpyAsync(l2.p + k1, parents.data(), sizeof(int32_t) * parents.size(), cudaMemcpyHostToDevice, st));
+    L2.labels = std::move(l2);
+    L2.n_items = k1n;
+    L2.members.alloc((size_t)k1n);
+    DevBuf<int32_t> cursor(L2.k);
+    launch_children(L2.labels.p, k1n, L2.k, L2.offsets.p, L2.members.p, cursor.p, st);
+    L2.P_trace.release();
+    L2.lab_trace.release();
+    L2.trace_T = -1;
+  }
+  if (idx->Xpart.p) {
+    idx->Xpart.release();
+    gather_partition_best_effort(idx, st);
+  }
+  MASK_CUDA(cudaStreamSynchronize(st));
+  std::lock_guard<std::mutex> lock(idx->cover_mu);
+  idx->cover_valid = false;
+}
+
 int32_t query_impl(const mask_index* idx, const mask_matrix* queries, int32_t k_nn, int32_t beam,
                    int64_t* ids_out, float* d2_out, void* stream, const uint8_t* routed, int64_t rstride,
                    int64_t id_base) {
@@ -1626,6 +1749,11 @@ int32_t query_impl(const mask_index* idx, const mask_matrix* queries, int32_t k_
   });
 }
 }  // namespace
+
+int32_t mask_split(mask_index* idx, const mask_split_params* params, int64_t* n_split_out, void* stream) {
+  NvtxRange range("mask_split");
+  return guarded([&] { split_impl(idx, params, n_split_out, as_stream(stream)); });
+}
 
 int32_t mask_query(const mask_index* idx, const mask_matrix* queries, int32_t k_nn, int32_t beam,
                    int64_t* ids_out, float* d2_out, void* stream) {

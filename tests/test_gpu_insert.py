@@ -50,3 +50,77 @@ def test_insert_parity_and_closure(cid, div, borrow):
     part2 = idx.insert(np.ascontiguousarray(new[:5] + 1e-3))
     assert part2.shape == (5,) and idx.labels(1).shape[0] == n + len(new) + 5
     idx.free()
+
+
+def _index_state(idx):
+    L = idx.num_levels
+    return ([idx.prototypes(l).astype(np.float64) for l in range(1, L + 1)],
+            [idx.labels(l).astype(np.int64) for l in range(1, L + 1)])
+
+
+@pytest.mark.parametrize("cid,div,thr", [(2, 64, 300), (3, 2048, 100), (5, 4096, 120)])
+def test_split_partitions_parity(cid, div, thr):
+    """Partition split + local rebuild (reading S1) against oracle.split_partitions
+    applied to the same (GPU-built) index: new prototypes within 1e-4, labels identical except
+    rows in the oracle's tie window, level-2 parents identical, child lists = {i : labels = j},
+    and queries over the rebuilt index equal the oracle descent over it."""
+    from parity import check_assignment, check_prototypes, check_queries
+
+    cfg = datagen.CONFIGS[cid].scaled(div)
+    X = datagen.data(cfg)
+    idx = mk.build(torch.from_numpy(X).cuda(), cfg.levels, 6, datagen.all_init_indices(cfg))
+    P0, L0 = _index_state(idx)
+    nsplit = idx.split(thr, iters=8, seed=11)
+    Pr, Lr, split = oracle.split_partitions(P0, L0, X, threshold=thr, T=8, seed=11)
+    assert nsplit == len(split) and nsplit > 0
+    P1, L1 = _index_state(idx)
+    assert P1[0].shape == Pr[0].shape
+    check_prototypes(P1[0], Pr[0], what="split level 1")
+    for l in range(1, len(P1)):
+        np.testing.assert_array_equal(P1[l], P0[l])  # upper levels untouched
+        np.testing.assert_array_equal(L1[l], Lr[l])
+    # labels: within each split partition the GPU's local assignment vs the oracle's
+    X64 = X.astype(np.float64)
+    for j in split:
+        rows = np.nonzero(L0[0] == j)[0]
+        ids = sorted(set(Lr[0][rows].tolist()) | set(L1[0][rows].tolist()))
+        loc_g = np.searchsorted(ids, L1[0][rows])
+        check_assignment(X64[rows], P1[0][ids], loc_g, what=f"split partition {j}")
+    same = np.isin(L0[0], split, invert=True)
+    np.testing.assert_array_equal(L1[0][same], L0[0][same])
+    for l in range(1, len(P1) + 1):
+        off, mem = idx.children(l)
+        o_ref, m_ref = oracle.children(L1[l - 1], P1[l - 1].shape[0])
+        np.testing.assert_array_equal(off, o_ref)
+        np.testing.assert_array_equal(mem, m_ref)
+    Q = datagen.queries(cfg, count=200)
+    ch = [idx.children(l) for l in range(1, len(P1) + 1)]
+    rids, rd2, gap = oracle.query(P1, [c[0] for c in ch], [c[1] for c in ch], X, Q, 10, 2)
+    ids, d2 = idx.query(torch.from_numpy(Q).cuda(), knn=10, beam=2)
+    check_queries(ids.cpu().numpy(), d2.cpu().numpy(), rids, rd2, gap, what="queries after the split")
+    assert idx.split(thr * 1000, iters=8) == 0  # nothing above the threshold: no change
+    idx.free()
+
+
+def test_insert_then_split_restores_the_partition_size():
+    """The paper's scenario: many new points land in one region, its partition grows past the
+    threshold, and the split rebuilds only that part; inserted points stay findable."""
+    cfg = datagen.CONFIGS[2].scaled(64)
+    X = datagen.data(cfg)
+    idx = mk.build(torch.from_numpy(X).cuda(), cfg.levels, 6, datagen.all_init_indices(cfg))
+    P1 = idx.prototypes(1)
+    rng = np.random.default_rng(5)
+    new = (P1[7] + 0.3 * rng.standard_normal((2000, cfg.dim))).astype(np.float32)
+    part = idx.insert(torch.from_numpy(new).cuda()).cpu().numpy()
+    k_before = idx.level_info(1)["k"]
+    big = np.bincount(idx.labels(1), minlength=k_before).max()
+    thr = 600
+    assert big > thr
+    ns = idx.split(thr, iters=10, seed=3)
+    assert ns >= 1 and idx.level_info(1)["k"] > k_before
+    sizes = np.bincount(idx.labels(1), minlength=idx.level_info(1)["k"])
+    assert sizes.sum() == X.shape[0] + len(new)
+    assert sizes.max() < big
+    ids, d2 = idx.query(torch.from_numpy(new[:50]).cuda(), knn=1, beam=4)
+    assert float(d2.cpu().numpy().min()) == 0.0
+    idx.free()
