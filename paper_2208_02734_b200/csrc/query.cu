@@ -193,6 +193,66 @@ __device__ __forceinline__ float coop_dist(const float* __restrict__ q, const fl
   }
 }
 
+// Distances of 32 CONTIGUOUS rows (row-major, d = 4G floats, 16-byte aligned) to q, with
+// coalesced loads: lane l loads float4 number l + 32 i (i < G) of the block -- column group
+// c = l % G of row i (32/G) + l / G -- so every load instruction reads 512 contiguous bytes (4
+// L1 wavefronts, against 32 for one row per lane); the G partial sums of a row, spread over G
+// lanes, are then combined by a transposed butterfly (G - 1 shuffles per lane), after which lane
+// l holds the distance of row (l % G)(32/G) + l / G.  Rows >= nvalid give +inf.
+template <int G>
+__device__ __forceinline__ float block_dist32(const float4* __restrict__ base4, int nvalid, float4 qc, int lane,
+                                              int& row_out) {
+  constexpr int RPI = 32 / G;  // rows per load instruction
+  float v[G];
+#pragma unroll
+  for (int i = 0; i < G; ++i) {
+    const int r = i * RPI + lane / G;
+    float acc = 0.f;
+    if (r < nvalid) {
+      const float4 xv = __ldg(base4 + lane + 32 * i);
+      float t = qc.x - xv.x;
+      acc = fmaf(t, t, acc);
+      t = qc.y - xv.y;
+      acc = fmaf(t, t, acc);
+      t = qc.z - xv.z;
+      acc = fmaf(t, t, acc);
+      t = qc.w - xv.w;
+      acc = fmaf(t, t, acc);
+    }
+    v[i] = acc;
+  }
+  // step with lane mask m keeps the lower half of the values on lanes with (l & m) == 0 and the
+  // upper half on the others, adding the partner's copy: after the last step lane l holds index
+  // i = l % G summed over its G lanes
+#pragma unroll
+  for (int m = G / 2, n = G; m >= 1; m >>= 1, n >>= 1) {
+    const bool upper = (lane & m) != 0;
+#pragma unroll
+    for (int j = 0; j < n / 2; ++j) {
+      const float send = upper ? v[j] : v[j + n / 2];
+      const float keep = upper ? v[j + n / 2] : v[j];
+      v[j] = keep + __shfl_xor_sync(FULL, send, m);
+    }
+  }
+  const int r = (lane % G) * RPI + lane / G;
+  row_out = r;
+  return r < nvalid ? v[0] : INFINITY;
+}
+
+// Leaf scan of rows [m0, m1) of the partition-ordered copy Xp into the running top-k.
+template <int G>
+__device__ __forceinline__ void leaf_scan_coalesced(const QIndex& qi, const float* q, int64_t m0, int64_t m1,
+                                                    const int32_t* __restrict__ members, WarpTopK& top, int lane) {
+  const float4 qc = reinterpret_cast<const float4*>(q)[lane % G];
+  for (int64_t m = m0; m < m1; m += 32) {
+    const int nvalid = (int)min64(32, m1 - m);
+    int r;
+    const float cd = block_dist32<G>(reinterpret_cast<const float4*>(qi.Xp + m * (int64_t)(4 * G)), nvalid, qc, lane, r);
+    const int32_t cid = r < nvalid ? members[m + r] : PAD_ID;
+    top.offer(cd, cid, lane);
+  }
+}
+
 // Dense queries against a dense index.  Shared memory: one q vector (d floats) per warp.
 template <int LPC>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32)
@@ -261,10 +321,22 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
       const int32_t sel_id = top.id;
       (void)sel_d;
       top.reset(knn);
+      // partition-ordered rows with d = 4G (G a power of two <= 32): 32 contiguous rows per
+      // coalesced block (block_dist32); otherwise one row (or LPC lanes) per candidate
+      const int G = (qi.Xp && (d & 3) == 0) ? d >> 2 : 0;
       for (int s = 0; s < beam; ++s) {
         const int32_t p = __shfl_sync(FULL, sel_id, s);
         if (p == PAD_ID) continue;
         const int64_t m0 = L1.offsets[p], m1 = L1.offsets[p + 1];
+        switch (G) {
+          case 1: leaf_scan_coalesced<1>(qi, q, m0, m1, L1.members, top, lane); continue;
+          case 2: leaf_scan_coalesced<2>(qi, q, m0, m1, L1.members, top, lane); continue;
+          case 4: leaf_scan_coalesced<4>(qi, q, m0, m1, L1.members, top, lane); continue;
+          case 8: leaf_scan_coalesced<8>(qi, q, m0, m1, L1.members, top, lane); continue;
+          case 16: leaf_scan_coalesced<16>(qi, q, m0, m1, L1.members, top, lane); continue;
+          case 32: leaf_scan_coalesced<32>(qi, q, m0, m1, L1.members, top, lane); continue;
+          default: break;
+        }
         for (int64_t m = m0; m < m1; m += 32) {
           const int64_t mm = m + lane;
           const int32_t cid = mm < m1 ? (int32_t)L1.members[mm] : PAD_ID;
