@@ -284,6 +284,23 @@ __device__ __forceinline__ void chunk_top2(uint32_t* r, uint32_t mask, uint32_t 
   c2 = (int32_t)(umin(umin(ua, ub), umin(uc, ud)) - nc);
 }
 
+// Top-3 of a chunk: chunk_top2, then one more pass over the registers (which then hold
+// key - c1 - 1, wrapped): key - c2 - 1 = r - (c2 - c1) is the smallest for the third key (c1's and
+// c2's own entries wrap to the top), so c3 = c2 + 1 + min.  Only keyed chunks pay for it.
+__device__ __forceinline__ void chunk_top3(uint32_t* r, uint32_t mask, uint32_t colbase, uint32_t one, int32_t& c1,
+                                           int32_t& c2, int32_t& c3) {
+  chunk_top2(r, mask, colbase, one, c1, c2);
+  const uint32_t delta = (uint32_t)c2 - (uint32_t)c1;
+  uint32_t w[11];
+#pragma unroll
+  for (int j = 0; j < 10; ++j)
+    w[j] = umin(umin(r[3 * j] - delta, r[3 * j + 1] - delta), r[3 * j + 2] - delta);
+  w[10] = umin(r[30] - delta, r[31] - delta);
+  const uint32_t ua = umin(umin(w[0], w[1]), w[2]), ub = umin(umin(w[3], w[4]), w[5]);
+  const uint32_t uc = umin(umin(w[6], w[7]), w[8]), ud = umin(w[9], w[10]);
+  c3 = (int32_t)((uint32_t)c2 + 1u + umin(umin(ua, ub), umin(uc, ud)));
+}
+
 // merge a chunk's (c1 < c2) into a running (b1 <= b2)
 __device__ __forceinline__ void merge_top2(int32_t& b1, int32_t& b2, int32_t c1, int32_t c2) {
   b2 = imin(imin(b2, c2), imax(b1, c1));
@@ -1117,9 +1134,10 @@ __global__ void __launch_bounds__(256 + 128 * EPI_WG, 1)
             continue;
           }
 #endif
-          int32_t c1, c2;
-          chunk_top2(r[cc & 1], key_mask, (uint32_t)(cc * 32), key_mask >> 31, c1, c2);
-          t3 = imin(imin(t3, c2), imax(t2, c1));  // merge path of sorted triples (old t2, old k1)
+          int32_t c1, c2, c3;
+          chunk_top3(r[cc & 1], key_mask, (uint32_t)(cc * 32), key_mask >> 31, c1, c2, c3);
+          // merge path of sorted triples (k1, t2, t3) and (c1, c2, c3) (old values on the right)
+          t3 = imin(imin(t3, c3), imin(imax(k1, c2), imax(t2, c1)));
           t2 = imin(imin(t2, c2), imax(k1, c1));
           merge_top2(k1, k2, c1, c2);
         }

@@ -10,6 +10,10 @@
 // Paper: assignment = `euclideanDistance` + `searchPosMin`, update =
 // k-means prototype = mean of members, levels P:631-638.
 #include <cuda_runtime.h>
+#include <cstdio>
+#include <cstdlib>
+#include <type_traits>
+#include <utility>
 
 #include <map>
 #include <mutex>
@@ -138,6 +142,9 @@ __global__ void __launch_bounds__(256) k_blocked_argmin(const float* __restrict_
                                                         const int32_t* __restrict__ count_dev, int64_t cap,
                                                         int nsm, unsigned long long* __restrict__ keys,
                                                         const int* __restrict__ active) {
+  using Acc = float;  // (FP32 keys: the shared key code below)
+  constexpr bool EXACT = false;
+  constexpr int jbits = 0;
   if (active && !*active) return;  // level converged: this pass is skipped on the device
   __shared__ float xs[FX_R * (FX_DK + 1)];
   __shared__ float cs[FX_P * (FX_DK + 1)];
@@ -156,11 +163,11 @@ __global__ void __launch_bounds__(256) k_blocked_argmin(const float* __restrict_
     const int64_t f0 = (w / splits) * FX_R;
     const int64_t t0 = (w % splits) * tps;
     const int64_t t1 = min64(ntile, t0 + tps);
-    float bv[4];
+    Acc bv[4];
     int64_t bj[4];
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
-      bv[a] = INFINITY;
+      bv[a] = (Acc)INFINITY;
       bj[a] = INT64_MAX;
     }
     for (int64_t tile = t0; tile < t1; ++tile) {
@@ -216,8 +223,13 @@ __global__ void __launch_bounds__(256) k_blocked_argmin(const float* __restrict_
     for (int a = 0; a < 4; ++a) {
       const int64_t f = f0 + rg * 4 + a;
       if (f < nf && bj[a] != INT64_MAX) {
-        const unsigned long long key =
-            ((unsigned long long)__float_as_uint(fmaxf(bv[a], 0.f)) << 32) | (unsigned long long)(uint32_t)bj[a];
+        unsigned long long key;
+        if constexpr (EXACT) {
+          const unsigned long long m = (1ull << jbits) - 1ull;
+          key = ((unsigned long long)__double_as_longlong((double)bv[a]) & ~m) | (unsigned long long)bj[a];
+        } else {
+          key = ((unsigned long long)__float_as_uint(fmaxf((float)bv[a], 0.f)) << 32) | (unsigned long long)(uint32_t)bj[a];
+        }
         atomicMin(keys + f, key);
       }
     }
@@ -232,16 +244,24 @@ __global__ void k_keys_init(const int32_t* __restrict__ count_dev, int64_t cap, 
     keys[f] = ~0ull;
 }
 
+// key formats: jbits == 0: (fp32 bits of d^2) << 32 | j;  jbits > 0 (exact re-check): the FP64
+// d^2 bits with the low jbits replaced by j (order = d^2 to 2^-(52-jbits) relative, then j)
 __global__ void k_keys_write(const int32_t* __restrict__ rows, const int32_t* __restrict__ count_dev, int64_t cap,
                              const unsigned long long* __restrict__ keys, int32_t* __restrict__ labels,
-                             float* __restrict__ best, const int* __restrict__ active) {
+                             float* __restrict__ best, const int* __restrict__ active, int jbits) {
   if (active && !*active) return;  // level converged: this pass is skipped on the device
   const int64_t nf = count_dev ? min64(*count_dev, cap) : cap;
   for (int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; f < nf; f += (int64_t)gridDim.x * blockDim.x) {
     const unsigned long long key = keys[f];
     const int64_t row = rows ? (int64_t)rows[f] : f;
-    labels[row] = (int32_t)(key & 0xffffffffu);
-    if (best) best[row] = __uint_as_float((uint32_t)(key >> 32));
+    if (jbits == 0) {
+      labels[row] = (int32_t)(key & 0xffffffffu);
+      if (best) best[row] = __uint_as_float((uint32_t)(key >> 32));
+    } else {
+      const unsigned long long m = (1ull << jbits) - 1ull;
+      labels[row] = (int32_t)(key & m);
+      if (best) best[row] = (float)__longlong_as_double((long long)(key & ~m));
+    }
   }
 }
 
@@ -252,12 +272,16 @@ __global__ void k_keys_write(const int32_t* __restrict__ rows, const int32_t* __
 // dimension order, the same arithmetic as the FP32 direct form of the oracle comparison.
 constexpr int RB_R = 32, RB_P = 128;
 
+// EXACT (the K4 full re-check): FP64 sums of separately rounded squares of the FP64 differences
+// in dimension order (the oracle's arithmetic), key = FP64 d^2 with its low jbits replaced by j.
+template <bool EXACT>
 __global__ void __launch_bounds__(256) k_rb_argmin(const float* __restrict__ X, int d, int d4p,
                                                    const float* __restrict__ P, int64_t k,
                                                    const int32_t* __restrict__ rows,
                                                    const int32_t* __restrict__ count_dev, int64_t cap, int nsm,
                                                    unsigned long long* __restrict__ keys,
-                                                   const int* __restrict__ active) {
+                                                   const int* __restrict__ active, int jbits) {
+  using Acc = typename std::conditional<EXACT, double, float>::type;
   if (active && !*active) return;  // level converged: this pass is skipped on the device
   extern __shared__ float4 rsm[];
   const int64_t nf = count_dev ? min64(*count_dev, cap) : cap;
@@ -300,11 +324,11 @@ __global__ void __launch_bounds__(256) k_rb_argmin(const float* __restrict__ X, 
       }
       xs[r * d4p + c4] = v;
     }
-    float bv[4];
+    Acc bv[4];
     int64_t bj[4];
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
-      bv[a] = INFINITY;
+      bv[a] = (Acc)INFINITY;
       bj[a] = INT64_MAX;
     }
     for (int64_t tile = t0; tile < t1; ++tile) {
@@ -327,11 +351,11 @@ __global__ void __launch_bounds__(256) k_rb_argmin(const float* __restrict__ X, 
         cs[pr * d4p + c4] = v;
       }
       __syncthreads();
-      float acc[4][4];
+      Acc acc[4][4];
 #pragma unroll
       for (int a = 0; a < 4; ++a)
 #pragma unroll
-        for (int b = 0; b < 4; ++b) acc[a][b] = 0.f;
+        for (int b = 0; b < 4; ++b) acc[a][b] = (Acc)0;
       for (int c4 = 0; c4 < d4; ++c4) {
         float4 xv[4], cv[4];
 #pragma unroll
@@ -342,14 +366,25 @@ __global__ void __launch_bounds__(256) k_rb_argmin(const float* __restrict__ X, 
         for (int a = 0; a < 4; ++a)
 #pragma unroll
           for (int b = 0; b < 4; ++b) {  // dimensions in increasing order (zero padding adds 0)
-            float df = xv[a].x - cv[b].x;
-            acc[a][b] = fmaf(df, df, acc[a][b]);
-            df = xv[a].y - cv[b].y;
-            acc[a][b] = fmaf(df, df, acc[a][b]);
-            df = xv[a].z - cv[b].z;
-            acc[a][b] = fmaf(df, df, acc[a][b]);
-            df = xv[a].w - cv[b].w;
-            acc[a][b] = fmaf(df, df, acc[a][b]);
+            if constexpr (EXACT) {
+              double df = (double)xv[a].x - (double)cv[b].x;
+              acc[a][b] = __dadd_rn(acc[a][b], __dmul_rn(df, df));
+              df = (double)xv[a].y - (double)cv[b].y;
+              acc[a][b] = __dadd_rn(acc[a][b], __dmul_rn(df, df));
+              df = (double)xv[a].z - (double)cv[b].z;
+              acc[a][b] = __dadd_rn(acc[a][b], __dmul_rn(df, df));
+              df = (double)xv[a].w - (double)cv[b].w;
+              acc[a][b] = __dadd_rn(acc[a][b], __dmul_rn(df, df));
+            } else {
+              float df = xv[a].x - cv[b].x;
+              acc[a][b] = fmaf(df, df, acc[a][b]);
+              df = xv[a].y - cv[b].y;
+              acc[a][b] = fmaf(df, df, acc[a][b]);
+              df = xv[a].z - cv[b].z;
+              acc[a][b] = fmaf(df, df, acc[a][b]);
+              df = xv[a].w - cv[b].w;
+              acc[a][b] = fmaf(df, df, acc[a][b]);
+            }
           }
       }
 #pragma unroll
@@ -369,8 +404,13 @@ __global__ void __launch_bounds__(256) k_rb_argmin(const float* __restrict__ X, 
     for (int a = 0; a < 4; ++a) {
       const int64_t f = f0 + a * 8 + rg;
       if (f < nf && bj[a] != INT64_MAX) {
-        const unsigned long long key =
-            ((unsigned long long)__float_as_uint(fmaxf(bv[a], 0.f)) << 32) | (unsigned long long)(uint32_t)bj[a];
+        unsigned long long key;
+        if constexpr (EXACT) {
+          const unsigned long long m = (1ull << jbits) - 1ull;
+          key = ((unsigned long long)__double_as_longlong((double)bv[a]) & ~m) | (unsigned long long)bj[a];
+        } else {
+          key = ((unsigned long long)__float_as_uint(fmaxf((float)bv[a], 0.f)) << 32) | (unsigned long long)(uint32_t)bj[a];
+        }
         atomicMin(keys + f, key);
       }
     }
@@ -379,40 +419,46 @@ __global__ void __launch_bounds__(256) k_rb_argmin(const float* __restrict__ X, 
 
 static void launch_blocked(const float* X, int d, const float* P, int64_t k, const int32_t* rows,
                            const int32_t* count_dev, int64_t cap, unsigned long long* keys_ws, int32_t* labels,
-                           float* best, cudaStream_t st, const int* active) {
+                           float* best, cudaStream_t st, const int* active, bool exact = false) {
   k_keys_init<<<num_sms() * 2, 256, 0, st>>>(count_dev, cap, keys_ws, active);
   MASK_LAUNCH_CHECK();
   const int d4 = (d + 3) / 4;
   const int d4p = d4 | 1;  // odd float4 stride
   const size_t rb_smem = (size_t)(RB_R + RB_P) * d4p * sizeof(float4);
+  int jbits = 0;  // exact keys: bits of j (the rest of the 64-bit key orders the FP64 d^2)
+  if (exact)
+    while ((int64_t(1) << jbits) < k) ++jbits;
+  if (exact && jbits == 0) jbits = 1;
+  const auto kern = exact ? k_rb_argmin<true> : k_rb_argmin<false>;
   if (d <= 256 && rb_smem <= 200 * 1024) {
-    static int attr_for = -1;
-    if (rb_smem > 48 * 1024 && attr_for < (int)rb_smem) {
-      MASK_CUDA(cudaFuncSetAttribute(k_rb_argmin, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-      attr_for = 200 * 1024;
+    static int attr_for[2] = {-1, -1};
+    if (rb_smem > 48 * 1024 && attr_for[exact] < (int)rb_smem) {
+      MASK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      attr_for[exact] = 200 * 1024;
     }
     // one wave of resident CTAs (the flagged count is only known on the device: small counts
     // split the prototypes finely so every CTA gets one short item)
-    static std::map<size_t, int> occ_cache;
+    static std::map<std::pair<size_t, bool>, int> occ_cache;
     int occ = 0;
     {
       static std::mutex mu;
       std::lock_guard<std::mutex> lock(mu);
-      auto it = occ_cache.find(rb_smem);
+      auto it = occ_cache.find({rb_smem, exact});
       if (it == occ_cache.end()) {
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_rb_argmin, 256, rb_smem) != cudaSuccess) occ = 2;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, rb_smem) != cudaSuccess) occ = 2;
         (void)cudaGetLastError();
-        it = occ_cache.emplace(rb_smem, std::max(1, std::min(occ, 8))).first;
+        it = occ_cache.emplace(std::make_pair(rb_smem, exact), std::max(1, std::min(occ, 8))).first;
       }
       occ = it->second;
     }
     const int grid = num_sms() * occ;
-    k_rb_argmin<<<grid, 256, rb_smem, st>>>(X, d, d4p, P, k, rows, count_dev, cap, grid, keys_ws, active);
+    kern<<<grid, 256, rb_smem, st>>>(X, d, d4p, P, k, rows, count_dev, cap, grid, keys_ws, active, jbits);
   } else {
+    jbits = 0;  // (the plain blocked kernel keeps FP32 keys)
     k_blocked_argmin<<<num_sms() * 4, 256, 0, st>>>(X, d, P, k, rows, count_dev, cap, num_sms(), keys_ws, active);
   }
   MASK_LAUNCH_CHECK();
-  k_keys_write<<<num_sms() * 2, 256, 0, st>>>(rows, count_dev, cap, keys_ws, labels, best, active);
+  k_keys_write<<<num_sms() * 2, 256, 0, st>>>(rows, count_dev, cap, keys_ws, labels, best, active, jbits);
   MASK_LAUNCH_CHECK();
 }
 
@@ -462,7 +508,21 @@ void launch_fixup_device(const float* X, int d, const float* P, int64_t k, const
   k_fix_pairs<<<num_sms() * 4, 256, 0, st>>>(X, d, P, flag_rows, flag_pair, flag_count, cap, labels, best,
                                              rescan_rows, rescan_count, active);
   MASK_LAUNCH_CHECK();
-  launch_blocked(X, d, P, k, rescan_rows, rescan_count, cap, keys_ws, labels, best, st, active);
+  static const bool dbg = getenv("MASK_DEBUG_FIXUP") != nullptr;
+  if (dbg) {  // development: flagged / re-scanned counts and the first pairs
+    int32_t hc[2] = {0, 0};
+    cudaMemcpyAsync(hc, flag_count, 4, cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(hc + 1, rescan_count, 4, cudaMemcpyDeviceToHost, st);
+    int2 hp[8];
+    int32_t hr[8];
+    cudaMemcpyAsync(hp, flag_pair, sizeof(hp), cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(hr, flag_rows, sizeof(hr), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    fprintf(stderr, "[fixup] flagged %d rescan %d |", hc[0], hc[1]);
+    for (int i = 0; i < 8 && i < hc[0]; ++i) fprintf(stderr, " %d:(%d,%d)", hr[i], hp[i].x, hp[i].y);
+    fprintf(stderr, "\n");
+  }
+  launch_blocked(X, d, P, k, rescan_rows, rescan_count, cap, keys_ws, labels, best, st, active, /*exact=*/true);
 }
 
 void launch_assign_blocked(const float* X, int64_t n, int d, const float* P, int64_t k, unsigned long long* keys_ws,
