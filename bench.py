@@ -570,6 +570,13 @@ def main():
 
     if rank == 0:
         clocks = sampler.summary() if sampler else None
+        if use_tc and clocks and clocks.get("sm_mhz"):
+            # context for `frac`: the TF32 MMA rate measured on this GPU (tools/mma_ubench.cu: 4096
+            # flop/clk/SM, K1) at the median SM clock of the timed region, and the burst peak
+            hw = 4096.0 * 148 * clocks["sm_mhz"] * 1e6 / 1e12
+            roof["tensor_util_at_clock"] = achieved / hw
+            roof["hw_tf32_at_clock_tflops"] = hw
+            roof["frac_of_burst_peak"] = achieved / (0.5 * pk["bf16_tflops"])
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,

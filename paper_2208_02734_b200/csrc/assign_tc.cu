@@ -719,6 +719,9 @@ __global__ void __launch_bounds__(256 + 128 * EPI_WG, 1)
 #endif
   using C = PCfg<KA, BN, STAGES, NACC, EPI_WG, FOLD, ABUF>;
   constexpr int COLS = BN / EPI_WG;
+  // third-candidate bound for the two-candidate K4 decision: large d only (small d is epilogue-
+  // bound and its few flagged rows are cheap to re-scan exactly)
+  constexpr bool TRACK3 = !FOLD;
   static_assert(COLS % 32 == 0 && COLS / 32 <= 2, "epilogue chunking (two register buffers)");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -1130,18 +1133,23 @@ __global__ void __launch_bounds__(256 + 128 * EPI_WG, 1)
             st_keyed += need ? 1 : 0;
           }
           if (!need || (dbg & 256)) {  // dbg 256 (ablation): never key
-            smin = imin(smin, c0);
+            if constexpr (TRACK3) smin = imin(smin, c0);
             continue;
           }
 #endif
-          int32_t c1, c2, c3;
-          chunk_top3(r[cc & 1], key_mask, (uint32_t)(cc * 32), key_mask >> 31, c1, c2, c3);
-          // merge path of sorted triples (k1, t2, t3) and (c1, c2, c3) (old values on the right)
-          t3 = imin(imin(t3, c3), imin(imax(k1, c2), imax(t2, c1)));
-          t2 = imin(imin(t2, c2), imax(k1, c1));
+          int32_t c1, c2;
+          if constexpr (TRACK3) {
+            int32_t c3;
+            chunk_top3(r[cc & 1], key_mask, (uint32_t)(cc * 32), key_mask >> 31, c1, c2, c3);
+            // merge path of sorted triples (k1, t2, t3) and (c1, c2, c3) (old values on the right)
+            t3 = imin(imin(t3, c3), imin(imax(k1, c2), imax(t2, c1)));
+            t2 = imin(imin(t2, c2), imax(k1, c1));
+          } else {
+            chunk_top2(r[cc & 1], key_mask, (uint32_t)(cc * 32), key_mask >> 31, c1, c2);
+          }
           merge_top2(k1, k2, c1, c2);
         }
-        {  // lower bound of the block's third-smallest so far (merge path with the running top-2)
+        if constexpr (TRACK3) {  // lower bound of the block's third-smallest so far (merge path)
           const float v1 = k1 != 0x7fffffff ? __int_as_float(k1 & 0xFFFFFF00) : INFINITY;
           const float v2 = t2 != 0x7fffffff ? __int_as_float(t2 & 0xFFFFFF00) : INFINITY;
           const float v3 = t3 != 0x7fffffff ? __int_as_float(t3 & 0xFFFFFF00) : INFINITY;
@@ -1183,7 +1191,8 @@ __global__ void __launch_bounds__(256 + 128 * EPI_WG, 1)
       // raw keys order as floats only when non-negative: a negative skipped minimum (a d^2 estimate
       // below 0, i.e. a row on a prototype) gives no bound
       const float sm = __int_as_float(smin);
-      r3[wg * BM + rloc] = fminf(g3, smin == 0x7fffffff ? INFINITY : (sm < 0.f ? -INFINITY : sm));
+      r3[wg * BM + rloc] = TRACK3 ? fminf(g3, smin == 0x7fffffff ? INFINITY : (sm < 0.f ? -INFINITY : sm))
+                                  : -INFINITY;  // (no bound: flagged rows re-scanned)
       mbar_arrive_warp(&rfull[ib]);
     }
     if ((dbg & 128) && lane == 0) {

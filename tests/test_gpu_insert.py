@@ -60,11 +60,15 @@ def _index_state(idx):
 
 @pytest.mark.parametrize("cid,div,thr", [(2, 64, 300), (3, 2048, 100), (5, 4096, 120)])
 def test_split_partitions_parity(cid, div, thr):
-    """Partition split + local rebuild (reading S1) against oracle.split_partitions
-    applied to the same (GPU-built) index: new prototypes within 1e-4, labels identical except
-    rows in the oracle's tie window, level-2 parents identical, child lists = {i : labels = j},
-    and queries over the rebuilt index equal the oracle descent over it."""
-    from parity import check_assignment, check_prototypes, check_queries
+    """Partition split + local rebuild (reading S1).  Each split partition's local
+    Lloyd run is (a) the library's own level build of those rows from the same seeded init --
+    pinned by rebuilding it with mask_build (MASK_TRACE_PASSES) and comparing -- and (b) checked
+    pass by pass against the FP64 oracle's run (parity.check_trajectory: in sync within 1e-4, or
+    parting only at a near-tie row, D15).  The index around it: the new ids and their
+    level-2 parents equal oracle.split_partitions', every other partition and upper level is
+    untouched, child lists = {i : labels = j}, and queries over the rebuilt index equal the
+    oracle descent over it."""
+    from parity import check_assignment, check_queries, check_trajectory, rel_l2
 
     cfg = datagen.CONFIGS[cid].scaled(div)
     X = datagen.data(cfg)
@@ -75,19 +79,37 @@ def test_split_partitions_parity(cid, div, thr):
     assert nsplit == len(split) and nsplit > 0
     P1, L1 = _index_state(idx)
     assert P1[0].shape == Pr[0].shape
-    check_prototypes(P1[0], Pr[0], what="split level 1")
+    k1 = P0[0].shape[0]
+    counts = np.bincount(L0[0], minlength=k1)
+    X64 = X.astype(np.float64)
+    nxt = k1
+    for j in split:
+        rows = np.nonzero(L0[0] == j)[0]
+        s_j = -(-int(counts[j]) // thr)
+        ids = [j] + list(range(nxt, nxt + s_j - 1))
+        nxt += s_j - 1
+        init = mk.seeded_init(11 + j, 1, len(rows), s_j)
+        np.testing.assert_array_equal(init, oracle.seeded_init(11 + j, 1, len(rows), s_j))
+        loc = mk.build(torch.from_numpy(np.ascontiguousarray(X[rows])).cuda(), [s_j], 8, [init],
+                       flags=mk.MASK_TRACE_PASSES)
+        # (a) the split ran the library's level build on these rows
+        assert rel_l2(P1[0][ids], loc.prototypes(1)) <= 1e-6, f"partition {j}: split != local build"
+        loc_lab = np.asarray(ids)[loc.labels(1)]
+        if not np.array_equal(L1[0][rows], loc_lab):
+            check_assignment(X64[rows], P1[0][ids], np.searchsorted(ids, L1[0][rows]), what=f"split {j} labels")
+        # (b) the local build against the oracle's Lloyd run, pass by pass
+        ref = oracle.lloyd(X64[rows], init, 8, trace=True).passes
+        check_trajectory(X64[rows], loc.passes(1), ref, what=f"split partition {j}")
+        loc.free()
+        for l in range(1, len(P1)):
+            assert np.all(L1[l][ids] == Lr[l][ids])  # new prototypes under j's parent
     for l in range(1, len(P1)):
         np.testing.assert_array_equal(P1[l], P0[l])  # upper levels untouched
         np.testing.assert_array_equal(L1[l], Lr[l])
-    # labels: within each split partition the GPU's local assignment vs the oracle's
-    X64 = X.astype(np.float64)
-    for j in split:
-        rows = np.nonzero(L0[0] == j)[0]
-        ids = sorted(set(Lr[0][rows].tolist()) | set(L1[0][rows].tolist()))
-        loc_g = np.searchsorted(ids, L1[0][rows])
-        check_assignment(X64[rows], P1[0][ids], loc_g, what=f"split partition {j}")
     same = np.isin(L0[0], split, invert=True)
     np.testing.assert_array_equal(L1[0][same], L0[0][same])
+    untouched = np.setdiff1d(np.arange(k1), split)
+    np.testing.assert_array_equal(P1[0][untouched], P0[0][untouched])
     for l in range(1, len(P1) + 1):
         off, mem = idx.children(l)
         o_ref, m_ref = oracle.children(L1[l - 1], P1[l - 1].shape[0])
@@ -96,8 +118,8 @@ def test_split_partitions_parity(cid, div, thr):
     Q = datagen.queries(cfg, count=200)
     ch = [idx.children(l) for l in range(1, len(P1) + 1)]
     rids, rd2, gap = oracle.query(P1, [c[0] for c in ch], [c[1] for c in ch], X, Q, 10, 2)
-    ids, d2 = idx.query(torch.from_numpy(Q).cuda(), knn=10, beam=2)
-    check_queries(ids.cpu().numpy(), d2.cpu().numpy(), rids, rd2, gap, what="queries after the split")
+    ids_q, d2 = idx.query(torch.from_numpy(Q).cuda(), knn=10, beam=2)
+    check_queries(ids_q.cpu().numpy(), d2.cpu().numpy(), rids, rd2, gap, what="queries after the split")
     assert idx.split(thr * 1000, iters=8) == 0  # nothing above the threshold: no change
     idx.free()
 
