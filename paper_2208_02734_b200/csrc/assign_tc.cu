@@ -1445,10 +1445,24 @@ void launch_assign_tc(const float* X, int64_t n, int d, const float* P, const fl
       tc::launch_persist<32, 192, 4, 2, 3, false, 2>(X, n, d, kc, kr, P, Pb, Ps, cn2, k, xn2, labels, best,
                                                      flag_rows, flag_count, c2, st, active, perm, prev_lab, lab2,
                                                      flag_pair);
-    else if (d <= 64)
-      tc::launch_persist<64, 128, 6, 2, 2, false, 2>(X, n, d, kc, kr, P, Pb, Ps, cn2, k, xn2, labels, best,
-                                                     flag_rows, flag_count, c2, st, active, perm, prev_lab, lab2,
-                                                     flag_pair);
+    else if (d <= 64) {
+      static const int var = [] {  // development A/B of the d = 64 tiling (MASK_TC_D64=1/2)
+        const char* e = getenv("MASK_TC_D64");
+        return e ? atoi(e) : 0;
+      }();
+      if (var == 1)
+        tc::launch_persist<64, 128, 6, 3, 2, false, 1>(X, n, d, kc, kr, P, Pb, Ps, cn2, k, xn2, labels, best,
+                                                       flag_rows, flag_count, c2, st, active, perm, prev_lab, lab2,
+                                                       flag_pair);
+      else if (var == 2)
+        tc::launch_persist<64, 192, 4, 2, 3, false, 1>(X, n, d, kc, kr, P, Pb, Ps, cn2, k, xn2, labels, best,
+                                                       flag_rows, flag_count, c2, st, active, perm, prev_lab, lab2,
+                                                       flag_pair);
+      else
+        tc::launch_persist<64, 128, 6, 2, 2, false, 2>(X, n, d, kc, kr, P, Pb, Ps, cn2, k, xn2, labels, best,
+                                                       flag_rows, flag_count, c2, st, active, perm, prev_lab, lab2,
+                                                       flag_pair);
+    }
     else if (d <= 96)
       tc::launch_persist<96, 128, 6, 2, 2, false, 1>(X, n, d, kc, kr, P, Pb, Ps, cn2, k, xn2, labels, best,
                                                      flag_rows, flag_count, c2, st, active, perm, prev_lab, lab2,
