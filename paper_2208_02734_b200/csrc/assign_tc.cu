@@ -1446,11 +1446,14 @@ void launch_assign_tc(const float* X, int64_t n, int d, const float* P, const fl
                                                      flag_rows, flag_count, c2, st, active, perm, prev_lab, lab2,
                                                      flag_pair);
     else if (d <= 64) {
-      static const int var = [] {  // development A/B of the d = 64 tiling (MASK_TC_D64=1/2)
+      // three accumulators (one A buffer): the extra tile of slack between the MMAs and the
+      // epilogue measured 32.5 -> 30.6 ms (n = 1e6, k = 65,536) and 349 -> 318 ms per C3 pass;
+      // MASK_TC_D64=1 / 2 select the two-accumulator / 192-wide variants (development A/B)
+      static const int var = [] {
         const char* e = getenv("MASK_TC_D64");
         return e ? atoi(e) : 0;
       }();
-      if (var == 1)
+      if (var == 0)
         tc::launch_persist<64, 128, 6, 3, 2, false, 1>(X, n, d, kc, kr, P, Pb, Ps, cn2, k, xn2, labels, best,
                                                        flag_rows, flag_count, c2, st, active, perm, prev_lab, lab2,
                                                        flag_pair);
@@ -1461,7 +1464,7 @@ void launch_assign_tc(const float* X, int64_t n, int d, const float* P, const fl
       else
         tc::launch_persist<64, 128, 6, 2, 2, false, 2>(X, n, d, kc, kr, P, Pb, Ps, cn2, k, xn2, labels, best,
                                                        flag_rows, flag_count, c2, st, active, perm, prev_lab, lab2,
-                                                       flag_pair);
+                                                       flag_pair);  // MASK_TC_D64=1
     }
     else if (d <= 96)
       tc::launch_persist<96, 128, 6, 2, 2, false, 1>(X, n, d, kc, kr, P, Pb, Ps, cn2, k, xn2, labels, best,
