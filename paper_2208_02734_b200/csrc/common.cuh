@@ -147,13 +147,18 @@ void launch_group_lloyd(const float* Y, int d, const int64_t* perm, int64_t n_it
 void launch_fixup_device(const float* X, int d, const float* P, int64_t k, const int32_t* flag_rows,
                          const int32_t* flag_count, int64_t cap, unsigned long long* keys_ws, int32_t* labels,
                          float* best, cudaStream_t st, const int* active = nullptr, const int2* flag_pair = nullptr,
-                         int32_t* rescan_rows = nullptr, int32_t* rescan_count = nullptr);
+                         int32_t* rescan_rows = nullptr, int32_t* rescan_count = nullptr,
+                         const double* P64 = nullptr);
+// FP64-prototype levels (D15): FP64 sums, FP64 finalize (P64 and its fp32 rounding P)
+void launch_update_dense64(const float* X, int64_t n, int d, const int32_t* labels, double* S, int32_t* counts,
+                           cudaStream_t st, const int* active, const int32_t* perm);
+void launch_f32_to_f64(const float* a, int64_t n, double* b, cudaStream_t st);
 // prototype operands for K1: Pb = tf32_rn(-2c), Ps = tf32_rn(-2c - Pb), cn2 = ||c||^2; with
 // kc > d the augmented columns [d] = split(||c||^2), [d+1] = (1, 0), rest 0 (row stride kc)
 // flag_count (optional): reset to 0 (the list K1 appends near-tie rows to)
 void launch_prep_protos(const float* P, int64_t k, int d, int kc, float* Pb, float* Ps, float* cn2,
                         cudaStream_t st, int64_t k_rows, int fold, const int* active = nullptr,
-                        int32_t* flag_count = nullptr);
+                        int32_t* flag_count = nullptr, const double* P64 = nullptr);
 // rows of the K1 B operand arrays (k padded to whole 256-prototype tiles)
 int64_t tc_operand_rows(int64_t k);
 void launch_row_norms(const float* X, int64_t n, int d, float* xn2, cudaStream_t st);
@@ -201,6 +206,8 @@ struct LoopCtl {
 // lc.ctrl: the tolerance stop / pass count of the loop (k_after_update's logic) in the last block.
 void launch_finalize(float* P, float* S, int32_t* counts, int64_t k, int d, uint32_t* stat,
                      int keep_counts, cudaStream_t st, const int* active = nullptr, LoopCtl lc = LoopCtl());
+void launch_finalize64(double* P64, float* P, double* S, int32_t* counts, int64_t k, int d, uint32_t* stat,
+                       cudaStream_t st, const int* active, LoopCtl lc);
 // pass statistics: J = sum best (double), changed = #(cur != prev).  With lc.ctrl: the
 // no-change stop test (k_after_stats's logic, single GPU) in the last block.
 void launch_pass_stats(const int32_t* cur, const int32_t* prev, const float* best, int64_t n,

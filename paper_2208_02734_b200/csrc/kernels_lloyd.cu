@@ -466,7 +466,8 @@ static void launch_blocked(const float* X, int d, const float* P, int64_t k, con
 // take (K4): FP64 direct sums of squares in dimension order (separately rounded
 // products and sums, as the oracle's FP64 loop), smaller distance, then lower index (D4).
 // Rows without a pair are appended to the full re-check list.
-__global__ void k_fix_pairs(const float* __restrict__ X, int d, const float* __restrict__ P,
+template <class T>
+__global__ void k_fix_pairs(const float* __restrict__ X, int d, const T* __restrict__ P,
                             const int32_t* __restrict__ flag_rows, const int2* __restrict__ flag_pair,
                             const int32_t* __restrict__ flag_count, int64_t cap, int32_t* __restrict__ labels,
                             float* __restrict__ best, int32_t* __restrict__ rescan_rows,
@@ -481,8 +482,8 @@ __global__ void k_fix_pairs(const float* __restrict__ X, int d, const float* __r
       continue;
     }
     const float* x = X + (int64_t)row * d;
-    const float* c1 = P + (int64_t)jp.x * d;
-    const float* c2 = P + (int64_t)jp.y * d;
+    const T* c1 = P + (int64_t)jp.x * d;
+    const T* c2 = P + (int64_t)jp.y * d;
     double s1 = 0.0, s2 = 0.0;
     for (int i = 0; i < d; ++i) {
       const double xi = (double)x[i];
@@ -496,18 +497,82 @@ __global__ void k_fix_pairs(const float* __restrict__ X, int d, const float* __r
   }
 }
 
+// Exact full re-check of one flagged row per block against the FP64 prototypes: the oracle's
+// distance arithmetic for every prototype, (d^2, j) minimum over the block.
+__global__ void __launch_bounds__(256) k_rescan64(const float* __restrict__ X, int d, const double* __restrict__ P,
+                                                  int64_t k, const int32_t* __restrict__ rows,
+                                                  const int32_t* __restrict__ count, int32_t* __restrict__ labels,
+                                                  float* __restrict__ best, const int* __restrict__ active) {
+  if (active && !*active) return;
+  __shared__ double sd[8];
+  __shared__ int64_t sj[8];
+  const int64_t nf = *count;
+  for (int64_t f = blockIdx.x; f < nf; f += gridDim.x) {
+    const int32_t row = rows[f];
+    const float* x = X + (int64_t)row * d;
+    double bd = INFINITY;
+    int64_t bj = INT64_MAX;
+    for (int64_t j = threadIdx.x; j < k; j += blockDim.x) {  // j increasing per thread: keeps lowest
+      const double* c = P + j * d;
+      double s = 0.0;
+      for (int i = 0; i < d; ++i) {
+        const double t = (double)x[i] - c[i];
+        s = __dadd_rn(s, __dmul_rn(t, t));
+      }
+      if (s < bd) {
+        bd = s;
+        bj = j;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double od = __shfl_xor_sync(0xffffffffu, bd, o);
+      const int64_t oj = __shfl_xor_sync(0xffffffffu, bj, o);
+      if (od < bd || (od == bd && oj < bj)) {
+        bd = od;
+        bj = oj;
+      }
+    }
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) {
+      sd[w] = bd;
+      sj[w] = bj;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int u = 1; u < (int)(blockDim.x >> 5); ++u)
+        if (sd[u] < bd || (sd[u] == bd && sj[u] < bj)) {
+          bd = sd[u];
+          bj = sj[u];
+        }
+      labels[row] = (int32_t)bj;
+      best[row] = (float)bd;
+    }
+    __syncthreads();
+  }
+}
+
 void launch_fixup_device(const float* X, int d, const float* P, int64_t k, const int32_t* flag_rows,
                          const int32_t* flag_count, int64_t cap, unsigned long long* keys_ws, int32_t* labels,
                          float* best, cudaStream_t st, const int* active, const int2* flag_pair,
-                         int32_t* rescan_rows, int32_t* rescan_count) {
+                         int32_t* rescan_rows, int32_t* rescan_count, const double* P64) {
   if (!flag_pair) {
     launch_blocked(X, d, P, k, flag_rows, flag_count, cap, keys_ws, labels, best, st, active);
     return;
   }
   MASK_CUDA(cudaMemsetAsync(rescan_count, 0, sizeof(int32_t), st));
-  k_fix_pairs<<<num_sms() * 4, 256, 0, st>>>(X, d, P, flag_rows, flag_pair, flag_count, cap, labels, best,
-                                             rescan_rows, rescan_count, active);
+  if (P64)
+    k_fix_pairs<double><<<num_sms() * 4, 256, 0, st>>>(X, d, P64, flag_rows, flag_pair, flag_count, cap, labels, best,
+                                                       rescan_rows, rescan_count, active);
+  else
+    k_fix_pairs<float><<<num_sms() * 4, 256, 0, st>>>(X, d, P, flag_rows, flag_pair, flag_count, cap, labels, best,
+                                                      rescan_rows, rescan_count, active);
   MASK_LAUNCH_CHECK();
+  if (P64) {  // the level's FP64 prototypes: the re-scan reads them (oracle arithmetic)
+    k_rescan64<<<num_sms() * 4, 256, 0, st>>>(X, d, P64, k, rescan_rows, rescan_count, labels, best, active);
+    MASK_LAUNCH_CHECK();
+    return;
+  }
   static const bool dbg = getenv("MASK_DEBUG_FIXUP") != nullptr;
   if (dbg) {  // development: flagged / re-scanned counts and the first pairs
     int32_t hc[2] = {0, 0};
@@ -540,7 +605,8 @@ __device__ __forceinline__ float tf32_rn(float x) {
 
 // One warp per prototype: Pb = tf32(-2c), Ps = tf32(-2c - Pb) (3xTF32 split of the B operand,
 // the factor -2 is exact), cn2 = ||c||^2 accumulated in FP64 then rounded.
-__global__ void k_prep_protos(const float* __restrict__ P, int64_t k, int64_t k_rows, int d, int kc, int fold,
+template <class T>
+__global__ void k_prep_protos(const T* __restrict__ P, int64_t k, int64_t k_rows, int d, int kc, int fold,
                               float* __restrict__ Pb, float* __restrict__ Ps, float* __restrict__ cn2,
                               const int* __restrict__ active, int32_t* __restrict__ flag_count) {
   if (active && !*active) return;  // level converged: this pass is skipped on the device
@@ -550,11 +616,13 @@ __global__ void k_prep_protos(const float* __restrict__ P, int64_t k, int64_t k_
   for (int64_t j = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); j < k; j += warps) {
     double s = 0.0;
     for (int i = lane; i < d; i += 32) {
-      float c = P[j * d + i];
+      const T c = P[j * d + i];
       s += (double)c * (double)c;
-      float m2 = -2.f * c;
-      float b = tf32_rn(m2);
-      float r = tf32_rn(m2 - b);
+      // -2c split into two TF32 parts (from the FP64 prototype when the level keeps one: the
+      // split then represents the FP64 value, not its fp32 rounding)
+      const double m2 = -2.0 * (double)c;
+      const float b = tf32_rn((float)m2);
+      const float r = tf32_rn((float)(m2 - (double)b));
       if (Pb) Pb[j * kc + i] = b;
       if (Ps) Ps[j * kc + i] = r;
     }
@@ -589,10 +657,15 @@ __global__ void k_prep_protos(const float* __restrict__ P, int64_t k, int64_t k_
 }
 
 void launch_prep_protos(const float* P, int64_t k, int d, int kc, float* Pb, float* Ps, float* cn2,
-                        cudaStream_t st, int64_t k_rows, int fold, const int* active, int32_t* flag_count) {
+                        cudaStream_t st, int64_t k_rows, int fold, const int* active, int32_t* flag_count,
+                        const double* P64) {
   if (k_rows < k) k_rows = k;
-  k_prep_protos<<<grid_for(k * 32, 256), 256, 0, st>>>(P, k, k_rows, d, kc, fold, Pb, Ps, cn2, active,
-                                                       flag_count);
+  if (P64)
+    k_prep_protos<double><<<grid_for(k * 32, 256), 256, 0, st>>>(P64, k, k_rows, d, kc, fold, Pb, Ps, cn2, active,
+                                                                  flag_count);
+  else
+    k_prep_protos<float><<<grid_for(k * 32, 256), 256, 0, st>>>(P, k, k_rows, d, kc, fold, Pb, Ps, cn2, active,
+                                                                 flag_count);
   MASK_LAUNCH_CHECK();
 }
 
@@ -662,10 +735,12 @@ __global__ void k_update_dense(const float* __restrict__ X, int64_t n, int d,
 // step.  Every lane group accumulates its run of equal labels in registers and flushes it with
 // one red.global.add.v4 per float4 when the label changes: a run of m rows costs d/4 vector
 // reds instead of m*d/4 (atomics were the limit of the element-parallel kernel).
-template <int L>
+// Acc = double (the FP64 sums of a level that keeps FP64 prototypes): the run is accumulated
+// in FP64 and flushed with four scalar FP64 reds.
+template <int L, class Acc = float>
 __global__ void __launch_bounds__(256) k_update_runs(const float4* __restrict__ X4, const int32_t* __restrict__ perm,
                                                       int64_t n, int d4, const int32_t* __restrict__ labels,
-                                                      float* __restrict__ S, int32_t* __restrict__ counts,
+                                                      Acc* __restrict__ S, int32_t* __restrict__ counts,
                                                       const int* __restrict__ active) {
   if (active && !*active) return;  // level converged: this pass is skipped on the device
   constexpr int R = 32 / L, U = 4, CH = R * U * 4;  // 4 batches of U independent rows per lane group
@@ -674,13 +749,24 @@ __global__ void __launch_bounds__(256) k_update_runs(const float4* __restrict__ 
   const int64_t p0 = w * CH;
   if (p0 >= n) return;
   const int64_t p1 = p0 + CH < n ? p0 + CH : n;
-  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  struct A4 {
+    Acc x, y, z, w;
+  } acc{0, 0, 0, 0};
   int32_t cur = -1, cnt = 0;
   auto flush = [&]() {
-    if (c4 < d4)
-      asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(S + ((int64_t)cur * d4 + c4) * 4),
-                   "f"(acc.x), "f"(acc.y), "f"(acc.z), "f"(acc.w)
-                   : "memory");
+    if (c4 < d4) {
+      Acc* dst = S + ((int64_t)cur * d4 + c4) * 4;
+      if constexpr (sizeof(Acc) == 4) {
+        asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "f"((float)acc.x), "f"((float)acc.y),
+                     "f"((float)acc.z), "f"((float)acc.w)
+                     : "memory");
+      } else {
+        atomicAdd(dst + 0, acc.x);
+        atomicAdd(dst + 1, acc.y);
+        atomicAdd(dst + 2, acc.z);
+        atomicAdd(dst + 3, acc.w);
+      }
+    }
     if (c4 == 0) atomicAdd(counts + cur, cnt);
   };
   for (int64_t pb = p0 + slot; pb < p1; pb += R * U) {
@@ -704,18 +790,62 @@ __global__ void __launch_bounds__(256) k_update_runs(const float4* __restrict__ 
       if (lab[u] != cur) {
         if (cur >= 0) flush();
         cur = lab[u];
-        acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        acc = A4{0, 0, 0, 0};
         cnt = 0;
       }
-      acc.x += v[u].x;
-      acc.y += v[u].y;
-      acc.z += v[u].z;
-      acc.w += v[u].w;
+      acc.x += (Acc)v[u].x;
+      acc.y += (Acc)v[u].y;
+      acc.z += (Acc)v[u].z;
+      acc.w += (Acc)v[u].w;
       ++cnt;
     }
   }
   if (cur >= 0) flush();
 }
+
+// FP64 sums (a level that keeps FP64 prototypes): run kernel over the label-sorted rows, or one
+// FP64 atomic per element without a sort
+__global__ void k_update_dense64(const float* __restrict__ X, int64_t n, int d, const int32_t* __restrict__ labels,
+                                 double* __restrict__ S, int32_t* __restrict__ counts, const int* __restrict__ active) {
+  if (active && !*active) return;
+  const int64_t total = n * (int64_t)d;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / d;
+    const int c = (int)(e - i * d);
+    const int32_t j = labels[i];
+    atomicAdd(S + (int64_t)j * d + c, (double)X[e]);
+    if (c == 0) atomicAdd(counts + j, 1);
+  }
+}
+
+void launch_update_dense64(const float* X, int64_t n, int d, const int32_t* labels, double* S, int32_t* counts,
+                           cudaStream_t st, const int* active, const int32_t* perm) {
+  if (n <= 0) return;
+  if (perm && d % 4 == 0 && d <= 128 && ((uintptr_t)X % 16) == 0) {
+    const int d4 = d / 4;
+    const int L = d4 <= 1 ? 1 : d4 <= 2 ? 2 : d4 <= 4 ? 4 : d4 <= 8 ? 8 : d4 <= 16 ? 16 : 32;
+    const int64_t ch = (32 / L) * 16;
+    const int64_t warps = (n + ch - 1) / ch;
+    const unsigned grid = (unsigned)((warps + 7) / 8);
+    const float4* X4 = reinterpret_cast<const float4*>(X);
+    if (d4 <= 1) k_update_runs<1, double><<<grid, 256, 0, st>>>(X4, perm, n, d4, labels, S, counts, active);
+    else if (d4 <= 2) k_update_runs<2, double><<<grid, 256, 0, st>>>(X4, perm, n, d4, labels, S, counts, active);
+    else if (d4 <= 4) k_update_runs<4, double><<<grid, 256, 0, st>>>(X4, perm, n, d4, labels, S, counts, active);
+    else if (d4 <= 8) k_update_runs<8, double><<<grid, 256, 0, st>>>(X4, perm, n, d4, labels, S, counts, active);
+    else if (d4 <= 16) k_update_runs<16, double><<<grid, 256, 0, st>>>(X4, perm, n, d4, labels, S, counts, active);
+    else k_update_runs<32, double><<<grid, 256, 0, st>>>(X4, perm, n, d4, labels, S, counts, active);
+  } else {
+    k_update_dense64<<<grid_for(n * d, 256, (int64_t)num_sms() * 16), 256, 0, st>>>(X, n, d, labels, S, counts,
+                                                                                   active);
+  }
+  MASK_LAUNCH_CHECK();
+}
+
+// K7 for FP64 sums: P64_j = S_j / n_j in FP64 (the oracle's "sum, then one division"), P_j its
+// fp32 rounding; empty clusters keep both (D5); displacement in FP64; S and counts zeroed.
+__global__ void k_finalize64(double* __restrict__ P64, float* __restrict__ P, double* __restrict__ S,
+                             int32_t* __restrict__ counts, int64_t k, int d, uint32_t* __restrict__ stat,
+                             const int* __restrict__ active, LoopCtl lc);
 
 void launch_update_dense(const float* X, int64_t n, int d, const int32_t* labels, int64_t k,
                          float* S, int32_t* counts, cudaStream_t st, const int* active, const int32_t* perm) {
@@ -994,6 +1124,61 @@ __global__ void __launch_bounds__(256) k_finalize_wide(float* __restrict__ P, fl
       lc.ctrl[1] = lc.T;
     }
   }
+}
+
+__global__ void k_finalize64(double* __restrict__ P64, float* __restrict__ P, double* __restrict__ S,
+                             int32_t* __restrict__ counts, int64_t k, int d, uint32_t* __restrict__ stat,
+                             const int* __restrict__ active, LoopCtl lc) {
+  if (active && !*active) return;  // level converged: this pass is skipped on the device
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t j = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); j < k; j += warps) {
+    if (lc.zero_cnt && lane == 0) lc.zero_cnt[j] = 0;  // label-sort counts of the next pass
+    const int32_t cnt = counts[j];
+    double disp = 0.0;
+    if (cnt > 0) {
+      for (int i = lane; i < d; i += 32) {
+        const double c = __ddiv_rn(S[j * d + i], (double)cnt);
+        const double t = c - P64[j * d + i];
+        disp = fma(t, t, disp);
+        P64[j * d + i] = c;
+        P[j * d + i] = (float)c;
+        S[j * d + i] = 0.0;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) disp += __shfl_xor_sync(0xffffffffu, disp, o);
+    if (lane == 0) {
+      atomicMax(stat, __float_as_uint((float)disp));
+      if (cnt == 0) atomicAdd(stat + 1, 1u);
+      counts[j] = 0;
+    }
+  }
+  if (lc.ctrl && last_block_done(lc.ctrl + 3) && threadIdx.x == 0) {
+    const double disp = sqrt((double)__uint_as_float(*(volatile uint32_t*)stat));
+    if (lc.tol > 0.0 && disp <= lc.tol) {
+      lc.ctrl[0] = 0;
+      lc.ctrl[1] = lc.t + 1;
+    } else if (lc.t == lc.T - 1) {
+      lc.ctrl[1] = lc.T;
+    }
+  }
+}
+
+void launch_finalize64(double* P64, float* P, double* S, int32_t* counts, int64_t k, int d, uint32_t* stat,
+                       cudaStream_t st, const int* active, LoopCtl lc) {
+  k_finalize64<<<grid_for(k * 32, 256), 256, 0, st>>>(P64, P, S, counts, k, d, stat, active, lc);
+  MASK_LAUNCH_CHECK();
+}
+
+__global__ void k_f32_to_f64(const float* __restrict__ a, int64_t n, double* __restrict__ b) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    b[i] = (double)a[i];
+}
+void launch_f32_to_f64(const float* a, int64_t n, double* b, cudaStream_t st) {
+  if (n <= 0) return;
+  k_f32_to_f64<<<grid_for(n, 256), 256, 0, st>>>(a, n, b);
+  MASK_LAUNCH_CHECK();
 }
 
 void launch_finalize(float* P, float* S, int32_t* counts, int64_t k, int d, uint32_t* stat,

@@ -437,6 +437,8 @@ struct LloydWS {
   DevBuf<float> Pb, Ps, cn2, xn2, PT;
   DevBuf<int32_t> flag_rows, flag_count;
   DevBuf<int2> flag_pair;                     // K1 -> K4: the two candidates of a flagged row
+  DevBuf<double> P64;  // FP64 prototypes of a dense per-pass level (D15); nullptr otherwise
+  DevBuf<double> S64;  // their FP64 sums (+ the packed counts / J / changed tail for N1)
   DevBuf<int32_t> rescan_rows, rescan_count;  // K4: flagged rows that need the full re-check
   DevBuf<unsigned long long> fix_keys;
   DevBuf<int16_t> colslot;  // K3 chunk-major: hot slot of each column (-1 = read from L2)
@@ -543,7 +545,7 @@ void assign_pass(const Input& in, const float* P, int64_t k, int flags, int32_t*
     ws.xn2_ready = true;
   }
   launch_prep_protos(P, k, d, kc, ws.Pb.p, ws.Ps.p, ws.cn2.p, st, tc_operand_rows(k), d <= 24 ? 1 : 0, active,
-                     ws.flag_count.p);
+                     ws.flag_count.p, ws.P64.p);
   ws.kernel_id = 1;
   if (ev) ev->mark(MASK_T_ASSIGN, st);
   // small d (persistent K1): visit rows grouped by their previous label (perm, sorted after
@@ -558,7 +560,7 @@ void assign_pass(const Input& in, const float* P, int64_t k, int flags, int32_t*
   if (!(flags & MASK_NO_FIXUP)) {
     if (ev) ev->mark(MASK_T_FIXUP, st);
     launch_fixup_device(in.X, d, P, k, ws.flag_rows.p, ws.flag_count.p, n, ws.fix_keys.p, labels_out, best, st,
-                        active, ws.flag_pair.p, ws.rescan_rows.p, ws.rescan_count.p);
+                        active, ws.flag_pair.p, ws.rescan_rows.p, ws.rescan_count.p, ws.P64.p);
     if (ev) ev->mark(MASK_T_FIXUP, st);
   }
 }
@@ -612,6 +614,35 @@ void launch_unpack_pass(const float* tail, int64_t k, int32_t* counts, double* J
   k_unpack_pass<<<grid_for(std::max<int64_t>(k, 1), 256), 256, 0, st>>>(tail, k, counts, J, ch, ctrl, t, active);
   MASK_LAUNCH_CHECK();
 }
+// FP64 levels: the pass's N1 buffer is FP64 throughout, [S (k x d) | counts (k) | J | changed]
+// (integers exact below 2^53)
+__global__ void k_pack_pass64(const int32_t* __restrict__ counts, int64_t k, const double* __restrict__ J,
+                              const unsigned long long* __restrict__ ch, double* __restrict__ tail,
+                              const int* __restrict__ active) {
+  if (active && !*active) return;
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < k; j += (int64_t)gridDim.x * blockDim.x)
+    tail[j] = (double)counts[j];
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    tail[k] = *J;
+    tail[k + 1] = (double)*ch;
+  }
+}
+__global__ void k_unpack_pass64(const double* __restrict__ tail, int64_t k, int32_t* __restrict__ counts,
+                                double* __restrict__ J, unsigned long long* __restrict__ ch, int* ctrl, int t,
+                                const int* __restrict__ active) {
+  if (active && !*active) return;
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < k; j += (int64_t)gridDim.x * blockDim.x)
+    counts[j] = (int32_t)tail[j];
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    *J = tail[k];
+    const unsigned long long c = (unsigned long long)tail[k + 1];
+    *ch = c;
+    if (ctrl && t > 0 && c == 0) {
+      ctrl[0] = 0;
+      ctrl[1] = t + 1;
+    }
+  }
+}
 __global__ void k_copy_labels(int32_t* __restrict__ dst, const int32_t* __restrict__ src, int64_t n,
                               const int* __restrict__ active) {
   if (active && !*active) return;
@@ -655,7 +686,17 @@ void run_level(const Input& in, int64_t k, const int64_t* init_idx_host, const m
   ws.lab_prev.alloc(std::max<int64_t>(n, 1));
   ws.lab_cur.alloc(std::max<int64_t>(n, 1));
   ws.best.alloc(std::max<int64_t>(n, 1));
-  ws.S.alloc((size_t)k * d + (comm ? 2 * (size_t)k + 8 : 0));  // + the packed tail (N1)
+  // dense levels run by the per-pass kernels keep FP64 prototypes and sums (D15): the K4
+  // decisions and the update then follow the oracle's FP64 arithmetic; fp32 P is their rounding
+  const bool fused_level = in.format == MASK_DENSE_F32 && !comm && !p->iter_cb && !(p->flags & MASK_FORCE_SIMT) &&
+                           !(p->flags & MASK_NO_FUSED) && small_level_supported(n, d, k);
+  const bool p64 = in.format == MASK_DENSE_F32 && !fused_level;
+  if (p64) {
+    ws.P64.alloc((size_t)k * d);
+    ws.S64.alloc((size_t)k * d + (size_t)k + 2);
+  } else {
+    ws.S.alloc((size_t)k * d + (comm ? 2 * (size_t)k + 8 : 0));  // + the packed tail (N1)
+  }
   ws.counts.alloc(k);
   // per-pass statistics (slot T+1 = final pass) and loop control
   DevBuf<double> Jd(T + 2);
@@ -667,7 +708,8 @@ void run_level(const Input& in, int64_t k, const int64_t* init_idx_host, const m
   MASK_CUDA(cudaMemsetAsync(fin.p, 0, sizeof(uint32_t) * 2 * (T + 2), st));
   const int ctrl_init[4] = {1, 0, 0, 0};
   MASK_CUDA(cudaMemcpyAsync(ctrl.p, ctrl_init, sizeof(ctrl_init), cudaMemcpyHostToDevice, st));
-  MASK_CUDA(cudaMemsetAsync(ws.S.p, 0, sizeof(float) * k * d, st));
+  if (p64) MASK_CUDA(cudaMemsetAsync(ws.S64.p, 0, sizeof(double) * k * d, st));
+  else MASK_CUDA(cudaMemsetAsync(ws.S.p, 0, sizeof(float) * k * d, st));
   MASK_CUDA(cudaMemsetAsync(ws.counts.p, 0, sizeof(int32_t) * k, st));
   MASK_CUDA(cudaMemsetAsync(ws.lab_prev.p, 0xff, sizeof(int32_t) * std::max<int64_t>(n, 1), st));
   const int* active = ctrl.p;
@@ -699,6 +741,7 @@ void run_level(const Input& in, int64_t k, const int64_t* init_idx_host, const m
     launch_gather_rows(in.X, d, idx.p, k, in.row_offset, n, L.P.p, st);
   }
   if (comm) coll_allreduce(comm, L.P.p, (size_t)k * d, kF32, false, st);
+  if (p64) launch_f32_to_f64(L.P.p, (int64_t)k * d, ws.P64.p, st);
 
   // every event pair costs a few microseconds of device time per pass (~5 % of a C2 build for
   // all four classes), so MASK_TIME_ASSIGN times the assignment kernel alone
@@ -729,6 +772,19 @@ void run_level(const Input& in, int64_t k, const int64_t* init_idx_host, const m
   // halves and the rest so every fp32 partial sum stays exact
   const size_t pack_tail = (size_t)k * d;
   auto combine = [&](int slot, int t, bool with_sums, const int* act) {
+    if (p64) {  // FP64 buffer: [S | counts | J | changed], or the stats alone after the sums
+      double* tail = ws.S64.p + (with_sums ? pack_tail : 0);
+      const int64_t kk = with_sums ? k : 0;
+      k_pack_pass64<<<grid_for(std::max<int64_t>(kk, 1), 256), 256, 0, st>>>(ws.counts.p, kk, Jd.p + slot,
+                                                                           chd.p + slot, tail, act);
+      MASK_LAUNCH_CHECK();
+      coll_allreduce(comm, ws.S64.p, with_sums ? pack_tail + (size_t)k + 2 : 2, kF64, false, st);
+      k_unpack_pass64<<<grid_for(std::max<int64_t>(kk, 1), 256), 256, 0, st>>>(tail, kk, ws.counts.p, Jd.p + slot,
+                                                                             chd.p + slot, with_sums ? ctrl.p : nullptr,
+                                                                             t, act);
+      MASK_LAUNCH_CHECK();
+      return;
+    }
     // with sums: the whole buffer; stats only (final pass, S no longer needed): its first 4 floats
     float* tail = ws.S.p + (with_sums ? pack_tail : 0);
     const int64_t kk = with_sums ? k : 0;
@@ -739,8 +795,7 @@ void run_level(const Input& in, int64_t k, const int64_t* init_idx_host, const m
   };
 
   // small dense level without a communicator or step hook: the whole loop in one launch (K11)
-  const bool fused = in.format == MASK_DENSE_F32 && !comm && !p->iter_cb && !(p->flags & MASK_FORCE_SIMT) &&
-                     !(p->flags & MASK_NO_FUSED) && small_level_supported(n, d, k);
+  const bool fused = fused_level;
   if (fused) {
     DevBuf<unsigned> bar(2);
     DevBuf<double> S64((size_t)k * d);
@@ -795,6 +850,8 @@ void run_level(const Input& in, int64_t k, const int64_t* init_idx_host, const m
                                ws.counts.p, st, active);
     else if (in.format == MASK_CSR_F32)
       launch_update_csr(in.rp, in.col, in.val, n, d, ws.lab_cur.p, ws.S.p, ws.counts.p, st, active);
+    else if (p64)
+      launch_update_dense64(in.X, n, d, ws.lab_cur.p, ws.S64.p, ws.counts.p, st, active, sorted ? ws.perm.p : nullptr);
     else
       launch_update_dense(in.X, n, d, ws.lab_cur.p, k, ws.S.p, ws.counts.p, st, active,
                           sorted ? ws.perm.p : nullptr);
@@ -806,7 +863,8 @@ void run_level(const Input& in, int64_t k, const int64_t* init_idx_host, const m
     LoopCtl lf = lc;
     lf.ctrl = ctrl.p;  // tolerance stop / pass count (fin is identical on every rank)
     lf.zero_cnt = sorted ? ws.sort_cnt.p : nullptr;
-    launch_finalize(L.P.p, ws.S.p, ws.counts.p, k, d, fin.p + 2 * t, 0, st, active, lf);
+    if (p64) launch_finalize64(ws.P64.p, L.P.p, ws.S64.p, ws.counts.p, k, d, fin.p + 2 * t, st, active, lf);
+    else launch_finalize(L.P.p, ws.S.p, ws.counts.p, k, d, fin.p + 2 * t, 0, st, active, lf);
     if (ev) ev->mark(MASK_T_FINALIZE, st);
     if (!sorted) {
       k_copy_labels<<<grid_for(n, 256), 256, 0, st>>>(ws.lab_prev.p, ws.lab_cur.p, n, active);
