@@ -713,3 +713,53 @@ def test_split_partitions_invariants():
     # nothing above the threshold: nothing changes
     P3, L3, sp3 = oracle.split_partitions([P1, P2l], [labels0, labels1], X, threshold=int(counts.max()), T=8, seed=9)
     assert sp3 == [] and np.array_equal(P3[0], P1) and np.array_equal(L3[0], labels0)
+
+
+# ------------------------------------------------------------------ hand-derived pins (round 2)
+def _hand_index(P_levels, labels_levels):
+    """An oracle.Index from explicit prototypes and labels (child lists = {i : labels = j})."""
+    levels, offs, mems = [], [], []
+    for P, lab in zip(P_levels, labels_levels):
+        P = np.asarray(P, np.float64)
+        lab = np.asarray(lab, np.int32)
+        levels.append(oracle.LevelResult(P, lab, np.zeros(1), np.zeros(1, np.int64), 0))
+        o, m = oracle.children(lab, P.shape[0])
+        offs.append(o)
+        mems.append(m)
+    return oracle.Index(levels, offs, mems, P_levels[0].shape[1] if np.ndim(P_levels[0]) == 2 else 1)
+
+
+def test_range_paper_mode_hand_derived():
+    """Algorithm 3 on a hand-built 1-D index: rows 0, 1, 10, 11, 20, 21; level-1
+    prototypes 0.5 {0,1}, 10.5 {10,11}, 20.5 {20,21}; top prototypes 5.5 {c0, c1}, 20.5 {c2}.
+    q = 9, r = 4: top keeps 5.5 (3.5 <= 4), drops 20.5; level 1 keeps 10.5 (1.5), drops 0.5 (8.5)
+    -> rows 10, 11 (d^2 1, 4).  q = 5.8, r = 4.3: top keeps 5.5; level 1 drops 0.5 (5.3) and
+    10.5 (4.7) -> nothing, although row 10 lies at 4.2 (the paper's rule is lossy); cover mode
+    (cover(10.5) = 0.5: 4.7 <= 4.8) finds it."""
+    X = np.array([[0.0], [1.0], [10.0], [11.0], [20.0], [21.0]])
+    idx = _hand_index([np.array([[0.5], [10.5], [20.5]]), np.array([[5.5], [20.5]])],
+                      [np.array([0, 0, 1, 1, 2, 2]), np.array([0, 0, 1])])
+    ids, d2 = oracle.range_query(idx.P, idx.offsets, idx.members, X, np.array([9.0]), 4.0)
+    np.testing.assert_array_equal(ids, [2, 3])
+    np.testing.assert_array_equal(d2, [1.0, 4.0])
+    ids, _ = oracle.range_query(idx.P, idx.offsets, idx.members, X, np.array([5.8]), 4.3)
+    assert ids.size == 0
+    cov = oracle.cover_radii(idx, X)
+    np.testing.assert_allclose(cov[0], [0.5, 0.5, 0.5])
+    np.testing.assert_allclose(cov[1], [5.5, 0.5])  # 5.5 -> farthest row below it: 0 or 11
+    ids, d2 = oracle.range_query(idx.P, idx.offsets, idx.members, X, np.array([5.8]), 4.3, cover=cov)
+    np.testing.assert_array_equal(ids, [2])
+    np.testing.assert_allclose(d2, [4.2 ** 2])
+
+
+def test_exhaustive_error_hand_derived_and_identity():
+    """The point-search error (SPEC exhaustive_error): on a hand-built 1-D index with
+    rows 0, 3, 4 and level-1 prototypes 0 {row 0} and 10 {rows 3, 4}, points 3 and 4 descend to
+    prototype 0 (3 < 7, 4 < 6) and are answered with row 0: error 2/3.  An identity index (every
+    point its own prototype) is exact search: error 0."""
+    X = np.array([[0.0], [3.0], [4.0]])
+    idx = _hand_index([np.array([[0.0], [10.0]])], [np.array([0, 1, 1])])
+    assert oracle.exhaustive_error(idx, X) == pytest.approx(2.0 / 3.0)
+    Xr = datagen.blobs(21, 300, 4, 5)
+    ident = oracle.build_index(Xr, [np.arange(300), np.arange(300)], 3)
+    assert oracle.exhaustive_error(ident, Xr) == 0.0
