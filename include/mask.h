@@ -222,7 +222,9 @@ int32_t mask_build_grouped(const mask_matrix* data, const mask_grouped_params* p
  * d2_out[...] (squared Euclidean distance, fp32) sorted by (d2, id) (D4); a partition
  * smaller than k_nn is padded with (-1, +inf) (D8).  Output buffers live in the same
  * memory kind as `queries` (device or host).  Non-collective; concurrent calls on one
- * index are allowed.  Errors: MASK_ERR_ARG (k_nn < 1 or > 32, beam < 1 or > 32, dim or
+ * index are allowed.  beam <= 32 keeps the per-level selection in registers (warp bitonic top-b);
+ * 32 < beam <= 256 (dense queries) keeps it in shared memory (merge-path top-b, same order and
+ * result).  Errors: MASK_ERR_ARG (k_nn < 1 or > 32, beam < 1 or > 256, dim or
  * format mismatch), MASK_ERR_CUDA. */
 int32_t mask_query(const mask_index* idx, const mask_matrix* queries, int32_t k_nn,
                    int32_t beam, int64_t* ids_out, float* d2_out, void* stream);

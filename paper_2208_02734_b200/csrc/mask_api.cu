@@ -1734,7 +1734,9 @@ int32_t query_impl(const mask_index* idx, const mask_matrix* queries, int32_t k_
     MASK_REQUIRE(idx != nullptr, MASK_ERR_ARG, "index is NULL");
     check_matrix(queries, "queries");
     MASK_REQUIRE(k_nn >= 1 && k_nn <= 32, MASK_ERR_ARG, "k_nn must be in [1, 32]");
-    MASK_REQUIRE(beam >= 1 && beam <= 32, MASK_ERR_ARG, "beam must be in [1, 32]");
+    MASK_REQUIRE(beam >= 1 && beam <= 256, MASK_ERR_ARG, "beam must be in [1, 256]");
+    MASK_REQUIRE(beam <= 32 || (queries->format == MASK_DENSE_F32 && !routed), MASK_ERR_UNSUPPORTED,
+                 "beam > 32 is supported for dense queries (mask_query)");
     MASK_REQUIRE(queries->dim == idx->dim, MASK_ERR_ARG, "query dim differs from the index dim");
     MASK_REQUIRE(queries->format == idx->format, MASK_ERR_UNSUPPORTED,
                  "query format must match the index format");

@@ -355,6 +355,157 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
   }
 }
 
+// ---------------------------------------------------------------------------------------
+// Wide beams (32 < b <= kMaxWideBeam): the per-level selection keeps its sorted top-b list in
+// shared memory.  A chunk of 32 candidates is filtered against the current b-th key (ballot),
+// sorted with the warp bitonic network, staged in shared memory and merged into the list by
+// merge path (every lane finds the split of its output positions by binary search), keeping the
+// first b: the same (d^2, id) order and the same result as a sort of all candidates (D4).
+constexpr int kMaxWideBeam = 256;
+constexpr int kWideWarps = 2;
+
+struct SmemTopK {
+  float* d;        // [K] sorted ascending by (d, id); first n valid
+  int32_t* id;
+  float* td;       // [K] merge output
+  int32_t* tid;
+  float* cd;       // [32] the staged chunk
+  int32_t* cid;
+  int K, n;
+  __device__ void reset(int k) {
+    K = k;
+    n = 0;
+  }
+  __device__ void offer(float v, int32_t j, int lane) {
+    const float thd = n == K ? d[K - 1] : INFINITY;
+    const int32_t thi = n == K ? id[K - 1] : PAD_ID;
+    const bool acc = j != PAD_ID && key_lt(v, j, thd, thi);
+    const unsigned m32 = __ballot_sync(FULL, acc);
+    if (!m32) return;
+    const int m = __popc(m32);
+    float cv = acc ? v : INFINITY;
+    int32_t cj = acc ? j : PAD_ID;
+    warp_sort32(cv, cj, lane);  // the m accepted keys first, ascending
+    cd[lane] = cv;
+    cid[lane] = cj;
+    __syncwarp();
+    const int out = min(K, n + m);
+    for (int o = lane; o < out; o += 32) {
+      int lo = max(0, o - m), hi = min(o, n);
+      while (lo < hi) {  // i = number of list keys among the first o outputs
+        const int mid = (lo + hi) >> 1;
+        if (key_lt(d[mid], id[mid], cd[o - 1 - mid], cid[o - 1 - mid])) lo = mid + 1;
+        else hi = mid;
+      }
+      const int i = lo, jj = o - lo;
+      const bool from_list = jj >= m || (i < n && key_lt(d[i], id[i], cd[jj], cid[jj]));
+      td[o] = from_list ? d[i] : cd[jj];
+      tid[o] = from_list ? id[i] : cid[jj];
+    }
+    __syncwarp();
+    for (int o = lane; o < out; o += 32) {
+      d[o] = td[o];
+      id[o] = tid[o];
+    }
+    n = out;
+    __syncwarp();
+  }
+};
+
+__global__ void __launch_bounds__(kWideWarps * 32)
+    k_query_dense_wide(QIndex qi, const float* __restrict__ Q, int64_t nq, int knn, int beam,
+                       int64_t* __restrict__ ids_out, float* __restrict__ d2_out) {
+  extern __shared__ __align__(16) float wsm[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int d = qi.dim;
+  const int dpad = (d + 3) & ~3;
+  // per warp: q (dpad floats), two lists + merge buffer of kMaxWideBeam (d, id), chunk of 32
+  const int per_warp = dpad + 6 * kMaxWideBeam + 64;
+  float* base = wsm + (size_t)w * per_warp;
+  float* q = base;
+  SmemTopK cur, nxt;
+  cur.d = base + dpad;
+  cur.id = reinterpret_cast<int32_t*>(cur.d + kMaxWideBeam);
+  nxt.d = reinterpret_cast<float*>(cur.id + kMaxWideBeam);
+  nxt.id = reinterpret_cast<int32_t*>(nxt.d + kMaxWideBeam);
+  cur.td = nxt.td = reinterpret_cast<float*>(nxt.id + kMaxWideBeam);
+  cur.tid = nxt.tid = reinterpret_cast<int32_t*>(cur.td + kMaxWideBeam);
+  cur.cd = nxt.cd = reinterpret_cast<float*>(cur.tid + kMaxWideBeam);
+  cur.cid = nxt.cid = reinterpret_cast<int32_t*>(cur.cd + 32);
+  const int64_t nwarps = (int64_t)gridDim.x * kWideWarps;
+  for (int64_t qid = (int64_t)blockIdx.x * kWideWarps + w; qid < nq; qid += nwarps) {
+    __syncwarp();
+    for (int i = lane; i < d; i += 32) q[i] = Q[qid * d + i];
+    __syncwarp();
+    {  // top level: every prototype with children
+      const QLevel& L = qi.lv[qi.L - 1];
+      cur.reset(beam);
+      for (int64_t j0 = 0; j0 < L.k; j0 += 32) {
+        const int64_t j = j0 + lane;
+        const int32_t cid = (j < L.k && has_children(L, j)) ? (int32_t)j : PAD_ID;
+        cur.offer(coop_dist<1>(q, L.P, d, cid, lane), cid, lane);
+      }
+    }
+    for (int l = qi.L - 2; l >= 0; --l) {  // children of the kept prototypes
+      const QLevel& up = qi.lv[l + 1];
+      const QLevel& L = qi.lv[l];
+      nxt.reset(beam);
+      for (int s = 0; s < cur.n; ++s) {
+        const int32_t p = cur.id[s];
+        const int64_t m0 = up.offsets[p], m1 = up.offsets[p + 1];
+        for (int64_t m = m0; m < m1; m += 32) {
+          const int64_t mm = m + lane;
+          int32_t cid = PAD_ID;
+          if (mm < m1) {
+            const int32_t j = up.members[mm];
+            if (has_children(L, j)) cid = j;
+          }
+          nxt.offer(coop_dist<1>(q, L.P, d, cid, lane), cid, lane);
+        }
+      }
+      // the next level's selection becomes the current one (swap the list storage)
+      float* td_ = cur.d;
+      int32_t* ti_ = cur.id;
+      cur.d = nxt.d;
+      cur.id = nxt.id;
+      cur.n = nxt.n;
+      nxt.d = td_;
+      nxt.id = ti_;
+      __syncwarp();
+    }
+    // data layer: rows of the reached partitions
+    const QLevel& L1 = qi.lv[0];
+    WarpTopK top;
+    top.reset(knn);
+    const int G = (qi.Xp && (d & 3) == 0) ? d >> 2 : 0;
+    for (int s = 0; s < cur.n; ++s) {
+      const int32_t p = cur.id[s];
+      const int64_t m0 = L1.offsets[p], m1 = L1.offsets[p + 1];
+      switch (G) {
+        case 1: leaf_scan_coalesced<1>(qi, q, m0, m1, L1.members, top, lane); continue;
+        case 2: leaf_scan_coalesced<2>(qi, q, m0, m1, L1.members, top, lane); continue;
+        case 4: leaf_scan_coalesced<4>(qi, q, m0, m1, L1.members, top, lane); continue;
+        case 8: leaf_scan_coalesced<8>(qi, q, m0, m1, L1.members, top, lane); continue;
+        case 16: leaf_scan_coalesced<16>(qi, q, m0, m1, L1.members, top, lane); continue;
+        case 32: leaf_scan_coalesced<32>(qi, q, m0, m1, L1.members, top, lane); continue;
+        default: break;
+      }
+      for (int64_t m = m0; m < m1; m += 32) {
+        const int64_t mm = m + lane;
+        const int32_t cid = mm < m1 ? (int32_t)L1.members[mm] : PAD_ID;
+        const float cd = qi.Xp ? coop_dist<1>(q, qi.Xp, d, mm < m1 ? (int32_t)mm : PAD_ID, lane)
+                               : coop_dist<1>(q, qi.X, d, cid, lane);
+        top.offer(cd, cid, lane);
+      }
+    }
+    if (lane < knn) {
+      const bool pad = top.id == PAD_ID;
+      ids_out[qid * knn + lane] = pad ? -1 : qi.id_base + (int64_t)top.id;
+      d2_out[qid * knn + lane] = pad ? INFINITY : top.d;
+    }
+  }
+}
+
 __global__ void k_gather_partition(const float* __restrict__ X, int d, const int32_t* __restrict__ members, int64_t n,
                                    float* __restrict__ Xp) {
   const int64_t total = n * d;
@@ -382,6 +533,19 @@ void launch_query_dense(const QIndex& qi, const float* Q, int64_t nq, int knn, i
   const int64_t blocks = (nq + kWarpsPerBlock - 1) / kWarpsPerBlock;
   const unsigned grid = (unsigned)(blocks < (int64_t)num_sms() * 16 ? blocks : (int64_t)num_sms() * 16);
   const int lo = leaf_only ? 1 : 0;
+  if (beam > 32) {  // wide beams: shared-memory selection lists
+    MASK_REQUIRE(!leaf_only && !qi.routed && beam <= kMaxWideBeam, MASK_ERR_UNSUPPORTED,
+                 "query: beam > 32 is supported for plain dense queries up to 256");
+    const size_t wsmem = (size_t)kWideWarps * (dpad + 6 * kMaxWideBeam + 64) * sizeof(float);
+    MASK_REQUIRE(wsmem <= 200 * 1024, MASK_ERR_UNSUPPORTED, "query: dim too large for wide beams");
+    if (wsmem > 48 * 1024)
+      MASK_CUDA(cudaFuncSetAttribute(k_query_dense_wide, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsmem));
+    const int64_t wblocks = (nq + kWideWarps - 1) / kWideWarps;
+    const unsigned wgrid = (unsigned)(wblocks < (int64_t)num_sms() * 32 ? wblocks : (int64_t)num_sms() * 32);
+    k_query_dense_wide<<<wgrid, kWideWarps * 32, wsmem, st>>>(qi, Q, nq, knn, beam, ids, d2);
+    MASK_LAUNCH_CHECK();
+    return;
+  }
   if (coop) {
     if (smem > 48 * 1024)
       MASK_CUDA(cudaFuncSetAttribute(k_query_dense<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

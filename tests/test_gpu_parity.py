@@ -496,3 +496,21 @@ def test_near_ties_are_decided_exactly(d):
     got = lab.cpu().numpy()
     bad = np.nonzero(got != ref)[0]
     assert bad.size == 0, f"{bad.size} labels differ from the oracle (rows {bad[:5].tolist()})"
+
+
+@pytest.mark.parametrize("cid,div,knn,beam", [(3, 256, 10, 40), (3, 256, 32, 256), (2, 64, 10, 100), (5, 2048, 5, 64)])
+def test_wide_beam_queries_match_the_oracle(cid, div, knn, beam):
+    """Beams above 32 (shared-memory merge-path selection): the same result lists as the
+    oracle's descent with the same beam, and recall never below the 32-wide beam's."""
+    cfg = datagen.CONFIGS[cid].scaled(div)
+    X = datagen.data(cfg)
+    idx = mk.build(t(X), cfg.levels, 6, datagen.all_init_indices(cfg))
+    Q = datagen.queries(cfg, count=150)
+    _query_parity(idx, X, Q, cfg.levels, knn=knn, beam=beam)
+    eids, _, _ = oracle.knn_exact(X, Q, knn)
+    wide, _ = idx.query(t(Q), knn=knn, beam=beam)
+    narrow, _ = idx.query(t(Q), knn=knn, beam=32)
+    assert oracle.recall(wide.cpu().numpy(), eids) >= oracle.recall(narrow.cpu().numpy(), eids)
+    with pytest.raises(mk.MaskError):
+        idx.query(t(Q), knn=knn, beam=257)
+    idx.free()
