@@ -295,6 +295,8 @@ def _cpu_model():
 
 # --------------------------------------------------------------------------- main arm
 def main():
+    # NCCL prints a version banner on stdout unless told otherwise: the contract is one JSON line
+    os.environ.setdefault("NCCL_DEBUG", "WARN")
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

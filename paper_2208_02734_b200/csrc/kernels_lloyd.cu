@@ -737,13 +737,16 @@ __global__ void k_update_dense(const float* __restrict__ X, int64_t n, int d,
 // reds instead of m*d/4 (atomics were the limit of the element-parallel kernel).
 // Acc = double (the FP64 sums of a level that keeps FP64 prototypes): the run is accumulated
 // in FP64 and flushed with four scalar FP64 reds.
+// NB batches of U rows per lane group and warp: FP64 sums flush with four scalar atomics, so
+// their warps cover 4x longer stretches of the sorted order (fewer run flushes per cluster).
 template <int L, class Acc = float>
 __global__ void __launch_bounds__(256) k_update_runs(const float4* __restrict__ X4, const int32_t* __restrict__ perm,
                                                       int64_t n, int d4, const int32_t* __restrict__ labels,
                                                       Acc* __restrict__ S, int32_t* __restrict__ counts,
                                                       const int* __restrict__ active) {
   if (active && !*active) return;  // level converged: this pass is skipped on the device
-  constexpr int R = 32 / L, U = 4, CH = R * U * 4;  // 4 batches of U independent rows per lane group
+  constexpr int NB = sizeof(Acc) == 8 ? 16 : 4;
+  constexpr int R = 32 / L, U = 4, CH = R * U * NB;  // NB batches of U independent rows per lane group
   const int lane = threadIdx.x & 31, slot = lane / L, c4 = lane % L;
   const int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int64_t p0 = w * CH;
@@ -824,7 +827,7 @@ void launch_update_dense64(const float* X, int64_t n, int d, const int32_t* labe
   if (perm && d % 4 == 0 && d <= 128 && ((uintptr_t)X % 16) == 0) {
     const int d4 = d / 4;
     const int L = d4 <= 1 ? 1 : d4 <= 2 ? 2 : d4 <= 4 ? 4 : d4 <= 8 ? 8 : d4 <= 16 ? 16 : 32;
-    const int64_t ch = (32 / L) * 16;
+    const int64_t ch = (32 / L) * 64;  // positions per warp (k_update_runs CH with NB = 16)
     const int64_t warps = (n + ch - 1) / ch;
     const unsigned grid = (unsigned)((warps + 7) / 8);
     const float4* X4 = reinterpret_cast<const float4*>(X);
