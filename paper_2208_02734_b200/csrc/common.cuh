@@ -148,7 +148,7 @@ void launch_fixup_device(const float* X, int d, const float* P, int64_t k, const
                          const int32_t* flag_count, int64_t cap, unsigned long long* keys_ws, int32_t* labels,
                          float* best, cudaStream_t st, const int* active = nullptr, const int2* flag_pair = nullptr,
                          int32_t* rescan_rows = nullptr, int32_t* rescan_count = nullptr,
-                         const double* P64 = nullptr);
+                         const double* P64 = nullptr, double* P64T = nullptr /* k*d workspace */);
 // FP64-prototype levels (D15): FP64 sums, FP64 finalize (P64 and its fp32 rounding P)
 void launch_update_dense64(const float* X, int64_t n, int d, const int32_t* labels, double* S, int32_t* counts,
                            cudaStream_t st, const int* active, const int32_t* perm);

@@ -497,26 +497,39 @@ __global__ void k_fix_pairs(const float* __restrict__ X, int d, const T* __restr
   }
 }
 
+// P64T[i * k + j] = P64[j * d + i] (dimension-major copy for the re-scan's coalesced reads)
+__global__ void k_transpose64(const double* __restrict__ P, int64_t k, int d, double* __restrict__ PT,
+                              const int* __restrict__ active) {
+  if (active && !*active) return;
+  const int64_t total = k * (int64_t)d;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / k, j = e - i * k;
+    PT[e] = P[j * d + i];
+  }
+}
+
 // Exact full re-check of one flagged row per block against the FP64 prototypes: the oracle's
-// distance arithmetic for every prototype, (d^2, j) minimum over the block.
-__global__ void __launch_bounds__(256) k_rescan64(const float* __restrict__ X, int d, const double* __restrict__ P,
+// distance arithmetic (sequential in the dimension) for every prototype, thread per prototype
+// reading the dimension-major copy (coalesced), (d^2, j) minimum over the block.
+__global__ void __launch_bounds__(256) k_rescan64(const float* __restrict__ X, int d, const double* __restrict__ PT,
                                                   int64_t k, const int32_t* __restrict__ rows,
                                                   const int32_t* __restrict__ count, int32_t* __restrict__ labels,
                                                   float* __restrict__ best, const int* __restrict__ active) {
   if (active && !*active) return;
   __shared__ double sd[8];
   __shared__ int64_t sj[8];
+  extern __shared__ double sx[];  // the row, FP64
   const int64_t nf = *count;
   for (int64_t f = blockIdx.x; f < nf; f += gridDim.x) {
     const int32_t row = rows[f];
-    const float* x = X + (int64_t)row * d;
+    for (int i = threadIdx.x; i < d; i += blockDim.x) sx[i] = (double)X[(int64_t)row * d + i];
+    __syncthreads();
     double bd = INFINITY;
     int64_t bj = INT64_MAX;
     for (int64_t j = threadIdx.x; j < k; j += blockDim.x) {  // j increasing per thread: keeps lowest
-      const double* c = P + j * d;
       double s = 0.0;
       for (int i = 0; i < d; ++i) {
-        const double t = (double)x[i] - c[i];
+        const double t = sx[i] - PT[(int64_t)i * k + j];
         s = __dadd_rn(s, __dmul_rn(t, t));
       }
       if (s < bd) {
@@ -555,7 +568,7 @@ __global__ void __launch_bounds__(256) k_rescan64(const float* __restrict__ X, i
 void launch_fixup_device(const float* X, int d, const float* P, int64_t k, const int32_t* flag_rows,
                          const int32_t* flag_count, int64_t cap, unsigned long long* keys_ws, int32_t* labels,
                          float* best, cudaStream_t st, const int* active, const int2* flag_pair,
-                         int32_t* rescan_rows, int32_t* rescan_count, const double* P64) {
+                         int32_t* rescan_rows, int32_t* rescan_count, const double* P64, double* P64T) {
   if (!flag_pair) {
     launch_blocked(X, d, P, k, flag_rows, flag_count, cap, keys_ws, labels, best, st, active);
     return;
@@ -569,7 +582,11 @@ void launch_fixup_device(const float* X, int d, const float* P, int64_t k, const
                                                       rescan_rows, rescan_count, active);
   MASK_LAUNCH_CHECK();
   if (P64) {  // the level's FP64 prototypes: the re-scan reads them (oracle arithmetic)
-    k_rescan64<<<num_sms() * 4, 256, 0, st>>>(X, d, P64, k, rescan_rows, rescan_count, labels, best, active);
+    MASK_REQUIRE(P64T != nullptr, MASK_ERR_CUDA, "fix-up: no FP64 transpose workspace");
+    k_transpose64<<<grid_for(k * d, 256), 256, 0, st>>>(P64, k, d, P64T, active);
+    MASK_LAUNCH_CHECK();
+    k_rescan64<<<num_sms() * 4, 256, (size_t)d * sizeof(double), st>>>(X, d, P64T, k, rescan_rows, rescan_count,
+                                                                        labels, best, active);
     MASK_LAUNCH_CHECK();
     return;
   }

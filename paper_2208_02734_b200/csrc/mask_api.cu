@@ -439,6 +439,7 @@ struct LloydWS {
   DevBuf<int2> flag_pair;                     // K1 -> K4: the two candidates of a flagged row
   DevBuf<double> P64;  // FP64 prototypes of a dense per-pass level (D15); nullptr otherwise
   DevBuf<double> S64;  // their FP64 sums (+ the packed counts / J / changed tail for N1)
+  DevBuf<double> P64T; // K4 re-scan: dimension-major copy of P64
   DevBuf<int32_t> rescan_rows, rescan_count;  // K4: flagged rows that need the full re-check
   DevBuf<unsigned long long> fix_keys;
   DevBuf<int16_t> colslot;  // K3 chunk-major: hot slot of each column (-1 = read from L2)
@@ -560,7 +561,7 @@ void assign_pass(const Input& in, const float* P, int64_t k, int flags, int32_t*
   if (!(flags & MASK_NO_FIXUP)) {
     if (ev) ev->mark(MASK_T_FIXUP, st);
     launch_fixup_device(in.X, d, P, k, ws.flag_rows.p, ws.flag_count.p, n, ws.fix_keys.p, labels_out, best, st,
-                        active, ws.flag_pair.p, ws.rescan_rows.p, ws.rescan_count.p, ws.P64.p);
+                        active, ws.flag_pair.p, ws.rescan_rows.p, ws.rescan_count.p, ws.P64.p, ws.P64T.p);
     if (ev) ev->mark(MASK_T_FIXUP, st);
   }
 }
@@ -693,6 +694,7 @@ void run_level(const Input& in, int64_t k, const int64_t* init_idx_host, const m
   const bool p64 = in.format == MASK_DENSE_F32 && !fused_level;
   if (p64) {
     ws.P64.alloc((size_t)k * d);
+    ws.P64T.alloc((size_t)k * d);
     ws.S64.alloc((size_t)k * d + (size_t)k + 2);
   } else {
     ws.S.alloc((size_t)k * d + (comm ? 2 * (size_t)k + 8 : 0));  // + the packed tail (N1)
