@@ -940,9 +940,9 @@ __global__ void __launch_bounds__(256 + 128 * EPI_WG, 1)
         const float thr = err_coef * (xx + __ldg(cn2 + gi)) + ldexpf(fmaxf(fabsf(g2), fabsf(g1)), -14);
         flag = (g2 - g1) <= thr;
         // a flagged row whose every other score (lower bound g3: keyed chunks' third-smallest,
-        // skipped chunks' minima) lies beyond twice the window has exactly two candidates:
+        // skipped chunks' minima) lies beyond the window (x 1.25: the window already holds twice the score error) has exactly two candidates:
         // K4 decides between them exactly, no re-scan
-        pair = flag && gi2 >= 0 && gi2 < k && gi2 != gi && (g3 - g1) > 2.f * thr;
+        pair = flag && gi2 >= 0 && gi2 < k && gi2 != gi && (g3 - g1) > 1.25f * thr;
       }
       const unsigned msk = __ballot_sync(0xffffffffu, flag);
       if (msk) {

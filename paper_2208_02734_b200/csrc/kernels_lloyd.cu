@@ -417,6 +417,114 @@ __global__ void __launch_bounds__(256) k_rb_argmin(const float* __restrict__ X, 
   }
 }
 
+// The exact re-check against FP64 prototypes, register-blocked like k_rb_argmin: 32 flagged rows
+// (FP64 in shared memory) x 128-prototype FP64 tiles, 4 rows x 4 prototypes per thread, the
+// oracle's arithmetic (FP64 difference, separately rounded square and sum, dimension order),
+// double2 shared-memory reads (row stride d2p double2, odd: conflict-free), merged across the
+// prototype splits with the exact 64-bit key (FP64 d^2 with the low jbits = j).
+__global__ void __launch_bounds__(256) k_rb_argmin64(const float* __restrict__ X, int d, int d2p,
+                                                     const double* __restrict__ P, int64_t k,
+                                                     const int32_t* __restrict__ rows,
+                                                     const int32_t* __restrict__ count_dev, int64_t cap, int nsm,
+                                                     unsigned long long* __restrict__ keys,
+                                                     const int* __restrict__ active, int jbits) {
+  if (active && !*active) return;
+  extern __shared__ double2 rsm64[];
+  const int64_t nf = count_dev ? min64(*count_dev, cap) : cap;
+  if (nf <= 0) return;
+  double2* xs = rsm64;               // [RB_R][d2p]
+  double2* cs = rsm64 + RB_R * d2p;  // [RB_P][d2p]
+  const int t = threadIdx.x;
+  const int rg = t & 7, pg = t >> 3;
+  const int d2 = (d + 1) / 2;
+  const int64_t row_blocks = (nf + RB_R - 1) / RB_R;
+  const int64_t ntile = (k + RB_P - 1) / RB_P;
+  int64_t splits = ((int64_t)nsm + row_blocks - 1) / row_blocks;
+  splits = splits < 1 ? 1 : (splits > ntile ? ntile : splits);
+  const int64_t tps = (ntile + splits - 1) / splits;
+  splits = (ntile + tps - 1) / tps;
+  const unsigned long long jm = (1ull << jbits) - 1ull;
+  for (int64_t w = blockIdx.x; w < row_blocks * splits; w += gridDim.x) {
+    const int64_t f0 = (w / splits) * RB_R;
+    const int64_t t0 = (w % splits) * tps;
+    const int64_t t1 = min64(ntile, t0 + tps);
+    __syncthreads();
+    for (int e = t; e < RB_R * d2; e += 256) {
+      const int r = e / d2, c2 = e - r * d2;
+      const int64_t f = f0 + r;
+      const int64_t row = f < nf ? (rows ? (int64_t)rows[f] : f) : -1;
+      double2 v = make_double2(0.0, 0.0);
+      if (row >= 0) {
+        const float* src = X + row * d + 2 * c2;
+        v.x = (double)src[0];
+        if (2 * c2 + 1 < d) v.y = (double)src[1];
+      }
+      xs[r * d2p + c2] = v;
+    }
+    double bv[4];
+    int64_t bj[4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      bv[a] = INFINITY;
+      bj[a] = INT64_MAX;
+    }
+    for (int64_t tile = t0; tile < t1; ++tile) {
+      const int64_t j0 = tile * RB_P;
+      __syncthreads();
+      for (int e = t; e < RB_P * d2; e += 256) {
+        const int pr = e / d2, c2 = e - pr * d2;
+        double2 v = make_double2(0.0, 0.0);
+        if (j0 + pr < k) {
+          const double* src = P + (j0 + pr) * d + 2 * c2;
+          v.x = src[0];
+          if (2 * c2 + 1 < d) v.y = src[1];
+        }
+        cs[pr * d2p + c2] = v;
+      }
+      __syncthreads();
+      double acc[4][4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+      for (int c2 = 0; c2 < d2; ++c2) {
+        double2 xv[4], cv[4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) xv[a] = xs[(a * 8 + rg) * d2p + c2];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) cv[b] = cs[(b * 32 + pg) * d2p + c2];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) {  // dimensions in increasing order (zero padding adds 0)
+            double df = xv[a].x - cv[b].x;
+            acc[a][b] = __dadd_rn(acc[a][b], __dmul_rn(df, df));
+            df = xv[a].y - cv[b].y;
+            acc[a][b] = __dadd_rn(acc[a][b], __dmul_rn(df, df));
+          }
+      }
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const int64_t j = j0 + b * 32 + pg;
+        if (j < k) {
+#pragma unroll
+          for (int a = 0; a < 4; ++a)
+            if (acc[a][b] < bv[a]) {
+              bv[a] = acc[a][b];
+              bj[a] = j;
+            }
+        }
+      }
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      const int64_t f = f0 + a * 8 + rg;
+      if (f < nf && bj[a] != INT64_MAX)
+        atomicMin(keys + f, ((unsigned long long)__double_as_longlong(bv[a]) & ~jm) | (unsigned long long)bj[a]);
+    }
+  }
+}
+
 static void launch_blocked(const float* X, int d, const float* P, int64_t k, const int32_t* rows,
                            const int32_t* count_dev, int64_t cap, unsigned long long* keys_ws, int32_t* labels,
                            float* best, cudaStream_t st, const int* active, bool exact = false) {
@@ -581,15 +689,6 @@ void launch_fixup_device(const float* X, int d, const float* P, int64_t k, const
     k_fix_pairs<float><<<num_sms() * 4, 256, 0, st>>>(X, d, P, flag_rows, flag_pair, flag_count, cap, labels, best,
                                                       rescan_rows, rescan_count, active);
   MASK_LAUNCH_CHECK();
-  if (P64) {  // the level's FP64 prototypes: the re-scan reads them (oracle arithmetic)
-    MASK_REQUIRE(P64T != nullptr, MASK_ERR_CUDA, "fix-up: no FP64 transpose workspace");
-    k_transpose64<<<grid_for(k * d, 256), 256, 0, st>>>(P64, k, d, P64T, active);
-    MASK_LAUNCH_CHECK();
-    k_rescan64<<<num_sms() * 4, 256, (size_t)d * sizeof(double), st>>>(X, d, P64T, k, rescan_rows, rescan_count,
-                                                                        labels, best, active);
-    MASK_LAUNCH_CHECK();
-    return;
-  }
   static const bool dbg = getenv("MASK_DEBUG_FIXUP") != nullptr;
   if (dbg) {  // development: flagged / re-scanned counts and the first pairs
     int32_t hc[2] = {0, 0};
@@ -603,6 +702,40 @@ void launch_fixup_device(const float* X, int d, const float* P, int64_t k, const
     fprintf(stderr, "[fixup] flagged %d rescan %d |", hc[0], hc[1]);
     for (int i = 0; i < 8 && i < hc[0]; ++i) fprintf(stderr, " %d:(%d,%d)", hr[i], hp[i].x, hp[i].y);
     fprintf(stderr, "\n");
+  }
+  if (P64) {  // the level's FP64 prototypes: the re-scan reads them (oracle arithmetic)
+    const int d2 = (d + 1) / 2;
+    const int d2p = d2 | 1;
+    const size_t smem = (size_t)(RB_R + RB_P) * d2p * sizeof(double2);
+    if (smem <= 200 * 1024) {  // register-blocked: 32 rows share every staged prototype tile
+      int jbits = 1;
+      while ((int64_t(1) << jbits) < k) ++jbits;
+      static int attr = 0;
+      if (smem > 48 * 1024 && !attr) {
+        MASK_CUDA(cudaFuncSetAttribute(k_rb_argmin64, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        attr = 1;
+      }
+      int occ = 1;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_rb_argmin64, 256, smem) != cudaSuccess) occ = 1;
+      (void)cudaGetLastError();
+      const int grid = num_sms() * std::max(1, std::min(occ, 8));
+      k_keys_init<<<num_sms() * 2, 256, 0, st>>>(rescan_count, cap, keys_ws, active);
+      MASK_LAUNCH_CHECK();
+      k_rb_argmin64<<<grid, 256, smem, st>>>(X, d, d2p, P64, k, rescan_rows, rescan_count, cap, grid, keys_ws, active,
+                                             jbits);
+      MASK_LAUNCH_CHECK();
+      k_keys_write<<<num_sms() * 2, 256, 0, st>>>(rescan_rows, rescan_count, cap, keys_ws, labels, best, active,
+                                                  jbits);
+      MASK_LAUNCH_CHECK();
+      return;
+    }
+    MASK_REQUIRE(P64T != nullptr, MASK_ERR_CUDA, "fix-up: no FP64 transpose workspace");
+    k_transpose64<<<grid_for(k * d, 256), 256, 0, st>>>(P64, k, d, P64T, active);
+    MASK_LAUNCH_CHECK();
+    k_rescan64<<<num_sms() * 4, 256, (size_t)d * sizeof(double), st>>>(X, d, P64T, k, rescan_rows, rescan_count,
+                                                                        labels, best, active);
+    MASK_LAUNCH_CHECK();
+    return;
   }
   launch_blocked(X, d, P, k, rescan_rows, rescan_count, cap, keys_ws, labels, best, st, active, /*exact=*/true);
 }
