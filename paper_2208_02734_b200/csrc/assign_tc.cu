@@ -1414,10 +1414,22 @@ void launch_assign_tc(const float* X, int64_t n, int d, const float* P, const fl
     tc::launch_persist<16, MASK_TC_P_BN, MASK_TC_P_STAGES, MASK_TC_P_NACC, MASK_TC_P_EPI>(
         X, n, d, kc, kr, P, Pb, Ps, cn2, k, xn2, labels, best, flag_rows, flag_count, coef, st, active, perm,
         prev_lab, lab2, flag_pair);
-  else if (d <= 16)
-    tc::launch_persist<24, MASK_TC_P_BN, MASK_TC_P_STAGES, MASK_TC_P_NACC, MASK_TC_P_EPI>(
-        X, n, d, kc, kr, P, Pb, Ps, cn2, k, xn2, labels, best, flag_rows, flag_count, coef, st, active, perm,
-        prev_lab, lab2, flag_pair);
+  else if (d <= 16) {
+    static const int var = [] {  // development A/B of the d = 16 tiling (MASK_TC_D16=1/2)
+      const char* e = getenv("MASK_TC_D16");
+      return e ? atoi(e) : 0;
+    }();
+    if (var == 1)  // three accumulators of 128 columns
+      tc::launch_persist<24, 128, 4, 3, 2>(X, n, d, kc, kr, P, Pb, Ps, cn2, k, xn2, labels, best, flag_rows,
+                                           flag_count, coef, st, active, perm, prev_lab, lab2, flag_pair);
+    else if (var == 2)  // three accumulators of 128 columns, four epilogue warpgroups of 32 columns
+      tc::launch_persist<24, 128, 4, 3, 4>(X, n, d, kc, kr, P, Pb, Ps, cn2, k, xn2, labels, best, flag_rows,
+                                           flag_count, coef, st, active, perm, prev_lab, lab2, flag_pair);
+    else
+      tc::launch_persist<24, MASK_TC_P_BN, MASK_TC_P_STAGES, MASK_TC_P_NACC, MASK_TC_P_EPI>(
+          X, n, d, kc, kr, P, Pb, Ps, cn2, k, xn2, labels, best, flag_rows, flag_count, coef, st, active, perm,
+          prev_lab, lab2, flag_pair);
+  }
   else if (d <= 24)
     tc::launch_persist<32, MASK_TC_P_BN, MASK_TC_P_STAGES, MASK_TC_P_NACC, MASK_TC_P_EPI>(
         X, n, d, kc, kr, P, Pb, Ps, cn2, k, xn2, labels, best, flag_rows, flag_count, coef, st, active, perm,
