@@ -161,6 +161,23 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
       : "memory");
 }
 
+// The same load with an L2 cache policy (createpolicy): the prototype operand B is re-read by
+// every row block of every CTA, so it is marked evict_last against the streaming rows.
+__device__ __forceinline__ void tma_load_2d_hint(void* dst, const CUtensorMap* map, uint64_t* bar, int x, int y,
+                                                 uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%3, "
+      "%4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y), "l"(policy)
+      : "memory");
+}
+
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
@@ -782,6 +799,7 @@ __global__ void __launch_bounds__(256 + 128 * EPI_WG, 1)
       int stage = 0;
       uint32_t phase = 0;
       int64_t gp = 0;
+      const uint64_t pol_b = l2_policy_evict_last();
       for (int64_t rb = blockIdx.x; rb < nblocks; rb += gridDim.x) {
         for (int t = 0; t < ntiles; ++t, ++gp) {
           for (int c = 0; c < C::NKC; ++c) {
@@ -792,8 +810,8 @@ __global__ void __launch_bounds__(256 + 128 * EPI_WG, 1)
               mbar_arrive(&full[stage]);
             } else {
               mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
-              tma_load_2d(dst, &tmBb, &full[stage], c * C::CW, t * BN);
-              tma_load_2d(dst + C::B_CHUNK, &tmBs, &full[stage], c * C::CW, t * BN);
+              tma_load_2d_hint(dst, &tmBb, &full[stage], c * C::CW, t * BN, pol_b);
+              tma_load_2d_hint(dst + C::B_CHUNK, &tmBs, &full[stage], c * C::CW, t * BN, pol_b);
             }
             if (++stage == STAGES) {
               stage = 0;
