@@ -172,6 +172,35 @@ __device__ __forceinline__ void tma_load_2d_hint(void* dst, const CUtensorMap* m
       : "memory");
 }
 
+// Multicast of one B half to both CTAs of a 2-CTA cluster (same smem offsets, complete_tx on the
+// mbarrier at the same offset in each destination CTA).
+__device__ __forceinline__ void tma_load_2d_mc(void* dst, const CUtensorMap* map, uint64_t* bar, int x, int y,
+                                               uint16_t mask, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.multicast::cluster"
+      ".L2::cache_hint [%0], [%1, {%3, %4}], [%2], %5, %6;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y), "h"(mask), "l"(policy)
+      : "memory");
+}
+
+__device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
 __device__ __forceinline__ uint64_t l2_policy_evict_last() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
@@ -721,7 +750,9 @@ struct PCfg {
   static_assert(SMEM <= 232448, "shared memory budget");
 };
 
-template <int KA, int BN, int STAGES, int NACC, int EPI_WG, bool FOLD, int ABUF>
+// MC = 2: the CTAs of a 2-CTA cluster walk the same prototype tiles in lockstep and each loads
+// one half of every B stage (big / small part) multicast to both: half the L2 reads of B.
+template <int KA, int BN, int STAGES, int NACC, int EPI_WG, bool FOLD, int ABUF, int MC = 1>
 __global__ void __launch_bounds__(256 + 128 * EPI_WG, 1)
     k_assign_tc_persist(const __grid_constant__ CUtensorMap tmBb, const __grid_constant__ CUtensorMap tmBs,
                         const float* __restrict__ X, const float* __restrict__ P, const float* __restrict__ cn2,
@@ -762,13 +793,18 @@ __global__ void __launch_bounds__(256 + 128 * EPI_WG, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ntiles = (int)((k + BN - 1) / BN);
   const int64_t nblocks = (n + BM - 1) / BM;
+  // every CTA of a cluster runs the same number of block iterations (a CTA past the last block
+  // processes a masked dummy block) so the multicast B stream stays in lockstep
+  const int64_t base_cta = (int64_t)(blockIdx.x / MC) * MC;
+  const int64_t iters = nblocks > base_cta ? (nblocks - base_cta + gridDim.x - 1) / gridDim.x : 0;
+  const uint32_t crank = MC > 1 ? cluster_rank() : 0;
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmBb);
     prefetch_tmap(&tmBs);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], MC);  // every CTA's MMA commit frees the stage in both CTAs
     }
     for (int a = 0; a < NACC; ++a) {
       mbar_init(&tfull[a], 1);
@@ -789,7 +825,8 @@ __global__ void __launch_bounds__(256 + 128 * EPI_WG, 1)
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tc_fence_before();
-  __syncthreads();
+  if (MC > 1) cluster_sync_all();  // the partner's barriers are initialised before any multicast
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -800,7 +837,7 @@ __global__ void __launch_bounds__(256 + 128 * EPI_WG, 1)
       uint32_t phase = 0;
       int64_t gp = 0;
       const uint64_t pol_b = l2_policy_evict_last();
-      for (int64_t rb = blockIdx.x; rb < nblocks; rb += gridDim.x) {
+      for (int64_t it = 0; it < iters; ++it) {
         for (int t = 0; t < ntiles; ++t, ++gp) {
           for (int c = 0; c < C::NKC; ++c) {
             mbar_wait_spin(&empty[stage], phase ^ 1);
@@ -808,6 +845,10 @@ __global__ void __launch_bounds__(256 + 128 * EPI_WG, 1)
             uint8_t* dst = Bst + stage * C::STAGE_BYTES;
             if (dbg & 4) {  // ablation: no B traffic
               mbar_arrive(&full[stage]);
+            } else if (MC > 1) {  // this CTA's half (big or small part) to both CTAs
+              mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
+              if (crank == 0) tma_load_2d_mc(dst, &tmBb, &full[stage], c * C::CW, t * BN, 0x3, pol_b);
+              else tma_load_2d_mc(dst + C::B_CHUNK, &tmBs, &full[stage], c * C::CW, t * BN, 0x3, pol_b);
             } else {
               mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
               tma_load_2d_hint(dst, &tmBb, &full[stage], c * C::CW, t * BN, pol_b);
@@ -830,7 +871,7 @@ __global__ void __launch_bounds__(256 + 128 * EPI_WG, 1)
     const int par = warp == 1 ? 0 : 1;
     int g0 = 0;       // first global tile of the block
     int i = 0;       // block iteration of this CTA
-    for (int64_t rb = blockIdx.x; rb < nblocks; rb += gridDim.x, ++i, g0 += ntiles) {
+    for (int64_t it = 0; it < iters; ++it, ++i, g0 += ntiles) {
       const int first = (int)((g0 & 1) == par ? 0 : 1);  // this issuer's first tile of the block
       const int ab = i % ABUF;
       // every block's afull phase is consumed, also by an issuer without tiles in it (k <= BN):
@@ -874,7 +915,8 @@ __global__ void __launch_bounds__(256 + 128 * EPI_WG, 1)
                 mma_tf32_ts(d_tmem, a_big + s8 * 8, dbb, C::IDESC, 1u);
               }
             }
-            mma_commit(&empty[stage]);
+            if (MC > 1) mma_commit_mc(&empty[stage], 0x3);
+            else mma_commit(&empty[stage]);
             if (c == C::NKC - 1) {
               mma_commit(&tfull[acc]);
               // this issuer's MMAs on the block's A are done (aempty counts one arrive per issuer
@@ -975,7 +1017,8 @@ __global__ void __launch_bounds__(256 + 128 * EPI_WG, 1)
       }
     };
     int i = 0;
-    for (int64_t rb = blockIdx.x; rb < nblocks; rb += gridDim.x, ++i) {
+    for (int64_t it = 0; it < iters; ++it, ++i) {
+      const int64_t rb = blockIdx.x + it * gridDim.x;  // (>= nblocks: a masked dummy block)
       const int ab = i % ABUF;  // TMEM A buffer
       const int ib = i & 1;     // block info slot
       mbar_wait_sleep(&aempty[ab], ((i / ABUF) & 1) ^ 1);
@@ -1063,7 +1106,7 @@ __global__ void __launch_bounds__(256 + 128 * EPI_WG, 1)
     int g = 0;
     int i = 0;
     unsigned long long st_seen = 0, st_keyed = 0;
-    for (int64_t rb = blockIdx.x; rb < nblocks; rb += gridDim.x, ++i) {
+    for (int64_t it = 0; it < iters; ++it, ++i) {
       const int ab = i % ABUF, ib = i & 1;
       mbar_wait_spin(&afull[ab], (i / ABUF) & 1);  // block info published with the A block
       const int32_t ubk = s_ub[ib * BM + rloc];
@@ -1219,7 +1262,8 @@ __global__ void __launch_bounds__(256 + 128 * EPI_WG, 1)
     }
   }
   tc_fence_before();
-  __syncthreads();
+  if (MC > 1) cluster_sync_all();  // no CTA leaves while its partner may still signal its barriers
+  else __syncthreads();
   tc_fence_after();
   if (warp == 2) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(C::TMEM_COLS));
@@ -1339,7 +1383,7 @@ void launch_cfg(const float* X, int64_t n, int d, int kc, int64_t k_rows, const 
   if (tc_debug_mode() & 8) dump_trace((int)grid);
 }
 
-template <int KA, int BN, int STAGES, int NACC, int EPI_WG, bool FOLD = true, int ABUF = 2>
+template <int KA, int BN, int STAGES, int NACC, int EPI_WG, bool FOLD = true, int ABUF = 2, int MC = 1>
 void launch_persist(const float* X, int64_t n, int d, int kc, int64_t k_rows, const float* P, const float* Pb,
                     const float* Ps, const float* cn2, int64_t k, const float* xn2, int32_t* labels, float* best,
                     int32_t* flag_rows, int32_t* flag_count, float err_coef, cudaStream_t st, const int* active,
@@ -1352,17 +1396,36 @@ void launch_persist(const float* X, int64_t n, int d, int kc, int64_t k_rows, co
 #else
   const CUtensorMap tBs = make_map(Ps, k_rows, kc, C::CW, BN);
 #endif
-  auto kern = k_assign_tc_persist<KA, BN, STAGES, NACC, EPI_WG, FOLD, ABUF>;
+  auto kern = k_assign_tc_persist<KA, BN, STAGES, NACC, EPI_WG, FOLD, ABUF, MC>;
   static bool attr_set = false;
   if (!attr_set) {
     MASK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    if (MC > 1) MASK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0));
     attr_set = true;
   }
   const int64_t nblocks = (n + BM - 1) / BM;
-  const unsigned grid = (unsigned)(nblocks < num_sms() ? nblocks : num_sms());
-  kern<<<grid, C::NTHREADS, C::SMEM, st>>>(tBb, tBs, X, P, cn2, xn2, n, d, k, labels, best, flag_rows, flag_count,
-                                           err_coef, 0xFFFFFF00u, active, perm, prev_lab, lab2, flag_pair,
-                                           tc_debug_mode());
+  unsigned grid = (unsigned)(nblocks < num_sms() ? nblocks : num_sms());
+  if (MC > 1) {
+    grid = (grid + MC - 1) / MC * MC;  // whole clusters (a CTA without blocks runs masked dummies)
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(C::NTHREADS);
+    cfg.dynamicSmemBytes = C::SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = MC;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    MASK_CUDA(cudaLaunchKernelEx(&cfg, kern, tBb, tBs, X, P, cn2, xn2, n, d, k, labels, best, flag_rows, flag_count,
+                                 err_coef, 0xFFFFFF00u, active, perm, prev_lab, lab2, flag_pair, tc_debug_mode()));
+  } else {
+    kern<<<grid, C::NTHREADS, C::SMEM, st>>>(tBb, tBs, X, P, cn2, xn2, n, d, k, labels, best, flag_rows, flag_count,
+                                             err_coef, 0xFFFFFF00u, active, perm, prev_lab, lab2, flag_pair,
+                                             tc_debug_mode());
+  }
   MASK_LAUNCH_CHECK();
   if (tc_debug_mode() & 8) dump_ptrace();
   if (tc_debug_mode() & 128) {
@@ -1443,6 +1506,14 @@ void launch_assign_tc(const float* X, int64_t n, int d, const float* P, const fl
     else if (var == 2)  // three accumulators of 128 columns, four epilogue warpgroups of 32 columns
       tc::launch_persist<24, 128, 4, 3, 4>(X, n, d, kc, kr, P, Pb, Ps, cn2, k, xn2, labels, best, flag_rows,
                                            flag_count, coef, st, active, perm, prev_lab, lab2, flag_pair);
+    else if (var == 3)  // the default tiling with B multicast over 2-CTA clusters
+      tc::launch_persist<24, MASK_TC_P_BN, MASK_TC_P_STAGES, MASK_TC_P_NACC, MASK_TC_P_EPI, true, 2, 2>(
+          X, n, d, kc, kr, P, Pb, Ps, cn2, k, xn2, labels, best, flag_rows, flag_count, coef, st, active, perm,
+          prev_lab, lab2, flag_pair);
+    else if (var == 4)  // three accumulators + multicast
+      tc::launch_persist<24, 128, 4, 3, 2, true, 2, 2>(X, n, d, kc, kr, P, Pb, Ps, cn2, k, xn2, labels, best,
+                                                       flag_rows, flag_count, coef, st, active, perm, prev_lab, lab2,
+                                                       flag_pair);
     else
       tc::launch_persist<24, MASK_TC_P_BN, MASK_TC_P_STAGES, MASK_TC_P_NACC, MASK_TC_P_EPI>(
           X, n, d, kc, kr, P, Pb, Ps, cn2, k, xn2, labels, best, flag_rows, flag_count, coef, st, active, perm,
@@ -1487,6 +1558,10 @@ void launch_assign_tc(const float* X, int64_t n, int d, const float* P, const fl
         tc::launch_persist<64, 128, 6, 3, 2, false, 1>(X, n, d, kc, kr, P, Pb, Ps, cn2, k, xn2, labels, best,
                                                        flag_rows, flag_count, c2, st, active, perm, prev_lab, lab2,
                                                        flag_pair);
+      else if (var == 3)  // multicast B over 2-CTA clusters
+        tc::launch_persist<64, 128, 6, 3, 2, false, 1, 2>(X, n, d, kc, kr, P, Pb, Ps, cn2, k, xn2, labels, best,
+                                                          flag_rows, flag_count, c2, st, active, perm, prev_lab, lab2,
+                                                          flag_pair);
       else if (var == 2)
         tc::launch_persist<64, 192, 4, 2, 3, false, 1>(X, n, d, kc, kr, P, Pb, Ps, cn2, k, xn2, labels, best,
                                                        flag_rows, flag_count, c2, st, active, perm, prev_lab, lab2,
