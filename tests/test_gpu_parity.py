@@ -381,8 +381,13 @@ def test_partition_ordered_rows_give_identical_queries():
                       what=f"partition-ordered leaf scan beam {beam}")
     a.free()
     b = mk.build(t(X), cfg.levels, 4, inits, flags=mk._lib.MASK_NO_PARTITION_COPY)
-    ids_b, _ = b.query(Q, knn=10, beam=3)
-    assert ids_b.shape == (300, 10)
+    chb = [b.children(l) for l in range(1, L + 1)]
+    for beam in (1, 3, 8, 64):  # member-id gathers (beam 64: the wide-beam kernel's path)
+        ids_b, d2_b = b.query(Q, knn=10, beam=beam)
+        ref_i, ref_d, gap = oracle.query([b.prototypes(l) for l in range(1, L + 1)], [c[0] for c in chb],
+                                         [c[1] for c in chb], X, datagen.queries(cfg, count=300), 10, beam)
+        check_queries(ids_b.cpu().numpy(), d2_b.cpu().numpy(), ref_i, ref_d, gap,
+                      what=f"member-id leaf scan beam {beam}")
     b.free()
 
 
