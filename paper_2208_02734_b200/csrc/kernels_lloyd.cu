@@ -1005,7 +1005,7 @@ __global__ void __launch_bounds__(256) k_update_seg64(const float4* __restrict__
                                                        double* __restrict__ S, int32_t* __restrict__ counts,
                                                        const int* __restrict__ active) {
   if (active && !*active) return;
-  constexpr int R = 32 / L, U = 4;
+  constexpr int R = 32 / L, U = 8;  // 8 rows in flight per lane group (latency-bound gathers)
   const int lane = threadIdx.x & 31, slot = lane / L, c4 = lane % L;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t j = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); j < k; j += warps) {
