@@ -155,8 +155,8 @@ void launch_update_dense64(const float* X, int64_t n, int d, const int32_t* labe
 void launch_f32_to_f64(const float* a, int64_t n, double* b, cudaStream_t st);
 // FP64 sums over label-sorted rows without atomics (warp per cluster; end = the sort's end offsets)
 bool update_seg64_supported(int d);
-void launch_update_seg64(const float* X, int d, const int32_t* perm, const int32_t* end, int64_t k, double* S,
-                         int32_t* counts, cudaStream_t st, const int* active);
+void launch_update_seg64(const float* X, int d, const int32_t* perm, const int32_t* labels, const int32_t* end,
+                         int64_t n, double* S, int32_t* counts, cudaStream_t st, const int* active);
 // prototype operands for K1: Pb = tf32_rn(-2c), Ps = tf32_rn(-2c - Pb), cn2 = ||c||^2; with
 // kc > d the augmented columns [d] = split(||c||^2), [d+1] = (1, 0), rest 0 (row stride kc)
 // flag_count (optional): reset to 0 (the list K1 appends near-tie rows to)

@@ -994,71 +994,95 @@ void launch_update_dense64(const float* X, int64_t n, int d, const int32_t* labe
   MASK_LAUNCH_CHECK();
 }
 
-// FP64 sums without atomics: over the label-sorted rows (perm; end[j] = the sort's end offset of
-// label j) a warp owns whole clusters -- L lanes per row (one float4 each), R = 32/L rows per
-// step, U rows in flight per lane group -- accumulates them in FP64 registers, combines its R row
-// groups with shuffles and writes S_j and n_j with plain stores (every cluster is written,
-// empty ones as zeros).  Traffic: the rows once, perm, S once.
+// FP64 sums over the label-sorted rows (perm; end[j] = the sort's end offset of label j), cut
+// into fixed chunks of kSeg64 positions, one warp per chunk: for every cluster piece in its
+// chunk the warp accumulates the rows in FP64 registers (L lanes per row, one float4 each, R =
+// 32/L rows per step, U rows in flight per lane group), combines its R row groups with
+// shuffles, and flushes -- a cluster wholly inside the chunk with plain stores of S_j and n_j,
+// a piece of a cluster cut by a chunk boundary with FP64 atomics (S and counts arrive zeroed).
+// Chunks keep a huge cluster spread over many warps; most clusters need no atomics.
+constexpr int kSeg64 = 256;
 template <int L>
 __global__ void __launch_bounds__(256) k_update_seg64(const float4* __restrict__ X4, const int32_t* __restrict__ perm,
-                                                       const int32_t* __restrict__ end, int64_t k, int d4,
+                                                       const int32_t* __restrict__ labels,
+                                                       const int32_t* __restrict__ end, int64_t n, int d4,
                                                        double* __restrict__ S, int32_t* __restrict__ counts,
                                                        const int* __restrict__ active) {
   if (active && !*active) return;
-  constexpr int R = 32 / L, U = 8;  // 8 rows in flight per lane group (latency-bound gathers)
+  constexpr int R = 32 / L, U = 4;
   const int lane = threadIdx.x & 31, slot = lane / L, c4 = lane % L;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t j = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); j < k; j += warps) {
-    const int32_t s0 = j ? end[j - 1] : 0, s1 = end[j];
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-    for (int32_t p = s0 + slot; p < s1; p += R * U) {
-      float4 v[U];
+  const int64_t nchunks = (n + kSeg64 - 1) / kSeg64;
+  for (int64_t ch = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); ch < nchunks; ch += warps) {
+    const int32_t q0 = (int32_t)(ch * kSeg64), q1 = (int32_t)min64(n, (ch + 1) * kSeg64);
+    int32_t j = __ldg(labels + __ldg(perm + q0));
+    for (int32_t a = q0; a < q1;) {
+      const int32_t cs = j ? __ldg(end + j - 1) : 0, ce = __ldg(end + j);
+      const int32_t b = ce < q1 ? ce : q1;  // this piece: positions [a, b)
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      for (int32_t p = a + slot; p < b; p += R * U) {
+        float4 v[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int32_t q = p + u * R;
-        v[u] = (q < s1 && c4 < d4) ? __ldg(X4 + (int64_t)__ldg(perm + q) * d4 + c4) : make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int u = 0; u < U; ++u) {
+          const int32_t q = p + u * R;
+          v[u] = (q < b && c4 < d4) ? __ldg(X4 + (int64_t)__ldg(perm + q) * d4 + c4) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          a0 += (double)v[u].x;
+          a1 += (double)v[u].y;
+          a2 += (double)v[u].z;
+          a3 += (double)v[u].w;
+        }
       }
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        a0 += (double)v[u].x;
-        a1 += (double)v[u].y;
-        a2 += (double)v[u].z;
-        a3 += (double)v[u].w;
+      for (int o = L; o < 32; o <<= 1) {
+        a0 += __shfl_xor_sync(0xffffffffu, a0, o);
+        a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+        a2 += __shfl_xor_sync(0xffffffffu, a2, o);
+        a3 += __shfl_xor_sync(0xffffffffu, a3, o);
       }
+      const bool whole = a == cs && b == ce;
+      if (slot == 0 && c4 < d4) {
+        double* dst = S + ((int64_t)j * d4 + c4) * 4;
+        if (whole) {
+          dst[0] = a0;
+          dst[1] = a1;
+          dst[2] = a2;
+          dst[3] = a3;
+        } else {
+          atomicAdd(dst + 0, a0);
+          atomicAdd(dst + 1, a1);
+          atomicAdd(dst + 2, a2);
+          atomicAdd(dst + 3, a3);
+        }
+      }
+      if (lane == 0) {
+        if (whole) counts[j] = b - a;
+        else atomicAdd(counts + j, b - a);
+      }
+      a = b;
+      if (a < q1) j = __ldg(labels + __ldg(perm + a));  // (empty clusters have no positions)
     }
-#pragma unroll
-    for (int o = L; o < 32; o <<= 1) {
-      a0 += __shfl_xor_sync(0xffffffffu, a0, o);
-      a1 += __shfl_xor_sync(0xffffffffu, a1, o);
-      a2 += __shfl_xor_sync(0xffffffffu, a2, o);
-      a3 += __shfl_xor_sync(0xffffffffu, a3, o);
-    }
-    if (slot == 0 && c4 < d4) {
-      double* dst = S + (j * d4 + c4) * 4;
-      dst[0] = a0;
-      dst[1] = a1;
-      dst[2] = a2;
-      dst[3] = a3;
-    }
-    if (lane == 0) counts[j] = s1 - s0;
   }
 }
 
 bool update_seg64_supported(int d) { return d % 4 == 0 && d <= 128; }
 
-void launch_update_seg64(const float* X, int d, const int32_t* perm, const int32_t* end, int64_t k, double* S,
-                         int32_t* counts, cudaStream_t st, const int* active) {
-  if (k <= 0) return;
+void launch_update_seg64(const float* X, int d, const int32_t* perm, const int32_t* labels, const int32_t* end,
+                         int64_t n, double* S, int32_t* counts, cudaStream_t st, const int* active) {
+  if (n <= 0) return;
   const int d4 = d / 4;
   const int L = d4 <= 1 ? 1 : d4 <= 2 ? 2 : d4 <= 4 ? 4 : d4 <= 8 ? 8 : d4 <= 16 ? 16 : 32;
-  const unsigned grid = grid_for(k * 32, 256, (int64_t)num_sms() * 16);
+  const int64_t nchunks = (n + kSeg64 - 1) / kSeg64;
+  const unsigned grid = grid_for(nchunks * 32, 256, (int64_t)num_sms() * 16);
   const float4* X4 = reinterpret_cast<const float4*>(X);
-  if (L == 1) k_update_seg64<1><<<grid, 256, 0, st>>>(X4, perm, end, k, d4, S, counts, active);
-  else if (L == 2) k_update_seg64<2><<<grid, 256, 0, st>>>(X4, perm, end, k, d4, S, counts, active);
-  else if (L == 4) k_update_seg64<4><<<grid, 256, 0, st>>>(X4, perm, end, k, d4, S, counts, active);
-  else if (L == 8) k_update_seg64<8><<<grid, 256, 0, st>>>(X4, perm, end, k, d4, S, counts, active);
-  else if (L == 16) k_update_seg64<16><<<grid, 256, 0, st>>>(X4, perm, end, k, d4, S, counts, active);
-  else k_update_seg64<32><<<grid, 256, 0, st>>>(X4, perm, end, k, d4, S, counts, active);
+  if (L == 1) k_update_seg64<1><<<grid, 256, 0, st>>>(X4, perm, labels, end, n, d4, S, counts, active);
+  else if (L == 2) k_update_seg64<2><<<grid, 256, 0, st>>>(X4, perm, labels, end, n, d4, S, counts, active);
+  else if (L == 4) k_update_seg64<4><<<grid, 256, 0, st>>>(X4, perm, labels, end, n, d4, S, counts, active);
+  else if (L == 8) k_update_seg64<8><<<grid, 256, 0, st>>>(X4, perm, labels, end, n, d4, S, counts, active);
+  else if (L == 16) k_update_seg64<16><<<grid, 256, 0, st>>>(X4, perm, labels, end, n, d4, S, counts, active);
+  else k_update_seg64<32><<<grid, 256, 0, st>>>(X4, perm, labels, end, n, d4, S, counts, active);
   MASK_LAUNCH_CHECK();
 }
 

@@ -853,7 +853,7 @@ void run_level(const Input& in, int64_t k, const int64_t* init_idx_host, const m
     else if (in.format == MASK_CSR_F32)
       launch_update_csr(in.rp, in.col, in.val, n, d, ws.lab_cur.p, ws.S.p, ws.counts.p, st, active);
     else if (p64 && sorted && update_seg64_supported(d) && ((uintptr_t)in.X % 16) == 0)
-      launch_update_seg64(in.X, d, ws.perm.p, ws.sort_cnt.p, k, ws.S64.p, ws.counts.p, st, active);
+      launch_update_seg64(in.X, d, ws.perm.p, ws.lab_cur.p, ws.sort_cnt.p, n, ws.S64.p, ws.counts.p, st, active);
     else if (p64)
       launch_update_dense64(in.X, n, d, ws.lab_cur.p, ws.S64.p, ws.counts.p, st, active, sorted ? ws.perm.p : nullptr);
     else
