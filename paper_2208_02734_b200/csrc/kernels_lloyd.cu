@@ -1001,7 +1001,7 @@ void launch_update_dense64(const float* X, int64_t n, int d, const int32_t* labe
 // shuffles, and flushes -- a cluster wholly inside the chunk with plain stores of S_j and n_j,
 // a piece of a cluster cut by a chunk boundary with FP64 atomics (S and counts arrive zeroed).
 // Chunks keep a huge cluster spread over many warps; most clusters need no atomics.
-constexpr int kSeg64 = 256;
+constexpr int kSeg64 = 128;  // (measured: 64 / 128 / 256 / 512 rows: C3 0.53 / 0.54 / 0.58 / 0.64 ms, C2 23 / 21 / 31 / 49 us per pass)
 template <int L>
 __global__ void __launch_bounds__(256) k_update_seg64(const float4* __restrict__ X4, const int32_t* __restrict__ perm,
                                                        const int32_t* __restrict__ labels,
