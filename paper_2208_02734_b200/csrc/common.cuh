@@ -244,6 +244,9 @@ struct QLevel {
   const int64_t* offsets;
   const int32_t* members;
   int64_t k;
+  // this level's prototypes in the parent level's child-list order (Pc[m] = P[parent.members[m]]),
+  // or nullptr: the descent then reads every parent's children as contiguous rows
+  const float* Pc = nullptr;
 };
 constexpr int kMaxLevels = 16;
 struct QIndex {
@@ -262,7 +265,16 @@ struct QIndex {
   // dense data rows in level-1 partition order (Xp[pos] = X[members_1[pos]]), or nullptr: leaf
   // scans then read contiguous rows at addresses known before the member ids arrive
   const float* Xp = nullptr;
+  // leaf-grouped queries: when set, the descent writes each query's selected level-1
+  // prototypes (beam entries, -1 padded) here and skips the leaf scan
+  int32_t* sel_out = nullptr;
 };
+// Leaf-grouped batched k-NN (dense, partition-ordered rows): descent -> (query, leaf) pairs
+// grouped by leaf -> every leaf's rows staged in shared memory once for all its queries ->
+// per-query merge of the per-leaf top-k lists.  Same result order (d^2, id) as the per-query
+// kernel.  Returns false (nothing launched) when the batch does not qualify.
+bool launch_query_grouped(const QIndex& qi, const float* Q, int64_t nq, int knn, int beam, int64_t* ids, float* d2,
+                          cudaStream_t st);
 // Xp[pos * d ...] = X[members[pos] * d ...] for pos < n (the partition-ordered copy of the rows)
 void launch_gather_partition(const float* X, int d, const int32_t* members, int64_t n, float* Xp, cudaStream_t st);
 // K13 range search: cover radii (cover[l] = k_l float bits) and the multi-path descent; returns

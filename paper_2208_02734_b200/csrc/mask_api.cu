@@ -356,6 +356,9 @@ struct mask_index {
   const float* val = nullptr;
   DevBuf<float> own_X, own_val;
   DevBuf<float> Xpart;  // dense rows in level-1 partition order (leaf scans of mask_query)
+  // Pchild[l]: level-(l+1) prototypes in level-(l+2) child-list order (the descent's contiguous
+  // child scans; dense indexes, l < L - 1; empty entries: none kept)
+  std::vector<DevBuf<float>> Pchild;
   DevBuf<int64_t> own_rp;
   DevBuf<int32_t> own_col;
   std::vector<Level> levels;
@@ -996,6 +999,31 @@ void gather_partition_best_effort(mask_index* idx, cudaStream_t st) {
   launch_gather_partition(idx->X, d, idx->levels[0].members.p, N, idx->Xpart.p, st);
 }
 
+// The child-ordered prototype copies (Pchild) are an optimisation like Xpart: sum_l k_l x d
+// floats, skipped per level when the device cannot hold them.  Rebuilt whenever child lists change.
+void gather_child_protos(mask_index* idx, cudaStream_t st) {
+  idx->Pchild.clear();
+  if (idx->format != MASK_DENSE_F32) return;
+  const int L = (int)idx->levels.size();
+  idx->Pchild.resize(std::max(L - 1, 0));
+  for (int l = 0; l + 1 < L; ++l) {
+    const int64_t k = idx->levels[l].k;
+    if (idx->levels[l + 1].n_items != k || k == 0) continue;
+    try {
+      idx->Pchild[l].alloc((size_t)k * idx->dim);
+    } catch (const Error& e) {
+      if (e.code != MASK_ERR_OOM) throw;
+      cudaGetLastError();
+      idx->Pchild[l].release();
+      continue;
+    }
+    launch_gather_partition(idx->levels[l].P.p, idx->dim, idx->levels[l + 1].members.p, k, idx->Pchild[l].p, st);
+  }
+}
+const float* pchild_ptr(const mask_index* idx, int l) {
+  return l < (int)idx->Pchild.size() ? idx->Pchild[l].p : nullptr;
+}
+
 void build_impl(const mask_matrix* data, const mask_build_params* p, mask_comm* comm,
                 cudaStream_t st, mask_index** out) {
   MASK_REQUIRE(out != nullptr, MASK_ERR_ARG, "out is NULL");
@@ -1250,6 +1278,7 @@ void build_impl(const mask_matrix* data, const mask_build_params* p, mask_comm* 
   // ---- dense rows in level-1 partition order for the leaf scans (one gather, n x d floats)
   if (idx->format == MASK_DENSE_F32 && !(p->flags & MASK_NO_PARTITION_COPY))
     gather_partition_best_effort(idx.get(), st);
+  gather_child_protos(idx.get(), st);
   if (idx->format == MASK_CSR_F32) {
     // ||c||^2 per level for sparse queries
     int64_t tot = 0;
@@ -1347,6 +1376,8 @@ void build_grouped_impl(const mask_matrix* data, const mask_grouped_params* p, c
     MASK_CUDA(cudaStreamSynchronize(st));  // cursor / perm scratch go out of scope
     Y = L.P.p;
   }
+  gather_child_protos(idx.get(), st);
+  MASK_CUDA(cudaStreamSynchronize(st));
   *out = idx.release();
 }
 
@@ -1457,6 +1488,7 @@ QIndex make_qindex(const mask_index* idx) {
     qi.lv[l].offsets = idx->levels[l].offsets.p;
     qi.lv[l].members = idx->levels[l].members.p;
     qi.lv[l].k = idx->levels[l].k;
+    qi.lv[l].Pc = pchild_ptr(idx, l);
   }
   return qi;
 }
@@ -1600,8 +1632,9 @@ int32_t mask_insert(mask_index* idx, const mask_matrix* points, int64_t* partiti
     if (idx->Xpart.p) {  // the partitions changed: re-gather the partition-ordered rows
       idx->Xpart.release();  // (the old copy goes first: peak = data + one copy)
       gather_partition_best_effort(idx, st);
-      MASK_CUDA(cudaStreamSynchronize(st));
     }
+    gather_child_protos(idx, st);
+    MASK_CUDA(cudaStreamSynchronize(st));
     std::lock_guard<std::mutex> lock(idx->cover_mu);
     idx->cover_valid = false;
   });
@@ -1726,6 +1759,7 @@ void split_impl(mask_index* idx, const mask_split_params* p, int64_t* n_split_ou
     idx->Xpart.release();
     gather_partition_best_effort(idx, st);
   }
+  gather_child_protos(idx, st);
   MASK_CUDA(cudaStreamSynchronize(st));
   std::lock_guard<std::mutex> lock(idx->cover_mu);
   idx->cover_valid = false;
@@ -1760,6 +1794,7 @@ int32_t query_impl(const mask_index* idx, const mask_matrix* queries, int32_t k_
       qi.lv[l].offsets = idx->levels[l].offsets.p;
       qi.lv[l].members = idx->levels[l].members.p;
       qi.lv[l].k = idx->levels[l].k;
+      qi.lv[l].Pc = pchild_ptr(idx, l);
     }
     const bool host = queries->memory == MASK_MEM_HOST;
     DevBuf<float> qv;
@@ -1801,8 +1836,10 @@ int32_t query_impl(const mask_index* idx, const mask_matrix* queries, int32_t k_
     qi.rstride = rstride;
     qi.id_base = id_base;
     qi.Xp = idx->Xpart.p;
-    if (idx->format == MASK_DENSE_F32)
-      launch_query_dense(qi, Qv, nq, k_nn, beam, ids, d2, st);
+    if (idx->format == MASK_DENSE_F32) {
+      if (!launch_query_grouped(qi, Qv, nq, k_nn, beam, ids, d2, st))
+        launch_query_dense(qi, Qv, nq, k_nn, beam, ids, d2, st);
+    }
     else
       launch_query_csr(qi, idx->cn2_flat.p, idx->cn2_off.p, Qrp, Qcol, Qv, nq, k_nn, beam, ids, d2, st);
     if (host) {

@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -77,7 +78,27 @@ struct WarpTopK {
   __device__ void offer(float cd, int32_t cid, int lane) {
     const float kd = __shfl_sync(FULL, d, K - 1);
     const int32_t ki = __shfl_sync(FULL, id, K - 1);
-    if (!__any_sync(FULL, key_lt(cd, cid, kd, ki))) return;
+    unsigned m = __ballot_sync(FULL, key_lt(cd, cid, kd, ki));
+    if (!m) return;
+    if (__popc(m) <= 4) {
+      // few entrants (the common case once the list has warmed up): insert them one at a time
+      // (shift the entries above each one's rank up by a lane; lane 31 drops out).  Keeps the
+      // same invariant as the sort + merge below: lanes < K hold the best K keys offered.
+      do {
+        const int src = __ffs(m) - 1;
+        m &= m - 1;
+        const float xd = __shfl_sync(FULL, cd, src);
+        const int32_t xi = __shfl_sync(FULL, cid, src);
+        const float pd = __shfl_up_sync(FULL, d, 1);
+        const int32_t pi = __shfl_up_sync(FULL, id, 1);
+        if (key_lt(xd, xi, d, id)) {
+          const bool shift = lane > 0 && key_lt(xd, xi, pd, pi);
+          d = shift ? pd : xd;
+          id = shift ? pi : xi;
+        }
+      } while (m);
+      return;
+    }
     warp_sort32(cd, cid, lane);
     const float rd = __shfl_sync(FULL, cd, 31 - lane);
     const int32_t ri = __shfl_sync(FULL, cid, 31 - lane);
@@ -253,6 +274,49 @@ __device__ __forceinline__ void leaf_scan_coalesced(const QIndex& qi, const floa
   }
 }
 
+// block_dist32 for a runtime G (d = 4G, G a power of two <= 32; others: G = 0, not called).
+// q: 16-byte aligned.
+__device__ __forceinline__ float block_dist_any(int G, const float* __restrict__ base, int nvalid, const float* q,
+                                                int lane, int& r) {
+  const float4* b4 = reinterpret_cast<const float4*>(base);
+  const float4 qc = reinterpret_cast<const float4*>(q)[lane % G];
+  switch (G) {
+    case 1: return block_dist32<1>(b4, nvalid, qc, lane, r);
+    case 2: return block_dist32<2>(b4, nvalid, qc, lane, r);
+    case 4: return block_dist32<4>(b4, nvalid, qc, lane, r);
+    case 8: return block_dist32<8>(b4, nvalid, qc, lane, r);
+    case 16: return block_dist32<16>(b4, nvalid, qc, lane, r);
+    default: return block_dist32<32>(b4, nvalid, qc, lane, r);
+  }
+}
+__host__ __device__ __forceinline__ int coalesced_g(int d) {
+  const int g = d >> 2;
+  return ((d & 3) == 0 && g >= 1 && g <= 32 && (g & (g - 1)) == 0) ? g : 0;
+}
+// Descent step over 32 consecutive candidates: the top level's prototypes j0.. (contiguous in
+// L.P) or the children m.. of a parent (contiguous in L.Pc).  Lane l gets one candidate (its
+// distance and id, PAD_ID / +inf for none or a prototype without children).
+__device__ __forceinline__ void top_block(const QLevel& L, int G, const float* q, int d, int64_t j0, int lane,
+                                          float& cd, int32_t& cid) {
+  const int nv = (int)min64(32, L.k - j0);
+  int r;
+  const float v = block_dist_any(G, L.P + j0 * d, nv, q, lane, r);
+  cid = (r < nv && has_children(L, j0 + r)) ? (int32_t)(j0 + r) : PAD_ID;
+  cd = cid == PAD_ID ? INFINITY : v;
+}
+__device__ __forceinline__ void child_block(const QLevel& L, const QLevel& up, int G, const float* q, int d, int64_t m,
+                                            int64_t m1, int lane, float& cd, int32_t& cid) {
+  const int nv = (int)min64(32, m1 - m);
+  int r;
+  const float v = block_dist_any(G, L.Pc + m * d, nv, q, lane, r);
+  cid = PAD_ID;
+  if (r < nv) {
+    const int32_t j = up.members[m + r];
+    if (has_children(L, j)) cid = j;
+  }
+  cd = cid == PAD_ID ? INFINITY : v;
+}
+
 // Dense queries against a dense index.  Shared memory: one q vector (d floats) per warp.
 template <int LPC>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32)
@@ -280,7 +344,15 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
     {
       const QLevel& L = qi.lv[qi.L - 1];
       top.reset(beam);
+      const int G = coalesced_g(d);
       for (int64_t j0 = 0; j0 < L.k; j0 += 32) {
+        if (G) {
+          float cd;
+          int32_t cid;
+          top_block(L, G, q, d, j0, lane, cd, cid);
+          top.offer(cd, cid, lane);
+          continue;
+        }
         const int64_t j = j0 + lane;
         const int32_t cid = (j < L.k && has_children(L, j)) ? (int32_t)j : PAD_ID;
         top.offer(coop_dist<LPC>(q, L.P, d, cid, lane), cid, lane);
@@ -299,7 +371,15 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
         const float pd = __shfl_sync(FULL, sel_d, s);
         if (p == PAD_ID || pd == INFINITY && p == PAD_ID) continue;
         const int64_t m0 = up.offsets[p], m1 = up.offsets[p + 1];
+        const int G = L.Pc ? coalesced_g(d) : 0;
         for (int64_t m = m0; m < m1; m += 32) {
+          if (G) {
+            float cd;
+            int32_t cid;
+            child_block(L, up, G, q, d, m, m1, lane, cd, cid);
+            top.offer(cd, cid, lane);
+            continue;
+          }
           const int64_t mm = m + lane;
           int32_t cid = PAD_ID;
           if (mm < m1) {
@@ -312,6 +392,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
     }
     if (leaf_only) {  // insertion: the level-1 prototype the descent reaches
       if (lane == 0) ids_out[qid] = top.id == PAD_ID ? -1 : (int64_t)top.id;
+      continue;
+    }
+    if (qi.sel_out) {  // leaf-grouped queries: hand the level-1 selection over
+      if (lane < beam) qi.sel_out[qid * beam + lane] = top.id == PAD_ID ? -1 : top.id;
       continue;
     }
     // ---- data layer: rows of the reached partition(s)
@@ -440,7 +524,15 @@ __global__ void __launch_bounds__(kWideWarps * 32)
     {  // top level: every prototype with children
       const QLevel& L = qi.lv[qi.L - 1];
       cur.reset(beam);
+      const int G = coalesced_g(d);
       for (int64_t j0 = 0; j0 < L.k; j0 += 32) {
+        if (G) {
+          float cd;
+          int32_t cid;
+          top_block(L, G, q, d, j0, lane, cd, cid);
+          cur.offer(cd, cid, lane);
+          continue;
+        }
         const int64_t j = j0 + lane;
         const int32_t cid = (j < L.k && has_children(L, j)) ? (int32_t)j : PAD_ID;
         cur.offer(coop_dist<1>(q, L.P, d, cid, lane), cid, lane);
@@ -453,7 +545,15 @@ __global__ void __launch_bounds__(kWideWarps * 32)
       for (int s = 0; s < cur.n; ++s) {
         const int32_t p = cur.id[s];
         const int64_t m0 = up.offsets[p], m1 = up.offsets[p + 1];
+        const int G = L.Pc ? coalesced_g(d) : 0;
         for (int64_t m = m0; m < m1; m += 32) {
+          if (G) {
+            float cd;
+            int32_t cid;
+            child_block(L, up, G, q, d, m, m1, lane, cd, cid);
+            nxt.offer(cd, cid, lane);
+            continue;
+          }
           const int64_t mm = m + lane;
           int32_t cid = PAD_ID;
           if (mm < m1) {
@@ -472,6 +572,10 @@ __global__ void __launch_bounds__(kWideWarps * 32)
       nxt.d = td_;
       nxt.id = ti_;
       __syncwarp();
+    }
+    if (qi.sel_out) {  // leaf-grouped queries: hand the level-1 selection over
+      for (int s2 = lane; s2 < beam; s2 += 32) qi.sel_out[qid * beam + s2] = s2 < cur.n ? cur.id[s2] : -1;
+      continue;
     }
     // data layer: rows of the reached partitions
     const QLevel& L1 = qi.lv[0];
@@ -504,6 +608,216 @@ __global__ void __launch_bounds__(kWideWarps * 32)
       d2_out[qid * knn + lane] = pad ? INFINITY : top.d;
     }
   }
+}
+
+// ---------------------------------------------------------------------------------------
+// Leaf-grouped scan (large batches).  The per-query kernel reads every reached partition once
+// per query: at C3 with beam 128 that is ~5 MB of rows per query, from HBM (the partitions a
+// query reaches are scattered over the 2.56 GB copy).  The grouped form sorts the (query,
+// leaf) pairs by leaf, so all queries of a leaf are served while its rows are on chip:
+//   pairs: e = q * beam + s for every selected leaf, grouped by leaf (counting sort);
+//   k_leaf_scan: a warp per work item of kLeafPG consecutive pairs (dynamic queue, items in
+//     leaf order so concurrently running items share leaves in L2); per leaf segment of the
+//     item: the segment's query vectors and running top-k lists in shared memory, then for
+//     each 32-row chunk of the leaf every lane holds one row in registers and the warp streams
+//     the segment's queries past it (q broadcast from shared memory);
+//   k_merge_partials: warp per query, the beam partial lists -> the final top-k.
+constexpr int kLeafPG = 16;
+constexpr int kLeafWarps = 4;
+
+__global__ void k_pair_hist(const int32_t* __restrict__ sel, int64_t m, int32_t* __restrict__ cnt) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t l = sel[e];
+    if (l >= 0) atomicAdd(cnt + l, 1);
+  }
+}
+// single-block exclusive scan of k counts -> off[0..k] (int64); cnt becomes the scatter cursor
+__global__ void __launch_bounds__(1024) k_pair_scan(int32_t* __restrict__ cnt, int64_t k, int64_t* __restrict__ off) {
+  __shared__ int64_t part[1024];
+  const int t = threadIdx.x;
+  const int64_t per = (k + blockDim.x - 1) / blockDim.x;
+  const int64_t a = t * per, b = min64(k, a + per);
+  int64_t s = 0;
+  for (int64_t j = a; j < b; ++j) s += cnt[j];
+  part[t] = s;
+  __syncthreads();
+  for (int o = 1; o < (int)blockDim.x; o <<= 1) {
+    const int64_t v = t >= o ? part[t - o] : 0;
+    __syncthreads();
+    part[t] += v;
+    __syncthreads();
+  }
+  int64_t run = part[t] - s;
+  for (int64_t j = a; j < b; ++j) {
+    off[j] = run;
+    const int32_t c = cnt[j];
+    cnt[j] = (int32_t)run;  // (counts per leaf < 2^31)
+    run += c;
+  }
+  if (t == blockDim.x - 1) off[k] = part[t];
+}
+__global__ void k_pair_scatter(const int32_t* __restrict__ sel, int64_t m, int32_t* __restrict__ cursor,
+                               int64_t* __restrict__ pairs) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t l = sel[e];
+    if (l >= 0) pairs[atomicAdd(cursor + l, 1)] = e;
+  }
+}
+
+template <int D4M>  // float4 registers per row: d / 4 <= D4M
+__global__ void __launch_bounds__(kLeafWarps * 32)
+    k_leaf_scan(QIndex qi, const float* __restrict__ Q, const int32_t* __restrict__ sel,
+                const int64_t* __restrict__ pairs, const int64_t* __restrict__ loff, int64_t k1, int beam, int knn,
+                int* __restrict__ queue, int32_t* __restrict__ part_id, float* __restrict__ part_d) {
+  extern __shared__ __align__(16) float4 lsm4[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int d = qi.dim, d4 = d >> 2;
+  float4* qs = lsm4 + (size_t)w * (kLeafPG * D4M + kLeafPG * 16);  // [kLeafPG][D4M]
+  float* ld = reinterpret_cast<float*>(qs + kLeafPG * D4M);          // [kLeafPG][32]
+  int32_t* li = reinterpret_cast<int32_t*>(ld + kLeafPG * 32);       // [kLeafPG][32]
+  const QLevel& L1 = qi.lv[0];
+  const float4* Xp4 = reinterpret_cast<const float4*>(qi.Xp);
+  const int64_t npairs = loff[k1];
+  const int64_t nitems = (npairs + kLeafPG - 1) / kLeafPG;
+  for (;;) {
+    int item = 0;
+    if (lane == 0) item = atomicAdd(queue, 1);
+    item = __shfl_sync(FULL, item, 0);
+    if (item >= nitems) break;
+    const int64_t i1 = min64(npairs, (int64_t)(item + 1) * kLeafPG);
+    for (int64_t s0 = (int64_t)item * kLeafPG; s0 < i1;) {
+      const int32_t p = sel[pairs[s0]];
+      const int64_t s1 = min64(i1, loff[p + 1]);
+      const int np = (int)(s1 - s0);
+      __syncwarp();
+      for (int j = 0; j < np; ++j) {
+        const int64_t e = pairs[s0 + j];
+        const float4* q4 = reinterpret_cast<const float4*>(Q + (e / beam) * d);
+        for (int f = lane; f < D4M; f += 32) qs[j * D4M + f] = f < d4 ? q4[f] : make_float4(0.f, 0.f, 0.f, 0.f);
+        ld[j * 32 + lane] = INFINITY;
+        li[j * 32 + lane] = PAD_ID;
+      }
+      __syncwarp();
+      const int64_t m0 = L1.offsets[p], m1 = L1.offsets[p + 1];
+      for (int64_t c = m0; c < m1; c += 32) {
+        const int64_t r = c + lane;
+        const bool valid = r < m1;
+        float4 x[D4M];
+#pragma unroll
+        for (int f = 0; f < D4M; ++f) x[f] = (valid && f < d4) ? __ldg(Xp4 + r * d4 + f) : make_float4(0.f, 0.f, 0.f, 0.f);
+        const int32_t cid = valid ? L1.members[r] : PAD_ID;
+        for (int j = 0; j < np; ++j) {
+          WarpTopK top;
+          top.K = knn;
+          top.d = ld[j * 32 + lane];
+          top.id = li[j * 32 + lane];
+          const float4* qj = qs + j * D4M;
+          float a0 = 0.f, a1 = 0.f;
+#pragma unroll
+          for (int f = 0; f < D4M; ++f) {
+            const float4 qv = qj[f];
+            float t = qv.x - x[f].x;
+            a0 = fmaf(t, t, a0);
+            t = qv.y - x[f].y;
+            a1 = fmaf(t, t, a1);
+            t = qv.z - x[f].z;
+            a0 = fmaf(t, t, a0);
+            t = qv.w - x[f].w;
+            a1 = fmaf(t, t, a1);
+          }
+          top.offer(valid ? a0 + a1 : INFINITY, cid, lane);
+          ld[j * 32 + lane] = top.d;
+          li[j * 32 + lane] = top.id;
+        }
+      }
+      __syncwarp();
+      for (int j = 0; j < np; ++j) {
+        const int64_t e = pairs[s0 + j];
+        if (lane < knn) {
+          part_d[e * knn + lane] = ld[j * 32 + lane];
+          part_id[e * knn + lane] = li[j * 32 + lane];
+        }
+      }
+      s0 = s1;
+    }
+  }
+}
+
+__global__ void k_merge_partials(const int32_t* __restrict__ sel, const int32_t* __restrict__ part_id,
+                                 const float* __restrict__ part_d, int64_t nq, int beam, int knn, int64_t id_base,
+                                 int64_t* __restrict__ ids_out, float* __restrict__ d2_out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t qid = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); qid < nq; qid += warps) {
+    WarpTopK top;
+    top.reset(knn);
+    // each partial list holds knn entries (padded); offer them 32 at a time
+    const int64_t tot = (int64_t)beam * knn;
+    for (int64_t c = 0; c < tot; c += 32) {
+      const int64_t e = c + lane;
+      float cd = INFINITY;
+      int32_t cid = PAD_ID;
+      if (e < tot && sel[qid * beam + e / knn] >= 0) {
+        cd = part_d[qid * tot + e];
+        cid = part_id[qid * tot + e];
+      }
+      top.offer(cd, cid, lane);
+    }
+    if (lane < knn) {
+      const bool pad = top.id == PAD_ID;
+      ids_out[qid * knn + lane] = pad ? -1 : id_base + (int64_t)top.id;
+      d2_out[qid * knn + lane] = pad ? INFINITY : top.d;
+    }
+  }
+}
+
+bool launch_query_grouped(const QIndex& qi, const float* Q, int64_t nq, int knn, int beam, int64_t* ids, float* d2,
+                          cudaStream_t st) {
+  // MASK_QUERY_GROUPED=0 / 1: never / always (A/B and tests; read per call)
+  const char* env = getenv("MASK_QUERY_GROUPED");
+  const int mode = env ? atoi(env) : -1;
+  const int64_t m = nq * (int64_t)beam;
+  const int d = qi.dim;
+  if (mode == 0 || !qi.Xp || qi.routed || qi.L < 1 || (d & 3) || d > 128) return false;
+  if (m == 0 || (mode != 1 && m < 65536)) return false;  // small batches: the per-query kernel
+  const size_t part_bytes = (size_t)m * knn * 8;
+  if (part_bytes > ((size_t)8 << 30)) return false;
+  const int d4 = d >> 2;
+  const int d4m = d4 <= 4 ? 4 : d4 <= 8 ? 8 : d4 <= 16 ? 16 : 32;
+  const size_t smem = (size_t)kLeafWarps * (kLeafPG * d4m + kLeafPG * 16) * sizeof(float4);
+  const int64_t k1 = qi.lv[0].k;
+  DevBuf<int32_t> sel(m), cnt(k1), pid((size_t)m * knn), queue(1);
+  DevBuf<int64_t> off(k1 + 1), pairs(m);
+  DevBuf<float> pd((size_t)m * knn);
+  QIndex q2 = qi;
+  q2.sel_out = sel.p;
+  launch_query_dense(q2, Q, nq, knn, beam, ids, d2, st, false);  // descent only
+  MASK_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(int32_t) * k1, st));
+  k_pair_hist<<<grid_for(m, 256), 256, 0, st>>>(sel.p, m, cnt.p);
+  MASK_LAUNCH_CHECK();
+  k_pair_scan<<<1, 1024, 0, st>>>(cnt.p, k1, off.p);
+  MASK_LAUNCH_CHECK();
+  k_pair_scatter<<<grid_for(m, 256), 256, 0, st>>>(sel.p, m, cnt.p, pairs.p);
+  MASK_LAUNCH_CHECK();
+  MASK_CUDA(cudaMemsetAsync(queue.p, 0, sizeof(int), st));
+  const unsigned lgrid = (unsigned)num_sms() * 8;
+  switch (d4m) {
+#define MASK_LEAF(D)                                                                                      \
+  case D:                                                                                                 \
+    MASK_CUDA(cudaFuncSetAttribute(k_leaf_scan<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+    k_leaf_scan<D><<<lgrid, kLeafWarps * 32, smem, st>>>(qi, Q, sel.p, pairs.p, off.p, k1, beam, knn, queue.p, \
+                                                         pid.p, pd.p);                                    \
+    break;
+    MASK_LEAF(4)
+    MASK_LEAF(8)
+    MASK_LEAF(16)
+    MASK_LEAF(32)
+#undef MASK_LEAF
+  }
+  MASK_LAUNCH_CHECK();
+  k_merge_partials<<<grid_for(nq * 32, 256), 256, 0, st>>>(sel.p, pid.p, pd.p, nq, beam, knn, qi.id_base, ids, d2);
+  MASK_LAUNCH_CHECK();
+  return true;
 }
 
 __global__ void k_gather_partition(const float* __restrict__ X, int d, const int32_t* __restrict__ members, int64_t n,

@@ -520,3 +520,29 @@ def test_wide_beam_queries_match_the_oracle(cid, div, knn, beam):
     with pytest.raises(mk.MaskError):
         idx.query(t(Q), knn=knn, beam=257)
     idx.free()
+
+
+@pytest.mark.parametrize("cid,div,nq,knn,beam", [(3, 256, 1024, 10, 64), (3, 256, 8192, 10, 8), (2, 64, 2048, 10, 32),
+                                                 (5, 2048, 1024, 5, 100), (3, 4096, 700, 32, 97)])
+def test_leaf_grouped_queries_match_the_oracle(monkeypatch, cid, div, nq, knn, beam):
+    """Large batches (nq x beam >= 65,536, or forced) take the leaf-grouped path: descent ->
+    (query, leaf) pairs sorted by leaf -> each leaf's rows staged once for all its queries ->
+    per-query merge.  Same result lists as the oracle's descent, and the same ids as the
+    per-query kernel wherever the oracle's k-th/(k+1)-th gap is clear."""
+    cfg = datagen.CONFIGS[cid].scaled(div)
+    X = datagen.data(cfg)
+    idx = mk.build(t(X), cfg.levels, 6, datagen.all_init_indices(cfg))
+    Q = datagen.queries(cfg, count=nq)
+    monkeypatch.setenv("MASK_QUERY_GROUPED", "1")
+    _query_parity(idx, X, Q, cfg.levels, knn=knn, beam=beam)
+    g_ids, g_d2 = idx.query(t(Q), knn=knn, beam=beam)
+    monkeypatch.setenv("MASK_QUERY_GROUPED", "0")
+    p_ids, p_d2 = idx.query(t(Q), knn=knn, beam=beam)
+    g_ids, p_ids = g_ids.cpu().numpy(), p_ids.cpu().numpy()
+    g_d2, p_d2 = g_d2.cpu().numpy(), p_d2.cpu().numpy()
+    fin = np.isfinite(p_d2)
+    np.testing.assert_array_equal(np.isfinite(g_d2), fin)
+    np.testing.assert_allclose(g_d2[fin], p_d2[fin], rtol=1e-5, atol=1e-6)
+    same = (g_ids == p_ids).all(1)
+    assert same.mean() > 0.99, f"{(~same).sum()} queries differ between the grouped and per-query paths"
+    idx.free()

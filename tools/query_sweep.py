@@ -27,6 +27,8 @@ def main():
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--sample", type=int, default=500)
     ap.add_argument("--beams", default="1,2,4,8,16,32")
+    ap.add_argument("--iters", type=int, default=0, help="Lloyd iterations (0: the config's)")
+    ap.add_argument("--modes", default="auto", help="MASK_QUERY_GROUPED values to compare, e.g. 0,1")
     a = ap.parse_args()
     cfg = datagen.CONFIGS[a.config]
     X = datagen.data(cfg)
@@ -35,7 +37,7 @@ def main():
     Xd = torch.from_numpy(X).to(dev)
     Qd = torch.from_numpy(Q).to(dev)
     t0 = time.time()
-    idx = mk.build(Xd, cfg.levels, cfg.iters, datagen.all_init_indices(cfg), flags=mk.MASK_BORROW_DATA)
+    idx = mk.build(Xd, cfg.levels, a.iters or cfg.iters, datagen.all_init_indices(cfg), flags=mk.MASK_BORROW_DATA)
     torch.cuda.synchronize()
     print(f"{cfg.name}: build {time.time() - t0:.2f} s", file=sys.stderr, flush=True)
     t0 = time.time()
@@ -43,19 +45,29 @@ def main():
     print(f"exact k-NN of {a.sample} queries on the host: {time.time() - t0:.1f} s", file=sys.stderr, flush=True)
     st = torch.cuda.current_stream(dev)
     for b in [int(x) for x in a.beams.split(",")]:
-        ms = []
-        for _ in range(6):
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(st)
-            ids, d2 = idx.query(Qd, knn=cfg.knn, beam=b, stream=st)
-            e1.record(st)
-            torch.cuda.synchronize()
-            ms.append(e0.elapsed_time(e1))
-        t = statistics.median(ms[1:])
-        rec = oracle.recall(ids[:a.sample].cpu().numpy(), eids)
-        print(json.dumps({"workload": cfg.name, "queries": int(Q.shape[0]), "knn": cfg.knn, "beam": b,
-                          "query_ms": t, "qps": Q.shape[0] / (t / 1e3), "recall": rec,
-                          "recall_sample": a.sample}), flush=True)
+        first = None
+        for mode in a.modes.split(","):
+            if mode == "auto":
+                os.environ.pop("MASK_QUERY_GROUPED", None)
+            else:
+                os.environ["MASK_QUERY_GROUPED"] = mode
+            ms = []
+            for _ in range(6):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(st)
+                ids, d2 = idx.query(Qd, knn=cfg.knn, beam=b, stream=st)
+                e1.record(st)
+                torch.cuda.synchronize()
+                ms.append(e0.elapsed_time(e1))
+            t = statistics.median(ms[1:])
+            rec = oracle.recall(ids[:a.sample].cpu().numpy(), eids)
+            h = ids.cpu().numpy()
+            agree = None if first is None else float((h == first).all(1).mean())
+            first = h if first is None else first
+            print(json.dumps({"workload": cfg.name, "queries": int(Q.shape[0]), "knn": cfg.knn, "beam": b,
+                              "grouped": mode, "query_ms": t, "qps": Q.shape[0] / (t / 1e3), "recall": rec,
+                              "recall_sample": a.sample, "ids_agree_with_first_mode": agree}), flush=True)
+        os.environ.pop("MASK_QUERY_GROUPED", None)
     idx.free()
 
 
