@@ -268,6 +268,8 @@ struct QIndex {
   // leaf-grouped queries: when set, the descent writes each query's selected level-1
   // prototypes (beam entries, -1 padded) here and skips the leaf scan
   int32_t* sel_out = nullptr;
+  // with sel_out: the level (index into lv) whose selection is handed over (0: level 1)
+  int sel_stop = 0;
 };
 // Leaf-grouped batched k-NN (dense, partition-ordered rows): descent -> (query, leaf) pairs
 // grouped by leaf -> every leaf's rows staged in shared memory once for all its queries ->

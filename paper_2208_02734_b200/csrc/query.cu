@@ -12,6 +12,7 @@
 // Distances are FP32 direct sums of squares.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <cstdlib>
 
@@ -80,8 +81,9 @@ struct WarpTopK {
     const int32_t ki = __shfl_sync(FULL, id, K - 1);
     unsigned m = __ballot_sync(FULL, key_lt(cd, cid, kd, ki));
     if (!m) return;
-    if (__popc(m) <= 4) {
+    if (__popc(m) <= 8) {
       // few entrants (the common case once the list has warmed up): insert them one at a time
+      // (up to 8: ~20 instructions each against ~250 for the sort + merge below)
       // (shift the entries above each one's rank up by a lane; lane 31 drops out).  Keeps the
       // same invariant as the sort + merge below: lanes < K hold the best K keys offered.
       do {
@@ -100,6 +102,11 @@ struct WarpTopK {
       return;
     }
     warp_sort32(cd, cid, lane);
+    if (__shfl_sync(FULL, id, 0) == PAD_ID) {  // empty list: the sorted chunk is the list
+      d = cd;
+      id = cid;
+      return;
+    }
     const float rd = __shfl_sync(FULL, cd, 31 - lane);
     const int32_t ri = __shfl_sync(FULL, cid, 31 - lane);
     if (key_lt(rd, ri, d, id)) {
@@ -359,7 +366,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
       }
     }
     // ---- levels L-1 .. 1: children of the kept prototypes
-    for (int l = qi.L - 2; l >= 0; --l) {
+    for (int l = qi.L - 2; l >= (qi.sel_out ? qi.sel_stop : 0); --l) {
       const QLevel& up = qi.lv[l + 1];
       const QLevel& L = qi.lv[l];
       const float sel_d = top.d;
@@ -538,7 +545,7 @@ __global__ void __launch_bounds__(kWideWarps * 32)
         cur.offer(coop_dist<1>(q, L.P, d, cid, lane), cid, lane);
       }
     }
-    for (int l = qi.L - 2; l >= 0; --l) {  // children of the kept prototypes
+    for (int l = qi.L - 2; l >= (qi.sel_out ? qi.sel_stop : 0); --l) {  // children of the kept prototypes
       const QLevel& up = qi.lv[l + 1];
       const QLevel& L = qi.lv[l];
       nxt.reset(beam);
@@ -623,6 +630,7 @@ __global__ void __launch_bounds__(kWideWarps * 32)
 //     the segment's queries past it (q broadcast from shared memory);
 //   k_merge_partials: warp per query, the beam partial lists -> the final top-k.
 constexpr int kLeafPG = 16;
+constexpr int kChildPG = 32;  // pairs per work item of the grouped level-1 step
 constexpr int kLeafWarps = 4;
 
 __global__ void k_pair_hist(const int32_t* __restrict__ sel, int64_t m, int32_t* __restrict__ cnt) {
@@ -771,6 +779,250 @@ __global__ void k_merge_partials(const int32_t* __restrict__ sel, const int32_t*
   }
 }
 
+// ---------------------------------------------------------------------------------------
+// Grouped descent step into level 1 (wide beams).  The per-query descent stops one level above
+// (sel_stop = 1) and hands over each query's selected level-2 prototypes; the (query, parent)
+// pairs are grouped by parent, a warp per work item holds 32 of the parent's children (rows of
+// the child-ordered copy Pc) in registers and streams the item's queries past them, writing
+// every child's distance to the pair's slice of a candidate buffer (offsets = exclusive scan of
+// the children counts, so a query's candidates are contiguous); a warp per query then selects
+// its top-beam from them (same (d^2, id) order as the per-query kernel).
+constexpr int kScanB = 1024;
+
+// counts[e] = children of the pair's parent (0 for a padded slot); block-local exclusive scan
+__global__ void __launch_bounds__(kScanB) k_cand_scan1(const int32_t* __restrict__ sel, const int64_t* __restrict__ up_off,
+                                                       int64_t m, int64_t* __restrict__ coff, int64_t* __restrict__ bsum) {
+  __shared__ int64_t wsum[32];
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const int64_t e = (int64_t)blockIdx.x * kScanB + t;
+  int64_t c = 0;
+  if (e < m) {
+    const int32_t p = sel[e];
+    c = p >= 0 ? up_off[p + 1] - up_off[p] : 0;
+  }
+  int64_t x = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int64_t y = __shfl_up_sync(FULL, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wsum[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    int64_t v = wsum[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t y = __shfl_up_sync(FULL, v, o);
+      if (lane >= o) v += y;
+    }
+    wsum[lane] = v;
+  }
+  __syncthreads();
+  const int64_t excl = x - c + (w ? wsum[w - 1] : 0);
+  if (e < m) coff[e] = excl;
+  if (t == kScanB - 1) bsum[blockIdx.x] = wsum[31];
+}
+// single block: exclusive scan of the block sums in place, total at bsum[nb]
+__global__ void __launch_bounds__(1024) k_cand_scan2(int64_t* __restrict__ bsum, int64_t nb) {
+  __shared__ int64_t part[1024];
+  const int t = threadIdx.x;
+  const int64_t per = (nb + blockDim.x - 1) / blockDim.x;
+  const int64_t a = t * per, b = min64(nb, a + per);
+  int64_t s = 0;
+  for (int64_t j = a; j < b; ++j) s += bsum[j];
+  part[t] = s;
+  __syncthreads();
+  for (int o = 1; o < (int)blockDim.x; o <<= 1) {
+    const int64_t v = t >= o ? part[t - o] : 0;
+    __syncthreads();
+    part[t] += v;
+    __syncthreads();
+  }
+  int64_t run = part[t] - s;
+  for (int64_t j = a; j < b; ++j) {
+    const int64_t c = bsum[j];
+    bsum[j] = run;
+    run += c;
+  }
+  if (t == blockDim.x - 1) bsum[nb] = part[t];
+}
+__global__ void k_cand_scan3(int64_t* __restrict__ coff, int64_t m, const int64_t* __restrict__ bsum) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e <= m; e += (int64_t)gridDim.x * blockDim.x)
+    coff[e] = e < m ? coff[e] + bsum[e / kScanB] : bsum[(m + kScanB - 1) / kScanB];
+}
+
+template <int D4M>
+__global__ void __launch_bounds__(kLeafWarps * 32)
+    k_child_dist(QIndex qi, int lvl, const float* __restrict__ Q, const int32_t* __restrict__ sel,
+                 const int64_t* __restrict__ pairs, const int64_t* __restrict__ poff, int64_t kp, int beam,
+                 const int64_t* __restrict__ coff, int* __restrict__ queue, float* __restrict__ cand_d,
+                 int32_t* __restrict__ cand_id) {
+  extern __shared__ __align__(16) float4 csm4[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int d = qi.dim, d4 = d >> 2;
+  float4* qs = csm4 + (size_t)w * (kChildPG * D4M + kChildPG / 2);  // [kChildPG][D4M] queries
+  int64_t* co = reinterpret_cast<int64_t*>(qs + kChildPG * D4M);      // [kChildPG] candidate offsets
+  const QLevel& L = qi.lv[lvl];
+  const QLevel& up = qi.lv[lvl + 1];
+  const float4* Pc4 = reinterpret_cast<const float4*>(L.Pc);
+  const int64_t npairs = poff[kp];
+  const int64_t nitems = (npairs + kChildPG - 1) / kChildPG;
+  for (;;) {
+    int item = 0;
+    if (lane == 0) item = atomicAdd(queue, 1);
+    item = __shfl_sync(FULL, item, 0);
+    if (item >= nitems) break;
+    const int64_t i1 = min64(npairs, (int64_t)(item + 1) * kChildPG);
+    for (int64_t s0 = (int64_t)item * kChildPG; s0 < i1;) {
+      const int32_t p = sel[pairs[s0]];
+      const int64_t s1 = min64(i1, poff[p + 1]);
+      const int np = (int)(s1 - s0);
+      __syncwarp();
+      for (int j = 0; j < np; ++j) {
+        const int64_t e = pairs[s0 + j];
+        const float4* q4 = reinterpret_cast<const float4*>(Q + (e / beam) * d);
+        for (int f = lane; f < D4M; f += 32) qs[j * D4M + f] = f < d4 ? q4[f] : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      if (lane < np) co[lane] = coff[pairs[s0 + lane]];
+      __syncwarp();
+      const int64_t m0 = up.offsets[p], m1 = up.offsets[p + 1];
+      for (int64_t c = m0; c < m1; c += 32) {
+        const int64_t r = c + lane;
+        int32_t cid = PAD_ID;
+        if (r < m1) {
+          const int32_t j = up.members[r];
+          if (has_children(L, j)) cid = j;
+        }
+        float4 x[D4M];
+#pragma unroll
+        for (int f = 0; f < D4M; ++f)
+          x[f] = (r < m1 && f < d4) ? __ldg(Pc4 + r * d4 + f) : make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int j = 0; j < np; ++j) {
+          const float4* qj = qs + j * D4M;
+          float a0 = 0.f, a1 = 0.f;
+#pragma unroll
+          for (int f = 0; f < D4M; ++f) {
+            const float4 qv = qj[f];
+            float t = qv.x - x[f].x;
+            a0 = fmaf(t, t, a0);
+            t = qv.y - x[f].y;
+            a1 = fmaf(t, t, a1);
+            t = qv.z - x[f].z;
+            a0 = fmaf(t, t, a0);
+            t = qv.w - x[f].w;
+            a1 = fmaf(t, t, a1);
+          }
+          if (r < m1) {
+            const int64_t o = co[j] + (r - m0);
+            cand_d[o] = cid == PAD_ID ? INFINITY : a0 + a1;
+            cand_id[o] = cid;
+          }
+        }
+      }
+      s0 = s1;
+    }
+  }
+}
+
+// warp per query: top-beam of its candidates [coff[q beam], coff[(q + 1) beam]) -> sel_out
+__global__ void __launch_bounds__(kWideWarps * 32)
+    k_select_cands(const int64_t* __restrict__ coff, const float* __restrict__ cand_d,
+                   const int32_t* __restrict__ cand_id, int64_t nq, int beam, int32_t* __restrict__ sel_out) {
+  extern __shared__ __align__(16) float ssm[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t nwarps = (int64_t)gridDim.x * kWideWarps;
+  float* base = ssm + (size_t)w * (4 * kMaxWideBeam + 64);
+  SmemTopK cur;
+  cur.d = base;
+  cur.id = reinterpret_cast<int32_t*>(cur.d + kMaxWideBeam);
+  cur.td = reinterpret_cast<float*>(cur.id + kMaxWideBeam);
+  cur.tid = reinterpret_cast<int32_t*>(cur.td + kMaxWideBeam);
+  cur.cd = reinterpret_cast<float*>(cur.tid + kMaxWideBeam);
+  cur.cid = reinterpret_cast<int32_t*>(cur.cd + 32);
+  for (int64_t q = (int64_t)blockIdx.x * kWideWarps + w; q < nq; q += nwarps) {
+    const int64_t a = coff[q * beam], b = coff[(q + 1) * beam];
+    if (beam <= 32) {
+      WarpTopK top;
+      top.reset(beam);
+      for (int64_t c = a; c < b; c += 32) {
+        const int64_t o = c + lane;
+        top.offer(o < b ? cand_d[o] : INFINITY, o < b ? cand_id[o] : PAD_ID, lane);
+      }
+      if (lane < beam) sel_out[q * beam + lane] = top.id == PAD_ID ? -1 : top.id;
+    } else {
+      __syncwarp();
+      cur.reset(beam);
+      for (int64_t c = a; c < b; c += 32) {
+        const int64_t o = c + lane;
+        cur.offer(o < b ? cand_d[o] : INFINITY, o < b ? cand_id[o] : PAD_ID, lane);
+      }
+      for (int s2 = lane; s2 < beam; s2 += 32) sel_out[q * beam + s2] = s2 < cur.n ? cur.id[s2] : -1;
+    }
+  }
+}
+
+// The grouped step into level 1: fills sel (nq x beam level-1 prototype ids, -1 padded).
+// Returns false (nothing launched) when the index has no level above 1 or no child-ordered copy.
+static bool grouped_level1_selection(const QIndex& qi, const float* Q, int64_t nq, int beam, int32_t* sel,
+                                     cudaStream_t st) {
+  if (qi.L < 2 || !qi.lv[0].Pc) return false;
+  const int d = qi.dim, d4 = d >> 2;
+  const int d4m = d4 <= 4 ? 4 : d4 <= 8 ? 8 : d4 <= 16 ? 16 : 32;
+  const int64_t m = nq * (int64_t)beam;
+  const int64_t k2 = qi.lv[1].k;
+  DevBuf<int32_t> sel2(m), cnt(k2), queue(1);
+  DevBuf<int64_t> poff(k2 + 1), pairs(m), coff(m + 1);
+  const int64_t nb = (m + kScanB - 1) / kScanB;
+  DevBuf<int64_t> bsum(nb + 1);
+  QIndex q2 = qi;
+  q2.sel_out = sel2.p;
+  q2.sel_stop = 1;
+  launch_query_dense(q2, Q, nq, 1, beam, nullptr, nullptr, st, false);  // descent down to level 2
+  // pairs grouped by parent
+  MASK_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(int32_t) * k2, st));
+  k_pair_hist<<<grid_for(m, 256), 256, 0, st>>>(sel2.p, m, cnt.p);
+  MASK_LAUNCH_CHECK();
+  k_pair_scan<<<1, 1024, 0, st>>>(cnt.p, k2, poff.p);
+  MASK_LAUNCH_CHECK();
+  k_pair_scatter<<<grid_for(m, 256), 256, 0, st>>>(sel2.p, m, cnt.p, pairs.p);
+  MASK_LAUNCH_CHECK();
+  // candidate offsets
+  k_cand_scan1<<<(unsigned)nb, kScanB, 0, st>>>(sel2.p, qi.lv[1].offsets, m, coff.p, bsum.p);
+  MASK_LAUNCH_CHECK();
+  k_cand_scan2<<<1, 1024, 0, st>>>(bsum.p, nb);
+  MASK_LAUNCH_CHECK();
+  k_cand_scan3<<<grid_for(m + 1, 256), 256, 0, st>>>(coff.p, m, bsum.p);
+  MASK_LAUNCH_CHECK();
+  int64_t ncand = 0;
+  MASK_CUDA(cudaMemcpyAsync(&ncand, coff.p + m, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  MASK_CUDA(cudaStreamSynchronize(st));
+  DevBuf<float> cd(std::max<int64_t>(ncand, 1));
+  DevBuf<int32_t> cid(std::max<int64_t>(ncand, 1));
+  MASK_CUDA(cudaMemsetAsync(queue.p, 0, sizeof(int), st));
+  const size_t smem = (size_t)kLeafWarps * (kChildPG * d4m + kChildPG / 2) * sizeof(float4);
+  const unsigned g = (unsigned)num_sms() * 8;
+  switch (d4m) {
+#define MASK_CD(D)                                                                                            \
+  case D:                                                                                                     \
+    MASK_CUDA(cudaFuncSetAttribute(k_child_dist<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+    k_child_dist<D><<<g, kLeafWarps * 32, smem, st>>>(qi, 0, Q, sel2.p, pairs.p, poff.p, k2, beam, coff.p,   \
+                                                      queue.p, cd.p, cid.p);                                  \
+    break;
+    MASK_CD(4)
+    MASK_CD(8)
+    MASK_CD(16)
+    MASK_CD(32)
+#undef MASK_CD
+  }
+  MASK_LAUNCH_CHECK();
+  const size_t ssmem = (size_t)kWideWarps * (4 * kMaxWideBeam + 64) * sizeof(float);
+  const unsigned sg = (unsigned)std::min<int64_t>((nq + kWideWarps - 1) / kWideWarps, (int64_t)num_sms() * 32);
+  k_select_cands<<<sg, kWideWarps * 32, ssmem, st>>>(coff.p, cd.p, cid.p, nq, beam, sel);
+  MASK_LAUNCH_CHECK();
+  MASK_CUDA(cudaStreamSynchronize(st));  // (the scratch above is released at return)
+  return true;
+}
+
 bool launch_query_grouped(const QIndex& qi, const float* Q, int64_t nq, int knn, int beam, int64_t* ids, float* d2,
                           cudaStream_t st) {
   // MASK_QUERY_GROUPED=0 / 1: never / always (A/B and tests; read per call)
@@ -789,9 +1041,14 @@ bool launch_query_grouped(const QIndex& qi, const float* Q, int64_t nq, int knn,
   DevBuf<int32_t> sel(m), cnt(k1), pid((size_t)m * knn), queue(1);
   DevBuf<int64_t> off(k1 + 1), pairs(m);
   DevBuf<float> pd((size_t)m * knn);
-  QIndex q2 = qi;
-  q2.sel_out = sel.p;
-  launch_query_dense(q2, Q, nq, knn, beam, ids, d2, st, false);  // descent only
+  // MASK_GROUPED_LEVEL=0/1 overrides the grouped step into level 1 (default: beams >= 2)
+  const char* glenv = getenv("MASK_GROUPED_LEVEL");
+  const bool glevel = glenv ? atoi(glenv) != 0 : beam >= 2;
+  if (!(glevel && grouped_level1_selection(qi, Q, nq, beam, sel.p, st))) {
+    QIndex q2 = qi;
+    q2.sel_out = sel.p;
+    launch_query_dense(q2, Q, nq, knn, beam, ids, d2, st, false);  // descent only
+  }
   MASK_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(int32_t) * k1, st));
   k_pair_hist<<<grid_for(m, 256), 256, 0, st>>>(sel.p, m, cnt.p);
   MASK_LAUNCH_CHECK();

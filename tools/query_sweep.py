@@ -47,9 +47,12 @@ def main():
     for b in [int(x) for x in a.beams.split(",")]:
         first = None
         for mode in a.modes.split(","):
-            if mode == "auto":
-                os.environ.pop("MASK_QUERY_GROUPED", None)
-            else:
+            os.environ.pop("MASK_QUERY_GROUPED", None)
+            os.environ.pop("MASK_GROUPED_LEVEL", None)
+            if mode.startswith("g"):  # g0 / g1: grouped leaf scan without / with the grouped level-1 step
+                os.environ["MASK_QUERY_GROUPED"] = "1"
+                os.environ["MASK_GROUPED_LEVEL"] = mode[1]
+            elif mode != "auto":
                 os.environ["MASK_QUERY_GROUPED"] = mode
             ms = []
             for _ in range(6):
@@ -68,6 +71,7 @@ def main():
                               "grouped": mode, "query_ms": t, "qps": Q.shape[0] / (t / 1e3), "recall": rec,
                               "recall_sample": a.sample, "ids_agree_with_first_mode": agree}), flush=True)
         os.environ.pop("MASK_QUERY_GROUPED", None)
+        os.environ.pop("MASK_GROUPED_LEVEL", None)
     idx.free()
 
 
