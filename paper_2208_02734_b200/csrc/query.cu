@@ -883,7 +883,7 @@ __global__ void __launch_bounds__(kLeafWarps * 32)
         const float4* q4 = reinterpret_cast<const float4*>(Q + (e / beam) * d);
         for (int f = lane; f < D4M; f += 32) qs[j * D4M + f] = f < d4 ? q4[f] : make_float4(0.f, 0.f, 0.f, 0.f);
       }
-      if (lane < np) co[lane] = coff[pairs[s0 + lane]];
+      for (int j = lane; j < np; j += 32) co[j] = coff[pairs[s0 + j]];
       __syncwarp();
       const int64_t m0 = up.offsets[p], m1 = up.offsets[p + 1];
       for (int64_t c = m0; c < m1; c += 32) {
