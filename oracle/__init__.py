@@ -85,6 +85,9 @@ def lib():
             L.orc_lloyd_trace.restype = C.c_int
             L.orc_lloyd_trace.argtypes = [C.c_int64, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p] + \
                 lloyd_args + [dp, i32p]
+            L.orc_lloyd_ex.restype = C.c_int
+            L.orc_lloyd_ex.argtypes = [C.c_int64, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p] + \
+                lloyd_args + [C.c_void_p, C.c_void_p, C.c_int]
             _lib = L
         return _lib
 
@@ -204,13 +207,18 @@ class LevelResult:
         self.passes = passes  # trace=True: [(P_t used by pass t, labels_t), ...] incl. the final pass
 
 
-def lloyd(Y, init_idx, T: int, tol: float = 0.0, csr_dim: Optional[int] = None, trace: bool = False) -> LevelResult:
+EMPTY_POLICIES = {"keep": 0, "farthest": 1}
+
+
+def lloyd(Y, init_idx, T: int, tol: float = 0.0, csr_dim: Optional[int] = None, trace: bool = False,
+          empty: str = "keep") -> LevelResult:
     """One level: Lloyd from Y[init_idx], T iterations, then a final assignment.
 
     trace=True also records, per assignment pass, the prototypes it used and its labels
-    (an output copy only: the arithmetic is the same code path)."""
-    if trace:
-        return _lloyd_trace(Y, init_idx, T, tol, csr_dim)
+    (an output copy only: the arithmetic is the same code path).  empty: "keep" (D5) or
+    "farthest" (D5b: emptied prototypes re-seeded at the pass's farthest rows)."""
+    if trace or empty != "keep":
+        return _lloyd_trace(Y, init_idx, T, tol, csr_dim, EMPTY_POLICIES[empty], trace)
     init_idx = np.ascontiguousarray(init_idx, np.int64)
     k = init_idx.size
     J = np.zeros(T + 1, np.float64)
@@ -231,7 +239,7 @@ def lloyd(Y, init_idx, T: int, tol: float = 0.0, csr_dim: Optional[int] = None, 
     return LevelResult(P, lab, J[:passes], ch[:passes], upd.value)
 
 
-def _lloyd_trace(Y, init_idx, T, tol, csr_dim):
+def _lloyd_trace(Y, init_idx, T, tol, csr_dim, policy=0, record=True):
     init_idx = np.ascontiguousarray(init_idx, np.int64)
     k = init_idx.size
     J = np.zeros(T + 1, np.float64)
@@ -249,11 +257,12 @@ def _lloyd_trace(Y, init_idx, T, tol, csr_dim):
         keep = (rp, col, val)
     P = np.empty((k, d), np.float64)
     lab = np.empty(n, np.int32)
-    Pp = np.empty((T + 1, k, d), np.float64)
-    Lp = np.empty((T + 1, max(n, 1)), np.int32)
-    passes = lib().orc_lloyd_trace(n, d, *args, k, init_idx, T, tol, P, lab, J, ch, C.byref(upd), Pp, Lp)
+    Pp = np.empty((T + 1, k, d), np.float64) if record else None
+    Lp = np.empty((T + 1, max(n, 1)), np.int32) if record else None
+    passes = lib().orc_lloyd_ex(n, d, *args, k, init_idx, T, tol, P, lab, J, ch, C.byref(upd),
+                                Pp.ctypes.data if record else None, Lp.ctypes.data if record else None, policy)
     del keep
-    seq = [(Pp[t], Lp[t, :n]) for t in range(passes)]
+    seq = [(Pp[t], Lp[t, :n]) for t in range(passes)] if record else None
     return LevelResult(P, lab, J[:passes], ch[:passes], upd.value, passes=seq)
 
 
@@ -282,13 +291,13 @@ class Index:
 
 
 def build_index(X, init_idx: Sequence[np.ndarray], T: int, tol: float = 0.0, csr_dim: Optional[int] = None,
-                trace: bool = False) -> Index:
+                trace: bool = False, empty: str = "keep") -> Index:
     """Bottom-up levels: level 1 clusters X, level l+1 clusters P_l (D1, D6)."""
     levels, offs, mems = [], [], []
     Y = X
     dim = csr_dim
     for l, idx in enumerate(init_idx):
-        res = lloyd(Y, idx, T, tol, csr_dim=csr_dim if l == 0 else None, trace=trace)
+        res = lloyd(Y, idx, T, tol, csr_dim=csr_dim if l == 0 else None, trace=trace, empty=empty)
         levels.append(res)
         o, m = children(res.labels, res.P.shape[0])
         offs.append(o)

@@ -17,7 +17,8 @@
  *     `kmeans.labels`; Lloyd cited P:176/P:293): assignment to the nearest
  *     prototype (`searchPosMin`; ties -> lowest ordinal, D4) then every
  *     prototype becomes the mean of its members (P:536 centroids minimise the sum
- *     of squared distances); an empty cluster keeps its prototype (D5);
+ *     of squared distances); an empty cluster keeps its prototype (D5), or -- the
+ *     SPEC option S:128 -- is re-seeded at the farthest row of the pass (D5b);
  *   - levels: the prototypes of level l are the points clustered at level l+1
  *     (Algorithm 1), one global k-means per level (D1);
  *   - query: descend from the top level choosing the nearest child(ren) of the
@@ -38,6 +39,8 @@
  */
 #include <math.h>
 #include <stdint.h>
+
+enum { ORC_EMPTY_KEEP = 0, ORC_EMPTY_FARTHEST = 1 };
 #include <stdlib.h>
 #include <string.h>
 
@@ -210,6 +213,57 @@ double orc_means_from_sums(int64_t k, int d, const double* S, const int64_t* cou
 
 /* ------------------------------------------------------------------ Lloyd */
 
+/* Empty-cluster repair, SPEC S:128 ("an emptied centroid is re-seeded at the point with the
+ * largest distance to its current centroid"; reading D5b): the m prototypes that
+ * this update leaves without members, taken in ascending j, are set to the m rows with the
+ * largest dist(Y_i, P_t[a_i]) of the pass (best[i]), ordered by (distance descending, i
+ * ascending), one row each; every other prototype keeps its member mean.  Returns the
+ * largest displacement of a re-seeded prototype (for the tolerance stop, D3). */
+typedef struct {
+  double d2;
+  int64_t i;
+} far_t;
+
+static int far_cmp(const void* pa, const void* pb) {
+  const far_t* a = (const far_t*)pa;
+  const far_t* b = (const far_t*)pb;
+  if (a->d2 > b->d2) return -1; /* larger distance first */
+  if (a->d2 < b->d2) return 1;
+  return (a->i > b->i) - (a->i < b->i); /* then lower row index */
+}
+
+static double reseed_farthest(int64_t n, int d, const double* Y, const int64_t* row_ptr,
+                              const int32_t* col, const double* val, int64_t k,
+                              const int64_t* counts, const double* best, const double* P_old,
+                              double* P_new) {
+  int64_t m = 0;
+  for (int64_t j = 0; j < k; ++j) m += counts[j] == 0;
+  if (m == 0 || n == 0) return 0.0;
+  far_t* order = (far_t*)malloc(sizeof(far_t) * (size_t)n);
+  for (int64_t i = 0; i < n; ++i) {
+    order[i].d2 = best[i];
+    order[i].i = i;
+  }
+  qsort(order, (size_t)n, sizeof(far_t), far_cmp);
+  double maxdisp = 0.0;
+  int64_t r = 0;
+  for (int64_t j = 0; j < k && r < n; ++j) {
+    if (counts[j] != 0) continue;
+    const int64_t row = order[r++].i;
+    double* c = P_new + j * d;
+    if (Y) {
+      memcpy(c, Y + row * (int64_t)d, sizeof(double) * (size_t)d);
+    } else {
+      memset(c, 0, sizeof(double) * (size_t)d);
+      for (int64_t p = row_ptr[row]; p < row_ptr[row + 1]; ++p) c[col[p]] = val[p];
+    }
+    double disp = sqrt(orc_dist2(d, c, P_old + j * d));
+    if (disp > maxdisp) maxdisp = disp;
+  }
+  free(order);
+  return maxdisp;
+}
+
 /* One level of the index: Lloyd k-means from the seeded init rows (D2), following the
  * pseudo-code of DESIGN.md "Oracle" step by step:
  *
@@ -229,7 +283,7 @@ static int lloyd_impl(int64_t n, int d, const double* Y, const int64_t* row_ptr,
                       const int32_t* col, const double* val, int64_t k,
                       const int64_t* init_idx, int T, double tol, double* P_out,
                       int32_t* labels_out, double* J_trace, int64_t* changed_trace,
-                      int* updates_run, double* P_pass, int32_t* lab_pass) {
+                      int* updates_run, double* P_pass, int32_t* lab_pass, int empty_policy) {
   double* P = P_out;
   double* P_new = (double*)malloc(sizeof(double) * (size_t)(k * d));
   double* S = (double*)malloc(sizeof(double) * (size_t)(k * d));
@@ -269,6 +323,10 @@ static int lloyd_impl(int64_t n, int d, const double* Y, const int64_t* row_ptr,
     if (Y) orc_cluster_sums(n, d, Y, a, k, S, counts);
     else orc_cluster_sums_csr(n, d, row_ptr, col, val, a, k, S, counts);
     double maxdisp = orc_means_from_sums(k, d, S, counts, P, P_new);
+    if (empty_policy == ORC_EMPTY_FARTHEST) {
+      double rd = reseed_farthest(n, d, Y, row_ptr, col, val, k, counts, best, P, P_new);
+      if (rd > maxdisp) maxdisp = rd;
+    }
     memcpy(P, P_new, sizeof(double) * (size_t)(k * d));
     ++updates;
     memcpy(prev, a, sizeof(int32_t) * (size_t)n);
@@ -305,7 +363,7 @@ int orc_lloyd(int64_t n, int d, const double* Y, int64_t k, const int64_t* init_
               double tol, double* P_out, int32_t* labels_out, double* J_trace,
               int64_t* changed_trace, int* updates_run) {
   return lloyd_impl(n, d, Y, NULL, NULL, NULL, k, init_idx, T, tol, P_out, labels_out, J_trace,
-                    changed_trace, updates_run, NULL, NULL);
+                    changed_trace, updates_run, NULL, NULL, ORC_EMPTY_KEEP);
 }
 
 /* orc_lloyd / orc_lloyd_csr with a per-pass record: P_pass ((T+1) x k x d) receives the
@@ -316,7 +374,17 @@ int orc_lloyd_trace(int64_t n, int d, const double* Y, const int64_t* row_ptr, c
                     double* P_out, int32_t* labels_out, double* J_trace, int64_t* changed_trace,
                     int* updates_run, double* P_pass, int32_t* lab_pass) {
   return lloyd_impl(n, d, Y, row_ptr, col, val, k, init_idx, T, tol, P_out, labels_out, J_trace,
-                    changed_trace, updates_run, P_pass, lab_pass);
+                    changed_trace, updates_run, P_pass, lab_pass, ORC_EMPTY_KEEP);
+}
+
+/* orc_lloyd_trace with an empty-cluster policy (ORC_EMPTY_KEEP = 0: D5; ORC_EMPTY_FARTHEST = 1:
+ * D5b).  Y dense or (row_ptr, col, val) CSR; P_pass / lab_pass may be NULL. */
+int orc_lloyd_ex(int64_t n, int d, const double* Y, const int64_t* row_ptr, const int32_t* col,
+                 const double* val, int64_t k, const int64_t* init_idx, int T, double tol,
+                 double* P_out, int32_t* labels_out, double* J_trace, int64_t* changed_trace,
+                 int* updates_run, double* P_pass, int32_t* lab_pass, int empty_policy) {
+  return lloyd_impl(n, d, Y, row_ptr, col, val, k, init_idx, T, tol, P_out, labels_out, J_trace,
+                    changed_trace, updates_run, P_pass, lab_pass, empty_policy);
 }
 
 int orc_lloyd_csr(int64_t n, int d, const int64_t* row_ptr, const int32_t* col,
@@ -324,7 +392,7 @@ int orc_lloyd_csr(int64_t n, int d, const int64_t* row_ptr, const int32_t* col,
                   double* P_out, int32_t* labels_out, double* J_trace, int64_t* changed_trace,
                   int* updates_run) {
   return lloyd_impl(n, d, NULL, row_ptr, col, val, k, init_idx, T, tol, P_out, labels_out,
-                    J_trace, changed_trace, updates_run, NULL, NULL);
+                    J_trace, changed_trace, updates_run, NULL, NULL, ORC_EMPTY_KEEP);
 }
 
 /* ------------------------------------------------------------------ query */

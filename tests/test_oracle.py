@@ -763,3 +763,66 @@ def test_exhaustive_error_hand_derived_and_identity():
     Xr = datagen.blobs(21, 300, 4, 5)
     ident = oracle.build_index(Xr, [np.arange(300), np.arange(300)], 3)
     assert oracle.exhaustive_error(ident, Xr) == 0.0
+
+
+# ---------------------------------------------------------------- empty-cluster repair (D5b)
+def test_lloyd_farthest_reseed_worked_example():
+    """SPEC S:128 reading D5b, derived by hand.  Y = (0,0), (0,0), (1,0), (10,0), init rows
+    {0, 1}: both prototypes (0,0), every row ties -> prototype 0 (D4), prototype 1 is empty.
+    Pass 0: J0 = 0 + 0 + 1 + 100 = 101; P0 <- mean of all = (2.75, 0); the farthest row from its
+    prototype is row 3 (d = 100) -> P1 <- (10, 0).  Pass 1: rows 0-2 -> 0 (7.5625, 7.5625,
+    3.0625), row 3 -> 1 (0): J1 = 18.1875; P0 <- (1/3, 0).  Pass 2: no label change -> stop.
+    Final J = 2/9 + 4/9 = 2/3.  Under "keep" prototype 1 stays at (0,0) and wins rows 0-2 in
+    pass 1 instead."""
+    Y = np.array([[0, 0], [0, 0], [1, 0], [10, 0]], np.float64)
+    r = oracle.lloyd(Y, np.array([0, 1]), 10, empty="farthest")
+    np.testing.assert_allclose(r.P, [[1 / 3, 0], [10, 0]], rtol=0, atol=1e-15)
+    np.testing.assert_array_equal(r.labels, [0, 0, 0, 1])
+    np.testing.assert_allclose(r.J, [101.0, 18.1875, 2 / 3, 2 / 3], rtol=1e-15)
+    assert r.updates == 2
+    keep = oracle.lloyd(Y, np.array([0, 1]), 10)
+    assert not np.allclose(keep.P, r.P)
+    # keep: pass 1 puts rows 0-2 on the unmoved prototype 1 at (0,0) (0, 0, 1 against 7.5625,
+    # 7.5625, 3.0625) and row 3 on prototype 0
+    np.testing.assert_array_equal(oracle.lloyd(Y, np.array([0, 1]), 1).labels, [1, 1, 1, 0])
+
+
+def test_lloyd_farthest_reseed_order_and_ties():
+    """Several empty prototypes take the farthest rows in ascending j; equal distances go to
+    the lower row index.  Y = (0,0) x3, (1,0), (7,0), (-9,0), init rows {0, 1, 2}: all rows ->
+    prototype 0, prototypes 1 and 2 empty; farthest (d desc): row 5 (81), row 4 (49) ->
+    P1 = (-9,0), P2 = (7,0).  Ties: Y = (0,0), (0,0), (-5,0), (5,0), init {0, 1}: rows 2 and 3
+    are both at 25 -> row 2 (lower index) -> P1 = (-5,0); pass 1 moves row 3 nowhere (25/9 vs
+    100) and P0 <- (5/3, 0)."""
+    Y = np.array([[0, 0], [0, 0], [0, 0], [1, 0], [7, 0], [-9, 0]], np.float64)
+    r = oracle.lloyd(Y, np.array([0, 1, 2]), 1, empty="farthest", trace=True)
+    P1 = r.passes[1][0]  # the prototypes the final pass used = after the one update
+    # P0 = mean of all six rows = (-1/6, 0); the two empties take rows 5 and 4
+    np.testing.assert_allclose(P1, [[-1 / 6, 0], [-9, 0], [7, 0]], rtol=0, atol=1e-15)
+    Y2 = np.array([[0, 0], [0, 0], [-5, 0], [5, 0]], np.float64)
+    r2 = oracle.lloyd(Y2, np.array([0, 1]), 10, empty="farthest")
+    np.testing.assert_allclose(r2.P, [[5 / 3, 0], [-5, 0]], rtol=0, atol=1e-15)
+    np.testing.assert_array_equal(r2.labels, [0, 0, 1, 0])
+
+
+def test_lloyd_farthest_csr_equals_dense_and_no_empty_is_keep():
+    """The CSR path re-seeds with the densified row; without empty clusters the policy does
+    not change the trajectory."""
+    rng = np.random.default_rng(5)
+    D = np.where(rng.random((300, 40)) < 0.2, rng.random((300, 40)), 0.0)
+    D[:40] = D[0]  # 40 identical rows: an init on them leaves empty clusters
+    init = np.arange(12)
+    rp = np.concatenate([[0], np.cumsum((D != 0).sum(1))]).astype(np.int64)
+    col = np.nonzero(D)[1].astype(np.int32)
+    val = D[D != 0].astype(np.float32).astype(np.float64)
+    D = np.zeros_like(D)
+    for i in range(D.shape[0]):
+        D[i, col[rp[i]:rp[i + 1]]] = val[rp[i]:rp[i + 1]]
+    a = oracle.lloyd(D, init, 8, empty="farthest")
+    b = oracle.lloyd((rp, col, val), init, 8, csr_dim=40, empty="farthest")
+    np.testing.assert_allclose(a.P, b.P, rtol=1e-12, atol=1e-12)
+    np.testing.assert_array_equal(a.labels, b.labels)
+    assert not np.allclose(a.P, oracle.lloyd(D, init, 8).P)  # the repair did change the run
+    Y = rng.standard_normal((500, 3))
+    init2 = rng.choice(500, 8, replace=False)
+    np.testing.assert_array_equal(oracle.lloyd(Y, init2, 6, empty="farthest").P, oracle.lloyd(Y, init2, 6).P)
