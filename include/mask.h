@@ -53,8 +53,14 @@ typedef enum {
 enum { MASK_DENSE_F32 = 0, MASK_CSR_F32 = 1 };
 /* mask_matrix.memory */
 enum { MASK_MEM_DEVICE = 0, MASK_MEM_HOST = 1 };
-/* mask_build_params.empty_policy (D5) */
-enum { MASK_EMPTY_KEEP = 0 };
+/* mask_build_params.empty_policy.  KEEP (D5, default): a prototype without members keeps its
+ * position.  FARTHEST (D5b, "an emptied centroid is re-seeded at the point with the
+ * largest distance to its current centroid"): after each update the m prototypes left empty,
+ * in ascending index, move to the m rows with the largest distance to their prototype in that
+ * pass (distance descending, then lower row index); the other prototypes keep their member
+ * means.  FARTHEST runs the per-pass loop (no fused small levels), synchronises once per pass
+ * to read the empty count, and is single-GPU (MASK_ERR_UNSUPPORTED with a multi-rank comm). */
+enum { MASK_EMPTY_KEEP = 0, MASK_EMPTY_FARTHEST = 1 };
 /* mask_build_params.flags */
 enum {
   MASK_VALIDATE_FINITE = 1 << 0, /* scan inputs for NaN/Inf -> MASK_ERR_NONFINITE          */
@@ -123,7 +129,7 @@ typedef struct {
   const int64_t* const* init_idx; /* host, optional; init_idx[l] = k[l] distinct indices
                                      into the level-l input (global row ids for level 1)
                                      (D2); NULL -> drawn from `seed`                       */
-  int32_t empty_policy;           /* MASK_EMPTY_KEEP                                       */
+  int32_t empty_policy;           /* MASK_EMPTY_KEEP (default) or MASK_EMPTY_FARTHEST        */
   int32_t flags;                  /* MASK_* flags above                                    */
   mask_iter_cb iter_cb;           /* NULL in production                                    */
   void* iter_cb_user;

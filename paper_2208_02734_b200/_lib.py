@@ -25,6 +25,7 @@ STATUS = {
 MASK_DENSE_F32, MASK_CSR_F32 = 0, 1
 MASK_MEM_DEVICE, MASK_MEM_HOST = 0, 1
 MASK_EMPTY_KEEP = 0
+MASK_EMPTY_FARTHEST = 1
 MASK_VALIDATE_FINITE = 1 << 0
 MASK_BORROW_DATA = 1 << 1
 MASK_FORCE_SIMT = 1 << 2

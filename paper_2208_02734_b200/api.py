@@ -384,12 +384,14 @@ def kernel_launches() -> int:
 
 def build(data, levels: Sequence[int], iters: int, init_idx: Optional[Sequence[np.ndarray]] = None,
           tol: float = 0.0, flags: int = 0, comm: Optional[Comm] = None, iter_cb: Optional[Callable] = None,
-          stream=None, n_global: Optional[int] = None, row_offset: int = 0, seed: int = 0) -> Index:
+          stream=None, n_global: Optional[int] = None, row_offset: int = 0, seed: int = 0,
+          empty: str = "keep") -> Index:
     """mask_build: multilevel index over ``data`` (this rank's shard when ``comm`` is given).
 
     init_idx: one array of distinct indices per level, or None to let the library draw them
     from ``seed`` (mask_seeded_init).  iter_cb(level, pass, P (k x dim float32 numpy), labels
-    (int32 numpy)) is the test-only step-parity hook."""
+    (int32 numpy)) is the test-only step-parity hook.  empty: "keep" (D5) or "farthest" (D5b,
+    SPEC S:128: emptied prototypes re-seeded at the pass's farthest rows)."""
     m, keep = matrix(data, n_global=n_global, row_offset=row_offset)
     L = len(levels)
     ks = (C.c_int64 * L)(*[int(k) for k in levels])
@@ -407,7 +409,7 @@ def build(data, levels: Sequence[int], iters: int, init_idx: Optional[Sequence[n
     p.seed = int(seed) & 0xFFFFFFFFFFFFFFFF
     if ptrs is not None:
         p.init_idx = ptrs
-    p.empty_policy = _lib.MASK_EMPTY_KEEP
+    p.empty_policy = {"keep": _lib.MASK_EMPTY_KEEP, "farthest": _lib.MASK_EMPTY_FARTHEST}[empty]
     p.flags = int(flags)
     cb_ref = None
     if iter_cb is not None:

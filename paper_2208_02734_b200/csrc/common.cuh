@@ -154,6 +154,11 @@ void launch_update_dense64(const float* X, int64_t n, int d, const int32_t* labe
                            cudaStream_t st, const int* active, const int32_t* perm);
 void launch_f32_to_f64(const float* a, int64_t n, double* b, cudaStream_t st);
 // FP64 sums over label-sorted rows without atomics (warp per cluster; end = the sort's end offsets)
+// D5b: re-seed the prototypes this update left empty at the pass's farthest rows
+// (dense X or CSR rp/col/val); single rank; synchronises the stream (rare-path option).
+void reseed_farthest(const float* X, const int64_t* rp, const int32_t* col, const float* val, int d, int64_t n,
+                     int64_t k, const float* best, const int32_t* counts, float* P, double* P64, uint32_t* stat,
+                     const int* active, cudaStream_t st);
 bool update_seg64_supported(int d);
 void launch_update_seg64(const float* X, int d, const int32_t* perm, const int32_t* labels, const int32_t* end,
                          int64_t n, double* S, int32_t* counts, cudaStream_t st, const int* active);

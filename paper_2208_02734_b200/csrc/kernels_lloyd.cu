@@ -19,7 +19,9 @@
 #include <mutex>
 
 #include <cfloat>
+#include <algorithm>
 #include <cstdint>
+#include <vector>
 
 #include "common.cuh"
 
@@ -1414,6 +1416,173 @@ void launch_finalize64(double* P64, float* P, double* S, int32_t* counts, int64_
                        cudaStream_t st, const int* active, LoopCtl lc) {
   k_finalize64<<<grid_for(k * 32, 256), 256, 0, st>>>(P64, P, S, counts, k, d, stat, active, lc);
   MASK_LAUNCH_CHECK();
+}
+
+// ====================================================================== D5b farthest-point repair
+// SPEC S:128 (reading D5b): the prototypes an update leaves without members, in ascending j,
+// are re-seeded at the rows with the largest distance to their prototype in this pass (best[],
+// the assignment's d^2), ordered by (distance descending, row ascending).  Runs between the
+// update and K7 (which keeps counts == 0 prototypes as they are), so only the re-seeded rows
+// are written here; their displacement joins K7's maximum for the tolerance stop.
+//
+// Ordered compaction of the empty prototypes (single block): emp[0..m) ascending, m_out[0] = m
+// (0 when the level already stopped: active == 0).
+__global__ void __launch_bounds__(1024) k_empty_list(const int32_t* __restrict__ counts, int64_t k,
+                                                     int32_t* __restrict__ emp, int* __restrict__ m_out,
+                                                     const int* __restrict__ active) {
+  __shared__ int part[1024];
+  const int t = threadIdx.x;
+  const bool on = !active || *active;
+  const int64_t per = (k + blockDim.x - 1) / blockDim.x;
+  const int64_t a = t * per, b = a + per < k ? a + per : k;
+  int c = 0;
+  if (on)
+    for (int64_t j = a; j < b; ++j) c += counts[j] == 0;
+  part[t] = c;
+  __syncthreads();
+  for (int o = 1; o < (int)blockDim.x; o <<= 1) {
+    const int v = t >= o ? part[t - o] : 0;
+    __syncthreads();
+    part[t] += v;
+    __syncthreads();
+  }
+  int w = part[t] - c;
+  if (on)
+    for (int64_t j = a; j < b; ++j)
+      if (counts[j] == 0) emp[w++] = (int32_t)j;
+  if (t == blockDim.x - 1) m_out[0] = part[t];
+}
+
+// number of rows whose d^2 (non-negative float, ordered as its bit pattern) is >= thr
+__global__ void k_count_ge(const float* __restrict__ best, int64_t n, uint32_t thr,
+                           unsigned long long* __restrict__ cnt) {
+  unsigned long long c = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    c += __float_as_uint(best[i]) >= thr;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(cnt, c);
+}
+
+__global__ void k_collect_ge(const float* __restrict__ best, int64_t n, uint32_t thr, int64_t* __restrict__ rows,
+                             uint32_t* __restrict__ keys, unsigned long long* __restrict__ cnt, int64_t cap) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t b = __float_as_uint(best[i]);
+    if (b >= thr) {
+      const unsigned long long at = atomicAdd(cnt, 1ull);
+      if ((int64_t)at < cap) {
+        rows[at] = i;
+        keys[at] = b;
+      }
+    }
+  }
+}
+
+// block per re-seeded prototype: P_j <- row (densified for CSR), P64_j likewise; the squared
+// displacement (against the FP64 prototype when there is one) into stat[0] (float bits, max)
+__global__ void __launch_bounds__(256) k_reseed(const float* __restrict__ X, const int64_t* __restrict__ rp,
+                                                const int32_t* __restrict__ col, const float* __restrict__ val,
+                                                int d, const int64_t* __restrict__ rows,
+                                                const int32_t* __restrict__ emp, float* __restrict__ P,
+                                                double* __restrict__ P64, uint32_t* __restrict__ stat) {
+  const int64_t j = emp[blockIdx.x], row = rows[blockIdx.x];
+  double acc = 0.0;
+  if (X) {
+    for (int c = threadIdx.x; c < d; c += blockDim.x) {
+      const float v = X[row * d + c];
+      const double old = P64 ? P64[j * d + c] : (double)P[j * d + c];
+      const double t = (double)v - old;
+      acc += t * t;
+      P[j * d + c] = v;
+      if (P64) P64[j * d + c] = (double)v;
+    }
+  } else {
+    // ||new - old||^2 = sum_c old_c^2 + sum_{nz} ((v - old_c)^2 - old_c^2), before overwriting
+    for (int c = threadIdx.x; c < d; c += blockDim.x) {
+      const double old = (double)P[j * d + c];
+      acc += old * old;
+    }
+    for (int64_t p = rp[row] + threadIdx.x; p < rp[row + 1]; p += blockDim.x) {
+      const double old = (double)P[j * d + col[p]];
+      const double t = (double)val[p] - old;
+      acc += t * t - old * old;
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < d; c += blockDim.x) P[j * d + c] = 0.f;
+    __syncthreads();
+    for (int64_t p = rp[row] + threadIdx.x; p < rp[row + 1]; p += blockDim.x) P[j * d + col[p]] = val[p];
+  }
+  __shared__ double red[8];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s2 = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s2 += red[w];
+    atomicMax(stat, __float_as_uint((float)(s2 > 0.0 ? s2 : 0.0)));
+  }
+}
+
+void reseed_farthest(const float* X, const int64_t* rp, const int32_t* col, const float* val, int d, int64_t n,
+                     int64_t k, const float* best, const int32_t* counts, float* P, double* P64, uint32_t* stat,
+                     const int* active, cudaStream_t st) {
+  if (n <= 0 || k <= 0) return;
+  DevBuf<int32_t> emp(k);
+  DevBuf<int> m_d(1);
+  k_empty_list<<<1, 1024, 0, st>>>(counts, k, emp.p, m_d.p, active);
+  MASK_LAUNCH_CHECK();
+  int m = 0;
+  MASK_CUDA(cudaMemcpyAsync(&m, m_d.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  MASK_CUDA(cudaStreamSynchronize(st));
+  if (m <= 0) return;
+  if (m > n) m = (int)n;
+  // the m-th largest key: largest thr with count(key >= thr) >= m (bisection on the bits)
+  DevBuf<unsigned long long> cnt(1);
+  auto count_ge = [&](uint32_t thr) {
+    MASK_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(unsigned long long), st));
+    k_count_ge<<<grid_for(n, 256, (int64_t)num_sms() * 8), 256, 0, st>>>(best, n, thr, cnt.p);
+    MASK_LAUNCH_CHECK();
+    unsigned long long h = 0;
+    MASK_CUDA(cudaMemcpyAsync(&h, cnt.p, sizeof(h), cudaMemcpyDeviceToHost, st));
+    MASK_CUDA(cudaStreamSynchronize(st));
+    return h;
+  };
+  uint32_t lo = 0, hi = 0x7f800001u;  // count(>= lo) = n >= m; count(>= hi) = 0 (finite d^2)
+  unsigned long long c_lo = (unsigned long long)n;
+  while (hi - lo > 1) {
+    const uint32_t mid = lo + (hi - lo) / 2;
+    const unsigned long long c = count_ge(mid);
+    if (c >= (unsigned long long)m) {
+      lo = mid;
+      c_lo = c;
+    } else {
+      hi = mid;
+    }
+  }
+  DevBuf<int64_t> rows(c_lo);
+  DevBuf<uint32_t> keys(c_lo);
+  MASK_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(unsigned long long), st));
+  k_collect_ge<<<grid_for(n, 256, (int64_t)num_sms() * 8), 256, 0, st>>>(best, n, lo, rows.p, keys.p, cnt.p,
+                                                                          (int64_t)c_lo);
+  MASK_LAUNCH_CHECK();
+  std::vector<int64_t> hr(c_lo);
+  std::vector<uint32_t> hk(c_lo);
+  MASK_CUDA(cudaMemcpyAsync(hr.data(), rows.p, sizeof(int64_t) * c_lo, cudaMemcpyDeviceToHost, st));
+  MASK_CUDA(cudaMemcpyAsync(hk.data(), keys.p, sizeof(uint32_t) * c_lo, cudaMemcpyDeviceToHost, st));
+  MASK_CUDA(cudaStreamSynchronize(st));
+  std::vector<size_t> ord(c_lo);
+  for (size_t i = 0; i < ord.size(); ++i) ord[i] = i;
+  std::sort(ord.begin(), ord.end(), [&](size_t a, size_t b) {
+    return hk[a] != hk[b] ? hk[a] > hk[b] : hr[a] < hr[b];  // distance descending, row ascending
+  });
+  std::vector<int64_t> far(m);
+  for (int r = 0; r < m; ++r) far[r] = hr[ord[r]];
+  DevBuf<int64_t> far_d(m);
+  MASK_CUDA(cudaMemcpyAsync(far_d.p, far.data(), sizeof(int64_t) * m, cudaMemcpyHostToDevice, st));
+  k_reseed<<<(unsigned)m, 256, 0, st>>>(X, rp, col, val, d, far_d.p, emp.p, P, P64, stat);
+  MASK_LAUNCH_CHECK();
+  MASK_CUDA(cudaStreamSynchronize(st));  // (host vectors and scratch go out of scope)
 }
 
 __global__ void k_f32_to_f64(const float* __restrict__ a, int64_t n, double* __restrict__ b) {

@@ -692,8 +692,9 @@ void run_level(const Input& in, int64_t k, const int64_t* init_idx_host, const m
   ws.best.alloc(std::max<int64_t>(n, 1));
   // dense levels run by the per-pass kernels keep FP64 prototypes and sums (D15): the K4
   // decisions and the update then follow the oracle's FP64 arithmetic; fp32 P is their rounding
+  const bool farthest = p->empty_policy == MASK_EMPTY_FARTHEST;
   const bool fused_level = in.format == MASK_DENSE_F32 && !comm && !p->iter_cb && !(p->flags & MASK_FORCE_SIMT) &&
-                           !(p->flags & MASK_NO_FUSED) && small_level_supported(n, d, k);
+                           !(p->flags & MASK_NO_FUSED) && !farthest && small_level_supported(n, d, k);
   const bool p64 = in.format == MASK_DENSE_F32 && !fused_level;
   if (p64) {
     ws.P64.alloc((size_t)k * d);
@@ -866,6 +867,9 @@ void run_level(const Input& in, int64_t k, const int64_t* init_idx_host, const m
     // the combined statistics decide the no-change stop identically on every rank (the update
     // of a pass that changed no label is then not applied: K7 is skipped, as in the oracle)
     if (comm) combine(t, t, true, active);
+    if (farthest)  // D5b: between the update (counts) and K7 (which keeps the re-seeded rows)
+      reseed_farthest(in.format == MASK_DENSE_F32 ? in.X : nullptr, in.rp, in.col, in.val, d, n, k, ws.best.p,
+                      ws.counts.p, L.P.p, p64 ? ws.P64.p : nullptr, fin.p + 2 * t, active, st);
     if (ev) ev->mark(MASK_T_FINALIZE, st);
     LoopCtl lf = lc;
     lf.ctrl = ctrl.p;  // tolerance stop / pass count (fin is identical on every rank)
@@ -1035,7 +1039,10 @@ void build_impl(const mask_matrix* data, const mask_build_params* p, mask_comm* 
   MASK_REQUIRE(p->max_iters >= 0, MASK_ERR_ARG, "max_iters must be >= 0");
   MASK_REQUIRE(p->tol >= 0.0, MASK_ERR_ARG, "tol must be >= 0");
   MASK_REQUIRE(p->k != nullptr, MASK_ERR_ARG, "k is NULL");
-  MASK_REQUIRE(p->empty_policy == MASK_EMPTY_KEEP, MASK_ERR_UNSUPPORTED, "only MASK_EMPTY_KEEP");
+  MASK_REQUIRE(p->empty_policy == MASK_EMPTY_KEEP || p->empty_policy == MASK_EMPTY_FARTHEST, MASK_ERR_ARG,
+               "empty_policy must be MASK_EMPTY_KEEP or MASK_EMPTY_FARTHEST");
+  MASK_REQUIRE(p->empty_policy == MASK_EMPTY_KEEP || !comm || comm->world == 1, MASK_ERR_UNSUPPORTED,
+               "MASK_EMPTY_FARTHEST is single-GPU (the farthest rows would need a cross-rank selection)");
   const int world = comm ? comm->world : 1;
   const int rank = comm ? comm->rank : 0;
   if (!comm) {

@@ -89,6 +89,12 @@ def _worker(rank, world, port, out_dir, cid, div, T, sparse_ok):
             out["mismatch"] = "no error"
         except mk.MaskError as e:
             out["mismatch"] = str(e)
+        # the farthest-point empty repair is single-GPU: MASK_ERR_UNSUPPORTED on every rank
+        try:
+            mk.build(data, cfg.levels, T, inits, comm=comm, n_global=cfg.n, row_offset=lo, empty="farthest")
+            out["farthest"] = "no error"
+        except mk.MaskError as e:
+            out["farthest"] = str(e)
         np.savez(os.path.join(out_dir, f"r{rank}.npz"), **out)
     finally:
         comm.free()
@@ -159,3 +165,4 @@ def test_sharded_build_two_ranks(tmp_path, cid, div, T):
         check_queries(ids, d2, rids, rd2, gap, what=f"{cfg.name} 2-rank queries")
     for r in res:
         assert "MASK_ERR_ARG" in str(r["mismatch"]) and "disagree" in str(r["mismatch"])
+        assert "MASK_ERR_UNSUPPORTED" in str(r["farthest"])

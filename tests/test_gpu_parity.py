@@ -552,3 +552,57 @@ def test_leaf_grouped_queries_match_the_oracle(monkeypatch, cid, div, nq, knn, b
         same = (g_ids == p_ids).all(1)
         assert same.mean() > 0.99, f"gl={gl}: {(~same).sum()} queries differ between grouped and per-query"
     idx.free()
+
+
+def _dup_data(seed, n, d, ndup, copies):
+    """Rows 0 .. ndup*copies-1 are `copies` copies of `ndup` points (so an init on the first
+    rows holds duplicate prototypes and leaves clusters empty), the rest Gaussian."""
+    rng = np.random.default_rng(seed)
+    X = rng.standard_normal((n, d)).astype(np.float32)
+    base = rng.standard_normal((ndup, d)).astype(np.float32)
+    X[:ndup * copies] = np.repeat(base, copies, axis=0)
+    return X
+
+
+@pytest.mark.parametrize("d,k,extra", [(16, 64, 0), (64, 96, 0), (64, 96, mk.MASK_FORCE_SIMT), (3, 40, 0)])
+def test_empty_farthest_reseed_trajectory(d, k, extra):
+    """MASK_EMPTY_FARTHEST (D5b) on data whose init leaves prototypes empty: the
+    production build's level-1 trajectory against the oracle's with the same policy (every
+    pass's prototypes, so every re-seed's rows, within 1e-4; tie-window rule of D15)."""
+    from parity import check_trajectory
+    X = _dup_data(700 + d, 6000, d, 30, 8)
+    init = [np.arange(k, dtype=np.int64), datagen.init_indices(701, 2, k, 8)]
+    idx = mk.build(t(X), [k, 8], 12, init, flags=mk.MASK_BORROW_DATA | mk.MASK_TRACE_PASSES | extra,
+                   empty="farthest")
+    ref = oracle.lloyd(X.astype(np.float64), init[0], 12, trace=True, empty="farthest")
+    assert (np.bincount(ref.passes[0][1], minlength=k) == 0).sum() > 0  # the repair did run
+    check_trajectory(X.astype(np.float64), idx.passes(1), ref.passes, what=f"farthest d={d}")
+    keep = oracle.lloyd(X.astype(np.float64), init[0], 12)
+    assert rel_l2(idx.prototypes(1), keep.P) > 1e-3  # differs from the keep policy's run
+    idx.free()
+
+
+def test_empty_farthest_reseed_csr():
+    """The CSR path re-seeds with densified rows (K6 update, K3 assignment)."""
+    from parity import check_trajectory
+    rp, col, val = datagen.random_csr(720, 4000, 300, 12)
+    # unit rows are all at d^2 ~ 2 from prototypes they share no column with: scale each row so
+    # the farthest-row order is decided well outside the 1e-5 tie window (D5b reading)
+    scale = np.random.default_rng(721).uniform(0.5, 2.0, 4000).astype(np.float32)
+    val = (val * np.repeat(scale, np.diff(rp))).astype(np.float32)
+    # rows 0..159: 8 copies of rows 0..19
+    dense_rows = []
+    for i in range(20):
+        dense_rows.append((col[rp[i]:rp[i + 1]], val[rp[i]:rp[i + 1]]))
+    rows = [dense_rows[i // 8] for i in range(160)] + [(col[rp[i]:rp[i + 1]], val[rp[i]:rp[i + 1]])
+                                                       for i in range(160, 4000)]
+    rp2 = np.concatenate([[0], np.cumsum([len(c) for c, _ in rows])]).astype(np.int64)
+    col2 = np.concatenate([c for c, _ in rows]).astype(np.int32)
+    val2 = np.concatenate([v for _, v in rows]).astype(np.float32)
+    k = 48
+    init = [np.arange(k, dtype=np.int64)]
+    idx = mk.build(_csr_dev(rp2, col2, val2, 300), [k], 10, init, flags=mk.MASK_TRACE_PASSES, empty="farthest")
+    ref = oracle.lloyd((rp2, col2, val2), init[0], 10, csr_dim=300, trace=True, empty="farthest")
+    assert (np.bincount(ref.passes[0][1], minlength=k) == 0).sum() > 0
+    check_trajectory((rp2, col2, val2), idx.passes(1), ref.passes, csr_dim=300, what="farthest CSR")
+    idx.free()
