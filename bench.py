@@ -54,6 +54,10 @@ def parse():
     ap.add_argument("--force-comm", action="store_true",
                     help="build through an NCCL communicator even on one rank (exercises the multi-GPU path)")
     ap.add_argument("--no-sweep", action="store_true", help="skip the QPS@recall beam sweep")
+    ap.add_argument("--seed", type=int, default=0, help="data / query / init streams (0 = the documented ones)")
+    ap.add_argument("--tol", type=float, default=0.0, help="Lloyd tolerance stop on max displacement (D3; 0 = off)")
+    ap.add_argument("--empty", default="keep", choices=["keep", "farthest"],
+                    help="empty-cluster policy (D5 keep / D5b farthest, single GPU)")
     return ap.parse_args()
 
 
@@ -210,9 +214,12 @@ def run_reference(args, rank, world):
     import oracle
 
     cfg = datagen.CONFIGS[args.config]
+    if args.seed:
+        import dataclasses
+        cfg = dataclasses.replace(cfg, seed=args.seed)
     k = cfg.levels[0]
     X_all = datagen.data(cfg) if cfg.sparse else datagen.data(cfg, 0, cfg.n)
-    P = _init_protos(cfg, X_all, datagen.init_indices(cfg.cid, 1, cfg.n, k))
+    P = _init_protos(cfg, X_all, datagen.init_indices(cfg.cid, 1, cfg.n, k, cfg.seed))
     cores = oracle.num_threads()
     # rows per step: ~3 s of one oracle Lloyd pass (assignment + update) on the box's cores
     rows = min(cfg.n, 4096)
@@ -328,11 +335,12 @@ def main():
         comm = mk.Comm.from_process_group()
 
     cfg = datagen.CONFIGS[args.config]
-    if args.knn is not None or args.iters is not None:  # optional overrides, reported in `config`
+    if args.knn is not None or args.iters is not None or args.seed:  # overrides, reported in `config`
         import dataclasses
         cfg = dataclasses.replace(cfg, knn=args.knn if args.knn is not None else cfg.knn,
-                                  iters=args.iters if args.iters is not None else cfg.iters)
+                                  iters=args.iters if args.iters is not None else cfg.iters, seed=args.seed)
     beam = args.beam
+    bkw = {"tol": args.tol, "empty": args.empty}  # harness flags (defaults = the configs' runs)
     # strong scaling: rank r owns rows [lo, hi) of the config's block-seeded generator
     lo, hi = mk.row_range(cfg.n, world, rank)
     n_local = hi - lo
@@ -369,7 +377,7 @@ def main():
             torch.empty((nq_local, cfg.knn), dtype=torch.float32, device=dev))  # result buffers, reused
 
     def step():
-        idx = mk.build(X, cfg.levels, cfg.iters, inits, flags=flags, comm=comm, n_global=n_global,
+        idx = mk.build(X, cfg.levels, cfg.iters, inits, **bkw, flags=flags, comm=comm, n_global=n_global,
                        row_offset=lo, stream=stream)
         ids, d2 = idx.query(Q, knn=cfg.knn, beam=beam, stream=stream, out=qout)
         return idx, ids, d2
@@ -401,7 +409,7 @@ def main():
         e1 = torch.cuda.Event(enable_timing=True)
         e2 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        idx = mk.build(X, cfg.levels, cfg.iters, inits, flags=flags, comm=comm, n_global=n_global,
+        idx = mk.build(X, cfg.levels, cfg.iters, inits, **bkw, flags=flags, comm=comm, n_global=n_global,
                        row_offset=lo, stream=stream)
         e1.record(stream)
         ids, d2 = idx.query(Q, knn=cfg.knn, beam=beam, stream=stream, out=qout)
@@ -423,7 +431,7 @@ def main():
         sampler.stop()
     # update kernel (K5/K6) times: two extra builds with every kernel class timed (untimed region)
     for _ in range(2):
-        idx_u = mk.build(X, cfg.levels, cfg.iters, inits, flags=(flags & ~mk.MASK_TIME_ASSIGN) | mk.MASK_TIME_KERNELS,
+        idx_u = mk.build(X, cfg.levels, cfg.iters, inits, **bkw, flags=(flags & ~mk.MASK_TIME_ASSIGN) | mk.MASK_TIME_KERNELS,
                          comm=comm, n_global=n_global, row_offset=lo, stream=stream)
         tu = idx_u.timing(1)
         kt["update"] += tu["update"]["ms"]
@@ -549,7 +557,7 @@ def main():
             flush.zero_()
             barrier()
             t0 = time.perf_counter()
-            idx_h = mk.build(Xp, cfg.levels, cfg.iters, inits, comm=comm, n_global=n_global, row_offset=lo,
+            idx_h = mk.build(Xp, cfg.levels, cfg.iters, inits, **bkw, comm=comm, n_global=n_global, row_offset=lo,
                              stream=stream)
             ids_h, d2_h = idx_h.query(Qp, knn=cfg.knn, beam=beam, stream=stream)
             torch.cuda.synchronize(dev)
@@ -588,7 +596,8 @@ def main():
             "config": {"workload": cfg.name, "n_per_gpu": n_local, "n_global": n_global, "dim": cfg.dim,
                        "levels": list(cfg.levels), "iters": cfg.iters, "queries": cfg.n_queries,
                        "knn": cfg.knn, "beam": beam, "parallelism": f"dp{world}" if world > 1 else "single",
-                       "l2": "flushed between timed steps (512 MiB write)"},
+                       "l2": "flushed between timed steps (512 MiB write)",
+                       "seed": args.seed, "tol": args.tol, "empty": args.empty},
             "per_level_distances": per_level, "build_ms": build_mean,
             "query_ms": query_mean, "query_qps": cfg.n_queries / (query_mean / 1000.0),
             "recall_at_k_sample": recall, "qps_at_recall": qps_at_recall, "roofline": roof, "update_roofline": upd,

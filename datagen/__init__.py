@@ -9,7 +9,8 @@ neighbour list.
 
 Recipe:
 
-* seeds: data = 1000+c, queries = 2000+c, init = 3000+c (c = config number);
+* seeds: data = 1000+c, queries = 2000+c, init = 3000+c (c = config number), each plus
+  100,000 s for the harness's ``--seed s`` (s = 0: the documented streams);
 * rows are generated in whole blocks of 2**14; block b draws from
   ``SeedSequence([seed, b])`` so any GPU count / shard sees identical rows;
 * mixture parameters (centres, scales, covariances, weights, the C4 column
@@ -49,6 +50,11 @@ class Config:
     n_queries: int
     knn: int
     sparse: bool = False
+    seed: int = 0  # harness --seed: 0 = the documented streams; s > 0 offsets every base seed by 100,000 s
+
+    @property
+    def seed_base(self) -> int:
+        return 100_000 * self.seed
 
     def scaled(self, div: int, min_k: int = 2) -> "Config":
         """Scaled-down replica: same generator and d, N and every k_l divided by ``div``."""
@@ -203,17 +209,17 @@ def _rows(cfg: Config, seed: int, n: int, start: int = 0):
 
 def _fill_blocks(args):
     """Worker of data_parallel: whole blocks [b0, b1) into the shared output array."""
-    name, shape, cid, b0, b1, n = args
+    name, shape, cid, b0, b1, n, seed = args
     from multiprocessing import shared_memory
 
-    cfg = CONFIGS[cid]
+    cfg = dataclasses.replace(CONFIGS[cid], seed=seed)
     shm = shared_memory.SharedMemory(name=name)
     try:
         out = np.ndarray(shape, dtype=np.float32, buffer=shm.buf)
-        params = _mixture_params(cfg, 1000 + cid)
+        params = _mixture_params(cfg, 1000 + cid + cfg.seed_base)
         for b in range(b0, b1):
             lo, hi = b * BLOCK_ROWS, min((b + 1) * BLOCK_ROWS, n)
-            out[lo:hi] = _dense_block(cfg, params, 1000 + cid, b, BLOCK_ROWS)[: hi - lo]
+            out[lo:hi] = _dense_block(cfg, params, 1000 + cid + cfg.seed_base, b, BLOCK_ROWS)[: hi - lo]
     finally:
         shm.close()
     return b1 - b0
@@ -234,7 +240,7 @@ def data_parallel(cfg: Config, workers: Optional[int] = None):
     nb = (n + BLOCK_ROWS - 1) // BLOCK_ROWS
     workers = workers or os.cpu_count() or 1
     step = max(1, (nb + 4 * workers - 1) // (4 * workers))
-    jobs = [(shm.name, shape, cfg.cid, b, min(b + step, nb), n) for b in range(0, nb, step)]
+    jobs = [(shm.name, shape, cfg.cid, b, min(b + step, nb), n, cfg.seed) for b in range(0, nb, step)]
     with mp.get_context("fork").Pool(workers) as pool:
         done = sum(pool.map(_fill_blocks, jobs))
     assert done == nb
@@ -268,20 +274,20 @@ def gaussian_clouds(seed: int, per_cloud: int, radius: float, sigma: float = 1.0
 def data(cfg: Config, start: int = 0, count: Optional[int] = None):
     """Rows [start, start+count) of config ``cfg``'s dataset (dense fp32 n x d, or CSR triple)."""
     count = cfg.n - start if count is None else count
-    return _rows(cfg, 1000 + cfg.cid, count, start)
+    return _rows(cfg, 1000 + cfg.cid + cfg.seed_base, count, start)
 
 
 def queries(cfg: Config, count: Optional[int] = None):
     """Queries drawn from an independent stream of the same generator."""
     count = cfg.n_queries if count is None else count
-    return _rows(cfg, 2000 + cfg.cid, count, 0)
+    return _rows(cfg, 2000 + cfg.cid + cfg.seed_base, count, 0)
 
 
-def init_indices(cfg_id: int, level: int, n_items: int, k: int) -> np.ndarray:
+def init_indices(cfg_id: int, level: int, n_items: int, k: int, seed: int = 0) -> np.ndarray:
     """k distinct indices in [0, n_items) for level ``level`` (1-based), seeded (D2)."""
     if not (1 <= k <= n_items):
         raise ValueError("need 1 <= k <= n_items")
-    g = _rng(3000 + cfg_id, level)
+    g = _rng(3000 + cfg_id + 100_000 * seed, level)
     return g.choice(n_items, size=k, replace=False).astype(np.int64)
 
 
@@ -289,7 +295,7 @@ def all_init_indices(cfg: Config) -> List[np.ndarray]:
     out = []
     prev = cfg.n
     for l, k in enumerate(cfg.levels, start=1):
-        out.append(init_indices(cfg.cid, l, prev, k))
+        out.append(init_indices(cfg.cid, l, prev, k, cfg.seed))
         prev = k
     return out
 
