@@ -67,7 +67,7 @@ enum {
   MASK_BORROW_DATA = 1 << 1,     /* index keeps a pointer to device `data` instead of a copy */
   MASK_FORCE_SIMT = 1 << 2,      /* dense assignment on the FP32 SIMT kernel only (testing) */
   MASK_NO_FIXUP = 1 << 3,        /* disable the near-tie re-check of the tensor path (testing)*/
-  MASK_SYNC_STATS = 1 << 4,      /* reserved: J/changed are read every pass (always on)       */
+  /* 1 << 4: unused (formerly a per-pass statistics read-back; the loop now reads back once per level) */
   MASK_TIME_KERNELS = 1 << 5,    /* record CUDA-event device times of the step kernels        */
   MASK_NO_SORT = 1 << 6,         /* small d: keep the data order in K1 (no per-pass label sort) */
   MASK_NO_FUSED = 1 << 7,        /* small levels: per-pass kernels instead of the fused loop    */
@@ -219,6 +219,22 @@ typedef struct {
 int32_t mask_grouped_depth(int64_t n, int32_t length_group, int32_t n_centroids, int64_t* layer_k, int32_t cap);
 int32_t mask_build_grouped(const mask_matrix* data, const mask_grouped_params* params, void* stream,
                            mask_index** out);
+
+/* §5.1 relocation step ("reassigned to that partition ... the multilevel index is
+ * built again"; reading G8) for a grouped index `idx` built over the data-layer order
+ * `order_in`, after a beam-1 1-NN point search of every point (`got[i]` = the row mask_query
+ * returned for point i, -1 = none).  A found point (got[i] == i) keeps its data-layer group
+ * (positions of order_in split into floor(n / length_group) balanced groups, the last n mod g
+ * one larger, G1), and so does a point whose search reached no partition; a missed point
+ * targets the group of the partition its search reached (level-1 prototype of got[i] //
+ * n_centroids).  order_out = the points sorted by (target group, keys[i]); keys: distinct
+ * values in [0, 2^32) (the iteration's seeded order keys).  reached_out (optional) = the group
+ * each point's search reached (-1 = none); *misses_out = the number of points not found.
+ * Device arrays of n_items(level 1) entries (int64); returns after the stream completes.
+ * Errors: MASK_ERR_ARG (NULL arguments, n_centroids not dividing the level-1 prototype count). */
+int32_t mask_relocate(const mask_index* idx, const int64_t* got, const int64_t* order_in, const int64_t* keys,
+                      int32_t n_centroids, int64_t* order_out, int64_t* reached_out, int64_t* misses_out,
+                      void* stream);
 
 /* ---------------------------------------------------------------- query
  * Batched approximate k-NN (Algorithm 2) of `queries` (same dim/format family

@@ -30,7 +30,6 @@ MASK_VALIDATE_FINITE = 1 << 0
 MASK_BORROW_DATA = 1 << 1
 MASK_FORCE_SIMT = 1 << 2
 MASK_NO_FIXUP = 1 << 3
-MASK_SYNC_STATS = 1 << 4
 MASK_TIME_KERNELS = 1 << 5
 MASK_NO_SORT = 1 << 6
 MASK_NO_FUSED = 1 << 7
@@ -49,7 +48,7 @@ EXPORTS = [
     "mask_grouped_depth", "mask_build_grouped", "mask_range_query", "mask_insert",
     "mask_top_prototypes", "mask_route", "mask_query_routed", "mask_merge", "mask_collective_count",
     "mask_seeded_init", "mask_debug_fail_alloc", "mask_get_displacement", "mask_get_pass",
-    "mask_comm_init_host", "mask_split",
+    "mask_comm_init_host", "mask_split", "mask_relocate",
 ]
 
 
@@ -157,6 +156,7 @@ def load():
             "mask_get_timing": (i32, [P, i32, P, i32]),
             "mask_grouped_depth": (i32, [i64, i32, i32, P, i32]),
             "mask_build_grouped": (i32, [C.POINTER(MaskMatrix), C.POINTER(MaskGroupedParams), P, C.POINTER(P)]),
+            "mask_relocate": (i32, [P, P, P, P, i32, P, P, C.POINTER(i64), P]),
             "mask_range_query": (i32, [P, C.POINTER(MaskMatrix), P, i32, i64, P, P, P, C.POINTER(i64), P]),
             "mask_insert": (i32, [P, C.POINTER(MaskMatrix), P, P]),
             "mask_top_prototypes": (i32, [P, P, C.POINTER(i64)]),

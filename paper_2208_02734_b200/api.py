@@ -444,6 +444,23 @@ def grouped_depth(n: int, length_group: int, n_centroids: int) -> Tuple[int, Lis
     return depth, [int(out[i]) for i in range(min(depth, cap))]
 
 
+def relocate(index: "Index", got, order, keys, n_centroids: int, stream=None):
+    """mask_relocate (§5.1, reading G8): the next data-layer order of a grouped index from the
+    point-search results ``got`` (device int64, one per point), the current order and the
+    iteration's keys (device int64).  Returns (order_out, reached, misses): device int64
+    tensors and the number of points the search did not return."""
+    n = int(got.shape[0])
+    for a in (got, order, keys):
+        if not (isinstance(a, torch.Tensor) and a.is_cuda and a.dtype == torch.int64 and a.is_contiguous()):
+            raise TypeError("got / order / keys must be contiguous int64 CUDA tensors")
+    out = torch.empty(n, dtype=torch.int64, device=got.device)
+    reached = torch.empty(n, dtype=torch.int64, device=got.device)
+    misses = C.c_int64(0)
+    check(load().mask_relocate(index.handle, _ptr(got), _ptr(order), _ptr(keys), int(n_centroids), _ptr(out),
+                               _ptr(reached), C.byref(misses), _stream(stream)))
+    return out, reached, int(misses.value)
+
+
 def build_grouped(data, length_group: int, n_centroids: int, iters: int, perm: Optional[np.ndarray] = None,
                   flags: int = 0, stream=None) -> Index:
     """mask_build_grouped: the paper's Algorithm 1 (groups of ``length_group`` items, each

@@ -1481,6 +1481,25 @@ int32_t mask_build_grouped(const mask_matrix* data, const mask_grouped_params* p
   return guarded([&] { build_grouped_impl(data, params, as_stream(stream), out); });
 }
 
+int32_t mask_relocate(const mask_index* idx, const int64_t* got, const int64_t* order_in, const int64_t* keys,
+                      int32_t n_centroids, int64_t* order_out, int64_t* reached_out, int64_t* misses_out,
+                      void* stream) {
+  return guarded([&] {
+    MASK_REQUIRE(idx && got && order_in && keys && order_out && misses_out, MASK_ERR_ARG, "NULL argument");
+    MASK_REQUIRE(!idx->levels.empty() && n_centroids >= 1 && idx->levels[0].k % n_centroids == 0, MASK_ERR_ARG,
+                 "n_centroids must divide the level-1 prototype count");
+    cudaStream_t st = as_stream(stream);
+    const int64_t n = idx->levels[0].n_items;
+    const int64_t groups = idx->levels[0].k / n_centroids;
+    DevBuf<unsigned long long> miss(1);
+    launch_relocate(got, order_in, keys, idx->levels[0].labels.p, n, groups, n_centroids, order_out, reached_out,
+                    miss.p, st);
+    unsigned long long h = 0;
+    MASK_CUDA(cudaMemcpy(&h, miss.p, sizeof(h), cudaMemcpyDeviceToHost));
+    *misses_out = (int64_t)h;
+  });
+}
+
 namespace {
 QIndex make_qindex(const mask_index* idx) {
   QIndex qi{};
