@@ -996,6 +996,11 @@ static bool grouped_level1_selection(const QIndex& qi, const float* Q, int64_t n
   int64_t ncand = 0;
   MASK_CUDA(cudaMemcpyAsync(&ncand, coff.p + m, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   MASK_CUDA(cudaStreamSynchronize(st));
+  {  // the candidate buffer (8 B per candidate) must leave room: otherwise the per-query descent
+    size_t free_b = 0, total_b = 0;
+    MASK_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    if ((size_t)ncand * 8 > free_b / 2) return false;
+  }
   DevBuf<float> cd(std::max<int64_t>(ncand, 1));
   DevBuf<int32_t> cid(std::max<int64_t>(ncand, 1));
   MASK_CUDA(cudaMemsetAsync(queue.p, 0, sizeof(int), st));

@@ -37,6 +37,7 @@ def main():
                     help="time one clean build (no step hook, no checks) and the 1e6-query batch")
     ap.add_argument("--recall-sample", type=int, default=20)
     ap.add_argument("--beams", default="1", help="--clean: beam widths of the query batch")
+    ap.add_argument("--modes", default="auto", help="--clean: MASK_QUERY_GROUPED values per beam (0 = per-query)")
     a = ap.parse_args()
     cfg = datagen.CONFIGS[5]
     t0 = time.time()
@@ -138,17 +139,23 @@ def clean(a, cfg, X, Xd, inits):
     eids, _, _ = oracle.knn_exact(X, Q[:m], cfg.knn)
     print(f"exact k-NN of {m} queries on the host: {time.time() - t0:.0f} s", flush=True)
     for beam in [int(b) for b in a.beams.split(",")]:
-        ms = []
-        for _ in range(3):
-            e1.record(st)
-            ids, d2 = idx.query(Qd, knn=cfg.knn, beam=beam, stream=st)
-            e2.record(st)
-            torch.cuda.synchronize()
-            ms.append(e1.elapsed_time(e2))
-        qms = min(ms)
-        rec = oracle.recall(ids[:m].cpu().numpy(), eids)
-        print(f"query beam {beam}: {Q.shape[0]} queries in {qms:.1f} ms = {Q.shape[0] / qms * 1e3:.3e} QPS, "
-              f"recall@{cfg.knn} {rec:.3f} on {m} queries", flush=True)
+        for mode in a.modes.split(","):
+            os.environ.pop("MASK_QUERY_GROUPED", None)
+            if mode != "auto":
+                os.environ["MASK_QUERY_GROUPED"] = mode
+            ms = []
+            for _ in range(3):
+                e1.record(st)
+                ids, d2 = idx.query(Qd, knn=cfg.knn, beam=beam, stream=st)
+                e2.record(st)
+                torch.cuda.synchronize()
+                ms.append(e1.elapsed_time(e2))
+            qms = min(ms)
+            rec = oracle.recall(ids[:m].cpu().numpy(), eids)
+            print(f"query beam {beam} ({'per-query' if mode == '0' else 'grouped' if mode == '1' else 'auto'}): "
+                  f"{Q.shape[0]} queries in {qms:.1f} ms = {Q.shape[0] / qms * 1e3:.3e} QPS, "
+                  f"recall@{cfg.knn} {rec:.3f} on {m} queries", flush=True)
+        os.environ.pop("MASK_QUERY_GROUPED", None)
     idx.free()
 
 
