@@ -284,6 +284,9 @@ bool launch_query_grouped(const QIndex& qi, const float* Q, int64_t nq, int knn,
                           cudaStream_t st);
 // Xp[pos * d ...] = X[members[pos] * d ...] for pos < n (the partition-ordered copy of the rows)
 void launch_gather_partition(const float* X, int d, const int32_t* members, int64_t n, float* Xp, cudaStream_t st);
+// stable LSD radix sort (sort.cu) of (key, value) pairs on key bits [begin_bit, end_bit), in
+// place; synchronises the stream
+void radix_sort_pairs(uint64_t* keys, int64_t* vals, int64_t n, int begin_bit, int end_bit, cudaStream_t st);
 // §5.1 relocation step (relocate.cu, reading G8): next data-layer order of a grouped index
 void launch_relocate(const int64_t* got, const int64_t* order_in, const int64_t* keys, const int32_t* lab1, int64_t n,
                      int64_t n_groups, int n_centroids, int64_t* order_out, int64_t* reached_out,

@@ -16,7 +16,6 @@
 // cover test carries a 1e-6 relative slack for the rounding of the radii themselves.
 #include <cuda_runtime.h>
 
-#include <cub/device/device_radix_sort.cuh>
 
 #include <algorithm>
 #include <cmath>
@@ -213,23 +212,17 @@ int64_t range_search(const QIndex& qi, const unsigned* const* cover, const float
   if (ids_out == nullptr || n > cap_out) return n;
   MASK_CUDA(cudaMemsetAsync(qcount, 0, sizeof(int64_t) * nq, st));
   if (n == 0) return 0;
-  DevBuf<unsigned long long> kqd(n), kid(n), kqd2(n), kid2(n);
-  DevBuf<int64_t> ix(n), ix2(n), ix3(n);
+  DevBuf<unsigned long long> kqd(n), kid(n), kqd_g(n);
+  DevBuf<int64_t> ix(n);
   k_range_keys<<<grid_for(n, 256), 256, 0, st>>>(cur.p, res_d2.p, n, kqd.p, kid.p, ix.p);
   MASK_LAUNCH_CHECK();
-  // LSD: stable sort by row id, then stable sort by (query, d^2 bits)
-  size_t tmp_bytes = 0, t2 = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, kid.p, kid2.p, ix.p, ix2.p, (int)n, 0, 64, st);
-  cub::DeviceRadixSort::SortPairs(nullptr, t2, kqd.p, kqd2.p, ix.p, ix2.p, (int)n, 0, 64, st);
-  DevBuf<uint8_t> tmp(std::max(tmp_bytes, t2));
-  MASK_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tmp_bytes, kid.p, kid2.p, ix.p, ix2.p, (int)n, 0, 64, st));
-  // gather the (q, d^2) keys in id order, then sort them stably carrying the permutation
-  DevBuf<unsigned long long> kqd_g(n);
-  k_gather_u64<<<grid_for(n, 256), 256, 0, st>>>(kqd.p, ix2.p, n, kqd_g.p);
+  // LSD on the two keys (sort.cu, stable): by row id, then by (query, d^2 bits) carrying the
+  // permutation -- equal (query, d^2) keep ascending row ids
+  radix_sort_pairs(reinterpret_cast<uint64_t*>(kid.p), ix.p, n, 0, 32, st);
+  k_gather_u64<<<grid_for(n, 256), 256, 0, st>>>(kqd.p, ix.p, n, kqd_g.p);
   MASK_LAUNCH_CHECK();
-  size_t t3 = std::max(tmp_bytes, t2);
-  MASK_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, t3, kqd_g.p, kqd2.p, ix2.p, ix3.p, (int)n, 0, 64, st));
-  k_range_write<<<grid_for(n, 256), 256, 0, st>>>(ix3.p, cur.p, res_d2.p, n, ids_out, d2_out, qcount);
+  radix_sort_pairs(reinterpret_cast<uint64_t*>(kqd_g.p), ix.p, n, 0, 64, st);
+  k_range_write<<<grid_for(n, 256), 256, 0, st>>>(ix.p, cur.p, res_d2.p, n, ids_out, d2_out, qcount);
   MASK_LAUNCH_CHECK();
   return n;
 }

@@ -6,9 +6,8 @@
 // target groups in order, the points of a group ordered by the iteration's keys.
 //
 // Groups of the current order: positions split into g balanced groups, the last (n mod g) one
-// larger (G1).  The order is a sort of the 64-bit keys (target << 32 | key) -- keys are a
-// permutation rank, so every key is distinct -- by a global-memory bitonic network (the
-// relocation sizes are 1e3-1e5 points: O(n log^2 n) compare-exchanges in log^2 launches).
+// larger (G1).  The order is a radix sort (sort.cu) of the 64-bit keys (target << 32 | key);
+// keys are a permutation rank, so every key is distinct.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -26,15 +25,10 @@ __device__ __forceinline__ int64_t group_of_pos(int64_t p, int64_t n, int64_t g)
 
 __global__ void k_reloc_keys(const int64_t* __restrict__ got, const int64_t* __restrict__ order_in,
                              const int64_t* __restrict__ keys, const int32_t* __restrict__ lab1, int64_t n,
-                             int64_t g, int n_centroids, int64_t n2, uint64_t* __restrict__ comp,
+                             int64_t g, int n_centroids, uint64_t* __restrict__ comp,
                              int64_t* __restrict__ val, int64_t* __restrict__ reached_out,
                              unsigned long long* __restrict__ misses) {
-  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n2; p += (int64_t)gridDim.x * blockDim.x) {
-    if (p >= n) {  // padding to the network size: after every real key
-      comp[p] = ~0ull;
-      val[p] = -1;
-      continue;
-    }
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = order_in[p];
     const int64_t gi = got[i];
     const bool found = gi == i;
@@ -47,50 +41,17 @@ __global__ void k_reloc_keys(const int64_t* __restrict__ got, const int64_t* __r
   }
 }
 
-__global__ void k_bitonic_step(uint64_t* __restrict__ comp, int64_t* __restrict__ val, int64_t n2, int64_t j,
-                               int64_t k) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n2; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t l = i ^ j;
-    if (l <= i) continue;
-    const bool up = (i & k) == 0;
-    const uint64_t a = comp[i], b = comp[l];
-    if ((a > b) == up) {
-      comp[i] = b;
-      comp[l] = a;
-      const int64_t t = val[i];
-      val[i] = val[l];
-      val[l] = t;
-    }
-  }
-}
-
-__global__ void k_copy_i64(const int64_t* __restrict__ a, int64_t n, int64_t* __restrict__ b) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    b[i] = a[i];
-}
-
 }  // namespace
 
 void launch_relocate(const int64_t* got, const int64_t* order_in, const int64_t* keys, const int32_t* lab1, int64_t n,
                      int64_t n_groups, int n_centroids, int64_t* order_out, int64_t* reached_out,
                      unsigned long long* misses, cudaStream_t st) {
-  int64_t n2 = 1;
-  while (n2 < n) n2 <<= 1;
-  DevBuf<uint64_t> comp(n2);
-  DevBuf<int64_t> val(n2);
+  DevBuf<uint64_t> comp(n);
   MASK_CUDA(cudaMemsetAsync(misses, 0, sizeof(unsigned long long), st));
-  const unsigned grid = grid_for(n2, 256);
-  k_reloc_keys<<<grid, 256, 0, st>>>(got, order_in, keys, lab1, n, n_groups, n_centroids, n2, comp.p, val.p,
-                                     reached_out, misses);
+  k_reloc_keys<<<grid_for(n, 256), 256, 0, st>>>(got, order_in, keys, lab1, n, n_groups, n_centroids, comp.p,
+                                                 order_out, reached_out, misses);
   MASK_LAUNCH_CHECK();
-  for (int64_t k = 2; k <= n2; k <<= 1)
-    for (int64_t j = k >> 1; j > 0; j >>= 1) {
-      k_bitonic_step<<<grid, 256, 0, st>>>(comp.p, val.p, n2, j, k);
-      MASK_LAUNCH_CHECK();
-    }
-  k_copy_i64<<<grid_for(n, 256), 256, 0, st>>>(val.p, n, order_out);
-  MASK_LAUNCH_CHECK();
-  MASK_CUDA(cudaStreamSynchronize(st));  // (scratch goes out of scope)
+  radix_sort_pairs(comp.p, order_out, n, 0, 64, st);  // (target, key): distinct keys
 }
 
 }  // namespace mask

@@ -92,3 +92,26 @@ def test_range_errors():
     off, ids, d2 = idx.range_query(torch.from_numpy(datagen.queries(cfg, 4)).cuda(), 0.0, "cover")
     assert off.shape[0] == 5
     idx.free()
+
+
+def test_range_many_results_sorted_across_tiles():
+    """~1e5 results (the result sort spans ~25 tiles of its radix passes): every query's list
+    is exactly the brute-force rows within r (boundary-exempt) ordered by (d^2, id), with
+    duplicated rows giving exact d^2 ties that must come out in ascending id."""
+    cfg = datagen.CONFIGS[2].scaled(256)
+    X = datagen.data(cfg)
+    X[100:200] = X[:100]  # exact duplicates: equal d^2 for every query
+    idx = mk.build(torch.from_numpy(X).cuda(), cfg.levels, 4, datagen.all_init_indices(cfg))
+    Q = datagen.queries(cfg, count=256)
+    bd = ((Q.astype(np.float64)[:, None, :] - X.astype(np.float64)[None]) ** 2).sum(-1)
+    r = np.sqrt(np.sort(bd, axis=1)[:, 399]).astype(np.float32)
+    off, ids, d2 = idx.range_query(torch.from_numpy(Q).cuda(), torch.from_numpy(r).cuda(), "cover")
+    lists = _gpu_lists(off, ids, d2)
+    assert int(off[-1]) > 90_000
+    for i, (ii, dd) in enumerate(lists):
+        ref = np.nonzero(bd[i] <= float(r[i]) ** 2)[0]
+        near = np.abs(np.sqrt(bd[i]) - r[i]) <= REL * r[i]
+        got = set(ii.tolist())
+        assert set(ref[~near[ref]].tolist()) <= got and not (got - set(ref.tolist()) - set(np.nonzero(near)[0].tolist()))
+        assert np.array_equal(np.lexsort((ii, dd)), np.arange(len(ii))), f"query {i}: not sorted by (d^2, id)"
+    idx.free()
