@@ -102,7 +102,7 @@ struct WarpTopK {
       return;
     }
     warp_sort32(cd, cid, lane);
-    if (__shfl_sync(FULL, id, 0) == PAD_ID) {  // empty list: the sorted chunk is the list
+    if (__shfl_sync(FULL, id, 0) == PAD_ID && __shfl_sync(FULL, d, 0) == INFINITY) {  // empty: the sorted chunk
       d = cd;
       id = cid;
       return;
@@ -663,10 +663,15 @@ constexpr int kLeafPG = 16;
 constexpr int kChildPG = 32;  // pairs per work item of the grouped level-1 step
 constexpr int kLeafWarps = 4;
 
-__global__ void k_pair_hist(const int32_t* __restrict__ sel, int64_t m, int32_t* __restrict__ cnt) {
+// slots: 0 = every slot of a query's selection, 1 = slot 0 only, 2 = slots 1 .. beam-1
+__device__ __forceinline__ bool slot_in(int64_t e, int beam, int slots) {
+  return slots == 0 || ((e % beam == 0) == (slots == 1));
+}
+__global__ void k_pair_hist(const int32_t* __restrict__ sel, int64_t m, int32_t* __restrict__ cnt, int beam = 1,
+                            int slots = 0) {
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
     const int32_t l = sel[e];
-    if (l >= 0) atomicAdd(cnt + l, 1);
+    if (l >= 0 && slot_in(e, beam, slots)) atomicAdd(cnt + l, 1);
   }
 }
 // single-block exclusive scan of k counts -> off[0..k] (int64); cnt becomes the scatter cursor
@@ -695,10 +700,10 @@ __global__ void __launch_bounds__(1024) k_pair_scan(int32_t* __restrict__ cnt, i
   if (t == blockDim.x - 1) off[k] = part[t];
 }
 __global__ void k_pair_scatter(const int32_t* __restrict__ sel, int64_t m, int32_t* __restrict__ cursor,
-                               int64_t* __restrict__ pairs) {
+                               int64_t* __restrict__ pairs, int beam = 1, int slots = 0) {
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
     const int32_t l = sel[e];
-    if (l >= 0) pairs[atomicAdd(cursor + l, 1)] = e;
+    if (l >= 0 && slot_in(e, beam, slots)) pairs[atomicAdd(cursor + l, 1)] = e;
   }
 }
 
@@ -706,7 +711,7 @@ template <int D4M>  // float4 registers per row: d / 4 <= D4M
 __global__ void __launch_bounds__(kLeafWarps * 32)
     k_leaf_scan(QIndex qi, const float* __restrict__ Q, const int32_t* __restrict__ sel,
                 const int64_t* __restrict__ pairs, const int64_t* __restrict__ loff, int64_t k1, int beam, int knn,
-                int* __restrict__ queue, int32_t* __restrict__ part_id, float* __restrict__ part_d) {
+                int* __restrict__ queue, int32_t* __restrict__ part_id, float* __restrict__ part_d, int use_tau) {
   extern __shared__ __align__(16) float4 lsm4[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int d = qi.dim, d4 = d >> 2;
@@ -732,7 +737,12 @@ __global__ void __launch_bounds__(kLeafWarps * 32)
         const int64_t e = pairs[s0 + j];
         const float4* q4 = reinterpret_cast<const float4*>(Q + (e / beam) * d);
         for (int f = lane; f < D4M; f += 32) qs[j * D4M + f] = f < d4 ? q4[f] : make_float4(0.f, 0.f, 0.f, 0.f);
-        ld[j * 32 + lane] = INFINITY;
+        // use_tau: the query's slot-0 list (its nearest partition, scanned in the first phase)
+        // already holds k rows at or below its k-th distance tau, so this pair's list starts
+        // as k sentinels (tau, PAD): only rows with d^2 <= tau enter it (exact: the merge
+        // takes the best k of all lists, and slot 0 supplies k keys <= (tau, its k-th id))
+        const float tau = use_tau ? part_d[(e - e % beam) * knn + knn - 1] : INFINITY;
+        ld[j * 32 + lane] = tau;
         li[j * 32 + lane] = PAD_ID;
       }
       __syncwarp();
@@ -1090,29 +1100,37 @@ bool launch_query_grouped(const QIndex& qi, const float* Q, int64_t nq, int knn,
     q2.sel_out = sel.p;
     launch_query_dense(q2, Q, nq, knn, beam, ids, d2, st, false);  // descent only
   }
-  MASK_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(int32_t) * k1, st));
-  k_pair_hist<<<grid_for(m, 256), 256, 0, st>>>(sel.p, m, cnt.p);
-  MASK_LAUNCH_CHECK();
-  k_pair_scan<<<1, 1024, 0, st>>>(cnt.p, k1, off.p);
-  MASK_LAUNCH_CHECK();
-  k_pair_scatter<<<grid_for(m, 256), 256, 0, st>>>(sel.p, m, cnt.p, pairs.p);
-  MASK_LAUNCH_CHECK();
-  MASK_CUDA(cudaMemsetAsync(queue.p, 0, sizeof(int), st));
+  // two phases for beams >= 8 (MASK_LEAF_TAU=0/1 overrides; C3 beam 128 69 -> 58 ms, beam 2
+  // 2.31 -> 2.61 ms): each query's nearest partition (slot 0) first, then the other slots with
+  // that list's k-th distance as the entry bar
+  const char* tauenv = getenv("MASK_LEAF_TAU");
+  const bool two_phase = beam >= 2 && (tauenv ? atoi(tauenv) != 0 : beam >= 8);
   const unsigned lgrid = (unsigned)num_sms() * 8;
-  switch (d4m) {
-#define MASK_LEAF(D)                                                                                      \
-  case D:                                                                                                 \
+  for (int phase = two_phase ? 1 : 0; phase <= (two_phase ? 2 : 0); ++phase) {
+    MASK_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(int32_t) * k1, st));
+    k_pair_hist<<<grid_for(m, 256), 256, 0, st>>>(sel.p, m, cnt.p, beam, phase);
+    MASK_LAUNCH_CHECK();
+    k_pair_scan<<<1, 1024, 0, st>>>(cnt.p, k1, off.p);
+    MASK_LAUNCH_CHECK();
+    k_pair_scatter<<<grid_for(m, 256), 256, 0, st>>>(sel.p, m, cnt.p, pairs.p, beam, phase);
+    MASK_LAUNCH_CHECK();
+    MASK_CUDA(cudaMemsetAsync(queue.p, 0, sizeof(int), st));
+    const int use_tau = phase == 2 ? 1 : 0;
+    switch (d4m) {
+#define MASK_LEAF(D)                                                                                        \
+  case D:                                                                                                   \
     MASK_CUDA(cudaFuncSetAttribute(k_leaf_scan<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
     k_leaf_scan<D><<<lgrid, kLeafWarps * 32, smem, st>>>(qi, Q, sel.p, pairs.p, off.p, k1, beam, knn, queue.p, \
-                                                         pid.p, pd.p);                                    \
+                                                         pid.p, pd.p, use_tau);                             \
     break;
-    MASK_LEAF(4)
-    MASK_LEAF(8)
-    MASK_LEAF(16)
-    MASK_LEAF(32)
+      MASK_LEAF(4)
+      MASK_LEAF(8)
+      MASK_LEAF(16)
+      MASK_LEAF(32)
 #undef MASK_LEAF
+    }
+    MASK_LAUNCH_CHECK();
   }
-  MASK_LAUNCH_CHECK();
   k_merge_partials<<<grid_for(nq * 32, 256), 256, 0, st>>>(sel.p, pid.p, pd.p, nq, beam, knn, qi.id_base, ids, d2);
   MASK_LAUNCH_CHECK();
   return true;

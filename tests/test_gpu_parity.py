@@ -537,20 +537,21 @@ def test_leaf_grouped_queries_match_the_oracle(monkeypatch, cid, div, nq, knn, b
     p_ids, p_d2 = idx.query(t(Q), knn=knn, beam=beam)
     p_ids, p_d2 = p_ids.cpu().numpy(), p_d2.cpu().numpy()
     monkeypatch.setenv("MASK_QUERY_GROUPED", "1")
-    # with and without the grouped step into level 1
-    for gl in ("0", "1"):
+    # with and without the grouped step into level 1, with and without the two-phase leaf scan
+    for gl, tau in (("0", "1"), ("1", "1"), ("1", "0")):
         monkeypatch.setenv("MASK_GROUPED_LEVEL", gl)
+        monkeypatch.setenv("MASK_LEAF_TAU", tau)
         try:
             _query_parity(idx, X, Q, cfg.levels, knn=knn, beam=beam)
         except AssertionError as e:
-            raise AssertionError(f"MASK_GROUPED_LEVEL={gl}: {e}") from None
+            raise AssertionError(f"MASK_GROUPED_LEVEL={gl} MASK_LEAF_TAU={tau}: {e}") from None
         g_ids, g_d2 = idx.query(t(Q), knn=knn, beam=beam)
         g_ids, g_d2 = g_ids.cpu().numpy(), g_d2.cpu().numpy()
         fin = np.isfinite(p_d2)
         np.testing.assert_array_equal(np.isfinite(g_d2), fin)
         np.testing.assert_allclose(g_d2[fin], p_d2[fin], rtol=1e-5, atol=1e-6)
         same = (g_ids == p_ids).all(1)
-        assert same.mean() > 0.99, f"gl={gl}: {(~same).sum()} queries differ between grouped and per-query"
+        assert same.mean() > 0.99, f"gl={gl} tau={tau}: {(~same).sum()} queries differ between grouped and per-query"
     idx.free()
 
 
