@@ -707,6 +707,34 @@ __global__ void k_pair_scatter(const int32_t* __restrict__ sel, int64_t m, int32
   }
 }
 
+// Stage the query vectors of pairs[s0 .. s0 + np) (np <= 32) into qs[j * D4M + c] (zero beyond
+// d4) with every load of the warp in flight together: lane j holds pair j's row offset, and
+// the warp sweeps the np x D4M grid of float4s four loads per lane at a time (a per-pair loop
+// would wait one L2 round trip per pair).
+template <int D4M>
+__device__ __forceinline__ void stage_queries(const float* __restrict__ Q, int d4, int beam,
+                                              const int64_t* __restrict__ pairs, int64_t s0, int np, float4* qs,
+                                              int lane) {
+  const int64_t my = lane < np ? (pairs[s0 + lane] / beam) * (int64_t)d4 : 0;
+  const float4* Q4 = reinterpret_cast<const float4*>(Q);
+  const int total = np * D4M;
+  for (int base = 0; base < total; base += 128) {
+    float4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int f = base + u * 32 + lane;
+      const int j = f / D4M, c = f % D4M;
+      const int64_t off = __shfl_sync(FULL, my, j & 31);
+      v[u] = (f < total && c < d4) ? __ldg(Q4 + off + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int f = base + u * 32 + lane;
+      if (f < total) qs[f] = v[u];
+    }
+  }
+}
+
 template <int D4M>  // float4 registers per row: d / 4 <= D4M
 __global__ void __launch_bounds__(kLeafWarps * 32)
     k_leaf_scan(QIndex qi, const float* __restrict__ Q, const int32_t* __restrict__ sel,
@@ -733,16 +761,18 @@ __global__ void __launch_bounds__(kLeafWarps * 32)
       const int64_t s1 = min64(i1, loff[p + 1]);
       const int np = (int)(s1 - s0);
       __syncwarp();
+      stage_queries<D4M>(Q, d4, beam, pairs, s0, np, qs, lane);
+      // use_tau: the query's slot-0 list (its nearest partition, scanned in the first phase)
+      // already holds k rows at or below its k-th distance tau, so this pair's list starts as k
+      // sentinels (tau, PAD): only rows with d^2 <= tau enter it (exact: the merge takes the
+      // best k of all lists, and slot 0 supplies k keys <= (tau, its k-th id))
+      float tau_l = INFINITY;
+      if (use_tau && lane < np) {
+        const int64_t e = pairs[s0 + lane];
+        tau_l = part_d[(e - e % beam) * knn + knn - 1];
+      }
       for (int j = 0; j < np; ++j) {
-        const int64_t e = pairs[s0 + j];
-        const float4* q4 = reinterpret_cast<const float4*>(Q + (e / beam) * d);
-        for (int f = lane; f < D4M; f += 32) qs[j * D4M + f] = f < d4 ? q4[f] : make_float4(0.f, 0.f, 0.f, 0.f);
-        // use_tau: the query's slot-0 list (its nearest partition, scanned in the first phase)
-        // already holds k rows at or below its k-th distance tau, so this pair's list starts
-        // as k sentinels (tau, PAD): only rows with d^2 <= tau enter it (exact: the merge
-        // takes the best k of all lists, and slot 0 supplies k keys <= (tau, its k-th id))
-        const float tau = use_tau ? part_d[(e - e % beam) * knn + knn - 1] : INFINITY;
-        ld[j * 32 + lane] = tau;
+        ld[j * 32 + lane] = __shfl_sync(FULL, tau_l, j);
         li[j * 32 + lane] = PAD_ID;
       }
       __syncwarp();
@@ -918,11 +948,7 @@ __global__ void __launch_bounds__(kLeafWarps * 32)
       const int64_t s1 = min64(i1, poff[p + 1]);
       const int np = (int)(s1 - s0);
       __syncwarp();
-      for (int j = 0; j < np; ++j) {
-        const int64_t e = pairs[s0 + j];
-        const float4* q4 = reinterpret_cast<const float4*>(Q + (e / beam) * d);
-        for (int f = lane; f < D4M; f += 32) qs[j * D4M + f] = f < d4 ? q4[f] : make_float4(0.f, 0.f, 0.f, 0.f);
-      }
+      stage_queries<D4M>(Q, d4, beam, pairs, s0, np, qs, lane);
       for (int j = lane; j < np; j += 32) co[j] = coff[pairs[s0 + j]];
       __syncwarp();
       const int64_t m0 = up.offsets[p], m1 = up.offsets[p + 1];
@@ -981,20 +1007,32 @@ __global__ void __launch_bounds__(kWideWarps * 32)
   cur.cid = reinterpret_cast<int32_t*>(cur.cd + 32);
   for (int64_t q = (int64_t)blockIdx.x * kWideWarps + w; q < nq; q += nwarps) {
     const int64_t a = coff[q * beam], b = coff[(q + 1) * beam];
+    // the next chunk's loads are issued before the current chunk is offered (the selection is
+    // otherwise bound by one load latency per 32 candidates)
+    float nv = a + lane < b ? cand_d[a + lane] : INFINITY;
+    int32_t ni = a + lane < b ? cand_id[a + lane] : PAD_ID;
     if (beam <= 32) {
       WarpTopK top;
       top.reset(beam);
       for (int64_t c = a; c < b; c += 32) {
-        const int64_t o = c + lane;
-        top.offer(o < b ? cand_d[o] : INFINITY, o < b ? cand_id[o] : PAD_ID, lane);
+        const float v = nv;
+        const int32_t j = ni;
+        const int64_t o = c + 32 + lane;
+        nv = o < b ? cand_d[o] : INFINITY;
+        ni = o < b ? cand_id[o] : PAD_ID;
+        top.offer(v, j, lane);
       }
       if (lane < beam) sel_out[q * beam + lane] = top.id == PAD_ID ? -1 : top.id;
     } else {
       __syncwarp();
       cur.reset(beam);
       for (int64_t c = a; c < b; c += 32) {
-        const int64_t o = c + lane;
-        cur.offer(o < b ? cand_d[o] : INFINITY, o < b ? cand_id[o] : PAD_ID, lane);
+        const float v = nv;
+        const int32_t j = ni;
+        const int64_t o = c + 32 + lane;
+        nv = o < b ? cand_d[o] : INFINITY;
+        ni = o < b ? cand_id[o] : PAD_ID;
+        cur.offer(v, j, lane);
       }
       for (int s2 = lane; s2 < beam; s2 += 32) sel_out[q * beam + s2] = s2 < cur.n ? cur.id[s2] : -1;
     }
