@@ -161,12 +161,13 @@ def test_e2e_C5_div256_T15():
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("cid,div", [(5, 64), (4, 1)])
+@pytest.mark.parametrize("cid,div", [(5, 64)])
 def test_e2e_survey_replicas_long(cid, div):
-    """SURVEY §8(c)'s exact replica sizes where they take the FP64 oracle tens of minutes on the
-    host (C5 / 64: 1.56M x 128, k = 4096 / 64 / 1, T = 15; C4 full: 1M CSR rows, k = 8192 / 256,
-    T = 15).  Opt-in (MASK_E2E_LONG=1) so the default GPU suite stays within minutes; the
-    committed report is profiles/r02_e2e_parity.jsonl."""
+    """SURVEY §8(c)'s exact C5 replica size (C5 / 64: 1.56M x 128, k = 4096 / 64 / 1, T = 15),
+    which takes the FP64 oracle tens of minutes on the host.  Opt-in (MASK_E2E_LONG=1) so the
+    default GPU suite stays within minutes; the committed report is profiles/r02_e2e_parity.jsonl
+    (all three levels in sync to the last pass, final rel L2 2.5e-8).  Full C4 needs more than
+    50 minutes of oracle time on the box's cores; C4 / 4 is in the default suite."""
     if os.environ.get("MASK_E2E_LONG") != "1":
         pytest.skip("set MASK_E2E_LONG=1 (tens of minutes of FP64 oracle time)")
     cfg = datagen.CONFIGS[cid].scaled(div) if div > 1 else datagen.CONFIGS[cid]
