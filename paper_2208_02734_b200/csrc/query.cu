@@ -1120,7 +1120,9 @@ bool launch_query_grouped(const QIndex& qi, const float* Q, int64_t nq, int knn,
   if (mode == 0 || !qi.Xp || qi.routed || qi.L < 1 || (d & 3) || d > 128) return false;
   // small batches, and batches averaging under two queries per partition (C3 at beam 1: 1.5,
   // per-query 1.50 vs grouped 1.54 ms; C5 at beam 1: 3.8, 71 vs 44 ms): the per-query kernel
-  if (m == 0 || (mode != 1 && (m < 65536 || m < 2 * qi.lv[0].k))) return false;
+  // and batches under 32,768 queries (C2: 1e4 queries at beam 16, 0.60 ms per-query against 0.68 ms
+  // grouped -- the grouped pipeline's dozen launches dominate a sub-millisecond batch)
+  if (m == 0 || (mode != 1 && (m < 65536 || m < 2 * qi.lv[0].k || nq < 32768))) return false;
   const size_t part_bytes = (size_t)m * knn * 8;
   if (part_bytes > ((size_t)8 << 30)) return false;
   const int d4 = d >> 2;
