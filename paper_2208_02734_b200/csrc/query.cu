@@ -1007,33 +1007,39 @@ __global__ void __launch_bounds__(kWideWarps * 32)
   cur.cid = reinterpret_cast<int32_t*>(cur.cd + 32);
   for (int64_t q = (int64_t)blockIdx.x * kWideWarps + w; q < nq; q += nwarps) {
     const int64_t a = coff[q * beam], b = coff[(q + 1) * beam];
-    // the next chunk's loads are issued before the current chunk is offered (the selection is
+    // the loads of the next kPF chunks are in flight while a chunk is offered (the selection is
     // otherwise bound by one load latency per 32 candidates)
-    float nv = a + lane < b ? cand_d[a + lane] : INFINITY;
-    int32_t ni = a + lane < b ? cand_id[a + lane] : PAD_ID;
+    constexpr int kPF = 4;
+    float pv[kPF];
+    int32_t pj[kPF];
+#pragma unroll
+    for (int i = 0; i < kPF; ++i) {
+      const int64_t o = a + 32 * i + lane;
+      pv[i] = o < b ? cand_d[o] : INFINITY;
+      pj[i] = o < b ? cand_id[o] : PAD_ID;
+    }
+    auto sweep = [&](auto&& offer) {
+      for (int64_t c = a; c < b; c += 32 * kPF) {
+#pragma unroll
+        for (int i = 0; i < kPF; ++i) {
+          const float v = pv[i];
+          const int32_t j = pj[i];
+          const int64_t o = c + 32 * (i + kPF) + lane;
+          pv[i] = o < b ? cand_d[o] : INFINITY;
+          pj[i] = o < b ? cand_id[o] : PAD_ID;
+          if (c + 32 * i < b) offer(v, j);  // (uniform across the warp)
+        }
+      }
+    };
     if (beam <= 32) {
       WarpTopK top;
       top.reset(beam);
-      for (int64_t c = a; c < b; c += 32) {
-        const float v = nv;
-        const int32_t j = ni;
-        const int64_t o = c + 32 + lane;
-        nv = o < b ? cand_d[o] : INFINITY;
-        ni = o < b ? cand_id[o] : PAD_ID;
-        top.offer(v, j, lane);
-      }
+      sweep([&](float v, int32_t j) { top.offer(v, j, lane); });
       if (lane < beam) sel_out[q * beam + lane] = top.id == PAD_ID ? -1 : top.id;
     } else {
       __syncwarp();
       cur.reset(beam);
-      for (int64_t c = a; c < b; c += 32) {
-        const float v = nv;
-        const int32_t j = ni;
-        const int64_t o = c + 32 + lane;
-        nv = o < b ? cand_d[o] : INFINITY;
-        ni = o < b ? cand_id[o] : PAD_ID;
-        cur.offer(v, j, lane);
-      }
+      sweep([&](float v, int32_t j) { cur.offer(v, j, lane); });
       for (int s2 = lane; s2 < beam; s2 += 32) sel_out[q * beam + s2] = s2 < cur.n ? cur.id[s2] : -1;
     }
   }
