@@ -1124,10 +1124,11 @@ bool launch_query_grouped(const QIndex& qi, const float* Q, int64_t nq, int knn,
   const int64_t m = nq * (int64_t)beam;
   const int d = qi.dim;
   if (mode == 0 || !qi.Xp || qi.routed || qi.L < 1 || (d & 3) || d > 128) return false;
-  // small batches, and batches averaging under two queries per partition (C3 at beam 1: 1.5,
-  // per-query 1.50 vs grouped 1.54 ms; C5 at beam 1: 3.8, 71 vs 44 ms): the per-query kernel
-  // and batches under 32,768 queries (C2: 1e4 queries at beam 16, 0.60 ms per-query against 0.68 ms
-  // grouped -- the grouped pipeline's dozen launches dominate a sub-millisecond batch)
+  // the per-query kernel keeps: batches under 32,768 queries (C2's 1e4 at beam 16: 0.60 ms
+  // per-query against 0.68 ms grouped -- the grouped pipeline's dozen launches dominate a
+  // sub-millisecond batch), fewer than 65,536 (query, partition) pairs, and batches averaging
+  // under two queries per partition (C3 at beam 1: 1.5, 1.50 vs 1.54 ms; C5 at beam 1: 3.8,
+  // 71 vs 44 ms)
   if (m == 0 || (mode != 1 && (m < 65536 || m < 2 * qi.lv[0].k || nq < 32768))) return false;
   const size_t part_bytes = (size_t)m * knn * 8;
   if (part_bytes > ((size_t)8 << 30)) return false;
