@@ -599,6 +599,10 @@ def main():
                        "l2": "flushed between timed steps (512 MiB write)",
                        "seed": args.seed, "tol": args.tol, "empty": args.empty},
             "per_level_distances": per_level, "build_ms": build_mean,
+            # SURVEY §8(d) variant (i): level-1 distances over the level-1 assignment kernels'
+            # own time (live CUDA events); `value` is variant (ii), the whole step
+            "level1_distances_per_s_assign_only": (per_level[0] * args.steps / (kt["assign"] / 1000.0)
+                                                   if kt["assign"] > 0 and akern != "K11-fused-small-level" else None),
             "query_ms": query_mean, "query_qps": cfg.n_queries / (query_mean / 1000.0),
             "recall_at_k_sample": recall, "qps_at_recall": qps_at_recall, "roofline": roof, "update_roofline": upd,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches // max(args.steps, 1)),
