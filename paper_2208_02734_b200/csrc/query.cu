@@ -14,6 +14,8 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <vector>
+#include <cstdio>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -925,8 +927,8 @@ template <int D4M>
 __global__ void __launch_bounds__(kLeafWarps * 32)
     k_child_dist(QIndex qi, int lvl, const float* __restrict__ Q, const int32_t* __restrict__ sel,
                  const int64_t* __restrict__ pairs, const int64_t* __restrict__ poff, int64_t kp, int beam,
-                 const int64_t* __restrict__ coff, int* __restrict__ queue, float* __restrict__ cand_d,
-                 int32_t* __restrict__ cand_id) {
+                 const int64_t* __restrict__ coff, int64_t base, int* __restrict__ queue,
+                 float* __restrict__ cand_d, int32_t* __restrict__ cand_id) {
   extern __shared__ __align__(16) float4 csm4[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int d = qi.dim, d4 = d >> 2;
@@ -949,7 +951,7 @@ __global__ void __launch_bounds__(kLeafWarps * 32)
       const int np = (int)(s1 - s0);
       __syncwarp();
       stage_queries<D4M>(Q, d4, beam, pairs, s0, np, qs, lane);
-      for (int j = lane; j < np; j += 32) co[j] = coff[pairs[s0 + j]];
+      for (int j = lane; j < np; j += 32) co[j] = coff[pairs[s0 + j]] - base;
       __syncwarp();
       const int64_t m0 = up.offsets[p], m1 = up.offsets[p + 1];
       for (int64_t c = m0; c < m1; c += 32) {
@@ -992,7 +994,7 @@ __global__ void __launch_bounds__(kLeafWarps * 32)
 
 // warp per query: top-beam of its candidates [coff[q beam], coff[(q + 1) beam]) -> sel_out
 __global__ void __launch_bounds__(kWideWarps * 32)
-    k_select_cands(const int64_t* __restrict__ coff, const float* __restrict__ cand_d,
+    k_select_cands(const int64_t* __restrict__ coff, int64_t cbase, const float* __restrict__ cand_d,
                    const int32_t* __restrict__ cand_id, int64_t nq, int beam, int32_t* __restrict__ sel_out) {
   extern __shared__ __align__(16) float ssm[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -1006,7 +1008,7 @@ __global__ void __launch_bounds__(kWideWarps * 32)
   cur.cd = reinterpret_cast<float*>(cur.tid + kMaxWideBeam);
   cur.cid = reinterpret_cast<int32_t*>(cur.cd + 32);
   for (int64_t q = (int64_t)blockIdx.x * kWideWarps + w; q < nq; q += nwarps) {
-    const int64_t a = coff[q * beam], b = coff[(q + 1) * beam];
+    const int64_t a = coff[q * beam] - cbase, b = coff[(q + 1) * beam] - cbase;
     // the loads of the next kPF chunks are in flight while a chunk is offered (the selection is
     // otherwise bound by one load latency per 32 candidates)
     constexpr int kPF = 4;
@@ -1047,6 +1049,21 @@ __global__ void __launch_bounds__(kWideWarps * 32)
 
 // The grouped step into level 1: fills sel (nq x beam level-1 prototype ids, -1 padded).
 // Returns false (nothing launched) when the index has no level above 1 or no child-ordered copy.
+__global__ void k_gather_coff(const int64_t* __restrict__ coff, int64_t nq, int beam, int64_t qb, int64_t nbnd,
+                              int64_t* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nbnd; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = coff[min64(i * qb, nq) * beam];
+}
+
+// Candidates held at once by the grouped step (8 B each): queries are taken in chunks whose
+// candidates fit (parents are skewed: C5 after Lloyd averages ~700 children per selected parent
+// against 64 per parent overall, 23e9 candidates for 1e6 queries at beam 32).
+constexpr int64_t kCandBudget = int64_t(1) << 29;  // 4 GiB of (d^2, id)
+constexpr int64_t kCandQB = 1024;                  // chunk boundary granularity (queries)
+
+// The grouped step into level 1: fills sel (nq x beam level-1 prototype ids, -1 padded).
+// Returns false when the index has no level above 1 or no child-ordered copy, or the candidate
+// buffer cannot be had (the caller then runs the per-query descent).
 static bool grouped_level1_selection(const QIndex& qi, const float* Q, int64_t nq, int beam, int32_t* sel,
                                      cudaStream_t st) {
   if (qi.L < 2 || !qi.lv[0].Pc) return false;
@@ -1062,56 +1079,80 @@ static bool grouped_level1_selection(const QIndex& qi, const float* Q, int64_t n
   q2.sel_out = sel2.p;
   q2.sel_stop = 1;
   launch_query_dense(q2, Q, nq, 1, beam, nullptr, nullptr, st, false);  // descent down to level 2
-  // pairs grouped by parent
-  MASK_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(int32_t) * k2, st));
-  k_pair_hist<<<grid_for(m, 256), 256, 0, st>>>(sel2.p, m, cnt.p);
-  MASK_LAUNCH_CHECK();
-  k_pair_scan<<<1, 1024, 0, st>>>(cnt.p, k2, poff.p);
-  MASK_LAUNCH_CHECK();
-  k_pair_scatter<<<grid_for(m, 256), 256, 0, st>>>(sel2.p, m, cnt.p, pairs.p);
-  MASK_LAUNCH_CHECK();
-  // candidate offsets
+  // candidate offsets (exclusive scan of the selected parents' children counts, query-major)
   k_cand_scan1<<<(unsigned)nb, kScanB, 0, st>>>(sel2.p, qi.lv[1].offsets, m, coff.p, bsum.p);
   MASK_LAUNCH_CHECK();
   k_cand_scan2<<<1, 1024, 0, st>>>(bsum.p, nb);
   MASK_LAUNCH_CHECK();
   k_cand_scan3<<<grid_for(m + 1, 256), 256, 0, st>>>(coff.p, m, bsum.p);
   MASK_LAUNCH_CHECK();
-  int64_t ncand = 0;
-  MASK_CUDA(cudaMemcpyAsync(&ncand, coff.p + m, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  // chunk boundaries every kCandQB queries
+  const int64_t nbnd = (nq + kCandQB - 1) / kCandQB + 1;
+  DevBuf<int64_t> bnd_d(nbnd);
+  k_gather_coff<<<grid_for(nbnd, 256), 256, 0, st>>>(coff.p, nq, beam, kCandQB, nbnd, bnd_d.p);
+  MASK_LAUNCH_CHECK();
+  std::vector<int64_t> bnd(nbnd);
+  MASK_CUDA(cudaMemcpyAsync(bnd.data(), bnd_d.p, sizeof(int64_t) * nbnd, cudaMemcpyDeviceToHost, st));
   MASK_CUDA(cudaStreamSynchronize(st));
-  // the candidate buffer (8 B per candidate) is best-effort: on OOM the per-query descent runs
+  std::vector<std::pair<int64_t, int64_t>> chunks;  // [boundary index a, b)
+  const char* benv = getenv("MASK_QUERY_CAND_BUDGET");  // (tests: force many chunks)
+  const int64_t budget = benv ? std::max<int64_t>(1, atoll(benv)) : kCandBudget;
+  int64_t most = 1;
+  for (int64_t i = 0; i + 1 < nbnd;) {
+    int64_t j = i + 1;
+    while (j + 1 < nbnd && bnd[j + 1] - bnd[i] <= budget) ++j;
+    chunks.emplace_back(i, j);
+    most = std::max<int64_t>(most, bnd[j] - bnd[i]);
+    i = j;
+  }
+  // the candidate buffer is best-effort: on OOM the per-query descent runs
   DevBuf<float> cd;
   DevBuf<int32_t> cid;
   try {
-    cd.alloc(std::max<int64_t>(ncand, 1));
-    cid.alloc(std::max<int64_t>(ncand, 1));
+    cd.alloc(most);
+    cid.alloc(most);
   } catch (const Error& e) {
     if (e.code != MASK_ERR_OOM) throw;
     cudaGetLastError();
+    if (getenv("MASK_DEBUG_QUERY")) fprintf(stderr, "grouped level step: %lld candidates: %s\n", (long long)most, e.what());
     return false;
   }
-  MASK_CUDA(cudaMemsetAsync(queue.p, 0, sizeof(int), st));
   const size_t smem = (size_t)kLeafWarps * (kChildPG * d4m + kChildPG / 2) * sizeof(float4);
   const unsigned g = (unsigned)num_sms() * 8;
-  switch (d4m) {
-#define MASK_CD(D)                                                                                            \
-  case D:                                                                                                     \
-    MASK_CUDA(cudaFuncSetAttribute(k_child_dist<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
-    k_child_dist<D><<<g, kLeafWarps * 32, smem, st>>>(qi, 0, Q, sel2.p, pairs.p, poff.p, k2, beam, coff.p,   \
-                                                      queue.p, cd.p, cid.p);                                  \
-    break;
-    MASK_CD(4)
-    MASK_CD(8)
-    MASK_CD(16)
-    MASK_CD(32)
-#undef MASK_CD
-  }
-  MASK_LAUNCH_CHECK();
   const size_t ssmem = (size_t)kWideWarps * (4 * kMaxWideBeam + 64) * sizeof(float);
-  const unsigned sg = (unsigned)std::min<int64_t>((nq + kWideWarps - 1) / kWideWarps, (int64_t)num_sms() * 32);
-  k_select_cands<<<sg, kWideWarps * 32, ssmem, st>>>(coff.p, cd.p, cid.p, nq, beam, sel);
-  MASK_LAUNCH_CHECK();
+  for (const auto& c : chunks) {
+    const int64_t qa = c.first * kCandQB, qb = std::min<int64_t>(c.second * kCandQB, nq);
+    const int64_t nqc = qb - qa, mc = nqc * beam, base = bnd[c.first];
+    const int32_t* sel2c = sel2.p + qa * beam;
+    const int64_t* coffc = coff.p + qa * beam;
+    const float* Qc = Q + qa * d;
+    // the chunk's (query, parent) pairs grouped by parent
+    MASK_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(int32_t) * k2, st));
+    k_pair_hist<<<grid_for(mc, 256), 256, 0, st>>>(sel2c, mc, cnt.p);
+    MASK_LAUNCH_CHECK();
+    k_pair_scan<<<1, 1024, 0, st>>>(cnt.p, k2, poff.p);
+    MASK_LAUNCH_CHECK();
+    k_pair_scatter<<<grid_for(mc, 256), 256, 0, st>>>(sel2c, mc, cnt.p, pairs.p);
+    MASK_LAUNCH_CHECK();
+    MASK_CUDA(cudaMemsetAsync(queue.p, 0, sizeof(int), st));
+    switch (d4m) {
+#define MASK_CD(D)                                                                                              \
+  case D:                                                                                                       \
+    MASK_CUDA(cudaFuncSetAttribute(k_child_dist<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));   \
+    k_child_dist<D><<<g, kLeafWarps * 32, smem, st>>>(qi, 0, Qc, sel2c, pairs.p, poff.p, k2, beam, coffc, base, \
+                                                      queue.p, cd.p, cid.p);                                    \
+    break;
+      MASK_CD(4)
+      MASK_CD(8)
+      MASK_CD(16)
+      MASK_CD(32)
+#undef MASK_CD
+    }
+    MASK_LAUNCH_CHECK();
+    const unsigned sg = (unsigned)std::min<int64_t>((nqc + kWideWarps - 1) / kWideWarps, (int64_t)num_sms() * 32);
+    k_select_cands<<<sg, kWideWarps * 32, ssmem, st>>>(coffc, base, cd.p, cid.p, nqc, beam, sel + qa * beam);
+    MASK_LAUNCH_CHECK();
+  }
   MASK_CUDA(cudaStreamSynchronize(st));  // (the scratch above is released at return)
   return true;
 }

@@ -538,9 +538,14 @@ def test_leaf_grouped_queries_match_the_oracle(monkeypatch, cid, div, nq, knn, b
     p_ids, p_d2 = p_ids.cpu().numpy(), p_d2.cpu().numpy()
     monkeypatch.setenv("MASK_QUERY_GROUPED", "1")
     # with and without the grouped step into level 1, with and without the two-phase leaf scan
-    for gl, tau in (("0", "1"), ("1", "1"), ("1", "0")):
+    # (the last run splits the grouped level step into many query chunks: a tiny candidate budget)
+    for gl, tau, budget in (("0", "1", None), ("1", "1", None), ("1", "0", None), ("1", "1", "3000")):
         monkeypatch.setenv("MASK_GROUPED_LEVEL", gl)
         monkeypatch.setenv("MASK_LEAF_TAU", tau)
+        if budget:
+            monkeypatch.setenv("MASK_QUERY_CAND_BUDGET", budget)
+        else:
+            monkeypatch.delenv("MASK_QUERY_CAND_BUDGET", raising=False)
         try:
             _query_parity(idx, X, Q, cfg.levels, knn=knn, beam=beam)
         except AssertionError as e:
