@@ -1064,23 +1064,20 @@ constexpr int64_t kCandQB = 1024;                  // chunk boundary granularity
 // The grouped step into level 1: fills sel (nq x beam level-1 prototype ids, -1 padded).
 // Returns false when the index has no level above 1 or no child-ordered copy, or the candidate
 // buffer cannot be had (the caller then runs the per-query descent).
-static bool grouped_level1_selection(const QIndex& qi, const float* Q, int64_t nq, int beam, int32_t* sel,
-                                     cudaStream_t st) {
-  if (qi.L < 2 || !qi.lv[0].Pc) return false;
+// One grouped descent step: from each query's selection sel2 at level lvl+1 (index into lv) to
+// its top-b among their children at level lvl, written to sel.
+static bool grouped_level_step(const QIndex& qi, const float* Q, int64_t nq, int beam, int lvl,
+                               const int32_t* sel2_in, int32_t* sel, cudaStream_t st) {
   const int d = qi.dim, d4 = d >> 2;
   const int d4m = d4 <= 4 ? 4 : d4 <= 8 ? 8 : d4 <= 16 ? 16 : 32;
   const int64_t m = nq * (int64_t)beam;
-  const int64_t k2 = qi.lv[1].k;
-  DevBuf<int32_t> sel2(m), cnt(k2), queue(1);
+  const int64_t k2 = qi.lv[lvl + 1].k;
+  DevBuf<int32_t> cnt(k2), queue(1);
   DevBuf<int64_t> poff(k2 + 1), pairs(m), coff(m + 1);
   const int64_t nb = (m + kScanB - 1) / kScanB;
   DevBuf<int64_t> bsum(nb + 1);
-  QIndex q2 = qi;
-  q2.sel_out = sel2.p;
-  q2.sel_stop = 1;
-  launch_query_dense(q2, Q, nq, 1, beam, nullptr, nullptr, st, false);  // descent down to level 2
   // candidate offsets (exclusive scan of the selected parents' children counts, query-major)
-  k_cand_scan1<<<(unsigned)nb, kScanB, 0, st>>>(sel2.p, qi.lv[1].offsets, m, coff.p, bsum.p);
+  k_cand_scan1<<<(unsigned)nb, kScanB, 0, st>>>(sel2_in, qi.lv[lvl + 1].offsets, m, coff.p, bsum.p);
   MASK_LAUNCH_CHECK();
   k_cand_scan2<<<1, 1024, 0, st>>>(bsum.p, nb);
   MASK_LAUNCH_CHECK();
@@ -1123,7 +1120,7 @@ static bool grouped_level1_selection(const QIndex& qi, const float* Q, int64_t n
   for (const auto& c : chunks) {
     const int64_t qa = c.first * kCandQB, qb = std::min<int64_t>(c.second * kCandQB, nq);
     const int64_t nqc = qb - qa, mc = nqc * beam, base = bnd[c.first];
-    const int32_t* sel2c = sel2.p + qa * beam;
+    const int32_t* sel2c = sel2_in + qa * beam;
     const int64_t* coffc = coff.p + qa * beam;
     const float* Qc = Q + qa * d;
     // the chunk's (query, parent) pairs grouped by parent
@@ -1139,7 +1136,7 @@ static bool grouped_level1_selection(const QIndex& qi, const float* Q, int64_t n
 #define MASK_CD(D)                                                                                              \
   case D:                                                                                                       \
     MASK_CUDA(cudaFuncSetAttribute(k_child_dist<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));   \
-    k_child_dist<D><<<g, kLeafWarps * 32, smem, st>>>(qi, 0, Qc, sel2c, pairs.p, poff.p, k2, beam, coffc, base, \
+    k_child_dist<D><<<g, kLeafWarps * 32, smem, st>>>(qi, lvl, Qc, sel2c, pairs.p, poff.p, k2, beam, coffc, base, \
                                                       queue.p, cd.p, cid.p);                                    \
     break;
       MASK_CD(4)
@@ -1154,6 +1151,34 @@ static bool grouped_level1_selection(const QIndex& qi, const float* Q, int64_t n
     MASK_LAUNCH_CHECK();
   }
   MASK_CUDA(cudaStreamSynchronize(st));  // (the scratch above is released at return)
+  return true;
+}
+
+// The grouped descent into level 1: the per-query kernel selects at level `start` (index into
+// lv; 1 = level 2), then grouped steps take every lower level down to level 1's selection in
+// sel.  False when an index level lacks its child-ordered copy or a step's candidate buffer
+// cannot be had (the caller then runs the per-query descent).
+static bool grouped_level1_selection(const QIndex& qi, const float* Q, int64_t nq, int beam, int32_t* sel,
+                                     cudaStream_t st) {
+  if (qi.L < 2) return false;
+  // grouped steps from the top level down for beams >= 32, from level 2 otherwise
+  // (MASK_GROUPED_FROM_TOP=0/1 overrides; C3 beam 128 53.4 -> 51.5 ms, beam 8 6.11 -> 6.19 ms)
+  const char* tenv = getenv("MASK_GROUPED_FROM_TOP");
+  const bool from_top = tenv ? atoi(tenv) != 0 : beam >= 32;
+  const int start = from_top ? qi.L - 1 : 1;
+  for (int l = 0; l < start; ++l)
+    if (!qi.lv[l].Pc) return false;
+  const int64_t m = nq * (int64_t)beam;
+  DevBuf<int32_t> cur(m), nxt(start > 1 ? m : 0);
+  QIndex q2 = qi;
+  q2.sel_out = cur.p;
+  q2.sel_stop = start;
+  launch_query_dense(q2, Q, nq, 1, beam, nullptr, nullptr, st, false);  // per-query descent to `start`
+  for (int lvl = start - 1; lvl >= 0; --lvl) {
+    int32_t* out = lvl == 0 ? sel : nxt.p;
+    if (!grouped_level_step(qi, Q, nq, beam, lvl, cur.p, out, st)) return false;
+    if (lvl > 0) std::swap(cur, nxt);
+  }
   return true;
 }
 

@@ -539,9 +539,12 @@ def test_leaf_grouped_queries_match_the_oracle(monkeypatch, cid, div, nq, knn, b
     monkeypatch.setenv("MASK_QUERY_GROUPED", "1")
     # with and without the grouped step into level 1, with and without the two-phase leaf scan
     # (the last run splits the grouped level step into many query chunks: a tiny candidate budget)
-    for gl, tau, budget in (("0", "1", None), ("1", "1", None), ("1", "0", None), ("1", "1", "3000")):
+    # (and one with grouped steps from the top level down)
+    for gl, tau, budget, top in (("0", "1", None, "0"), ("1", "1", None, "0"), ("1", "0", None, "0"),
+                                 ("1", "1", "3000", "0"), ("1", "1", None, "1")):
         monkeypatch.setenv("MASK_GROUPED_LEVEL", gl)
         monkeypatch.setenv("MASK_LEAF_TAU", tau)
+        monkeypatch.setenv("MASK_GROUPED_FROM_TOP", top)
         if budget:
             monkeypatch.setenv("MASK_QUERY_CAND_BUDGET", budget)
         else:

@@ -49,9 +49,12 @@ def main():
         for mode in a.modes.split(","):
             os.environ.pop("MASK_QUERY_GROUPED", None)
             os.environ.pop("MASK_GROUPED_LEVEL", None)
-            if mode.startswith("g"):  # g0 / g1: grouped leaf scan without / with the grouped level-1 step
+            os.environ.pop("MASK_GROUPED_FROM_TOP", None)
+            if mode.startswith("g"):  # g0 / g1 / g2: grouped leaf scan; + level-1 step; + steps from the top
                 os.environ["MASK_QUERY_GROUPED"] = "1"
-                os.environ["MASK_GROUPED_LEVEL"] = mode[1]
+                os.environ["MASK_GROUPED_LEVEL"] = "0" if mode == "g0" else "1"
+                if mode == "g2":
+                    os.environ["MASK_GROUPED_FROM_TOP"] = "1"
             elif mode != "auto":
                 os.environ["MASK_QUERY_GROUPED"] = mode
             ms = []
