@@ -314,6 +314,33 @@ def blobs(seed: int, n: int, d: int, m: int, spread: float = 10.0, sigma: float 
     return (centers[comp] + sigma * g.standard_normal((n, d))).astype(np.float32)
 
 
+def ragged_csr(seed: int, n: int, d: int, max_nnz: int, zipf: float = 1.2):
+    """Random CSR rows of 0..max_nnz distinct sorted columns (Zipf(``zipf``) column popularity,
+    so a hot set exists), non-negative L2-normalised values; row 0 is empty, row 1 (if any) has
+    min(max_nnz, d) non-zeros."""
+    g = _rng(seed, 17)
+    lens = g.integers(0, max_nnz + 1, size=n)
+    if n:
+        lens[0] = 0
+    if n > 1:
+        lens[1] = min(max_nnz, d)
+    cols, vals, rp = [], [], [0]
+    for i in range(n):
+        m = int(min(lens[i], d))
+        c = np.unique(_zipf_ranks(g, 8 * m + 8, zipf, d))[:m] if m else np.zeros(0, np.int64)
+        while c.size < m:
+            c = np.unique(np.concatenate([c, g.choice(d, size=m, replace=False)]))[:m]
+        v = g.lognormal(0.0, 1.0, size=c.size)
+        if c.size:
+            v /= np.sqrt((v * v).sum())
+        cols.append(np.sort(c))
+        vals.append(v)
+        rp.append(rp[-1] + c.size)
+    col = np.concatenate(cols).astype(np.int32) if n else np.zeros(0, np.int32)
+    val = np.concatenate(vals).astype(np.float32) if n else np.zeros(0, np.float32)
+    return np.asarray(rp, np.int64), col, val
+
+
 def random_csr(seed: int, n: int, d: int, nnz_row: int):
     """Random CSR rows with ``nnz_row`` distinct sorted columns, non-negative L2-normalised values."""
     g = _rng(seed, 13)

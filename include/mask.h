@@ -75,6 +75,9 @@ enum {
                                     event pair per pass: the cheapest live kernel timing)      */
   MASK_NO_PARTITION_COPY = 1 << 9, /* dense: skip the partition-ordered copy of the rows that
                                     mask_query's leaf scans read (saves n*dim floats)          */
+  MASK_CSR_TC = 1 << 11,         /* CSR: K3T (hot columns on tcgen05 3xTF32 + SIMT tail in the
+                                    epilogue) instead of the chunk-major SIMT K3; measured slower
+                                    at C4 (DESIGN.md §6 K3T), kept for A/B and testing         */
   MASK_TRACE_PASSES = 1 << 10    /* keep, per level, the prototypes every assignment pass used
                                     and the labels it produced, on the device, read back with
                                     mask_get_pass (parity tests of the production path: unlike

@@ -17,6 +17,7 @@ from ._lib import (
     MASK_TIME_ASSIGN,
     MASK_TIME_KERNELS,
     MASK_TRACE_PASSES,
+    MASK_CSR_TC,
     MASK_VALIDATE_FINITE,
     MaskError,
 )
@@ -28,4 +29,5 @@ __all__ = [
     "query_range", "MaskError", "MASK_BORROW_DATA", "MASK_FORCE_SIMT", "MASK_NO_FIXUP",
     "MASK_VALIDATE_FINITE", "MASK_TIME_KERNELS", "MASK_TIME_ASSIGN", "MASK_NO_SORT", "MASK_NO_FUSED",
     "MASK_TRACE_PASSES",
+    "MASK_CSR_TC",
 ]

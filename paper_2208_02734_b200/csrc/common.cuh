@@ -185,6 +185,18 @@ void launch_assign_csr_chunked(const int64_t* row_ptr, const int32_t* col, const
                                const float* PT, const float* cn2, int64_t k, const int16_t* colslot,
                                const int32_t* hotcols, float2* state, int32_t* labels, float* best, cudaStream_t st,
                                const int* active = nullptr);
+// K3T (assign_csr_tc.cu): CSR hot columns on tcgen05 (3xTF32) + SIMT tail in the epilogue.
+int64_t csr_tc_rows(int64_t k);  // prototype rows padded to whole tiles
+int csr_tc_hot();                // hot columns H
+// per level: Xh [n x H] dense hot block, tail {col, -2v} at each row's CSR offset, ntail [n], xn2 [n]
+void launch_csr_tc_level(const int64_t* rp, const int32_t* col, const float* val, int64_t n, const int16_t* colslot,
+                         float* Xh, int2* tail, int32_t* ntail, float* xn2, cudaStream_t st);
+// per pass: Hb/Hs [csr_tc_rows(k) x H] split -2 c_hot, cn2 [csr_tc_rows(k)] (+inf pad), PT [d x csr_tc_rows(k)]
+void launch_csr_tc_prep(const float* P, int64_t k, int d, const int32_t* hotcols, float* Hb, float* Hs, float* cn2,
+                        float* PT, cudaStream_t st, const int* active = nullptr);
+void launch_assign_csr_tc(const float* Xh, const int64_t* rp, const int2* tail, const int32_t* ntail, const float* xn2,
+                          int64_t n, const float* Hb, const float* Hs, const float* PT, const float* cn2, int64_t k,
+                          int32_t* labels, float* best, cudaStream_t st, const int* active = nullptr);
 void launch_i64_to_i32(const int64_t* a, int64_t n, int32_t* b, cudaStream_t st);
 // per-column non-zero counts (d int32, zeroed here)
 void launch_col_hist(const int32_t* col, int64_t nnz, int d, int32_t* cnt, cudaStream_t st);

@@ -322,7 +322,8 @@ struct Level {
   int updates = 0;
   double t_ms[MASK_T_NCLASS] = {0, 0, 0, 0};
   int64_t t_count[MASK_T_NCLASS] = {0, 0, 0, 0};
-  int assign_kernel = -1;  // 0 = K2 SIMT, 1 = K1 tcgen05 3xTF32, 2 = K3 CSR, 3 = K11 fused small level
+  int assign_kernel = -1;  // 0 = K2 SIMT, 1 = K1 tcgen05 3xTF32, 2 = K3 CSR, 3 = K11 fused small level,
+                           // 4 = K12 grouped, 5 = K3T CSR hot block on tcgen05
   // MASK_TRACE_PASSES: slot t < T = loop pass t, slot T = the final pass (T + 1 slots)
   DevBuf<float> P_trace;        // (T+1) x k x dim
   DevBuf<int32_t> lab_trace;    // (T+1) x n_items (this rank's items)
@@ -448,6 +449,11 @@ struct LloydWS {
   DevBuf<int16_t> colslot;  // K3 chunk-major: hot slot of each column (-1 = read from L2)
   DevBuf<int32_t> hotcols;  // the hot columns (most non-zeros)
   DevBuf<float2> csr_state; // running argmin across prototype chunks
+  // K3T (CSR, hot columns on tcgen05): per level the dense hot block, the tail non-zeros and
+  // their counts; per pass the split hot prototype slice, ||c||^2 (+inf padded), padded PT
+  DevBuf<float> k3_Xh, k3_Hb, k3_Hs, k3_cn2, k3_PT;
+  DevBuf<int2> k3_tail;
+  DevBuf<int32_t> k3_ntail;
   bool xn2_ready = false;
   int kernel_id = -1;
 };
@@ -490,6 +496,35 @@ void assign_pass(const Input& in, const float* P, int64_t k, int flags, int32_t*
   const int64_t n = in.n_local;
   const int d = in.dim;
   if (n == 0) return;
+  if (in.format == MASK_CSR_F32 && (flags & MASK_CSR_TC) && !(flags & MASK_FORCE_SIMT)) {
+    // K3T (opt-in): hot columns on tcgen05 (3xTF32), tail non-zeros in the epilogue (DESIGN.md §6 K3T)
+    const int H = csr_tc_hot();
+    const int64_t kr = csr_tc_rows(k);
+    if (!ws.k3_Xh.p) {  // per level: hot set, dense hot block, tail lists, ||x||^2
+      DevBuf<int32_t> cnt(d);
+      launch_col_hist(in.col, in.nnz, d, cnt.p, st);
+      ws.colslot.alloc(d);
+      ws.hotcols.alloc(H);
+      launch_select_hot(cnt.p, d, H, ws.hotcols.p, ws.colslot.p, st);
+      ws.k3_Xh.alloc((size_t)n * H);
+      ws.k3_tail.alloc((size_t)std::max<int64_t>(in.nnz, 1));
+      ws.k3_ntail.alloc(n);
+      ws.xn2.alloc(n);
+      launch_csr_tc_level(in.rp, in.col, in.val, n, ws.colslot.p, ws.k3_Xh.p, ws.k3_tail.p, ws.k3_ntail.p, ws.xn2.p,
+                          st);
+      ws.k3_Hb.alloc((size_t)kr * H);
+      ws.k3_Hs.alloc((size_t)kr * H);
+      ws.k3_cn2.alloc(kr);
+      ws.k3_PT.alloc((size_t)kr * d);
+    }
+    launch_csr_tc_prep(P, k, d, ws.hotcols.p, ws.k3_Hb.p, ws.k3_Hs.p, ws.k3_cn2.p, ws.k3_PT.p, st, active);
+    ws.kernel_id = 5;
+    if (ev) ev->mark(MASK_T_ASSIGN, st);
+    launch_assign_csr_tc(ws.k3_Xh.p, in.rp, ws.k3_tail.p, ws.k3_ntail.p, ws.xn2.p, n, ws.k3_Hb.p, ws.k3_Hs.p,
+                         ws.k3_PT.p, ws.k3_cn2.p, k, labels_out, best, st, active);
+    if (ev) ev->mark(MASK_T_ASSIGN, st);
+    return;
+  }
   if (in.format == MASK_CSR_F32) {
     if (!ws.PT.p) ws.PT.alloc((size_t)k * d);
     if (!ws.cn2.p) ws.cn2.alloc(k);
