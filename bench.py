@@ -461,7 +461,8 @@ def main():
     n1g = n_local  # rows this rank's level-1 assignment launches process
     assign_avg_ms = kt["assign"] / max(kt["assign_n"], 1)
     akern = idx.timing(1)["assign_kernel"]
-    use_tc = akern == "K1-tcgen05-3xtf32"
+    use_tc = akern in ("K1-tcgen05-3xtf32", "K1-tcgen05-3xfp16")
+    h16 = akern == "K1-tcgen05-3xfp16"
     if akern == "K11-fused-small-level":  # one launch runs the whole level: all its passes
         flops = 3.0 * n1 * k1 * d * lvl1["passes"]
         peak = 148 * 128 * 2 * pk["sm_max_mhz"] * 1e6 / 1e12
@@ -474,15 +475,21 @@ def main():
         roof = {"bound": "alu", "kernel": "K3 CSR assignment (level 1)", "unit": "TFLOP/s",
                 "peak_basis": "FP32 FMA = 148 SMs x 128 lanes x 2 flop x sm_max_mhz (DESIGN.md K3)"}
     elif use_tc:
-        flops = 6.0 * n1g * k1 * d  # 3xTF32: three TF32 products per useful multiply-add
+        flops = 6.0 * n1g * k1 * d  # 3xTF32 / 3xFP16: three MMA products per useful multiply-add
         # a kernel timed inside a long step runs at the sustained clock (B200_PROFILING.md):
         # steps over 1 s take the sustained bf16 figure, shorter ones the burst figure
         sustained = total_ms / args.steps > 1000.0
         bf = pk["bf16_tflops_sustained"] if sustained else pk["bf16_tflops"]
-        peak = 0.5 * bf
-        roof = {"bound": "tensor", "kernel": "K1 tcgen05 3xTF32 assignment (level 1)", "unit": "TFLOP/s",
-                "peak_basis": f"TF32 dense = 0.5 x {pk['source']} bf16 {'sustained' if sustained else 'burst'} "
-                              f"{bf} TFLOP/s (nominal ratio)"}
+        if h16:  # kind::f16 runs at the bf16 rate
+            peak = bf
+            roof = {"bound": "tensor", "kernel": "K1 tcgen05 3xFP16 assignment (level 1)", "unit": "TFLOP/s",
+                    "peak_basis": f"FP16 dense = {pk['source']} bf16 {'sustained' if sustained else 'burst'} "
+                                  f"{bf} TFLOP/s (same rate)"}
+        else:
+            peak = 0.5 * bf
+            roof = {"bound": "tensor", "kernel": "K1 tcgen05 3xTF32 assignment (level 1)", "unit": "TFLOP/s",
+                    "peak_basis": f"TF32 dense = 0.5 x {pk['source']} bf16 {'sustained' if sustained else 'burst'} "
+                                  f"{bf} TFLOP/s (nominal ratio)"}
     else:
         flops = 3.0 * n1 * k1 * d  # sub + fma per coordinate
         peak = 148 * 128 * 2 * pk["sm_max_mhz"] * 1e6 / 1e12
@@ -583,12 +590,12 @@ def main():
     if rank == 0:
         clocks = sampler.summary() if sampler else None
         if use_tc and clocks and clocks.get("sm_mhz"):
-            # context for `frac`: the TF32 MMA rate measured on this GPU (tools/mma_ubench.cu: 4096
+            # context for `frac`: the MMA rate measured on this GPU (tools/mma_ubench.cu: TF32 4096, FP16 twice that
             # flop/clk/SM, K1) at the median SM clock of the timed region, and the burst peak
-            hw = 4096.0 * 148 * clocks["sm_mhz"] * 1e6 / 1e12
+            hw = (8192.0 if h16 else 4096.0) * 148 * clocks["sm_mhz"] * 1e6 / 1e12
             roof["tensor_util_at_clock"] = achieved / hw
-            roof["hw_tf32_at_clock_tflops"] = hw
-            roof["frac_of_burst_peak"] = achieved / (0.5 * pk["bf16_tflops"])
+            roof["hw_tf32_at_clock_tflops" if not h16 else "hw_f16_at_clock_tflops"] = hw
+            roof["frac_of_burst_peak"] = achieved / ((1.0 if h16 else 0.5) * pk["bf16_tflops"])
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,

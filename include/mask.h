@@ -75,6 +75,7 @@ enum {
                                     event pair per pass: the cheapest live kernel timing)      */
   MASK_NO_PARTITION_COPY = 1 << 9, /* dense: skip the partition-ordered copy of the rows that
                                     mask_query's leaf scans read (saves n*dim floats)          */
+  MASK_TC_TF32 = 1 << 12,        /* dense d = 64 / 128: 3xTF32 even where 3xFP16 is enabled   */
   MASK_CSR_TC = 1 << 11,         /* CSR: K3T (hot columns on tcgen05 3xTF32 + SIMT tail in the
                                     epilogue) instead of the chunk-major SIMT K3; measured slower
                                     at C4 (DESIGN.md §6 K3T), kept for A/B and testing         */

@@ -18,6 +18,7 @@ from ._lib import (
     MASK_TIME_KERNELS,
     MASK_TRACE_PASSES,
     MASK_CSR_TC,
+    MASK_TC_TF32,
     MASK_VALIDATE_FINITE,
     MaskError,
 )
@@ -30,4 +31,5 @@ __all__ = [
     "MASK_VALIDATE_FINITE", "MASK_TIME_KERNELS", "MASK_TIME_ASSIGN", "MASK_NO_SORT", "MASK_NO_FUSED",
     "MASK_TRACE_PASSES",
     "MASK_CSR_TC",
+    "MASK_TC_TF32",
 ]

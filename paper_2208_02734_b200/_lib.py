@@ -37,6 +37,7 @@ MASK_TIME_ASSIGN = 1 << 8
 MASK_NO_PARTITION_COPY = 1 << 9
 MASK_TRACE_PASSES = 1 << 10
 MASK_CSR_TC = 1 << 11
+MASK_TC_TF32 = 1 << 12
 MASK_RANGE_PAPER, MASK_RANGE_COVER = 0, 1
 T_ASSIGN, T_FIXUP, T_UPDATE, T_FINALIZE = 0, 1, 2, 3
 

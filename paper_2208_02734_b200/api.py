@@ -373,7 +373,7 @@ class Index:
             check(n)
         names = ["assign", "fixup", "update", "finalize"]
         res = {nm: dict(ms=float(out[2 * i]), launches=int(out[2 * i + 1])) for i, nm in enumerate(names)}
-        res["assign_kernel"] = {0: "K2-simt", 1: "K1-tcgen05-3xtf32", 2: "K3-csr", 3: "K11-fused-small-level", 4: "K12-grouped", 5: "K3T-csr-tcgen05"}.get(int(out[8]), "none")
+        res["assign_kernel"] = {0: "K2-simt", 1: "K1-tcgen05-3xtf32", 2: "K3-csr", 3: "K11-fused-small-level", 4: "K12-grouped", 5: "K3T-csr-tcgen05", 6: "K1-tcgen05-3xfp16"}.get(int(out[8]), "none")
         return res
 
 

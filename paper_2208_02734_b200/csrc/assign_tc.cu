@@ -30,8 +30,10 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
+#include <cuda_fp16.h>
 
 #include <cmath>
+#include <cstring>
 #include <cstdint>
 #include <algorithm>
 #include <cstdio>
@@ -474,9 +476,14 @@ __global__ void __launch_bounds__(128 + 128 * EPI_WG, 1)
 //   ABUF  TMEM A buffers (2: the next block's A is staged while the current block runs; 1 for
 //         large d, where a block's thousands of tiles dwarf the A reload)
 //   NKC   128-byte K chunks per prototype tile (B stage = one chunk of the big and small parts)
-template <int KA, int BN, int STAGES, int NACC, int EPI_WG, bool FOLD = true, int ABUF = 2>
+//   H16   3xFP16 on kind::f16 (twice the kind::tf32 rate): B and A hold FP16 big / small parts of
+//         the scaled operands, 64 K columns per 128-byte chunk, K = 16 per MMA, two halves per
+//         TMEM column (K1 "3xFP16")
+template <int KA, int BN, int STAGES, int NACC, int EPI_WG, bool FOLD = true, int ABUF = 2, bool H16 = false>
 struct PCfg {
-  static constexpr int CW = 32, CWB = 128;
+  static constexpr int CW = H16 ? 64 : 32, CWB = 128;
+  static constexpr int KSTEP = H16 ? 16 : 8;     // K per MMA
+  static constexpr int ACOLS = H16 ? KA / 2 : KA;  // TMEM columns of one A part
   static constexpr int NKC = (KA + CW - 1) / CW;
   static constexpr int B_CHUNK = BN * CWB;
   static constexpr int STAGE_BYTES = 2 * B_CHUNK;
@@ -487,13 +494,14 @@ struct PCfg {
   static constexpr int SCRATCH_FLOATS = 2 * 5 * BM * EPI_WG;
   static constexpr int INFO_OFF = SCRATCH_OFF + SCRATCH_FLOATS * 4;  // [2][BM] rows, bounds, ||x||^2
   static constexpr int SMEM = INFO_OFF + 6 * BM * 4 + 1024;
-  static constexpr int A_COL = NACC * BN;  // A buffer b: big at A_COL + 2*KA*b, small at + KA
-  static constexpr int NEED = A_COL + 2 * ABUF * KA;
+  static constexpr int A_COL = NACC * BN;  // A buffer b: big at A_COL + 2*ACOLS*b, small at + ACOLS
+  static constexpr int NEED = A_COL + 2 * ABUF * ACOLS;
   static constexpr int TMEM_COLS = NEED <= 256 ? 256 : 512;
-  static constexpr uint32_t IDESC = idesc_tf32<BM, BN>();
+  static constexpr uint32_t IDESC = H16 ? idesc_f16<BM, BN>() : idesc_tf32<BM, BN>();
   static constexpr int NTHREADS = 256 + 128 * EPI_WG;
   static constexpr int EPI0 = 8;  // first epilogue warp
-  static constexpr int XSTEPS = FOLD ? KA / 8 - 1 : KA / 8;  // K steps of x (three MMAs each)
+  static constexpr int XSTEPS = FOLD ? KA / 8 - 1 : KA / KSTEP;  // K steps of x (three MMAs each)
+  static_assert(!H16 || (!FOLD && KA % 64 == 0), "3xFP16: large d, whole 64-column chunks");
   static_assert(NEED <= 512, "TMEM budget");
   static_assert(KA % 8 == 0 && KA <= NKC * CW, "K layout");
   static_assert(!FOLD || KA <= CW, "folded K fits one chunk");
@@ -503,7 +511,7 @@ struct PCfg {
 
 // MC = 2: the CTAs of a 2-CTA cluster walk the same prototype tiles in lockstep and each loads
 // one half of every B stage (big / small part) multicast to both: half the L2 reads of B.
-template <int KA, int BN, int STAGES, int NACC, int EPI_WG, bool FOLD, int ABUF, int MC = 1>
+template <int KA, int BN, int STAGES, int NACC, int EPI_WG, bool FOLD, int ABUF, int MC = 1, bool H16 = false>
 __global__ void __launch_bounds__(256 + 128 * EPI_WG, 1)
     k_assign_tc_persist(const __grid_constant__ CUtensorMap tmBb, const __grid_constant__ CUtensorMap tmBs,
                         const float* __restrict__ X, const float* __restrict__ P, const float* __restrict__ cn2,
@@ -511,12 +519,15 @@ __global__ void __launch_bounds__(256 + 128 * EPI_WG, 1)
                         float* __restrict__ best, int32_t* __restrict__ flag_rows, int32_t* __restrict__ flag_count,
                         float err_coef, uint32_t key_mask, const int* __restrict__ active,
                         const int32_t* __restrict__ perm, const int32_t* __restrict__ prev_lab,
-                        int32_t* __restrict__ lab2, int2* __restrict__ flag_pair, int dbg) {
+                        int32_t* __restrict__ lab2, int2* __restrict__ flag_pair, int dbg, float xscale,
+                        float dscale, float err_abs) {
+  // (H16: xscale = s scales x into FP16 range, B holds s (-2c), dscale = 1 / s^2 undoes both;
+  //  err_abs = the score-gap bound's absolute term for FP16 subnormals; TF32: 1, 1, 0)
   if (active && !*active) return;  // level converged: this pass is skipped on the device
 #if !defined(MASK_TC_ABLATE)
   dbg = 0;  // development ablations / counters only in -DMASK_TC_ABLATE builds (tools/build_variant.py)
 #endif
-  using C = PCfg<KA, BN, STAGES, NACC, EPI_WG, FOLD, ABUF>;
+  using C = PCfg<KA, BN, STAGES, NACC, EPI_WG, FOLD, ABUF, H16>;
   constexpr int COLS = BN / EPI_WG;
   // third-candidate bound for the two-candidate K4 decision: large d only (small d is epilogue-
   // bound and its few flagged rows are cheap to re-scan exactly)
@@ -631,7 +642,7 @@ __global__ void __launch_bounds__(256 + 128 * EPI_WG, 1)
       tc_fence_after();
       if (first >= ntiles) continue;
       const int last = first + (ntiles - 1 - first) / 2 * 2;
-      const uint32_t a_big = tmem_base + C::A_COL + 2 * KA * ab, a_small = a_big + KA;
+      const uint32_t a_big = tmem_base + C::A_COL + 2 * C::ACOLS * ab, a_small = a_big + C::ACOLS;
       for (int t = first; t < ntiles; t += 2) {
         const int g = g0 + t;
         const int acc = (int)(g % NACC);
@@ -654,9 +665,14 @@ __global__ void __launch_bounds__(256 + 128 * EPI_WG, 1)
 #pragma unroll
             for (int ks = 0; ks < 4; ++ks) {
               const int s8 = c * 4 + ks;  // global K step
-              if (s8 >= KA / 8 || (dbg & 2)) break;  // (dbg 2, ablation: no MMA)
+              if (s8 >= KA / C::KSTEP || (dbg & 2)) break;  // (dbg 2, ablation: no MMA)
               const uint64_t dbb = smem_desc<C::CWB>(bb + ks * 32);
-              if (s8 < C::XSTEPS) {
+              if constexpr (H16) {  // K step s8 = 16 halves = 8 TMEM columns, 32 bytes of B
+                const uint64_t dbs = smem_desc<C::CWB>(bs + ks * 32);
+                mma_f16_ts(d_tmem, a_small + s8 * 8, dbb, C::IDESC, s8 != 0);
+                mma_f16_ts(d_tmem, a_big + s8 * 8, dbs, C::IDESC, 1u);
+                mma_f16_ts(d_tmem, a_big + s8 * 8, dbb, C::IDESC, 1u);
+              } else if (s8 < C::XSTEPS) {
                 const uint64_t dbs = smem_desc<C::CWB>(bs + ks * 32);
                 mma_tf32_ts(d_tmem, a_small + s8 * 8, dbb, C::IDESC, s8 != 0);
                 mma_tf32_ts(d_tmem, a_big + s8 * 8, dbs, C::IDESC, 1u);
@@ -748,7 +764,7 @@ __global__ void __launch_bounds__(256 + 128 * EPI_WG, 1)
         }
         best[row] = dd;
         const float xx = __ldg(xn2 + row);
-        const float thr = err_coef * (xx + __ldg(cn2 + gi)) + ldexpf(fmaxf(fabsf(g2), fabsf(g1)), -14);
+        const float thr = err_coef * (xx + __ldg(cn2 + gi)) + ldexpf(fmaxf(fabsf(g2), fabsf(g1)), -14) + err_abs;
         flag = (g2 - g1) <= thr;
         // a flagged row whose every other score (lower bound g3: keyed chunks' third-smallest,
         // skipped chunks' minima) lies beyond the window (x 1.25: the window already holds twice the score error) has exactly two candidates:
@@ -802,7 +818,7 @@ __global__ void __launch_bounds__(256 + 128 * EPI_WG, 1)
           const float U = fmaxf(s1, s2);
           // ||c_j|| <= ||x|| + sqrt(U) for every j with d^2 <= U; doubled error coefficient
           const float cm = sqrtf(xx) + sqrtf(U);
-          ub = (U + 2.f * err_coef * (xx + cm * cm)) * (1.f + 0x1p-12f) + 0x1p-100f;
+          ub = (U + 2.f * err_coef * (xx + cm * cm) + err_abs) * (1.f + 0x1p-12f) + 0x1p-100f;
         }
       }
       s_row[ib * BM + rloc] = (int32_t)row;
@@ -814,7 +830,30 @@ __global__ void __launch_bounds__(256 + 128 * EPI_WG, 1)
         tail(i - 1);
         continue;
       }
-      const uint32_t a_big = lane_base + C::A_COL + 2 * KA * ab, a_small = a_big + KA;
+      const uint32_t a_big = lane_base + C::A_COL + 2 * C::ACOLS * ab, a_small = a_big + C::ACOLS;
+      if constexpr (H16) {
+        // 16 columns of s x -> FP16 big / small parts, two halves per TMEM column
+#pragma unroll 1
+        for (int g16 = 0; g16 < KA; g16 += 16) {
+          uint32_t vb[8], vs[8];
+#pragma unroll
+          for (int u = 0; u < 16; u += 4) {
+            const int col = g16 + u;
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (row < n && col < d) v = __ldg(reinterpret_cast<const float4*>(xr + col));
+            const float e[4] = {v.x * xscale, v.y * xscale, v.z * xscale, v.w * xscale};
+#pragma unroll
+            for (int w = 0; w < 4; w += 2) {
+              const __half b0 = __float2half_rn(e[w]), b1 = __float2half_rn(e[w + 1]);
+              const __half s0 = __float2half_rn(e[w] - __half2float(b0)), s1 = __float2half_rn(e[w + 1] - __half2float(b1));
+              vb[(u + w) >> 1] = (uint32_t)__half_as_ushort(b0) | ((uint32_t)__half_as_ushort(b1) << 16);
+              vs[(u + w) >> 1] = (uint32_t)__half_as_ushort(s0) | ((uint32_t)__half_as_ushort(s1) << 16);
+            }
+          }
+          tmem_st8(a_big + g16 / 2, vb);
+          tmem_st8(a_small + g16 / 2, vs);
+        }
+      } else
 #pragma unroll
       for (int g8 = 0; g8 < KA; g8 += 8) {
         uint32_t vb[8], vs[8];
@@ -911,10 +950,11 @@ __global__ void __launch_bounds__(256 + 128 * EPI_WG, 1)
 #pragma unroll
             for (int e4 = 0; e4 < 8; ++e4) {
               const float4 cv = __ldg(c4 + e4);
-              r[cc][4 * e4 + 0] = __float_as_uint((__uint_as_float(r[cc][4 * e4 + 0]) + cv.x) + xx);
-              r[cc][4 * e4 + 1] = __float_as_uint((__uint_as_float(r[cc][4 * e4 + 1]) + cv.y) + xx);
-              r[cc][4 * e4 + 2] = __float_as_uint((__uint_as_float(r[cc][4 * e4 + 2]) + cv.z) + xx);
-              r[cc][4 * e4 + 3] = __float_as_uint((__uint_as_float(r[cc][4 * e4 + 3]) + cv.w) + xx);
+              // (dscale = 1 for TF32: fmaf(D, 1, c) rounds like D + c)
+              r[cc][4 * e4 + 0] = __float_as_uint(fmaf(__uint_as_float(r[cc][4 * e4 + 0]), dscale, cv.x) + xx);
+              r[cc][4 * e4 + 1] = __float_as_uint(fmaf(__uint_as_float(r[cc][4 * e4 + 1]), dscale, cv.y) + xx);
+              r[cc][4 * e4 + 2] = __float_as_uint(fmaf(__uint_as_float(r[cc][4 * e4 + 2]), dscale, cv.z) + xx);
+              r[cc][4 * e4 + 3] = __float_as_uint(fmaf(__uint_as_float(r[cc][4 * e4 + 3]), dscale, cv.w) + xx);
             }
           }
         }
@@ -1099,6 +1139,20 @@ CUtensorMap make_map(const float* base, int64_t rows, int cols, int box_cols, in
   return m;
 }
 
+CUtensorMap make_map16(const void* base, int64_t rows, int cols, int box_cols, int box_rows) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+  cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  MASK_REQUIRE(box_cols * 2 == 128, MASK_ERR_CUDA, "make_map16: 128-byte rows only");
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  MASK_REQUIRE(r == CUDA_SUCCESS, MASK_ERR_CUDA, "cuTensorMapEncodeTiled (fp16) failed (" + std::to_string((int)r) + ")");
+  return m;
+}
+
 #ifndef MASK_TC_EPI_WG
 #define MASK_TC_EPI_WG 4
 #endif
@@ -1134,20 +1188,28 @@ void launch_cfg(const float* X, int64_t n, int d, int kc, int64_t k_rows, const 
   if (tc_debug_mode() & 8) dump_trace((int)grid);
 }
 
-template <int KA, int BN, int STAGES, int NACC, int EPI_WG, bool FOLD = true, int ABUF = 2, int MC = 1>
-void launch_persist(const float* X, int64_t n, int d, int kc, int64_t k_rows, const float* P, const float* Pb,
-                    const float* Ps, const float* cn2, int64_t k, const float* xn2, int32_t* labels, float* best,
+template <int KA, int BN, int STAGES, int NACC, int EPI_WG, bool FOLD = true, int ABUF = 2, int MC = 1,
+          bool H16 = false>
+void launch_persist(const float* X, int64_t n, int d, int kc, int64_t k_rows, const float* P, const void* Pb,
+                    const void* Ps, const float* cn2, int64_t k, const float* xn2, int32_t* labels, float* best,
                     int32_t* flag_rows, int32_t* flag_count, float err_coef, cudaStream_t st, const int* active,
-                    const int32_t* perm, const int32_t* prev_lab, int32_t* lab2, int2* flag_pair) {
-  using C = PCfg<KA, BN, STAGES, NACC, EPI_WG, FOLD, ABUF>;
-  const CUtensorMap tBb = make_map(Pb, k_rows, kc, C::CW, BN);
-  // the small part is only read by the x steps (KA - 8 columns); the fold step uses Pb alone
+                    const int32_t* perm, const int32_t* prev_lab, int32_t* lab2, int2* flag_pair,
+                    float xscale = 1.f, float dscale = 1.f, float err_abs = 0.f) {
+  using C = PCfg<KA, BN, STAGES, NACC, EPI_WG, FOLD, ABUF, H16>;
+  CUtensorMap tBb, tBs;
+  if constexpr (H16) {  // FP16 [k_rows x KA] big / small parts
+    tBb = make_map16(Pb, k_rows, KA, C::CW, BN);
+    tBs = make_map16(Ps, k_rows, KA, C::CW, BN);
+  } else {
+    tBb = make_map(static_cast<const float*>(Pb), k_rows, kc, C::CW, BN);
+    // the small part is only read by the x steps (KA - 8 columns); the fold step uses Pb alone
 #if defined(MASK_TC_PS_TRIM)
-  const CUtensorMap tBs = make_map(Ps, k_rows, kc, C::CW, BN, FOLD ? KA - 8 : 0);
+    tBs = make_map(static_cast<const float*>(Ps), k_rows, kc, C::CW, BN, FOLD ? KA - 8 : 0);
 #else
-  const CUtensorMap tBs = make_map(Ps, k_rows, kc, C::CW, BN);
+    tBs = make_map(static_cast<const float*>(Ps), k_rows, kc, C::CW, BN);
 #endif
-  auto kern = k_assign_tc_persist<KA, BN, STAGES, NACC, EPI_WG, FOLD, ABUF, MC>;
+  }
+  auto kern = k_assign_tc_persist<KA, BN, STAGES, NACC, EPI_WG, FOLD, ABUF, MC, H16>;
   static bool attr_set = false;
   if (!attr_set) {
     MASK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
@@ -1171,11 +1233,12 @@ void launch_persist(const float* X, int64_t n, int d, int kc, int64_t k_rows, co
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     MASK_CUDA(cudaLaunchKernelEx(&cfg, kern, tBb, tBs, X, P, cn2, xn2, n, d, k, labels, best, flag_rows, flag_count,
-                                 err_coef, 0xFFFFFF00u, active, perm, prev_lab, lab2, flag_pair, tc_debug_mode()));
+                                 err_coef, 0xFFFFFF00u, active, perm, prev_lab, lab2, flag_pair, tc_debug_mode(),
+                                 xscale, dscale, err_abs));
   } else {
     kern<<<grid, C::NTHREADS, C::SMEM, st>>>(tBb, tBs, X, P, cn2, xn2, n, d, k, labels, best, flag_rows, flag_count,
                                              err_coef, 0xFFFFFF00u, active, perm, prev_lab, lab2, flag_pair,
-                                             tc_debug_mode());
+                                             tc_debug_mode(), xscale, dscale, err_abs);
   }
   MASK_LAUNCH_CHECK();
   if (tc_debug_mode() & 8) dump_ptrace();
@@ -1228,7 +1291,8 @@ float tc_err_coef(int d) {
 void launch_assign_tc(const float* X, int64_t n, int d, const float* P, const float* Pb, const float* Ps,
                       const float* cn2, int64_t k, const float* xn2, int32_t* labels, float* best,
                       int32_t* flag_rows, int32_t* flag_count, cudaStream_t st, const int* active,
-                      const int32_t* perm, const int32_t* prev_lab, int32_t* lab2, int2* flag_pair) {
+                      const int32_t* perm, const int32_t* prev_lab, int32_t* lab2, int2* flag_pair,
+                      const void* Hb, const void* Hs, float h16_scale, float h16_err_abs) {
   const float coef = tc_err_coef(d);
   const int kc = tc_operand_cols(d);
   const int64_t kr = tc_operand_rows(k);
@@ -1305,7 +1369,35 @@ void launch_assign_tc(const float* X, int64_t n, int d, const float* P, const fl
         const char* e = getenv("MASK_TC_D64");
         return e ? atoi(e) : 0;
       }();
-      if (var == 0)
+      // 3xFP16 tiling: four epilogue warpgroups of 32 columns (the MMAs take half the TF32 time,
+      // so the epilogue needs the extra warps: C3 rows, n = 2e6, 63.6 -> 47.4 ms per pass; the
+      // TF32 tiling at twice the rate: 50.4 ms).  MASK_TC_H16V selects development variants
+      static const int hv = [] {
+        const char* e = getenv("MASK_TC_H16V");
+        return e ? atoi(e) : 2;
+      }();
+      const float ds = 1.f / (h16_scale * h16_scale);
+      if (Hb && hv == 1)
+        tc::launch_persist<64, 192, 4, 2, 3, false, 2, 1, true>(
+            X, n, d, kc, kr, P, Hb, Hs, cn2, k, xn2, labels, best, flag_rows, flag_count, 2.f * c2, st, active, perm,
+            prev_lab, lab2, flag_pair, h16_scale, ds, h16_err_abs);
+      else if (Hb && hv == 2)  // (default)
+        tc::launch_persist<64, 128, 6, 3, 4, false, 1, 1, true>(
+            X, n, d, kc, kr, P, Hb, Hs, cn2, k, xn2, labels, best, flag_rows, flag_count, 2.f * c2, st, active, perm,
+            prev_lab, lab2, flag_pair, h16_scale, ds, h16_err_abs);
+      else if (Hb && hv == 3)
+        tc::launch_persist<64, 192, 4, 2, 3, false, 1, 1, true>(
+            X, n, d, kc, kr, P, Hb, Hs, cn2, k, xn2, labels, best, flag_rows, flag_count, 2.f * c2, st, active, perm,
+            prev_lab, lab2, flag_pair, h16_scale, ds, h16_err_abs);
+      else if (Hb && hv == 4)
+        tc::launch_persist<64, 128, 6, 3, 2, false, 2, 1, true>(
+            X, n, d, kc, kr, P, Hb, Hs, cn2, k, xn2, labels, best, flag_rows, flag_count, 2.f * c2, st, active, perm,
+            prev_lab, lab2, flag_pair, h16_scale, ds, h16_err_abs);
+      else if (Hb)  // 3xFP16 (kind::f16): the TF32 tiling at twice the MMA rate
+        tc::launch_persist<64, 128, 6, 3, 2, false, 1, 1, true>(
+            X, n, d, kc, kr, P, Hb, Hs, cn2, k, xn2, labels, best, flag_rows, flag_count, 2.f * c2, st, active, perm,
+            prev_lab, lab2, flag_pair, h16_scale, ds, h16_err_abs);
+      else if (var == 0)
         tc::launch_persist<64, 128, 6, 3, 2, false, 1>(X, n, d, kc, kr, P, Pb, Ps, cn2, k, xn2, labels, best,
                                                        flag_rows, flag_count, c2, st, active, perm, prev_lab, lab2,
                                                        flag_pair);
@@ -1326,11 +1418,83 @@ void launch_assign_tc(const float* X, int64_t n, int d, const float* P, const fl
       tc::launch_persist<96, 128, 6, 2, 2, false, 1>(X, n, d, kc, kr, P, Pb, Ps, cn2, k, xn2, labels, best,
                                                      flag_rows, flag_count, c2, st, active, perm, prev_lab, lab2,
                                                      flag_pair);
+    else if (Hb && d == 128 && getenv("MASK_TC_H16V") && atoi(getenv("MASK_TC_H16V")) == 1)
+      tc::launch_persist<128, 192, 4, 2, 3, false, 1, 1, true>(
+          X, n, d, kc, kr, P, Hb, Hs, cn2, k, xn2, labels, best, flag_rows, flag_count, 2.f * c2, st, active, perm,
+          prev_lab, lab2, flag_pair, h16_scale, 1.f / (h16_scale * h16_scale), h16_err_abs);
+    else if (Hb && d == 128)
+      tc::launch_persist<128, 128, 6, 2, 2, false, 1, 1, true>(
+          X, n, d, kc, kr, P, Hb, Hs, cn2, k, xn2, labels, best, flag_rows, flag_count, 2.f * c2, st, active, perm,
+          prev_lab, lab2, flag_pair, h16_scale, 1.f / (h16_scale * h16_scale), h16_err_abs);
     else
       tc::launch_persist<128, 128, 6, 2, 2, false, 1>(X, n, d, kc, kr, P, Pb, Ps, cn2, k, xn2, labels, best,
                                                       flag_rows, flag_count, c2, st, active, perm, prev_lab, lab2,
                                                      flag_pair);
   }
+}
+
+// ---------------------------------------------------------------------------------------------
+// 3xFP16 operands (K1 H16).  Per level: max |x| -> the power-of-two scale s with max |s x| in
+// (2^11, 2^12] (|s (-2c)| <= 2^13: prototypes are member means).  Per pass: the split
+// s (-2c) = big + small in FP16 (from the FP64 prototypes when the level keeps them).
+__global__ void k_maxabs(const float* __restrict__ X, int64_t cnt, unsigned* __restrict__ out) {
+  float m = 0.f;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += (int64_t)gridDim.x * blockDim.x)
+    m = fmaxf(m, fabsf(X[i]));
+  const unsigned u = __reduce_max_sync(0xffffffffu, __float_as_uint(m));  // (non-negative floats order as uints)
+  if ((threadIdx.x & 31) == 0 && u) atomicMax(out, u);
+}
+
+bool tc_h16_enabled() {  // default on; MASK_TC_H16=0 keeps 3xTF32 everywhere (A/B runs)
+  static const bool v = [] {
+    const char* e = getenv("MASK_TC_H16");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
+
+float h16_level_scale(const float* X, int64_t cnt, float* maxabs_out, cudaStream_t st) {
+  unsigned* dv = nullptr;
+  MASK_CUDA(cudaMallocAsync(&dv, sizeof(unsigned), st));
+  MASK_CUDA(cudaMemsetAsync(dv, 0, sizeof(unsigned), st));
+  if (cnt > 0) {
+    k_maxabs<<<grid_for(cnt, 256, (int64_t)num_sms() * 8), 256, 0, st>>>(X, cnt, dv);
+    MASK_LAUNCH_CHECK();
+  }
+  unsigned h = 0;
+  MASK_CUDA(cudaMemcpyAsync(&h, dv, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+  MASK_CUDA(cudaFreeAsync(dv, st));
+  MASK_CUDA(cudaStreamSynchronize(st));
+  float m = 0.f;
+  std::memcpy(&m, &h, sizeof(m));
+  *maxabs_out = m;
+  if (!(m > 0.f) || !std::isfinite(m)) return 1.f;
+  int e = 0;
+  std::frexp(m, &e);  // m = f 2^e, f in [0.5, 1)
+  return std::ldexp(1.0f, 12 - e);
+}
+
+template <typename T>
+__global__ void k_prep_h16(const T* __restrict__ P, int64_t k, int d, float s, __half* __restrict__ Hb,
+                           __half* __restrict__ Hs, const int* __restrict__ active) {
+  if (active && !*active) return;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < k * d; e += (int64_t)gridDim.x * blockDim.x) {
+    const double m2 = -2.0 * (double)P[e] * (double)s;
+    const __half b = __float2half_rn((float)m2);
+    Hb[e] = b;
+    Hs[e] = __float2half_rn((float)(m2 - (double)__half2float(b)));
+  }
+}
+
+void launch_prep_h16(const float* P, const double* P64, int64_t k, int d, float s, void* Hb, void* Hs, cudaStream_t st,
+                     const int* active) {
+  if (k <= 0) return;
+  const unsigned grid = grid_for(k * d, 256, (int64_t)num_sms() * 16);
+  if (P64)
+    k_prep_h16<double><<<grid, 256, 0, st>>>(P64, k, d, s, static_cast<__half*>(Hb), static_cast<__half*>(Hs), active);
+  else
+    k_prep_h16<float><<<grid, 256, 0, st>>>(P, k, d, s, static_cast<__half*>(Hb), static_cast<__half*>(Hs), active);
+  MASK_LAUNCH_CHECK();
 }
 
 }  // namespace mask

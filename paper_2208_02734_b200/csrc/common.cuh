@@ -118,7 +118,15 @@ void launch_assign_tc(const float* X, int64_t n, int d, const float* P, const fl
                       const float* Ps, const float* cn2, int64_t k, const float* xn2,
                       int32_t* labels, float* best, int32_t* flag_rows, int32_t* flag_count,
                       cudaStream_t st, const int* active = nullptr, const int32_t* perm = nullptr,
-                      const int32_t* prev_lab = nullptr, int32_t* lab2 = nullptr, int2* flag_pair = nullptr);
+                      const int32_t* prev_lab = nullptr, int32_t* lab2 = nullptr, int2* flag_pair = nullptr,
+                      const void* Hb = nullptr, const void* Hs = nullptr, float h16_scale = 1.f,
+                      float h16_err_abs = 0.f);
+// K1 3xFP16 operands: per-level power-of-two scale of the data (one host read of max |x|) and the
+// per-pass FP16 split of s (-2c) [k x d] (big, small)
+bool tc_h16_enabled();  // 3xFP16 for d = 64 / 128 (default; environment MASK_TC_H16=0 disables)
+float h16_level_scale(const float* X, int64_t cnt, float* maxabs_out, cudaStream_t st);
+void launch_prep_h16(const float* P, const double* P64, int64_t k, int d, float s, void* Hb, void* Hs, cudaStream_t st,
+                     const int* active = nullptr);
 // Counting sort of rows by label: perm = rows of label 0, then 1, ...; cnt_ws = k int32.
 // perm_old (optional): a previous sort, visited in its order (equal labels adjacent -> warp-
 // aggregated atomics); perm must not alias it.  copy_to (optional): copy_to[row] = labels[row].

@@ -323,7 +323,7 @@ struct Level {
   double t_ms[MASK_T_NCLASS] = {0, 0, 0, 0};
   int64_t t_count[MASK_T_NCLASS] = {0, 0, 0, 0};
   int assign_kernel = -1;  // 0 = K2 SIMT, 1 = K1 tcgen05 3xTF32, 2 = K3 CSR, 3 = K11 fused small level,
-                           // 4 = K12 grouped, 5 = K3T CSR hot block on tcgen05
+                           // 4 = K12 grouped, 5 = K3T CSR hot block on tcgen05, 6 = K1 3xFP16
   // MASK_TRACE_PASSES: slot t < T = loop pass t, slot T = the final pass (T + 1 slots)
   DevBuf<float> P_trace;        // (T+1) x k x dim
   DevBuf<int32_t> lab_trace;    // (T+1) x n_items (this rank's items)
@@ -454,6 +454,9 @@ struct LloydWS {
   DevBuf<float> k3_Xh, k3_Hb, k3_Hs, k3_cn2, k3_PT;
   DevBuf<int2> k3_tail;
   DevBuf<int32_t> k3_ntail;
+  // K1 3xFP16 (d = 64 / 128): per-level scale of the data, per-pass FP16 split of s (-2c)
+  DevBuf<uint16_t> h16_b, h16_s;
+  float h16_scale = 1.f, h16_err_abs = 0.f;
   bool xn2_ready = false;
   int kernel_id = -1;
 };
@@ -578,14 +581,28 @@ void assign_pass(const Input& in, const float* P, int64_t k, int flags, int32_t*
     ws.lab2.alloc(n);
     MASK_CUDA(cudaMemsetAsync(ws.lab2.p, 0xff, sizeof(int32_t) * n, st));
   }
+  const bool h16 = tc_h16_enabled() && (d == 64 || d == 128) && !(flags & MASK_TC_TF32);
   if (!ws.xn2_ready) {
     ws.xn2.alloc(n);
     launch_row_norms(in.X, n, d, ws.xn2.p, st);
     ws.xn2_ready = true;
+    if (h16) {  // one host read per level: max |x| -> the FP16 scale and the subnormal error term
+      float maxabs = 0.f;
+      ws.h16_scale = h16_level_scale(in.X, n * (int64_t)d, &maxabs, st);
+      // a score's absolute error from FP16 subnormal parts <= 2^-25 / s per operand element:
+      // sum_i (|dx_i| |2c_i| + |x_i| |d(2c)_i|) <= 3 d maxabs 2^-25 / s; doubled for a gap
+      ws.h16_err_abs = (float)(6.0 * d * (double)maxabs * std::ldexp(1.0, -25) / ws.h16_scale);
+      ws.h16_b.alloc((size_t)tc_operand_rows(k) * d);
+      ws.h16_s.alloc((size_t)tc_operand_rows(k) * d);
+      MASK_CUDA(cudaMemsetAsync(ws.h16_b.p, 0, sizeof(uint16_t) * tc_operand_rows(k) * d, st));
+      MASK_CUDA(cudaMemsetAsync(ws.h16_s.p, 0, sizeof(uint16_t) * tc_operand_rows(k) * d, st));
+    }
   }
   launch_prep_protos(P, k, d, kc, ws.Pb.p, ws.Ps.p, ws.cn2.p, st, tc_operand_rows(k), d <= 24 ? 1 : 0, active,
                      ws.flag_count.p, ws.P64.p);
-  ws.kernel_id = 1;
+  const bool h16_on = h16 && ws.h16_b.p;
+  if (h16_on) launch_prep_h16(P, ws.P64.p, k, d, ws.h16_scale, ws.h16_b.p, ws.h16_s.p, st, active);
+  ws.kernel_id = h16_on ? 6 : 1;
   if (ev) ev->mark(MASK_T_ASSIGN, st);
   // small d (persistent K1): visit rows grouped by their previous label (perm, sorted after
   // the previous pass), so the rows of a warp share their nearest prototypes and the
@@ -593,7 +610,8 @@ void assign_pass(const Input& in, const float* P, int64_t k, int flags, int32_t*
   const int32_t* perm = (ws.have_perm && !(flags & MASK_NO_SORT)) ? ws.perm.p : nullptr;
   launch_assign_tc(in.X, n, d, P, ws.Pb.p, ws.Ps.p, ws.cn2.p, k, ws.xn2.p, labels_out, best, ws.flag_rows.p,
                    ws.flag_count.p, st, active, perm, ws.have_prev ? ws.lab_prev.p : nullptr, ws.lab2.p,
-                   ws.flag_pair.p);
+                   ws.flag_pair.p, h16_on ? ws.h16_b.p : nullptr, h16_on ? ws.h16_s.p : nullptr, ws.h16_scale,
+                   ws.h16_err_abs);
   if (ev) ev->mark(MASK_T_ASSIGN, st);
   // near-tie re-check (K4), sized on the device from the flagged count (no host round trip)
   if (!(flags & MASK_NO_FIXUP)) {

@@ -207,6 +207,22 @@ __host__ __device__ constexpr uint32_t idesc_tf32() {
          | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
+// Instruction descriptor: kind::f16 with A/B = FP16 (format 0), D = F32, both K-major, M x N.
+template <int M, int N>
+__host__ __device__ constexpr uint32_t idesc_f16() {
+  return (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+// D (+)= A . B^T, A from TMEM (two FP16 per 32-bit column), B from shared memory, K = 16
+__device__ __forceinline__ void mma_f16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t idesc,
+                                           uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}" ::"r"(
+          d_tmem),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
 __device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
                                          uint32_t accumulate) {
   asm volatile(
@@ -263,6 +279,8 @@ __device__ __forceinline__ uint32_t umin(uint32_t a, uint32_t b) { return a < b 
 
 // host: 2-D fp32 row-major [rows x cols] tensor map with a {box_cols x box_rows} box (assign_tc.cu)
 CUtensorMap make_map(const float* base, int64_t rows, int cols, int box_cols, int box_rows, int width = 0);
+// the same for a 2-D FP16 [rows x cols] array (box_cols halves)
+CUtensorMap make_map16(const void* base, int64_t rows, int cols, int box_cols, int box_rows);
 
 }  // namespace tc
 }  // namespace mask
