@@ -374,7 +374,7 @@ void mask_free(mask_index* idx); /* NULL-safe */
  * mask_assign: a_i = argmin_j ||x_i - c_j||^2 (lowest j on ties, D4) for every
  * row of `data` against prototypes P (device, k x dim fp32, row-major).  Writes device
  * labels_out[rows] (int32) and, if non-NULL, device d2_out[rows] (fp32 squared distance
- * to the chosen prototype).  Dense rows use the tcgen05 3xTF32 kernel with a near-tie
+ * to the chosen prototype).  Dense rows use the tcgen05 3xTF32 (d = 64 / 128: 3xFP16) kernel with a near-tie
  * FP32 re-check when dim allows, else the FP32 SIMT kernel; CSR rows the sparse kernel.
  * *n_flagged (optional, host) receives the number of rows the near-tie re-check recomputed.
  */
@@ -427,7 +427,8 @@ int64_t mask_kernel_launches(void);
  * out[2*c] = total milliseconds, out[2*c+1] = number of launches, for kernel class
  * c = MASK_T_ASSIGN .. MASK_T_FINALIZE; cap = number of doubles out can hold (>= 2*c+2 for
  * class c to be written); out[2*MASK_T_NCLASS] (cap > 8) = the assignment kernel the level
- * used (0 = K2 FP32 SIMT, 1 = K1 tcgen05 3xTF32, 2 = K3 CSR).  Returns the number of
+ * used (0 = K2 FP32 SIMT, 1 = K1 tcgen05 3xTF32, 2 = K3 CSR, 3 = K11 fused small level,
+ * 4 = K12 grouped, 5 = K3T CSR on tcgen05, 6 = K1 tcgen05 3xFP16).  Returns the number of
  * doubles written or < 0 on error. */
 int32_t mask_get_timing(const mask_index* idx, int32_t level, double* out, int32_t cap);
 
