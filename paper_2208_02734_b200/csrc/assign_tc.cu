@@ -488,15 +488,12 @@ struct PCfg {
   static constexpr int B_CHUNK = BN * CWB;
   static constexpr int STAGE_BYTES = 2 * B_CHUNK;
   static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
-  static constexpr int NCN = NACC + 1;  // ||c||^2 tile slots (no fold): one more than accumulators
-  static constexpr int NBARS = 2 * STAGES + 2 * NACC + 10 + NCN;
+  static constexpr int NBARS = 2 * STAGES + 2 * NACC + 10;
   static constexpr int SCRATCH_OFF = BAR_OFF + NBARS * 8 + 16;
   // per-block results of each epilogue warpgroup {s1, s2, j1, j2, s3lb} x BM, double-buffered
   static constexpr int SCRATCH_FLOATS = 2 * 5 * BM * EPI_WG;
   static constexpr int INFO_OFF = SCRATCH_OFF + SCRATCH_FLOATS * 4;  // [2][BM] rows, bounds, ||x||^2
-  static constexpr int CN2_OFF = (INFO_OFF + 6 * BM * 4 + 127) / 128 * 128;  // [NCN][BN] ||c||^2 tiles
-  static constexpr bool CN2S = H16;  // ||c||^2 tiles staged in shared memory (3xFP16 path)
-  static constexpr int SMEM = CN2_OFF + (CN2S ? NCN * BN * 4 : 0) + 1024;
+  static constexpr int SMEM = INFO_OFF + 6 * BM * 4 + 1024;
   static constexpr int A_COL = NACC * BN;  // A buffer b: big at A_COL + 2*ACOLS*b, small at + ACOLS
   static constexpr int NEED = A_COL + 2 * ABUF * ACOLS;
   static constexpr int TMEM_COLS = NEED <= 256 ? 256 : 512;
@@ -549,8 +546,6 @@ __global__ void __launch_bounds__(256 + 128 * EPI_WG, 1)
   uint64_t* iempty = afull + 4;  // block info (rows, bounds) consumed by the epilogue
   uint64_t* rfull = afull + 6;   // epilogue results of a block ready for the tail
   uint64_t* rempty = afull + 8;  // tail done with a result buffer
-  uint64_t* cfull = afull + 10;  // ||c||^2 tile g landed in slot g % NCN (bulk copy by the issuer)
-  float* cn2s = reinterpret_cast<float*>(smem + C::CN2_OFF);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::NBARS);
   float* scratch = reinterpret_cast<float*>(smem + C::SCRATCH_OFF);
   int32_t* s_row = reinterpret_cast<int32_t*>(smem + C::INFO_OFF);
@@ -584,7 +579,6 @@ __global__ void __launch_bounds__(256 + 128 * EPI_WG, 1)
       mbar_init(&rfull[a], 4 * EPI_WG * kArrivePerWarp);
       mbar_init(&rempty[a], 4 * kArrivePerWarp);
     }
-    for (int a = 0; a < C::NCN; ++a) mbar_init(&cfull[a], 1);
     fence_barrier_init();
   }
   if (warp == 2) {
@@ -655,17 +649,6 @@ __global__ void __launch_bounds__(256 + 128 * EPI_WG, 1)
         const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
         mbar_wait_spin(&tempty[acc], ((g / NACC) & 1) ^ 1);
         tc_fence_after();
-        if (C::CN2S && lane == 0) {
-          // the tile's ||c||^2 into slot g % NCN: its previous reader (tile g - NCN) finished before
-          // the epilogue released accumulator tile g - NACC, which the wait above observed
-          const int cs = g % C::NCN;
-          mbar_arrive_expect_tx(&cfull[cs], BN * 4);
-          asm volatile(
-              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                  smem_u32(cn2s + cs * BN)),
-              "l"(cn2 + (int64_t)t * BN), "r"(BN * 4), "r"(smem_u32(&cfull[cs]))
-              : "memory");
-        }
         const bool ptr = (dbg & 8) && blockIdx.x == 0 && lane == 0 && g < kPT;
         PT_STAMP(ptr, 0, g);
 #pragma unroll
@@ -961,16 +944,12 @@ __global__ void __launch_bounds__(256 + 128 * EPI_WG, 1)
         if (!FOLD) {
           // the d^2 estimate: accumulator (-2 x.c) + ||c_j||^2 + ||x||^2 (FMA pipe; cn2 is padded
           // with +inf beyond k, so pad columns never win)
-          const int cs = g % C::NCN;
-          if (C::CN2S) mbar_wait_spin(&cfull[cs], (uint32_t)((g / C::NCN) & 1));
 #pragma unroll
           for (int cc = 0; cc < COLS / 32; ++cc) {
-            // (3xFP16: the tile staged in shared memory by the issuer, broadcast reads; else L2)
-            const float4* c4 = reinterpret_cast<const float4*>(C::CN2S ? cn2s + cs * BN + col0 + cc * 32
-                                                                        : cn2 + (int64_t)t * BN + col0 + cc * 32);
+            const float4* c4 = reinterpret_cast<const float4*>(cn2 + (int64_t)t * BN + col0 + cc * 32);
 #pragma unroll
             for (int e4 = 0; e4 < 8; ++e4) {
-              const float4 cv = C::CN2S ? c4[e4] : __ldg(c4 + e4);
+              const float4 cv = __ldg(c4 + e4);
               // (dscale = 1 for TF32: fmaf(D, 1, c) rounds like D + c)
               r[cc][4 * e4 + 0] = __float_as_uint(fmaf(__uint_as_float(r[cc][4 * e4 + 0]), dscale, cv.x) + xx);
               r[cc][4 * e4 + 1] = __float_as_uint(fmaf(__uint_as_float(r[cc][4 * e4 + 1]), dscale, cv.y) + xx);
