@@ -1426,6 +1426,18 @@ void launch_assign_tc(const float* X, int64_t n, int d, const float* P, const fl
       tc::launch_persist<128, 192, 4, 2, 3, false, 1, 1, true>(
           X, n, d, kc, kr, P, Hb, Hs, cn2, k, xn2, labels, best, flag_rows, flag_count, 2.f * c2, st, active, perm,
           prev_lab, lab2, flag_pair, h16_scale, 1.f / (h16_scale * h16_scale), h16_err_abs);
+    else if (Hb && d == 128 && getenv("MASK_TC_H16V") && atoi(getenv("MASK_TC_H16V")) == 2)
+      tc::launch_persist<128, 128, 6, 3, 4, false, 1, 1, true>(
+          X, n, d, kc, kr, P, Hb, Hs, cn2, k, xn2, labels, best, flag_rows, flag_count, 2.f * c2, st, active, perm,
+          prev_lab, lab2, flag_pair, h16_scale, 1.f / (h16_scale * h16_scale), h16_err_abs);
+    else if (Hb && d == 128 && getenv("MASK_TC_H16V") && atoi(getenv("MASK_TC_H16V")) == 3)
+      tc::launch_persist<128, 128, 6, 3, 2, false, 1, 1, true>(
+          X, n, d, kc, kr, P, Hb, Hs, cn2, k, xn2, labels, best, flag_rows, flag_count, 2.f * c2, st, active, perm,
+          prev_lab, lab2, flag_pair, h16_scale, 1.f / (h16_scale * h16_scale), h16_err_abs);
+    else if (Hb && d == 128 && getenv("MASK_TC_H16V") && atoi(getenv("MASK_TC_H16V")) == 4)
+      tc::launch_persist<128, 128, 6, 2, 4, false, 1, 1, true>(
+          X, n, d, kc, kr, P, Hb, Hs, cn2, k, xn2, labels, best, flag_rows, flag_count, 2.f * c2, st, active, perm,
+          prev_lab, lab2, flag_pair, h16_scale, 1.f / (h16_scale * h16_scale), h16_err_abs);
     else if (Hb && d == 128)
       tc::launch_persist<128, 128, 6, 2, 2, false, 1, 1, true>(
           X, n, d, kc, kr, P, Hb, Hs, cn2, k, xn2, labels, best, flag_rows, flag_count, 2.f * c2, st, active, perm,
