@@ -596,6 +596,13 @@ def main():
             roof["tensor_util_at_clock"] = achieved / hw
             roof["hw_tf32_at_clock_tflops" if not h16 else "hw_f16_at_clock_tflops"] = hw
             roof["frac_of_burst_peak"] = achieved / ((1.0 if h16 else 0.5) * pk["bf16_tflops"])
+        if akern == "K3-csr" and clocks and clocks.get("sm_mhz") and assign_avg_ms > 0:
+            # the binding unit of K3 (DESIGN.md §6 K3/K3T): every FMA consumes one 4-byte prototype
+            # operand through the L1/shared-memory data path (128 B/clk/SM); operand bytes/s
+            # against that path at the timed region's median clock
+            opb = 4.0 * X_host[0][-1] * k1 / (assign_avg_ms / 1000.0)
+            l1 = 148 * 128.0 * clocks["sm_mhz"] * 1e6
+            roof["l1_datapath"] = {"operand_gbs": opb / 1e9, "peak_gbs": l1 / 1e9, "frac": opb / l1}
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
