@@ -44,7 +44,7 @@ __device__ __forceinline__ float rndf(uint32_t i) {
   return (float)(i & 0xFFFFFF) * (1.0f / 16777216.0f) * 20.f - 10.f;
 }
 
-template <int N, int MODE, bool RND = false>  // MODE 0 = tf32 TS, 1 = tf32 SS, 2 = f16 SS
+template <int N, int MODE, bool RND = false>  // MODE 0 = tf32 TS, 1 = tf32 SS, 2 = f16 SS, 3 = f16 TS
 __global__ void k_bench(int reps, long long* out) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t bar;
@@ -80,7 +80,7 @@ __global__ void k_bench(int reps, long long* out) {
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   if (threadIdx.x == 0) {
-    constexpr uint32_t ID = MODE == 2 ? idesc<128, N, 0>() : idesc<128, N, 2>();
+    constexpr uint32_t ID = MODE >= 2 ? idesc<128, N, 0>() : idesc<128, N, 2>();
     const uint32_t a_s = smem_u32(smem), b_s = smem_u32(smem + 32768);
     const uint64_t da = smem_desc<128>(a_s), db = smem_desc<128>(b_s);
     const uint32_t a_t = tmem + 256 + 32;  // A columns in TMEM (TS mode)
@@ -93,6 +93,10 @@ __global__ void k_bench(int reps, long long* out) {
       else if (MODE == 1)
         asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(tmem),
                      "l"(da), "l"(db), "r"(ID), "r"(1)
+                     : "memory");
+      else if (MODE == 3)
+        asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}" ::"r"(tmem),
+                     "r"(a_t), "l"(db), "r"(ID), "r"(1)
                      : "memory");
       else
         asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(tmem),
@@ -558,14 +562,24 @@ void run(const char* name) {
   cudaError_t e = cudaDeviceSynchronize();
   long long h = 0;
   cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
-  const int K = MODE == 2 ? 16 : 8;
+  const int K = MODE >= 2 ? 16 : 8;
   const double cyc = (double)h / reps;
   printf("%-14s N=%3d: %7.1f cyc/MMA  %6.0f flops/clk/SM  (%s)\n", name, N, cyc, 2.0 * 128 * N * K / cyc,
          cudaGetErrorString(e));
   cudaFree(d);
 }
 
-int main() {
+int main(int argc, char** argv) {
+  if (argc > 1) {  // f16 TS (K1 3xFP16's MMA) beside tf32 TS, zero and random operands
+    run<128, 0>("tf32 TS");
+    run<128, 3>("f16 TS");
+    run<256, 0>("tf32 TS");
+    run<256, 3>("f16 TS");
+    run<128, 0, true>("tf32 TS rnd");
+    run<128, 3, true>("f16 TS rnd");
+    run<128, 2, true>("f16 SS rnd");
+    return 0;
+  }
   run<128, 0>("tf32 TS");
   run<192, 0>("tf32 TS");
   run<256, 0>("tf32 TS");
