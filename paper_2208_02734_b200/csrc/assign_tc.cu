@@ -1393,6 +1393,14 @@ void launch_assign_tc(const float* X, int64_t n, int d, const float* P, const fl
         tc::launch_persist<64, 128, 6, 3, 4, false, 1, 2, true>(
             X, n, d, kc, kr, P, Hb, Hs, cn2, k, xn2, labels, best, flag_rows, flag_count, 2.f * c2, st, active, perm,
             prev_lab, lab2, flag_pair, h16_scale, ds, h16_err_abs);
+      else if (Hb && hv == 6)  // more accumulator slack: 96-wide tiles, four accumulators
+        tc::launch_persist<64, 96, 8, 4, 3, false, 1, 1, true>(
+            X, n, d, kc, kr, P, Hb, Hs, cn2, k, xn2, labels, best, flag_rows, flag_count, 2.f * c2, st, active, perm,
+            prev_lab, lab2, flag_pair, h16_scale, ds, h16_err_abs);
+      else if (Hb && hv == 7)  // 64-wide tiles, six accumulators
+        tc::launch_persist<64, 64, 8, 6, 2, false, 1, 1, true>(
+            X, n, d, kc, kr, P, Hb, Hs, cn2, k, xn2, labels, best, flag_rows, flag_count, 2.f * c2, st, active, perm,
+            prev_lab, lab2, flag_pair, h16_scale, ds, h16_err_abs);
       else if (Hb && hv == 4)
         tc::launch_persist<64, 128, 6, 3, 2, false, 2, 1, true>(
             X, n, d, kc, kr, P, Hb, Hs, cn2, k, xn2, labels, best, flag_rows, flag_count, 2.f * c2, st, active, perm,
