@@ -1173,6 +1173,9 @@ __global__ void __launch_bounds__(256) k_update_csr_sorted(const int64_t* __rest
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const bool vec = (d & 3) == 0;
   const int64_t nseg = (n + kSegRows - 1) / kSegRows;
+  // acc is zeroed once here; every write-out below leaves it zeroed for the next piece
+  for (int c = threadIdx.x; c < d; c += blockDim.x) acc[c] = 0.f;
+  __syncthreads();
   for (int64_t sg = blockIdx.x; sg < nseg; sg += gridDim.x) {
     const int32_t q0 = (int32_t)(sg * kSegRows), q1 = (int32_t)min64(n, (sg + 1) * kSegRows);
     const int32_t j0 = labels[perm[q0]], j1 = labels[perm[q1 - 1]];
@@ -1180,8 +1183,6 @@ __global__ void __launch_bounds__(256) k_update_csr_sorted(const int64_t* __rest
       const int32_t cs = j ? end[j - 1] : 0, ce = end[j];
       const int32_t a = cs > q0 ? cs : q0, b = ce < q1 ? ce : q1;
       if (b <= a) continue;  // empty cluster (uniform across the CTA)
-      for (int c = threadIdx.x; c < d; c += blockDim.x) acc[c] = 0.f;
-      __syncthreads();
       // a warp takes 4 rows at a time and issues all their loads (2 non-zeros per lane and
       // row) before the shared atomics: perm -> row_ptr -> (col, val) is a latency chain
       constexpr int RW = 4;
@@ -1215,22 +1216,32 @@ __global__ void __launch_bounds__(256) k_update_csr_sorted(const int64_t* __rest
       }
       __syncthreads();
       float* Sj = S + (int64_t)j * d;
-      if (a == cs && b == ce) {  // the whole cluster: plain stores
+      // S is zero on entry (zeroed at the level start and by K7 after every pass), so only the
+      // non-zero parts of the piece are written; the read also re-zeroes acc for the next piece
+      if (a == cs && b == ce) {  // the whole cluster: plain stores of the non-zero float4s
         if (vec) {
-          for (int c = threadIdx.x; c < d / 4; c += blockDim.x)
-            reinterpret_cast<float4*>(Sj)[c] = reinterpret_cast<const float4*>(acc)[c];
+          for (int c = threadIdx.x; c < d / 4; c += blockDim.x) {
+            const float4 v = reinterpret_cast<const float4*>(acc)[c];
+            reinterpret_cast<float4*>(acc)[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (v.x != 0.f || v.y != 0.f || v.z != 0.f || v.w != 0.f) reinterpret_cast<float4*>(Sj)[c] = v;
+          }
         } else {
-          for (int c = threadIdx.x; c < d; c += blockDim.x) Sj[c] = acc[c];
+          for (int c = threadIdx.x; c < d; c += blockDim.x) {
+            const float v = acc[c];
+            acc[c] = 0.f;
+            if (v != 0.f) Sj[c] = v;
+          }
         }
         if (threadIdx.x == 0) counts[j] = b - a;
       } else {  // a piece of a cluster that other segments share
         for (int c = threadIdx.x; c < d; c += blockDim.x) {
           const float v = acc[c];
+          acc[c] = 0.f;
           if (v != 0.f) atomicAdd(Sj + c, v);
         }
         if (threadIdx.x == 0) atomicAdd(counts + j, b - a);
       }
-      __syncthreads();  // acc is reused by the next cluster
+      __syncthreads();  // acc (zeroed) is reused by the next cluster
     }
   }
 }
